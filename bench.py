@@ -1,0 +1,492 @@
+#!/usr/bin/env python
+"""Benchmark: update-magnitude selective composite merge (LLMTailor hot path) on B200.
+
+Workload (BASELINE.json configs[2], the config the metric is quoted on at
+1/2/4/8 GPUs): Llama-3.1-8B-shaped model (reference ModelSpec semantics:
+L32 h4096 f14336 v128256, untied, no GQA/bias; 8.84 B params), ZeRO-3 layout
+over 8 ranks, 4 consecutive synthetic snapshots, rho = 0.5 magnitude selection.
+
+Unit of work = one ZeRO rank partition: optimizer shard r (13.25 GB) plus the
+r-th tensor-aligned share of the consolidated bf16 weights (~2.2 GB). GPU g of
+G owns rank partition g (weak scaling: fixed work per GPU). One step =
+  K3/K4 score the 4 resident snapshots' fp32 masters of the partition (3 pairs)
+  -> NCCL all-gather of the FP64 partials (G > 1)
+  -> fixed-order rank combine + magnitude selection + recipe (C++, host)
+  -> K2 gather/scatter of the composite shard partition and weights share.
+Inputs are resident in HBM (62 GB per GPU, >> 126 MB L2, so no L2 flush is needed).
+
+`e2e`: the same step through the C ABI with HOST (pinned) buffers: masters
+staged H2D for scoring, then the shard pipeline (H2D of exactly the selected
+bytes -> K2 -> D2H) per partition.
+
+`--impl reference`: the reference's own CPU implementation (oracle/_ref/ref_tool:
+reference read_checkpoint + scorer restatement + resolve_plan + execute_merge,
+file I/O and re-verify included) on a bounded sample on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import shutil
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_PATH = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM = 6650.0
+WORKLOADS = {
+    # name: (L, h, f, v, tied, ZeRO ranks N, snapshots K, rho, description)
+    "cfg3": (32, 4096, 14336, 128256, False, 8, 4, 0.5,
+             "Llama-3.1-8B-shaped ZeRO-3 8-rank partitions, update-magnitude selective merge of 4 sources"),
+    "cfg2": (28, 3584, 18944, 152064, False, 8, 2, 0.5,
+             "Qwen2.5-7B-shaped, half-layer merge of 2 sources (as 8 ZeRO-rank partitions)"),
+    "cfg1": (4, 256, 688, 32000, False, 1, 2, 0.5,
+             "tiny Llama-style 4-layer (hidden 256), 2 sources half-layer merge, 1 ZeRO rank"),
+}
+# Reference-arm / cpu_baseline sample: cfg3's merge, shrunk to fit a few
+# seconds of CPU work per step (same layout rules, 8 ranks, 4 snapshots).
+SAMPLE = (1, 1024, 3584, 4096, False, 8, 4, 0.5)
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def peaks():
+    try:
+        p = json.loads(PEAKS_PATH.read_text())
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        if shutil.which("nvidia-smi"):
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.reader = threading.Thread(target=self._read, daemon=True)
+            self.reader.start()
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.reader.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def ncu_traffic(kernel: str):
+    """dram read+write bytes per launch from the committed ncu capture (profiles/), or None."""
+    for p in sorted((ROOT / "profiles").glob("*ncu_summary*.json"), reverse=True):
+        try:
+            d = json.loads(p.read_text())
+            k = d.get("kernels", {}).get(kernel)
+            if k and k.get("dram_bytes_per_launch"):
+                return float(k["dram_bytes_per_launch"]), p.name
+        except Exception:
+            continue
+    return None, None
+
+
+# ----------------------------------------------------------------- reference arm --
+def ref_tool_path():
+    return ROOT / "oracle" / "_ref" / "ref_tool"
+
+
+def run_reference_sample(workdir: pathlib.Path, workers: int):
+    """One bounded sample of the workload through the reference library: returns
+    (seconds, composite_bytes, detail). Score (reference read_checkpoint + FP64
+    scorer restatement) -> select -> resolve_plan -> execute_merge (+ re-verify)."""
+    L, h, f, v, tied, N, K, rho = SAMPLE
+    tool = str(ref_tool_path())
+    src = workdir / "src"
+    if not src.exists():
+        subprocess.run([tool, "gen", "--layers", str(L), "--hidden", str(h), "--ffn", str(f), "--vocab", str(v),
+                        "--seed", "42", "--ranks", str(N), "--snapshots", str(K), "--out", str(src)],
+                       check=True, stdout=subprocess.DEVNULL)
+    out = workdir / f"merged-{time.time_ns()}"
+    snaps = ",".join(str(src / f"checkpoint-{k * 100}") for k in range(1, K + 1))
+    t0 = time.perf_counter()
+    p = subprocess.run([tool, "select-merge", "--snapshots", snaps, "--rho", str(rho), "--out", str(out),
+                        "--workers", str(workers)], capture_output=True, text=True, check=True)
+    dt = time.perf_counter() - t0
+    detail = json.loads(p.stdout)
+    composite = os.path.getsize(out / "model.weights") + sum(
+        os.path.getsize(out / "optim" / f"rank_{r}.shard") for r in range(N))
+    shutil.rmtree(out, ignore_errors=True)
+    return dt, composite, detail
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    wl = WORKLOADS[args.workload]
+    if not ref_tool_path().exists():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_tool not built"}))
+        return 0
+    work = pathlib.Path(tempfile.mkdtemp(prefix="tailor-ref-"))
+    try:
+        for _ in range(args.warmup):
+            run_reference_sample(work, cores)
+        times, comp = [], 0
+        for _ in range(args.steps):
+            dt, comp, _ = run_reference_sample(work, cores)
+            times.append(dt)
+    finally:
+        shutil.rmtree(work, ignore_errors=True)
+    total = sum(times)
+    value = comp * args.steps / total / 1e9
+    L, h, f, v, tied, N, K, rho = SAMPLE
+    sample = (f"reference select-merge (read_checkpoint + FP64 scorer + resolve_plan + execute_merge with re-verify, "
+              f"files in /tmp) on L{L} h{h} f{f} v{v} N{N} K{K} rho{rho}: {comp / 1e9:.3f} GB composite per step")
+    line = {"metric": "composite-checkpoint merge GB/s (score+select+merge)", "value": round(value, 4),
+            "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8/f32/f64", "data": "synthetic",
+            "config": {"workload": args.workload, "description": wl[8], "sample": sample},
+            "impl": "reference",
+            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------- our arm --------
+def our_arm(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_22158_b200 as t
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    L, h, f, v, tied, N, K, rho, desc = WORKLOADS[args.workload]
+    if world > N:
+        raise SystemExit(f"{args.workload} has {N} rank partitions; cannot run on {world} GPUs")
+    spec = t.ModelSpec(L, h, f, v, tied, 42)
+    fam = t.SynthFamily(spec, N, K, 100)
+    M = fam.num_modules
+    r = rank  # this GPU's rank partition
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+
+    # ---- resident inputs: K snapshots of partition r (shard + weights share) ------
+    shards = [torch.empty(fam.shard_bytes(k, r), dtype=torch.uint8, device=dev) for k in range(1, K + 1)]
+    fam.gen_shard(r, 1, K, [b.data_ptr() for b in shards], sp)
+    base_yaml = t.MergeRecipe(num_ranks=N, base_checkpoint=f"S{K}").to_yaml()
+    wshare = t.MergePartition(fam, base_yaml, -1, r, N)
+    wlo, whi, wtotal = wshare.range()
+    wbufs = [torch.empty(max(16, whi - wlo), dtype=torch.uint8, device=dev) for _ in range(K)]
+    fam.gen_weights(1, K, wlo, whi, [b.data_ptr() for b in wbufs], sp)
+    scorer = t.Scorer(fam, r, 1, K)
+    partials = torch.zeros((K - 1) * M * 2, dtype=torch.float64, device=dev)
+    gathered = torch.zeros(world * (K - 1) * M * 2, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize(dev)
+
+    plans = {}
+
+    def plans_for(yaml):
+        # Plan construction is a pure function of the recipe; memoized, and its
+        # uncached cost is reported separately as plan_ms.
+        if yaml not in plans:
+            t0 = time.perf_counter()
+            sp_ = t.MergePartition(fam, yaml, r)
+            sp_.bind([shards[k - 1].data_ptr() + lo for k, c, lo, hi in sp_.windows()])
+            wp_ = t.MergePartition(fam, yaml, -1, r, N)
+            wp_.bind([wbufs[k - 1].data_ptr() + (lo - wlo) for k, c, lo, hi in wp_.windows()])
+            plans[yaml] = (sp_, wp_, (time.perf_counter() - t0) * 1e3)
+        return plans[yaml]
+
+    yaml0 = base_yaml
+    sp0, wp0, _ = plans_for(yaml0)
+    out_shard = torch.empty(sp0.bytes, dtype=torch.uint8, device=dev)
+    out_w = torch.empty(max(16, wp0.bytes), dtype=torch.uint8, device=dev)
+    composite = sp0.bytes + wp0.bytes
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    kt = {"score": [], "gather_shard": [], "gather_weights": []}
+    state = {"yaml": None, "src": None, "gap": None}
+
+    def step(record):
+        e0, e1, e2, e3, e4 = ev(), ev(), ev(), ev(), ev()
+        e0.record(stream)
+        scorer.run([b.data_ptr() for b in shards], partials.data_ptr(), sp)
+        e1.record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, partials)
+            parts = gathered.cpu()
+        else:
+            parts = partials.cpu()
+        yaml, src_of, _, gap = fam.select(parts.tolist(), world, rho)
+        state.update(yaml=yaml, src=src_of, gap=gap)
+        spl, wpl, _ = plans_for(yaml)
+        e2.record(stream)
+        spl.run(out_shard.data_ptr(), args.variant, sp)
+        e3.record(stream)
+        wpl.run(out_w.data_ptr(), args.variant, sp)
+        e4.record(stream)
+        if record is not None:
+            record.append((e0, e1, e2, e3, e4))
+
+    for _ in range(args.warmup):
+        step(None)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    recs = []
+    with ClockSampler(local_rank) as clocks:
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        start, end = ev(), ev()
+        start.record(stream)
+        for _ in range(args.steps):
+            step(recs)
+        end.record(stream)
+        torch.cuda.synchronize(dev)
+    total_ms = start.elapsed_time(end)
+    for e0, e1, e2, e3, e4 in recs:
+        kt["score"].append(e0.elapsed_time(e1))
+        kt["gather_shard"].append(e2.elapsed_time(e3))
+        kt["gather_weights"].append(e3.elapsed_time(e4))
+    max_ms = total_ms
+    if world > 1:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        max_ms = float(tt.item())
+    sec = max_ms / 1e3
+    total_bytes = composite * world * args.steps
+    value = total_bytes / sec / 1e9
+    scores_per_s = M * (K - 1) * args.steps / sec
+
+    # ---- uncached plan cost, for the record ----------------------------------------
+    t0 = time.perf_counter()
+    t.MergePartition(fam, state["yaml"], r)
+    t.MergePartition(fam, state["yaml"], -1, r, N)
+    plan_ms = (time.perf_counter() - t0) * 1e3
+
+    # ---- e2e through the C ABI with host buffers ------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_run(args, t, torch, fam, scorer, shards, wbufs, wlo, state["yaml"], r, N, world, dev, sp, K, M, rho)
+
+    # ---- roofline of the dominant kernel ----------------------------------------------
+    hbm, peak_kind = peaks()
+    g_ms = statistics.mean(kt["gather_shard"])
+    s_ms = statistics.mean(kt["score"])
+    gather_achieved = 2 * sp0.bytes / (g_ms / 1e3) / 1e9
+    score_achieved = scorer.bytes_read / (s_ms / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic("gather_bulk_kernel" if sp0.bulk_ok and args.variant != 1 else "gather_lsu_kernel")
+
+    if rank != 0:
+        return 0
+    line = {
+        "metric": "composite-checkpoint merge GB/s (score+select+merge) vs HBM roofline",
+        "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8 (payload bytes) / f32->f64 (scores)", "data": "synthetic",
+        "config": {"workload": args.workload, "description": desc, "model": "Llama-3.1-8B-shaped (reference ModelSpec)",
+                   "params": fam.parameter_count, "zero_ranks": N, "snapshots": K, "rho": rho,
+                   "unit_of_work": "one ZeRO rank partition per GPU (optimizer shard + weights share)",
+                   "composite_bytes_per_gpu_step": composite, "parallelism": f"zero-partition x{world}",
+                   "l2": "inputs 62 GB/GPU >> 126 MB L2 (no flush needed)",
+                   "gather_variant": {0: "auto", 1: "lsu", 2: "bulk"}[args.variant],
+                   "plan_ms_uncached": round(plan_ms, 3), "min_boundary_gap": state["gap"]},
+        "layers_scored_per_s": round(scores_per_s, 1),
+        "kernels_ms": {k: round(statistics.mean(x), 4) for k, x in kt.items()},
+        "roofline": {"bound": "hbm", "kernel": "K2 gather (rank shard partition)",
+                     "achieved": round(gather_achieved, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(gather_achieved / hbm, 4), "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": 2 * sp0.bytes,
+                     "traffic": traffic, "traffic_source": traffic_src},
+        "scorer_roofline": {"achieved": round(score_achieved, 1), "peak": hbm, "unit": "GB/s",
+                            "frac": round(score_achieved / hbm, 4), "bytes_per_launch": scorer.bytes_read},
+        "gpu_launches": args.steps * 4,
+        "clocks": clocks.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if not args.no_cpu_baseline and world == 1 and ref_tool_path().exists():
+        work = pathlib.Path(tempfile.mkdtemp(prefix="tailor-cpu-"))
+        try:
+            cores = os.cpu_count() or 1
+            dt, comp, _ = run_reference_sample(work, cores)
+            L2, h2, f2, v2, _, N2, K2, rho2 = SAMPLE
+            line["cpu_baseline"] = {"value": round(comp / dt / 1e9, 4), "unit": "GB/s", "cores": cores,
+                                    "kind": "reference",
+                                    "sample": f"reference select-merge on L{L2} h{h2} f{f2} v{v2} N{N2} K{K2}, "
+                                              f"{comp / 1e9:.3f} GB composite, {dt:.1f} s, files in /tmp"}
+        finally:
+            shutil.rmtree(work, ignore_errors=True)
+    print(json.dumps(line))
+    return 0
+
+
+def e2e_run(args, t, torch, fam, scorer, shards, wbufs, wlo, yaml, r, N, world, dev, sp, K, M, rho):
+    """Same step, host buffers: H2D the masters for scoring, then the shard pipeline."""
+    import torch.distributed as dist
+
+    try:
+        hshards = [b.cpu().pin_memory() for b in shards]
+        hw = [b.cpu().pin_memory() for b in wbufs]
+    except RuntimeError as exc:  # host memory
+        return {"value": None, "unit": "GB/s", "error": f"pinned host staging failed: {exc}"}
+    stage = [torch.empty(b.numel(), dtype=torch.uint8, device=dev) for b in shards]
+    spl = t.MergePartition(fam, yaml, r)
+    wpl = t.MergePartition(fam, yaml, -1, r, N)
+    hout = torch.empty(spl.bytes, dtype=torch.uint8).pin_memory()
+    hwout = torch.empty(max(16, wpl.bytes), dtype=torch.uint8).pin_memory()
+    partials = torch.zeros((K - 1) * M * 2, dtype=torch.float64, device=dev)
+    gathered = torch.zeros(world * (K - 1) * M * 2, dtype=torch.float64, device=dev)
+    # Master fields of each snapshot partition (H2D only these for scoring).
+    master_ranges = master_byte_ranges(fam, r, K)
+    h2d_bytes = d2h_bytes = 0
+
+    def one():
+        nonlocal h2d_bytes, d2h_bytes
+        h2d = d2h = 0
+        for k in range(K):
+            for lo, hi in master_ranges:
+                stage[k][lo:hi].copy_(hshards[k][lo:hi], non_blocking=True)
+                h2d += hi - lo
+        scorer.run([b.data_ptr() for b in stage], partials.data_ptr(), sp)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, partials)
+            parts = gathered.cpu()
+        else:
+            parts = partials.cpu()
+        y, _, _, _ = fam.select(parts.tolist(), world, rho)
+        assert y == yaml
+        a, b = spl.run_host([hshards[k - 1].data_ptr() + lo for k, c, lo, hi in spl.windows()], hout.data_ptr(),
+                            args.variant)
+        h2d += a
+        d2h += b
+        a, b = wpl.run_host([hw[k - 1].data_ptr() + (lo - wlo) for k, c, lo, hi in wpl.windows()], hwout.data_ptr(),
+                            args.variant)
+        h2d += a
+        d2h += b + parts.numel() * 8
+        h2d_bytes, d2h_bytes = h2d, d2h
+
+    one()
+    torch.cuda.synchronize(dev)
+    steps = max(1, min(args.steps, 3))
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    torch.cuda.synchronize(dev)
+    dt = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+    comp = spl.bytes + wpl.bytes
+    return {"value": round(comp * world * steps / dt / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d_bytes,
+            "d2h_bytes_per_step": d2h_bytes, "steps": steps, "ms_per_step": round(dt / steps * 1e3, 2),
+            "path": "tg_mplan_run_host (C ABI) + H2D of master fields for tg_scorer_run; pinned host sources"}
+
+
+def master_byte_ranges(fam, r, K):
+    """Byte ranges of the g*.master entries in rank r's shard payload (from the oracle-free layout)."""
+    import json as _json
+
+    lm = __import__("paper_2602_22158_b200").layer_map(fam.spec, fam.num_ranks)
+    # Recreate the container order: lexicographic keys g<i>.exp_avg, g<i>.exp_avg_sq, g<i>.master
+    keys = []
+    for g in lm["groups"]:
+        for fld in (".exp_avg", ".exp_avg_sq", ".master"):
+            keys.append((f"g{g['index']}{fld}", g["shard_length"] * 4))
+    keys.sort(key=lambda x: x[0].encode())
+    out, off = [], 0
+    for name, n in keys:
+        if name.endswith(".master"):
+            out.append((off, off + n))
+        off += n
+    assert off == fam.shard_bytes(1, r)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3")
+    ap.add_argument("--variant", type=int, default=0, help="gather: 0 auto, 1 LSU, 2 TMA bulk")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return our_arm(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

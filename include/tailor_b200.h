@@ -1,0 +1,188 @@
+/*
+ * tailor_b200.h — C ABI of the B200-native checkpoint-tailoring hot path.
+ *
+ * The reference (LLMTailor C++ library, /root/reference/proj) exposes this
+ * path only as C++ (R/include/tailor/merge.hpp, R/include/tailor/recipe.hpp)
+ * and as the `tailor merge` / `tailor plan` CLI; it has no FFI. These entry
+ * points are what a binding of that path (ctypes, cgo, JNI) needs: plain
+ * pointers, sizes and int codes; no C++ or torch types, no exceptions.
+ * Each function cites the reference interface it replaces.
+ *
+ * Errors: every int-returning function returns TG_OK (0) or the reference's
+ * ErrorKind code below; tg_last_error() holds the message (thread-local).
+ * User errors (codes 1..9) are the reference's exit-code-1 class; 10, 11, 12
+ * and 100 are internal (exit 2), as R/include/tailor/errors.hpp:51-54.
+ *
+ * Device pointers are CUDA global-memory addresses on the current device;
+ * `stream` is a cudaStream_t (NULL = legacy default stream). Launches are
+ * asynchronous on that stream; the caller synchronizes.
+ */
+#ifndef TAILOR_B200_H
+#define TAILOR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    TG_OK = 0,
+    TG_E_INVALID_MODULE = 1,
+    TG_E_GEOMETRY = 2,
+    TG_E_NON_FINITE = 3,
+    TG_E_RECIPE = 4,
+    TG_E_SOURCE_LACKS_MODULE = 5,
+    TG_E_MISSING_ARTIFACT = 6,
+    TG_E_CORRUPT_CONTAINER = 7,
+    TG_E_UNRECOVERABLE_MODULE = 8,
+    TG_E_MISSING_MODULES = 9,
+    TG_E_CONSISTENCY = 10,
+    TG_E_STORAGE = 11,
+    TG_E_DEVICE = 12,
+    TG_E_INTERNAL = 100
+};
+
+/* ModelSpec (R/include/tailor/model.hpp:14-30). */
+typedef struct tg_model_spec {
+    int32_t num_layers;
+    int32_t hidden_dim;
+    int32_t ffn_dim;
+    int32_t vocab_size;
+    int32_t weight_tied;
+    int32_t reserved;
+    uint64_t seed;
+} tg_model_spec;
+
+/* MergeOptions / MergeStats (R/include/tailor/merge.hpp:46-55), extended with
+ * device timing and the composite byte count. */
+typedef struct tg_merge_options {
+    int32_t workers;  /* host read threads; 0 = num_ranks */
+    int32_t uncached; /* reload source shard per group copy (benchmark mode) */
+    int32_t device;
+    int32_t verify; /* device re-verify of the output (reference always re-verifies) */
+} tg_merge_options;
+
+typedef struct tg_merge_stats {
+    int64_t shard_files_read;
+    int64_t weight_files_read;
+    double wall_ms;
+    double device_ms;
+    uint64_t bytes_moved;
+} tg_merge_stats;
+
+/* K2 segment: dst[dst_off, dst_off+bytes) <- src[0, bytes). */
+typedef struct tg_gather_seg {
+    const uint8_t* src;
+    uint64_t dst_off;
+    uint64_t bytes;
+} tg_gather_seg;
+
+/* K3 tile over `count` master elements of field `field` of module `module`. */
+typedef struct tg_score_tile {
+    uint32_t module;
+    uint32_t field;
+    uint32_t count;
+    uint32_t pad;
+    uint64_t elem_start;
+} tg_score_tile;
+
+typedef struct tg_family tg_family;
+typedef struct tg_scorer tg_scorer;
+typedef struct tg_mplan tg_mplan;
+
+/* ---- errors / info ---------------------------------------------------------- */
+const char* tg_last_error(void);
+int tg_last_error_kind(void);
+const char* tg_version(void);
+int tg_device_count(void);
+
+/* ---- L5 drop-ins on checkpoint directories ------------------------------------
+ * Text outputs (JSON / YAML) use the (buf, cap, needed) convention: `needed`
+ * receives strlen+1; the call fails with TG_E_GEOMETRY if cap is too small. */
+
+/* parse_recipe (R/src/recipe.cpp:67-132) -> recipe as JSON. */
+int tg_parse_recipe(const char* yaml, char* json_out, size_t cap, size_t* needed);
+/* recipe_to_yaml (R/src/recipe.cpp:139-169) of a JSON recipe. */
+int tg_recipe_to_yaml(const char* recipe_json, char* yaml_out, size_t cap, size_t* needed);
+/* resolve_plan (R/src/merge.cpp:39-152) -> MergePlan as JSON. */
+int tg_resolve_plan(const char* recipe_yaml, char* plan_json, size_t cap, size_t* needed);
+/* cmd_merge -> execute_merge (R/tools/tailor_main.cpp:75-103, R/src/merge.cpp:226-357). */
+int tg_execute_merge(const char* recipe_yaml, const char* out_dir, const tg_merge_options* options,
+                     tg_merge_stats* stats);
+/* recipe_from_manifests (R/src/merge.cpp:359-418) -> recipe YAML. */
+int tg_recipe_from_manifests(const char* run_dir, int64_t failure_step, char* yaml_out, size_t cap, size_t* needed);
+/* read_checkpoint's invariants (R/src/checkpoint.cpp:485-575), checked on the device. */
+int tg_verify_checkpoint(const char* dir, int32_t device);
+/* Update-magnitude scores of consecutive snapshot directories on the device
+ * (SURVEY §8 a13): sums[(p*M + m)*2 + {0,1}] = (sum delta^2, sum ref^2) of
+ * pair p = (dirs[p], dirs[p+1]); scores[p*M + m]. Capacity: (n-1)*M. */
+int tg_score_snapshots(const char* const* dirs, int32_t n, int32_t device, double* sums, double* scores,
+                       int32_t* num_modules);
+/* Score -> magnitude selection (a14) -> recipe (latest-version rule,
+ * R/src/merge.cpp:375-417). source_of[m] = index into dirs. */
+int tg_select_recipe(const char* const* dirs, int32_t n, double rho, int32_t device, char* yaml_out, size_t cap,
+                     size_t* needed, int32_t* source_of, double* min_boundary_gap);
+/* Layer map (R/src/model.cpp, R/src/groups.cpp, R/src/shard.cpp) as JSON. */
+int tg_layer_map(const tg_model_spec* spec, int32_t num_ranks, char* json_out, size_t cap, size_t* needed);
+
+/* ---- device primitives (caller-owned buffers) ---------------------------------- */
+/* variant: 0 auto, 1 LSU vector path, 2 TMA bulk path (requires bulk_ok). */
+int tg_gather(const tg_gather_seg* d_segs, uint32_t nseg, uint8_t* d_dst, uint64_t dst_bytes, int32_t variant,
+              int32_t bulk_ok, void* stream);
+int tg_score_partials(const tg_score_tile* d_tiles, uint32_t ntiles, const float* const* d_field_base,
+                      uint32_t nfields, int32_t K, int32_t vec_ok, double* d_tile_partials, void* stream);
+int tg_score_combine(const double* d_tile_partials, const uint32_t* d_module_tile_begin, int32_t M, int32_t K,
+                     double* d_out, void* stream);
+
+/* ---- synthetic snapshot families S_1..S_K --------------------------- */
+tg_family* tg_family_create(const tg_model_spec* spec, int32_t num_ranks, int32_t snapshots, int64_t interval);
+void tg_family_destroy(tg_family* f);
+int tg_family_set_partial(tg_family* f, int32_t k, const char* modules_csv);
+int tg_family_set_id(tg_family* f, int32_t k, const char* id);
+int32_t tg_family_num_modules(const tg_family* f);
+uint64_t tg_family_shard_bytes(tg_family* f, int32_t k, int32_t rank);
+uint64_t tg_family_weights_bytes(tg_family* f, int32_t k);
+uint64_t tg_family_packed_master_bytes(tg_family* f, int32_t rank);
+uint64_t tg_family_parameter_count(tg_family* f);
+int tg_family_gen_shard(tg_family* f, int32_t rank, int32_t k0, int32_t k1, uint8_t* const* outs, void* stream);
+int tg_family_gen_weights(tg_family* f, int32_t k0, int32_t k1, uint64_t lo, uint64_t hi, uint8_t* const* outs,
+                          void* stream);
+int tg_family_gen_masters(tg_family* f, int32_t rank, int32_t k0, int32_t k1, uint8_t* const* outs, void* stream);
+int tg_family_write_dir(tg_family* f, int32_t k, const char* dir);
+/* Combine per-rank partials [nranks][K-1][M][2] in rank order, select (a14),
+ * emit the recipe over the family's snapshot ids. */
+int tg_family_select(tg_family* f, const double* rank_partials, int32_t nranks, double rho, char* yaml_out,
+                     size_t cap, size_t* needed, int32_t* source_of, double* scores, double* min_boundary_gap);
+
+/* Scorer over snapshots k0..k1 of a family, rank partition `rank`; packed=1 reads
+ * tg_family_gen_masters buffers, packed=0 full shard payloads. */
+tg_scorer* tg_scorer_create(tg_family* f, int32_t rank, int32_t k0, int32_t k1, int32_t packed);
+void tg_scorer_destroy(tg_scorer* s);
+uint64_t tg_scorer_bytes(const tg_scorer* s);
+/* d_out: [K-1][M][2] FP64 partial sums for this rank. */
+int tg_scorer_run(tg_scorer* s, const uint8_t* const* bases, double* d_out, void* stream);
+
+/* Merge plan of one output partition of a recipe over family snapshots:
+ * container = -1 -> weights bytes of share unit/units, r >= 0 -> rank r shard. */
+tg_mplan* tg_mplan_create(tg_family* f, const char* recipe_yaml, int32_t container, int32_t unit, int32_t units);
+void tg_mplan_destroy(tg_mplan* p);
+uint64_t tg_mplan_bytes(const tg_mplan* p);
+int tg_mplan_range(const tg_mplan* p, uint64_t* lo, uint64_t* hi, uint64_t* payload_bytes);
+int32_t tg_mplan_num_windows(const tg_mplan* p);
+int tg_mplan_window(const tg_mplan* p, int32_t i, int32_t* snapshot, int32_t* container, uint64_t* lo, uint64_t* hi);
+uint32_t tg_mplan_num_segments(const tg_mplan* p);
+int tg_mplan_prefix(const tg_mplan* p, char* out, size_t cap, size_t* needed); /* 8-B length + header */
+int tg_mplan_bind(tg_mplan* p, const uint8_t* const* window_ptrs);
+int32_t tg_mplan_bulk_ok(const tg_mplan* p);
+int tg_mplan_run(tg_mplan* p, uint8_t* d_dst, int32_t variant, void* stream);
+/* Shard pipeline: host windows -> H2D (needed bytes only) -> K2 -> D2H into h_dst. */
+int tg_mplan_run_host(tg_mplan* p, const uint8_t* const* h_windows, uint8_t* h_dst, int32_t variant,
+                      uint64_t chunk_bytes, uint64_t* h2d_bytes, uint64_t* d2h_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TAILOR_B200_H */

@@ -1,0 +1,577 @@
+// The C ABI (include/tailor_b200.h) over the C++ engine. Every entry point
+// catches: no exception crosses the boundary; the error kind becomes the
+// return code and the message goes to tg_last_error().
+#include "tailor_b200.h"
+
+#include <cmath>
+#include <cstring>
+#include <filesystem>
+#include <fcntl.h>
+#include <memory>
+#include <string>
+#include <unistd.h>
+
+#include <json.hpp>
+
+#include "tailor/engine.hpp"
+#include "tailor/errors.hpp"
+#include "tailor/merge.hpp"
+
+using nlohmann::json;
+using namespace tailor;
+namespace fs = std::filesystem;
+
+struct tg_family {
+    std::unique_ptr<SynthFamily> fam;
+};
+struct tg_scorer {
+    std::unique_ptr<ScorePlan> plan;
+};
+struct tg_mplan {
+    std::unique_ptr<DeviceMerge> dev;
+    std::unique_ptr<HostMerge> host;
+    std::uint64_t host_chunk = 0;
+    std::vector<int> window_k;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_kind = 0;
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        g_err.clear();
+        g_kind = 0;
+        return TG_OK;
+    } catch (const TailorError& e) {
+        g_err = e.what();
+        g_kind = static_cast<int>(e.kind());
+    } catch (const std::exception& e) {
+        g_err = std::string("internal error: ") + e.what();
+        g_kind = TG_E_INTERNAL;
+    }
+    return g_kind;
+}
+
+int put_text(const std::string& s, char* out, size_t cap, size_t* needed) {
+    if (needed) *needed = s.size() + 1;
+    if (!out || cap < s.size() + 1) fail(ErrorKind::Geometry, "output buffer too small (need " + std::to_string(s.size() + 1) + ")");
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+}
+
+ModelSpec to_spec(const tg_model_spec* s) {
+    if (!s) fail(ErrorKind::Geometry, "null model spec");
+    ModelSpec m;
+    m.num_layers = s->num_layers;
+    m.hidden_dim = s->hidden_dim;
+    m.ffn_dim = s->ffn_dim;
+    m.vocab_size = s->vocab_size;
+    m.weight_tied = s->weight_tied != 0;
+    m.seed = s->seed;
+    m.validate();
+    return m;
+}
+
+json recipe_json(const MergeRecipe& r) {
+    json slices = json::array();
+    for (const auto& s : r.slices) slices.push_back({{"source", s.source}, {"layers", s.layers}, {"targets", s.targets}});
+    json aux = json::object();
+    for (const auto& [k, v] : r.aux) aux[k] = v;
+    return {{"base_checkpoint", r.base_checkpoint}, {"num_ranks", r.num_ranks}, {"slices", slices},
+            {"aux", aux}, {"config_from", r.config_from}};
+}
+
+MergeRecipe recipe_from_json(const json& j) {
+    MergeRecipe r;
+    r.base_checkpoint = j.value("base_checkpoint", std::string());
+    r.num_ranks = j.value("num_ranks", 0);
+    if (j.contains("slices"))
+        for (const auto& s : j.at("slices")) {
+            RecipeSlice sl;
+            sl.source = s.at("source").get<std::string>();
+            sl.layers = s.at("layers").get<std::vector<int>>();
+            sl.targets = s.contains("targets") ? s.at("targets").get<std::vector<int>>() : sl.layers;
+            r.slices.push_back(sl);
+        }
+    if (j.contains("aux"))
+        for (const auto& [k, v] : j.at("aux").items()) r.aux[k] = v.get<std::string>();
+    r.config_from = j.value("config_from", std::string("latest"));
+    return r;
+}
+
+json plan_json(const MergePlan& p) {
+    json copies = json::array();
+    for (const auto& c : p.group_copies)
+        copies.push_back({{"source", c.source}, {"source_group", c.source_group}, {"target_group", c.target_group}});
+    json assign = json::object();
+    for (const auto& [t, a] : p.assignment)
+        assign[module_name(t)] = {{"source", a.source}, {"source_module", module_name(a.source_module)},
+                                  {"source_step", a.source_step}};
+    return {{"num_ranks", p.num_ranks}, {"config_source", p.config_source}, {"sources", p.sources},
+            {"group_copies", copies}, {"assignment", assign}};
+}
+
+CheckpointSummary family_summary(const SynthFamily& f, const std::string& id) {
+    const int k = f.index_of(id);
+    if (k == 0) fail(ErrorKind::MissingArtifact, "checkpoint directory '" + id + "' does not exist");
+    return f.summary(k, id);
+}
+
+// Reads each snapshot's rank-r master fields into one packed device buffer.
+void load_packed_masters(const std::vector<std::string>& dirs, int rank, const ModelLayout& model, int num_ranks,
+                         std::vector<DeviceBuffer>& out, std::vector<std::vector<std::uint64_t>>& offs) {
+    const auto fields = score_fields(model, num_ranks);
+    out.clear();
+    out.resize(dirs.size());
+    offs.assign(dirs.size(), {});
+    PinnedBuffer stage;
+    for (std::size_t k = 0; k < dirs.size(); ++k) {
+        const fs::path p = shard_path(dirs[k], rank);
+        const ContainerLayout lay = read_layout(p);
+        std::uint64_t total = 0;
+        std::vector<std::pair<const Entry*, std::uint64_t>> where;
+        for (const auto& f : fields) {
+            const Entry* e = lay.find(shard_key(f.group, ".master"));
+            if (!e) fail(ErrorKind::MissingModules, p.string() + ": scoring needs every module; missing '" + shard_key(f.group, ".master") + "'");
+            if (e->dtype != Dtype::F32 || e->shape != std::vector<std::int64_t>{f.chunk})
+                fail(ErrorKind::Geometry, p.string() + ": master '" + e->name + "' has unexpected dtype/shape");
+            where.push_back({e, total});
+            offs[k].push_back(total);
+            total = (total + e->bytes() + 15) & ~15ull;
+        }
+        stage.resize(std::max<std::uint64_t>(16, total));
+        const int fd = ::open(p.c_str(), O_RDONLY);
+        if (fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + p.string() + "'");
+        for (const auto& [e, at] : where) {
+            std::uint64_t got = 0;
+            while (got < e->bytes()) {
+                const ssize_t r = ::pread(fd, stage.get() + at + got, e->bytes() - got,
+                                          static_cast<off_t>(lay.payload_offset() + e->begin + got));
+                if (r <= 0) {
+                    ::close(fd);
+                    fail(ErrorKind::Storage, "read failed for '" + p.string() + "'");
+                }
+                got += static_cast<std::uint64_t>(r);
+            }
+        }
+        ::close(fd);
+        out[k].resize(std::max<std::uint64_t>(16, total));
+        cuda_check(cudaMemcpy(out[k].get(), stage.get(), total, cudaMemcpyHostToDevice), "H2D");
+    }
+}
+
+// Device scores over snapshot directories: per rank, packed masters -> K3/K4;
+// ranks combined in rank order on the host (FP64, fixed order).
+void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<std::vector<double>>& sd,
+                std::vector<std::vector<double>>& sr, std::vector<CheckpointSummary>& sums) {
+    if (dirs.size() < 2) fail(ErrorKind::Recipe, "scoring needs at least two snapshots");
+    if (dirs.size() > 16) fail(ErrorKind::Geometry, "at most 16 snapshots per scoring sweep");
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    sums.clear();
+    for (const auto& d : dirs) sums.push_back(read_checkpoint_summary(d));
+    const ModelSpec& spec = sums.front().spec;
+    const int N = sums.front().optim.num_ranks;
+    for (const auto& s : sums) {
+        if (!s.spec.same_geometry(spec)) fail(ErrorKind::Geometry, "snapshots disagree on model geometry");
+        if (s.optim.num_ranks != N) fail(ErrorKind::Geometry, "snapshots disagree on the rank count");
+        if (s.optim.grouping != Grouping::Fine) fail(ErrorKind::Geometry, "scoring needs the fine grouping");
+    }
+    const ModelLayout model(spec);
+    const int K = static_cast<int>(dirs.size()), M = model.module_count();
+    sd.assign(static_cast<std::size_t>(K - 1), std::vector<double>(static_cast<std::size_t>(M), 0.0));
+    sr = sd;
+    DeviceBuffer dout(static_cast<std::size_t>(K - 1) * M * 2 * sizeof(double));
+    std::vector<double> h(static_cast<std::size_t>(K - 1) * M * 2);
+    for (int r = 0; r < N; ++r) {
+        std::vector<DeviceBuffer> bufs;
+        std::vector<std::vector<std::uint64_t>> offs;
+        load_packed_masters(dirs, r, model, N, bufs, offs);
+        ScorePlan plan(model, N, offs);
+        std::vector<const std::uint8_t*> bases;
+        for (auto& b : bufs) bases.push_back(b.get());
+        plan.run(bases.data(), dout.get<double>(), nullptr);
+        cuda_check(cudaMemcpy(h.data(), dout.get(), h.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+        for (int p = 0; p < K - 1; ++p)
+            for (int m = 0; m < M; ++m) {
+                sd[static_cast<std::size_t>(p)][static_cast<std::size_t>(m)] += h[(static_cast<std::size_t>(p) * M + m) * 2];
+                sr[static_cast<std::size_t>(p)][static_cast<std::size_t>(m)] += h[(static_cast<std::size_t>(p) * M + m) * 2 + 1];
+            }
+    }
+}
+
+} // namespace
+
+extern "C" {
+
+const char* tg_last_error(void) { return g_err.c_str(); }
+int tg_last_error_kind(void) { return g_kind; }
+const char* tg_version(void) { return "tailor-b200 0.1 (sm_100a)"; }
+int tg_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int tg_parse_recipe(const char* yaml, char* out, size_t cap, size_t* needed) {
+    return guard([&] { put_text(recipe_json(parse_recipe(yaml ? yaml : "")).dump(), out, cap, needed); });
+}
+
+int tg_recipe_to_yaml(const char* rj, char* out, size_t cap, size_t* needed) {
+    return guard([&] { put_text(recipe_to_yaml(recipe_from_json(json::parse(rj ? rj : "{}"))), out, cap, needed); });
+}
+
+int tg_resolve_plan(const char* yaml, char* out, size_t cap, size_t* needed) {
+    return guard([&] { put_text(plan_json(resolve_plan(parse_recipe(yaml ? yaml : ""))).dump(), out, cap, needed); });
+}
+
+int tg_execute_merge(const char* yaml, const char* out_dir, const tg_merge_options* o, tg_merge_stats* st) {
+    return guard([&] {
+        const MergePlan plan = resolve_plan(parse_recipe(yaml ? yaml : ""));
+        MergeOptions opt;
+        if (o) {
+            opt.workers = o->workers;
+            opt.uncached = o->uncached != 0;
+            opt.device = o->device;
+            opt.verify = o->verify != 0;
+        }
+        const MergeStats s = execute_merge(plan, out_dir ? out_dir : "", opt);
+        if (st) {
+            st->shard_files_read = s.shard_files_read;
+            st->weight_files_read = s.weight_files_read;
+            st->wall_ms = s.wall_ms;
+            st->device_ms = s.device_ms;
+            st->bytes_moved = s.bytes_moved;
+        }
+    });
+}
+
+int tg_recipe_from_manifests(const char* run_dir, int64_t failure_step, char* out, size_t cap, size_t* needed) {
+    return guard([&] { put_text(recipe_to_yaml(recipe_from_manifests(run_dir ? run_dir : "", failure_step)), out, cap, needed); });
+}
+
+int tg_verify_checkpoint(const char* dir, int32_t device) {
+    return guard([&] { verify_checkpoint_dir(dir ? dir : "", device); });
+}
+
+int tg_score_snapshots(const char* const* dirs, int32_t n, int32_t device, double* sums, double* scores, int32_t* nm) {
+    return guard([&] {
+        std::vector<std::string> ds(dirs, dirs + n);
+        std::vector<std::vector<double>> sd, sr;
+        std::vector<CheckpointSummary> summ;
+        score_dirs(ds, device, sd, sr, summ);
+        const int M = static_cast<int>(sd.front().size());
+        if (nm) *nm = M;
+        for (std::size_t p = 0; p < sd.size(); ++p)
+            for (int m = 0; m < M; ++m) {
+                if (sums) {
+                    sums[(p * M + m) * 2] = sd[p][static_cast<std::size_t>(m)];
+                    sums[(p * M + m) * 2 + 1] = sr[p][static_cast<std::size_t>(m)];
+                }
+                if (scores) scores[p * M + m] = magnitude_score(sd[p][static_cast<std::size_t>(m)], sr[p][static_cast<std::size_t>(m)]);
+            }
+    });
+}
+
+int tg_select_recipe(const char* const* dirs, int32_t n, double rho, int32_t device, char* out, size_t cap,
+                     size_t* needed, int32_t* source_of, double* min_gap) {
+    return guard([&] {
+        std::vector<std::string> ds(dirs, dirs + n);
+        std::vector<std::vector<double>> sd, sr;
+        std::vector<CheckpointSummary> summ;
+        score_dirs(ds, device, sd, sr, summ);
+        std::vector<std::vector<double>> sc = sd;
+        for (std::size_t p = 0; p < sd.size(); ++p)
+            for (std::size_t m = 0; m < sd[p].size(); ++m) sc[p][m] = magnitude_score(sd[p][m], sr[p][m]);
+        const Selection sel = select_by_magnitude(sc, static_cast<int>(sd.front().size()), rho);
+        if (source_of)
+            for (std::size_t m = 0; m < sel.source_of.size(); ++m) source_of[m] = sel.source_of[m];
+        if (min_gap) *min_gap = sel.min_boundary_gap;
+        put_text(recipe_to_yaml(recipe_from_selection(summ, sel)), out, cap, needed);
+    });
+}
+
+int tg_layer_map(const tg_model_spec* spec, int32_t num_ranks, char* out, size_t cap, size_t* needed) {
+    return guard([&] {
+        const ModelLayout model(to_spec(spec));
+        const ShardGeometry geom{num_ranks};
+        json mods = json::array();
+        for (int m = 0; m < model.module_count(); ++m) {
+            json ts = json::array();
+            for (const auto& t : tensors_of(model.spec(), model.modules()[static_cast<std::size_t>(m)]))
+                ts.push_back({{"name", t.name}, {"shape", t.shape}, {"decay", t.decay == DecayClass::Decay ? "decay" : "no_decay"}});
+            mods.push_back({{"name", module_name(model.modules()[static_cast<std::size_t>(m)])},
+                            {"model_offset", model.module_offset(m)},
+                            {"tensors", ts},
+                            {"groups", group_indices_for(model.table(), model.modules()[static_cast<std::size_t>(m)])}});
+        }
+        json groups = json::array();
+        for (const auto& g : model.table().groups) {
+            json sl = json::array();
+            for (const auto& s : model.slices(g.index))
+                sl.push_back({{"name", s.decl.name}, {"group_offset", s.group_offset}, {"model_offset", s.model_offset}});
+            groups.push_back({{"index", g.index}, {"owner", module_name(*g.owner)},
+                              {"decay", g.decay == DecayClass::Decay ? "decay" : "no_decay"},
+                              {"true_length", g.element_count}, {"padded_length", geom.padded_length(g.element_count)},
+                              {"shard_length", geom.shard_length(g.element_count)}, {"slices", sl}});
+        }
+        put_text(json{{"modules", mods}, {"groups", groups}, {"parameters", model.parameter_count()}}.dump(), out, cap, needed);
+    });
+}
+
+int tg_gather(const tg_gather_seg* d_segs, uint32_t nseg, uint8_t* d_dst, uint64_t dst_bytes, int32_t variant,
+              int32_t bulk_ok, void* stream) {
+    return guard([&] {
+        cuda_check(dev::launch_gather(reinterpret_cast<const dev::GatherSeg*>(d_segs), nseg, d_dst, dst_bytes, variant,
+                                      bulk_ok != 0, static_cast<cudaStream_t>(stream)),
+                   "tg_gather");
+    });
+}
+
+int tg_score_partials(const tg_score_tile* d_tiles, uint32_t ntiles, const float* const* d_field_base, uint32_t nfields,
+                      int32_t K, int32_t vec_ok, double* d_tile_partials, void* stream) {
+    return guard([&] {
+        cuda_check(dev::launch_score_partials(reinterpret_cast<const dev::ScoreTile*>(d_tiles), ntiles, d_field_base, nfields,
+                                              K, vec_ok != 0, d_tile_partials, static_cast<cudaStream_t>(stream)),
+                   "tg_score_partials");
+    });
+}
+
+int tg_score_combine(const double* d_tile_partials, const uint32_t* d_begin, int32_t M, int32_t K, double* d_out,
+                     void* stream) {
+    return guard([&] {
+        cuda_check(dev::launch_score_combine(d_tile_partials, d_begin, M, K, d_out, static_cast<cudaStream_t>(stream)),
+                   "tg_score_combine");
+    });
+}
+
+tg_family* tg_family_create(const tg_model_spec* spec, int32_t num_ranks, int32_t snapshots, int64_t interval) {
+    tg_family* out = nullptr;
+    guard([&] { out = new tg_family{std::make_unique<SynthFamily>(to_spec(spec), num_ranks, snapshots, interval)}; });
+    return out;
+}
+
+void tg_family_destroy(tg_family* f) { delete f; }
+
+int tg_family_set_partial(tg_family* f, int32_t k, const char* csv) {
+    return guard([&] {
+        std::vector<ModuleId> mods;
+        std::string cur;
+        for (const char* c = csv; c && *c; ++c) {
+            if (*c == ',') {
+                if (!cur.empty()) mods.push_back(parse_module_name(cur));
+                cur.clear();
+            } else {
+                cur.push_back(*c);
+            }
+        }
+        if (!cur.empty()) mods.push_back(parse_module_name(cur));
+        f->fam->set_partial(k, mods);
+    });
+}
+
+int tg_family_set_id(tg_family* f, int32_t k, const char* id) {
+    return guard([&] {
+        if (k < 1 || k > f->fam->snapshots()) fail(ErrorKind::Geometry, "snapshot index out of range");
+        f->fam->set_id(k, id ? id : "");
+    });
+}
+
+int32_t tg_family_num_modules(const tg_family* f) { return f->fam->model().module_count(); }
+
+uint64_t tg_family_shard_bytes(tg_family* f, int32_t k, int32_t rank) {
+    uint64_t n = 0;
+    guard([&] { n = f->fam->layout(k).shards.at(static_cast<std::size_t>(rank)).payload_bytes; });
+    return n;
+}
+
+uint64_t tg_family_weights_bytes(tg_family* f, int32_t k) {
+    uint64_t n = 0;
+    guard([&] { n = f->fam->layout(k).weights.payload_bytes; });
+    return n;
+}
+
+uint64_t tg_family_packed_master_bytes(tg_family* f, int32_t rank) {
+    uint64_t n = 0;
+    guard([&] { n = f->fam->packed_master_bytes(rank); });
+    return n;
+}
+
+uint64_t tg_family_parameter_count(tg_family* f) { return static_cast<uint64_t>(f->fam->model().parameter_count()); }
+
+int tg_family_gen_shard(tg_family* f, int32_t rank, int32_t k0, int32_t k1, uint8_t* const* outs, void* stream) {
+    return guard([&] { f->fam->gen_shard(rank, k0, k1, outs, static_cast<cudaStream_t>(stream)); });
+}
+
+int tg_family_gen_weights(tg_family* f, int32_t k0, int32_t k1, uint64_t lo, uint64_t hi, uint8_t* const* outs,
+                          void* stream) {
+    return guard([&] { f->fam->gen_weights(k0, k1, lo, hi, outs, static_cast<cudaStream_t>(stream)); });
+}
+
+int tg_family_gen_masters(tg_family* f, int32_t rank, int32_t k0, int32_t k1, uint8_t* const* outs, void* stream) {
+    return guard([&] { f->fam->gen_masters_packed(rank, k0, k1, outs, static_cast<cudaStream_t>(stream)); });
+}
+
+int tg_family_write_dir(tg_family* f, int32_t k, const char* dir) {
+    return guard([&] { f->fam->write_dir(k, dir ? dir : ""); });
+}
+
+int tg_family_select(tg_family* f, const double* parts, int32_t nranks, double rho, char* out, size_t cap,
+                     size_t* needed, int32_t* source_of, double* scores, double* min_gap) {
+    return guard([&] {
+        const SynthFamily& fam = *f->fam;
+        const int K = fam.snapshots(), M = fam.model().module_count();
+        std::vector<std::vector<double>> sc(static_cast<std::size_t>(K - 1), std::vector<double>(static_cast<std::size_t>(M)));
+        for (int p = 0; p < K - 1; ++p)
+            for (int m = 0; m < M; ++m) {
+                double d2 = 0.0, r2 = 0.0;
+                for (int r = 0; r < nranks; ++r) { // rank order == canonical chunk order
+                    const std::size_t at = ((static_cast<std::size_t>(r) * (K - 1) + p) * M + m) * 2;
+                    d2 += parts[at];
+                    r2 += parts[at + 1];
+                }
+                sc[static_cast<std::size_t>(p)][static_cast<std::size_t>(m)] = magnitude_score(d2, r2);
+                if (scores) scores[static_cast<std::size_t>(p) * M + m] = sc[static_cast<std::size_t>(p)][static_cast<std::size_t>(m)];
+            }
+        const Selection sel = select_by_magnitude(sc, M, rho);
+        std::vector<CheckpointSummary> summ;
+        for (int k = 1; k <= K; ++k) summ.push_back(fam.summary(k, fam.id(k)));
+        if (source_of)
+            for (int m = 0; m < M; ++m) source_of[m] = sel.source_of[static_cast<std::size_t>(m)];
+        if (min_gap) *min_gap = sel.min_boundary_gap;
+        put_text(recipe_to_yaml(recipe_from_selection(summ, sel)), out, cap, needed);
+    });
+}
+
+tg_scorer* tg_scorer_create(tg_family* f, int32_t rank, int32_t k0, int32_t k1, int32_t packed) {
+    tg_scorer* out = nullptr;
+    guard([&] {
+        const SynthFamily& fam = *f->fam;
+        const auto fields = score_fields(fam.model(), fam.num_ranks());
+        std::vector<std::vector<std::uint64_t>> offs;
+        for (int k = k0; k <= k1; ++k) {
+            std::vector<std::uint64_t> o;
+            if (packed) {
+                std::uint64_t at = 0;
+                for (const auto& fl : fields) {
+                    o.push_back(at);
+                    at = (at + static_cast<std::uint64_t>(fl.chunk) * 4 + 15) & ~15ull;
+                }
+            } else {
+                const ContainerLayout& c = fam.layout(k).shards.at(static_cast<std::size_t>(rank));
+                for (const auto& fl : fields) {
+                    const Entry* e = c.find(shard_key(fl.group, ".master"));
+                    if (!e) fail(ErrorKind::MissingModules, "snapshot " + std::to_string(k) + " lacks " + shard_key(fl.group, ".master"));
+                    o.push_back(e->begin);
+                }
+            }
+            offs.push_back(std::move(o));
+        }
+        out = new tg_scorer{std::make_unique<ScorePlan>(fam.model(), fam.num_ranks(), std::move(offs))};
+    });
+    return out;
+}
+
+void tg_scorer_destroy(tg_scorer* s) { delete s; }
+uint64_t tg_scorer_bytes(const tg_scorer* s) { return s->plan->bytes_read(); }
+
+int tg_scorer_run(tg_scorer* s, const uint8_t* const* bases, double* d_out, void* stream) {
+    return guard([&] { s->plan->run(bases, d_out, static_cast<cudaStream_t>(stream)); });
+}
+
+tg_mplan* tg_mplan_create(tg_family* f, const char* yaml, int32_t container, int32_t unit, int32_t units) {
+    tg_mplan* out = nullptr;
+    guard([&] {
+        const SynthFamily& fam = *f->fam;
+        const MergePlan plan =
+            resolve_plan_with(parse_recipe(yaml ? yaml : ""), [&](const std::string& id) { return family_summary(fam, id); });
+        std::map<std::string, SourceLayout> lays;
+        const LayoutLookup lay_of = [&](const std::string& id) -> const SourceLayout& {
+            auto it = lays.find(id);
+            if (it == lays.end()) {
+                const int k = fam.index_of(id);
+                if (k == 0) fail(ErrorKind::MissingArtifact, "unknown snapshot '" + id + "'");
+                SourceLayout sl{fam.layout(k).weights, fam.layout(k).shards};
+                it = lays.emplace(id, std::move(sl)).first;
+            }
+            return it->second;
+        };
+        PartitionPlan pp;
+        if (container < 0) {
+            const PartitionPlan full = plan_weights(plan, lay_of);
+            const auto [lo, hi] = weights_share(full.out, unit, units);
+            pp = plan_weights(plan, lay_of, lo, hi);
+        } else {
+            if (container >= plan.num_ranks) fail(ErrorKind::Geometry, "rank out of range");
+            pp = plan_shard(plan, lay_of, container);
+        }
+        auto* p = new tg_mplan{};
+        for (const auto& w : pp.windows) p->window_k.push_back(fam.index_of(w.source));
+        p->dev = std::make_unique<DeviceMerge>(pp);
+        out = p;
+    });
+    return out;
+}
+
+void tg_mplan_destroy(tg_mplan* p) { delete p; }
+uint64_t tg_mplan_bytes(const tg_mplan* p) { return p->dev->bytes(); }
+
+int tg_mplan_range(const tg_mplan* p, uint64_t* lo, uint64_t* hi, uint64_t* payload) {
+    return guard([&] {
+        const PartitionPlan& pp = p->dev->plan();
+        if (lo) *lo = pp.dst_lo;
+        if (hi) *hi = pp.dst_hi;
+        if (payload) *payload = pp.out.payload_bytes;
+    });
+}
+
+int32_t tg_mplan_num_windows(const tg_mplan* p) { return static_cast<int32_t>(p->dev->plan().windows.size()); }
+
+int tg_mplan_window(const tg_mplan* p, int32_t i, int32_t* k, int32_t* container, uint64_t* lo, uint64_t* hi) {
+    return guard([&] {
+        const auto& w = p->dev->plan().windows.at(static_cast<std::size_t>(i));
+        if (k) *k = p->window_k.at(static_cast<std::size_t>(i));
+        if (container) *container = w.container;
+        if (lo) *lo = w.lo;
+        if (hi) *hi = w.hi;
+    });
+}
+
+uint32_t tg_mplan_num_segments(const tg_mplan* p) { return static_cast<uint32_t>(p->dev->plan().segments.size()); }
+
+int tg_mplan_prefix(const tg_mplan* p, char* out, size_t cap, size_t* needed) {
+    return guard([&] {
+        const std::string s = p->dev->plan().out.prefix();
+        if (needed) *needed = s.size();
+        if (!out || cap < s.size()) fail(ErrorKind::Geometry, "output buffer too small");
+        std::memcpy(out, s.data(), s.size());
+    });
+}
+
+int tg_mplan_bind(tg_mplan* p, const uint8_t* const* ptrs) {
+    return guard([&] { p->dev->bind(std::vector<const std::uint8_t*>(ptrs, ptrs + p->dev->plan().windows.size())); });
+}
+
+int32_t tg_mplan_bulk_ok(const tg_mplan* p) { return p->dev->bulk_ok() ? 1 : 0; }
+
+int tg_mplan_run(tg_mplan* p, uint8_t* d_dst, int32_t variant, void* stream) {
+    return guard([&] { p->dev->run(d_dst, variant, static_cast<cudaStream_t>(stream)); });
+}
+
+int tg_mplan_run_host(tg_mplan* p, const uint8_t* const* h_windows, uint8_t* h_dst, int32_t variant, uint64_t chunk,
+                      uint64_t* h2d, uint64_t* d2h) {
+    return guard([&] {
+        if (!p->host || p->host_chunk != chunk) {
+            p->host = std::make_unique<HostMerge>(p->dev->plan(), chunk ? chunk : (256ull << 20));
+            p->host_chunk = chunk;
+        }
+        p->host->run(std::vector<const std::uint8_t*>(h_windows, h_windows + p->dev->plan().windows.size()), h_dst, variant);
+        if (h2d) *h2d = p->host->h2d_bytes();
+        if (d2h) *d2h = p->host->d2h_bytes();
+    });
+}
+
+} // extern "C"

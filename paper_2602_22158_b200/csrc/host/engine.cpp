@@ -1,0 +1,629 @@
+// Host engine: synthetic families, scorer plans, device/host merge plans and
+// the device re-verify (see tailor/engine.hpp).
+#include "tailor/engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <fcntl.h>
+#include <filesystem>
+#include <fstream>
+#include <unistd.h>
+
+#include "tailor/errors.hpp"
+
+namespace tailor {
+
+namespace fs = std::filesystem;
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(ErrorKind::Device, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+DeviceBuffer::~DeviceBuffer() {
+    if (p_) cudaFree(p_);
+}
+
+void DeviceBuffer::resize(std::size_t n) {
+    if (n <= n_ && p_) return;
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+    if (n == 0) return;
+    cuda_check(cudaMalloc(&p_, n), "cudaMalloc");
+    n_ = n;
+}
+
+void DeviceBuffer::upload(const void* src, std::size_t n, cudaStream_t s) {
+    resize(std::max<std::size_t>(n, 1));
+    if (n == 0) return;
+    if (s) cuda_check(cudaMemcpyAsync(p_, src, n, cudaMemcpyHostToDevice, s), "upload");
+    else cuda_check(cudaMemcpy(p_, src, n, cudaMemcpyHostToDevice), "upload");
+}
+
+PinnedBuffer::~PinnedBuffer() {
+    if (p_) cudaFreeHost(p_);
+}
+
+void PinnedBuffer::resize(std::size_t n) {
+    if (n <= n_ && p_) return;
+    if (p_) cudaFreeHost(p_);
+    p_ = nullptr;
+    n_ = 0;
+    if (n == 0) return;
+    cuda_check(cudaMallocHost(&p_, n), "cudaMallocHost");
+    n_ = n;
+}
+
+// ---- synthetic family ---------------------------------------------------------
+namespace {
+
+std::uint64_t mix64(std::uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ULL;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    return z;
+}
+
+std::uint64_t hash3(std::uint64_t seed, std::uint64_t t, std::uint64_t e) {
+    std::uint64_t h = mix64(seed + 0x9E3779B97F4A7C15ULL);
+    h = mix64(h ^ (t * 0xD1B54A32D192ED03ULL));
+    return mix64(h ^ (e * 0x8CB92BA72F3D8DD7ULL));
+}
+
+constexpr std::uint64_t kPermSalt = 0x9E2AULL;
+
+std::uint64_t align16(std::uint64_t x) { return (x + 15) & ~15ull; }
+
+} // namespace
+
+std::vector<float> synth_sigma(std::uint64_t seed, int M, int j) {
+    std::vector<int> perm(static_cast<std::size_t>(M));
+    for (int i = 0; i < M; ++i) perm[static_cast<std::size_t>(i)] = i;
+    for (int i = M - 1; i >= 1; --i) {
+        const std::uint64_t r = hash3(seed ^ kPermSalt, static_cast<std::uint64_t>(j), static_cast<std::uint64_t>(i));
+        std::swap(perm[static_cast<std::size_t>(i)], perm[static_cast<std::size_t>(r % static_cast<std::uint64_t>(i + 1))]);
+    }
+    const double g = M > 1 ? std::pow(1000.0, 1.0 / static_cast<double>(M - 1)) : 1.0;
+    std::vector<float> s(static_cast<std::size_t>(M));
+    for (int m = 0; m < M; ++m)
+        s[static_cast<std::size_t>(m)] = static_cast<float>(1e-6 * std::pow(g, static_cast<double>(perm[static_cast<std::size_t>(m)])));
+    return s;
+}
+
+SynthFamily::SynthFamily(const ModelSpec& spec, int num_ranks, int snapshots, std::int64_t interval)
+    : model_(spec), num_ranks_(num_ranks), K_(snapshots), interval_(interval) {
+    if (num_ranks < 1) fail(ErrorKind::Geometry, "num_ranks must be >= 1");
+    if (snapshots < 1) fail(ErrorKind::Geometry, "need at least one snapshot");
+    if (interval < 1) fail(ErrorKind::Geometry, "interval must be >= 1");
+    modules_.assign(static_cast<std::size_t>(K_), model_.modules());
+    layouts_.resize(static_cast<std::size_t>(K_));
+    for (int k = 1; k <= K_; ++k) ids_.push_back("S" + std::to_string(k));
+}
+
+void SynthFamily::set_partial(int k, const std::vector<ModuleId>& modules) {
+    if (k < 1 || k > K_) fail(ErrorKind::Geometry, "snapshot index out of range");
+    std::vector<ModuleId> sorted;
+    for (const auto& m : model_.modules())
+        if (std::find(modules.begin(), modules.end(), m) != modules.end()) sorted.push_back(m);
+    if (sorted.empty()) fail(ErrorKind::Consistency, "manifest module list is empty");
+    modules_[static_cast<std::size_t>(k - 1)] = sorted;
+    layouts_[static_cast<std::size_t>(k - 1)].reset();
+    for (auto it = tables_.begin(); it != tables_.end();)
+        it = std::get<0>(it->first) == k ? tables_.erase(it) : std::next(it);
+}
+
+const CheckpointLayout& SynthFamily::layout(int k) const {
+    if (k < 1 || k > K_) fail(ErrorKind::Geometry, "snapshot index out of range");
+    auto& slot = const_cast<std::unique_ptr<CheckpointLayout>&>(layouts_[static_cast<std::size_t>(k - 1)]);
+    if (!slot) slot = std::make_unique<CheckpointLayout>(checkpoint_layout(model_, num_ranks_, modules_[static_cast<std::size_t>(k - 1)]));
+    return *slot;
+}
+
+int SynthFamily::index_of(const std::string& id) const {
+    for (int k = 1; k <= K_; ++k)
+        if (ids_[static_cast<std::size_t>(k - 1)] == id) return k;
+    return 0;
+}
+
+CheckpointSummary SynthFamily::summary(int k, const std::string& dir) const {
+    const CheckpointLayout& lay = layout(k);
+    CheckpointSummary s;
+    s.dir = dir;
+    s.spec = model_.spec();
+    s.trainer.step = step(k);
+    s.trainer.optimizer_t = step(k);
+    s.trainer.strategy.interval = static_cast<int>(interval_);
+    s.trainer.checkpoint_counter = k;
+    s.trainer.rng_seed = model_.spec().seed;
+    s.manifest.step = step(k);
+    s.manifest.strategy = lay.modules.size() == model_.modules().size() ? "full" : "manual";
+    s.manifest.modules = lay.modules;
+    AdamHyperparams base;
+    base.weight_decay = kDefaultWeightDecay;
+    std::map<int, AdamHyperparams> hyp;
+    for (int g : lay.groups) hyp[g] = hyper_for_class(base, model_.table().groups[static_cast<std::size_t>(g)].decay);
+    s.optim = make_optim_meta(model_.table(), hyp, ShardGeometry{num_ranks_}, step(k));
+    return s;
+}
+
+std::string SynthFamily::trainer_state_json(int k) const { return render_trainer_state_json(summary(k, "").trainer); }
+std::string SynthFamily::manifest_json(int k) const { return render_manifest_json(summary(k, "").manifest); }
+std::string SynthFamily::optim_meta_json(int k) const { return render_optim_meta_json(summary(k, "").optim); }
+
+void SynthFamily::ensure_sigma(int kmax) {
+    if (kmax <= sigma_rows_) return;
+    const int M = model_.module_count();
+    std::vector<float> all;
+    for (int j = 1; j <= kmax; ++j) {
+        const auto row = synth_sigma(model_.spec().seed, M, j);
+        all.insert(all.end(), row.begin(), row.end());
+    }
+    sigma_.upload(all.data(), all.size() * sizeof(float));
+    sigma_rows_ = kmax;
+}
+
+std::vector<ScoreField> score_fields(const ModelLayout& model, int num_ranks) {
+    const ShardGeometry geom{num_ranks};
+    std::vector<ScoreField> out;
+    for (int m = 0; m < model.module_count(); ++m)
+        for (int g : group_indices_for(model.table(), model.modules()[static_cast<std::size_t>(m)]))
+            out.push_back({m, g, geom.shard_length(model.table().groups[static_cast<std::size_t>(g)].element_count)});
+    return out;
+}
+
+std::uint64_t SynthFamily::packed_master_bytes(int /*rank*/) const {
+    std::uint64_t off = 0;
+    for (const auto& f : score_fields(model_, num_ranks_)) off = align16(off + static_cast<std::uint64_t>(f.chunk) * 4);
+    return off;
+}
+
+SynthFamily::ShardTables& SynthFamily::shard_tables(int k, int rank, bool packed) {
+    auto key = std::make_tuple(packed ? 0 : k, rank, packed);
+    auto it = tables_.find(key);
+    if (it != tables_.end()) return *it->second;
+    auto t = std::make_unique<ShardTables>();
+    const ShardGeometry geom{num_ranks_};
+    std::vector<dev::SynthGroup> groups;
+    std::vector<dev::SynthSlice> slices;
+    std::uint64_t begin = 0;
+    const auto add_group = [&](int g, std::uint64_t o_m, std::uint64_t o_v, std::uint64_t o_w) {
+        const GroupInfo& info = model_.table().groups[static_cast<std::size_t>(g)];
+        const std::int64_t chunk = geom.shard_length(info.element_count);
+        dev::SynthGroup sg{};
+        sg.begin = begin;
+        sg.chunk = static_cast<std::uint64_t>(chunk);
+        sg.group_first = static_cast<std::uint64_t>(rank) * static_cast<std::uint64_t>(chunk);
+        sg.true_len = static_cast<std::uint64_t>(info.element_count);
+        sg.off[0] = o_m;
+        sg.off[1] = o_v;
+        sg.off[2] = o_w;
+        sg.slice_begin = static_cast<std::uint32_t>(slices.size());
+        for (const auto& s : model_.slices(g)) slices.push_back({s.group_offset, s.model_offset, s.decl.numel()});
+        sg.slice_count = static_cast<std::uint32_t>(model_.slices(g).size());
+        sg.module = static_cast<std::uint32_t>(model_.owner_index(g));
+        if (chunk > 0) groups.push_back(sg);
+        begin += static_cast<std::uint64_t>(chunk);
+    };
+    if (packed) {
+        std::uint64_t off = 0;
+        for (const auto& f : score_fields(model_, num_ranks_)) {
+            add_group(f.group, ~0ull, ~0ull, off);
+            off = align16(off + static_cast<std::uint64_t>(f.chunk) * 4);
+        }
+    } else {
+        const ContainerLayout& c = layout(k).shards[static_cast<std::size_t>(rank)];
+        for (int g : layout(k).groups)
+            add_group(g, c.find(shard_key(g, ".exp_avg"))->begin, c.find(shard_key(g, ".exp_avg_sq"))->begin,
+                      c.find(shard_key(g, ".master"))->begin);
+    }
+    t->ngroups = static_cast<std::uint32_t>(groups.size());
+    t->total = begin;
+    t->groups.upload(groups.data(), groups.size() * sizeof(dev::SynthGroup));
+    t->slices.upload(slices.data(), slices.size() * sizeof(dev::SynthSlice));
+    return *tables_.emplace(key, std::move(t)).first->second;
+}
+
+namespace {
+dev::OutPtrs out_ptrs(std::uint8_t* const* outs, int n) {
+    if (n < 1 || n > dev::kMaxSnapshots) fail(ErrorKind::Geometry, "at most 16 snapshots per generator launch");
+    dev::OutPtrs o{};
+    for (int i = 0; i < n; ++i) o.p[i] = outs[i];
+    return o;
+}
+} // namespace
+
+void SynthFamily::gen_shard(int rank, int k0, int k1, std::uint8_t* const* outs, cudaStream_t s) {
+    if (rank < 0 || rank >= num_ranks_) fail(ErrorKind::Geometry, "rank out of range");
+    if (k0 < 1 || k1 > K_ || k0 > k1) fail(ErrorKind::Geometry, "snapshot range out of bounds");
+    for (int k = k0 + 1; k <= k1; ++k)
+        if (modules_[static_cast<std::size_t>(k - 1)] != modules_[static_cast<std::size_t>(k0 - 1)])
+            fail(ErrorKind::Geometry, "snapshots generated together must share one layout");
+    ensure_sigma(k1);
+    ShardTables& t = shard_tables(k0, rank, false);
+    cuda_check(dev::launch_synth_shard(t.groups.get<dev::SynthGroup>(), t.ngroups, t.slices.get<dev::SynthSlice>(),
+                                       sigma_.get<float>(), model_.module_count(), model_.spec().seed, k0, k1,
+                                       out_ptrs(outs, k1 - k0 + 1), t.total, s),
+               "synth shard");
+}
+
+void SynthFamily::gen_masters_packed(int rank, int k0, int k1, std::uint8_t* const* outs, cudaStream_t s) {
+    if (rank < 0 || rank >= num_ranks_) fail(ErrorKind::Geometry, "rank out of range");
+    if (k0 < 1 || k1 > K_ || k0 > k1) fail(ErrorKind::Geometry, "snapshot range out of bounds");
+    ensure_sigma(k1);
+    ShardTables& t = shard_tables(0, rank, true);
+    cuda_check(dev::launch_synth_shard(t.groups.get<dev::SynthGroup>(), t.ngroups, t.slices.get<dev::SynthSlice>(),
+                                       sigma_.get<float>(), model_.module_count(), model_.spec().seed, k0, k1,
+                                       out_ptrs(outs, k1 - k0 + 1), t.total, s),
+               "synth masters");
+}
+
+void SynthFamily::gen_weights(int k0, int k1, std::uint64_t lo, std::uint64_t hi, std::uint8_t* const* outs,
+                              cudaStream_t s) {
+    if (k0 < 1 || k1 > K_ || k0 > k1) fail(ErrorKind::Geometry, "snapshot range out of bounds");
+    ensure_sigma(k1);
+    const CheckpointLayout& lay = layout(k0);
+    std::map<std::string, std::pair<std::int64_t, int>> where; // tensor -> (model offset, module)
+    for (int m = 0; m < model_.module_count(); ++m) {
+        std::int64_t off = model_.module_offset(m);
+        for (const auto& t : tensors_of(model_.spec(), model_.modules()[static_cast<std::size_t>(m)])) {
+            where[t.name] = {off, m};
+            off += t.numel();
+        }
+    }
+    std::vector<dev::SynthTensor> tabs;
+    std::uint64_t begin = 0;
+    for (const auto& e : lay.weights.entries) {
+        if (e.end <= lo || e.begin >= hi) continue;
+        if (e.begin < lo || e.end > hi) fail(ErrorKind::Geometry, "weights window must be tensor-aligned");
+        const auto& w = where.at(e.name);
+        const std::uint64_t n = e.bytes() / 2;
+        tabs.push_back({begin, n, e.begin - lo, w.first, static_cast<std::uint32_t>(w.second), 0});
+        begin += n;
+    }
+    if (tabs.empty()) return;
+    if (s) cuda_check(cudaStreamSynchronize(s), "sync");
+    wtab_.upload(tabs.data(), tabs.size() * sizeof(dev::SynthTensor));
+    cuda_check(dev::launch_synth_weights(wtab_.get<dev::SynthTensor>(), static_cast<std::uint32_t>(tabs.size()),
+                                         sigma_.get<float>(), model_.module_count(), model_.spec().seed, k0, k1,
+                                         out_ptrs(outs, k1 - k0 + 1), begin, s),
+               "synth weights");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+}
+
+namespace {
+
+void write_bytes_file(const fs::path& path, const std::string& prefix, const std::uint8_t* payload, std::uint64_t n) {
+    std::ofstream out(path, std::ios::binary | std::ios::trunc);
+    if (!out) fail(ErrorKind::Storage, "cannot create '" + path.string() + "'");
+    out.write(prefix.data(), static_cast<std::streamsize>(prefix.size()));
+    if (n) out.write(reinterpret_cast<const char*>(payload), static_cast<std::streamsize>(n));
+    out.flush();
+    if (!out) fail(ErrorKind::Storage, "write failed for '" + path.string() + "'");
+}
+
+} // namespace
+
+void SynthFamily::write_dir(int k, const std::string& dir) {
+    const CheckpointLayout& lay = layout(k);
+    std::error_code ec;
+    fs::create_directories(fs::path(dir) / "optim", ec);
+    if (ec) fail(ErrorKind::Storage, "cannot create '" + dir + "': " + ec.message());
+    std::uint64_t most = lay.weights.payload_bytes;
+    for (const auto& c : lay.shards) most = std::max(most, c.payload_bytes);
+    DeviceBuffer d(std::max<std::uint64_t>(most, 16));
+    std::vector<std::uint8_t> h(most);
+    std::uint8_t* outs[1] = {d.get()};
+    gen_weights(k, k, 0, lay.weights.payload_bytes, outs, nullptr);
+    cuda_check(cudaMemcpy(h.data(), d.get(), lay.weights.payload_bytes, cudaMemcpyDeviceToHost), "D2H");
+    write_bytes_file(weights_path(dir), lay.weights.prefix(), h.data(), lay.weights.payload_bytes);
+    for (int r = 0; r < num_ranks_; ++r) {
+        gen_shard(r, k, k, outs, nullptr);
+        const auto& c = lay.shards[static_cast<std::size_t>(r)];
+        cuda_check(cudaMemcpy(h.data(), d.get(), c.payload_bytes, cudaMemcpyDeviceToHost), "D2H");
+        write_bytes_file(shard_path(dir, r), c.prefix(), h.data(), c.payload_bytes);
+    }
+    const CheckpointSummary s = summary(k, dir);
+    write_text_file(optim_meta_path(dir), render_optim_meta_json(s.optim));
+    write_text_file(config_path(dir), render_config_json(s.spec));
+    write_text_file(trainer_state_path(dir), render_trainer_state_json(s.trainer));
+    write_text_file(manifest_path(dir), render_manifest_json(s.manifest));
+    set_id(k, dir);
+}
+
+// ---- scorer plan ----------------------------------------------------------------
+ScorePlan::ScorePlan(const ModelLayout& model, int num_ranks, std::vector<std::vector<std::uint64_t>> field_offsets,
+                     std::uint32_t tile_elems)
+    : K_(static_cast<int>(field_offsets.size())), M_(model.module_count()), offs_(std::move(field_offsets)) {
+    if (K_ < 2 || K_ > dev::kMaxSnapshots) fail(ErrorKind::Geometry, "scoring needs 2..16 snapshots");
+    tile_elems = std::max<std::uint32_t>(4, tile_elems & ~3u);
+    fields_ = score_fields(model, num_ranks);
+    for (const auto& o : offs_) {
+        if (o.size() != fields_.size()) fail(ErrorKind::Geometry, "field offset table has the wrong size");
+        for (auto x : o) aligned_offsets_ = aligned_offsets_ && (x % 16 == 0);
+    }
+    begin_.assign(static_cast<std::size_t>(M_) + 1, 0);
+    int cur = -1;
+    for (std::size_t f = 0; f < fields_.size(); ++f) {
+        const ScoreField& sf = fields_[f];
+        while (cur < sf.module) begin_[static_cast<std::size_t>(++cur)] = static_cast<std::uint32_t>(tiles_.size());
+        for (std::int64_t s = 0; s < sf.chunk; s += tile_elems) {
+            const std::uint32_t n = static_cast<std::uint32_t>(std::min<std::int64_t>(tile_elems, sf.chunk - s));
+            tiles_.push_back({static_cast<std::uint32_t>(sf.module), static_cast<std::uint32_t>(f), n, 0,
+                              static_cast<std::uint64_t>(s)});
+        }
+        bytes_ += static_cast<std::uint64_t>(sf.chunk) * 4 * static_cast<std::uint64_t>(K_);
+    }
+    while (cur < M_) begin_[static_cast<std::size_t>(++cur)] = static_cast<std::uint32_t>(tiles_.size());
+    d_tiles_.upload(tiles_.data(), tiles_.size() * sizeof(dev::ScoreTile));
+    d_begin_.upload(begin_.data(), begin_.size() * sizeof(std::uint32_t));
+    d_partials_.resize(std::max<std::size_t>(1, tiles_.size()) * 2 * static_cast<std::size_t>(K_ - 1) * sizeof(double));
+    h_bases_.resize(static_cast<std::size_t>(K_) * fields_.size() * sizeof(void*) + 8);
+    d_bases_.resize(static_cast<std::size_t>(K_) * fields_.size() * sizeof(void*) + 8);
+}
+
+void ScorePlan::run(const std::uint8_t* const* snap_bases, double* d_out, cudaStream_t s) {
+    const std::vector<const std::uint8_t*> want(snap_bases, snap_bases + K_);
+    bool vec = aligned_offsets_;
+    for (auto* p : want) vec = vec && (reinterpret_cast<std::uintptr_t>(p) % 16 == 0);
+    if (want != bound_) {
+        const float** h = reinterpret_cast<const float**>(h_bases_.get());
+        for (int k = 0; k < K_; ++k)
+            for (std::size_t f = 0; f < fields_.size(); ++f)
+                h[static_cast<std::size_t>(k) * fields_.size() + f] =
+                    reinterpret_cast<const float*>(want[static_cast<std::size_t>(k)] + offs_[static_cast<std::size_t>(k)][f]);
+        cuda_check(cudaMemcpyAsync(d_bases_.get(), h, static_cast<std::size_t>(K_) * fields_.size() * sizeof(void*),
+                                   cudaMemcpyHostToDevice, s),
+                   "bases upload");
+        cuda_check(cudaStreamSynchronize(s), "sync");
+        bound_ = want;
+    }
+    cuda_check(dev::launch_score_partials(d_tiles_.get<dev::ScoreTile>(), static_cast<std::uint32_t>(tiles_.size()),
+                                          d_bases_.get<const float*>(), static_cast<std::uint32_t>(fields_.size()), K_,
+                                          vec, d_partials_.get<double>(), s),
+               "score partials");
+    cuda_check(dev::launch_score_combine(d_partials_.get<double>(), d_begin_.get<std::uint32_t>(), M_, K_, d_out, s),
+               "score combine");
+}
+
+// ---- device merge -----------------------------------------------------------------
+DeviceMerge::DeviceMerge(const PartitionPlan& plan) : plan_(plan) {
+    nseg_ = static_cast<std::uint32_t>(plan_.segments.size());
+}
+
+void DeviceMerge::bind(const std::vector<const std::uint8_t*>& window_ptrs) {
+    if (window_ptrs.size() != plan_.windows.size()) fail(ErrorKind::Geometry, "window pointer count mismatch");
+    std::vector<dev::GatherSeg> segs;
+    segs.reserve(plan_.segments.size());
+    bool ok = true;
+    std::uint64_t expect = plan_.dst_lo;
+    for (const auto& s : plan_.segments) {
+        const std::uint8_t* src = window_ptrs[s.window] + s.src_off;
+        segs.push_back({src, s.dst_off - plan_.dst_lo, s.bytes});
+        ok = ok && s.dst_off == expect && (s.dst_off - plan_.dst_lo) % 16 == 0 && s.bytes % 16 == 0 &&
+             reinterpret_cast<std::uintptr_t>(src) % 16 == 0;
+        expect = s.dst_off + s.bytes;
+    }
+    bulk_ok_ = ok && expect == plan_.dst_hi;
+    d_segs_.upload(segs.data(), segs.size() * sizeof(dev::GatherSeg));
+}
+
+void DeviceMerge::run(std::uint8_t* d_dst, int variant, cudaStream_t s) {
+    const bool ok = bulk_ok_ && reinterpret_cast<std::uintptr_t>(d_dst) % 16 == 0;
+    cuda_check(dev::launch_gather(d_segs_.get<dev::GatherSeg>(), nseg_, d_dst, bytes(), variant, ok, s), "gather");
+}
+
+// ---- host-staged merge (shard pipeline) ------------------------------------------
+HostMerge::HostMerge(const PartitionPlan& plan, std::uint64_t chunk_bytes) : plan_(plan) {
+    chunk_bytes = std::max<std::uint64_t>(16, chunk_bytes & ~15ull);
+    const std::uint64_t total = plan_.dst_hi - plan_.dst_lo;
+    std::size_t si = 0;
+    for (std::uint64_t lo = 0; lo < total; lo += chunk_bytes) {
+        Chunk c;
+        c.lo = lo;
+        c.hi = std::min(total, lo + chunk_bytes);
+        struct P {
+            std::uint32_t w;
+            std::uint64_t src, dst, n;
+        };
+        std::vector<P> ps;
+        while (si < plan_.segments.size() && plan_.segments[si].dst_off + plan_.segments[si].bytes - plan_.dst_lo <= c.lo) ++si;
+        for (std::size_t j = si; j < plan_.segments.size(); ++j) {
+            const auto& s = plan_.segments[j];
+            const std::uint64_t d0 = s.dst_off - plan_.dst_lo, d1 = d0 + s.bytes;
+            if (d0 >= c.hi) break;
+            const std::uint64_t a = std::max(d0, c.lo), b = std::min(d1, c.hi);
+            if (a < b) ps.push_back({s.window, s.src_off + (a - d0), a, b - a});
+        }
+        // Stage in source order per window, coalescing contiguous source bytes.
+        std::vector<std::size_t> order(ps.size());
+        for (std::size_t i = 0; i < ps.size(); ++i) order[i] = i;
+        std::sort(order.begin(), order.end(), [&](std::size_t x, std::size_t y) {
+            return ps[x].w != ps[y].w ? ps[x].w < ps[y].w : ps[x].src < ps[y].src;
+        });
+        std::vector<std::uint64_t> stage_of(ps.size());
+        std::uint64_t at = 0;
+        for (std::size_t oi = 0; oi < order.size(); ++oi) {
+            const P& p = ps[order[oi]];
+            if (!c.reads.empty() && c.reads.back().first == p.w && c.reads.back().second.second == p.src) {
+                stage_of[order[oi]] = c.read_at.back() + (p.src - c.reads.back().second.first);
+                c.reads.back().second.second = p.src + p.n;
+                at = c.read_at.back() + (c.reads.back().second.second - c.reads.back().second.first);
+                continue;
+            }
+            at = align16(at);
+            c.reads.push_back({p.w, {p.src, p.src + p.n}});
+            c.read_at.push_back(at);
+            stage_of[order[oi]] = at;
+            at += p.n;
+        }
+        c.staging = align16(at);
+        std::uint64_t expect = c.lo;
+        for (std::size_t i = 0; i < ps.size(); ++i) {
+            c.segs.push_back({reinterpret_cast<const std::uint8_t*>(stage_of[i]), ps[i].dst - c.lo, ps[i].n});
+            c.bulk_ok = c.bulk_ok && ps[i].dst == expect && stage_of[i] % 16 == 0 && ps[i].n % 16 == 0 && (ps[i].dst - c.lo) % 16 == 0;
+            expect = ps[i].dst + ps[i].n;
+        }
+        c.bulk_ok = c.bulk_ok && expect == c.hi;
+        max_staging_ = std::max(max_staging_, c.staging);
+        max_out_ = std::max(max_out_, c.hi - c.lo);
+        chunks_.push_back(std::move(c));
+    }
+}
+
+HostMerge::~HostMerge() {
+    for (auto& s : stream_)
+        if (s) cudaStreamDestroy(s);
+}
+
+void HostMerge::run(const std::vector<const std::uint8_t*>& h_windows, std::uint8_t* h_dst, int variant) {
+    if (h_windows.size() != plan_.windows.size()) fail(ErrorKind::Geometry, "window pointer count mismatch");
+    std::size_t max_segs = 1;
+    for (const auto& c : chunks_) max_segs = std::max(max_segs, c.segs.size());
+    for (int i = 0; i < 2; ++i) {
+        if (!stream_[i]) cuda_check(cudaStreamCreateWithFlags(&stream_[i], cudaStreamNonBlocking), "stream");
+        stage_[i].resize(std::max<std::uint64_t>(16, max_staging_));
+        out_[i].resize(std::max<std::uint64_t>(16, max_out_));
+        segs_[i].resize(max_segs * sizeof(dev::GatherSeg));
+    }
+    std::vector<std::vector<dev::GatherSeg>> patched(chunks_.size());
+    h2d_ = d2h_ = 0;
+    for (std::size_t ci = 0; ci < chunks_.size(); ++ci) {
+        const Chunk& c = chunks_[ci];
+        const int slot = static_cast<int>(ci & 1);
+        cudaStream_t s = stream_[slot];
+        for (std::size_t r = 0; r < c.reads.size(); ++r) {
+            const auto& rd = c.reads[r];
+            const std::uint64_t n = rd.second.second - rd.second.first;
+            cuda_check(cudaMemcpyAsync(stage_[slot].get() + c.read_at[r], h_windows[rd.first] + rd.second.first, n,
+                                       cudaMemcpyHostToDevice, s),
+                       "H2D");
+            h2d_ += n;
+        }
+        patched[ci] = c.segs;
+        for (auto& g : patched[ci]) g.src = stage_[slot].get() + reinterpret_cast<std::uintptr_t>(g.src);
+        cuda_check(cudaMemcpyAsync(segs_[slot].get(), patched[ci].data(), patched[ci].size() * sizeof(dev::GatherSeg),
+                                   cudaMemcpyHostToDevice, s),
+                   "segs");
+        cuda_check(dev::launch_gather(segs_[slot].get<dev::GatherSeg>(), static_cast<std::uint32_t>(patched[ci].size()),
+                                      out_[slot].get(), c.hi - c.lo, variant, c.bulk_ok, s),
+                   "gather");
+        cuda_check(cudaMemcpyAsync(h_dst + c.lo, out_[slot].get(), c.hi - c.lo, cudaMemcpyDeviceToHost, s), "D2H");
+        d2h_ += c.hi - c.lo;
+    }
+    for (auto& s : stream_) cuda_check(cudaStreamSynchronize(s), "sync");
+}
+
+// ---- device re-verify --------------------------------------------------------------
+namespace {
+
+void load_payload(const fs::path& path, const ContainerLayout& lay, DeviceBuffer& dst, PinnedBuffer& stage) {
+    dst.resize(std::max<std::uint64_t>(16, lay.payload_bytes));
+    const int fd = ::open(path.c_str(), O_RDONLY);
+    if (fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + path.string() + "'");
+    const std::uint64_t step = 64ull << 20;
+    stage.resize(step);
+    for (std::uint64_t off = 0; off < lay.payload_bytes; off += step) {
+        const std::uint64_t n = std::min(step, lay.payload_bytes - off);
+        std::uint64_t got = 0;
+        while (got < n) {
+            const ssize_t r = ::pread(fd, stage.get() + got, n - got, static_cast<off_t>(lay.payload_offset() + off + got));
+            if (r <= 0) {
+                ::close(fd);
+                fail(ErrorKind::Storage, "read failed for '" + path.string() + "'");
+            }
+            got += static_cast<std::uint64_t>(r);
+        }
+        cuda_check(cudaMemcpy(dst.get() + off, stage.get(), n, cudaMemcpyHostToDevice), "H2D");
+    }
+    ::close(fd);
+}
+
+} // namespace
+
+void verify_checkpoint_dir(const std::string& dir_s, int device) {
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    const fs::path dir(dir_s);
+    const CheckpointSummary s = read_checkpoint_summary(dir);
+    if (s.optim.grouping != Grouping::Fine) fail(ErrorKind::Geometry, "device verify supports the fine grouping only");
+    const fs::path optim = dir / "optim";
+    if (!fs::exists(optim)) fail(ErrorKind::MissingArtifact, "'" + optim.string() + "' does not exist");
+    std::size_t files = 0;
+    for ([[maybe_unused]] const auto& e : fs::directory_iterator(optim)) ++files;
+    if (files != static_cast<std::size_t>(s.optim.num_ranks))
+        fail(ErrorKind::Geometry, dir.string() + ": found " + std::to_string(files) + " shard files for " +
+                                      std::to_string(s.optim.num_ranks) + " ranks");
+    const ModelLayout model(s.spec);
+    const ContainerLayout wl = read_layout(weights_path(dir));
+    std::size_t expect_tensors = 0;
+    for (const auto& m : s.manifest.modules)
+        for (const auto& t : tensors_of(s.spec, m)) {
+            ++expect_tensors;
+            const Entry* e = wl.find(t.name);
+            if (!e) fail(ErrorKind::CorruptContainer, weights_path(dir).string() + ": missing tensor '" + t.name + "'");
+            if (e->dtype != Dtype::BF16 || e->shape != t.shape)
+                fail(ErrorKind::Geometry, weights_path(dir).string() + ": tensor '" + t.name + "' has unexpected dtype/shape");
+        }
+    if (wl.entries.size() != expect_tensors)
+        fail(ErrorKind::CorruptContainer, weights_path(dir).string() + ": contains tensors not in the manifest");
+
+    DeviceBuffer dw, ds, dpairs, dranges, derr(3 * sizeof(unsigned long long));
+    PinnedBuffer stage;
+    load_payload(weights_path(dir), wl, dw, stage);
+    unsigned long long err[3] = {0, 0, 0};
+    cuda_check(cudaMemset(derr.get(), 0, sizeof(err)), "memset");
+    for (int r = 0; r < s.optim.num_ranks; ++r) {
+        const ContainerLayout sl = read_layout(shard_path(dir, r));
+        auto mr = sl.metadata.find("rank");
+        if (mr != sl.metadata.end() && mr->second != std::to_string(r))
+            fail(ErrorKind::CorruptContainer, shard_path(dir, r).string() + ": rank metadata mismatch");
+        load_payload(shard_path(dir, r), sl, ds, stage);
+        std::vector<dev::VerifyPair> pairs;
+        std::vector<dev::VerifyRange> ranges;
+        for (const auto& g : s.optim.groups) {
+            const Entry* f[3];
+            const char* names[3] = {".master", ".exp_avg", ".exp_avg_sq"};
+            for (int i = 0; i < 3; ++i) {
+                f[i] = sl.find(shard_key(g.index, names[i]));
+                if (!f[i])
+                    fail(ErrorKind::CorruptContainer,
+                         shard_path(dir, r).string() + ": missing tensor '" + shard_key(g.index, names[i]) + "'");
+                if (f[i]->dtype != Dtype::F32 || f[i]->shape != std::vector<std::int64_t>{g.shard_length})
+                    fail(ErrorKind::Geometry, shard_path(dir, r).string() + ": tensor '" + shard_key(g.index, names[i]) +
+                                                  "' has unexpected dtype/shape");
+            }
+            const std::int64_t c = g.shard_length, first = static_cast<std::int64_t>(r) * c;
+            const std::int64_t valid = std::clamp<std::int64_t>(g.true_length - first, 0, c);
+            for (int i = 0; i < 3; ++i)
+                if (valid < c)
+                    ranges.push_back({reinterpret_cast<const std::uint32_t*>(ds.get() + f[i]->begin) + valid,
+                                      static_cast<std::uint64_t>(c - valid), 0, 0});
+            if (valid > 0)
+                ranges.push_back({reinterpret_cast<const std::uint32_t*>(ds.get() + f[2]->begin),
+                                  static_cast<std::uint64_t>(valid), 1, 0});
+            for (const auto& sl2 : model.slices(g.index)) {
+                const std::int64_t a = std::max(first, sl2.group_offset);
+                const std::int64_t b = std::min(first + valid, sl2.group_offset + sl2.decl.numel());
+                if (a >= b) continue;
+                const Entry* we = wl.find(sl2.decl.name);
+                pairs.push_back({reinterpret_cast<const float*>(ds.get() + f[0]->begin) + (a - first),
+                                 reinterpret_cast<const std::uint16_t*>(dw.get() + we->begin) + (a - sl2.group_offset),
+                                 static_cast<std::uint64_t>(b - a)});
+            }
+        }
+        dpairs.upload(pairs.data(), pairs.size() * sizeof(dev::VerifyPair));
+        dranges.upload(ranges.data(), ranges.size() * sizeof(dev::VerifyRange));
+        cuda_check(dev::launch_verify(dpairs.get<dev::VerifyPair>(), static_cast<std::uint32_t>(pairs.size()),
+                                      dranges.get<dev::VerifyRange>(), static_cast<std::uint32_t>(ranges.size()),
+                                      derr.get<unsigned long long>(), nullptr),
+                   "verify");
+        cuda_check(cudaMemcpy(err, derr.get(), sizeof(err), cudaMemcpyDeviceToHost), "D2H");
+        if (err[1]) fail(ErrorKind::CorruptContainer, dir.string() + ": nonzero padding in rank " + std::to_string(r));
+        if (err[2]) fail(ErrorKind::Consistency, "exp_avg_sq contains a negative or non-finite element");
+    }
+    if (err[0]) fail(ErrorKind::Consistency, dir.string() + ": a weight tensor disagrees with its FP32 master");
+}
+
+} // namespace tailor

@@ -1,0 +1,261 @@
+// K2 — segmented gather/scatter of checkpoint payload bytes (the composite
+// assembly of R/src/merge.cpp:244-303, which the reference performs as
+// per-tensor std::vector copies). Pure data movement: HBM-bound, no tensor
+// cores. Two implementations over the same segment table:
+//
+//  * bulk (default when every segment is 16-B aligned and the segments tile
+//    the destination): a persistent CTA per SM whose single elected thread
+//    drives the TMA copy engine — cp.async.bulk global->shared into a 4-stage
+//    ring completed by mbarrier transaction counts, then cp.async.bulk
+//    shared->global (bulk_group) out of the same stage. No register staging,
+//    ~3 issue instructions per 48 KB.
+//  * lsu: 256-thread CTAs, 16-B ld.global.nc / st.global with UNROLL loads in
+//    flight per thread, head/tail peeling and 4/2/1-byte fallbacks for the
+//    misaligned segments the reference's randomized shapes produce (12-B
+//    chunks, 2-B bf16 tensors).
+//
+// Work split: the destination is cut into fixed tiles; CTA b owns tiles
+// b, b+G, b+2G... (static, so the byte placement never depends on timing).
+#include <algorithm>
+
+#include "tailor/device.hpp"
+
+namespace tailor::dev {
+
+namespace {
+
+constexpr int kLsuThreads = 256;
+constexpr std::uint64_t kLsuTile = 64 * 1024;
+constexpr int kLsuUnroll = 8;
+
+constexpr int kBulkStages = 4;
+constexpr std::uint32_t kBulkStage = 48 * 1024;
+
+__device__ __forceinline__ int seg_lookup(const GatherSeg* __restrict__ segs, std::uint32_t n, std::uint64_t x) {
+    int lo = 0, hi = static_cast<int>(n) - 1, ans = -1;
+    while (lo <= hi) {
+        const int mid = (lo + hi) >> 1;
+        if (segs[mid].dst_off <= x) {
+            ans = mid;
+            lo = mid + 1;
+        } else {
+            hi = mid - 1;
+        }
+    }
+    return ans < 0 ? 0 : ans;
+}
+
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void st_stream(int4* p, const int4& v) {
+    asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+
+template <typename W>
+__device__ __forceinline__ void cta_copy_words(std::uint8_t* dst, const std::uint8_t* src, std::uint64_t n) {
+    // dst and src share alignment mod sizeof(W); peel to W alignment.
+    const int tid = threadIdx.x;
+    std::uint64_t head = (sizeof(W) - (reinterpret_cast<std::uintptr_t>(dst) & (sizeof(W) - 1))) & (sizeof(W) - 1);
+    if (head > n) head = n;
+    if (static_cast<std::uint64_t>(tid) < head) dst[tid] = src[tid];
+    const std::uint64_t nw = (n - head) / sizeof(W);
+    const W* s = reinterpret_cast<const W*>(src + head);
+    W* d = reinterpret_cast<W*>(dst + head);
+    for (std::uint64_t i = tid; i < nw; i += kLsuThreads) d[i] = s[i];
+    const std::uint64_t done = head + nw * sizeof(W);
+    if (static_cast<std::uint64_t>(tid) < n - done) dst[done + tid] = src[done + tid];
+}
+
+__device__ __forceinline__ void cta_copy(std::uint8_t* __restrict__ dst, const std::uint8_t* __restrict__ src,
+                                         std::uint64_t n) {
+    const std::uintptr_t mis = reinterpret_cast<std::uintptr_t>(dst) ^ reinterpret_cast<std::uintptr_t>(src);
+    if ((mis & 15) == 0) {
+        const int tid = threadIdx.x;
+        std::uint64_t head = (16 - (reinterpret_cast<std::uintptr_t>(dst) & 15)) & 15;
+        if (head > n) head = n;
+        if (static_cast<std::uint64_t>(tid) < head) dst[tid] = src[tid];
+        const std::uint64_t nv = (n - head) >> 4;
+        const int4* s4 = reinterpret_cast<const int4*>(src + head);
+        int4* d4 = reinterpret_cast<int4*>(dst + head);
+        std::uint64_t i = tid;
+        for (; i + static_cast<std::uint64_t>(kLsuUnroll - 1) * kLsuThreads < nv; i += kLsuUnroll * kLsuThreads) {
+            int4 v[kLsuUnroll];
+#pragma unroll
+            for (int u = 0; u < kLsuUnroll; ++u) v[u] = ld_stream(s4 + i + u * kLsuThreads);
+#pragma unroll
+            for (int u = 0; u < kLsuUnroll; ++u) st_stream(d4 + i + u * kLsuThreads, v[u]);
+        }
+        for (; i < nv; i += kLsuThreads) st_stream(d4 + i, ld_stream(s4 + i));
+        const std::uint64_t done = head + (nv << 4);
+        if (static_cast<std::uint64_t>(tid) < n - done) dst[done + tid] = src[done + tid];
+    } else if ((mis & 3) == 0) {
+        cta_copy_words<std::uint32_t>(dst, src, n);
+    } else if ((mis & 1) == 0) {
+        cta_copy_words<std::uint16_t>(dst, src, n);
+    } else {
+        for (std::uint64_t i = threadIdx.x; i < n; i += kLsuThreads) dst[i] = src[i];
+    }
+}
+
+__global__ void __launch_bounds__(kLsuThreads) gather_lsu_kernel(const GatherSeg* __restrict__ segs, std::uint32_t nseg,
+                                                                  std::uint8_t* __restrict__ dst, std::uint64_t dst_bytes) {
+    const std::uint64_t ntiles = (dst_bytes + kLsuTile - 1) / kLsuTile;
+    for (std::uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        std::uint64_t lo = t * kLsuTile;
+        const std::uint64_t hi = min(lo + kLsuTile, dst_bytes);
+        for (int s = seg_lookup(segs, nseg, lo); lo < hi && s < static_cast<int>(nseg); ++s) {
+            const GatherSeg g = segs[s];
+            const std::uint64_t end = g.dst_off + g.bytes;
+            if (end <= lo) continue;
+            if (g.dst_off >= hi) break;
+            const std::uint64_t a = max(lo, g.dst_off), b = min(hi, end);
+            cta_copy(dst + a, g.src + (a - g.dst_off), b - a);
+            lo = b;
+        }
+    }
+}
+
+// ---- TMA bulk path -----------------------------------------------------------
+__device__ __forceinline__ std::uint32_t smem_addr(const void* p) {
+    return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, std::uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(std::uint64_t* bar, std::uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_parity(std::uint64_t* bar, std::uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "TG_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra TG_WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, std::uint32_t bytes, std::uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(smem_dst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, std::uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_addr(smem_src)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__global__ void __launch_bounds__(32, 1) gather_bulk_kernel(const GatherSeg* __restrict__ segs, std::uint32_t nseg,
+                                                             std::uint8_t* __restrict__ dst, std::uint64_t dst_bytes) {
+    extern __shared__ __align__(128) std::uint8_t smem[];
+    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kBulkStages * kBulkStage);
+    if (threadIdx.x != 0) return; // one thread drives the copy engine
+    for (int s = 0; s < kBulkStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+
+    const std::uint64_t ntiles = (dst_bytes + kBulkStage - 1) / kBulkStage;
+    const std::uint64_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+    const auto tile_lo = [&](std::uint64_t i) { return (blockIdx.x + i * gridDim.x) * static_cast<std::uint64_t>(kBulkStage); };
+    const auto issue_load = [&](std::uint64_t i) {
+        const int stage = static_cast<int>(i % kBulkStages);
+        const std::uint64_t lo = tile_lo(i);
+        const std::uint64_t hi = min(lo + kBulkStage, dst_bytes);
+        std::uint8_t* buf = smem + stage * kBulkStage;
+        mbar_arrive_expect_tx(&bars[stage], static_cast<std::uint32_t>(hi - lo));
+        std::uint64_t at = lo;
+        for (int s = seg_lookup(segs, nseg, lo); at < hi && s < static_cast<int>(nseg); ++s) {
+            const GatherSeg g = segs[s];
+            const std::uint64_t end = g.dst_off + g.bytes;
+            if (end <= at) continue;
+            const std::uint64_t b = min(hi, end);
+            bulk_load(buf + (at - lo), g.src + (at - g.dst_off), static_cast<std::uint32_t>(b - at), &bars[stage]);
+            at = b;
+        }
+    };
+
+    const std::uint64_t prologue = mine < kBulkStages - 1 ? mine : static_cast<std::uint64_t>(kBulkStages - 1);
+    for (std::uint64_t i = 0; i < prologue; ++i) issue_load(i);
+    for (std::uint64_t i = 0; i < mine; ++i) {
+        const int stage = static_cast<int>(i % kBulkStages);
+        mbar_wait_parity(&bars[stage], static_cast<std::uint32_t>((i / kBulkStages) & 1));
+        const std::uint64_t lo = tile_lo(i);
+        const std::uint64_t hi = min(lo + kBulkStage, dst_bytes);
+        bulk_store(dst + lo, smem + stage * kBulkStage, static_cast<std::uint32_t>(hi - lo));
+        bulk_commit();
+        const std::uint64_t next = i + kBulkStages - 1; // lands in tile i-1's stage
+        if (next < mine) {
+            if (i >= 1) bulk_wait_read_1(); // store of tile i-1 has finished reading smem
+            issue_load(next);
+        }
+    }
+    bulk_wait_all();
+}
+
+int g_sms = 0;
+int g_lsu_blocks_per_sm = 0;
+bool g_bulk_attr = false;
+
+} // namespace
+
+int sm_count() {
+    if (g_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_sms <= 0) g_sms = 148;
+    }
+    return g_sms;
+}
+
+cudaError_t launch_gather(const GatherSeg* d_segs, std::uint32_t nseg, std::uint8_t* d_dst, std::uint64_t dst_bytes,
+                          int variant, bool bulk_ok, cudaStream_t stream) {
+    if (dst_bytes == 0 || nseg == 0) return cudaSuccess;
+    const int sms = sm_count();
+    const bool bulk = variant == kGatherBulk || (variant == kGatherAuto && bulk_ok);
+    if (bulk && bulk_ok) {
+        const std::size_t smem = kBulkStages * kBulkStage + kBulkStages * sizeof(std::uint64_t);
+        if (!g_bulk_attr) {
+            const cudaError_t e =
+                cudaFuncSetAttribute(gather_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            g_bulk_attr = true;
+        }
+        const std::uint64_t tiles = (dst_bytes + kBulkStage - 1) / kBulkStage;
+        const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(tiles, static_cast<std::uint64_t>(sms)));
+        gather_bulk_kernel<<<grid, 32, smem, stream>>>(d_segs, nseg, d_dst, dst_bytes);
+        return cudaGetLastError();
+    }
+    if (g_lsu_blocks_per_sm == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_lsu_blocks_per_sm, gather_lsu_kernel, kLsuThreads, 0);
+        g_lsu_blocks_per_sm = std::max(1, std::min(g_lsu_blocks_per_sm, 4));
+    }
+    const std::uint64_t tiles = (dst_bytes + kLsuTile - 1) / kLsuTile;
+    const unsigned grid =
+        static_cast<unsigned>(std::min<std::uint64_t>(tiles, static_cast<std::uint64_t>(sms) * g_lsu_blocks_per_sm));
+    gather_lsu_kernel<<<grid, kLsuThreads, 0, stream>>>(d_segs, nseg, d_dst, dst_bytes);
+    return cudaGetLastError();
+}
+
+} // namespace tailor::dev

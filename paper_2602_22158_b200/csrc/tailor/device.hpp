@@ -1,0 +1,113 @@
+// Device tables and kernel launchers (sm_100a). Tables are built on the host
+// from the layer map (tailor/model.hpp, tailor/merge.hpp), uploaded once and
+// read-only during a launch; kernels never allocate. All launches are
+// asynchronous on the caller's stream.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace tailor::dev {
+
+// ---- K2: segmented gather/scatter ------------------------------------------
+// Destination bytes [dst_off, dst_off + bytes) <- src[0, bytes). Segments are
+// sorted by dst_off and do not overlap.
+struct GatherSeg {
+    const std::uint8_t* src;
+    std::uint64_t dst_off;
+    std::uint64_t bytes;
+};
+static_assert(sizeof(GatherSeg) == 24, "GatherSeg is part of the C ABI");
+
+enum GatherVariant : int { kGatherAuto = 0, kGatherLsu = 1, kGatherBulk = 2 };
+
+// `bulk_ok` (host-checked): every segment has 16-B aligned src/dst/bytes and
+// the segments tile [0, dst_bytes) exactly — the TMA bulk path's contract.
+cudaError_t launch_gather(const GatherSeg* d_segs, std::uint32_t nseg, std::uint8_t* d_dst, std::uint64_t dst_bytes,
+                          int variant, bool bulk_ok, cudaStream_t stream);
+
+// ---- K3/K4: update-magnitude scorer -----------------------------------------
+// A tile covers `count` consecutive master elements of one field (one group's
+// rank chunk) of one module; every snapshot k reads the same element range at
+// field_base[k * nfields + field].
+struct ScoreTile {
+    std::uint32_t module;
+    std::uint32_t field;
+    std::uint32_t count;
+    std::uint32_t pad;
+    std::uint64_t elem_start;
+};
+static_assert(sizeof(ScoreTile) == 24, "ScoreTile is part of the C ABI");
+
+// tile_partials[t][p][0|1] = (sum (B-A)^2, sum A^2) over tile t for pair
+// p = (snapshot p, snapshot p+1), FP64. 2 <= K <= 16.
+cudaError_t launch_score_partials(const ScoreTile* d_tiles, std::uint32_t ntiles, const float* const* d_field_base,
+                                  std::uint32_t nfields, int K, bool vec_ok, double* d_tile_partials, cudaStream_t stream);
+// out[p][m][0|1] = fixed-order sum over module m's tiles [tile_begin[m], tile_begin[m+1]).
+cudaError_t launch_score_combine(const double* d_tile_partials, const std::uint32_t* d_module_tile_begin, int M, int K,
+                                 double* d_out, cudaStream_t stream);
+
+// ---- K5: synthetic snapshot generator (SURVEY §8d contract) -----------------
+struct SynthGroup {
+    std::uint64_t begin;       // first virtual element of this group in the launch
+    std::uint64_t chunk;       // elements in the rank chunk
+    std::uint64_t group_first; // group-local index of chunk element 0 (rank * chunk)
+    std::uint64_t true_len;
+    std::uint64_t off[3];      // byte offsets of exp_avg, exp_avg_sq, master; ~0 = not generated
+    std::uint32_t slice_begin;
+    std::uint32_t slice_count;
+    std::uint32_t module; // canonical module index (sigma row)
+    std::uint32_t pad;
+};
+struct SynthSlice {
+    std::int64_t group_offset;
+    std::int64_t model_offset;
+    std::int64_t count;
+};
+struct SynthTensor {
+    std::uint64_t begin;  // first virtual element
+    std::uint64_t count;
+    std::uint64_t dst_off; // byte offset in the output window
+    std::int64_t model_offset;
+    std::uint32_t module;
+    std::uint32_t pad;
+};
+
+// Output buffers travel by value in the launch parameters (no upload).
+constexpr int kMaxSnapshots = 16;
+struct OutPtrs {
+    std::uint8_t* p[kMaxSnapshots];
+};
+
+// Generates snapshots k0..k1 (1-based, k1 - k0 < 16) in one pass; outs.p[k - k0]
+// receives snapshot k. sigma is [k1][M] floats (row j-1 = sigma_j).
+cudaError_t launch_synth_shard(const SynthGroup* d_groups, std::uint32_t ngroups, const SynthSlice* d_slices,
+                               const float* d_sigma, int M, std::uint64_t seed, int k0, int k1, OutPtrs outs,
+                               std::uint64_t total, cudaStream_t stream);
+cudaError_t launch_synth_weights(const SynthTensor* d_tensors, std::uint32_t ntensors, const float* d_sigma, int M,
+                                 std::uint64_t seed, int k0, int k1, OutPtrs outs, std::uint64_t total,
+                                 cudaStream_t stream);
+
+// ---- K6: composite re-verify (R/src/checkpoint.cpp:515-572 invariants) ------
+// Pairs: bf16_round(master[i]) == weight[i] for i < count. Zero ranges: every
+// 32-bit word must be 0 (shard padding). Nonneg ranges: exp_avg_sq >= 0.
+struct VerifyPair {
+    const float* master;
+    const std::uint16_t* weight;
+    std::uint64_t count;
+};
+struct VerifyRange {
+    const std::uint32_t* words;
+    std::uint64_t count;
+    std::uint32_t kind; // 0 = must be zero, 1 = must be >= 0 (float)
+    std::uint32_t pad;
+};
+// err[0] = number of failing pair elements, err[1] = failing zero words,
+// err[2] = failing non-negative elements (accumulated; caller zeroes).
+cudaError_t launch_verify(const VerifyPair* d_pairs, std::uint32_t npairs, const VerifyRange* d_ranges,
+                          std::uint32_t nranges, unsigned long long* d_err, cudaStream_t stream);
+
+int sm_count();
+
+} // namespace tailor::dev

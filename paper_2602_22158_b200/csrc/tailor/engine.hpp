@@ -1,0 +1,198 @@
+// Host-side engine binding layer-map plans to the device kernels:
+//   SynthFamily  — synthetic snapshots S_1..S_K (layouts, sidecars, K5 launches)
+//   ScorePlan    — K3/K4 tile tables for one rank partition of K snapshots
+//   DeviceMerge  — K2 segment table for one output partition, bound to device windows
+//   HostMerge    — the shard pipeline: pinned host sources -> H2D -> K2 -> D2H, chunked,
+//                  on two streams so transfers overlap the gather
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "tailor/checkpoint.hpp"
+#include "tailor/device.hpp"
+#include "tailor/merge.hpp"
+
+namespace tailor {
+
+void cuda_check(cudaError_t e, const char* what);
+
+class DeviceBuffer {
+  public:
+    DeviceBuffer() = default;
+    explicit DeviceBuffer(std::size_t n) { resize(n); }
+    ~DeviceBuffer();
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+    DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+    void resize(std::size_t n); // discards contents
+    template <typename T = std::uint8_t>
+    T* get() const { return static_cast<T*>(p_); }
+    std::size_t size() const { return n_; }
+    void upload(const void* src, std::size_t n, cudaStream_t s = nullptr);
+
+  private:
+    void* p_ = nullptr;
+    std::size_t n_ = 0;
+};
+
+class PinnedBuffer {
+  public:
+    PinnedBuffer() = default;
+    explicit PinnedBuffer(std::size_t n) { resize(n); }
+    ~PinnedBuffer();
+    PinnedBuffer(const PinnedBuffer&) = delete;
+    PinnedBuffer& operator=(const PinnedBuffer&) = delete;
+    void resize(std::size_t n);
+    std::uint8_t* get() const { return static_cast<std::uint8_t*>(p_); }
+    std::size_t size() const { return n_; }
+
+  private:
+    void* p_ = nullptr;
+    std::size_t n_ = 0;
+};
+
+// sigma_j(m) = 1e-6 * g^{pi_j(m)}, g = 1000^{1/(M-1)} (SURVEY §8d ladder).
+std::vector<float> synth_sigma(std::uint64_t seed, int M, int j);
+
+class SynthFamily {
+  public:
+    SynthFamily(const ModelSpec& spec, int num_ranks, int snapshots, std::int64_t interval);
+    void set_partial(int k, const std::vector<ModuleId>& modules);
+
+    const ModelLayout& model() const { return model_; }
+    int num_ranks() const { return num_ranks_; }
+    int snapshots() const { return K_; }
+    std::int64_t step(int k) const { return interval_ * k; }
+    const CheckpointLayout& layout(int k) const;
+    CheckpointSummary summary(int k, const std::string& dir) const;
+    std::string trainer_state_json(int k) const;
+    std::string manifest_json(int k) const;
+    std::string optim_meta_json(int k) const;
+    const std::string& id(int k) const { return ids_[static_cast<std::size_t>(k - 1)]; }
+    void set_id(int k, const std::string& id) { ids_[static_cast<std::size_t>(k - 1)] = id; }
+    int index_of(const std::string& id) const; // 1-based; 0 if unknown
+
+    // Device generation. Snapshots k0..k1 must share one layout.
+    void gen_shard(int rank, int k0, int k1, std::uint8_t* const* outs, cudaStream_t s);
+    // Weights payload bytes [lo, hi) of snapshot layout (tensor-aligned), window base = lo.
+    void gen_weights(int k0, int k1, std::uint64_t lo, std::uint64_t hi, std::uint8_t* const* outs, cudaStream_t s);
+    // Masters only, packed per field in score-field order (for scorer-only sweeps).
+    void gen_masters_packed(int rank, int k0, int k1, std::uint8_t* const* outs, cudaStream_t s);
+    std::uint64_t packed_master_bytes(int rank) const;
+    // GPU-generate snapshot k and write it as a checkpoint directory.
+    void write_dir(int k, const std::string& dir);
+
+  private:
+    struct ShardTables {
+        DeviceBuffer groups, slices;
+        std::uint32_t ngroups = 0;
+        std::uint64_t total = 0;
+    };
+    ShardTables& shard_tables(int k, int rank, bool packed);
+    void ensure_sigma(int kmax);
+
+    ModelLayout model_;
+    int num_ranks_;
+    int K_;
+    std::int64_t interval_;
+    std::vector<std::vector<ModuleId>> modules_;
+    std::vector<std::unique_ptr<CheckpointLayout>> layouts_;
+    std::vector<std::string> ids_;
+    std::map<std::tuple<int, int, bool>, std::unique_ptr<ShardTables>> tables_;
+    DeviceBuffer sigma_;
+    int sigma_rows_ = 0;
+    DeviceBuffer wtab_;
+};
+
+// Score fields of one rank partition: every group's master chunk, module-major
+// in canonical module order (groups in group_indices_for order).
+struct ScoreField {
+    int module;
+    int group;
+    std::int64_t chunk;
+};
+std::vector<ScoreField> score_fields(const ModelLayout& model, int num_ranks);
+
+class ScorePlan {
+  public:
+    // field_offsets[k][f]: byte offset of field f's master chunk inside
+    // snapshot k's buffer.
+    ScorePlan(const ModelLayout& model, int num_ranks, std::vector<std::vector<std::uint64_t>> field_offsets,
+              std::uint32_t tile_elems = 32768);
+    int K() const { return K_; }
+    int M() const { return M_; }
+    std::uint64_t bytes_read() const { return bytes_; }
+    // out: device [K-1][M][2] FP64 (sum delta^2, sum ref^2) for this rank.
+    void run(const std::uint8_t* const* snap_bases, double* d_out, cudaStream_t s);
+
+  private:
+    int K_, M_;
+    std::vector<ScoreField> fields_;
+    std::vector<std::vector<std::uint64_t>> offs_;
+    std::vector<dev::ScoreTile> tiles_;
+    std::vector<std::uint32_t> begin_;
+    DeviceBuffer d_tiles_, d_begin_, d_bases_, d_partials_;
+    PinnedBuffer h_bases_;
+    std::vector<const std::uint8_t*> bound_;
+    std::uint64_t bytes_ = 0;
+    bool aligned_offsets_ = true;
+};
+
+class DeviceMerge {
+  public:
+    explicit DeviceMerge(const PartitionPlan& plan);
+    const PartitionPlan& plan() const { return plan_; }
+    // window_ptrs[w] = device address of window w's first byte (window.lo).
+    void bind(const std::vector<const std::uint8_t*>& window_ptrs);
+    // d_dst points at output payload byte dst_lo.
+    void run(std::uint8_t* d_dst, int variant, cudaStream_t s);
+    bool bulk_ok() const { return bulk_ok_; }
+    std::uint64_t bytes() const { return plan_.dst_hi - plan_.dst_lo; }
+
+  private:
+    PartitionPlan plan_;
+    DeviceBuffer d_segs_;
+    std::uint32_t nseg_ = 0;
+    bool bulk_ok_ = false;
+};
+
+// Pipelined host->device->host assembly of one partition from host (pinned)
+// source windows into a host destination: per chunk, only the bytes the
+// chunk needs are copied in, gathered on the device and copied out.
+class HostMerge {
+  public:
+    explicit HostMerge(const PartitionPlan& plan, std::uint64_t chunk_bytes = 256ull << 20);
+    ~HostMerge();
+    // h_windows[w] = host address of window w's first byte; h_dst = output byte dst_lo.
+    void run(const std::vector<const std::uint8_t*>& h_windows, std::uint8_t* h_dst, int variant);
+    std::uint64_t h2d_bytes() const { return h2d_; }
+    std::uint64_t d2h_bytes() const { return d2h_; }
+
+  private:
+    struct Chunk {
+        std::uint64_t lo, hi;                  // output range (relative to dst_lo)
+        std::vector<dev::GatherSeg> segs;      // src = staging offset (patched at run)
+        std::vector<std::pair<std::uint32_t, std::pair<std::uint64_t, std::uint64_t>>> reads; // window, [a,b) -> staging at offset
+        std::vector<std::uint64_t> read_at;
+        std::uint64_t staging = 0;
+        bool bulk_ok = true;
+    };
+    PartitionPlan plan_;
+    std::vector<Chunk> chunks_;
+    std::uint64_t max_staging_ = 0, max_out_ = 0;
+    DeviceBuffer stage_[2], out_[2], segs_[2];
+    cudaStream_t stream_[2]{};
+    std::uint64_t h2d_ = 0, d2h_ = 0;
+};
+
+// Device re-verify of a checkpoint directory (duality, zero padding,
+// exp_avg_sq >= 0) plus the structural checks of read_checkpoint.
+void verify_checkpoint_dir(const std::string& dir, int device);
+
+} // namespace tailor

@@ -1,0 +1,207 @@
+// `tailor` CLI for the tailoring path, over the C ABI only (include/tailor_b200.h).
+// Mirrors the reference's merge / plan subcommands and exit codes
+// (R/tools/tailor_main.cpp:66-103, :291-299, :351-357) and adds the
+// update-magnitude `select` / `score` subcommands.
+//
+//   tailor merge  --recipe r.yaml --out DIR [--workers W] [--uncached] [--json] [--device D] [--no-verify]
+//   tailor plan   --run RUN --failure-step S --out r.yaml
+//   tailor select --snapshots A,B,... [--rho 0.5] --out r.yaml [--device D] [--json]
+//   tailor score  --snapshots A,B,... [--device D]
+//   tailor check  --ckpt DIR [--device D]
+// Exit codes: 0 success, 1 user error, 2 internal/consistency error.
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <iostream>
+#include <map>
+#include <set>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "tailor_b200.h"
+
+namespace {
+
+struct Args {
+    std::map<std::string, std::string> kv;
+    std::set<std::string> flags;
+};
+
+int exit_for(int code) { return (code >= 1 && code <= 9) ? 1 : 2; }
+
+int report(int code) {
+    std::cerr << "error: " << tg_last_error() << "\n";
+    return exit_for(code);
+}
+
+std::string read_file(const std::string& p, bool* ok) {
+    std::ifstream in(p, std::ios::binary);
+    *ok = static_cast<bool>(in);
+    return std::string((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+}
+
+std::vector<std::string> split_csv(const std::string& s) {
+    std::vector<std::string> out;
+    std::stringstream ss(s);
+    std::string x;
+    while (std::getline(ss, x, ','))
+        if (!x.empty()) out.push_back(x);
+    return out;
+}
+
+template <typename F>
+int text_call(F&& f, std::string& out) {
+    std::vector<char> buf(1 << 16);
+    size_t need = 0;
+    int rc = f(buf.data(), buf.size(), &need);
+    if (rc != TG_OK && need > buf.size()) {
+        buf.resize(need);
+        rc = f(buf.data(), buf.size(), &need);
+    }
+    if (rc == TG_OK) out = buf.data();
+    return rc;
+}
+
+bool require(const Args& a, std::initializer_list<const char*> keys) {
+    for (const char* k : keys)
+        if (!a.kv.count(k)) {
+            std::cerr << "missing required option --" << k << "\n";
+            return false;
+        }
+    return true;
+}
+
+int cmd_merge(const Args& a) {
+    if (!require(a, {"recipe", "out"})) return 1;
+    bool ok = false;
+    const std::string yaml = read_file(a.kv.at("recipe"), &ok);
+    if (!ok) {
+        std::cerr << "error: MissingArtifact: cannot open '" << a.kv.at("recipe") << "'\n";
+        return 1;
+    }
+    tg_merge_options opt{};
+    opt.workers = a.kv.count("workers") ? std::stoi(a.kv.at("workers")) : 0;
+    opt.uncached = a.flags.count("uncached") ? 1 : 0;
+    opt.device = a.kv.count("device") ? std::stoi(a.kv.at("device")) : 0;
+    opt.verify = a.flags.count("no-verify") ? 0 : 1;
+    tg_merge_stats st{};
+    const int rc = tg_execute_merge(yaml.c_str(), a.kv.at("out").c_str(), &opt, &st);
+    if (rc != TG_OK) return report(rc);
+    if (a.flags.count("json")) {
+        std::printf("{\"bytes_moved\":%llu,\"device_ms\":%.6f,\"out\":\"%s\",\"shard_files_read\":%lld,\"wall_ms\":%.6f,\"weight_files_read\":%lld}\n",
+                    static_cast<unsigned long long>(st.bytes_moved), st.device_ms, a.kv.at("out").c_str(),
+                    static_cast<long long>(st.shard_files_read), st.wall_ms, static_cast<long long>(st.weight_files_read));
+        return 0;
+    }
+    std::cout << "merged checkpoint written to " << a.kv.at("out") << "\n";
+    std::cout << "optimizer shard files read: " << st.shard_files_read << "\n";
+    std::cout << "weight files read: " << st.weight_files_read << "\n";
+    std::cout << "composite bytes: " << st.bytes_moved << " (device gather " << st.device_ms << " ms)\n";
+    std::cout << "wall time: " << st.wall_ms << " ms\n";
+    return 0;
+}
+
+int write_out(const std::string& path, const std::string& text) {
+    std::ofstream out(path, std::ios::binary | std::ios::trunc);
+    out << text;
+    if (!out) {
+        std::cerr << "error: StorageError: cannot write '" << path << "'\n";
+        return 2;
+    }
+    return 0;
+}
+
+int cmd_plan(const Args& a) {
+    if (!require(a, {"run", "failure-step", "out"})) return 1;
+    std::string yaml;
+    const long long step = std::stoll(a.kv.at("failure-step"));
+    const int rc = text_call([&](char* b, size_t c, size_t* n) { return tg_recipe_from_manifests(a.kv.at("run").c_str(), step, b, c, n); }, yaml);
+    if (rc != TG_OK) return report(rc);
+    if (int w = write_out(a.kv.at("out"), yaml)) return w;
+    std::cout << "recipe for failure at step " << step << " written to " << a.kv.at("out") << "\n" << yaml;
+    return 0;
+}
+
+int cmd_select(const Args& a) {
+    if (!require(a, {"snapshots", "out"})) return 1;
+    const auto dirs = split_csv(a.kv.at("snapshots"));
+    std::vector<const char*> ptrs;
+    for (const auto& d : dirs) ptrs.push_back(d.c_str());
+    const double rho = a.kv.count("rho") ? std::stod(a.kv.at("rho")) : 0.5;
+    const int device = a.kv.count("device") ? std::stoi(a.kv.at("device")) : 0;
+    std::vector<int32_t> src(4096);
+    double gap = 0.0;
+    std::string yaml;
+    const int rc = text_call(
+        [&](char* b, size_t c, size_t* n) {
+            return tg_select_recipe(ptrs.data(), static_cast<int32_t>(ptrs.size()), rho, device, b, c, n, src.data(), &gap);
+        },
+        yaml);
+    if (rc != TG_OK) return report(rc);
+    if (int w = write_out(a.kv.at("out"), yaml)) return w;
+    std::cout << yaml << "# min boundary gap " << gap << "\n";
+    return 0;
+}
+
+int cmd_score(const Args& a) {
+    if (!require(a, {"snapshots"})) return 1;
+    const auto dirs = split_csv(a.kv.at("snapshots"));
+    std::vector<const char*> ptrs;
+    for (const auto& d : dirs) ptrs.push_back(d.c_str());
+    const int device = a.kv.count("device") ? std::stoi(a.kv.at("device")) : 0;
+    std::vector<double> scores(dirs.size() * 4096);
+    int32_t M = 0;
+    const int rc = tg_score_snapshots(ptrs.data(), static_cast<int32_t>(ptrs.size()), device, nullptr, scores.data(), &M);
+    if (rc != TG_OK) return report(rc);
+    std::printf("{\"scores\":[");
+    for (size_t p = 0; p + 1 < dirs.size(); ++p) {
+        std::printf("%s[", p ? "," : "");
+        for (int m = 0; m < M; ++m) std::printf("%s%.17g", m ? "," : "", scores[p * static_cast<size_t>(M) + static_cast<size_t>(m)]);
+        std::printf("]");
+    }
+    std::printf("]}\n");
+    return 0;
+}
+
+int cmd_check(const Args& a) {
+    if (!require(a, {"ckpt"})) return 1;
+    const int device = a.kv.count("device") ? std::stoi(a.kv.at("device")) : 0;
+    const int rc = tg_verify_checkpoint(a.kv.at("ckpt").c_str(), device);
+    if (rc != TG_OK) return report(rc);
+    std::cout << "ok\n";
+    return 0;
+}
+
+} // namespace
+
+int main(int argc, char** argv) {
+    if (argc < 2) {
+        std::cerr << "usage: tailor <merge|plan|select|score|check> [options]\n";
+        return 1;
+    }
+    Args a;
+    for (int i = 2; i < argc; ++i) {
+        std::string k = argv[i];
+        if (k.rfind("--", 0) != 0) {
+            std::cerr << "unexpected argument " << k << "\n";
+            return 1;
+        }
+        k = k.substr(2);
+        if (i + 1 < argc && std::string(argv[i + 1]).rfind("--", 0) != 0) a.kv[k] = argv[++i];
+        else a.flags.insert(k);
+    }
+    const std::string cmd = argv[1];
+    try {
+        if (cmd == "merge") return cmd_merge(a);
+        if (cmd == "plan") return cmd_plan(a);
+        if (cmd == "select") return cmd_select(a);
+        if (cmd == "score") return cmd_score(a);
+        if (cmd == "check") return cmd_check(a);
+    } catch (const std::exception& e) {
+        std::cerr << "error: " << e.what() << "\n";
+        return 1;
+    }
+    std::cerr << "unknown subcommand " << cmd << "\n";
+    return 1;
+}

@@ -1,0 +1,339 @@
+"""Python mirror of the reference's tailoring interface, bound to the B200 engine.
+
+Names and semantics follow the reference's C++ surface so parity tests read
+like the reference's own tests:
+
+* ``parse_recipe`` / ``recipe_to_yaml``   — R/src/recipe.cpp:67-169
+* ``resolve_plan``                        — R/src/merge.cpp:39-152
+* ``execute_merge``                       — R/src/merge.cpp:226-357 (device gather + device re-verify)
+* ``recipe_from_manifests``               — R/src/merge.cpp:359-418
+* ``score_snapshots`` / ``select_recipe`` — the update-magnitude strategy
+* ``SynthFamily`` / ``Scorer`` / ``MergePartition`` — device-resident partitions (bench, multi-GPU)
+
+Every call goes through ``libtailor_b200.so`` (include/tailor_b200.h); errors
+surface as :class:`TailorError` with the reference's ``ErrorKind``.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import json
+import os
+from typing import Dict, List, Optional, Sequence
+
+from ._lib import (ErrorKind, GatherSegC, MergeOptionsC, MergeStatsC, ModelSpecC, TailorError, check,
+                   check_handle, lib, ptr_array, text_call)
+
+__all__ = ["ErrorKind", "TailorError", "ModelSpec", "RecipeSlice", "MergeRecipe", "MergeOptions", "MergeStats",
+           "parse_recipe", "recipe_to_yaml", "resolve_plan", "execute_merge", "recipe_from_manifests",
+           "verify_checkpoint", "score_snapshots", "select_recipe", "layer_map", "SynthFamily", "Scorer",
+           "MergePartition", "gather"]
+
+
+@dataclasses.dataclass
+class ModelSpec:
+    """R/include/tailor/model.hpp:14-30."""
+
+    num_layers: int
+    hidden_dim: int
+    ffn_dim: int
+    vocab_size: int
+    weight_tied: bool = False
+    seed: int = 42
+
+    def to_c(self) -> ModelSpecC:
+        return ModelSpecC(self.num_layers, self.hidden_dim, self.ffn_dim, self.vocab_size,
+                          1 if self.weight_tied else 0, 0, self.seed)
+
+    @property
+    def module_count(self) -> int:
+        return self.num_layers + (2 if self.weight_tied else 3)
+
+
+@dataclasses.dataclass
+class RecipeSlice:
+    source: str
+    layers: List[int]
+    targets: Optional[List[int]] = None
+
+    def __post_init__(self):
+        if self.targets is None:
+            self.targets = list(self.layers)
+
+
+@dataclasses.dataclass
+class MergeRecipe:
+    """R/include/tailor/recipe.hpp:19-25."""
+
+    num_ranks: int = 0
+    base_checkpoint: str = ""
+    slices: List[RecipeSlice] = dataclasses.field(default_factory=list)
+    aux: Dict[str, str] = dataclasses.field(default_factory=dict)
+    config_from: str = "latest"
+
+    def to_json(self) -> str:
+        return json.dumps({"base_checkpoint": self.base_checkpoint, "num_ranks": self.num_ranks,
+                           "slices": [{"source": s.source, "layers": s.layers, "targets": s.targets}
+                                      for s in self.slices],
+                           "aux": self.aux, "config_from": self.config_from})
+
+    @staticmethod
+    def from_json(text: str) -> "MergeRecipe":
+        j = json.loads(text)
+        return MergeRecipe(num_ranks=j["num_ranks"], base_checkpoint=j["base_checkpoint"],
+                           slices=[RecipeSlice(s["source"], s["layers"], s["targets"]) for s in j["slices"]],
+                           aux=dict(j["aux"]), config_from=j["config_from"])
+
+    def to_yaml(self) -> str:
+        return recipe_to_yaml(self)
+
+
+@dataclasses.dataclass
+class MergeOptions:
+    """R/include/tailor/merge.hpp:46-49 (+ device, verify)."""
+
+    workers: int = 0
+    uncached: bool = False
+    device: int = 0
+    verify: bool = True
+
+
+@dataclasses.dataclass
+class MergeStats:
+    """R/include/tailor/merge.hpp:51-55 (+ device_ms, bytes_moved)."""
+
+    shard_files_read: int
+    weight_files_read: int
+    wall_ms: float
+    device_ms: float
+    bytes_moved: int
+
+
+def _b(s: str) -> bytes:
+    return os.fsencode(s)
+
+
+def parse_recipe(yaml_text: str) -> MergeRecipe:
+    return MergeRecipe.from_json(text_call(lib().tg_parse_recipe, yaml_text.encode()))
+
+
+def recipe_to_yaml(recipe: MergeRecipe) -> str:
+    return text_call(lib().tg_recipe_to_yaml, recipe.to_json().encode())
+
+
+def _yaml_of(recipe) -> bytes:
+    return (recipe if isinstance(recipe, str) else recipe_to_yaml(recipe)).encode()
+
+
+def resolve_plan(recipe) -> dict:
+    """MergePlan as a dict: num_ranks, config_source, sources, group_copies, assignment."""
+    return json.loads(text_call(lib().tg_resolve_plan, _yaml_of(recipe)))
+
+
+def execute_merge(recipe, out_dir: str, options: Optional[MergeOptions] = None) -> MergeStats:
+    o = options or MergeOptions()
+    copt = MergeOptionsC(o.workers, 1 if o.uncached else 0, o.device, 1 if o.verify else 0)
+    st = MergeStatsC()
+    check(lib().tg_execute_merge(_yaml_of(recipe), _b(str(out_dir)), ctypes.byref(copt), ctypes.byref(st)))
+    return MergeStats(st.shard_files_read, st.weight_files_read, st.wall_ms, st.device_ms, st.bytes_moved)
+
+
+def recipe_from_manifests(run_dir: str, failure_step: int) -> MergeRecipe:
+    return parse_recipe(text_call(lib().tg_recipe_from_manifests, _b(str(run_dir)), failure_step))
+
+
+def verify_checkpoint(path: str, device: int = 0) -> None:
+    check(lib().tg_verify_checkpoint(_b(str(path)), device))
+
+
+def _dirs_arg(dirs: Sequence[str]):
+    arr = (ctypes.c_char_p * len(dirs))()
+    for i, d in enumerate(dirs):
+        arr[i] = _b(str(d))
+    return arr
+
+
+def score_snapshots(dirs: Sequence[str], device: int = 0):
+    """Device scores over consecutive snapshot dirs -> (sums[p][m][2], scores[p][m])."""
+    n = len(dirs)
+    cap = max(1, (n - 1)) * 8192
+    sums = (ctypes.c_double * (cap * 2))()
+    scores = (ctypes.c_double * cap)()
+    m = ctypes.c_int32(0)
+    check(lib().tg_score_snapshots(_dirs_arg(dirs), n, device, sums, scores, ctypes.byref(m)))
+    M = m.value
+    return ([[[sums[(p * M + i) * 2], sums[(p * M + i) * 2 + 1]] for i in range(M)] for p in range(n - 1)],
+            [[scores[p * M + i] for i in range(M)] for p in range(n - 1)])
+
+
+def select_recipe(dirs: Sequence[str], rho: float = 0.5, device: int = 0):
+    """Score -> magnitude selection -> recipe. Returns (recipe, source_of, min_boundary_gap)."""
+    src = (ctypes.c_int32 * 8192)()
+    gap = ctypes.c_double(0)
+    yaml = text_call(lambda b, c, n: lib().tg_select_recipe(_dirs_arg(dirs), len(dirs), rho, device, b, c, n, src,
+                                                             ctypes.byref(gap)))
+    rec = parse_recipe(yaml)
+    M = None
+    # source_of length = module count; recover from the layer map of the first snapshot's spec.
+    with open(os.path.join(str(dirs[0]), "config.json")) as f:
+        cfg = json.load(f)
+    M = cfg["num_layers"] + (2 if cfg["weight_tied"] else 3)
+    return rec, [src[i] for i in range(M)], gap.value
+
+
+def layer_map(spec: ModelSpec, num_ranks: int = 1) -> dict:
+    c = spec.to_c()
+    return json.loads(text_call(lambda b, cap, n: lib().tg_layer_map(ctypes.byref(c), num_ranks, b, cap, n)))
+
+
+def gather(d_segs_ptr: int, nseg: int, d_dst: int, dst_bytes: int, variant: int = 0, bulk_ok: bool = False,
+           stream: int = 0) -> None:
+    """Raw K2 launch over a device segment table (tg_gather)."""
+    check(lib().tg_gather(d_segs_ptr, nseg, d_dst, dst_bytes, variant, 1 if bulk_ok else 0, stream))
+
+
+class SynthFamily:
+    """Synthetic snapshots S_1..S_K of SURVEY §8(d), generated on the device."""
+
+    def __init__(self, spec: ModelSpec, num_ranks: int, snapshots: int, interval: int = 100):
+        self.spec, self.num_ranks, self.snapshots, self.interval = spec, num_ranks, snapshots, interval
+        c = spec.to_c()
+        self._h = check_handle(lib().tg_family_create(ctypes.byref(c), num_ranks, snapshots, interval))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().tg_family_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def num_modules(self) -> int:
+        return lib().tg_family_num_modules(self._h)
+
+    @property
+    def parameter_count(self) -> int:
+        return lib().tg_family_parameter_count(self._h)
+
+    def set_partial(self, k: int, modules: Sequence[str]) -> None:
+        check(lib().tg_family_set_partial(self._h, k, ",".join(modules).encode()))
+
+    def set_id(self, k: int, ident: str) -> None:
+        check(lib().tg_family_set_id(self._h, k, ident.encode()))
+
+    def shard_bytes(self, k: int, rank: int) -> int:
+        return lib().tg_family_shard_bytes(self._h, k, rank)
+
+    def weights_bytes(self, k: int) -> int:
+        return lib().tg_family_weights_bytes(self._h, k)
+
+    def packed_master_bytes(self, rank: int) -> int:
+        return lib().tg_family_packed_master_bytes(self._h, rank)
+
+    def gen_shard(self, rank: int, k0: int, k1: int, outs: Sequence[int], stream: int = 0) -> None:
+        check(lib().tg_family_gen_shard(self._h, rank, k0, k1, ptr_array(outs), stream))
+
+    def gen_weights(self, k0: int, k1: int, lo: int, hi: int, outs: Sequence[int], stream: int = 0) -> None:
+        check(lib().tg_family_gen_weights(self._h, k0, k1, lo, hi, ptr_array(outs), stream))
+
+    def gen_masters(self, rank: int, k0: int, k1: int, outs: Sequence[int], stream: int = 0) -> None:
+        check(lib().tg_family_gen_masters(self._h, rank, k0, k1, ptr_array(outs), stream))
+
+    def write_dir(self, k: int, path: str) -> None:
+        check(lib().tg_family_write_dir(self._h, k, _b(str(path))))
+
+    def select(self, rank_partials: Sequence[float], nranks: int, rho: float = 0.5):
+        """Combine [nranks][K-1][M][2] partials in rank order -> (recipe_yaml, source_of, scores, gap)."""
+        M, K = self.num_modules, self.snapshots
+        arr = (ctypes.c_double * len(rank_partials))(*rank_partials)
+        src = (ctypes.c_int32 * M)()
+        scores = (ctypes.c_double * max(1, (K - 1) * M))()
+        gap = ctypes.c_double(0)
+        yaml = text_call(lambda b, c, n: lib().tg_family_select(self._h, arr, nranks, rho, b, c, n, src, scores,
+                                                                 ctypes.byref(gap)))
+        return (yaml, [src[i] for i in range(M)],
+                [[scores[p * M + m] for m in range(M)] for p in range(K - 1)], gap.value)
+
+
+class Scorer:
+    """K3/K4 scorer plan for one rank partition of snapshots k0..k1 of a family."""
+
+    def __init__(self, family: SynthFamily, rank: int, k0: int, k1: int, packed: bool = False):
+        self._fam = family
+        self._h = check_handle(lib().tg_scorer_create(family.handle, rank, k0, k1, 1 if packed else 0))
+        self.K = k1 - k0 + 1
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().tg_scorer_destroy(h)
+            self._h = None
+
+    @property
+    def bytes_read(self) -> int:
+        return lib().tg_scorer_bytes(self._h)
+
+    def run(self, bases: Sequence[int], d_out: int, stream: int = 0) -> None:
+        check(lib().tg_scorer_run(self._h, ptr_array(bases), d_out, stream))
+
+
+class MergePartition:
+    """K2 plan for one output partition: container=-1 -> weights share unit/units, r -> rank-r shard."""
+
+    def __init__(self, family: SynthFamily, recipe_yaml: str, container: int, unit: int = 0, units: int = 1):
+        self._fam = family
+        self._h = check_handle(lib().tg_mplan_create(family.handle, recipe_yaml.encode(), container, unit, units))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().tg_mplan_destroy(h)
+            self._h = None
+
+    @property
+    def bytes(self) -> int:
+        return lib().tg_mplan_bytes(self._h)
+
+    @property
+    def num_segments(self) -> int:
+        return lib().tg_mplan_num_segments(self._h)
+
+    @property
+    def bulk_ok(self) -> bool:
+        return bool(lib().tg_mplan_bulk_ok(self._h))
+
+    def range(self):
+        lo, hi, pb = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib().tg_mplan_range(self._h, ctypes.byref(lo), ctypes.byref(hi), ctypes.byref(pb)))
+        return lo.value, hi.value, pb.value
+
+    def windows(self):
+        out = []
+        for i in range(lib().tg_mplan_num_windows(self._h)):
+            k, c, lo, hi = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_uint64(), ctypes.c_uint64()
+            check(lib().tg_mplan_window(self._h, i, ctypes.byref(k), ctypes.byref(c), ctypes.byref(lo),
+                                        ctypes.byref(hi)))
+            out.append((k.value, c.value, lo.value, hi.value))
+        return out
+
+    def prefix(self) -> bytes:
+        need = ctypes.c_size_t(0)
+        lib().tg_mplan_prefix(self._h, None, 0, ctypes.byref(need))
+        buf = ctypes.create_string_buffer(need.value)
+        check(lib().tg_mplan_prefix(self._h, buf, need.value, ctypes.byref(need)))
+        return buf.raw[:need.value]
+
+    def bind(self, window_ptrs: Sequence[int]) -> None:
+        check(lib().tg_mplan_bind(self._h, ptr_array(window_ptrs)))
+
+    def run(self, d_dst: int, variant: int = 0, stream: int = 0) -> None:
+        check(lib().tg_mplan_run(self._h, d_dst, variant, stream))
+
+    def run_host(self, h_windows: Sequence[int], h_dst: int, variant: int = 0, chunk_bytes: int = 0):
+        h2d, d2h = ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib().tg_mplan_run_host(self._h, ptr_array(h_windows), h_dst, variant, chunk_bytes,
+                                      ctypes.byref(h2d), ctypes.byref(d2h)))
+        return h2d.value, d2h.value

@@ -1,0 +1,411 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+Oracles: oracle/tailor_oracle.py (numpy restatement, pinned in test_oracle.py)
+and oracle/_ref/ref_tool (the reference library itself, compiled from
+/root/reference by oracle/Makefile; the binary travels to the GPU box).
+Bar: bit-exact bytes for every payload, header and sidecar; scores within
+1e-6 relative; identical selections and recipes.
+"""
+import filecmp
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2602_22158_b200 as t  # noqa: E402
+import tailor_oracle as o  # noqa: E402
+from conftest import ref_tool, spec_args  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+SCORE_RTOL = 1e-6  # SURVEY §8 a13 tolerance for FP64 scores
+
+
+def need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def ospec(s: t.ModelSpec) -> dict:
+    return dict(num_layers=s.num_layers, hidden_dim=s.hidden_dim, ffn_dim=s.ffn_dim, vocab_size=s.vocab_size,
+                weight_tied=s.weight_tied, seed=s.seed)
+
+
+SHAPES = [
+    (t.ModelSpec(4, 8, 16, 32, False, 42), 4),
+    (t.ModelSpec(3, 4, 4, 8, True, 50001), 3),     # tied; 12-B chunks (misaligned segments)
+    (t.ModelSpec(2, 6, 10, 11, False, 9), 2),      # ragged, odd vocab
+    (t.ModelSpec(1, 1, 1, 1, False, 1), 8),        # degenerate: padding-only ranks
+    (t.ModelSpec(4, 64, 172, 512, False, 42), 8),
+]
+
+
+def dev(n):
+    return torch.empty(max(16, n), dtype=torch.uint8, device="cuda")
+
+
+def host_bytes(buf, n):
+    return bytes(buf[:n].cpu().numpy())
+
+
+@pytest.mark.parametrize("spec,N", SHAPES)
+def test_generator_matches_oracle(spec, N):
+    need_gpu()
+    K = 3
+    fam = t.SynthFamily(spec, N, K)
+    os_ = ospec(spec)
+    exp = [o.snapshot_payloads(os_, N, k) for k in range(1, K + 1)]
+    for r in range(N):
+        bufs = [dev(fam.shard_bytes(k, r)) for k in range(1, K + 1)]
+        fam.gen_shard(r, 1, K, [b.data_ptr() for b in bufs])
+        torch.cuda.synchronize()
+        for k in range(K):
+            assert host_bytes(bufs[k], fam.shard_bytes(k + 1, r)) == exp[k][1][r], (r, k)
+    wb = fam.weights_bytes(1)
+    bufs = [dev(wb) for _ in range(K)]
+    fam.gen_weights(1, K, 0, wb, [b.data_ptr() for b in bufs])
+    torch.cuda.synchronize()
+    for k in range(K):
+        assert host_bytes(bufs[k], wb) == exp[k][0]
+
+
+def test_write_dir_matches_reference_writer(tmp_path):
+    """GPU generator + our writer == reference write_checkpoint, every file, every byte."""
+    need_gpu()
+    spec = t.ModelSpec(3, 8, 12, 20, False, 7)
+    N, K = 3, 3
+    ref_tool("gen", *spec_args(ospec(spec)), "--ranks", N, "--snapshots", K, "--out", tmp_path / "ref")
+    fam = t.SynthFamily(spec, N, K)
+    for k in range(1, K + 1):
+        fam.write_dir(k, str(tmp_path / "ours" / f"checkpoint-{k * 100}"))
+    cmp = filecmp.dircmp(tmp_path / "ref", tmp_path / "ours")
+    _assert_same_tree(tmp_path / "ref", tmp_path / "ours")
+
+
+def _assert_same_tree(a, b):
+    fa = sorted(str(p.relative_to(a)) for p in a.rglob("*") if p.is_file())
+    fb = sorted(str(p.relative_to(b)) for p in b.rglob("*") if p.is_file())
+    assert fa == fb
+    for rel in fa:
+        assert (a / rel).read_bytes() == (b / rel).read_bytes(), rel
+
+
+@pytest.mark.parametrize("K", [2, 3, 4, 16])
+def test_scorer_matches_oracle(K):
+    need_gpu()
+    spec = t.ModelSpec(3, 16, 40, 50, False, 1234)
+    N = 4
+    fam = t.SynthFamily(spec, N, K)
+    M = fam.num_modules
+    parts = []
+    for r in range(N):
+        bufs = [dev(fam.shard_bytes(k, r)) for k in range(1, K + 1)]
+        fam.gen_shard(r, 1, K, [b.data_ptr() for b in bufs])
+        out = torch.zeros((K - 1) * M * 2, dtype=torch.float64, device="cuda")
+        t.Scorer(fam, r, 1, K).run([b.data_ptr() for b in bufs], out.data_ptr())
+        torch.cuda.synchronize()
+        parts += out.cpu().tolist()
+    yaml, src, scores, gap = fam.select(parts, N, 0.5)
+    os_ = ospec(spec)
+    W = [o.model_vectors(os_, k)[0] for k in range(1, K + 1)]
+    ref = [[o.magnitude_score(*x) for x in o.score_pair(os_, W[p], W[p + 1])] for p in range(K - 1)]
+    for p in range(K - 1):
+        for m in range(M):
+            assert scores[p][m] == pytest.approx(ref[p][m], rel=SCORE_RTOL)
+    _, ref_src, ref_gap = o.select(ref, M, 0.5)
+    assert src == ref_src
+    assert ref_gap > 1e-4
+
+
+def test_scorer_packed_equals_full():
+    need_gpu()
+    spec = t.ModelSpec(2, 32, 64, 100, False, 5)
+    N, K = 2, 4
+    fam = t.SynthFamily(spec, N, K)
+    M = fam.num_modules
+    for r in range(N):
+        full = [dev(fam.shard_bytes(k, r)) for k in range(1, K + 1)]
+        packed = [dev(fam.packed_master_bytes(r)) for _ in range(K)]
+        fam.gen_shard(r, 1, K, [b.data_ptr() for b in full])
+        fam.gen_masters(r, 1, K, [b.data_ptr() for b in packed])
+        a = torch.zeros((K - 1) * M * 2, dtype=torch.float64, device="cuda")
+        b = torch.zeros_like(a)
+        t.Scorer(fam, r, 1, K).run([x.data_ptr() for x in full], a.data_ptr())
+        t.Scorer(fam, r, 1, K, packed=True).run([x.data_ptr() for x in packed], b.data_ptr())
+        torch.cuda.synchronize()
+        assert torch.equal(a, b)  # same tiles, same order: bitwise
+
+
+def _random_assignment(rng, spec, K):
+    mods = o.modules(ospec(spec))
+    L = spec.num_layers
+    targets = list(range(L))
+    if rng.random() < 0.3:
+        rng.shuffle(targets)
+    assign, slices = {}, {}
+    for i in range(L):
+        k = rng.randrange(1, K + 1)
+        assign[f"layers.{targets[i]}"] = (f"S{k}", f"layers.{i}")
+        slices.setdefault(k, ([], []))
+        slices[k][0].append(i)
+        slices[k][1].append(targets[i])
+    recipe = t.MergeRecipe(num_ranks=0)
+    for k, (ls, ts) in sorted(slices.items()):
+        recipe.slices.append(t.RecipeSlice(f"S{k}", ls, ts))
+    for m in mods:
+        if m.startswith("layers."):
+            continue
+        k = rng.randrange(1, K + 1)
+        assign[m] = (f"S{k}", m)
+        recipe.aux[m] = f"S{k}"
+    return recipe, assign
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_partition_merge_matches_oracle(seed):
+    """Device-resident K2 over random recipes (layer moves, tied, misaligned shapes)."""
+    need_gpu()
+    rng = random.Random(seed)
+    spec, N = SHAPES[seed % len(SHAPES)]
+    K = 3
+    fam = t.SynthFamily(spec, N, K)
+    recipe, assign = _random_assignment(rng, spec, K)
+    recipe.num_ranks = N
+    yaml = recipe.to_yaml()
+    os_ = ospec(spec)
+    mods = o.modules(os_)
+    srcs = {f"S{k}": (*o.snapshot_payloads(os_, N, k), mods) for k in range(1, K + 1)}
+    exp_w, exp_r, exp_wp, exp_rp = o.merge_payloads(os_, N, assign, srcs)
+    for r in range(N):
+        bufs = [dev(fam.shard_bytes(k, r)) for k in range(1, K + 1)]
+        fam.gen_shard(r, 1, K, [b.data_ptr() for b in bufs])
+        mp = t.MergePartition(fam, yaml, r)
+        assert mp.prefix() == exp_rp[r]
+        mp.bind([bufs[k - 1].data_ptr() + lo for k, c, lo, hi in mp.windows()])
+        for variant in (0, 1):
+            out = dev(mp.bytes)
+            mp.run(out.data_ptr(), variant)
+            torch.cuda.synchronize()
+            assert host_bytes(out, mp.bytes) == exp_r[r], (r, variant)
+    wb = fam.weights_bytes(1)
+    wbufs = [dev(wb) for _ in range(K)]
+    fam.gen_weights(1, K, 0, wb, [b.data_ptr() for b in wbufs])
+    for units in (1, 3):
+        got = b""
+        for u in range(units):
+            mp = t.MergePartition(fam, yaml, -1, u, units)
+            lo, hi, total = mp.range()
+            mp.bind([wbufs[k - 1].data_ptr() + wlo for k, c, wlo, whi in mp.windows()])
+            out = dev(mp.bytes)
+            mp.run(out.data_ptr())
+            torch.cuda.synchronize()
+            got += host_bytes(out, mp.bytes)
+        assert got == exp_w
+        assert mp.prefix() == exp_wp
+
+
+def test_host_pipeline_matches_device():
+    need_gpu()
+    spec = t.ModelSpec(4, 64, 172, 512, False, 3)
+    N, K = 2, 3
+    fam = t.SynthFamily(spec, N, K)
+    recipe = t.MergeRecipe(num_ranks=N, base_checkpoint="S3", slices=[t.RecipeSlice("S1", [0, 2]), t.RecipeSlice("S2", [1])],
+                           aux={"embed_tokens": "S2"})
+    yaml = recipe.to_yaml()
+    for r in range(N):
+        bufs = [dev(fam.shard_bytes(k, r)) for k in range(1, K + 1)]
+        fam.gen_shard(r, 1, K, [b.data_ptr() for b in bufs])
+        mp = t.MergePartition(fam, yaml, r)
+        mp.bind([bufs[k - 1].data_ptr() + lo for k, c, lo, hi in mp.windows()])
+        out = dev(mp.bytes)
+        mp.run(out.data_ptr())
+        hsrc = [b.cpu().pin_memory() for b in bufs]
+        hdst = torch.empty(mp.bytes, dtype=torch.uint8).pin_memory()
+        h2d, d2h = mp.run_host([hsrc[k - 1].data_ptr() + lo for k, c, lo, hi in mp.windows()], hdst.data_ptr(),
+                               chunk_bytes=4096)
+        torch.cuda.synchronize()
+        assert bytes(hdst.numpy()) == host_bytes(out, mp.bytes)
+        assert h2d == mp.bytes and d2h == mp.bytes  # only the needed bytes cross PCIe
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_gather_variants_random_segments(seed):
+    """Raw K2 (tg_gather): LSU and bulk paths vs a torch reference copy."""
+    need_gpu()
+    import ctypes
+
+    g = torch.Generator().manual_seed(seed)
+    src = torch.randint(0, 256, (1 << 20,), dtype=torch.uint8, generator=g).cuda()
+    align = 16 if seed % 2 == 0 else 1
+    segs, dst_off = [], 0
+    expect = []
+    while dst_off < 600_000:
+        n = int(torch.randint(1, 40_000, (1,), generator=g)) // align * align or align
+        so = int(torch.randint(0, (1 << 20) - n, (1,), generator=g)) // align * align
+        segs.append((src.data_ptr() + so, dst_off, n))
+        expect.append(src[so:so + n])
+        dst_off += n
+    expect = torch.cat(expect)
+    table = (t._lib.GatherSegC * len(segs))(*[t._lib.GatherSegC(a, b, c) for a, b, c in segs])
+    raw = torch.frombuffer(bytearray(bytes(table)), dtype=torch.uint8).cuda()
+    variants = [1] + ([2] if align == 16 else [])
+    for v in variants:
+        dst = torch.zeros(dst_off, dtype=torch.uint8, device="cuda")
+        t.gather(raw.data_ptr(), len(segs), dst.data_ptr(), dst_off, v, bulk_ok=(v == 2))
+        torch.cuda.synchronize()
+        assert torch.equal(dst, expect), v
+
+
+# ---------------------------------------------------------------- files ----------
+def _gen_ref(tmp, spec, N, K, name="run", partial=None):
+    args = ["gen", *spec_args(ospec(spec)), "--ranks", N, "--snapshots", K, "--out", tmp / name]
+    if partial:
+        args += ["--partial", partial]
+    return ref_tool(*args)[1]["snapshots"]
+
+
+def _ref_merge(recipe: t.MergeRecipe, out, extra=()):
+    p = out.parent / (out.name + ".recipe.json")
+    p.write_text(recipe.to_json())
+    return ref_tool("merge", "--recipe", p, "--out", out, *extra)[1]
+
+
+def _both_merge(tmp, recipe, name="m", **opt):
+    ref_out, our_out = tmp / f"{name}_ref", tmp / f"{name}_ours"
+    ref = _ref_merge(recipe, ref_out, ["--uncached"] if opt.get("uncached") else [])
+    st = t.execute_merge(recipe, str(our_out), t.MergeOptions(**opt))
+    _assert_same_tree(ref_out, our_out)
+    assert st.shard_files_read == ref["stats"]["shard_files_read"]
+    assert st.weight_files_read == ref["stats"]["weight_files_read"]
+    return st
+
+
+def test_execute_merge_parity_recipe_matches_reference(tmp_path):
+    """R/tests/test_merge.cpp:100-139 shape: L=4, N=4, two sources, 11 group copies."""
+    need_gpu()
+    spec = t.ModelSpec(4, 8, 16, 32, False, 909)
+    d = _gen_ref(tmp_path, spec, 4, 2)
+    recipe = t.MergeRecipe(num_ranks=4, slices=[t.RecipeSlice(d[0], [0, 2]), t.RecipeSlice(d[1], [1, 3])],
+                           aux={"embed_tokens": d[0], "norm": d[1], "lm_head": d[1]})
+    assert len(t.resolve_plan(recipe)["group_copies"]) == 11
+    st = _both_merge(tmp_path, recipe)
+    assert st.shard_files_read <= 8 and st.weight_files_read == 2
+
+
+def test_execute_merge_identity_is_fixed_point(tmp_path):
+    need_gpu()
+    spec = t.ModelSpec(3, 8, 16, 32, False, 808)
+    d = _gen_ref(tmp_path, spec, 2, 1)
+    st = _both_merge(tmp_path, t.MergeRecipe(num_ranks=2, base_checkpoint=d[0]))
+    assert st.shard_files_read == 2
+    for rel in ["model.weights", "optim/rank_0.shard", "optim/rank_1.shard", "config.json", "trainer_state.json"]:
+        assert (tmp_path / "m_ours" / rel).read_bytes() == open(os.path.join(d[0], rel), "rb").read()
+    t.execute_merge(t.MergeRecipe(num_ranks=2, base_checkpoint=str(tmp_path / "m_ours")), str(tmp_path / "m2"))
+    for rel in ["model.weights", "optim/rank_0.shard", "optim/rank_1.shard"]:
+        assert (tmp_path / "m2" / rel).read_bytes() == (tmp_path / "m_ours" / rel).read_bytes()
+
+
+def test_execute_merge_cross_position_tied(tmp_path):
+    need_gpu()
+    spec = t.ModelSpec(4, 8, 16, 32, True, 1212)
+    d = _gen_ref(tmp_path, spec, 2, 1)
+    _both_merge(tmp_path, t.MergeRecipe(num_ranks=2, base_checkpoint=d[0], slices=[t.RecipeSlice(d[0], [0, 1], [3, 2])]))
+
+
+def test_execute_merge_uncached_counts_and_bytes(tmp_path):
+    need_gpu()
+    spec = t.ModelSpec(4, 8, 16, 32, False, 2323)
+    d = _gen_ref(tmp_path, spec, 4, 2)
+    recipe = t.MergeRecipe(num_ranks=4, slices=[t.RecipeSlice(d[0], [0, 2]), t.RecipeSlice(d[1], [1, 3])],
+                           aux={"embed_tokens": d[0], "norm": d[1], "lm_head": d[1]})
+    st = _both_merge(tmp_path, recipe, uncached=True)
+    assert st.shard_files_read == 4 * 11
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_execute_merge_random_cases_match_reference(tmp_path, case):
+    """Acceptance c4-style: random L<=8, tied, h in {4,8}, N<=4, K<=3, layer permutations."""
+    need_gpu()
+    rng = random.Random(1000 + case)
+    L = 1 + rng.randrange(8)
+    spec = t.ModelSpec(L, 4 << rng.randrange(2), 4 << rng.randrange(2), 8 << rng.randrange(2), rng.random() < 0.5,
+                       50000 + case)
+    N = 1 + rng.randrange(4)
+    K = 1 + rng.randrange(3)
+    d = _gen_ref(tmp_path, spec, N, K)
+    ids = {f"S{k}": d[k - 1] for k in range(1, K + 1)}
+    recipe, _ = _random_assignment(rng, spec, K)
+    recipe.num_ranks = N
+    recipe.slices = [t.RecipeSlice(ids[s.source], s.layers, s.targets) for s in recipe.slices]
+    recipe.aux = {k: ids[v] for k, v in recipe.aux.items()}
+    if rng.random() < 0.5:
+        recipe.base_checkpoint = d[-1]
+    _both_merge(tmp_path, recipe, workers=1 + rng.randrange(4))
+
+
+def test_execute_merge_partial_sources_and_errors(tmp_path):
+    need_gpu()
+    spec = t.ModelSpec(4, 8, 16, 32, False, 4)
+    d = _gen_ref(tmp_path, spec, 2, 2, partial="2=layers.0,norm")
+    # source 2 holds only layers.0 + norm
+    _both_merge(tmp_path, t.MergeRecipe(num_ranks=2, base_checkpoint=d[0], slices=[t.RecipeSlice(d[1], [0])],
+                                        aux={"norm": d[1]}))
+    with pytest.raises(t.TailorError) as e:
+        t.execute_merge(t.MergeRecipe(num_ranks=2, base_checkpoint=d[0], slices=[t.RecipeSlice(d[1], [2])]),
+                        str(tmp_path / "x"))
+    assert e.value.kind == t.ErrorKind.SourceLacksModule
+    (tmp_path / "full").mkdir()
+    (tmp_path / "full" / "f").write_text("x")
+    with pytest.raises(t.TailorError) as e:
+        t.execute_merge(t.MergeRecipe(num_ranks=2, base_checkpoint=d[0]), str(tmp_path / "full"))
+    assert e.value.kind == t.ErrorKind.Storage
+
+
+def test_reference_trained_parity_pipeline(tmp_path):
+    """Acceptance c5 shape on reference-written partial checkpoints: train(parity) -> fail -> plan -> merge."""
+    need_gpu()
+    spec = dict(num_layers=4, hidden_dim=8, ffn_dim=16, vocab_size=32, seed=31415)
+    ref_tool("train", *spec_args(spec), "--strategy", "parity", "--steps", 100, "--interval", 25, "--ranks", 2,
+             "--out", tmp_path / "run", "--fail-at", 110)
+    ours = t.recipe_from_manifests(str(tmp_path / "run"), 110)
+    ref = t.MergeRecipe.from_json(json.dumps(ref_tool("plan", "--run", tmp_path / "run", "--failure-step", 110)[1]["recipe"]))
+    assert ours == ref
+    _both_merge(tmp_path, ours)
+
+
+def test_verify_detects_corruption(tmp_path):
+    need_gpu()
+    spec = t.ModelSpec(2, 8, 16, 32, False, 77)
+    d = _gen_ref(tmp_path, spec, 3, 1)
+    t.verify_checkpoint(d[0])
+    import shutil
+
+    bad = tmp_path / "bad"
+    shutil.copytree(d[0], bad)
+    w = bytearray((bad / "model.weights").read_bytes())
+    w[-1] ^= 0x01
+    (bad / "model.weights").write_bytes(bytes(w))
+    with pytest.raises(t.TailorError) as e:
+        t.verify_checkpoint(str(bad))
+    assert e.value.kind == t.ErrorKind.Consistency
+    rc, _, err = ref_tool("read", "--dir", bad, check=False)
+    assert rc == 2 and "ConsistencyError" in err
+
+
+def test_select_recipe_matches_reference_scorer(tmp_path):
+    need_gpu()
+    spec = t.ModelSpec(4, 16, 40, 64, False, 42)
+    d = _gen_ref(tmp_path, spec, 2, 4)
+    rec, src, gap = t.select_recipe(d, 0.5)
+    ref = ref_tool("score", "--snapshots", ",".join(d), "--rho", "0.5")[1]
+    _, scores = t.score_snapshots(d)
+    for p, row in enumerate(ref["scores"]):
+        for m, v in enumerate(row):
+            assert scores[p][m] == pytest.approx(v, rel=SCORE_RTOL)
+    assert rec == t.MergeRecipe.from_json(json.dumps(ref["recipe"]))
+    assert gap == pytest.approx(ref["min_boundary_gap"], rel=1e-6)
+    _both_merge(tmp_path, rec)
