@@ -50,6 +50,8 @@ WORKLOADS = {
              "Qwen2.5-7B-shaped, half-layer merge of 2 sources (as 8 ZeRO-rank partitions)"),
     "cfg1": (4, 256, 688, 32000, False, 1, 2, 0.5,
              "tiny Llama-style 4-layer (hidden 256), 2 sources half-layer merge, 1 ZeRO rank"),
+    "cfg4": (32, 4096, 14336, 128256, False, 8, 16, 0.5,
+             "Llama-3.1-8B-shaped update-norm scoring sweep over 16 consecutive snapshots (scorer only)"),
 }
 # Reference-arm / cpu_baseline sample: cfg3's merge, shrunk to fit a few
 # seconds of CPU work per step (same layout rules, 8 ranks, 4 snapshots).
@@ -86,7 +88,7 @@ class ClockSampler:
     def __enter__(self):
         if shutil.which("nvidia-smi"):
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.reader = threading.Thread(target=self._read, daemon=True)
             self.reader.start()
@@ -171,7 +173,7 @@ def reference_arm(args, rank, world):
     if rank != 0:
         return 0
     cores = os.cpu_count() or 1
-    wl = WORKLOADS[args.workload]
+    wl = WORKLOADS.get(args.workload, WORKLOADS["cfg3"])
     if not ref_tool_path().exists():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_tool not built"}))
         return 0
@@ -231,6 +233,7 @@ def our_arm(args, rank, world, local_rank):
     wbufs = [torch.empty(max(16, whi - wlo), dtype=torch.uint8, device=dev) for _ in range(K)]
     fam.gen_weights(1, K, wlo, whi, [b.data_ptr() for b in wbufs], sp)
     scorer = t.Scorer(fam, r, 1, K)
+    scorer.set_variant(args.score_variant)
     partials = torch.zeros((K - 1) * M * 2, dtype=torch.float64, device=dev)
     gathered = torch.zeros(world * (K - 1) * M * 2, dtype=torch.float64, device=dev)
     torch.cuda.synchronize(dev)
@@ -343,6 +346,7 @@ def our_arm(args, rank, world, local_rank):
                    "composite_bytes_per_gpu_step": composite, "parallelism": f"zero-partition x{world}",
                    "l2": "inputs 62 GB/GPU >> 126 MB L2 (no flush needed)",
                    "gather_variant": {0: "auto", 1: "lsu", 2: "bulk"}[args.variant],
+                   "score_variant": {0: "auto", 1: "register", 2: "staged"}[args.score_variant],
                    "plan_ms_uncached": round(plan_ms, 3), "min_boundary_gap": state["gap"]},
         "layers_scored_per_s": round(scores_per_s, 1),
         "kernels_ms": {k: round(statistics.mean(x), 4) for k, x in kt.items()},
@@ -439,6 +443,150 @@ def e2e_run(args, t, torch, fam, scorer, shards, wbufs, wlo, yaml, r, N, world, 
             "path": "tg_mplan_run_host (C ABI) + H2D of master fields for tg_scorer_run; pinned host sources"}
 
 
+def scorer_arm(args, rank, world, local_rank):
+    """cfg4: scorer-only sweep. Each GPU holds the packed fp32 masters of its rank
+    partition for 16 consecutive snapshots (16 x 4.4 GB) and scores the 15
+    consecutive pairs in one pass (each snapshot read once), then the partials are
+    all-gathered and combined. Metric: module-scores per second."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_22158_b200 as t
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    L, h, f, v, tied, N, K, rho, desc = WORKLOADS[args.workload]
+    fam = t.SynthFamily(t.ModelSpec(L, h, f, v, tied, 42), N, K, 100)
+    M, r = fam.num_modules, rank
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    bufs = [torch.empty(fam.packed_master_bytes(r), dtype=torch.uint8, device=dev) for _ in range(K)]
+    fam.gen_masters(r, 1, K, [b.data_ptr() for b in bufs], sp)
+    scorer = t.Scorer(fam, r, 1, K, packed=True)
+    scorer.set_variant(args.score_variant)
+    partials = torch.zeros((K - 1) * M * 2, dtype=torch.float64, device=dev)
+    gathered = torch.zeros(world * (K - 1) * M * 2, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize(dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    kms = []
+
+    def step(rec):
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        scorer.run([b.data_ptr() for b in bufs], partials.data_ptr(), sp)
+        e1.record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, partials)
+            parts = gathered.cpu()
+        else:
+            parts = partials.cpu()
+        out = fam.select(parts.tolist(), world, rho)
+        if rec is not None:
+            rec.append((e0, e1))
+        return out
+
+    for _ in range(args.warmup):
+        step(None)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    recs = []
+    with ClockSampler(local_rank) as clocks:
+        start, end = ev(), ev()
+        start.record(stream)
+        for _ in range(args.steps):
+            res = step(recs)
+        end.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = start.elapsed_time(end)
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    kms = statistics.mean(a.elapsed_time(b) for a, b in recs)
+    hbm, peak_kind = peaks()
+    achieved = scorer.bytes_read / (kms / 1e3) / 1e9
+    traffic, src = ncu_traffic("score_staged_kernel<16>" if args.score_variant != 1 else "score_partials_kernel<16>")
+    if rank != 0:
+        return 0
+    # Units: one rank partition of every module-pair score per GPU per step; all G
+    # GPUs together produce (K-1) x M complete module scores per step once G = N.
+    value = (K - 1) * M * world / N * args.steps / (ms / 1e3)
+    print(json.dumps({
+        "metric": "module update-magnitude scores per second (scorer-only sweep)", "value": round(value, 1),
+        "unit": "module-scores/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 -> f64 accumulate", "data": "synthetic",
+        "config": {"workload": "cfg4", "description": desc, "snapshots": K, "pairs": K - 1, "modules": M,
+                   "zero_ranks": N, "unit_of_work": "one ZeRO rank partition of 16 snapshots' masters per GPU",
+                   "score_variant": {0: "auto", 1: "register", 2: "staged"}[args.score_variant],
+                   "bytes_per_gpu_step": scorer.bytes_read, "min_boundary_gap": res[3]},
+        "roofline": {"bound": "hbm", "kernel": "K3 score_partials<16>", "achieved": round(achieved, 1), "peak": hbm,
+                     "unit": "GB/s", "frac": round(achieved / hbm, 4), "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": scorer.bytes_read, "traffic": traffic, "traffic_source": src},
+        "gpu_launches": args.steps * 2, "clocks": clocks.summary()}))
+    return 0
+
+
+FILES_SPEC = (8, 1024, 2752, 32000, False, 8, 4, 0.5)  # BASELINE.md §2 "medium" shape
+
+
+def files_arm(args):
+    """Drop-in comparison on files (the reference's own definition of a merge:
+    file reads, assembly, writes and the mandatory re-verify): our select+merge
+    (device scorer on the snapshot files -> selection -> execute_merge with the
+    device gather and device re-verify) vs the reference's (ref_tool select-merge:
+    read_checkpoint scorer restatement + resolve_plan + execute_merge) on the same
+    synthetic snapshot directories (page cache warm, /tmp)."""
+    import paper_2602_22158_b200 as t
+
+    L, h, f, v, tied, N, K, rho = FILES_SPEC
+    cores = os.cpu_count() or 1
+    work = pathlib.Path(tempfile.mkdtemp(prefix="tailor-files-"))
+    try:
+        fam = t.SynthFamily(t.ModelSpec(L, h, f, v, tied, 42), N, K, 100)
+        dirs = [str(work / "run" / f"checkpoint-{k * 100}") for k in range(1, K + 1)]
+        for k in range(1, K + 1):
+            fam.write_dir(k, dirs[k - 1])
+        ours, refs, comp = [], [], 0
+        for i in range(args.warmup + args.steps):
+            out = work / f"ours-{i}"
+            t0 = time.perf_counter()
+            rec, _, gap = t.select_recipe(dirs, rho)
+            st = t.execute_merge(rec, str(out), t.MergeOptions(workers=cores))
+            dt = time.perf_counter() - t0
+            comp = st.bytes_moved
+            shutil.rmtree(out, ignore_errors=True)
+            if i >= args.warmup:
+                ours.append(dt)
+        ref_steps = max(1, min(args.steps, 3))
+        for i in range(1 + ref_steps):
+            out = work / f"ref-{i}"
+            t0 = time.perf_counter()
+            subprocess.run([str(ref_tool_path()), "select-merge", "--snapshots", ",".join(dirs), "--rho", str(rho),
+                            "--out", str(out), "--workers", str(cores)], check=True, capture_output=True)
+            dt = time.perf_counter() - t0
+            shutil.rmtree(out, ignore_errors=True)
+            if i >= 1:
+                refs.append(dt)
+    finally:
+        shutil.rmtree(work, ignore_errors=True)
+    o_v = comp / statistics.median(ours) / 1e9
+    r_v = comp / statistics.median(refs) / 1e9
+    print(json.dumps({
+        "metric": "composite-checkpoint merge GB/s on files (score+select+merge+re-verify)",
+        "value": round(o_v, 4), "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(statistics.median(ours) * 1e3, 2), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8/f32/f64", "data": "synthetic (written by the GPU writer, byte-identical "
+                                                          "to the reference writer), page cache warm",
+        "config": {"workload": "files", "shape": f"L{L} h{h} f{f} v{v} N{N} K{K} rho{rho}",
+                   "composite_bytes": comp, "min_boundary_gap": gap},
+        "reference": {"value": round(r_v, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
+                      "ms_per_step": round(statistics.median(refs) * 1e3, 1)},
+        "speedup_vs_reference": round(o_v / r_v, 2)}))
+    return 0
+
+
 def master_byte_ranges(fam, r, K):
     """Byte ranges of the g*.master entries in rank r's shard payload (from the oracle-free layout)."""
     import json as _json
@@ -465,14 +613,23 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS) + ["files"], default="cfg3")
     ap.add_argument("--variant", type=int, default=0, help="gather: 0 auto, 1 LSU, 2 TMA bulk")
+    ap.add_argument("--score-variant", type=int, default=0, help="scorer: 0 auto, 1 register, 2 TMA-staged")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
         return reference_arm(args, rank, world)
+    if args.workload == "cfg4":
+        return init_and(scorer_arm, args, rank, world, local_rank)
+    if args.workload == "files":
+        return files_arm(args) if rank == 0 else 0
+    return init_and(our_arm, args, rank, world, local_rank)
+
+
+def init_and(fn, args, rank, world, local_rank):
     if world > 1:
         import torch
         import torch.distributed as dist
@@ -480,7 +637,7 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        return our_arm(args, rank, world, local_rank)
+        return fn(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

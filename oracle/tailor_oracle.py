@@ -352,3 +352,18 @@ def select(scores: Sequence[Sequence[float]], M: int, rho: float):
         for m in s:
             src[m] = k
     return saved, src, gap
+
+
+def element_values(spec, k: int, e: np.ndarray, module_index: np.ndarray):
+    """(master, exp_avg, exp_avg_sq) of snapshot k at global element ids `e` whose owning
+    canonical modules are `module_index` — the generator at arbitrary points, for
+    full-size spot checks without materialising the model."""
+    seed = spec["seed"]
+    M = len(modules(spec))
+    e = e.astype(np.uint64)
+    w = np.float32(0.02) * unit_noise(seed, 0, e)
+    for j in range(1, k + 1):
+        sig = sigma_table(seed, M, j)[module_index]
+        neg = (hash3(seed ^ SIGN_SALT, j, e) >> np.uint64(63)).astype(bool)
+        w = (w + np.where(neg, -sig, sig)).astype(np.float32)
+    return w, np.float32(0.1) * unit_noise(seed ^ M_SALT, k, e), np.abs(np.float32(0.01) * unit_noise(seed ^ V_SALT, k, e))

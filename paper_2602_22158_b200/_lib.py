@@ -120,6 +120,7 @@ SIGNATURES = {
     "tg_scorer_create": (_P, [_P, _I32, _I32, _I32, _I32]),
     "tg_scorer_destroy": (None, [_P]),
     "tg_scorer_bytes": (_U64, [_P]),
+    "tg_scorer_set_variant": (_I, [_P, _I32]),
     "tg_scorer_run": (_I, [_P, _PP, _P, _P]),
     "tg_mplan_create": (_P, [_P, _S, _I32, _I32, _I32]),
     "tg_mplan_destroy": (None, [_P]),

@@ -476,6 +476,13 @@ tg_scorer* tg_scorer_create(tg_family* f, int32_t rank, int32_t k0, int32_t k1, 
 }
 
 void tg_scorer_destroy(tg_scorer* s) { delete s; }
+
+int tg_scorer_set_variant(tg_scorer* s, int32_t variant) {
+    return guard([&] {
+        if (variant < 0 || variant > 2) fail(ErrorKind::Geometry, "scorer variant must be 0 (auto), 1 (register) or 2 (staged)");
+        s->plan->set_variant(variant);
+    });
+}
 uint64_t tg_scorer_bytes(const tg_scorer* s) { return s->plan->bytes_read(); }
 
 int tg_scorer_run(tg_scorer* s, const uint8_t* const* bases, double* d_out, void* stream) {

@@ -382,7 +382,7 @@ void ScorePlan::run(const std::uint8_t* const* snap_bases, double* d_out, cudaSt
     }
     cuda_check(dev::launch_score_partials(d_tiles_.get<dev::ScoreTile>(), static_cast<std::uint32_t>(tiles_.size()),
                                           d_bases_.get<const float*>(), static_cast<std::uint32_t>(fields_.size()), K_,
-                                          vec, d_partials_.get<double>(), s),
+                                          vec, d_partials_.get<double>(), s, variant_),
                "score partials");
     cuda_check(dev::launch_score_combine(d_partials_.get<double>(), d_begin_.get<std::uint32_t>(), M_, K_, d_out, s),
                "score combine");

@@ -19,6 +19,7 @@
 #include <algorithm>
 
 #include "tailor/device.hpp"
+#include "tma.cuh"
 
 namespace tailor::dev {
 
@@ -124,46 +125,7 @@ __global__ void __launch_bounds__(kLsuThreads) gather_lsu_kernel(const GatherSeg
 }
 
 // ---- TMA bulk path -----------------------------------------------------------
-__device__ __forceinline__ std::uint32_t smem_addr(const void* p) {
-    return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(std::uint64_t* bar, std::uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(std::uint64_t* bar, std::uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait_parity(std::uint64_t* bar, std::uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "TG_WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra TG_WAIT_%=;\n"
-        "}\n" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, std::uint32_t bytes, std::uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(smem_dst)),
-        "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, std::uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_addr(smem_src)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+using namespace tma;
 
 __global__ void __launch_bounds__(32, 1) gather_bulk_kernel(const GatherSeg* __restrict__ segs, std::uint32_t nseg,
                                                              std::uint8_t* __restrict__ dst, std::uint64_t dst_bytes) {
@@ -171,8 +133,7 @@ __global__ void __launch_bounds__(32, 1) gather_bulk_kernel(const GatherSeg* __r
     std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kBulkStages * kBulkStage);
     if (threadIdx.x != 0) return; // one thread drives the copy engine
     for (int s = 0; s < kBulkStages; ++s) mbar_init(&bars[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    fence_barrier_init();
 
     const std::uint64_t ntiles = (dst_bytes + kBulkStage - 1) / kBulkStage;
     const std::uint64_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;

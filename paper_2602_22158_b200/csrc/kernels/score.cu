@@ -16,6 +16,7 @@
 #include <algorithm>
 
 #include "tailor/device.hpp"
+#include "tma.cuh"
 
 namespace tailor::dev {
 
@@ -125,6 +126,150 @@ __global__ void score_combine_kernel(const double* __restrict__ partials, const 
     if (lane == 0) out[(static_cast<std::uint64_t>(v / 2) * M + m) * 2 + (v & 1)] = s;
 }
 
+
+// ---- staged variant: TMA bulk copies into a shared-memory ring ------------------
+// For large K the register-staged kernel above needs K float4 per thread in
+// flight (172 registers at K=16 -> 12.5% occupancy, latency-bound). Here one
+// elected thread streams 1024-element chunks of all K snapshots into smem with
+// cp.async.bulk (completion by mbarrier transaction count), S stages deep, and
+// all threads reduce out of smem rolling over k (two float4 live). Loads in
+// flight are set by the ring depth, not by registers. Same tile -> partial
+// contract (one partial per tile, fixed order); summation order inside a tile
+// differs from the register kernel, so the two variants agree to ~1e-15, not
+// bitwise.
+constexpr int kChunkElems = 4 * kScoreThreads; // one float4 per thread per snapshot row
+constexpr int kStagedSmem = 192 * 1024;
+
+template <int K>
+__host__ __device__ constexpr int staged_stages() {
+    constexpr int per = K * kChunkElems * 4;
+    constexpr int s = kStagedSmem / per;
+    return s < 2 ? 2 : (s > 6 ? 6 : s);
+}
+
+template <int K>
+__host__ __device__ constexpr std::size_t staged_smem_bytes() {
+    return static_cast<std::size_t>(staged_stages<K>()) * K * kChunkElems * 4 + 8 * staged_stages<K>();
+}
+
+template <int K>
+__device__ __forceinline__ void accumulate4(double (&acc)[2 * (K - 1)], int p, const float4& a, const float4& b) {
+    const double ax = a.x, ay = a.y, az = a.z, aw = a.w;
+    const double dx = static_cast<double>(b.x) - ax, dy = static_cast<double>(b.y) - ay;
+    const double dz = static_cast<double>(b.z) - az, dw = static_cast<double>(b.w) - aw;
+    acc[2 * p] = fma(dw, dw, fma(dz, dz, fma(dy, dy, fma(dx, dx, acc[2 * p]))));
+    acc[2 * p + 1] = fma(aw, aw, fma(az, az, fma(ay, ay, fma(ax, ax, acc[2 * p + 1]))));
+}
+
+template <int K>
+__global__ void __launch_bounds__(kScoreThreads, 1) score_staged_kernel(const ScoreTile* __restrict__ tiles,
+                                                                         std::uint32_t ntiles,
+                                                                         const float* const* __restrict__ field_base,
+                                                                         std::uint32_t nfields, double* __restrict__ out) {
+    using namespace tma;
+    constexpr int S = staged_stages<K>();
+    constexpr int V = 2 * (K - 1);
+    extern __shared__ __align__(128) float ring[];
+    std::uint64_t* full = reinterpret_cast<std::uint64_t*>(ring + S * K * kChunkElems);
+    __shared__ double red[kWarps][V];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    const std::uint32_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const auto tile_at = [&](std::uint32_t i) { return blockIdx.x + i * gridDim.x; };
+    // producer cursor (thread 0 only)
+    std::uint32_t p_tile = 0, p_chunk = 0;
+    const auto issue = [&](int stage) {
+        while (p_tile < mine) {
+            const ScoreTile t = tiles[tile_at(p_tile)];
+            if (p_chunk * kChunkElems < t.count) {
+                const std::uint32_t start = p_chunk * kChunkElems;
+                const std::uint32_t n = min(static_cast<std::uint32_t>(kChunkElems), t.count - start);
+                const std::uint32_t nb = (n & ~3u) * 4u;
+                mbar_arrive_expect_tx(&full[stage], nb * K);
+                if (nb)
+                    for (int k = 0; k < K; ++k)
+                        bulk_load(ring + (stage * K + k) * kChunkElems, field_base[k * nfields + t.field] + t.elem_start + start,
+                                  nb, &full[stage]);
+                ++p_chunk;
+                return;
+            }
+            ++p_tile;
+            p_chunk = 0;
+        }
+    };
+    if (tid == 0)
+        for (int st = 0; st < S; ++st) issue(st);
+
+    std::uint32_t item = 0;
+    for (std::uint32_t i = 0; i < mine; ++i) {
+        const ScoreTile t = tiles[tile_at(i)];
+        double acc[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[v] = 0.0;
+        const std::uint32_t nchunks = (t.count + kChunkElems - 1) / kChunkElems;
+        for (std::uint32_t c = 0; c < nchunks; ++c, ++item) {
+            const int stage = static_cast<int>(item % S);
+            mbar_wait_parity(&full[stage], (item / S) & 1u);
+            const std::uint32_t start = c * kChunkElems;
+            const std::uint32_t n = min(static_cast<std::uint32_t>(kChunkElems), t.count - start);
+            const std::uint32_t n4 = n & ~3u;
+            const std::uint32_t e = static_cast<std::uint32_t>(tid) * 4u;
+            if (e < n4) {
+                const float* row = ring + stage * K * kChunkElems + e;
+                float4 prev = *reinterpret_cast<const float4*>(row);
+#pragma unroll
+                for (int k = 1; k < K; ++k) {
+                    const float4 cur = *reinterpret_cast<const float4*>(row + k * kChunkElems);
+                    accumulate4<K>(acc, k - 1, prev, cur);
+                    prev = cur;
+                }
+            }
+            if (static_cast<std::uint32_t>(tid) < n - n4) { // ragged tail straight from global
+                float x[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) x[k] = __ldg(field_base[k * nfields + t.field] + t.elem_start + start + n4 + tid);
+                accumulate<K>(acc, x);
+            }
+            __syncthreads(); // every thread is done with this stage
+            if (tid == 0) issue(stage);
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const double sv = warp_sum(acc[v]);
+            if (lane == 0) red[warp][v] = sv;
+        }
+        __syncthreads();
+        if (tid < V) {
+            double sv = 0.0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) sv += red[w][tid];
+            out[static_cast<std::uint64_t>(tile_at(i)) * V + tid] = sv;
+        }
+        __syncthreads();
+    }
+}
+
+template <int K>
+cudaError_t launch_staged(const ScoreTile* d_tiles, std::uint32_t ntiles, const float* const* d_field_base,
+                          std::uint32_t nfields, double* d_out, cudaStream_t stream) {
+    static bool attr = false;
+    constexpr std::size_t smem = staged_smem_bytes<K>();
+    if (!attr) {
+        const cudaError_t e = cudaFuncSetAttribute(score_staged_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ntiles, static_cast<std::uint64_t>(sm_count())));
+    score_staged_kernel<K><<<grid, kScoreThreads, smem, stream>>>(d_tiles, ntiles, d_field_base, nfields, d_out);
+    return cudaGetLastError();
+}
+
 template <int K>
 cudaError_t launch_k(const ScoreTile* d_tiles, std::uint32_t ntiles, const float* const* d_field_base,
                      std::uint32_t nfields, bool vec_ok, double* d_out, cudaStream_t stream) {
@@ -141,12 +286,17 @@ cudaError_t launch_k(const ScoreTile* d_tiles, std::uint32_t ntiles, const float
 } // namespace
 
 cudaError_t launch_score_partials(const ScoreTile* d_tiles, std::uint32_t ntiles, const float* const* d_field_base,
-                                  std::uint32_t nfields, int K, bool vec_ok, double* d_out, cudaStream_t stream) {
+                                  std::uint32_t nfields, int K, bool vec_ok, double* d_out, cudaStream_t stream,
+                                  int variant) {
     if (ntiles == 0) return cudaSuccess;
+    // auto: the bulk-staged kernel wherever its alignment contract holds and K is
+    // large enough that the register kernel loses occupancy.
+    const bool staged = vec_ok && (variant == kScoreStaged || (variant == kScoreAuto && K >= kStagedMinK));
     switch (K) {
-#define TG_K(k)                                                                          \
-    case k:                                                                              \
-        return launch_k<k>(d_tiles, ntiles, d_field_base, nfields, vec_ok, d_out, stream);
+#define TG_K(k)                                                                                     \
+    case k:                                                                                         \
+        return staged ? launch_staged<k>(d_tiles, ntiles, d_field_base, nfields, d_out, stream)     \
+                      : launch_k<k>(d_tiles, ntiles, d_field_base, nfields, vec_ok, d_out, stream);
         TG_K(2) TG_K(3) TG_K(4) TG_K(5) TG_K(6) TG_K(7) TG_K(8) TG_K(9) TG_K(10) TG_K(11) TG_K(12) TG_K(13) TG_K(14)
             TG_K(15) TG_K(16)
 #undef TG_K

@@ -42,8 +42,14 @@ static_assert(sizeof(ScoreTile) == 24, "ScoreTile is part of the C ABI");
 
 // tile_partials[t][p][0|1] = (sum (B-A)^2, sum A^2) over tile t for pair
 // p = (snapshot p, snapshot p+1), FP64. 2 <= K <= 16.
+// variant: 0 auto, 1 register-staged 128-bit loads, 2 TMA-bulk smem ring (needs vec_ok).
+enum ScoreVariant : int { kScoreAuto = 0, kScoreRegister = 1, kScoreStaged = 2 };
+// Measured (profiles/r1_*): the staged ring is barrier-bound with one 8-warp CTA
+// per SM (K=16: 88% vs 90% register; K=4: 61% vs 106%), so auto never picks it.
+constexpr int kStagedMinK = 1 << 20;
 cudaError_t launch_score_partials(const ScoreTile* d_tiles, std::uint32_t ntiles, const float* const* d_field_base,
-                                  std::uint32_t nfields, int K, bool vec_ok, double* d_tile_partials, cudaStream_t stream);
+                                  std::uint32_t nfields, int K, bool vec_ok, double* d_tile_partials, cudaStream_t stream,
+                                  int variant = kScoreAuto);
 // out[p][m][0|1] = fixed-order sum over module m's tiles [tile_begin[m], tile_begin[m+1]).
 cudaError_t launch_score_combine(const double* d_tile_partials, const std::uint32_t* d_module_tile_begin, int M, int K,
                                  double* d_out, cudaStream_t stream);

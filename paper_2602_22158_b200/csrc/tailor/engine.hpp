@@ -130,8 +130,10 @@ class ScorePlan {
     std::uint64_t bytes_read() const { return bytes_; }
     // out: device [K-1][M][2] FP64 (sum delta^2, sum ref^2) for this rank.
     void run(const std::uint8_t* const* snap_bases, double* d_out, cudaStream_t s);
+    void set_variant(int v) { variant_ = v; }
 
   private:
+    int variant_ = dev::kScoreAuto;
     int K_, M_;
     std::vector<ScoreField> fields_;
     std::vector<std::vector<std::uint64_t>> offs_;

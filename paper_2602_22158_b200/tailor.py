@@ -279,6 +279,10 @@ class Scorer:
     def run(self, bases: Sequence[int], d_out: int, stream: int = 0) -> None:
         check(lib().tg_scorer_run(self._h, ptr_array(bases), d_out, stream))
 
+    def set_variant(self, variant: int) -> None:
+        """0 auto, 1 register-staged loads, 2 TMA-bulk shared-memory ring."""
+        check(lib().tg_scorer_set_variant(self._h, variant))
+
 
 class MergePartition:
     """K2 plan for one output partition: container=-1 -> weights share unit/units, r -> rank-r shard."""

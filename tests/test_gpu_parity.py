@@ -409,3 +409,25 @@ def test_select_recipe_matches_reference_scorer(tmp_path):
     assert rec == t.MergeRecipe.from_json(json.dumps(ref["recipe"]))
     assert gap == pytest.approx(ref["min_boundary_gap"], rel=1e-6)
     _both_merge(tmp_path, rec)
+
+
+@pytest.mark.parametrize("K", [2, 4, 7, 16])
+def test_scorer_variants_agree(K):
+    """Register-staged vs TMA-bulk-staged scorer: same tiles, different in-tile order."""
+    need_gpu()
+    spec = t.ModelSpec(2, 40, 100, 333, False, 11)   # ragged chunk counts (tails not multiple of 4)
+    N = 3
+    fam = t.SynthFamily(spec, N, K)
+    M = fam.num_modules
+    for r in range(N):
+        bufs = [dev(fam.packed_master_bytes(r)) for _ in range(K)]
+        fam.gen_masters(r, 1, K, [b.data_ptr() for b in bufs])
+        outs = []
+        for v in (1, 2):
+            sc = t.Scorer(fam, r, 1, K, packed=True)
+            sc.set_variant(v)
+            out = torch.zeros((K - 1) * M * 2, dtype=torch.float64, device="cuda")
+            sc.run([b.data_ptr() for b in bufs], out.data_ptr())
+            outs.append(out)
+        torch.cuda.synchronize()
+        assert torch.allclose(outs[0], outs[1], rtol=1e-12, atol=0)
