@@ -179,9 +179,15 @@ int tg_mplan_prefix(const tg_mplan* p, char* out, size_t cap, size_t* needed); /
 int tg_mplan_bind(tg_mplan* p, const uint8_t* const* window_ptrs);
 int32_t tg_mplan_bulk_ok(const tg_mplan* p);
 int tg_mplan_run(tg_mplan* p, uint8_t* d_dst, int32_t variant, void* stream);
-/* Shard pipeline: host windows -> H2D (needed bytes only) -> K2 -> D2H into h_dst. */
-int tg_mplan_run_host(tg_mplan* p, const uint8_t* const* h_windows, uint8_t* h_dst, int32_t variant,
-                      uint64_t chunk_bytes, uint64_t* h2d_bytes, uint64_t* d2h_bytes);
+/* Shard pipeline: host windows -> H2D (needed bytes only) -> K2 -> D2H into h_dst.
+ * Fields in `resident_fields` (bit0 exp_avg, bit1 exp_avg_sq, bit2 master) are read
+ * from d_windows[w] (device copies of shard windows, e.g. masters staged for
+ * scoring) instead of crossing PCIe again. async=1 returns before completion;
+ * tg_mplan_wait() (or the next run) synchronizes. */
+int tg_mplan_run_host(tg_mplan* p, const uint8_t* const* h_windows, const uint8_t* const* d_windows,
+                      uint32_t resident_fields, uint8_t* h_dst, int32_t variant, uint64_t chunk_bytes, int32_t async,
+                      uint64_t* h2d_bytes, uint64_t* d2h_bytes);
+int tg_mplan_wait(tg_mplan* p);
 
 #ifdef __cplusplus
 }

@@ -133,7 +133,8 @@ SIGNATURES = {
     "tg_mplan_bind": (_I, [_P, _PP]),
     "tg_mplan_bulk_ok": (_I32, [_P]),
     "tg_mplan_run": (_I, [_P, _P, _I32, _P]),
-    "tg_mplan_run_host": (_I, [_P, _PP, _P, _I32, _U64, _c.POINTER(_U64), _c.POINTER(_U64)]),
+    "tg_mplan_run_host": (_I, [_P, _PP, _PP, _U32, _P, _I32, _U64, _I32, _c.POINTER(_U64), _c.POINTER(_U64)]),
+    "tg_mplan_wait": (_I, [_P]),
 }
 
 _lib = None

@@ -31,7 +31,9 @@ struct tg_mplan {
     std::unique_ptr<DeviceMerge> dev;
     std::unique_ptr<HostMerge> host;
     std::uint64_t host_chunk = 0;
+    std::uint32_t host_fields = 0;
     std::vector<int> window_k;
+    std::vector<ContainerLayout> window_layout; // source container of each window
 };
 
 namespace {
@@ -516,7 +518,11 @@ tg_mplan* tg_mplan_create(tg_family* f, const char* yaml, int32_t container, int
             pp = plan_shard(plan, lay_of, container);
         }
         auto* p = new tg_mplan{};
-        for (const auto& w : pp.windows) p->window_k.push_back(fam.index_of(w.source));
+        for (const auto& w : pp.windows) {
+            p->window_k.push_back(fam.index_of(w.source));
+            const SourceLayout& sl = lay_of(w.source);
+            p->window_layout.push_back(w.container < 0 ? sl.weights : sl.shards.at(static_cast<std::size_t>(w.container)));
+        }
         p->dev = std::make_unique<DeviceMerge>(pp);
         out = p;
     });
@@ -568,16 +574,45 @@ int tg_mplan_run(tg_mplan* p, uint8_t* d_dst, int32_t variant, void* stream) {
     return guard([&] { p->dev->run(d_dst, variant, static_cast<cudaStream_t>(stream)); });
 }
 
-int tg_mplan_run_host(tg_mplan* p, const uint8_t* const* h_windows, uint8_t* h_dst, int32_t variant, uint64_t chunk,
+int tg_mplan_run_host(tg_mplan* p, const uint8_t* const* h_windows, const uint8_t* const* d_windows,
+                      uint32_t resident_fields, uint8_t* h_dst, int32_t variant, uint64_t chunk, int32_t async,
                       uint64_t* h2d, uint64_t* d2h) {
     return guard([&] {
-        if (!p->host || p->host_chunk != chunk) {
-            p->host = std::make_unique<HostMerge>(p->dev->plan(), chunk ? chunk : (256ull << 20));
+        const PartitionPlan& pp = p->dev->plan();
+        if (!d_windows) resident_fields = 0;
+        if (!p->host || p->host_chunk != chunk || p->host_fields != resident_fields) {
+            HostMerge::Resident res(pp.windows.size());
+            static const char* kField[3] = {".exp_avg", ".exp_avg_sq", ".master"};
+            for (std::size_t w = 0; w < pp.windows.size(); ++w) {
+                if (pp.windows[w].container < 0) continue; // weights are never resident
+                for (const auto& e : p->window_layout[w].entries)
+                    for (int f = 0; f < 3; ++f) {
+                        if (!(resident_fields & (1u << f))) continue;
+                        const std::string& n = e.name;
+                        const std::string suf = kField[f];
+                        if (n.size() < suf.size() || n.compare(n.size() - suf.size(), suf.size(), suf) != 0) continue;
+                        if (f == 0 && n.size() >= 11 && n.compare(n.size() - 11, 11, ".exp_avg_sq") == 0) continue;
+                        const std::uint64_t a = std::max(e.begin, pp.windows[w].lo), b = std::min(e.end, pp.windows[w].hi);
+                        if (a < b) res[w].push_back({a - pp.windows[w].lo, b - pp.windows[w].lo});
+                    }
+                std::sort(res[w].begin(), res[w].end());
+            }
+            p->host = std::make_unique<HostMerge>(pp, chunk ? chunk : (256ull << 20), std::move(res));
             p->host_chunk = chunk;
+            p->host_fields = resident_fields;
         }
-        p->host->run(std::vector<const std::uint8_t*>(h_windows, h_windows + p->dev->plan().windows.size()), h_dst, variant);
+        std::vector<const std::uint8_t*> dw(pp.windows.size(), nullptr);
+        if (d_windows) dw.assign(d_windows, d_windows + pp.windows.size());
+        p->host->run(std::vector<const std::uint8_t*>(h_windows, h_windows + pp.windows.size()), dw, h_dst, variant,
+                     async != 0);
         if (h2d) *h2d = p->host->h2d_bytes();
         if (d2h) *d2h = p->host->d2h_bytes();
+    });
+}
+
+int tg_mplan_wait(tg_mplan* p) {
+    return guard([&] {
+        if (p->host) p->host->wait();
     });
 }
 

@@ -416,7 +416,9 @@ void DeviceMerge::run(std::uint8_t* d_dst, int variant, cudaStream_t s) {
 }
 
 // ---- host-staged merge (shard pipeline) ------------------------------------------
-HostMerge::HostMerge(const PartitionPlan& plan, std::uint64_t chunk_bytes) : plan_(plan) {
+HostMerge::HostMerge(const PartitionPlan& plan, std::uint64_t chunk_bytes, Resident resident)
+    : plan_(plan), resident_(std::move(resident)) {
+    resident_.resize(plan_.windows.size());
     chunk_bytes = std::max<std::uint64_t>(16, chunk_bytes & ~15ull);
     const std::uint64_t total = plan_.dst_hi - plan_.dst_lo;
     std::size_t si = 0;
@@ -424,49 +426,54 @@ HostMerge::HostMerge(const PartitionPlan& plan, std::uint64_t chunk_bytes) : pla
         Chunk c;
         c.lo = lo;
         c.hi = std::min(total, lo + chunk_bytes);
-        struct P {
-            std::uint32_t w;
-            std::uint64_t src, dst, n;
-        };
-        std::vector<P> ps;
+        std::vector<Piece> ps;
         while (si < plan_.segments.size() && plan_.segments[si].dst_off + plan_.segments[si].bytes - plan_.dst_lo <= c.lo) ++si;
         for (std::size_t j = si; j < plan_.segments.size(); ++j) {
             const auto& s = plan_.segments[j];
             const std::uint64_t d0 = s.dst_off - plan_.dst_lo, d1 = d0 + s.bytes;
             if (d0 >= c.hi) break;
-            const std::uint64_t a = std::max(d0, c.lo), b = std::min(d1, c.hi);
-            if (a < b) ps.push_back({s.window, s.src_off + (a - d0), a, b - a});
+            std::uint64_t a = std::max(d0, c.lo);
+            const std::uint64_t b = std::min(d1, c.hi);
+            // split at device-resident source ranges: those bytes never cross PCIe
+            while (a < b) {
+                const std::uint64_t src = s.src_off + (a - d0);
+                std::uint64_t n = b - a;
+                bool dev_side = false;
+                for (const auto& [r0, r1] : resident_[s.window]) {
+                    if (src >= r0 && src < r1) {
+                        dev_side = true;
+                        n = std::min(n, r1 - src);
+                        break;
+                    }
+                    if (r0 > src) n = std::min(n, r0 - src);
+                }
+                ps.push_back({s.window, src, a, n, dev_side});
+                a += n;
+            }
         }
-        // Stage in source order per window, coalescing contiguous source bytes.
-        std::vector<std::size_t> order(ps.size());
-        for (std::size_t i = 0; i < ps.size(); ++i) order[i] = i;
+        // Stage host pieces in source order per window, coalescing contiguous bytes.
+        std::vector<std::size_t> order;
+        for (std::size_t i = 0; i < ps.size(); ++i)
+            if (!ps[i].dev) order.push_back(i);
         std::sort(order.begin(), order.end(), [&](std::size_t x, std::size_t y) {
             return ps[x].w != ps[y].w ? ps[x].w < ps[y].w : ps[x].src < ps[y].src;
         });
-        std::vector<std::uint64_t> stage_of(ps.size());
         std::uint64_t at = 0;
-        for (std::size_t oi = 0; oi < order.size(); ++oi) {
-            const P& p = ps[order[oi]];
-            if (!c.reads.empty() && c.reads.back().first == p.w && c.reads.back().second.second == p.src) {
-                stage_of[order[oi]] = c.read_at.back() + (p.src - c.reads.back().second.first);
-                c.reads.back().second.second = p.src + p.n;
-                at = c.read_at.back() + (c.reads.back().second.second - c.reads.back().second.first);
+        for (std::size_t i : order) {
+            Piece& p = ps[i];
+            if (!c.reads.empty() && c.reads.back().w == p.w && c.reads.back().b == p.src) {
+                p.stage = c.reads.back().at + (p.src - c.reads.back().a);
+                c.reads.back().b += p.n;
+                at = c.reads.back().at + (c.reads.back().b - c.reads.back().a);
                 continue;
             }
-            at = align16(at);
-            c.reads.push_back({p.w, {p.src, p.src + p.n}});
-            c.read_at.push_back(at);
-            stage_of[order[oi]] = at;
+            at = align16(at) + ((p.dst - c.lo) & 15); // keep src == dst (mod 16)
+            c.reads.push_back({p.w, p.src, p.src + p.n, at});
+            p.stage = at;
             at += p.n;
         }
         c.staging = align16(at);
-        std::uint64_t expect = c.lo;
-        for (std::size_t i = 0; i < ps.size(); ++i) {
-            c.segs.push_back({reinterpret_cast<const std::uint8_t*>(stage_of[i]), ps[i].dst - c.lo, ps[i].n});
-            c.bulk_ok = c.bulk_ok && ps[i].dst == expect && stage_of[i] % 16 == 0 && ps[i].n % 16 == 0 && (ps[i].dst - c.lo) % 16 == 0;
-            expect = ps[i].dst + ps[i].n;
-        }
-        c.bulk_ok = c.bulk_ok && expect == c.hi;
+        c.pieces = std::move(ps);
         max_staging_ = std::max(max_staging_, c.staging);
         max_out_ = std::max(max_out_, c.hi - c.lo);
         chunks_.push_back(std::move(c));
@@ -475,45 +482,68 @@ HostMerge::HostMerge(const PartitionPlan& plan, std::uint64_t chunk_bytes) : pla
 
 HostMerge::~HostMerge() {
     for (auto& s : stream_)
-        if (s) cudaStreamDestroy(s);
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
 }
 
-void HostMerge::run(const std::vector<const std::uint8_t*>& h_windows, std::uint8_t* h_dst, int variant) {
+void HostMerge::wait() {
+    for (auto& s : stream_)
+        if (s) cuda_check(cudaStreamSynchronize(s), "sync");
+}
+
+void HostMerge::run(const std::vector<const std::uint8_t*>& h_windows, const std::vector<const std::uint8_t*>& d_windows,
+                    std::uint8_t* h_dst, int variant, bool async) {
     if (h_windows.size() != plan_.windows.size()) fail(ErrorKind::Geometry, "window pointer count mismatch");
+    wait(); // a previous asynchronous run still owns the staging buffers
     std::size_t max_segs = 1;
-    for (const auto& c : chunks_) max_segs = std::max(max_segs, c.segs.size());
+    for (const auto& c : chunks_) max_segs = std::max(max_segs, c.pieces.size());
     for (int i = 0; i < 2; ++i) {
         if (!stream_[i]) cuda_check(cudaStreamCreateWithFlags(&stream_[i], cudaStreamNonBlocking), "stream");
         stage_[i].resize(std::max<std::uint64_t>(16, max_staging_));
         out_[i].resize(std::max<std::uint64_t>(16, max_out_));
         segs_[i].resize(max_segs * sizeof(dev::GatherSeg));
     }
-    std::vector<std::vector<dev::GatherSeg>> patched(chunks_.size());
+    patched_.assign(chunks_.size(), {});
     h2d_ = d2h_ = 0;
     for (std::size_t ci = 0; ci < chunks_.size(); ++ci) {
         const Chunk& c = chunks_[ci];
         const int slot = static_cast<int>(ci & 1);
         cudaStream_t s = stream_[slot];
-        for (std::size_t r = 0; r < c.reads.size(); ++r) {
-            const auto& rd = c.reads[r];
-            const std::uint64_t n = rd.second.second - rd.second.first;
-            cuda_check(cudaMemcpyAsync(stage_[slot].get() + c.read_at[r], h_windows[rd.first] + rd.second.first, n,
+        for (const auto& rd : c.reads) {
+            cuda_check(cudaMemcpyAsync(stage_[slot].get() + rd.at, h_windows[rd.w] + rd.a, rd.b - rd.a,
                                        cudaMemcpyHostToDevice, s),
                        "H2D");
-            h2d_ += n;
+            h2d_ += rd.b - rd.a;
         }
-        patched[ci] = c.segs;
-        for (auto& g : patched[ci]) g.src = stage_[slot].get() + reinterpret_cast<std::uintptr_t>(g.src);
-        cuda_check(cudaMemcpyAsync(segs_[slot].get(), patched[ci].data(), patched[ci].size() * sizeof(dev::GatherSeg),
+        auto& segs = patched_[ci];
+        bool bulk = true;
+        std::uint64_t expect = c.lo;
+        for (const auto& p : c.pieces) {
+            const std::uint8_t* src;
+            if (p.dev) {
+                if (d_windows.size() <= p.w || !d_windows[p.w]) fail(ErrorKind::Geometry, "resident window without a device pointer");
+                src = d_windows[p.w] + p.src;
+            } else {
+                src = stage_[slot].get() + p.stage;
+            }
+            segs.push_back({src, p.dst - c.lo, p.n});
+            bulk = bulk && p.dst == expect && reinterpret_cast<std::uintptr_t>(src) % 16 == 0 && p.n % 16 == 0 &&
+                   (p.dst - c.lo) % 16 == 0;
+            expect = p.dst + p.n;
+        }
+        bulk = bulk && expect == c.hi;
+        cuda_check(cudaMemcpyAsync(segs_[slot].get(), segs.data(), segs.size() * sizeof(dev::GatherSeg),
                                    cudaMemcpyHostToDevice, s),
                    "segs");
-        cuda_check(dev::launch_gather(segs_[slot].get<dev::GatherSeg>(), static_cast<std::uint32_t>(patched[ci].size()),
-                                      out_[slot].get(), c.hi - c.lo, variant, c.bulk_ok, s),
+        cuda_check(dev::launch_gather(segs_[slot].get<dev::GatherSeg>(), static_cast<std::uint32_t>(segs.size()),
+                                      out_[slot].get(), c.hi - c.lo, variant, bulk, s),
                    "gather");
         cuda_check(cudaMemcpyAsync(h_dst + c.lo, out_[slot].get(), c.hi - c.lo, cudaMemcpyDeviceToHost, s), "D2H");
         d2h_ += c.hi - c.lo;
     }
-    for (auto& s : stream_) cuda_check(cudaStreamSynchronize(s), "sync");
+    if (!async) wait();
 }
 
 // ---- device re-verify --------------------------------------------------------------

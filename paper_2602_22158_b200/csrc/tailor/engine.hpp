@@ -166,30 +166,47 @@ class DeviceMerge {
 
 // Pipelined host->device->host assembly of one partition from host (pinned)
 // source windows into a host destination: per chunk, only the bytes the
-// chunk needs are copied in, gathered on the device and copied out.
+// chunk needs are copied in, gathered on the device and copied out, on two
+// streams so H2D, the gather and D2H of consecutive chunks overlap. Source
+// byte ranges listed as `resident` (window-relative) are read straight from
+// device copies instead (e.g. masters already staged for scoring).
 class HostMerge {
   public:
-    explicit HostMerge(const PartitionPlan& plan, std::uint64_t chunk_bytes = 256ull << 20);
+    using Resident = std::vector<std::vector<std::pair<std::uint64_t, std::uint64_t>>>;
+    explicit HostMerge(const PartitionPlan& plan, std::uint64_t chunk_bytes = 256ull << 20, Resident resident = {});
     ~HostMerge();
-    // h_windows[w] = host address of window w's first byte; h_dst = output byte dst_lo.
-    void run(const std::vector<const std::uint8_t*>& h_windows, std::uint8_t* h_dst, int variant);
+    // h_windows[w] = host address of window w's first byte; d_windows[w] = device
+    // address (only needed for windows with resident ranges); h_dst = output byte dst_lo.
+    void run(const std::vector<const std::uint8_t*>& h_windows, const std::vector<const std::uint8_t*>& d_windows,
+             std::uint8_t* h_dst, int variant, bool async = false);
+    void wait();
     std::uint64_t h2d_bytes() const { return h2d_; }
     std::uint64_t d2h_bytes() const { return d2h_; }
 
   private:
+    struct Piece {
+        std::uint32_t w;
+        std::uint64_t src, dst, n;
+        bool dev;
+        std::uint64_t stage = 0;
+    };
+    struct Read {
+        std::uint32_t w;
+        std::uint64_t a, b, at;
+    };
     struct Chunk {
-        std::uint64_t lo, hi;                  // output range (relative to dst_lo)
-        std::vector<dev::GatherSeg> segs;      // src = staging offset (patched at run)
-        std::vector<std::pair<std::uint32_t, std::pair<std::uint64_t, std::uint64_t>>> reads; // window, [a,b) -> staging at offset
-        std::vector<std::uint64_t> read_at;
+        std::uint64_t lo, hi; // output range (relative to dst_lo)
+        std::vector<Piece> pieces;
+        std::vector<Read> reads;
         std::uint64_t staging = 0;
-        bool bulk_ok = true;
     };
     PartitionPlan plan_;
+    Resident resident_;
     std::vector<Chunk> chunks_;
     std::uint64_t max_staging_ = 0, max_out_ = 0;
     DeviceBuffer stage_[2], out_[2], segs_[2];
     cudaStream_t stream_[2]{};
+    std::vector<std::vector<dev::GatherSeg>> patched_;
     std::uint64_t h2d_ = 0, d2h_ = 0;
 };
 

@@ -336,8 +336,15 @@ class MergePartition:
     def run(self, d_dst: int, variant: int = 0, stream: int = 0) -> None:
         check(lib().tg_mplan_run(self._h, d_dst, variant, stream))
 
-    def run_host(self, h_windows: Sequence[int], h_dst: int, variant: int = 0, chunk_bytes: int = 0):
+    def run_host(self, h_windows: Sequence[int], h_dst: int, variant: int = 0, chunk_bytes: int = 0,
+                 d_windows: Optional[Sequence[int]] = None, resident_fields: int = 0, async_: bool = False):
+        """Shard pipeline from pinned host windows; `resident_fields` (1 exp_avg, 2 exp_avg_sq,
+        4 master) are read from `d_windows` instead of crossing PCIe."""
         h2d, d2h = ctypes.c_uint64(), ctypes.c_uint64()
-        check(lib().tg_mplan_run_host(self._h, ptr_array(h_windows), h_dst, variant, chunk_bytes,
-                                      ctypes.byref(h2d), ctypes.byref(d2h)))
+        dw = ptr_array(d_windows) if d_windows is not None else None
+        check(lib().tg_mplan_run_host(self._h, ptr_array(h_windows), dw, resident_fields if dw else 0, h_dst, variant,
+                                      chunk_bytes, 1 if async_ else 0, ctypes.byref(h2d), ctypes.byref(d2h)))
         return h2d.value, d2h.value
+
+    def wait(self) -> None:
+        check(lib().tg_mplan_wait(self._h))

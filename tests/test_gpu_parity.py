@@ -230,6 +230,15 @@ def test_host_pipeline_matches_device():
         torch.cuda.synchronize()
         assert bytes(hdst.numpy()) == host_bytes(out, mp.bytes)
         assert h2d == mp.bytes and d2h == mp.bytes  # only the needed bytes cross PCIe
+        # masters (and then m/v too) read from device copies: fewer H2D bytes, same result
+        for fields, frac in ((4, 3), (7, 0)):
+            hdst2 = torch.zeros(mp.bytes, dtype=torch.uint8).pin_memory()
+            h2d2, _ = mp.run_host([hsrc[k - 1].data_ptr() + lo for k, c, lo, hi in mp.windows()], hdst2.data_ptr(),
+                                  chunk_bytes=1 << 14, d_windows=[bufs[k - 1].data_ptr() + lo for k, c, lo, hi in mp.windows()],
+                                  resident_fields=fields, async_=True)
+            mp.wait()
+            assert bytes(hdst2.numpy()) == host_bytes(out, mp.bytes)
+            assert h2d2 == mp.bytes * frac // 3 or (fields == 4 and 0 < h2d2 < mp.bytes)
 
 
 @pytest.mark.parametrize("seed", range(4))
