@@ -389,11 +389,24 @@ def e2e_run(args, t, torch, fam, scorer, shards, wbufs, wlo, yaml, r, N, world, 
     scoring overlap unit i's merge (two staging sets)."""
     import torch.distributed as dist
 
+    need = sum(b.numel() for b in shards) + sum(b.numel() for b in wbufs) + 2 * shards[0].numel() + (2 << 30)
+    local = env_int("LOCAL_WORLD_SIZE", world)
     try:
-        hshards = [b.cpu().pin_memory() for b in shards]
-        hw = [b.cpu().pin_memory() for b in wbufs]
-    except RuntimeError as exc:  # host memory
-        return {"value": None, "unit": "GB/s", "error": f"pinned host staging failed: {exc}"}
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    fits = need * local <= 0.85 * avail
+    if world > 1:  # every rank must take the same branch (collectives follow)
+        flag = torch.tensor([1 if fits else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        fits = bool(flag.item())
+    if not fits:
+        return {"value": None, "unit": "GB/s",
+                "skipped": f"host RAM: {local} ranks x {need / 1e9:.0f} GB pinned > 85% of {avail / 1e9:.0f} GB available"}
+    hshards = [b.cpu().pin_memory() for b in shards]
+    hw = [b.cpu().pin_memory() for b in wbufs]
     # staging set 0 = the resident source buffers (the device-only measurement is done),
     # staging set 1 = fresh buffers of the same layout
     stage = [shards, [torch.empty(b.numel(), dtype=torch.uint8, device=dev) for b in shards]]
