@@ -611,8 +611,11 @@ def files_arm(args):
             out = work / f"ours-{i}"
             t0 = time.perf_counter()
             rec, _, gap = t.select_recipe(dirs, rho)
+            t1 = time.perf_counter()
             st = t.execute_merge(rec, str(out), t.MergeOptions(workers=cores))
             dt = time.perf_counter() - t0
+            phases = {"select_ms": round((t1 - t0) * 1e3, 1), "merge_ms": round(st.wall_ms, 1),
+                      "gather_device_ms": round(st.device_ms, 2)}
             comp = st.bytes_moved
             shutil.rmtree(out, ignore_errors=True)
             if i >= args.warmup:
@@ -638,7 +641,7 @@ def files_arm(args):
         "vs_baseline": None, "dtype": "u8/f32/f64", "data": "synthetic (written by the GPU writer, byte-identical "
                                                           "to the reference writer), page cache warm",
         "config": {"workload": "files", "shape": f"L{L} h{h} f{f} v{v} N{N} K{K} rho{rho}",
-                   "composite_bytes": comp, "min_boundary_gap": gap},
+                   "composite_bytes": comp, "min_boundary_gap": gap, "last_step_phases": phases},
         "reference": {"value": round(r_v, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
                       "ms_per_step": round(statistics.median(refs) * 1e3, 1)},
         "speedup_vs_reference": round(o_v / r_v, 2)}))

@@ -15,6 +15,7 @@
 
 #include "tailor/engine.hpp"
 #include "tailor/errors.hpp"
+#include "tailor/io.hpp"
 #include "tailor/merge.hpp"
 
 using nlohmann::json;
@@ -148,17 +149,13 @@ void load_packed_masters(const std::vector<std::string>& dirs, int rank, const M
         stage.resize(std::max<std::uint64_t>(16, total));
         const int fd = ::open(p.c_str(), O_RDONLY);
         if (fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + p.string() + "'");
-        for (const auto& [e, at] : where) {
-            std::uint64_t got = 0;
-            while (got < e->bytes()) {
-                const ssize_t r = ::pread(fd, stage.get() + at + got, e->bytes() - got,
-                                          static_cast<off_t>(lay.payload_offset() + e->begin + got));
-                if (r <= 0) {
-                    ::close(fd);
-                    fail(ErrorKind::Storage, "read failed for '" + p.string() + "'");
-                }
-                got += static_cast<std::uint64_t>(r);
-            }
+        std::vector<ReadJob> jobs;
+        for (const auto& [e, at] : where) jobs.push_back({fd, stage.get() + at, e->bytes(), lay.payload_offset() + e->begin});
+        try {
+            run_reads(jobs, io_threads(), p.string());
+        } catch (...) {
+            ::close(fd);
+            throw;
         }
         ::close(fd);
         out[k].resize(std::max<std::uint64_t>(16, total));

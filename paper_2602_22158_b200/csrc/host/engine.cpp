@@ -11,6 +11,7 @@
 #include <unistd.h>
 
 #include "tailor/errors.hpp"
+#include "tailor/io.hpp"
 
 namespace tailor {
 
@@ -553,21 +554,39 @@ void load_payload(const fs::path& path, const ContainerLayout& lay, DeviceBuffer
     dst.resize(std::max<std::uint64_t>(16, lay.payload_bytes));
     const int fd = ::open(path.c_str(), O_RDONLY);
     if (fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + path.string() + "'");
-    const std::uint64_t step = 64ull << 20;
-    stage.resize(step);
-    for (std::uint64_t off = 0; off < lay.payload_bytes; off += step) {
-        const std::uint64_t n = std::min(step, lay.payload_bytes - off);
-        std::uint64_t got = 0;
-        while (got < n) {
-            const ssize_t r = ::pread(fd, stage.get() + got, n - got, static_cast<off_t>(lay.payload_offset() + off + got));
-            if (r <= 0) {
-                ::close(fd);
-                fail(ErrorKind::Storage, "read failed for '" + path.string() + "'");
-            }
-            got += static_cast<std::uint64_t>(r);
+    // 512 MB windows read by the I/O pool, alternating two halves of the pinned
+    // stage so the H2D of one overlaps the reads of the next.
+    const std::uint64_t step = 512ull << 20;
+    stage.resize(2 * step);
+    cudaStream_t s = nullptr;
+    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    cudaEvent_t done[2];
+    cuda_check(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming), "event");
+    bool used[2] = {false, false};
+    try {
+        int half = 0;
+        for (std::uint64_t off = 0; off < lay.payload_bytes; off += step, half ^= 1) {
+            const std::uint64_t n = std::min(step, lay.payload_bytes - off);
+            std::uint8_t* buf = stage.get() + static_cast<std::uint64_t>(half) * step;
+            if (used[half]) cuda_check(cudaEventSynchronize(done[half]), "event");
+            run_reads({{fd, buf, n, lay.payload_offset() + off}}, io_threads(), path.string());
+            cuda_check(cudaMemcpyAsync(dst.get() + off, buf, n, cudaMemcpyHostToDevice, s), "H2D");
+            cuda_check(cudaEventRecord(done[half], s), "event");
+            used[half] = true;
         }
-        cuda_check(cudaMemcpy(dst.get() + off, stage.get(), n, cudaMemcpyHostToDevice), "H2D");
+        cuda_check(cudaStreamSynchronize(s), "sync");
+    } catch (...) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+        cudaEventDestroy(done[0]);
+        cudaEventDestroy(done[1]);
+        ::close(fd);
+        throw;
     }
+    cudaStreamDestroy(s);
+    cudaEventDestroy(done[0]);
+    cudaEventDestroy(done[1]);
     ::close(fd);
 }
 

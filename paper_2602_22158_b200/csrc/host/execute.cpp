@@ -19,6 +19,7 @@
 
 #include "tailor/engine.hpp"
 #include "tailor/errors.hpp"
+#include "tailor/io.hpp"
 
 namespace tailor {
 
@@ -33,15 +34,6 @@ struct Fd {
         if (fd >= 0) ::close(fd);
     }
 };
-
-void pread_all(int fd, std::uint8_t* dst, std::uint64_t n, std::uint64_t off, const std::string& what) {
-    std::uint64_t got = 0;
-    while (got < n) {
-        const ssize_t r = ::pread(fd, dst + got, n - got, static_cast<off_t>(off + got));
-        if (r <= 0) fail(ErrorKind::Storage, "read failed for '" + what + "'");
-        got += static_cast<std::uint64_t>(r);
-    }
-}
 
 void pwrite_all(int fd, const std::uint8_t* src, std::uint64_t n, std::uint64_t off, const std::string& what) {
     std::uint64_t put = 0;
@@ -59,13 +51,17 @@ class FileAssembler {
   public:
     FileAssembler(int workers, bool uncached) : workers_(std::max(1, workers)), uncached_(uncached) {
         for (auto& s : stream_) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-        cuda_check(cudaEventCreate(&ev0_), "event");
-        cuda_check(cudaEventCreate(&ev1_), "event");
+        for (int i = 0; i < 2; ++i) {
+            cuda_check(cudaEventCreate(&ev0_[i]), "event");
+            cuda_check(cudaEventCreate(&ev1_[i]), "event");
+        }
     }
     ~FileAssembler() {
         for (auto& s : stream_) cudaStreamDestroy(s);
-        cudaEventDestroy(ev0_);
-        cudaEventDestroy(ev1_);
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(ev0_[i]);
+            cudaEventDestroy(ev1_[i]);
+        }
     }
 
     double device_ms = 0.0;
@@ -101,6 +97,9 @@ class FileAssembler {
         const auto flush = [&](int slot) {
             if (pending[slot] < 0) return;
             cuda_check(cudaStreamSynchronize(stream_[slot]), "sync");
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev0_[slot], ev1_[slot]);
+            device_ms += ms;
             const auto& c = plan.chunks[static_cast<std::size_t>(pending[slot])];
             pwrite_all(out.fd, pin_out_[slot].get(), c.hi - c.lo, base + c.lo, out_path.string());
             pending[slot] = -1;
@@ -109,39 +108,23 @@ class FileAssembler {
             const int slot = static_cast<int>(ci & 1);
             flush(slot);
             const auto& c = plan.chunks[ci];
-            // Parallel reads of this chunk's source ranges into pinned staging.
-            const auto read_one = [&](std::size_t r) {
-                const auto& rd = c.reads[r];
-                const std::uint64_t n = rd.b - rd.a;
+            // This chunk's source ranges -> pinned staging, via the parallel pread pool
+            // (uncached mode re-opens the source file per read, as the reference
+            // reloads a shard per group copy).
+            std::vector<std::unique_ptr<Fd>> opened;
+            std::vector<ReadJob> jobs;
+            for (const auto& rd : c.reads) {
+                int fd;
                 if (uncached_) {
-                    Fd f(window_files[rd.w], O_RDONLY);
-                    if (f.fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + window_files[rd.w].string() + "'");
-                    pread_all(f.fd, pin_in_[slot].get() + rd.at, n, file_off[rd.w] + rd.a, window_files[rd.w].string());
+                    opened.push_back(std::make_unique<Fd>(window_files[rd.w], O_RDONLY));
+                    if (opened.back()->fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + window_files[rd.w].string() + "'");
+                    fd = opened.back()->fd;
                 } else {
-                    pread_all(fds[rd.w]->fd, pin_in_[slot].get() + rd.at, n, file_off[rd.w] + rd.a, window_files[rd.w].string());
+                    fd = fds[rd.w]->fd;
                 }
-            };
-            if (workers_ > 1 && c.reads.size() > 1) {
-                std::vector<std::thread> pool;
-                std::exception_ptr err;
-                std::mutex mu;
-                const std::size_t nt = std::min<std::size_t>(static_cast<std::size_t>(workers_), c.reads.size());
-                for (std::size_t t = 0; t < nt; ++t)
-                    pool.emplace_back([&, t] {
-                        for (std::size_t r = t; r < c.reads.size(); r += nt) {
-                            try {
-                                read_one(r);
-                            } catch (...) {
-                                std::lock_guard<std::mutex> lk(mu);
-                                if (!err) err = std::current_exception();
-                            }
-                        }
-                    });
-                for (auto& th : pool) th.join();
-                if (err) std::rethrow_exception(err);
-            } else {
-                for (std::size_t r = 0; r < c.reads.size(); ++r) read_one(r);
+                jobs.push_back({fd, pin_in_[slot].get() + rd.at, rd.b - rd.a, file_off[rd.w] + rd.a});
             }
+            run_reads(jobs, workers_, out_path.string());
             cudaStream_t s = stream_[slot];
             cuda_check(cudaMemcpyAsync(d_in_[slot].get(), pin_in_[slot].get(), c.staging, cudaMemcpyHostToDevice, s), "H2D");
             patched[ci] = c.segs;
@@ -149,15 +132,11 @@ class FileAssembler {
             cuda_check(cudaMemcpyAsync(d_segs_[slot].get(), patched[ci].data(), patched[ci].size() * sizeof(dev::GatherSeg),
                                        cudaMemcpyHostToDevice, s),
                        "segs");
-            cuda_check(cudaEventRecord(ev0_, s), "event");
+            cuda_check(cudaEventRecord(ev0_[slot], s), "event");
             cuda_check(dev::launch_gather(d_segs_[slot].get<dev::GatherSeg>(), static_cast<std::uint32_t>(patched[ci].size()),
                                           d_out_[slot].get(), c.hi - c.lo, dev::kGatherAuto, c.bulk_ok, s),
                        "gather");
-            cuda_check(cudaEventRecord(ev1_, s), "event");
-            cuda_check(cudaEventSynchronize(ev1_), "event sync");
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, ev0_, ev1_);
-            device_ms += ms;
+            cuda_check(cudaEventRecord(ev1_[slot], s), "event");
             cuda_check(cudaMemcpyAsync(pin_out_[slot].get(), d_out_[slot].get(), c.hi - c.lo, cudaMemcpyDeviceToHost, s), "D2H");
             pending[slot] = static_cast<int>(ci);
             bytes += c.hi - c.lo;
@@ -251,7 +230,7 @@ class FileAssembler {
     int workers_;
     bool uncached_;
     cudaStream_t stream_[2]{};
-    cudaEvent_t ev0_{}, ev1_{};
+    cudaEvent_t ev0_[2]{}, ev1_[2]{};
     PinnedBuffer pin_in_[2], pin_out_[2];
     DeviceBuffer d_in_[2], d_out_[2], d_segs_[2];
     std::map<std::string, std::uint64_t> payload_off_;
@@ -301,7 +280,7 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
     // All inputs validated; write.
     fs::create_directories(out_dir / "optim", ec);
     if (ec) fail(ErrorKind::Storage, "cannot create '" + out_dir.string() + "': " + ec.message());
-    const int workers = options.workers > 0 ? options.workers : plan.num_ranks;
+    const int workers = options.workers > 0 ? options.workers : std::max(plan.num_ranks, io_threads());
     FileAssembler fa(workers, options.uncached);
     {
         std::vector<fs::path> files;
