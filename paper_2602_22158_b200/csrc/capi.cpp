@@ -188,6 +188,7 @@ void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<st
     for (int r = 0; r < N; ++r) {
         std::vector<DeviceBuffer> bufs;
         std::vector<std::vector<std::uint64_t>> offs;
+        PhaseTimer pt("score.rank");
         load_packed_masters(dirs, r, model, N, bufs, offs);
         ScorePlan plan(model, N, offs);
         std::vector<const std::uint8_t*> bases;

@@ -8,6 +8,8 @@
 #include <fcntl.h>
 #include <filesystem>
 #include <fstream>
+#include <map>
+#include <mutex>
 #include <unistd.h>
 
 #include "tailor/errors.hpp"
@@ -42,18 +44,63 @@ void DeviceBuffer::upload(const void* src, std::size_t n, cudaStream_t s) {
     else cuda_check(cudaMemcpy(p_, src, n, cudaMemcpyHostToDevice), "upload");
 }
 
+// Pinning pages costs ~0.4 s per GB, far more than the reads the staging
+// buffers serve, so released pinned buffers are kept in a process-wide pool
+// (bounded) and reused by later calls.
+namespace {
+struct PinnedPool {
+    static constexpr std::size_t kCap = 8ull << 30;
+    std::mutex mu;
+    std::multimap<std::size_t, void*> free_; // size -> block
+    std::size_t pooled = 0;
+
+    void* take(std::size_t n, std::size_t* got) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            auto it = free_.lower_bound(n);
+            if (it != free_.end() && it->first <= 4 * n + (64u << 20)) {
+                void* p = it->second;
+                *got = it->first;
+                pooled -= it->first;
+                free_.erase(it);
+                return p;
+            }
+        }
+        const std::size_t sz = (n + (2u << 20) - 1) & ~((2ull << 20) - 1); // 2 MB granules
+        void* p = nullptr;
+        cuda_check(cudaMallocHost(&p, sz), "cudaMallocHost");
+        *got = sz;
+        return p;
+    }
+    void give(void* p, std::size_t n) {
+        std::lock_guard<std::mutex> lk(mu);
+        free_.emplace(n, p);
+        pooled += n;
+        while (pooled > kCap && !free_.empty()) { // drop the largest blocks first
+            auto it = std::prev(free_.end());
+            pooled -= it->first;
+            cudaFreeHost(it->second);
+            free_.erase(it);
+        }
+    }
+};
+PinnedPool& pinned_pool() {
+    static PinnedPool* pool = new PinnedPool(); // intentionally leaked: lives for the process
+    return *pool;
+}
+} // namespace
+
 PinnedBuffer::~PinnedBuffer() {
-    if (p_) cudaFreeHost(p_);
+    if (p_) pinned_pool().give(p_, n_);
 }
 
 void PinnedBuffer::resize(std::size_t n) {
     if (n <= n_ && p_) return;
-    if (p_) cudaFreeHost(p_);
+    if (p_) pinned_pool().give(p_, n_);
     p_ = nullptr;
     n_ = 0;
     if (n == 0) return;
-    cuda_check(cudaMallocHost(&p_, n), "cudaMallocHost");
-    n_ = n;
+    p_ = pinned_pool().take(n, &n_);
 }
 
 // ---- synthetic family ---------------------------------------------------------
@@ -620,7 +667,10 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
 
     DeviceBuffer dw, ds, dpairs, dranges, derr(3 * sizeof(unsigned long long));
     PinnedBuffer stage;
-    load_payload(weights_path(dir), wl, dw, stage);
+    {
+        PhaseTimer pt("verify.load_weights");
+        load_payload(weights_path(dir), wl, dw, stage);
+    }
     unsigned long long err[3] = {0, 0, 0};
     cuda_check(cudaMemset(derr.get(), 0, sizeof(err)), "memset");
     for (int r = 0; r < s.optim.num_ranks; ++r) {

@@ -246,6 +246,7 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
         fail(ErrorKind::Storage, "refusing to write into non-empty directory '" + out_dir.string() + "'");
     cuda_check(cudaSetDevice(options.device), "cudaSetDevice");
 
+    auto phase = std::make_unique<PhaseTimer>("merge.headers+plan");
     std::map<std::string, CheckpointSummary> sums;
     for (const auto& p : plan.sources) sums.emplace(p, read_checkpoint_summary(p));
     if (!sums.count(plan.config_source)) sums.emplace(plan.config_source, read_checkpoint_summary(plan.config_source));
@@ -281,6 +282,7 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
     fs::create_directories(out_dir / "optim", ec);
     if (ec) fail(ErrorKind::Storage, "cannot create '" + out_dir.string() + "': " + ec.message());
     const int workers = options.workers > 0 ? options.workers : std::max(plan.num_ranks, io_threads());
+    phase = std::make_unique<PhaseTimer>("merge.assemble");
     FileAssembler fa(workers, options.uncached);
     {
         std::vector<fs::path> files;
@@ -297,7 +299,9 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
     write_text_file(trainer_state_path(out_dir), read_text_file(trainer_state_path(plan.config_source)));
     write_text_file(manifest_path(out_dir), render_manifest_json(manifest));
 
+    phase = std::make_unique<PhaseTimer>("merge.verify");
     if (options.verify) verify_checkpoint_dir(out_dir.string(), options.device);
+    phase.reset();
 
     stats.device_ms = fa.device_ms;
     stats.bytes_moved = fa.bytes;

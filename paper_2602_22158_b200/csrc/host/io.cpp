@@ -3,6 +3,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <exception>
 #include <mutex>
 #include <thread>
@@ -11,6 +14,27 @@
 #include "tailor/errors.hpp"
 
 namespace tailor {
+
+namespace {
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+bool trace_on() {
+    static const bool on = [] {
+        const char* v = std::getenv("TAILOR_TRACE");
+        return v && *v && *v != '0';
+    }();
+    return on;
+}
+} // namespace
+
+PhaseTimer::PhaseTimer(const char* name) : name_(name), on_(trace_on()) {
+    if (on_) t0_ = now_ms();
+}
+
+PhaseTimer::~PhaseTimer() {
+    if (on_) std::fprintf(stderr, "[tailor] %s %.2f ms\n", name_, now_ms() - t0_);
+}
 
 int io_threads() {
     const unsigned hw = std::thread::hardware_concurrency();

@@ -23,4 +23,19 @@ void run_reads(const std::vector<ReadJob>& jobs, int threads, const std::string&
 // Default worker count for host I/O: hardware threads, capped at 16.
 int io_threads();
 
+// Phase timer for the file-facing paths: prints "[tailor] <name> <ms>" to
+// stderr at scope exit when TAILOR_TRACE=1 (no cost otherwise).
+class PhaseTimer {
+  public:
+    explicit PhaseTimer(const char* name);
+    ~PhaseTimer();
+    PhaseTimer(const PhaseTimer&) = delete;
+    PhaseTimer& operator=(const PhaseTimer&) = delete;
+
+  private:
+    const char* name_;
+    double t0_ = 0.0;
+    bool on_;
+};
+
 } // namespace tailor

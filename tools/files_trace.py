@@ -1,0 +1,32 @@
+#!/usr/bin/env python
+"""Phase trace of the file-facing drop-in path (TAILOR_TRACE=1): medium shape
+L8 h1024 f2752 v32000, N=8, K=4 written to /tmp, then select_recipe + execute_merge."""
+import os
+import pathlib
+import shutil
+import sys
+import tempfile
+import time
+
+os.environ["TAILOR_TRACE"] = "1"
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import paper_2602_22158_b200 as t  # noqa: E402
+
+work = pathlib.Path(tempfile.mkdtemp(prefix="tailor-trace-"))
+try:
+    fam = t.SynthFamily(t.ModelSpec(8, 1024, 2752, 32000, False, 42), 8, 4, 100)
+    dirs = [str(work / f"checkpoint-{k * 100}") for k in range(1, 5)]
+    for k in range(1, 5):
+        fam.write_dir(k, dirs[k - 1])
+    for i in range(3):
+        t0 = time.perf_counter()
+        rec, _, _ = t.select_recipe(dirs, 0.5)
+        t1 = time.perf_counter()
+        st = t.execute_merge(rec, str(work / f"m{i}"))
+        t2 = time.perf_counter()
+        print(f"iter {i}: select {1e3 * (t1 - t0):.1f} ms, merge {1e3 * (t2 - t1):.1f} ms ({st.bytes_moved / 1e9:.2f} GB)",
+              file=sys.stderr, flush=True)
+        shutil.rmtree(work / f"m{i}")
+finally:
+    shutil.rmtree(work, ignore_errors=True)
