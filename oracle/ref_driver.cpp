@@ -297,6 +297,7 @@ json cmd_train(const Args& a) {
     cfg.strategy.sparse_multiple = static_cast<int>(a.i64("sparse-multiple", 5));
     cfg.total_steps = static_cast<int>(a.i64("steps", 100));
     cfg.num_ranks = static_cast<int>(a.i64("ranks", 1));
+    cfg.grouping = a.str("grouping", "fine") == "coarse" ? Grouping::Coarse : Grouping::Fine;
     cfg.hyper.lr = a.f64("lr", kDefaultLr);
     cfg.hyper.weight_decay = a.f64("weight-decay", kDefaultWeightDecay);
     const TrainResult res = train(cfg, a.str("out"));

@@ -1,0 +1,164 @@
+"""File-level drop-in behaviour vs the reference binary: error kinds on corrupt /
+missing / incompatible sources, the CLI (exit codes, --json), hyperparameter and
+config provenance, tied models. Every successful merge is compared file by file."""
+import json
+import os
+import shutil
+import subprocess
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2602_22158_b200 as t  # noqa: E402
+from conftest import ref_tool, spec_args  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def gen(tmp, spec, N, K, name="run"):
+    return ref_tool("gen", *spec_args(spec), "--ranks", N, "--snapshots", K, "--out", tmp / name)[1]["snapshots"]
+
+
+def ref_error(recipe, out):
+    p = out.parent / (out.name + ".json")
+    p.write_text(recipe.to_json())
+    rc, _, err = ref_tool("merge", "--recipe", p, "--out", out, check=False)
+    return rc, json.loads(err.strip().splitlines()[-1])["error"] if rc else None
+
+
+def our_error(recipe, out):
+    try:
+        t.execute_merge(recipe, str(out))
+    except t.TailorError as e:
+        return e
+    return None
+
+
+def same_tree(a, b):
+    fa = sorted(str(p.relative_to(a)) for p in a.rglob("*") if p.is_file())
+    fb = sorted(str(p.relative_to(b)) for p in b.rglob("*") if p.is_file())
+    assert fa == fb
+    for rel in fa:
+        assert (a / rel).read_bytes() == (b / rel).read_bytes(), rel
+
+
+SPEC = dict(num_layers=3, hidden_dim=8, ffn_dim=16, vocab_size=32, weight_tied=False, seed=11)
+KIND_NAME = {t.ErrorKind.CorruptContainer: "CorruptContainer", t.ErrorKind.MissingArtifact: "MissingArtifact",
+             t.ErrorKind.Geometry: "GeometryError", t.ErrorKind.Storage: "StorageError",
+             t.ErrorKind.Consistency: "ConsistencyError", t.ErrorKind.Recipe: "RecipeError"}
+
+
+@pytest.mark.parametrize("damage", ["truncate_shard", "bad_header_json", "missing_shard", "missing_weights",
+                                    "shape_mismatch_header"])
+def test_corrupt_sources_fail_like_the_reference(tmp_path, damage):
+    need_gpu()
+    d = gen(tmp_path, SPEC, 2, 2)
+    bad = tmp_path / "bad"
+    shutil.copytree(d[0], bad)
+    shard = bad / "optim" / "rank_1.shard"
+    if damage == "truncate_shard":
+        shard.write_bytes(shard.read_bytes()[:-4])
+    elif damage == "bad_header_json":
+        b = bytearray(shard.read_bytes())
+        b[9] = ord("!")
+        shard.write_bytes(bytes(b))
+    elif damage == "missing_shard":
+        shard.unlink()
+    elif damage == "missing_weights":
+        (bad / "model.weights").unlink()
+    elif damage == "shape_mismatch_header":
+        b = shard.read_bytes()
+        hlen = int.from_bytes(b[:8], "little")
+        text = b[8:8 + hlen].decode()
+        at = text.index('"shape":[', text.index('"g1.master"'))  # a tensor the recipe reads
+        h = text[:at] + '"shape":[1,' + text[at + len('"shape":['):]
+        h = h.rstrip(" ")
+        h += " " * ((8 - (8 + len(h)) % 8) % 8)
+        shard.write_bytes(len(h).to_bytes(8, "little") + h.encode() + b[8 + hlen:])
+    recipe = t.MergeRecipe(num_ranks=2, base_checkpoint=d[1], slices=[t.RecipeSlice(str(bad), [0, 2])])
+    rc, ref_kind = ref_error(recipe, tmp_path / "ref_out")
+    err = our_error(recipe, tmp_path / "our_out")
+    assert rc != 0 and err is not None
+    assert KIND_NAME.get(err.kind, str(err.kind)) == ref_kind, (err, ref_kind)
+    # validation happens before any write, exactly as the reference (no partial output)
+    assert not (tmp_path / "our_out").exists() or not any((tmp_path / "our_out").rglob("*.shard"))
+
+
+def test_coarse_source_is_rejected(tmp_path):
+    need_gpu()
+    ref_tool("train", *spec_args(SPEC), "--strategy", "full", "--steps", 10, "--interval", 10, "--ranks", 2,
+             "--grouping", "coarse", "--out", tmp_path / "coarse")
+    recipe = t.MergeRecipe(num_ranks=2, base_checkpoint=str(tmp_path / "coarse" / "checkpoint-10"))
+    err = our_error(recipe, tmp_path / "o")
+    assert err is not None and err.kind == t.ErrorKind.Geometry
+    assert ref_error(recipe, tmp_path / "r")[1] == "GeometryError"
+
+
+def test_hyper_and_config_provenance(tmp_path):
+    """R/tests/test_merge.cpp:241-300: per-group hyper from each module's source; config_from rules."""
+    need_gpu()
+    for i, lr in enumerate(["0.001", "0.0005"]):
+        ref_tool("train", *spec_args(SPEC), "--strategy", "full", "--steps", 10 * (i + 1), "--interval", 10 * (i + 1),
+                 "--ranks", 1, "--lr", lr, "--out", tmp_path / f"s{i}")
+    a, b = str(tmp_path / "s0" / "checkpoint-10"), str(tmp_path / "s1" / "checkpoint-20")
+    for rec, name in [(t.MergeRecipe(num_ranks=1, base_checkpoint=a, slices=[t.RecipeSlice(b, [1])]), "latest"),
+                      (t.MergeRecipe(num_ranks=1, base_checkpoint=b, slices=[t.RecipeSlice(a, [0])], config_from=a),
+                       "explicit")]:
+        ours, refd = tmp_path / f"ours-{name}", tmp_path / f"ref-{name}"
+        t.execute_merge(rec, str(ours))
+        p = tmp_path / f"{name}.json"
+        p.write_text(rec.to_json())
+        ref_tool("merge", "--recipe", p, "--out", refd)
+        same_tree(refd, ours)
+    meta = json.loads((tmp_path / "ours-latest" / "optim_meta.json").read_text())
+    lrs = {g["owner"]: g["lr"] for g in meta["groups"] if g["decay"] == "decay"}
+    assert lrs["layers.1"] == 0.0005 and lrs["layers.0"] == 0.001
+    assert json.loads((tmp_path / "ours-explicit" / "trainer_state.json").read_text())["step"] == 10
+
+
+def test_cli_merge_plan_select(tmp_path):
+    need_gpu()
+    cli = str(t.CLI_PATH)
+    spec = dict(SPEC, num_layers=4)
+    d = gen(tmp_path, spec, 2, 3)
+    rec = t.MergeRecipe(num_ranks=2, base_checkpoint=d[2], slices=[t.RecipeSlice(d[0], [0, 2])], aux={"norm": d[1]})
+    (tmp_path / "r.yaml").write_text(rec.to_yaml())
+    p = subprocess.run([cli, "merge", "--recipe", str(tmp_path / "r.yaml"), "--out", str(tmp_path / "cli"), "--json"],
+                       capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr
+    js = json.loads(p.stdout)
+    assert js["shard_files_read"] == 2 * 3 and js["weight_files_read"] == 3
+    (tmp_path / "r.json").write_text(rec.to_json())
+    ref_tool("merge", "--recipe", tmp_path / "r.json", "--out", tmp_path / "ref")
+    same_tree(tmp_path / "ref", tmp_path / "cli")
+    # non-empty output directory -> StorageError -> exit 2
+    p = subprocess.run([cli, "merge", "--recipe", str(tmp_path / "r.yaml"), "--out", str(tmp_path / "cli")],
+                       capture_output=True, text=True)
+    assert p.returncode == 2 and "StorageError" in p.stderr
+    # select: magnitude strategy -> recipe identical to the reference-side restatement
+    p = subprocess.run([cli, "select", "--snapshots", ",".join(d), "--out", str(tmp_path / "sel.yaml")],
+                       capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr
+    ref = ref_tool("score", "--snapshots", ",".join(d))[1]["recipe"]
+    assert t.parse_recipe((tmp_path / "sel.yaml").read_text()) == t.MergeRecipe.from_json(json.dumps(ref))
+    # check: device re-verify of a merged checkpoint
+    p = subprocess.run([cli, "check", "--ckpt", str(tmp_path / "cli")], capture_output=True, text=True)
+    assert p.returncode == 0 and "ok" in p.stdout
+
+
+def test_tied_merge_has_no_lm_head(tmp_path):
+    need_gpu()
+    spec = dict(SPEC, weight_tied=True)
+    d = gen(tmp_path, spec, 1, 1)
+    t.execute_merge(t.MergeRecipe(num_ranks=1, base_checkpoint=d[0]), str(tmp_path / "m"))
+    b = (tmp_path / "m" / "model.weights").read_bytes()
+    hdr = json.loads(b[8:8 + int.from_bytes(b[:8], "little")])
+    assert "lm_head.weight" not in hdr
+    man = json.loads((tmp_path / "m" / "manifest.json").read_text())
+    assert len(man["modules"]) == 5 and man["strategy"] == "merged" and len(man["provenance"]) == 5
