@@ -127,11 +127,14 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def ncu_traffic(kernel: str):
-    """dram read+write bytes per launch from the committed ncu capture (profiles/), or None."""
+def ncu_traffic(kernel: str, workload: str):
+    """dram read+write bytes per launch of `kernel` from the committed ncu capture of the
+    same workload (profiles/*ncu_summary*.json), or None."""
     for p in sorted((ROOT / "profiles").glob("*ncu_summary*.json"), reverse=True):
         try:
             d = json.loads(p.read_text())
+            if d.get("workload") != workload:
+                continue
             k = d.get("kernels", {}).get(kernel)
             if k and k.get("dram_bytes_per_launch"):
                 return float(k["dram_bytes_per_launch"]), p.name
@@ -331,7 +334,8 @@ def our_arm(args, rank, world, local_rank):
     s_ms = statistics.mean(kt["score"])
     gather_achieved = 2 * sp0.bytes / (g_ms / 1e3) / 1e9
     score_achieved = scorer.bytes_read / (s_ms / 1e3) / 1e9
-    traffic, traffic_src = ncu_traffic("gather_bulk_kernel" if sp0.bulk_ok and args.variant != 1 else "gather_lsu_kernel")
+    traffic, traffic_src = ncu_traffic("gather_bulk_kernel" if sp0.bulk_ok and args.variant != 1 else "gather_lsu_kernel",
+                                       args.workload)
 
     if rank != 0:
         return 0
@@ -564,7 +568,8 @@ def scorer_arm(args, rank, world, local_rank):
     kms = statistics.mean(a.elapsed_time(b) for a, b in recs)
     hbm, peak_kind = peaks()
     achieved = scorer.bytes_read / (kms / 1e3) / 1e9
-    traffic, src = ncu_traffic("score_staged_kernel<16>" if args.score_variant != 1 else "score_partials_kernel<16>")
+    traffic, src = ncu_traffic("score_staged_kernel<16>" if args.score_variant == 2 else "score_partials_kernel<16>",
+                               args.workload)
     if rank != 0:
         return 0
     # Units: one rank partition of every module-pair score per GPU per step; all G

@@ -88,8 +88,9 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--full")
     ap.add_argument("--note", default="")
+    ap.add_argument("--workload", default="cfg3", help="bench workload the capture was taken on")
     a = ap.parse_args()
-    res = {"tag": a.tag, "note": a.note}
+    res = {"tag": a.tag, "note": a.note, "workload": a.workload}
     if a.launches:
         res["launch_list"] = launches(a.launches)
     if a.full:
