@@ -113,6 +113,10 @@ int tg_execute_merge(const char* recipe_yaml, const char* out_dir, const tg_merg
                      tg_merge_stats* stats);
 /* recipe_from_manifests (R/src/merge.cpp:359-418) -> recipe YAML. */
 int tg_recipe_from_manifests(const char* run_dir, int64_t failure_step, char* yaml_out, size_t cap, size_t* needed);
+/* coarse_to_fine / fine_to_coarse of a complete checkpoint directory (R/src/groups.cpp:152-220
+ * between read_checkpoint and write_checkpoint), as a device gather: to_fine=1 -> 2L+3 groups. */
+int tg_regroup(const char* src_dir, const char* out_dir, int32_t to_fine, const tg_merge_options* options,
+               tg_merge_stats* stats);
 /* read_checkpoint's invariants (R/src/checkpoint.cpp:485-575), checked on the device. */
 int tg_verify_checkpoint(const char* dir, int32_t device);
 /* Update-magnitude scores of consecutive snapshot directories on the device

@@ -456,6 +456,23 @@ json cmd_verify(const Args& a) {
     return {{"equal", r.equal}, {"first_divergence", r.first_divergence}};
 }
 
+// Regroup a checkpoint directory with reference primitives only:
+// read_checkpoint -> coarse_to_fine / fine_to_coarse (R/src/groups.cpp:212-220)
+// -> write_checkpoint (R/src/checkpoint.cpp:387-428).
+json cmd_regroup(const Args& a) {
+    CheckpointData d = read_checkpoint(a.str("dir"));
+    const bool to_fine = a.str("to", "fine") == "fine";
+    const GroupTable fine = build_group_table(d.spec);
+    OptimizerState src;
+    for (int g = 0; g < d.table.group_count(); ++g) src.push_back(d.groups.at(g));
+    OptimizerState dst = to_fine ? coarse_to_fine(d.spec, src, fine) : fine_to_coarse(d.spec, src, fine);
+    d.table = to_fine ? fine : build_coarse_table(d.spec);
+    d.groups.clear();
+    for (int g = 0; g < d.table.group_count(); ++g) d.groups.emplace(g, dst[static_cast<std::size_t>(g)]);
+    write_checkpoint(a.str("out"), d);
+    return {{"groups", d.table.group_count()}};
+}
+
 json cmd_read(const Args& a) {
     const CheckpointData d = read_checkpoint(a.str("dir"));
     return {{"ok", true}, {"groups", d.groups.size()}, {"tensors", d.weights.tensors.size()}};
@@ -481,6 +498,7 @@ int main(int argc, char** argv) {
         else if (cmd == "select-merge") out = cmd_select_merge(a);
         else if (cmd == "verify") out = cmd_verify(a);
         else if (cmd == "read") out = cmd_read(a);
+        else if (cmd == "regroup") out = cmd_regroup(a);
         else {
             std::cerr << "unknown subcommand " << cmd << "\n";
             return 1;

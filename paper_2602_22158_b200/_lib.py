@@ -95,6 +95,7 @@ SIGNATURES = {
     "tg_execute_merge": (_I, [_S, _S, _c.POINTER(MergeOptionsC), _c.POINTER(MergeStatsC)]),
     "tg_recipe_from_manifests": (_I, [_S, _I64, _c.c_char_p, _SZ, _PSZ]),
     "tg_verify_checkpoint": (_I, [_S, _I32]),
+    "tg_regroup": (_I, [_S, _S, _I32, _c.POINTER(MergeOptionsC), _c.POINTER(MergeStatsC)]),
     "tg_score_snapshots": (_I, [_c.POINTER(_S), _I32, _I32, _c.POINTER(_D), _c.POINTER(_D), _c.POINTER(_I32)]),
     "tg_select_recipe": (_I, [_c.POINTER(_S), _I32, _D, _I32, _c.c_char_p, _SZ, _PSZ, _c.POINTER(_I32),
                               _c.POINTER(_D)]),

@@ -253,6 +253,26 @@ int tg_recipe_from_manifests(const char* run_dir, int64_t failure_step, char* ou
     return guard([&] { put_text(recipe_to_yaml(recipe_from_manifests(run_dir ? run_dir : "", failure_step)), out, cap, needed); });
 }
 
+int tg_regroup(const char* src_dir, const char* out_dir, int32_t to_fine, const tg_merge_options* o, tg_merge_stats* st) {
+    return guard([&] {
+        MergeOptions opt;
+        if (o) {
+            opt.workers = o->workers;
+            opt.device = o->device;
+            opt.verify = o->verify != 0;
+        }
+        const MergeStats s = execute_regroup(src_dir ? src_dir : "", out_dir ? out_dir : "",
+                                             to_fine ? Grouping::Fine : Grouping::Coarse, opt);
+        if (st) {
+            st->shard_files_read = s.shard_files_read;
+            st->weight_files_read = s.weight_files_read;
+            st->wall_ms = s.wall_ms;
+            st->device_ms = s.device_ms;
+            st->bytes_moved = s.bytes_moved;
+        }
+    });
+}
+
 int tg_verify_checkpoint(const char* dir, int32_t device) {
     return guard([&] { verify_checkpoint_dir(dir ? dir : "", device); });
 }

@@ -643,7 +643,9 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
     const fs::path dir(dir_s);
     const CheckpointSummary s = read_checkpoint_summary(dir);
-    if (s.optim.grouping != Grouping::Fine) fail(ErrorKind::Geometry, "device verify supports the fine grouping only");
+    const GroupTable table = s.optim.grouping == Grouping::Fine ? build_group_table(s.spec) : build_coarse_table(s.spec);
+    std::map<int, std::vector<TensorSlice>> group_slices;
+    for (const auto& g : s.optim.groups) group_slices[g.index] = group_tensor_slices(s.spec, table, g.index);
     const fs::path optim = dir / "optim";
     if (!fs::exists(optim)) fail(ErrorKind::MissingArtifact, "'" + optim.string() + "' does not exist");
     std::size_t files = 0;
@@ -651,7 +653,6 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
     if (files != static_cast<std::size_t>(s.optim.num_ranks))
         fail(ErrorKind::Geometry, dir.string() + ": found " + std::to_string(files) + " shard files for " +
                                       std::to_string(s.optim.num_ranks) + " ranks");
-    const ModelLayout model(s.spec);
     const ContainerLayout wl = read_layout(weights_path(dir));
     std::size_t expect_tensors = 0;
     for (const auto& m : s.manifest.modules)
@@ -702,7 +703,7 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
             if (valid > 0)
                 ranges.push_back({reinterpret_cast<const std::uint32_t*>(ds.get() + f[2]->begin),
                                   static_cast<std::uint64_t>(valid), 1, 0});
-            for (const auto& sl2 : model.slices(g.index)) {
+            for (const auto& sl2 : group_slices.at(g.index)) {
                 const std::int64_t a = std::max(first, sl2.group_offset);
                 const std::int64_t b = std::min(first + valid, sl2.group_offset + sl2.decl.numel());
                 if (a >= b) continue;

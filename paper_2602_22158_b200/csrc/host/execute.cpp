@@ -10,6 +10,7 @@
 // chunks on two CUDA streams; the re-verify is the device kernel K6.
 #include <algorithm>
 #include <chrono>
+#include <cstring>
 #include <fcntl.h>
 #include <filesystem>
 #include <map>
@@ -78,6 +79,7 @@ class FileAssembler {
         std::vector<std::uint64_t> file_off(pp.windows.size());
         std::vector<std::unique_ptr<Fd>> fds(pp.windows.size());
         for (std::size_t w = 0; w < pp.windows.size(); ++w) {
+            if (pp.windows[w].container == kZeroContainer) continue; // zero fill: no source file
             file_off[w] = source_payload_offset(window_files[w]) + pp.windows[w].lo;
             if (!uncached_) {
                 fds[w] = std::make_unique<Fd>(window_files[w], O_RDONLY);
@@ -115,6 +117,10 @@ class FileAssembler {
             std::vector<ReadJob> jobs;
             for (const auto& rd : c.reads) {
                 int fd;
+                if (pp.windows[rd.w].container == kZeroContainer) {
+                    std::memset(pin_in_[slot].get() + rd.at, 0, rd.b - rd.a);
+                    continue;
+                }
                 if (uncached_) {
                     opened.push_back(std::make_unique<Fd>(window_files[rd.w], O_RDONLY));
                     if (opened.back()->fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + window_files[rd.w].string() + "'");
@@ -303,6 +309,139 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
     if (options.verify) verify_checkpoint_dir(out_dir.string(), options.device);
     phase.reset();
 
+    stats.device_ms = fa.device_ms;
+    stats.bytes_moved = fa.bytes;
+    stats.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return stats;
+}
+
+// ---- regroup: coarse <-> fine re-slicing on files -------------------
+// Same result as read_checkpoint -> coarse_to_fine / fine_to_coarse
+// (R/src/groups.cpp:152-220, a gather by model offset) -> write_checkpoint, but
+// expressed as byte segments: every target rank chunk is a run of pieces of
+// source rank chunks (split at tensor and rank-chunk boundaries) plus zero
+// padding, assembled by K2 without materialising the unsharded state.
+MergeStats execute_regroup(const fs::path& src, const fs::path& out_dir, Grouping target, const MergeOptions& options) {
+    const auto t0 = std::chrono::steady_clock::now();
+    MergeStats stats;
+    std::error_code ec;
+    if (fs::exists(out_dir) && !fs::is_empty(out_dir, ec))
+        fail(ErrorKind::Storage, "refusing to write into non-empty directory '" + out_dir.string() + "'");
+    cuda_check(cudaSetDevice(options.device), "cudaSetDevice");
+    const CheckpointSummary s = read_checkpoint_summary(src);
+    const ModelSpec& spec = s.spec;
+    const int N = s.optim.num_ranks;
+    for (const auto& m : enumerate_modules(spec))
+        if (!s.manifest.contains(m))
+            fail(ErrorKind::MissingModules, "regrouping needs a complete checkpoint; '" + src.string() + "' lacks '" +
+                                                module_name(m) + "'");
+    const GroupTable src_table = s.optim.grouping == Grouping::Fine ? build_group_table(spec) : build_coarse_table(spec);
+    const GroupTable dst_table = target == Grouping::Fine ? build_group_table(spec) : build_coarse_table(spec);
+    const ShardGeometry geom{N};
+    const std::string key = src.string();
+
+    // source side: tensor -> (group, group offset); shard layouts per rank
+    std::map<std::string, std::pair<int, std::int64_t>> where;
+    for (int g = 0; g < src_table.group_count(); ++g)
+        for (const auto& sl : group_tensor_slices(spec, src_table, g)) where[sl.decl.name] = {g, sl.group_offset};
+    std::vector<ContainerLayout> shards;
+    for (int r = 0; r < N; ++r) {
+        shards.push_back(read_layout(shard_path(src, r)));
+        for (const auto& gm : s.optim.groups)
+            for (const char* f : {".master", ".exp_avg", ".exp_avg_sq"}) {
+                const Entry* e = shards.back().find(shard_key(gm.index, f));
+                if (!e) fail(ErrorKind::CorruptContainer, shard_path(src, r).string() + ": missing tensor '" + shard_key(gm.index, f) + "'");
+                if (e->dtype != Dtype::F32 || e->shape != std::vector<std::int64_t>{gm.shard_length})
+                    fail(ErrorKind::Geometry, shard_path(src, r).string() + ": tensor '" + e->name + "' has unexpected dtype/shape");
+            }
+    }
+    stats.shard_files_read = N;
+
+    // target optim_meta: hyper inherited from the source group of the first slice,
+    // weight decay by decay class; conflicts are a GeometryError (as reslice).
+    std::map<int, AdamHyperparams> hyp;
+    std::vector<std::vector<TensorSlice>> dst_slices(static_cast<std::size_t>(dst_table.group_count()));
+    for (int g = 0; g < dst_table.group_count(); ++g) {
+        dst_slices[static_cast<std::size_t>(g)] = group_tensor_slices(spec, dst_table, g);
+        const DecayClass d = dst_table.groups[static_cast<std::size_t>(g)].decay;
+        bool set = false;
+        for (const auto& sl : dst_slices[static_cast<std::size_t>(g)]) {
+            const AdamHyperparams h = hyper_for_class(s.optim.find(where.at(sl.decl.name).first)->hyper, d);
+            if (!set) {
+                hyp[g] = h;
+                set = true;
+            } else if (!(hyp[g] == h)) {
+                fail(ErrorKind::Geometry, "conflicting hyperparams while re-slicing group " + std::to_string(g));
+            }
+        }
+    }
+    const OptimMeta optim = make_optim_meta(dst_table, hyp, geom, s.optim.step);
+
+    std::vector<PartitionPlan> plans;
+    for (int r = 0; r < N; ++r) {
+        std::vector<EntryDecl> decls;
+        for (int g = 0; g < dst_table.group_count(); ++g)
+            for (const char* f : {".exp_avg", ".exp_avg_sq", ".master"})
+                decls.push_back({shard_key(g, f), Dtype::F32, {geom.shard_length(dst_table.groups[static_cast<std::size_t>(g)].element_count)}});
+        PartitionPlan pp;
+        pp.out = layout_for(std::move(decls), {{"num_ranks", std::to_string(N)}, {"rank", std::to_string(r)}});
+        pp.dst_lo = 0;
+        pp.dst_hi = pp.out.payload_bytes;
+        std::vector<CopyPiece> pieces;
+        for (int g = 0; g < dst_table.group_count(); ++g) {
+            const std::int64_t len = dst_table.groups[static_cast<std::size_t>(g)].element_count;
+            const std::int64_t c = geom.shard_length(len), first = static_cast<std::int64_t>(r) * c;
+            for (const char* f : {".exp_avg", ".exp_avg_sq", ".master"}) {
+                const std::uint64_t dbase = pp.out.find(shard_key(g, f))->begin;
+                for (const auto& sl : dst_slices[static_cast<std::size_t>(g)]) {
+                    std::int64_t a = std::max(first, sl.group_offset);
+                    const std::int64_t b = std::min(first + c, sl.group_offset + sl.decl.numel());
+                    const auto [sg, soff] = where.at(sl.decl.name);
+                    const std::int64_t sc = geom.shard_length(src_table.groups[static_cast<std::size_t>(sg)].element_count);
+                    while (a < b) { // split at source rank-chunk boundaries
+                        const std::int64_t x = soff + (a - sl.group_offset); // source group element
+                        const std::int64_t rr = x / sc, pos = x % sc;
+                        const std::int64_t n = std::min(b - a, sc - pos);
+                        const Entry* se = shards[static_cast<std::size_t>(rr)].find(shard_key(sg, f));
+                        pieces.push_back({key, static_cast<int>(rr), se->begin + static_cast<std::uint64_t>(pos) * 4,
+                                          dbase + static_cast<std::uint64_t>(a - first) * 4, static_cast<std::uint64_t>(n) * 4});
+                        a += n;
+                    }
+                }
+                const std::int64_t valid = std::clamp<std::int64_t>(len - first, 0, c);
+                if (valid < c) // zero padding
+                    pieces.push_back({"", kZeroContainer, 0, dbase + static_cast<std::uint64_t>(valid) * 4,
+                                      static_cast<std::uint64_t>(c - valid) * 4});
+            }
+        }
+        finalize_partition(pp, std::move(pieces));
+        plans.push_back(std::move(pp));
+    }
+    // weights: the tensor set and order do not depend on the grouping
+    PartitionPlan wp;
+    wp.out = read_layout(weights_path(src));
+    stats.weight_files_read = 1;
+    wp.dst_lo = 0;
+    wp.dst_hi = wp.out.payload_bytes;
+    finalize_partition(wp, {{key, -1, 0, 0, wp.out.payload_bytes}});
+
+    fs::create_directories(out_dir / "optim", ec);
+    if (ec) fail(ErrorKind::Storage, "cannot create '" + out_dir.string() + "': " + ec.message());
+    const int workers = options.workers > 0 ? options.workers : std::max(N, io_threads());
+    FileAssembler fa(workers, false);
+    const auto files_of = [&](const PartitionPlan& pp) {
+        std::vector<fs::path> files;
+        for (const auto& w : pp.windows)
+            files.push_back(w.container == kZeroContainer ? fs::path() : w.container < 0 ? weights_path(src) : shard_path(src, w.container));
+        return files;
+    };
+    fa.assemble(wp, files_of(wp), weights_path(out_dir));
+    for (int r = 0; r < N; ++r) fa.assemble(plans[static_cast<std::size_t>(r)], files_of(plans[static_cast<std::size_t>(r)]), shard_path(out_dir, r));
+    write_text_file(optim_meta_path(out_dir), render_optim_meta_json(optim));
+    write_text_file(config_path(out_dir), render_config_json(spec));
+    write_text_file(trainer_state_path(out_dir), render_trainer_state_json(s.trainer));
+    write_text_file(manifest_path(out_dir), render_manifest_json(s.manifest));
+    if (options.verify) verify_checkpoint_dir(out_dir.string(), options.device);
     stats.device_ms = fa.device_ms;
     stats.bytes_moved = fa.bytes;
     stats.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

@@ -122,17 +122,16 @@ MergePlan resolve_plan_with(const MergeRecipe& recipe, const SummaryLookup& look
 }
 
 namespace {
+using Piece = CopyPiece;
+void finish_plan(PartitionPlan& pp, std::vector<Piece> pieces);
+} // namespace
+
+void finalize_partition(PartitionPlan& pp, std::vector<CopyPiece> pieces) { finish_plan(pp, std::move(pieces)); }
+
+namespace {
 
 // Builds windows + coalesced segments from (source, container, src range,
 // dst range) pieces in destination order.
-struct Piece {
-    std::string source;
-    int container;
-    std::uint64_t src_off; // payload-relative in the source container
-    std::uint64_t dst_off;
-    std::uint64_t bytes;
-};
-
 void finish_plan(PartitionPlan& pp, std::vector<Piece> pieces) {
     std::map<std::pair<std::string, int>, std::pair<std::uint64_t, std::uint64_t>> span;
     for (const auto& p : pieces) {

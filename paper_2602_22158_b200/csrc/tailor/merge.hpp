@@ -79,6 +79,13 @@ struct MergeStats {
 
 MergeStats execute_merge(const MergePlan& plan, const std::filesystem::path& out_dir, const MergeOptions& options = {});
 
+// Re-slice a complete checkpoint between the coarse (2-group) and fine
+// (2L+3 / 2L+2) optimizer layouts (R/src/groups.cpp:152-220)
+// as a device gather; output bytes equal read_checkpoint -> coarse_to_fine /
+// fine_to_coarse -> write_checkpoint.
+MergeStats execute_regroup(const std::filesystem::path& src, const std::filesystem::path& out_dir, Grouping target,
+                           const MergeOptions& options = {});
+
 std::vector<std::filesystem::path> list_checkpoints(const std::filesystem::path& run_dir);
 MergeRecipe recipe_from_manifests(const std::filesystem::path& run_dir, std::int64_t failure_step);
 
@@ -115,6 +122,19 @@ struct SourceLayout {
     std::vector<ContainerLayout> shards;
 };
 using LayoutLookup = std::function<const SourceLayout&(const std::string&)>;
+
+// A copy expressed against a source container: windows and coalesced
+// segments are derived by finalize_partition. container -1 = weights,
+// r >= 0 = rank-r shard, kZeroContainer = zero fill (no source file).
+inline constexpr int kZeroContainer = -2;
+struct CopyPiece {
+    std::string source;
+    int container;
+    std::uint64_t src_off; // payload-relative in the source container
+    std::uint64_t dst_off;
+    std::uint64_t bytes;
+};
+void finalize_partition(PartitionPlan& pp, std::vector<CopyPiece> pieces);
 
 // Weights container plan (validates tensor presence/dtype/shape exactly as
 // R/src/merge.cpp:254-266) restricted to output bytes [lo, hi).

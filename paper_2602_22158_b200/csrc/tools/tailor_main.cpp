@@ -8,6 +8,7 @@
 //   tailor select --snapshots A,B,... [--rho 0.5] --out r.yaml [--device D] [--json]
 //   tailor score  --snapshots A,B,... [--device D]
 //   tailor check  --ckpt DIR [--device D]
+//   tailor regroup --ckpt DIR --out DIR [--to fine|coarse] [--device D] [--no-verify]
 // Exit codes: 0 success, 1 user error, 2 internal/consistency error.
 #include <cstdio>
 #include <cstring>
@@ -164,6 +165,24 @@ int cmd_score(const Args& a) {
     return 0;
 }
 
+int cmd_regroup(const Args& a) {
+    if (!require(a, {"ckpt", "out"})) return 1;
+    const std::string to = a.kv.count("to") ? a.kv.at("to") : "fine";
+    if (to != "fine" && to != "coarse") {
+        std::cerr << "error: RecipeError: --to must be fine or coarse\n";
+        return 1;
+    }
+    tg_merge_options opt{};
+    opt.device = a.kv.count("device") ? std::stoi(a.kv.at("device")) : 0;
+    opt.verify = a.flags.count("no-verify") ? 0 : 1;
+    tg_merge_stats st{};
+    const int rc = tg_regroup(a.kv.at("ckpt").c_str(), a.kv.at("out").c_str(), to == "fine" ? 1 : 0, &opt, &st);
+    if (rc != TG_OK) return report(rc);
+    std::cout << "regrouped (" << to << ") checkpoint written to " << a.kv.at("out") << " (" << st.bytes_moved
+              << " bytes, " << st.wall_ms << " ms)\n";
+    return 0;
+}
+
 int cmd_check(const Args& a) {
     if (!require(a, {"ckpt"})) return 1;
     const int device = a.kv.count("device") ? std::stoi(a.kv.at("device")) : 0;
@@ -198,6 +217,7 @@ int main(int argc, char** argv) {
         if (cmd == "select") return cmd_select(a);
         if (cmd == "score") return cmd_score(a);
         if (cmd == "check") return cmd_check(a);
+        if (cmd == "regroup") return cmd_regroup(a);
     } catch (const std::exception& e) {
         std::cerr << "error: " << e.what() << "\n";
         return 1;

@@ -26,7 +26,7 @@ from ._lib import (ErrorKind, GatherSegC, MergeOptionsC, MergeStatsC, ModelSpecC
 
 __all__ = ["ErrorKind", "TailorError", "ModelSpec", "RecipeSlice", "MergeRecipe", "MergeOptions", "MergeStats",
            "parse_recipe", "recipe_to_yaml", "resolve_plan", "execute_merge", "recipe_from_manifests",
-           "verify_checkpoint", "score_snapshots", "select_recipe", "layer_map", "SynthFamily", "Scorer",
+           "verify_checkpoint", "regroup", "score_snapshots", "select_recipe", "layer_map", "SynthFamily", "Scorer",
            "MergePartition", "gather"]
 
 
@@ -140,6 +140,16 @@ def execute_merge(recipe, out_dir: str, options: Optional[MergeOptions] = None) 
 
 def recipe_from_manifests(run_dir: str, failure_step: int) -> MergeRecipe:
     return parse_recipe(text_call(lib().tg_recipe_from_manifests, _b(str(run_dir)), failure_step))
+
+
+def regroup(src_dir: str, out_dir: str, to_fine: bool = True, options: Optional[MergeOptions] = None) -> MergeStats:
+    """coarse_to_fine / fine_to_coarse of a checkpoint directory on the device (R/src/groups.cpp:152-220)."""
+    o = options or MergeOptions()
+    copt = MergeOptionsC(o.workers, 0, o.device, 1 if o.verify else 0)
+    st = MergeStatsC()
+    check(lib().tg_regroup(_b(str(src_dir)), _b(str(out_dir)), 1 if to_fine else 0, ctypes.byref(copt),
+                           ctypes.byref(st)))
+    return MergeStats(st.shard_files_read, st.weight_files_read, st.wall_ms, st.device_ms, st.bytes_moved)
 
 
 def verify_checkpoint(path: str, device: int = 0) -> None:

@@ -162,3 +162,39 @@ def test_tied_merge_has_no_lm_head(tmp_path):
     assert "lm_head.weight" not in hdr
     man = json.loads((tmp_path / "m" / "manifest.json").read_text())
     assert len(man["modules"]) == 5 and man["strategy"] == "merged" and len(man["provenance"]) == 5
+
+
+@pytest.mark.parametrize("N,tied", [(1, False), (3, False), (4, True), (8, False)])
+def test_regroup_matches_reference(tmp_path, N, tied):
+    """f3: coarse -> fine -> coarse through the device gather == reference read/coarse_to_fine/write."""
+    need_gpu()
+    spec = dict(SPEC, weight_tied=tied, num_layers=4)
+    ref_tool("train", *spec_args(spec), "--strategy", "full", "--steps", 20, "--interval", 20, "--ranks", N,
+             "--grouping", "coarse", "--out", tmp_path / "run")
+    src = tmp_path / "run" / "checkpoint-20"
+    ref_tool("regroup", "--dir", src, "--out", tmp_path / "ref_fine")
+    st = t.regroup(str(src), str(tmp_path / "fine"), to_fine=True)
+    same_tree(tmp_path / "ref_fine", tmp_path / "fine")
+    assert st.bytes_moved > 0
+    ref_tool("regroup", "--dir", tmp_path / "ref_fine", "--to", "coarse", "--out", tmp_path / "ref_coarse")
+    t.regroup(str(tmp_path / "fine"), str(tmp_path / "coarse"), to_fine=False)
+    same_tree(tmp_path / "ref_coarse", tmp_path / "coarse")
+    same_tree(src, tmp_path / "coarse")  # round trip is the identity on bytes
+    # the regrouped (fine) checkpoint is now mergeable
+    t.execute_merge(t.MergeRecipe(num_ranks=N, base_checkpoint=str(tmp_path / "fine")), str(tmp_path / "merged"))
+    t.verify_checkpoint(str(tmp_path / "coarse"))
+
+
+def test_regroup_cli_and_errors(tmp_path):
+    need_gpu()
+    d = gen(tmp_path, SPEC, 2, 1)
+    p = subprocess.run([str(t.CLI_PATH), "regroup", "--ckpt", d[0], "--out", str(tmp_path / "c"), "--to", "coarse"],
+                       capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr
+    ref_tool("regroup", "--dir", d[0], "--to", "coarse", "--out", tmp_path / "rc")
+    same_tree(tmp_path / "rc", tmp_path / "c")
+    ref_tool("gen", *spec_args(SPEC), "--ranks", 2, "--snapshots", 1, "--out", tmp_path / "part",
+             "--partial", "1=layers.0,norm")
+    with pytest.raises(t.TailorError) as e:
+        t.regroup(str(tmp_path / "part" / "checkpoint-100"), str(tmp_path / "x"))
+    assert e.value.kind == t.ErrorKind.MissingModules
