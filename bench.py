@@ -56,6 +56,7 @@ WORKLOADS = {
 # Reference-arm / cpu_baseline sample: cfg3's merge, shrunk to fit a few
 # seconds of CPU work per step (same layout rules, 8 ranks, 4 snapshots).
 SAMPLE = (1, 1024, 3584, 4096, False, 8, 4, 0.5)
+SCORE_VARIANTS = {0: "auto", 1: "register", 2: "staged", 3: "register-128b", 4: "register-64b"}
 
 
 def env_int(name, default):
@@ -350,7 +351,7 @@ def our_arm(args, rank, world, local_rank):
                    "composite_bytes_per_gpu_step": composite, "parallelism": f"zero-partition x{world}",
                    "l2": "inputs 62 GB/GPU >> 126 MB L2 (no flush needed)",
                    "gather_variant": {0: "auto", 1: "lsu", 2: "bulk"}[args.variant],
-                   "score_variant": {0: "auto", 1: "register", 2: "staged"}[args.score_variant],
+                   "score_variant": SCORE_VARIANTS[args.score_variant],
                    "plan_ms_uncached": round(plan_ms, 3), "min_boundary_gap": state["gap"]},
         "layers_scored_per_s": round(scores_per_s, 1),
         "kernels_ms": {k: round(statistics.mean(x), 4) for k, x in kt.items()},
@@ -582,7 +583,7 @@ def scorer_arm(args, rank, world, local_rank):
         "dtype": "f32 -> f64 accumulate", "data": "synthetic",
         "config": {"workload": "cfg4", "description": desc, "snapshots": K, "pairs": K - 1, "modules": M,
                    "zero_ranks": N, "unit_of_work": "one ZeRO rank partition of 16 snapshots' masters per GPU",
-                   "score_variant": {0: "auto", 1: "register", 2: "staged"}[args.score_variant],
+                   "score_variant": SCORE_VARIANTS[args.score_variant],
                    "bytes_per_gpu_step": scorer.bytes_read, "min_boundary_gap": res[3]},
         "roofline": {"bound": "hbm", "kernel": "K3 score_partials<16>", "achieved": round(achieved, 1), "peak": hbm,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "peak_kind": peak_kind,

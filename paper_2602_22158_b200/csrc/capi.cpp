@@ -499,7 +499,8 @@ void tg_scorer_destroy(tg_scorer* s) { delete s; }
 
 int tg_scorer_set_variant(tg_scorer* s, int32_t variant) {
     return guard([&] {
-        if (variant < 0 || variant > 2) fail(ErrorKind::Geometry, "scorer variant must be 0 (auto), 1 (register) or 2 (staged)");
+        if (variant < 0 || variant > 4)
+            fail(ErrorKind::Geometry, "scorer variant: 0 auto, 1 register, 2 staged, 3 register-128b, 4 register-64b");
         s->plan->set_variant(variant);
     });
 }

@@ -43,7 +43,11 @@ static_assert(sizeof(ScoreTile) == 24, "ScoreTile is part of the C ABI");
 // tile_partials[t][p][0|1] = (sum (B-A)^2, sum A^2) over tile t for pair
 // p = (snapshot p, snapshot p+1), FP64. 2 <= K <= 16.
 // variant: 0 auto, 1 register-staged 128-bit loads, 2 TMA-bulk smem ring (needs vec_ok).
-enum ScoreVariant : int { kScoreAuto = 0, kScoreRegister = 1, kScoreStaged = 2 };
+// Register variants: 3 forces 128-bit loads, 4 forces 64-bit loads. Measured
+// at K=16: 128-bit 0.938, 64-bit 0.675 (spills at the 2-CTA register cap), so
+// auto always uses 128-bit loads.
+enum ScoreVariant : int { kScoreAuto = 0, kScoreRegister = 1, kScoreStaged = 2, kScoreWide = 3, kScoreNarrow = 4 };
+constexpr int kNarrowMinK = 1 << 20;
 // Measured (profiles/r1_*): the staged ring is barrier-bound with one 8-warp CTA
 // per SM (K=16: 88% vs 90% register; K=4: 61% vs 106%), so auto never picks it.
 constexpr int kStagedMinK = 1 << 20;

@@ -432,11 +432,12 @@ def test_scorer_variants_agree(K):
         bufs = [dev(fam.packed_master_bytes(r)) for _ in range(K)]
         fam.gen_masters(r, 1, K, [b.data_ptr() for b in bufs])
         outs = []
-        for v in (1, 2):
+        for v in (1, 2, 3, 4):
             sc = t.Scorer(fam, r, 1, K, packed=True)
             sc.set_variant(v)
             out = torch.zeros((K - 1) * M * 2, dtype=torch.float64, device="cuda")
             sc.run([b.data_ptr() for b in bufs], out.data_ptr())
             outs.append(out)
         torch.cuda.synchronize()
-        assert torch.allclose(outs[0], outs[1], rtol=1e-12, atol=0)
+        for o_ in outs[1:]:
+            assert torch.allclose(outs[0], o_, rtol=1e-12, atol=0)
