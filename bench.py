@@ -569,7 +569,8 @@ def scorer_arm(args, rank, world, local_rank):
     kms = statistics.mean(a.elapsed_time(b) for a, b in recs)
     hbm, peak_kind = peaks()
     achieved = scorer.bytes_read / (kms / 1e3) / 1e9
-    traffic, src = ncu_traffic("score_staged_kernel<16>" if args.score_variant == 2 else "score_partials_kernel<16>",
+    traffic, src = ncu_traffic("score_staged_kernel<16>" if args.score_variant == 2 else
+                               "score_partials_kernel<16,2>" if args.score_variant == 4 else "score_partials_kernel<16,4>",
                                args.workload)
     if rank != 0:
         return 0

@@ -21,8 +21,8 @@ ROOT = pathlib.Path(__file__).resolve().parents[1]
 
 
 def short(name: str) -> str:
-    m = re.search(r"(\w+_kernel)(<\d+>)?", name)
-    return (m.group(1) + (m.group(2) or "")) if m else name[:60]
+    m = re.search(r"(\w+_kernel)(<[\d, ]+>)?", name)
+    return (m.group(1) + (m.group(2) or "").replace(" ", "")) if m else name[:60]
 
 
 def launches(path):
