@@ -117,6 +117,25 @@ int tg_recipe_from_manifests(const char* run_dir, int64_t failure_step, char* ya
  * between read_checkpoint and write_checkpoint), as a device gather: to_fine=1 -> 2L+3 groups. */
 int tg_regroup(const char* src_dir, const char* out_dir, int32_t to_fine, const tg_merge_options* options,
                tg_merge_stats* stats);
+/* Device-resident trainer: train() (R/src/trainer.cpp:109-123) with the
+ * optimizer state in HBM and bit-exact AdamW (R/src/adamw.cpp:10-66); strategy 0 full,
+ * 1 parity, 2 filter (R/src/strategy.cpp:48-91), 3 magnitude (in-situ update-magnitude
+ * selection, rho = fraction of modules saved per checkpoint after the first). */
+typedef struct tg_train_config {
+    int32_t total_steps;
+    int32_t num_ranks;
+    int32_t interval;
+    int32_t strategy;
+    int32_t head_count;
+    int32_t tail_count;
+    int32_t sparse_multiple;
+    int32_t device;
+    double lr;
+    double weight_decay;
+    double rho;
+} tg_train_config;
+int tg_train(const tg_model_spec* spec, const tg_train_config* config, const char* out_dir,
+             int32_t* checkpoints_written);
 /* read_checkpoint's invariants (R/src/checkpoint.cpp:485-575), checked on the device. */
 int tg_verify_checkpoint(const char* dir, int32_t device);
 /* Update-magnitude scores of consecutive snapshot directories on the device

@@ -28,6 +28,7 @@
 #include <filesystem>
 #include <iostream>
 #include <map>
+#include <optional>
 #include <set>
 #include <string>
 #include <vector>
@@ -452,7 +453,12 @@ json cmd_select_merge(const Args& a) {
 }
 
 json cmd_verify(const Args& a) {
-    const VerifyResult r = verify_checkpoints(a.str("a"), a.str("b"));
+    std::optional<std::vector<ModuleId>> mods;
+    if (a.has("modules")) {
+        mods.emplace();
+        for (const auto& n : split(a.str("modules"), ',')) mods->push_back(parse_module_name(n));
+    }
+    const VerifyResult r = verify_checkpoints(a.str("a"), a.str("b"), mods);
     return {{"equal", r.equal}, {"first_divergence", r.first_divergence}};
 }
 

@@ -62,6 +62,13 @@ class MergeStatsC(ctypes.Structure):
                 ("wall_ms", ctypes.c_double), ("device_ms", ctypes.c_double), ("bytes_moved", ctypes.c_uint64)]
 
 
+class TrainConfigC(ctypes.Structure):
+    _fields_ = [("total_steps", ctypes.c_int32), ("num_ranks", ctypes.c_int32), ("interval", ctypes.c_int32),
+                ("strategy", ctypes.c_int32), ("head_count", ctypes.c_int32), ("tail_count", ctypes.c_int32),
+                ("sparse_multiple", ctypes.c_int32), ("device", ctypes.c_int32), ("lr", ctypes.c_double),
+                ("weight_decay", ctypes.c_double), ("rho", ctypes.c_double)]
+
+
 class GatherSegC(ctypes.Structure):
     _fields_ = [("src", ctypes.c_void_p), ("dst_off", ctypes.c_uint64), ("bytes", ctypes.c_uint64)]
 
@@ -96,6 +103,7 @@ SIGNATURES = {
     "tg_recipe_from_manifests": (_I, [_S, _I64, _c.c_char_p, _SZ, _PSZ]),
     "tg_verify_checkpoint": (_I, [_S, _I32]),
     "tg_regroup": (_I, [_S, _S, _I32, _c.POINTER(MergeOptionsC), _c.POINTER(MergeStatsC)]),
+    "tg_train": (_I, [_c.POINTER(ModelSpecC), _c.POINTER(TrainConfigC), _S, _c.POINTER(_I32)]),
     "tg_score_snapshots": (_I, [_c.POINTER(_S), _I32, _I32, _c.POINTER(_D), _c.POINTER(_D), _c.POINTER(_I32)]),
     "tg_select_recipe": (_I, [_c.POINTER(_S), _I32, _D, _I32, _c.c_char_p, _SZ, _PSZ, _c.POINTER(_I32),
                               _c.POINTER(_D)]),

@@ -17,6 +17,7 @@
 #include "tailor/errors.hpp"
 #include "tailor/io.hpp"
 #include "tailor/merge.hpp"
+#include "tailor/trainer.hpp"
 
 using nlohmann::json;
 using namespace tailor;
@@ -270,6 +271,36 @@ int tg_regroup(const char* src_dir, const char* out_dir, int32_t to_fine, const 
             st->device_ms = s.device_ms;
             st->bytes_moved = s.bytes_moved;
         }
+    });
+}
+
+int tg_train(const tg_model_spec* spec, const tg_train_config* c, const char* out_dir, int32_t* written) {
+    return guard([&] {
+        if (!c) fail(ErrorKind::Recipe, "null train config");
+        DeviceTrainConfig cfg;
+        cfg.spec = to_spec(spec);
+        cfg.total_steps = c->total_steps;
+        cfg.num_ranks = c->num_ranks;
+        cfg.strategy.interval = c->interval;
+        cfg.strategy.head_count = c->head_count;
+        cfg.strategy.tail_count = c->tail_count;
+        cfg.strategy.sparse_multiple = c->sparse_multiple;
+        switch (c->strategy) {
+            case 0: cfg.strategy.kind = StrategyKind::Full; break;
+            case 1: cfg.strategy.kind = StrategyKind::Parity; break;
+            case 2: cfg.strategy.kind = StrategyKind::Filter; break;
+            case 3: // magnitude: saved on the full schedule (readable by reference tools), label "magnitude"
+                cfg.strategy.kind = StrategyKind::Full;
+                cfg.magnitude = true;
+                break;
+            default: fail(ErrorKind::Recipe, "unknown strategy code " + std::to_string(c->strategy));
+        }
+        cfg.hyper.lr = c->lr;
+        cfg.hyper.weight_decay = c->weight_decay;
+        cfg.rho = c->rho;
+        cfg.device = c->device;
+        const auto dirs = device_train(cfg, out_dir ? out_dir : "");
+        if (written) *written = static_cast<int32_t>(dirs.size());
     });
 }
 

@@ -1,0 +1,380 @@
+// Device-resident trainer (see tailor/trainer.hpp).
+#include "tailor/trainer.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <fstream>
+#include <map>
+#include <set>
+
+#include <json.hpp>
+
+#include "tailor/errors.hpp"
+
+namespace tailor {
+
+namespace fs = std::filesystem;
+
+void validate_strategy(const StrategyConfig& cfg, const ModelSpec& spec) {
+    if (cfg.interval < 1) fail(ErrorKind::Recipe, "checkpoint interval must be >= 1");
+    if (cfg.kind == StrategyKind::Filter) {
+        if (cfg.head_count < 0 || cfg.tail_count < 0 || cfg.sparse_multiple < 1)
+            fail(ErrorKind::Recipe, "invalid filter parameters");
+        if (cfg.head_count + cfg.tail_count > spec.num_layers)
+            fail(ErrorKind::Recipe, "filter head_count + tail_count exceeds the layer count");
+    }
+}
+
+std::vector<ModuleId> modules_to_save(const StrategyConfig& cfg, const ModelSpec& spec, std::int64_t counter) {
+    spec.validate();
+    validate_strategy(cfg, spec);
+    if (counter < 1) fail(ErrorKind::Geometry, "checkpoint counter starts at 1");
+    const int L = spec.num_layers;
+    if (cfg.kind == StrategyKind::Full) return enumerate_modules(spec);
+    std::set<ModuleId> pick;
+    if (cfg.kind == StrategyKind::Parity) {
+        // odd counters: even layers + norm + lm_head; even counters: odd layers + embed
+        const bool odd = counter % 2 == 1;
+        for (int i = odd ? 0 : 1; i < L; i += 2) pick.insert(ModuleId::transformer_layer(i));
+        if (odd) {
+            pick.insert(ModuleId::norm());
+            if (!spec.weight_tied) pick.insert(ModuleId::lm_head());
+        } else {
+            pick.insert(ModuleId::embed_tokens());
+        }
+    } else {
+        for (int i = 0; i < cfg.head_count; ++i) pick.insert(ModuleId::transformer_layer(i));
+        for (int i = L - cfg.tail_count; i < L; ++i) pick.insert(ModuleId::transformer_layer(i));
+        pick.insert(ModuleId::norm());
+        if (counter % cfg.sparse_multiple == 0) {
+            const std::int64_t multiple = counter / cfg.sparse_multiple;
+            const int lo = cfg.head_count, hi = L - cfg.tail_count; // middle [lo, hi)
+            const int lower = (hi - lo + 1) / 2;
+            if (multiple % 2 == 1) {
+                for (int i = lo; i < lo + lower; ++i) pick.insert(ModuleId::transformer_layer(i));
+                pick.insert(ModuleId::embed_tokens());
+            } else {
+                for (int i = lo + lower; i < hi; ++i) pick.insert(ModuleId::transformer_layer(i));
+                if (!spec.weight_tied) pick.insert(ModuleId::lm_head());
+            }
+        }
+    }
+    std::vector<ModuleId> out;
+    for (const auto& m : enumerate_modules(spec))
+        if (pick.count(m)) out.push_back(m);
+    return out;
+}
+
+struct DeviceTrainer::Rank {
+    DeviceBuffer part, groups, slices, grad_part, delta_part;
+    std::uint32_t ngroups = 0;
+    std::uint64_t total = 0;
+    unsigned grid = 0;
+    // in-situ scorer state
+    DeviceBuffer kept, keep_segs, score_out;
+    std::uint32_t nkeep = 0;
+    std::uint64_t kept_bytes = 0;
+    std::unique_ptr<ScorePlan> plan;
+};
+
+namespace {
+
+std::uint64_t align16(std::uint64_t x) { return (x + 15) & ~15ull; }
+
+void write_container_file(const fs::path& path, const ContainerLayout& lay, const std::vector<std::uint8_t>& payload) {
+    std::ofstream out(path, std::ios::binary | std::ios::trunc);
+    if (!out) fail(ErrorKind::Storage, "cannot create '" + path.string() + "'");
+    const std::string prefix = lay.prefix();
+    out.write(prefix.data(), static_cast<std::streamsize>(prefix.size()));
+    out.write(reinterpret_cast<const char*>(payload.data()), static_cast<std::streamsize>(lay.payload_bytes));
+    out.flush();
+    if (!out) fail(ErrorKind::Storage, "write failed for '" + path.string() + "'");
+}
+
+} // namespace
+
+DeviceTrainer::DeviceTrainer(const ModelSpec& spec, int num_ranks, const AdamHyperparams& base, int device)
+    : model_(spec), N_(num_ranks), base_(base) {
+    base_.validate();
+    if (num_ranks < 1) fail(ErrorKind::Recipe, "num_ranks must be >= 1");
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+    full_ = checkpoint_layout(model_, N_, model_.modules());
+    const ShardGeometry geom{N_};
+    std::vector<const std::uint8_t*> ptrs;
+    for (int r = 0; r < N_; ++r) {
+        auto rk = std::make_unique<Rank>();
+        const ContainerLayout& lay = full_.shards[static_cast<std::size_t>(r)];
+        rk->part.resize(std::max<std::uint64_t>(16, lay.payload_bytes));
+        cuda_check(cudaMemsetAsync(rk->part.get(), 0, lay.payload_bytes, stream_), "memset");
+        std::vector<dev::TrainGroup> tg;
+        std::vector<dev::SynthGroup> sg;
+        std::vector<dev::SynthSlice> sl;
+        std::uint64_t begin = 0;
+        for (int g = 0; g < model_.table().group_count(); ++g) {
+            const std::int64_t len = model_.table().groups[static_cast<std::size_t>(g)].element_count;
+            const std::uint64_t chunk = static_cast<std::uint64_t>(geom.shard_length(len));
+            const std::uint32_t sb = static_cast<std::uint32_t>(sl.size());
+            for (const auto& s : model_.slices(g)) sl.push_back({s.group_offset, s.model_offset, s.decl.numel()});
+            const std::uint64_t om = lay.find(shard_key(g, ".exp_avg"))->begin, ov = lay.find(shard_key(g, ".exp_avg_sq"))->begin,
+                                ow = lay.find(shard_key(g, ".master"))->begin;
+            if (chunk == 0) continue;
+            tg.push_back({begin, chunk, static_cast<std::uint64_t>(r) * chunk, static_cast<std::uint64_t>(len), om, ov, ow, sb,
+                          static_cast<std::uint32_t>(model_.slices(g).size()), static_cast<std::uint32_t>(g), 0});
+            dev::SynthGroup s{};
+            s.begin = begin;
+            s.chunk = chunk;
+            s.group_first = static_cast<std::uint64_t>(r) * chunk;
+            s.true_len = static_cast<std::uint64_t>(len);
+            s.off[0] = ~0ull; // exp_avg / exp_avg_sq start at zero (memset)
+            s.off[1] = ~0ull;
+            s.off[2] = ow;
+            s.slice_begin = sb;
+            s.slice_count = static_cast<std::uint32_t>(model_.slices(g).size());
+            s.module = static_cast<std::uint32_t>(model_.owner_index(g));
+            sg.push_back(s);
+            begin += chunk;
+        }
+        rk->ngroups = static_cast<std::uint32_t>(tg.size());
+        rk->total = begin;
+        rk->groups.upload(tg.data(), tg.size() * sizeof(dev::TrainGroup));
+        rk->slices.upload(sl.data(), sl.size() * sizeof(dev::SynthSlice));
+        rk->grid = dev::adamw_grid(begin);
+        rk->grad_part.resize(rk->grid * sizeof(double));
+        rk->delta_part.resize(rk->grid * sizeof(double));
+        // W_0 = 0.02 * u(seed, 0, e) (init_state, R/src/gradients.cpp:51-66): the
+        // generator with k1 = 0 writes exactly the initial masters.
+        DeviceBuffer sgb;
+        sgb.upload(sg.data(), sg.size() * sizeof(dev::SynthGroup));
+        dev::OutPtrs outs{};
+        outs.p[0] = rk->part.get();
+        cuda_check(dev::launch_synth_shard(sgb.get<dev::SynthGroup>(), static_cast<std::uint32_t>(sg.size()),
+                                           rk->slices.get<dev::SynthSlice>(), nullptr, model_.module_count(),
+                                           model_.spec().seed, 0, 0, outs, begin, stream_),
+                   "init masters");
+        cuda_check(cudaStreamSynchronize(stream_), "sync");
+        ptrs.push_back(rk->part.get());
+        ranks_.push_back(std::move(rk));
+    }
+    part_ptrs_.upload(ptrs.data(), ptrs.size() * sizeof(void*));
+    flag_.resize(sizeof(unsigned int));
+    coef_.resize(static_cast<std::size_t>(model_.table().group_count()) * sizeof(dev::AdamCoef));
+}
+
+DeviceTrainer::~DeviceTrainer() {
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+std::pair<double, double> DeviceTrainer::step(std::int64_t s) {
+    const dev::TrainParams p{model_.spec().seed, static_cast<std::uint64_t>(s), 0.05f, 0.01f};
+    cuda_check(cudaMemsetAsync(flag_.get(), 0, sizeof(unsigned int), stream_), "memset");
+    for (auto& rk : ranks_)
+        cuda_check(dev::launch_grad_check(rk->groups.get<dev::TrainGroup>(), rk->ngroups, rk->slices.get<dev::SynthSlice>(),
+                                          rk->part.get(), rk->total, p, rk->grad_part.get<double>(),
+                                          flag_.get<unsigned int>(), stream_),
+                   "grad check");
+    unsigned int bad = 0;
+    cuda_check(cudaMemcpyAsync(&bad, flag_.get(), sizeof(bad), cudaMemcpyDeviceToHost, stream_), "D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+    if (bad) fail(ErrorKind::NonFinite, "non-finite gradient at step " + std::to_string(s));
+    t_ += 1;
+    std::vector<dev::AdamCoef> coef(static_cast<std::size_t>(model_.table().group_count()));
+    for (const auto& g : model_.table().groups) {
+        const AdamHyperparams h = hyper_for_class(base_, g.decay);
+        dev::AdamCoef& c = coef[static_cast<std::size_t>(g.index)];
+        c.b1 = static_cast<float>(h.beta1);
+        c.one_minus_b1 = static_cast<float>(1.0 - h.beta1);
+        c.b2 = static_cast<float>(h.beta2);
+        c.one_minus_b2 = static_cast<float>(1.0 - h.beta2);
+        c.bias1 = static_cast<float>(1.0 - std::pow(h.beta1, static_cast<double>(t_)));
+        c.bias2 = static_cast<float>(1.0 - std::pow(h.beta2, static_cast<double>(t_)));
+        c.lr = static_cast<float>(h.lr);
+        c.eps = static_cast<float>(h.eps);
+        c.wd = static_cast<float>(h.weight_decay);
+    }
+    cuda_check(cudaMemcpyAsync(coef_.get(), coef.data(), coef.size() * sizeof(dev::AdamCoef), cudaMemcpyHostToDevice, stream_),
+               "coef");
+    for (auto& rk : ranks_)
+        cuda_check(dev::launch_adamw(rk->groups.get<dev::TrainGroup>(), rk->ngroups, rk->slices.get<dev::SynthSlice>(),
+                                     coef_.get<dev::AdamCoef>(), rk->part.get(), rk->total, p, rk->delta_part.get<double>(),
+                                     stream_),
+                   "adamw");
+    double g2 = 0.0, d2 = 0.0;
+    std::vector<double> h;
+    for (auto& rk : ranks_) {
+        h.resize(2 * rk->grid);
+        cuda_check(cudaMemcpyAsync(h.data(), rk->grad_part.get(), rk->grid * sizeof(double), cudaMemcpyDeviceToHost, stream_), "D2H");
+        cuda_check(cudaMemcpyAsync(h.data() + rk->grid, rk->delta_part.get(), rk->grid * sizeof(double), cudaMemcpyDeviceToHost,
+                                   stream_),
+                   "D2H");
+        cuda_check(cudaStreamSynchronize(stream_), "sync");
+        for (unsigned b = 0; b < rk->grid; ++b) {
+            g2 += h[b];
+            d2 += h[rk->grid + b];
+        }
+    }
+    return {std::sqrt(g2), std::sqrt(d2)};
+}
+
+void DeviceTrainer::save(const fs::path& dir, const TrainerMeta& meta, const std::vector<ModuleId>& modules,
+                         const std::string& label) {
+    const CheckpointLayout lay = checkpoint_layout(model_, N_, modules);
+    const ShardGeometry geom{N_};
+    std::error_code ec;
+    fs::create_directories(dir / "optim", ec);
+    if (ec) fail(ErrorKind::Storage, "cannot create '" + dir.string() + "': " + ec.message());
+    // weights: K8 from the sharded masters
+    std::map<std::string, std::pair<int, std::int64_t>> where;
+    for (const auto& g : model_.table().groups)
+        for (const auto& s : model_.slices(g.index)) where[s.decl.name] = {g.index, s.group_offset};
+    std::vector<dev::WeightTensor> wt;
+    std::uint64_t begin = 0;
+    for (const auto& e : lay.weights.entries) {
+        const auto [g, goff] = where.at(e.name);
+        const std::uint64_t chunk = static_cast<std::uint64_t>(geom.shard_length(model_.table().groups[static_cast<std::size_t>(g)].element_count));
+        wt.push_back({begin, e.begin, static_cast<std::uint64_t>(goff), chunk, full_.shards[0].find(shard_key(g, ".master"))->begin});
+        begin += e.bytes() / 2;
+    }
+    std::uint64_t most = lay.weights.payload_bytes;
+    for (const auto& c : lay.shards) most = std::max(most, c.payload_bytes);
+    DeviceBuffer out(std::max<std::uint64_t>(16, most)), wtab, segs;
+    std::vector<std::uint8_t> host(most);
+    wtab.upload(wt.data(), wt.size() * sizeof(dev::WeightTensor));
+    cuda_check(dev::launch_derive_weights(wtab.get<dev::WeightTensor>(), static_cast<std::uint32_t>(wt.size()),
+                                          part_ptrs_.get<const std::uint8_t*>(), out.get(), begin, stream_),
+               "derive weights");
+    cuda_check(cudaMemcpyAsync(host.data(), out.get(), lay.weights.payload_bytes, cudaMemcpyDeviceToHost, stream_), "D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+    write_container_file(weights_path(dir), lay.weights, host);
+    // shards: the kept groups' fields gathered (K2) out of the full partitions
+    const bool complete = lay.groups.size() == static_cast<std::size_t>(model_.table().group_count());
+    for (int r = 0; r < N_; ++r) {
+        const ContainerLayout& sl = lay.shards[static_cast<std::size_t>(r)];
+        const std::uint8_t* src = ranks_[static_cast<std::size_t>(r)]->part.get();
+        if (complete) {
+            cuda_check(cudaMemcpyAsync(host.data(), src, sl.payload_bytes, cudaMemcpyDeviceToHost, stream_), "D2H");
+        } else {
+            std::vector<dev::GatherSeg> gs;
+            const ContainerLayout& fl = full_.shards[static_cast<std::size_t>(r)];
+            for (const auto& e : sl.entries) gs.push_back({src + fl.find(e.name)->begin, e.begin, e.bytes()});
+            segs.upload(gs.data(), gs.size() * sizeof(dev::GatherSeg));
+            cuda_check(dev::launch_gather(segs.get<dev::GatherSeg>(), static_cast<std::uint32_t>(gs.size()), out.get(),
+                                          sl.payload_bytes, dev::kGatherLsu, false, stream_),
+                       "gather");
+            cuda_check(cudaMemcpyAsync(host.data(), out.get(), sl.payload_bytes, cudaMemcpyDeviceToHost, stream_), "D2H");
+        }
+        cuda_check(cudaStreamSynchronize(stream_), "sync");
+        write_container_file(shard_path(dir, r), sl, host);
+    }
+    std::map<int, AdamHyperparams> hyp;
+    for (int g : lay.groups) hyp[g] = hyper_for_class(base_, model_.table().groups[static_cast<std::size_t>(g)].decay);
+    SaveManifest man;
+    man.step = meta.step;
+    man.strategy = label;
+    man.modules = modules;
+    write_text_file(optim_meta_path(dir), render_optim_meta_json(make_optim_meta(model_.table(), hyp, geom, meta.optimizer_t)));
+    write_text_file(config_path(dir), render_config_json(model_.spec()));
+    write_text_file(trainer_state_path(dir), render_trainer_state_json(meta));
+    write_text_file(manifest_path(dir), render_manifest_json(man));
+}
+
+void DeviceTrainer::keep_masters() {
+    const auto fields = score_fields(model_, N_);
+    for (int r = 0; r < N_; ++r) {
+        Rank& rk = *ranks_[static_cast<std::size_t>(r)];
+        const ContainerLayout& fl = full_.shards[static_cast<std::size_t>(r)];
+        if (!rk.plan) {
+            std::vector<dev::GatherSeg> gs;
+            std::vector<std::vector<std::uint64_t>> offs(2);
+            std::uint64_t at = 0;
+            for (const auto& f : fields) {
+                const Entry* e = fl.find(shard_key(f.group, ".master"));
+                gs.push_back({rk.part.get() + e->begin, at, e->bytes()});
+                offs[0].push_back(at);
+                offs[1].push_back(e->begin);
+                at = align16(at + e->bytes());
+            }
+            rk.kept_bytes = at;
+            rk.kept.resize(std::max<std::uint64_t>(16, at));
+            // zero the alignment gaps once; the gather never writes them
+            cuda_check(cudaMemsetAsync(rk.kept.get(), 0, std::max<std::uint64_t>(16, at), stream_), "memset");
+            rk.keep_segs.upload(gs.data(), gs.size() * sizeof(dev::GatherSeg));
+            rk.nkeep = static_cast<std::uint32_t>(gs.size());
+            rk.plan = std::make_unique<ScorePlan>(model_, N_, std::move(offs));
+            rk.score_out.resize(static_cast<std::size_t>(model_.module_count()) * 2 * sizeof(double));
+        }
+        cuda_check(dev::launch_gather(rk.keep_segs.get<dev::GatherSeg>(), rk.nkeep, rk.kept.get(), rk.kept_bytes,
+                                      dev::kGatherLsu, false, stream_),
+                   "keep masters");
+    }
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+}
+
+std::vector<std::pair<double, double>> DeviceTrainer::score_against_kept() {
+    const int M = model_.module_count();
+    std::vector<std::pair<double, double>> sums(static_cast<std::size_t>(M), {0.0, 0.0});
+    std::vector<double> h(static_cast<std::size_t>(M) * 2);
+    for (auto& rk : ranks_) { // rank order == canonical chunk order
+        if (!rk->plan) fail(ErrorKind::Consistency, "score_against_kept before keep_masters");
+        const std::uint8_t* bases[2] = {rk->kept.get(), rk->part.get()};
+        rk->plan->run(bases, rk->score_out.get<double>(), stream_);
+        cuda_check(cudaMemcpyAsync(h.data(), rk->score_out.get(), h.size() * sizeof(double), cudaMemcpyDeviceToHost, stream_),
+                   "D2H");
+        cuda_check(cudaStreamSynchronize(stream_), "sync");
+        for (int m = 0; m < M; ++m) {
+            sums[static_cast<std::size_t>(m)].first += h[static_cast<std::size_t>(m) * 2];
+            sums[static_cast<std::size_t>(m)].second += h[static_cast<std::size_t>(m) * 2 + 1];
+        }
+    }
+    return sums;
+}
+
+std::vector<fs::path> device_train(const DeviceTrainConfig& cfg, const fs::path& out_dir) {
+    cfg.spec.validate();
+    validate_strategy(cfg.strategy, cfg.spec);
+    cfg.hyper.validate();
+    if (cfg.total_steps < 0) fail(ErrorKind::Recipe, "total_steps must be >= 0");
+    std::error_code ec;
+    if (fs::exists(out_dir) && !fs::is_empty(out_dir, ec))
+        fail(ErrorKind::Storage, "refusing to write into non-empty directory '" + out_dir.string() + "'");
+    fs::create_directories(out_dir, ec);
+    if (ec) fail(ErrorKind::Storage, "cannot create '" + out_dir.string() + "': " + ec.message());
+    DeviceTrainer tr(cfg.spec, cfg.num_ranks, cfg.hyper, cfg.device);
+    std::ofstream log(out_dir / "log.jsonl", std::ios::binary);
+    if (!log) fail(ErrorKind::Storage, "cannot create log in '" + out_dir.string() + "'");
+    TrainerMeta meta;
+    meta.lr = cfg.hyper.lr;
+    meta.strategy = cfg.strategy;
+    meta.rng_seed = cfg.spec.seed;
+    const int M = tr.model().module_count();
+    std::vector<fs::path> saved;
+    for (std::int64_t s = 1; s <= cfg.total_steps; ++s) {
+        const auto [gn, un] = tr.step(s);
+        log << nlohmann::json{{"grad_norm", gn}, {"step", s}, {"update_norm", un}}.dump() << "\n";
+        meta.step = s;
+        meta.optimizer_t = tr.optimizer_t();
+        if (s % cfg.strategy.interval != 0) continue;
+        meta.checkpoint_counter = s / cfg.strategy.interval;
+        std::vector<ModuleId> mods;
+        if (!cfg.magnitude) {
+            mods = modules_to_save(cfg.strategy, cfg.spec, meta.checkpoint_counter);
+        } else if (meta.checkpoint_counter == 1) {
+            mods = enumerate_modules(cfg.spec); // S_1 holds the complete state
+        } else {
+            const auto sums = tr.score_against_kept(); // r_k = score(S_{k-1} -> S_k), in situ
+            std::vector<double> row(static_cast<std::size_t>(M));
+            for (int m = 0; m < M; ++m) row[static_cast<std::size_t>(m)] = magnitude_score(sums[static_cast<std::size_t>(m)].first, sums[static_cast<std::size_t>(m)].second);
+            const Selection sel = select_by_magnitude({row}, M, cfg.rho);
+            for (int m : sel.saved[1]) mods.push_back(tr.model().modules()[static_cast<std::size_t>(m)]);
+        }
+        const fs::path dir = out_dir / checkpoint_dir_name(s);
+        tr.save(dir, meta, mods, cfg.magnitude ? "magnitude" : strategy_kind_name(cfg.strategy.kind));
+        if (cfg.magnitude) tr.keep_masters();
+        saved.push_back(dir);
+    }
+    log.flush();
+    if (!log) fail(ErrorKind::Storage, "log write failed");
+    return saved;
+}
+
+} // namespace tailor

@@ -86,6 +86,10 @@ __global__ void synth_shard_kernel(const SynthGroup* __restrict__ groups, std::u
         while (s + 1 < g.slice_begin + g.slice_count && static_cast<std::int64_t>(go) >= slices[s + 1].group_offset) ++s;
         const std::uint64_t e = static_cast<std::uint64_t>(slices[s].model_offset + (static_cast<std::int64_t>(go) - slices[s].group_offset));
         float w = __fmul_rn(0.02f, unit_noise(seed, 0, e));
+        if (k1 == 0) { // initial state only (the trainer's init_state)
+            if (g.off[2] != ~0ULL) reinterpret_cast<float*>(outs.p[0] + g.off[2])[i] = w;
+            continue;
+        }
         for (int j = 1; j <= k1; ++j) {
             w = master_step(w, sigma, M, g.module, seed, j, e);
             if (j < k0) continue;

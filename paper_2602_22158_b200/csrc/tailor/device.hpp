@@ -118,6 +118,48 @@ struct VerifyRange {
 cudaError_t launch_verify(const VerifyPair* d_pairs, std::uint32_t npairs, const VerifyRange* d_ranges,
                           std::uint32_t nranges, unsigned long long* d_err, cudaStream_t stream);
 
+// ---- K7: AdamW step over rank partitions ------------------------
+struct TrainGroup {
+    std::uint64_t begin;       // first virtual element of this group in the partition
+    std::uint64_t chunk;
+    std::uint64_t group_first; // rank * chunk
+    std::uint64_t true_len;
+    std::uint64_t off_m, off_v, off_w; // payload byte offsets of exp_avg, exp_avg_sq, master
+    std::uint32_t slice_begin;
+    std::uint32_t slice_count;
+    std::uint32_t coef; // index into the AdamCoef table
+    std::uint32_t pad;
+};
+// Per-group FP32 coefficients, each rounded once from FP64 (R/src/adamw.cpp:19-27).
+struct AdamCoef {
+    float b1, one_minus_b1, b2, one_minus_b2, bias1, bias2, lr, eps, wd, pad[3];
+};
+struct TrainParams {
+    std::uint64_t seed;
+    std::uint64_t step;
+    float state_coeff; // GradientSource c1 (R/include/tailor/gradients.hpp:20-24)
+    float noise_coeff; // c2
+};
+cudaError_t launch_grad_check(const TrainGroup* d_groups, std::uint32_t ngroups, const SynthSlice* d_slices,
+                              const std::uint8_t* d_part, std::uint64_t total, const TrainParams& p,
+                              double* d_grad_partials, unsigned int* d_nonfinite, cudaStream_t s);
+cudaError_t launch_adamw(const TrainGroup* d_groups, std::uint32_t ngroups, const SynthSlice* d_slices,
+                         const AdamCoef* d_coef, std::uint8_t* d_part, std::uint64_t total, const TrainParams& p,
+                         double* d_delta_partials, cudaStream_t s);
+unsigned adamw_grid(std::uint64_t total);
+
+// ---- K8: bf16 weights derived from sharded masters ---------------------------------
+struct WeightTensor {
+    std::uint64_t begin;        // first virtual element
+    std::uint64_t dst_off;      // byte offset in the weights payload
+    std::uint64_t group_offset; // tensor's first element within its group
+    std::uint64_t chunk;        // group's shard length
+    std::uint64_t master_off;   // byte offset of the group's master field in every rank payload
+};
+cudaError_t launch_derive_weights(const WeightTensor* d_tensors, std::uint32_t ntensors,
+                                  const std::uint8_t* const* d_parts, std::uint8_t* d_out, std::uint64_t total,
+                                  cudaStream_t s);
+
 int sm_count();
 
 } // namespace tailor::dev

@@ -1,0 +1,69 @@
+// Device-resident trainer over ZeRO rank partitions: the
+// reference's deterministic toy trainer (R/src/trainer.cpp:26-123) with the
+// state living in HBM in checkpoint-payload layout, AdamW on the device (K7,
+// bit-exact), and checkpoints written straight from the partitions. It adds the
+// update-magnitude strategy at training time: at every checkpoint the current
+// masters are scored against the previous checkpoint's (K3, in-situ) and only
+// the top-rho modules are saved — the selective checkpointing that
+// recipe_from_manifests + execute_merge later recover from.
+#pragma once
+
+#include <filesystem>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "tailor/checkpoint.hpp"
+#include "tailor/engine.hpp"
+
+namespace tailor {
+
+// R/src/strategy.cpp:48-91 (full / parity / filter schedules).
+std::vector<ModuleId> modules_to_save(const StrategyConfig& cfg, const ModelSpec& spec, std::int64_t counter);
+void validate_strategy(const StrategyConfig& cfg, const ModelSpec& spec);
+
+struct DeviceTrainConfig {
+    ModelSpec spec;
+    StrategyConfig strategy;
+    int total_steps = 0;
+    int num_ranks = 1;
+    AdamHyperparams hyper; // base; weight_decay applies to decay groups
+    bool magnitude = false; // update-magnitude selective checkpointing (label "magnitude")
+    double rho = 0.5;
+    int device = 0;
+};
+
+class DeviceTrainer {
+  public:
+    DeviceTrainer(const ModelSpec& spec, int num_ranks, const AdamHyperparams& base, int device);
+    ~DeviceTrainer();
+    // One train_step at training step `step` (R/src/trainer.cpp:26-35): returns
+    // {grad_norm, update_norm}. Throws NonFinite before touching the state.
+    std::pair<double, double> step(std::int64_t step);
+    std::int64_t optimizer_t() const { return t_; }
+    // write_checkpoint of the given module subset (R/src/trainer.cpp:60-79).
+    void save(const std::filesystem::path& dir, const TrainerMeta& meta, const std::vector<ModuleId>& modules,
+              const std::string& label);
+    // In-situ scorer: keep a device copy of the current masters; score the
+    // current state against the kept copy -> per module (sum d^2, sum ref^2).
+    void keep_masters();
+    std::vector<std::pair<double, double>> score_against_kept();
+    const ModelLayout& model() const { return model_; }
+
+  private:
+    struct Rank;
+    ModelLayout model_;
+    int N_;
+    AdamHyperparams base_;
+    CheckpointLayout full_;
+    std::vector<std::unique_ptr<Rank>> ranks_;
+    DeviceBuffer coef_, part_ptrs_, flag_;
+    std::int64_t t_ = 0;
+    cudaStream_t stream_ = nullptr;
+};
+
+// The reference's train() (R/src/trainer.cpp:109-123) on the device: same run
+// directory layout, checkpoints byte-identical for full/parity/filter.
+std::vector<std::filesystem::path> device_train(const DeviceTrainConfig& cfg, const std::filesystem::path& out_dir);
+
+} // namespace tailor

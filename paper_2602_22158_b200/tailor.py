@@ -26,7 +26,7 @@ from ._lib import (ErrorKind, GatherSegC, MergeOptionsC, MergeStatsC, ModelSpecC
 
 __all__ = ["ErrorKind", "TailorError", "ModelSpec", "RecipeSlice", "MergeRecipe", "MergeOptions", "MergeStats",
            "parse_recipe", "recipe_to_yaml", "resolve_plan", "execute_merge", "recipe_from_manifests",
-           "verify_checkpoint", "regroup", "score_snapshots", "select_recipe", "layer_map", "SynthFamily", "Scorer",
+           "verify_checkpoint", "regroup", "train", "score_snapshots", "select_recipe", "layer_map", "SynthFamily", "Scorer",
            "MergePartition", "gather"]
 
 
@@ -150,6 +150,25 @@ def regroup(src_dir: str, out_dir: str, to_fine: bool = True, options: Optional[
     check(lib().tg_regroup(_b(str(src_dir)), _b(str(out_dir)), 1 if to_fine else 0, ctypes.byref(copt),
                            ctypes.byref(st)))
     return MergeStats(st.shard_files_read, st.weight_files_read, st.wall_ms, st.device_ms, st.bytes_moved)
+
+
+STRATEGIES = {"full": 0, "parity": 1, "filter": 2, "magnitude": 3}
+
+
+def train(spec: ModelSpec, out_dir: str, steps: int, interval: int = 50, strategy: str = "full", num_ranks: int = 1,
+          lr: float = 1e-3, weight_decay: float = 0.01, head: int = 2, tail: int = 2, sparse_multiple: int = 5,
+          rho: float = 0.5, device: int = 0) -> int:
+    """Device-resident train() (R/src/trainer.cpp:109-123) -> number of checkpoints written.
+    strategy 'magnitude' saves all modules at the first checkpoint, then the top-rho by
+    update magnitude against the previous checkpoint (scored in situ)."""
+    from ._lib import TrainConfigC
+
+    c = spec.to_c()
+    cfg = TrainConfigC(steps, num_ranks, interval, STRATEGIES[strategy], head, tail, sparse_multiple, device, lr,
+                       weight_decay, rho)
+    n = ctypes.c_int32(0)
+    check(lib().tg_train(ctypes.byref(c), ctypes.byref(cfg), _b(str(out_dir)), ctypes.byref(n)))
+    return n.value
 
 
 def verify_checkpoint(path: str, device: int = 0) -> None:
