@@ -350,7 +350,8 @@ def our_arm(args, rank, world, local_rank):
                    "unit_of_work": "one ZeRO rank partition per GPU (optimizer shard + weights share)",
                    "composite_bytes_per_gpu_step": composite, "parallelism": f"zero-partition x{world}",
                    "l2": "inputs 62 GB/GPU >> 126 MB L2 (no flush needed)",
-                   "gather_variant": {0: "auto", 1: "lsu", 2: "bulk"}[args.variant],
+                   "gather_variant": {0: "auto", 1: "lsu", 2: "bulk-4x48K", 3: "bulk-6x32K", 4: "bulk-2cta-3x32K",
+                                      5: "bulk-3x64K", 6: "bulk-8x24K"}[args.variant],
                    "score_variant": SCORE_VARIANTS[args.score_variant],
                    "plan_ms_uncached": round(plan_ms, 3), "min_boundary_gap": state["gap"]},
         "layers_scored_per_s": round(scores_per_s, 1),

@@ -127,23 +127,24 @@ __global__ void __launch_bounds__(kLsuThreads) gather_lsu_kernel(const GatherSeg
 // ---- TMA bulk path -----------------------------------------------------------
 using namespace tma;
 
-__global__ void __launch_bounds__(32, 1) gather_bulk_kernel(const GatherSeg* __restrict__ segs, std::uint32_t nseg,
-                                                             std::uint8_t* __restrict__ dst, std::uint64_t dst_bytes) {
+template <int STAGES, std::uint32_t STAGE>
+__global__ void __launch_bounds__(32) gather_bulk_kernel(const GatherSeg* __restrict__ segs, std::uint32_t nseg,
+                                                          std::uint8_t* __restrict__ dst, std::uint64_t dst_bytes) {
     extern __shared__ __align__(128) std::uint8_t smem[];
-    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kBulkStages * kBulkStage);
+    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + STAGES * STAGE);
     if (threadIdx.x != 0) return; // one thread drives the copy engine
-    for (int s = 0; s < kBulkStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
     fence_barrier_init();
 
-    const std::uint64_t ntiles = (dst_bytes + kBulkStage - 1) / kBulkStage;
+    const std::uint64_t ntiles = (dst_bytes + STAGE - 1) / STAGE;
     const std::uint64_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
-    const auto tile_lo = [&](std::uint64_t i) { return (blockIdx.x + i * gridDim.x) * static_cast<std::uint64_t>(kBulkStage); };
+    const auto tile_lo = [&](std::uint64_t i) { return (blockIdx.x + i * gridDim.x) * static_cast<std::uint64_t>(STAGE); };
     const auto issue_load = [&](std::uint64_t i) {
-        const int stage = static_cast<int>(i % kBulkStages);
+        const int stage = static_cast<int>(i % STAGES);
         const std::uint64_t lo = tile_lo(i);
-        const std::uint64_t hi = min(lo + kBulkStage, dst_bytes);
-        std::uint8_t* buf = smem + stage * kBulkStage;
+        const std::uint64_t hi = min(lo + STAGE, dst_bytes);
+        std::uint8_t* buf = smem + stage * STAGE;
         mbar_arrive_expect_tx(&bars[stage], static_cast<std::uint32_t>(hi - lo));
         std::uint64_t at = lo;
         for (int s = seg_lookup(segs, nseg, lo); at < hi && s < static_cast<int>(nseg); ++s) {
@@ -156,16 +157,16 @@ __global__ void __launch_bounds__(32, 1) gather_bulk_kernel(const GatherSeg* __r
         }
     };
 
-    const std::uint64_t prologue = mine < kBulkStages - 1 ? mine : static_cast<std::uint64_t>(kBulkStages - 1);
+    const std::uint64_t prologue = mine < STAGES - 1 ? mine : static_cast<std::uint64_t>(STAGES - 1);
     for (std::uint64_t i = 0; i < prologue; ++i) issue_load(i);
     for (std::uint64_t i = 0; i < mine; ++i) {
-        const int stage = static_cast<int>(i % kBulkStages);
-        mbar_wait_parity(&bars[stage], static_cast<std::uint32_t>((i / kBulkStages) & 1));
+        const int stage = static_cast<int>(i % STAGES);
+        mbar_wait_parity(&bars[stage], static_cast<std::uint32_t>((i / STAGES) & 1));
         const std::uint64_t lo = tile_lo(i);
-        const std::uint64_t hi = min(lo + kBulkStage, dst_bytes);
-        bulk_store(dst + lo, smem + stage * kBulkStage, static_cast<std::uint32_t>(hi - lo));
+        const std::uint64_t hi = min(lo + STAGE, dst_bytes);
+        bulk_store(dst + lo, smem + stage * STAGE, static_cast<std::uint32_t>(hi - lo));
         bulk_commit();
-        const std::uint64_t next = i + kBulkStages - 1; // lands in tile i-1's stage
+        const std::uint64_t next = i + STAGES - 1; // lands in tile i-1's stage
         if (next < mine) {
             if (i >= 1) bulk_wait_read_1(); // store of tile i-1 has finished reading smem
             issue_load(next);
@@ -174,9 +175,25 @@ __global__ void __launch_bounds__(32, 1) gather_bulk_kernel(const GatherSeg* __r
     bulk_wait_all();
 }
 
+template <int STAGES, std::uint32_t STAGE>
+cudaError_t launch_bulk(const GatherSeg* d_segs, std::uint32_t nseg, std::uint8_t* d_dst, std::uint64_t dst_bytes,
+                        int ctas_per_sm, cudaStream_t stream) {
+    static bool attr = false;
+    const std::size_t smem = STAGES * STAGE + STAGES * sizeof(std::uint64_t);
+    if (!attr) {
+        const cudaError_t e = cudaFuncSetAttribute(gather_bulk_kernel<STAGES, STAGE>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const std::uint64_t tiles = (dst_bytes + STAGE - 1) / STAGE;
+    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(tiles, static_cast<std::uint64_t>(sm_count()) * ctas_per_sm));
+    gather_bulk_kernel<STAGES, STAGE><<<grid, 32, smem, stream>>>(d_segs, nseg, d_dst, dst_bytes);
+    return cudaGetLastError();
+}
+
 int g_sms = 0;
 int g_lsu_blocks_per_sm = 0;
-bool g_bulk_attr = false;
 
 } // namespace
 
@@ -194,19 +211,15 @@ cudaError_t launch_gather(const GatherSeg* d_segs, std::uint32_t nseg, std::uint
                           int variant, bool bulk_ok, cudaStream_t stream) {
     if (dst_bytes == 0 || nseg == 0) return cudaSuccess;
     const int sms = sm_count();
-    const bool bulk = variant == kGatherBulk || (variant == kGatherAuto && bulk_ok);
+    const bool bulk = variant >= kGatherBulk || (variant == kGatherAuto && bulk_ok);
     if (bulk && bulk_ok) {
-        const std::size_t smem = kBulkStages * kBulkStage + kBulkStages * sizeof(std::uint64_t);
-        if (!g_bulk_attr) {
-            const cudaError_t e =
-                cudaFuncSetAttribute(gather_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            if (e != cudaSuccess) return e;
-            g_bulk_attr = true;
+        switch (variant) { // ring shapes for experiments; auto/2 = 4 x 48 KB, one CTA per SM
+            case kGatherBulk6x32: return launch_bulk<6, 32 * 1024>(d_segs, nseg, d_dst, dst_bytes, 1, stream);
+            case kGatherBulk2Cta: return launch_bulk<3, 32 * 1024>(d_segs, nseg, d_dst, dst_bytes, 2, stream);
+            case kGatherBulk3x64: return launch_bulk<3, 64 * 1024>(d_segs, nseg, d_dst, dst_bytes, 1, stream);
+            case kGatherBulk8x24: return launch_bulk<8, 24 * 1024>(d_segs, nseg, d_dst, dst_bytes, 1, stream);
+            default: return launch_bulk<kBulkStages, kBulkStage>(d_segs, nseg, d_dst, dst_bytes, 1, stream);
         }
-        const std::uint64_t tiles = (dst_bytes + kBulkStage - 1) / kBulkStage;
-        const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(tiles, static_cast<std::uint64_t>(sms)));
-        gather_bulk_kernel<<<grid, 32, smem, stream>>>(d_segs, nseg, d_dst, dst_bytes);
-        return cudaGetLastError();
     }
     if (g_lsu_blocks_per_sm == 0) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_lsu_blocks_per_sm, gather_lsu_kernel, kLsuThreads, 0);

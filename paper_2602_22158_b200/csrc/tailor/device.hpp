@@ -20,7 +20,17 @@ struct GatherSeg {
 };
 static_assert(sizeof(GatherSeg) == 24, "GatherSeg is part of the C ABI");
 
-enum GatherVariant : int { kGatherAuto = 0, kGatherLsu = 1, kGatherBulk = 2 };
+// kGatherBulk = 4 x 48 KB ring, one CTA per SM (default); the other bulk
+// shapes exist for measured comparisons (profiles/).
+enum GatherVariant : int {
+    kGatherAuto = 0,
+    kGatherLsu = 1,
+    kGatherBulk = 2,
+    kGatherBulk6x32 = 3,
+    kGatherBulk2Cta = 4,
+    kGatherBulk3x64 = 5,
+    kGatherBulk8x24 = 6
+};
 
 // `bulk_ok` (host-checked): every segment has 16-B aligned src/dst/bytes and
 // the segments tile [0, dst_bytes) exactly — the TMA bulk path's contract.
