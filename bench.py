@@ -266,23 +266,35 @@ def our_arm(args, rank, world, local_rank):
     kt = {"score": [], "gather_shard": [], "gather_weights": []}
     state = {"yaml": None, "src": None, "gap": None}
 
+    # Default step: fully on the device — scorer (K3/K4) -> NCCL all-gather of the
+    # partials -> K9 selection + segment tables -> K2 gathers; no host round trip.
+    # --host-select: the host computes the selection and plan (D2H of the partials).
+    dstep = t.SelectStep(fam, r, r, N, rho)
+    dstep.bind([b.data_ptr() for b in shards], [b.data_ptr() for b in wbufs])
+    bases = [b.data_ptr() for b in shards]
+
     def step(record):
         e0, e1, e2, e3, e4 = ev(), ev(), ev(), ev(), ev()
         e0.record(stream)
-        scorer.run([b.data_ptr() for b in shards], partials.data_ptr(), sp)
+        scorer.run(bases, partials.data_ptr(), sp)
         e1.record(stream)
         if world > 1:
             dist.all_gather_into_tensor(gathered, partials)
-            parts = gathered.cpu()
+        allparts = gathered if world > 1 else partials
+        if args.host_select:
+            yaml, src_of, _, gap = fam.select(allparts.cpu().tolist(), world, rho)
+            state.update(yaml=yaml, src=src_of, gap=gap)
+            spl, wpl, _ = plans_for(yaml)
+            e2.record(stream)
+            spl.run(out_shard.data_ptr(), args.variant, sp)
+            e3.record(stream)
+            wpl.run(out_w.data_ptr(), args.variant, sp)
         else:
-            parts = partials.cpu()
-        yaml, src_of, _, gap = fam.select(parts.tolist(), world, rho)
-        state.update(yaml=yaml, src=src_of, gap=gap)
-        spl, wpl, _ = plans_for(yaml)
-        e2.record(stream)
-        spl.run(out_shard.data_ptr(), args.variant, sp)
-        e3.record(stream)
-        wpl.run(out_w.data_ptr(), args.variant, sp)
+            dstep.run(allparts.data_ptr(), world, out_shard.data_ptr(), out_w.data_ptr(), args.variant, sp, phases=1)
+            e2.record(stream)
+            dstep.run(allparts.data_ptr(), world, out_shard.data_ptr(), out_w.data_ptr(), args.variant, sp, phases=2)
+            e3.record(stream)
+            dstep.run(allparts.data_ptr(), world, out_shard.data_ptr(), out_w.data_ptr(), args.variant, sp, phases=4)
         e4.record(stream)
         if record is not None:
             record.append((e0, e1, e2, e3, e4))
@@ -317,6 +329,20 @@ def our_arm(args, rank, world, local_rank):
     total_bytes = composite * world * args.steps
     value = total_bytes / sec / 1e9
     scores_per_s = M * (K - 1) * args.steps / sec
+
+    # ---- the device selection must be the host's, and so must the composite ------------
+    allparts = gathered if world > 1 else partials
+    yaml_h, src_h, _, gap_h = fam.select(allparts.cpu().tolist(), world, rho)
+    select_check = None
+    if not args.host_select:
+        src_d, _ = dstep.result(sp)
+        spl_h, wpl_h, _ = plans_for(yaml_h)
+        ref_out = torch.empty_like(out_shard)
+        spl_h.run(ref_out.data_ptr(), args.variant, sp)
+        torch.cuda.synchronize(dev)
+        select_check = bool(src_d == src_h and torch.equal(ref_out, out_shard))
+        del ref_out
+    state.update(yaml=yaml_h, src=src_h, gap=gap_h)
 
     # ---- uncached plan cost, for the record ----------------------------------------
     t0 = time.perf_counter()
@@ -353,7 +379,9 @@ def our_arm(args, rank, world, local_rank):
                    "gather_variant": {0: "auto", 1: "lsu", 2: "bulk-4x48K", 3: "bulk-6x32K", 4: "bulk-2cta-3x32K",
                                       5: "bulk-3x64K", 6: "bulk-8x24K"}[args.variant],
                    "score_variant": SCORE_VARIANTS[args.score_variant],
-                   "plan_ms_uncached": round(plan_ms, 3), "min_boundary_gap": state["gap"]},
+                   "plan_ms_uncached": round(plan_ms, 3), "min_boundary_gap": state["gap"],
+                   "selection": "host (D2H partials)" if args.host_select else "device (K9, no host round trip)",
+                   "device_selection_matches_host": select_check},
         "layers_scored_per_s": round(scores_per_s, 1),
         "kernels_ms": {k: round(statistics.mean(x), 4) for k, x in kt.items()},
         "roofline": {"bound": "hbm", "kernel": "K2 gather (rank shard partition)",
@@ -363,7 +391,7 @@ def our_arm(args, rank, world, local_rank):
                      "traffic": traffic, "traffic_source": traffic_src},
         "scorer_roofline": {"achieved": round(score_achieved, 1), "peak": hbm, "unit": "GB/s",
                             "frac": round(score_achieved / hbm, 4), "bytes_per_launch": scorer.bytes_read},
-        "gpu_launches": args.steps * 4,
+        "gpu_launches": args.steps * (4 if args.host_select else 5),
         "clocks": clocks.summary(),
     }
     if e2e:
@@ -686,6 +714,7 @@ def main():
     ap.add_argument("--variant", type=int, default=0, help="gather: 0 auto, 1 LSU, 2 TMA bulk")
     ap.add_argument("--score-variant", type=int, default=0, help="scorer: 0 auto, 1 register, 2 TMA-staged")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--host-select", action="store_true", help="select + plan on the host instead of K9")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)

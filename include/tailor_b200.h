@@ -212,6 +212,21 @@ int tg_mplan_run_host(tg_mplan* p, const uint8_t* const* h_windows, const uint8_
                       uint64_t* h2d_bytes, uint64_t* d2h_bytes);
 int tg_mplan_wait(tg_mplan* p);
 
+/* Whole score -> select -> merge step on the device for one unit (rank-r shard +
+ * weights share unit/units) of a family of full snapshots: selection (a14) and both
+ * segment tables are built by a device kernel from the all-gathered per-rank partials
+ * [nranks][K-1][M][2]; no host synchronization (graph-capturable). */
+typedef struct tg_dstep tg_dstep;
+tg_dstep* tg_dstep_create(tg_family* f, int32_t rank, int32_t unit, int32_t units, double rho);
+void tg_dstep_destroy(tg_dstep* s);
+int tg_dstep_range(const tg_dstep* s, uint64_t* shard_bytes, uint64_t* weights_lo, uint64_t* weights_hi);
+int tg_dstep_bind(tg_dstep* s, const uint8_t* const* shard_bases, const uint8_t* const* weights_window_bases);
+/* phases: bitmask 1 = select + plan (K9), 2 = gather shard, 4 = gather weights (7 = all). */
+int tg_dstep_run(tg_dstep* s, const double* d_rank_partials, int32_t nranks, uint8_t* d_out_shard, uint8_t* d_out_weights,
+                 int32_t variant, int32_t phases, void* stream);
+/* Synchronous reads of the last run's selection: source_of[M] (0-based snapshot), scores[(K-1)*M]. */
+int tg_dstep_result(tg_dstep* s, int32_t* source_of, double* scores, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

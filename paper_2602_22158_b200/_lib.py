@@ -144,6 +144,12 @@ SIGNATURES = {
     "tg_mplan_run": (_I, [_P, _P, _I32, _P]),
     "tg_mplan_run_host": (_I, [_P, _PP, _PP, _U32, _P, _I32, _U64, _I32, _c.POINTER(_U64), _c.POINTER(_U64)]),
     "tg_mplan_wait": (_I, [_P]),
+    "tg_dstep_create": (_P, [_P, _I32, _I32, _I32, _D]),
+    "tg_dstep_destroy": (None, [_P]),
+    "tg_dstep_range": (_I, [_P, _c.POINTER(_U64), _c.POINTER(_U64), _c.POINTER(_U64)]),
+    "tg_dstep_bind": (_I, [_P, _PP, _PP]),
+    "tg_dstep_run": (_I, [_P, _P, _I32, _P, _P, _I32, _I32, _P]),
+    "tg_dstep_result": (_I, [_P, _c.POINTER(_I32), _c.POINTER(_D), _P]),
 }
 
 _lib = None

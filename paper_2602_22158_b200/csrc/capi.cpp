@@ -29,6 +29,9 @@ struct tg_family {
 struct tg_scorer {
     std::unique_ptr<ScorePlan> plan;
 };
+struct tg_dstep {
+    std::unique_ptr<DeviceSelectStep> step;
+};
 struct tg_mplan {
     std::unique_ptr<DeviceMerge> dev;
     std::unique_ptr<HostMerge> host;
@@ -663,6 +666,44 @@ int tg_mplan_run_host(tg_mplan* p, const uint8_t* const* h_windows, const uint8_
 int tg_mplan_wait(tg_mplan* p) {
     return guard([&] {
         if (p->host) p->host->wait();
+    });
+}
+
+tg_dstep* tg_dstep_create(tg_family* f, int32_t rank, int32_t unit, int32_t units, double rho) {
+    tg_dstep* out = nullptr;
+    guard([&] { out = new tg_dstep{std::make_unique<DeviceSelectStep>(*f->fam, rank, unit, units, rho)}; });
+    return out;
+}
+
+void tg_dstep_destroy(tg_dstep* s) { delete s; }
+
+int tg_dstep_range(const tg_dstep* s, uint64_t* shard_bytes, uint64_t* wlo, uint64_t* whi) {
+    return guard([&] {
+        if (shard_bytes) *shard_bytes = s->step->shard_bytes();
+        if (wlo) *wlo = s->step->weights_lo();
+        if (whi) *whi = s->step->weights_hi();
+    });
+}
+
+int tg_dstep_bind(tg_dstep* s, const uint8_t* const* shard_bases, const uint8_t* const* wwin_bases) {
+    return guard([&] { s->step->bind(shard_bases, wwin_bases); });
+}
+
+int tg_dstep_run(tg_dstep* s, const double* d_parts, int32_t nranks, uint8_t* d_out_shard, uint8_t* d_out_w, int32_t variant,
+                 int32_t phases, void* stream) {
+    return guard([&] {
+        s->step->run(d_parts, nranks, d_out_shard, d_out_w, variant, static_cast<cudaStream_t>(stream), phases);
+    });
+}
+
+int tg_dstep_result(tg_dstep* s, int32_t* source_of, double* scores, void* stream) {
+    return guard([&] {
+        const auto src = s->step->source_of(static_cast<cudaStream_t>(stream));
+        if (source_of) std::copy(src.begin(), src.end(), source_of);
+        if (scores) {
+            const auto sc = s->step->scores(static_cast<cudaStream_t>(stream));
+            std::copy(sc.begin(), sc.end(), scores);
+        }
     });
 }
 

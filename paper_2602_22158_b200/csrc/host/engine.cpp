@@ -594,6 +594,86 @@ void HostMerge::run(const std::vector<const std::uint8_t*>& h_windows, const std
     if (!async) wait();
 }
 
+// ---- device select + plan step ---------------------------------------------------------
+DeviceSelectStep::DeviceSelectStep(const SynthFamily& fam, int rank, int unit, int units, double rho)
+    : K_(fam.snapshots()), M_(fam.model().module_count()) {
+    if (K_ < 2 || K_ > dev::kMaxSnapshots) fail(ErrorKind::Geometry, "device selection needs 2..16 snapshots");
+    if (!(rho > 0.0 && rho <= 1.0)) fail(ErrorKind::Recipe, "selection ratio rho must lie in (0, 1]");
+    if (rank < 0 || rank >= fam.num_ranks()) fail(ErrorKind::Geometry, "rank out of range");
+    n_save_ = std::max(1, std::min(M_, static_cast<int>(std::ceil(rho * M_))));
+    for (int k = 1; k <= K_; ++k)
+        if (fam.layout(k).modules.size() != static_cast<std::size_t>(M_))
+            fail(ErrorKind::Geometry, "device selection merges full snapshots only");
+    const CheckpointLayout& lay = fam.layout(K_);
+    const ModelLayout& model = fam.model();
+    std::vector<dev::PlanEntry> se, we;
+    const ContainerLayout& sl = lay.shards[static_cast<std::size_t>(rank)];
+    for (const auto& e : sl.entries) {
+        const int g = std::stoi(e.name.substr(1, e.name.find('.') - 1));
+        se.push_back({static_cast<std::uint32_t>(model.owner_index(g)), 0, e.begin, e.begin, e.bytes()});
+    }
+    shard_bytes_ = sl.payload_bytes;
+    std::tie(wlo_, whi_) = weights_share(lay.weights, unit, units);
+    std::map<std::string, int> owner;
+    for (int m = 0; m < M_; ++m)
+        for (const auto& t : tensors_of(model.spec(), model.modules()[static_cast<std::size_t>(m)])) owner[t.name] = m;
+    for (const auto& e : lay.weights.entries)
+        if (e.begin >= wlo_ && e.end <= whi_)
+            we.push_back({static_cast<std::uint32_t>(owner.at(e.name)), 0, e.begin - wlo_, e.begin - wlo_, e.bytes()});
+    n_shard_ = static_cast<std::uint32_t>(se.size());
+    n_w_ = static_cast<std::uint32_t>(we.size());
+    bool aligned = true;
+    for (const auto* v : {&se, &we})
+        for (const auto& p : *v) aligned = aligned && p.dst_off % 16 == 0 && p.bytes % 16 == 0;
+    bulk_ = aligned;
+    shard_entries_.upload(se.data(), se.size() * sizeof(dev::PlanEntry));
+    w_entries_.upload(we.data(), we.size() * sizeof(dev::PlanEntry));
+    shard_segs_.resize(std::max<std::size_t>(1, se.size()) * sizeof(dev::GatherSeg));
+    w_segs_.resize(std::max<std::size_t>(1, we.size()) * sizeof(dev::GatherSeg));
+    source_.resize(static_cast<std::size_t>(M_) * sizeof(int));
+    scores_.resize(static_cast<std::size_t>(M_) * (K_ - 1) * sizeof(double));
+}
+
+void DeviceSelectStep::bind(const std::uint8_t* const* shard_bases, const std::uint8_t* const* wwin_bases) {
+    for (int k = 0; k < K_; ++k) {
+        bases_.shard[k] = shard_bases[k];
+        bases_.weights[k] = wwin_bases[k];
+        bulk_ = bulk_ && reinterpret_cast<std::uintptr_t>(shard_bases[k]) % 16 == 0 &&
+                reinterpret_cast<std::uintptr_t>(wwin_bases[k]) % 16 == 0;
+    }
+}
+
+void DeviceSelectStep::run(const double* d_parts, int nranks, std::uint8_t* d_out_shard, std::uint8_t* d_out_w, int variant,
+                           cudaStream_t s, int phases) {
+    if (phases & kPhaseSelect)
+        cuda_check(dev::launch_select_plan(d_parts, nranks, K_, M_, n_save_, shard_entries_.get<dev::PlanEntry>(), n_shard_,
+                                           w_entries_.get<dev::PlanEntry>(), n_w_, bases_, shard_segs_.get<dev::GatherSeg>(),
+                                           w_segs_.get<dev::GatherSeg>(), source_.get<int>(), scores_.get<double>(), s),
+                   "select plan");
+    const bool ok_s = bulk_ && reinterpret_cast<std::uintptr_t>(d_out_shard) % 16 == 0;
+    const bool ok_w = bulk_ && reinterpret_cast<std::uintptr_t>(d_out_w) % 16 == 0;
+    if (phases & kPhaseShard)
+        cuda_check(dev::launch_gather(shard_segs_.get<dev::GatherSeg>(), n_shard_, d_out_shard, shard_bytes_, variant, ok_s, s),
+                   "gather shard");
+    if (phases & kPhaseWeights)
+        cuda_check(dev::launch_gather(w_segs_.get<dev::GatherSeg>(), n_w_, d_out_w, whi_ - wlo_, variant, ok_w, s),
+                   "gather weights");
+}
+
+std::vector<int> DeviceSelectStep::source_of(cudaStream_t s) {
+    std::vector<int> h(static_cast<std::size_t>(M_));
+    cuda_check(cudaMemcpyAsync(h.data(), source_.get(), h.size() * sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+    return h;
+}
+
+std::vector<double> DeviceSelectStep::scores(cudaStream_t s) {
+    std::vector<double> h(static_cast<std::size_t>(M_) * (K_ - 1));
+    cuda_check(cudaMemcpyAsync(h.data(), scores_.get(), h.size() * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+    return h;
+}
+
 // ---- device re-verify --------------------------------------------------------------
 namespace {
 

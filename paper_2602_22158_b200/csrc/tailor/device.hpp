@@ -170,6 +170,23 @@ cudaError_t launch_derive_weights(const WeightTensor* d_tensors, std::uint32_t n
                                   const std::uint8_t* const* d_parts, std::uint8_t* d_out, std::uint64_t total,
                                   cudaStream_t s);
 
+// ---- K9: device-side magnitude selection + merge plan ---------------------------
+struct PlanEntry {
+    std::uint32_t module; // canonical owner module of the entry
+    std::uint32_t pad;
+    std::uint64_t src_off; // relative to the snapshot buffer base
+    std::uint64_t dst_off;
+    std::uint64_t bytes;
+};
+struct SnapshotBases {
+    const std::uint8_t* shard[kMaxSnapshots];
+    const std::uint8_t* weights[kMaxSnapshots];
+};
+cudaError_t launch_select_plan(const double* d_parts, int nranks, int K, int M, int n_save, const PlanEntry* d_shard_entries,
+                               std::uint32_t n_shard, const PlanEntry* d_w_entries, std::uint32_t n_w,
+                               const SnapshotBases& bases, GatherSeg* d_shard_segs, GatherSeg* d_w_segs, int* d_source_of,
+                               double* d_scores, cudaStream_t s);
+
 int sm_count();
 
 } // namespace tailor::dev

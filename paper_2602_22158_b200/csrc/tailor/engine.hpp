@@ -164,6 +164,35 @@ class DeviceMerge {
     bool bulk_ok_ = false;
 };
 
+// A whole score -> select -> merge step on the device for one unit (rank-r
+// shard + weights share u/units) of a family of FULL snapshots: K9 turns the
+// (all-gathered) per-rank scorer partials into the selection and both segment
+// tables, then K2 gathers. No host synchronization; graph-capturable. The
+// selection is bitwise the host's (select_by_magnitude).
+class DeviceSelectStep {
+  public:
+    DeviceSelectStep(const SynthFamily& fam, int rank, int unit, int units, double rho);
+    std::uint64_t shard_bytes() const { return shard_bytes_; }
+    std::uint64_t weights_lo() const { return wlo_; }
+    std::uint64_t weights_hi() const { return whi_; }
+    // shard_bases[k]: snapshot k+1's rank shard payload; wwin_bases[k]: its weights bytes [wlo, whi)
+    void bind(const std::uint8_t* const* shard_bases, const std::uint8_t* const* wwin_bases);
+    // phases: bitmask of kPhaseSelect (K9), kPhaseShard / kPhaseWeights (the two K2 gathers)
+    static constexpr int kPhaseSelect = 1, kPhaseShard = 2, kPhaseWeights = 4, kPhaseAll = 7;
+    void run(const double* d_parts, int nranks, std::uint8_t* d_out_shard, std::uint8_t* d_out_w, int variant, cudaStream_t s,
+             int phases = kPhaseAll);
+    std::vector<int> source_of(cudaStream_t s);
+    std::vector<double> scores(cudaStream_t s);
+
+  private:
+    int K_, M_, n_save_;
+    std::uint64_t shard_bytes_ = 0, wlo_ = 0, whi_ = 0;
+    std::uint32_t n_shard_ = 0, n_w_ = 0;
+    DeviceBuffer shard_entries_, w_entries_, shard_segs_, w_segs_, source_, scores_;
+    dev::SnapshotBases bases_{};
+    bool bulk_ = false;
+};
+
 // Pipelined host->device->host assembly of one partition from host (pinned)
 // source windows into a host destination: per chunk, only the bytes the
 // chunk needs are copied in, gathered on the device and copied out, on two

@@ -27,7 +27,7 @@ from ._lib import (ErrorKind, GatherSegC, MergeOptionsC, MergeStatsC, ModelSpecC
 __all__ = ["ErrorKind", "TailorError", "ModelSpec", "RecipeSlice", "MergeRecipe", "MergeOptions", "MergeStats",
            "parse_recipe", "recipe_to_yaml", "resolve_plan", "execute_merge", "recipe_from_manifests",
            "verify_checkpoint", "regroup", "train", "score_snapshots", "select_recipe", "layer_map", "SynthFamily", "Scorer",
-           "MergePartition", "gather"]
+           "MergePartition", "SelectStep", "gather"]
 
 
 @dataclasses.dataclass
@@ -377,3 +377,38 @@ class MergePartition:
 
     def wait(self) -> None:
         check(lib().tg_mplan_wait(self._h))
+
+
+class SelectStep:
+    """Device score -> select -> merge step for one unit of a family of full snapshots
+    (tg_dstep_*): selection and segment tables built on the device, no host sync."""
+
+    def __init__(self, family: SynthFamily, rank: int, unit: int, units: int, rho: float = 0.5):
+        self._fam = family
+        self.K, self.M = family.snapshots, family.num_modules
+        self._h = check_handle(lib().tg_dstep_create(family.handle, rank, unit, units, rho))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().tg_dstep_destroy(h)
+            self._h = None
+
+    def range(self):
+        a, b, c = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib().tg_dstep_range(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return a.value, b.value, c.value  # shard bytes, weights lo, weights hi
+
+    def bind(self, shard_bases: Sequence[int], weights_window_bases: Sequence[int]) -> None:
+        check(lib().tg_dstep_bind(self._h, ptr_array(shard_bases), ptr_array(weights_window_bases)))
+
+    def run(self, d_partials: int, nranks: int, d_out_shard: int, d_out_weights: int, variant: int = 0,
+            stream: int = 0, phases: int = 7) -> None:
+        """phases: 1 select+plan, 2 gather shard, 4 gather weights (bitmask)."""
+        check(lib().tg_dstep_run(self._h, d_partials, nranks, d_out_shard, d_out_weights, variant, phases, stream))
+
+    def result(self, stream: int = 0):
+        src = (ctypes.c_int32 * self.M)()
+        sc = (ctypes.c_double * max(1, (self.K - 1) * self.M))()
+        check(lib().tg_dstep_result(self._h, src, sc, stream))
+        return [src[i] for i in range(self.M)], [[sc[p * self.M + m] for m in range(self.M)] for p in range(self.K - 1)]

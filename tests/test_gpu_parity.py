@@ -420,6 +420,58 @@ def test_select_recipe_matches_reference_scorer(tmp_path):
     _both_merge(tmp_path, rec)
 
 
+@pytest.mark.parametrize("seed", range(5))
+def test_device_select_step_matches_host_path(seed):
+    """K9: on-device selection + segment tables == host select_by_magnitude + plan, bitwise."""
+    need_gpu()
+    rng = random.Random(seed)
+    spec = t.ModelSpec(1 + rng.randrange(6), 8 * (1 + rng.randrange(3)), 16, 48, rng.random() < 0.3, 100 + seed)
+    N, K = 1 + rng.randrange(4), 2 + rng.randrange(4)
+    fam = t.SynthFamily(spec, N, K)
+    M = fam.num_modules
+    r, units = rng.randrange(N), 1 + rng.randrange(3)
+    unit = rng.randrange(units)
+    rho = rng.choice([0.2, 0.5, 0.75])
+    shards = [dev(fam.shard_bytes(k, r)) for k in range(1, K + 1)]
+    fam.gen_shard(r, 1, K, [b.data_ptr() for b in shards])
+    st = t.SelectStep(fam, r, unit, units, rho)
+    sbytes, wlo, whi = st.range()
+    wb = [dev(whi - wlo) for _ in range(K)]
+    if whi > wlo:
+        fam.gen_weights(1, K, wlo, whi, [b.data_ptr() for b in wb])
+    st.bind([b.data_ptr() for b in shards], [b.data_ptr() for b in wb])
+    for trial in range(2):
+        if trial == 0:  # real scorer partials of every rank
+            parts = []
+            for rr in range(N):
+                bufs = [dev(fam.shard_bytes(k, rr)) for k in range(1, K + 1)]
+                fam.gen_shard(rr, 1, K, [b.data_ptr() for b in bufs])
+                out = torch.zeros((K - 1) * M * 2, dtype=torch.float64, device="cuda")
+                t.Scorer(fam, rr, 1, K).run([b.data_ptr() for b in bufs], out.data_ptr())
+                torch.cuda.synchronize()
+                parts += out.cpu().tolist()
+        else:  # adversarial: coarse values with exact ties
+            parts = [float(rng.randrange(4)) for _ in range(N * (K - 1) * M * 2)]
+        d_parts = torch.tensor(parts, dtype=torch.float64, device="cuda")
+        out_s, out_w = dev(sbytes), dev(whi - wlo)
+        st.run(d_parts.data_ptr(), N, out_s.data_ptr(), out_w.data_ptr())
+        torch.cuda.synchronize()
+        src_d, sc_d = st.result()
+        yaml, src_h, sc_h, _ = fam.select(parts, N, rho)
+        assert src_d == src_h and sc_d == sc_h
+        mp = t.MergePartition(fam, yaml, r)
+        mp.bind([shards[k - 1].data_ptr() + lo for k, c, lo, hi in mp.windows()])
+        ref = dev(mp.bytes)
+        mp.run(ref.data_ptr())
+        wp = t.MergePartition(fam, yaml, -1, unit, units)
+        wp.bind([wb[k - 1].data_ptr() + (lo - wlo) for k, c, lo, hi in wp.windows()])
+        wref = dev(wp.bytes)
+        wp.run(wref.data_ptr())
+        torch.cuda.synchronize()
+        assert torch.equal(out_s[:sbytes], ref[:sbytes])
+        assert torch.equal(out_w[:whi - wlo], wref[:whi - wlo])
+
+
 @pytest.mark.parametrize("K", [2, 4, 7, 16])
 def test_scorer_variants_agree(K):
     """Register-staged vs TMA-bulk-staged scorer: same tiles, different in-tile order."""
