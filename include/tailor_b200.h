@@ -136,6 +136,14 @@ typedef struct tg_train_config {
 } tg_train_config;
 int tg_train(const tg_model_spec* spec, const tg_train_config* config, const char* out_dir,
              int32_t* checkpoints_written);
+/* A resident trainer over rank partitions [rank_begin, rank_end) of a num_ranks layout
+ * (one per GPU in a ZeRO job): train_step (R/src/trainer.cpp:26-35) on the device. */
+typedef struct tg_trainer tg_trainer;
+tg_trainer* tg_trainer_create(const tg_model_spec* spec, int32_t num_ranks, int32_t rank_begin, int32_t rank_end, double lr,
+                              double weight_decay, int32_t device);
+void tg_trainer_destroy(tg_trainer* t);
+uint64_t tg_trainer_elements(const tg_trainer* t);
+int tg_trainer_step(tg_trainer* t, int64_t step, double* grad_norm, double* update_norm);
 /* read_checkpoint's invariants (R/src/checkpoint.cpp:485-575), checked on the device. */
 int tg_verify_checkpoint(const char* dir, int32_t device);
 /* Update-magnitude scores of consecutive snapshot directories on the device

@@ -29,6 +29,9 @@ struct tg_family {
 struct tg_scorer {
     std::unique_ptr<ScorePlan> plan;
 };
+struct tg_trainer {
+    std::unique_ptr<DeviceTrainer> tr;
+};
 struct tg_dstep {
     std::unique_ptr<DeviceSelectStep> step;
 };
@@ -304,6 +307,29 @@ int tg_train(const tg_model_spec* spec, const tg_train_config* c, const char* ou
         cfg.device = c->device;
         const auto dirs = device_train(cfg, out_dir ? out_dir : "");
         if (written) *written = static_cast<int32_t>(dirs.size());
+    });
+}
+
+tg_trainer* tg_trainer_create(const tg_model_spec* spec, int32_t num_ranks, int32_t r0, int32_t r1, double lr, double wd,
+                              int32_t device) {
+    tg_trainer* out = nullptr;
+    guard([&] {
+        AdamHyperparams h;
+        h.lr = lr;
+        h.weight_decay = wd;
+        out = new tg_trainer{std::make_unique<DeviceTrainer>(to_spec(spec), num_ranks, h, device, r0, r1)};
+    });
+    return out;
+}
+
+void tg_trainer_destroy(tg_trainer* t) { delete t; }
+uint64_t tg_trainer_elements(const tg_trainer* t) { return t->tr->elements(); }
+
+int tg_trainer_step(tg_trainer* t, int64_t step, double* gn, double* un) {
+    return guard([&] {
+        const auto [g, u] = t->tr->step(step);
+        if (gn) *gn = g;
+        if (un) *un = u;
     });
 }
 

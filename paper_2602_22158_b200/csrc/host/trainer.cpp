@@ -66,7 +66,7 @@ std::vector<ModuleId> modules_to_save(const StrategyConfig& cfg, const ModelSpec
 }
 
 struct DeviceTrainer::Rank {
-    DeviceBuffer part, groups, slices, grad_part, delta_part;
+    DeviceBuffer part, groups, slices, grad, grad_part, delta_part;
     std::uint32_t ngroups = 0;
     std::uint64_t total = 0;
     unsigned grid = 0;
@@ -93,16 +93,20 @@ void write_container_file(const fs::path& path, const ContainerLayout& lay, cons
 
 } // namespace
 
-DeviceTrainer::DeviceTrainer(const ModelSpec& spec, int num_ranks, const AdamHyperparams& base, int device)
+DeviceTrainer::DeviceTrainer(const ModelSpec& spec, int num_ranks, const AdamHyperparams& base, int device, int rank_begin,
+                             int rank_end)
     : model_(spec), N_(num_ranks), base_(base) {
     base_.validate();
     if (num_ranks < 1) fail(ErrorKind::Recipe, "num_ranks must be >= 1");
+    r0_ = rank_begin;
+    r1_ = rank_end < 0 ? num_ranks : rank_end;
+    if (r0_ < 0 || r1_ > num_ranks || r0_ >= r1_) fail(ErrorKind::Geometry, "bad rank range for the trainer");
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
     cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
     full_ = checkpoint_layout(model_, N_, model_.modules());
     const ShardGeometry geom{N_};
     std::vector<const std::uint8_t*> ptrs;
-    for (int r = 0; r < N_; ++r) {
+    for (int r = r0_; r < r1_; ++r) {
         auto rk = std::make_unique<Rank>();
         const ContainerLayout& lay = full_.shards[static_cast<std::size_t>(r)];
         rk->part.resize(std::max<std::uint64_t>(16, lay.payload_bytes));
@@ -119,6 +123,8 @@ DeviceTrainer::DeviceTrainer(const ModelSpec& spec, int num_ranks, const AdamHyp
             const std::uint64_t om = lay.find(shard_key(g, ".exp_avg"))->begin, ov = lay.find(shard_key(g, ".exp_avg_sq"))->begin,
                                 ow = lay.find(shard_key(g, ".master"))->begin;
             if (chunk == 0) continue;
+            elements_ += static_cast<std::uint64_t>(std::clamp<std::int64_t>(len - static_cast<std::int64_t>(r) * static_cast<std::int64_t>(chunk), 0,
+                                                                             static_cast<std::int64_t>(chunk)));
             tg.push_back({begin, chunk, static_cast<std::uint64_t>(r) * chunk, static_cast<std::uint64_t>(len), om, ov, ow, sb,
                           static_cast<std::uint32_t>(model_.slices(g).size()), static_cast<std::uint32_t>(g), 0});
             dev::SynthGroup s{};
@@ -141,6 +147,7 @@ DeviceTrainer::DeviceTrainer(const ModelSpec& spec, int num_ranks, const AdamHyp
         rk->slices.upload(sl.data(), sl.size() * sizeof(dev::SynthSlice));
         rk->grid = dev::adamw_grid(begin);
         rk->grad_part.resize(rk->grid * sizeof(double));
+        rk->grad.resize(std::max<std::uint64_t>(16, begin * sizeof(float)));
         rk->delta_part.resize(rk->grid * sizeof(double));
         // W_0 = 0.02 * u(seed, 0, e) (init_state, R/src/gradients.cpp:51-66): the
         // generator with k1 = 0 writes exactly the initial masters.
@@ -165,12 +172,14 @@ DeviceTrainer::~DeviceTrainer() {
     if (stream_) cudaStreamDestroy(stream_);
 }
 
+std::uint64_t DeviceTrainer::elements() const { return elements_; }
+
 std::pair<double, double> DeviceTrainer::step(std::int64_t s) {
-    const dev::TrainParams p{model_.spec().seed, static_cast<std::uint64_t>(s), 0.05f, 0.01f};
+    const dev::TrainParams p{dev::noise_prefix(model_.spec().seed, static_cast<std::uint64_t>(s)), 0.05f, 0.01f};
     cuda_check(cudaMemsetAsync(flag_.get(), 0, sizeof(unsigned int), stream_), "memset");
     for (auto& rk : ranks_)
         cuda_check(dev::launch_grad_check(rk->groups.get<dev::TrainGroup>(), rk->ngroups, rk->slices.get<dev::SynthSlice>(),
-                                          rk->part.get(), rk->total, p, rk->grad_part.get<double>(),
+                                          rk->part.get(), rk->total, p, rk->grad.get<float>(), rk->grad_part.get<double>(),
                                           flag_.get<unsigned int>(), stream_),
                    "grad check");
     unsigned int bad = 0;
@@ -195,9 +204,8 @@ std::pair<double, double> DeviceTrainer::step(std::int64_t s) {
     cuda_check(cudaMemcpyAsync(coef_.get(), coef.data(), coef.size() * sizeof(dev::AdamCoef), cudaMemcpyHostToDevice, stream_),
                "coef");
     for (auto& rk : ranks_)
-        cuda_check(dev::launch_adamw(rk->groups.get<dev::TrainGroup>(), rk->ngroups, rk->slices.get<dev::SynthSlice>(),
-                                     coef_.get<dev::AdamCoef>(), rk->part.get(), rk->total, p, rk->delta_part.get<double>(),
-                                     stream_),
+        cuda_check(dev::launch_adamw(rk->groups.get<dev::TrainGroup>(), rk->ngroups, coef_.get<dev::AdamCoef>(), rk->part.get(),
+                                     rk->grad.get<float>(), rk->total, rk->delta_part.get<double>(), stream_),
                    "adamw");
     double g2 = 0.0, d2 = 0.0;
     std::vector<double> h;
@@ -218,6 +226,7 @@ std::pair<double, double> DeviceTrainer::step(std::int64_t s) {
 
 void DeviceTrainer::save(const fs::path& dir, const TrainerMeta& meta, const std::vector<ModuleId>& modules,
                          const std::string& label) {
+    if (r0_ != 0 || r1_ != N_) fail(ErrorKind::Consistency, "saving a checkpoint needs every rank partition");
     const CheckpointLayout lay = checkpoint_layout(model_, N_, modules);
     const ShardGeometry geom{N_};
     std::error_code ec;
@@ -280,8 +289,8 @@ void DeviceTrainer::save(const fs::path& dir, const TrainerMeta& meta, const std
 
 void DeviceTrainer::keep_masters() {
     const auto fields = score_fields(model_, N_);
-    for (int r = 0; r < N_; ++r) {
-        Rank& rk = *ranks_[static_cast<std::size_t>(r)];
+    for (int r = r0_; r < r1_; ++r) {
+        Rank& rk = *ranks_[static_cast<std::size_t>(r - r0_)];
         const ContainerLayout& fl = full_.shards[static_cast<std::size_t>(r)];
         if (!rk.plan) {
             std::vector<dev::GatherSeg> gs;

@@ -32,10 +32,8 @@ __device__ __forceinline__ std::uint64_t mix64(std::uint64_t z) {
     return z;
 }
 
-__device__ __forceinline__ float unit_noise(std::uint64_t seed, std::uint64_t t, std::uint64_t e) {
-    std::uint64_t h = mix64(seed + 0x9E3779B97F4A7C15ULL);
-    h = mix64(h ^ (t * 0xD1B54A32D192ED03ULL));
-    h = mix64(h ^ (e * 0x8CB92BA72F3D8DD7ULL));
+__device__ __forceinline__ float unit_noise_from(std::uint64_t prefix, std::uint64_t e) {
+    const std::uint64_t h = mix64(prefix ^ (e * 0x8CB92BA72F3D8DD7ULL));
     const double unit = __dmul_rn(__ull2double_rn(h >> 11), 0x1.0p-53);
     return __double2float_rn(__dadd_rn(__dmul_rn(2.0, unit), -1.0));
 }
@@ -70,7 +68,7 @@ __device__ __forceinline__ bool locate(const TrainGroup* __restrict__ groups, st
 }
 
 __device__ __forceinline__ float grad_of(float w, const TrainParams& p, std::uint64_t e) {
-    return __fadd_rn(__fmul_rn(p.state_coeff, w), __fmul_rn(p.noise_coeff, unit_noise(p.seed, p.step, e)));
+    return __fadd_rn(__fmul_rn(p.state_coeff, w), __fmul_rn(p.noise_coeff, unit_noise_from(p.noise_prefix, e)));
 }
 
 __device__ __forceinline__ double block_sum(double v, double* red) {
@@ -88,7 +86,8 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 __global__ void __launch_bounds__(kThreads) grad_check_kernel(const TrainGroup* __restrict__ groups, std::uint32_t ngroups,
                                                               const SynthSlice* __restrict__ slices,
                                                               const std::uint8_t* __restrict__ part, std::uint64_t total,
-                                                              TrainParams p, double* __restrict__ grad_partials,
+                                                              TrainParams p, float* __restrict__ grad,
+                                                              double* __restrict__ grad_partials,
                                                               unsigned int* __restrict__ nonfinite) {
     __shared__ double red[kThreads / 32];
     double acc = 0.0;
@@ -100,6 +99,7 @@ __global__ void __launch_bounds__(kThreads) grad_check_kernel(const TrainGroup* 
         if (!locate(groups, ngroups, slices, v, g, i, e)) continue;
         const float w = reinterpret_cast<const float*>(part + g->off_w)[i];
         const float gr = grad_of(w, p, e);
+        grad[v] = gr;
         bad = bad || !isfinite(gr);
         acc += static_cast<double>(gr) * static_cast<double>(gr);
     }
@@ -109,23 +109,22 @@ __global__ void __launch_bounds__(kThreads) grad_check_kernel(const TrainGroup* 
 }
 
 __global__ void __launch_bounds__(kThreads) adamw_update_kernel(const TrainGroup* __restrict__ groups, std::uint32_t ngroups,
-                                                                const SynthSlice* __restrict__ slices,
                                                                 const AdamCoef* __restrict__ coef, std::uint8_t* __restrict__ part,
-                                                                std::uint64_t total, TrainParams p,
+                                                                const float* __restrict__ grad, std::uint64_t total,
                                                                 double* __restrict__ delta_partials) {
     __shared__ double red[kThreads / 32];
     double acc = 0.0;
     const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
     for (std::uint64_t v = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; v < total; v += stride) {
-        const TrainGroup* g;
-        std::uint64_t i, e;
-        if (!locate(groups, ngroups, slices, v, g, i, e)) continue;
+        const TrainGroup* g = &groups[find_group(groups, ngroups, v)];
+        const std::uint64_t i = v - g->begin;
+        if (g->group_first + i >= g->true_len) continue; // shard padding stays zero
         const AdamCoef c = coef[g->coef];
         float* wp = reinterpret_cast<float*>(part + g->off_w) + i;
         float* mp = reinterpret_cast<float*>(part + g->off_m) + i;
         float* vp = reinterpret_cast<float*>(part + g->off_v) + i;
         const float w = *wp;
-        const float gr = grad_of(w, p, e);
+        const float gr = grad[v];
         const float m = __fadd_rn(__fmul_rn(c.b1, *mp), __fmul_rn(c.one_minus_b1, gr));
         const float vv = __fadd_rn(__fmul_rn(c.b2, *vp), __fmul_rn(c.one_minus_b2, __fmul_rn(gr, gr)));
         const float m_hat = __fdiv_rn(m, c.bias1);
@@ -183,20 +182,31 @@ unsigned adamw_grid(std::uint64_t total) {
     return static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(want, static_cast<std::uint64_t>(sm_count()) * 8)));
 }
 
+std::uint64_t noise_prefix(std::uint64_t seed, std::uint64_t step) {
+    const auto mix = [](std::uint64_t z) {
+        z ^= z >> 30;
+        z *= 0xBF58476D1CE4E5B9ULL;
+        z ^= z >> 27;
+        z *= 0x94D049BB133111EBULL;
+        z ^= z >> 31;
+        return z;
+    };
+    return mix(mix(seed + 0x9E3779B97F4A7C15ULL) ^ (step * 0xD1B54A32D192ED03ULL));
+}
+
 cudaError_t launch_grad_check(const TrainGroup* d_groups, std::uint32_t ngroups, const SynthSlice* d_slices,
-                              const std::uint8_t* d_part, std::uint64_t total, const TrainParams& p,
+                              const std::uint8_t* d_part, std::uint64_t total, const TrainParams& p, float* d_grad,
                               double* d_grad_partials, unsigned int* d_nonfinite, cudaStream_t s) {
     if (total == 0) return cudaSuccess;
-    grad_check_kernel<<<adamw_grid(total), kThreads, 0, s>>>(d_groups, ngroups, d_slices, d_part, total, p, d_grad_partials,
-                                                            d_nonfinite);
+    grad_check_kernel<<<adamw_grid(total), kThreads, 0, s>>>(d_groups, ngroups, d_slices, d_part, total, p, d_grad,
+                                                            d_grad_partials, d_nonfinite);
     return cudaGetLastError();
 }
 
-cudaError_t launch_adamw(const TrainGroup* d_groups, std::uint32_t ngroups, const SynthSlice* d_slices,
-                         const AdamCoef* d_coef, std::uint8_t* d_part, std::uint64_t total, const TrainParams& p,
-                         double* d_delta_partials, cudaStream_t s) {
+cudaError_t launch_adamw(const TrainGroup* d_groups, std::uint32_t ngroups, const AdamCoef* d_coef, std::uint8_t* d_part,
+                         const float* d_grad, std::uint64_t total, double* d_delta_partials, cudaStream_t s) {
     if (total == 0) return cudaSuccess;
-    adamw_update_kernel<<<adamw_grid(total), kThreads, 0, s>>>(d_groups, ngroups, d_slices, d_coef, d_part, total, p,
+    adamw_update_kernel<<<adamw_grid(total), kThreads, 0, s>>>(d_groups, ngroups, d_coef, d_part, d_grad, total,
                                                               d_delta_partials);
     return cudaGetLastError();
 }

@@ -145,17 +145,20 @@ struct AdamCoef {
     float b1, one_minus_b1, b2, one_minus_b2, bias1, bias2, lr, eps, wd, pad[3];
 };
 struct TrainParams {
-    std::uint64_t seed;
-    std::uint64_t step;
+    // unit_noise(seed, step, e) = f(mix64(noise_prefix ^ e * C3)): the first two
+    // hash rounds depend only on (seed, step) and are computed once on the host.
+    std::uint64_t noise_prefix;
     float state_coeff; // GradientSource c1 (R/include/tailor/gradients.hpp:20-24)
     float noise_coeff; // c2
 };
+std::uint64_t noise_prefix(std::uint64_t seed, std::uint64_t step);
+// Pass 1: gradients -> d_grad (one float per virtual element), FP64 sum g^2 per
+// block, non-finite flag. Pass 2 (only if no flag): AdamW from d_grad.
 cudaError_t launch_grad_check(const TrainGroup* d_groups, std::uint32_t ngroups, const SynthSlice* d_slices,
-                              const std::uint8_t* d_part, std::uint64_t total, const TrainParams& p,
+                              const std::uint8_t* d_part, std::uint64_t total, const TrainParams& p, float* d_grad,
                               double* d_grad_partials, unsigned int* d_nonfinite, cudaStream_t s);
-cudaError_t launch_adamw(const TrainGroup* d_groups, std::uint32_t ngroups, const SynthSlice* d_slices,
-                         const AdamCoef* d_coef, std::uint8_t* d_part, std::uint64_t total, const TrainParams& p,
-                         double* d_delta_partials, cudaStream_t s);
+cudaError_t launch_adamw(const TrainGroup* d_groups, std::uint32_t ngroups, const AdamCoef* d_coef, std::uint8_t* d_part,
+                         const float* d_grad, std::uint64_t total, double* d_delta_partials, cudaStream_t s);
 unsigned adamw_grid(std::uint64_t total);
 
 // ---- K8: bf16 weights derived from sharded masters ---------------------------------

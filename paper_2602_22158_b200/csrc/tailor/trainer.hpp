@@ -35,7 +35,12 @@ struct DeviceTrainConfig {
 
 class DeviceTrainer {
   public:
-    DeviceTrainer(const ModelSpec& spec, int num_ranks, const AdamHyperparams& base, int device);
+    // Holds rank partitions [rank_begin, rank_end) of the num_ranks layout
+    // (default: all). save() needs every rank; step() works on any subset —
+    // one rank partition per GPU in a ZeRO job.
+    DeviceTrainer(const ModelSpec& spec, int num_ranks, const AdamHyperparams& base, int device, int rank_begin = 0,
+                  int rank_end = -1);
+    std::uint64_t elements() const; // true (unpadded) optimizer elements held
     ~DeviceTrainer();
     // One train_step at training step `step` (R/src/trainer.cpp:26-35): returns
     // {grad_norm, update_norm}. Throws NonFinite before touching the state.
@@ -54,6 +59,8 @@ class DeviceTrainer {
     struct Rank;
     ModelLayout model_;
     int N_;
+    int r0_ = 0, r1_ = 0;
+    std::uint64_t elements_ = 0;
     AdamHyperparams base_;
     CheckpointLayout full_;
     std::vector<std::unique_ptr<Rank>> ranks_;

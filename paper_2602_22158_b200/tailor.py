@@ -27,7 +27,7 @@ from ._lib import (ErrorKind, GatherSegC, MergeOptionsC, MergeStatsC, ModelSpecC
 __all__ = ["ErrorKind", "TailorError", "ModelSpec", "RecipeSlice", "MergeRecipe", "MergeOptions", "MergeStats",
            "parse_recipe", "recipe_to_yaml", "resolve_plan", "execute_merge", "recipe_from_manifests",
            "verify_checkpoint", "regroup", "train", "score_snapshots", "select_recipe", "layer_map", "SynthFamily", "Scorer",
-           "MergePartition", "SelectStep", "gather"]
+           "MergePartition", "SelectStep", "Trainer", "STRATEGIES", "gather"]
 
 
 @dataclasses.dataclass
@@ -377,6 +377,31 @@ class MergePartition:
 
     def wait(self) -> None:
         check(lib().tg_mplan_wait(self._h))
+
+
+class Trainer:
+    """Resident device trainer over rank partitions [rank_begin, rank_end) (tg_trainer_*)."""
+
+    def __init__(self, spec: ModelSpec, num_ranks: int, rank_begin: int = 0, rank_end: int = -1, lr: float = 1e-3,
+                 weight_decay: float = 0.01, device: int = 0):
+        c = spec.to_c()
+        self._h = check_handle(lib().tg_trainer_create(ctypes.byref(c), num_ranks, rank_begin, rank_end, lr,
+                                                       weight_decay, device))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().tg_trainer_destroy(h)
+            self._h = None
+
+    @property
+    def elements(self) -> int:
+        return lib().tg_trainer_elements(self._h)
+
+    def step(self, step: int):
+        g, u = ctypes.c_double(), ctypes.c_double()
+        check(lib().tg_trainer_step(self._h, step, ctypes.byref(g), ctypes.byref(u)))
+        return g.value, u.value
 
 
 class SelectStep:
