@@ -155,6 +155,8 @@ int tg_score_snapshots(const char* const* dirs, int32_t n, int32_t device, doubl
  * R/src/merge.cpp:375-417). source_of[m] = index into dirs. */
 int tg_select_recipe(const char* const* dirs, int32_t n, double rho, int32_t device, char* yaml_out, size_t cap,
                      size_t* needed, int32_t* source_of, double* min_boundary_gap);
+/* parse_config_json (R/src/checkpoint.cpp:123-136): model config.json text -> spec. */
+int tg_parse_config(const char* config_json, tg_model_spec* spec);
 /* Layer map (R/src/model.cpp, R/src/groups.cpp, R/src/shard.cpp) as JSON. */
 int tg_layer_map(const tg_model_spec* spec, int32_t num_ranks, char* json_out, size_t cap, size_t* needed);
 

@@ -112,6 +112,7 @@ SIGNATURES = {
     "tg_select_recipe": (_I, [_c.POINTER(_S), _I32, _D, _I32, _c.c_char_p, _SZ, _PSZ, _c.POINTER(_I32),
                               _c.POINTER(_D)]),
     "tg_layer_map": (_I, [_c.POINTER(ModelSpecC), _I32, _c.c_char_p, _SZ, _PSZ]),
+    "tg_parse_config": (_I, [_S, _c.POINTER(ModelSpecC)]),
     "tg_gather": (_I, [_P, _U32, _P, _U64, _I32, _I32, _P]),
     "tg_score_partials": (_I, [_P, _U32, _P, _U32, _I32, _I32, _P, _P]),
     "tg_score_combine": (_I, [_P, _P, _I32, _I32, _P, _P]),

@@ -374,6 +374,13 @@ int tg_select_recipe(const char* const* dirs, int32_t n, double rho, int32_t dev
     });
 }
 
+int tg_parse_config(const char* text, tg_model_spec* out) {
+    return guard([&] {
+        const ModelSpec s = parse_config_json(text ? text : "", "config");
+        if (out) *out = tg_model_spec{s.num_layers, s.hidden_dim, s.ffn_dim, s.vocab_size, s.weight_tied ? 1 : 0, 0, s.seed};
+    });
+}
+
 int tg_layer_map(const tg_model_spec* spec, int32_t num_ranks, char* out, size_t cap, size_t* needed) {
     return guard([&] {
         const ModelLayout model(to_spec(spec));

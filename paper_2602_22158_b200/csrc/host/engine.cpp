@@ -443,6 +443,9 @@ DeviceMerge::DeviceMerge(const PartitionPlan& plan) : plan_(plan) {
 
 void DeviceMerge::bind(const std::vector<const std::uint8_t*>& window_ptrs) {
     if (window_ptrs.size() != plan_.windows.size()) fail(ErrorKind::Geometry, "window pointer count mismatch");
+    // The table is immutable while launches may read it: a rebind waits for all
+    // outstanding device work (rare; binds happen once per plan in practice).
+    if (d_segs_.size()) cuda_check(cudaDeviceSynchronize(), "bind sync");
     std::vector<dev::GatherSeg> segs;
     segs.reserve(plan_.segments.size());
     bool ok = true;
@@ -625,7 +628,7 @@ DeviceSelectStep::DeviceSelectStep(const SynthFamily& fam, int rank, int unit, i
     bool aligned = true;
     for (const auto* v : {&se, &we})
         for (const auto& p : *v) aligned = aligned && p.dst_off % 16 == 0 && p.bytes % 16 == 0;
-    bulk_ = aligned;
+    entries_aligned_ = aligned;
     shard_entries_.upload(se.data(), se.size() * sizeof(dev::PlanEntry));
     w_entries_.upload(we.data(), we.size() * sizeof(dev::PlanEntry));
     shard_segs_.resize(std::max<std::size_t>(1, se.size()) * sizeof(dev::GatherSeg));
@@ -635,6 +638,9 @@ DeviceSelectStep::DeviceSelectStep(const SynthFamily& fam, int rank, int unit, i
 }
 
 void DeviceSelectStep::bind(const std::uint8_t* const* shard_bases, const std::uint8_t* const* wwin_bases) {
+    // Bases travel by value in the K9 launch parameters: rebinding never races
+    // with launches already queued.
+    bulk_ = entries_aligned_;
     for (int k = 0; k < K_; ++k) {
         bases_.shard[k] = shard_bases[k];
         bases_.weights[k] = wwin_bases[k];

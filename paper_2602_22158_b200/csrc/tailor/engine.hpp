@@ -190,6 +190,7 @@ class DeviceSelectStep {
     std::uint32_t n_shard_ = 0, n_w_ = 0;
     DeviceBuffer shard_entries_, w_entries_, shard_segs_, w_segs_, source_, scores_;
     dev::SnapshotBases bases_{};
+    bool entries_aligned_ = false;
     bool bulk_ = false;
 };
 

@@ -9,6 +9,8 @@
 //   tailor score  --snapshots A,B,... [--device D]
 //   tailor check  --ckpt DIR [--device D]
 //   tailor regroup --ckpt DIR --out DIR [--to fine|coarse] [--device D] [--no-verify]
+//   tailor train  --config c.json --steps S --interval I --strategy full|parity|filter|magnitude
+//                 --ranks N --out RUN [--lr --weight-decay --head --tail --sparse-multiple --rho --device]
 // Exit codes: 0 success, 1 user error, 2 internal/consistency error.
 #include <cstdio>
 #include <cstring>
@@ -165,6 +167,52 @@ int cmd_score(const Args& a) {
     return 0;
 }
 
+// R/tools/tailor_main.cpp:40-64 flags, on the device trainer; --strategy adds
+// `magnitude` (in-situ update-magnitude selective checkpointing, --rho).
+int cmd_train(const Args& a) {
+    if (!require(a, {"config", "steps", "interval", "strategy", "ranks", "out"})) return 1;
+    bool ok = false;
+    const std::string text = read_file(a.kv.at("config"), &ok);
+    if (!ok) {
+        std::cerr << "error: MissingArtifact: cannot open '" << a.kv.at("config") << "'\n";
+        return 1;
+    }
+    tg_model_spec spec{};
+    if (int rc = tg_parse_config(text.c_str(), &spec); rc != TG_OK) return report(rc);
+    static const std::map<std::string, int> kinds = {{"full", 0}, {"parity", 1}, {"filter", 2}, {"magnitude", 3}};
+    const auto it = kinds.find(a.kv.at("strategy"));
+    if (it == kinds.end()) {
+        std::cerr << "error: RecipeError: unknown strategy '" << a.kv.at("strategy") << "'\n";
+        return 1;
+    }
+    if (a.kv.count("grouping") && a.kv.at("grouping") != "fine") {
+        std::cerr << "error: RecipeError: "
+                  << (a.kv.at("grouping") == "coarse"
+                          ? std::string("the device trainer writes fine grouping; convert with `tailor regroup --to coarse`")
+                          : "unknown grouping '" + a.kv.at("grouping") + "' (expected fine or coarse)")
+                  << "\n";
+        return 1;
+    }
+    const auto num = [&](const char* k, double d) { return a.kv.count(k) ? std::stod(a.kv.at(k)) : d; };
+    tg_train_config cfg{};
+    cfg.total_steps = std::stoi(a.kv.at("steps"));
+    cfg.num_ranks = std::stoi(a.kv.at("ranks"));
+    cfg.interval = std::stoi(a.kv.at("interval"));
+    cfg.strategy = it->second;
+    cfg.head_count = static_cast<int32_t>(num("head", 2));
+    cfg.tail_count = static_cast<int32_t>(num("tail", 2));
+    cfg.sparse_multiple = static_cast<int32_t>(num("sparse-multiple", 5));
+    cfg.device = static_cast<int32_t>(num("device", 0));
+    cfg.lr = num("lr", 1e-3);
+    cfg.weight_decay = num("weight-decay", 0.01);
+    cfg.rho = num("rho", 0.5);
+    int32_t written = 0;
+    if (int rc = tg_train(&spec, &cfg, a.kv.at("out").c_str(), &written); rc != TG_OK) return report(rc);
+    std::cout << "trained " << cfg.total_steps << " steps (" << a.kv.at("strategy") << ", interval " << cfg.interval
+              << ", ranks " << cfg.num_ranks << "): " << written << " checkpoints in " << a.kv.at("out") << "\n";
+    return 0;
+}
+
 int cmd_regroup(const Args& a) {
     if (!require(a, {"ckpt", "out"})) return 1;
     const std::string to = a.kv.count("to") ? a.kv.at("to") : "fine";
@@ -218,6 +266,7 @@ int main(int argc, char** argv) {
         if (cmd == "score") return cmd_score(a);
         if (cmd == "check") return cmd_check(a);
         if (cmd == "regroup") return cmd_regroup(a);
+        if (cmd == "train") return cmd_train(a);
     } catch (const std::exception& e) {
         std::cerr << "error: " << e.what() << "\n";
         return 1;

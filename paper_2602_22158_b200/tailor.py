@@ -45,6 +45,13 @@ class ModelSpec:
         return ModelSpecC(self.num_layers, self.hidden_dim, self.ffn_dim, self.vocab_size,
                           1 if self.weight_tied else 0, 0, self.seed)
 
+    @classmethod
+    def from_config(cls, text: str) -> "ModelSpec":
+        """parse_config_json (R/src/checkpoint.cpp:123-136) through tg_parse_config."""
+        c = ModelSpecC()
+        check(lib().tg_parse_config(text.encode(), ctypes.byref(c)))
+        return cls(c.num_layers, c.hidden_dim, c.ffn_dim, c.vocab_size, bool(c.weight_tied), c.seed)
+
     @property
     def module_count(self) -> int:
         return self.num_layers + (2 if self.weight_tied else 3)

@@ -6,7 +6,6 @@ and oracle/_ref/ref_tool (the reference library itself, compiled from
 Bar: bit-exact bytes for every payload, header and sidecar; scores within
 1e-6 relative; identical selections and recipes.
 """
-import filecmp
 import json
 import os
 import random
@@ -82,7 +81,6 @@ def test_write_dir_matches_reference_writer(tmp_path):
     fam = t.SynthFamily(spec, N, K)
     for k in range(1, K + 1):
         fam.write_dir(k, str(tmp_path / "ours" / f"checkpoint-{k * 100}"))
-    cmp = filecmp.dircmp(tmp_path / "ref", tmp_path / "ours")
     _assert_same_tree(tmp_path / "ref", tmp_path / "ours")
 
 

@@ -87,3 +87,26 @@ def test_magnitude_strategy_in_situ(tmp_path):
                [f"optim/rank_{r}.shard" for r in range(N)]:
         assert (tmp_path / "merged" / rel).read_bytes() == (tmp_path / "ref_merged" / rel).read_bytes(), rel
     t.verify_checkpoint(str(tmp_path / "merged"))
+
+
+def test_cli_train_matches_reference_cli(tmp_path):
+    """`tailor train` (R/tools/tailor_main.cpp:40-64 flags) on the device trainer."""
+    need_gpu()
+    import subprocess
+    spec = dict(num_layers=3, hidden_dim=8, ffn_dim=16, vocab_size=32, weight_tied=False, seed=4242)
+    ref_tool("train", *spec_args(spec), "--strategy", "filter", "--steps", 40, "--interval", 10, "--ranks", 2,
+             "--head", 1, "--tail", 1, "--sparse-multiple", 2, "--out", tmp_path / "ref")
+    cfg = tmp_path / "config.json"
+    cfg.write_bytes((tmp_path / "ref" / "checkpoint-10" / "config.json").read_bytes())
+    cli = str(t._lib.CLI_PATH)
+    base = [cli, "train", "--config", str(cfg), "--steps", "40", "--interval", "10", "--ranks", "2"]
+    r = subprocess.run(base + ["--strategy", "filter", "--head", "1", "--tail", "1", "--sparse-multiple", "2",
+                               "--out", str(tmp_path / "ours")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert "4 checkpoints" in r.stdout
+    same_tree(tmp_path / "ref", tmp_path / "ours")
+    logs_close(tmp_path / "ref", tmp_path / "ours")
+    for bad in [["--strategy", "sometimes", "--out", str(tmp_path / "x")],
+                ["--strategy", "full", "--grouping", "coarse", "--out", str(tmp_path / "y")]]:
+        r = subprocess.run(base + bad, capture_output=True, text=True)
+        assert r.returncode == 1 and "RecipeError" in r.stderr

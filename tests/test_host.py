@@ -205,6 +205,19 @@ def test_recipe_from_manifests_matches_reference(tmp_path, strategy, steps, inte
     assert t.recipe_from_manifests(str(tmp_path / "run"), fail_at) == t.MergeRecipe.from_json(json.dumps(ref))
 
 
+def test_parse_config_reads_reference_config(tmp_path):
+    _need_ref()
+    spec = dict(num_layers=3, hidden_dim=8, ffn_dim=16, vocab_size=32, weight_tied=True, seed=77)
+    d = ref_tool("gen", *spec_args(spec), "--ranks", 2, "--snapshots", 1, "--out", tmp_path / "run")[1]["snapshots"]
+    got = t.ModelSpec.from_config((tmp_path / "run" / d[0] / "config.json").read_text()
+                                  if not d[0].startswith("/") else open(d[0] + "/config.json").read())
+    assert got == t.ModelSpec(3, 8, 16, 32, True, 77)
+    for bad in ["", "{", '{"num_layers": 2}', '{"num_layers": "x", "hidden_dim": 8, "ffn_dim": 16, '
+                '"vocab_size": 32, "tie_word_embeddings": false, "seed": 1}']:
+        with pytest.raises(t.TailorError):
+            t.ModelSpec.from_config(bad)
+
+
 def test_recipe_from_manifests_unrecoverable(tmp_path):
     _need_ref()
     spec = dict(num_layers=4, hidden_dim=8, ffn_dim=16, vocab_size=32, weight_tied=False, seed=5)
