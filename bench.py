@@ -11,13 +11,16 @@ r-th tensor-aligned share of the consolidated bf16 weights (~2.2 GB). GPU g of
 G owns rank partition g (weak scaling: fixed work per GPU). One step =
   K3/K4 score the 4 resident snapshots' fp32 masters of the partition (3 pairs)
   -> NCCL all-gather of the FP64 partials (G > 1)
-  -> fixed-order rank combine + magnitude selection + recipe (C++, host)
+  -> K9: fixed-order rank combine + magnitude selection + segment tables on the
+     device (--host-select: the same in C++ on the host, plan memoized)
   -> K2 gather/scatter of the composite shard partition and weights share.
 Inputs are resident in HBM (62 GB per GPU, >> 126 MB L2, so no L2 flush is needed).
+TAILOR_BENCH_SHARE_GPU=1 (tests only) runs N>1 ranks on one GPU over gloo.
 
 `e2e`: the same step through the C ABI with HOST (pinned) buffers: masters
 staged H2D for scoring, then the shard pipeline (H2D of exactly the selected
-bytes -> K2 -> D2H) per partition.
+bytes -> K2 -> D2H) per partition, carrying the next unit's masters between
+its own inputs so both link directions stay busy.
 
 `--impl reference`: the reference's own CPU implementation (oracle/_ref/ref_tool:
 reference read_checkpoint + scorer restatement + resolve_plan + execute_merge,
@@ -56,7 +59,39 @@ WORKLOADS = {
 # Reference-arm / cpu_baseline sample: cfg3's merge, shrunk to fit a few
 # seconds of CPU work per step (same layout rules, 8 ranks, 4 snapshots).
 SAMPLE = (1, 1024, 3584, 4096, False, 8, 4, 0.5)
+MODEL_NAMES = {"cfg1": "tiny Llama-style (reference ModelSpec)", "cfg2": "Qwen2.5-7B-shaped (reference ModelSpec)",
+               "cfg3": "Llama-3.1-8B-shaped (reference ModelSpec)", "cfg4": "Llama-3.1-8B-shaped (reference ModelSpec)"}
 SCORE_VARIANTS = {0: "auto", 1: "register", 2: "staged", 3: "register-128b", 4: "register-64b"}
+
+
+def shared_gpu() -> bool:
+    """TAILOR_BENCH_SHARE_GPU=1: every rank on the visible GPU(s) round-robin, gloo
+    for the collectives (exercises the N>1 path on a single-GPU box; tests only)."""
+    return os.environ.get("TAILOR_BENCH_SHARE_GPU") == "1"
+
+
+def all_gather(out, inp):
+    """NCCL all-gather of the score partials (gloo: staged through host tensors)."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend() == "nccl":
+        dist.all_gather_into_tensor(out, inp)
+        return
+    parts = [torch.empty(inp.numel(), dtype=inp.dtype) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, inp.cpu())
+    out.copy_(torch.cat(parts))
+
+
+def all_reduce(x, op):
+    import torch.distributed as dist
+
+    if dist.get_backend() == "nccl":
+        dist.all_reduce(x, op=op)
+        return
+    h = x.cpu()
+    dist.all_reduce(h, op=op)
+    x.copy_(h)
 
 
 def env_int(name, default):
@@ -85,8 +120,46 @@ class ClockSampler:
         self.gpu = gpu_index
         self.proc = None
         self.lines = []
+        self.nvml = None
+
+    def _nvml_handle(self):
+        """NVML handle of the CUDA device (by PCI bus id, so CUDA_VISIBLE_DEVICES is honoured)."""
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        p = torch.cuda.get_device_properties(self.gpu)
+        bus = f"{p.pci_domain_id:08X}:{p.pci_bus_id:02X}:{p.pci_device_id:02X}.0"
+        try:
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+
+    def _poll(self):
+        # NVML directly, every ~2 ms: a 75 ms timed region still gets dozens of samples
+        nv, h = self.nvml
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        while not self.stop.is_set():
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            act = [n for n, b in bits.items() if r & b]
+            self.lines.append(f"{self.gpu}, {sm}, {mx}, 0, 0, " + ", ".join(
+                "Active" if n in act else "Not Active" for n in bits))
+            self.stop.wait(0.002)
 
     def __enter__(self):
+        try:
+            self.nvml = self._nvml_handle()
+            self.stop = threading.Event()
+            self.reader = threading.Thread(target=self._poll, daemon=True)
+            self.reader.start()
+            return self
+        except Exception:
+            self.nvml = None
         if shutil.which("nvidia-smi"):
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "20"],
@@ -100,6 +173,9 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self.nvml:
+            self.stop.set()
+            self.reader.join(timeout=2)
         if self.proc:
             self.proc.terminate()
             try:
@@ -125,7 +201,8 @@ class ClockSampler:
                     reasons.add(n)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml 2 ms" if self.nvml else "nvidia-smi -lms 20"}
 
 
 def ncu_traffic(kernel: str, workload: str):
@@ -261,6 +338,7 @@ def our_arm(args, rank, world, local_rank):
     out_shard = torch.empty(sp0.bytes, dtype=torch.uint8, device=dev)
     out_w = torch.empty(max(16, wp0.bytes), dtype=torch.uint8, device=dev)
     composite = sp0.bytes + wp0.bytes
+    resident = sum(b.numel() for b in shards) + sum(b.numel() for b in wbufs)
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     kt = {"score": [], "gather_shard": [], "gather_weights": []}
@@ -279,7 +357,7 @@ def our_arm(args, rank, world, local_rank):
         scorer.run(bases, partials.data_ptr(), sp)
         e1.record(stream)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, partials)
+            all_gather(gathered, partials)
         allparts = gathered if world > 1 else partials
         if args.host_select:
             yaml, src_of, _, gap = fam.select(allparts.cpu().tolist(), world, rho)
@@ -323,7 +401,7 @@ def our_arm(args, rank, world, local_rank):
     max_ms = total_ms
     if world > 1:
         tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        all_reduce(tt, dist.ReduceOp.MAX)
         max_ms = float(tt.item())
     sec = max_ms / 1e3
     total_bytes = composite * world * args.steps
@@ -371,11 +449,12 @@ def our_arm(args, rank, world, local_rank):
         "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8 (payload bytes) / f32->f64 (scores)", "data": "synthetic",
-        "config": {"workload": args.workload, "description": desc, "model": "Llama-3.1-8B-shaped (reference ModelSpec)",
+        "config": {"workload": args.workload, "description": desc, "model": MODEL_NAMES[args.workload],
                    "params": fam.parameter_count, "zero_ranks": N, "snapshots": K, "rho": rho,
                    "unit_of_work": "one ZeRO rank partition per GPU (optimizer shard + weights share)",
                    "composite_bytes_per_gpu_step": composite, "parallelism": f"zero-partition x{world}",
-                   "l2": "inputs 62 GB/GPU >> 126 MB L2 (no flush needed)",
+                   "l2": f"inputs {resident / 1e9:.1f} GB/GPU vs 126 MB L2"
+                         + (" (no flush needed)" if resident > 1e9 else " (L2-resident: small workload)"),
                    "gather_variant": {0: "auto", 1: "lsu", 2: "bulk-4x48K", 3: "bulk-6x32K", 4: "bulk-2cta-3x32K",
                                       5: "bulk-3x64K", 6: "bulk-8x24K"}[args.variant],
                    "score_variant": SCORE_VARIANTS[args.score_variant],
@@ -419,8 +498,10 @@ def e2e_run(args, t, torch, fam, scorer, shards, wbufs, wlo, yaml, r, N, world, 
     made (tg_family_select); the shard pipeline (tg_mplan_run_host) then copies in
     only the selected bytes that are not already on the device (m, v, weights —
     the selected masters are read from the staged copy), gathers them with K2 and
-    copies the composite out. Units are pipelined: unit i+1's masters H2D and
-    scoring overlap unit i's merge (two staging sets)."""
+    copies the composite out. Units are pipelined: unit i+1's masters ride on unit
+    i's shard pipeline as `prefetch` copies, interleaved with its own inputs on its
+    single H2D stream (one copy engine serves all H2D in submission order), so H2D
+    and D2H stay busy together; two staging sets alternate."""
     import torch.distributed as dist
 
     need = sum(b.numel() for b in shards) + sum(b.numel() for b in wbufs) + 2 * shards[0].numel() + (2 << 30)
@@ -434,7 +515,7 @@ def e2e_run(args, t, torch, fam, scorer, shards, wbufs, wlo, yaml, r, N, world, 
     fits = need * local <= 0.85 * avail
     if world > 1:  # every rank must take the same branch (collectives follow)
         flag = torch.tensor([1 if fits else 0], dtype=torch.int32, device=dev)
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        all_reduce(flag, dist.ReduceOp.MIN)
         fits = bool(flag.item())
     if not fits:
         return {"value": None, "unit": "GB/s",
@@ -454,35 +535,46 @@ def e2e_run(args, t, torch, fam, scorer, shards, wbufs, wlo, yaml, r, N, world, 
     side = torch.cuda.Stream(dev)
     counters = {"h2d": 0, "d2h": 0}
 
+    def masters_of(i):
+        """(host src, device dst, bytes) of unit i's K snapshots' master fields."""
+        st = stage[i % 2]
+        return [(hshards[k].data_ptr() + lo, st[k].data_ptr() + lo, hi - lo)
+                for lo, hi in master_ranges for k in range(K)]
+
     def unit(i):
+        # unit i's masters are on the device already (prefetched by unit i-1's pipeline)
         st = stage[i % 2]
         h2d = d2h = 0
+        spl.wait()
+        wpl.wait()
         with torch.cuda.stream(side):
-            for k in range(K):
-                for lo, hi in master_ranges:
-                    st[k][lo:hi].copy_(hshards[k][lo:hi], non_blocking=True)
-                    h2d += hi - lo
             scorer.run([b.data_ptr() for b in st], partials.data_ptr(), side.cuda_stream)
             if world > 1:
-                dist.all_gather_into_tensor(gathered, partials)
+                all_gather(gathered, partials)
                 parts = gathered.cpu()
             else:
                 parts = partials.cpu()
             d2h += parts.numel() * 8
         y, _, _, _ = fam.select(parts.tolist(), world, rho)
         assert y == yaml
-        wins = spl.windows()
-        a, b = spl.run_host([hshards[k - 1].data_ptr() + lo for k, c, lo, hi in wins], hout.data_ptr(), args.variant,
-                            d_windows=[st[k - 1].data_ptr() + lo for k, c, lo, hi in wins], resident_fields=4,
-                            async_=True)
-        h2d += a
-        d2h += b
         a, b = wpl.run_host([hw[k - 1].data_ptr() + (lo - wlo) for k, c, lo, hi in wpl.windows()], hwout.data_ptr(),
                             args.variant, async_=True)
         h2d += a
         d2h += b
+        # the shard pipeline carries the next unit's masters between its own inputs
+        wins = spl.windows()
+        a, b = spl.run_host([hshards[k - 1].data_ptr() + lo for k, c, lo, hi in wins], hout.data_ptr(), args.variant,
+                            d_windows=[st[k - 1].data_ptr() + lo for k, c, lo, hi in wins], resident_fields=4,
+                            async_=True, prefetch=masters_of(i + 1))
+        h2d += a
+        d2h += b
         counters.update(h2d=h2d, d2h=d2h)
 
+    with torch.cuda.stream(side):  # unit 0's masters (untimed warm-up unit)
+        for k in range(K):
+            for lo, hi in master_ranges:
+                stage[0][k][lo:hi].copy_(hshards[k][lo:hi], non_blocking=True)
+    side.synchronize()
     unit(0)
     spl.wait()
     wpl.wait()
@@ -499,24 +591,43 @@ def e2e_run(args, t, torch, fam, scorer, shards, wbufs, wlo, yaml, r, N, world, 
     dt = time.perf_counter() - t0
     if world > 1:
         tt = torch.tensor([dt], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        all_reduce(tt, dist.ReduceOp.MAX)
         dt = float(tt.item())
     comp = spl.bytes + wpl.bytes
-    # PCIe roofline: measured pinned copy bandwidth each way (1 GiB, best of 3)
-    probe_h = torch.empty(1 << 30, dtype=torch.uint8).pin_memory()
-    probe_d = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
-    bw = {}
-    for name, (dst, src) in {"h2d": (probe_d, probe_h), "d2h": (probe_h, probe_d)}.items():
-        best = 0.0
-        for _ in range(3):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            dst.copy_(src, non_blocking=True)
-            e1.record()
-            torch.cuda.synchronize(dev)
-            best = max(best, (1 << 30) / (e0.elapsed_time(e1) / 1e3) / 1e9)
-        bw[name] = best
-    pcie_floor_s = max(counters["h2d"] / (bw["h2d"] * 1e9), counters["d2h"] / (bw["d2h"] * 1e9))
+    # PCIe roofline: measured pinned copy bandwidth each way alone and both ways at once
+    # (1 GiB, best of 3; tools/pcie_probe.py). While both directions stream, each gets
+    # less than alone (B200 box: ~46 vs ~56 GB/s), so the floor is: the smaller
+    # direction overlapped at the concurrent rate, the rest of the larger one alone.
+    n = 1 << 30
+    probe = [torch.empty(n, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    probe_d = [torch.empty(n, dtype=torch.uint8, device=dev) for _ in range(2)]
+    s_up, s_dn = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def probe_time(up, dn):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record()
+        s_up.wait_event(e0)
+        s_dn.wait_event(e0)
+        if up:
+            with torch.cuda.stream(s_up):
+                probe_d[0].copy_(probe[0], non_blocking=True)
+        if dn:
+            with torch.cuda.stream(s_dn):
+                probe[1].copy_(probe_d[1], non_blocking=True)
+        torch.cuda.current_stream(dev).wait_stream(s_up)
+        torch.cuda.current_stream(dev).wait_stream(s_dn)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / 1e3
+
+    bw = {name: max(n / probe_time(*flags) / 1e9 for _ in range(3))
+          for name, flags in {"h2d": (True, False), "d2h": (False, True), "bidir_each": (True, True)}.items()}
+    H, D = counters["h2d"] / 1e9, counters["d2h"] / 1e9
+    both = min(H, D) / bw["bidir_each"]
+    rest = (H - min(H, D)) / bw["h2d"] + (D - min(H, D)) / bw["d2h"]
+    pcie_floor_s = both + rest
+    naive_floor_s = max(H / bw["h2d"], D / bw["d2h"])
     # the composite the host received must be the device-resident result
     ref = torch.empty(spl.bytes, dtype=torch.uint8, device=dev)
     spl.bind([shards[k - 1].data_ptr() + lo for k, c, lo, hi in spl.windows()])
@@ -528,11 +639,14 @@ def e2e_run(args, t, torch, fam, scorer, shards, wbufs, wlo, yaml, r, N, world, 
             "ms_per_step": round(dt / steps * 1e3, 2), "composite_matches_device_path": ok,
             "pcie_roofline": {"bound": "pcie (host link)", "h2d_gbs_measured": round(bw["h2d"], 1),
                               "d2h_gbs_measured": round(bw["d2h"], 1),
+                              "bidir_gbs_each_measured": round(bw["bidir_each"], 1),
                               "floor_ms_per_step": round(pcie_floor_s * 1e3, 2),
+                              "floor_model": "min(H,D) both ways at the concurrent rate + the rest one way",
+                              "independent_directions_floor_ms": round(naive_floor_s * 1e3, 2),
                               "frac": round(pcie_floor_s / (dt / steps), 4)},
             "path": "C ABI: tg_scorer_run on H2D-staged masters -> tg_family_select -> tg_mplan_run_host "
-                    "(selected masters read from the device staging copy; pinned host sources/destination; "
-                    "units pipelined)"}
+                    "(selected masters read from the device staging copy; the next unit's masters prefetched "
+                    "inside the pipeline's H2D stream; pinned host sources/destination)"}
 
 
 def scorer_arm(args, rank, world, local_rank):
@@ -568,7 +682,7 @@ def scorer_arm(args, rank, world, local_rank):
         scorer.run([b.data_ptr() for b in bufs], partials.data_ptr(), sp)
         e1.record(stream)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, partials)
+            all_gather(gathered, partials)
             parts = gathered.cpu()
         else:
             parts = partials.cpu()
@@ -593,7 +707,7 @@ def scorer_arm(args, rank, world, local_rank):
     ms = start.elapsed_time(end)
     if world > 1:
         tt = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        all_reduce(tt, dist.ReduceOp.MAX)
         ms = float(tt.item())
     kms = statistics.mean(a.elapsed_time(b) for a, b in recs)
     hbm, peak_kind = peaks()
@@ -650,7 +764,7 @@ def trainer_arm(args, rank, world, local_rank):
         dt = time.perf_counter() - t0
     if world > 1:
         tt = torch.tensor([dt], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        all_reduce(tt, dist.ReduceOp.MAX)
         dt = float(tt.item())
     hbm, kind = peaks()
     gbs = 36 * n * args.steps / dt / 1e9
@@ -781,8 +895,13 @@ def init_and(fn, args, rank, world, local_rank):
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if shared_gpu():
+            local_rank %= max(1, torch.cuda.device_count())
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         return fn(args, rank, world, local_rank)
     finally:

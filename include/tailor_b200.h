@@ -217,9 +217,18 @@ int tg_mplan_run(tg_mplan* p, uint8_t* d_dst, int32_t variant, void* stream);
  * from d_windows[w] (device copies of shard windows, e.g. masters staged for
  * scoring) instead of crossing PCIe again. async=1 returns before completion;
  * tg_mplan_wait() (or the next run) synchronizes. */
+typedef struct {
+    const uint8_t* src; /* pinned host */
+    uint8_t* dst;       /* device */
+    uint64_t bytes;
+} tg_host_copy;
+/* `prefetch` (may be NULL): extra host->device copies (e.g. the next unit's
+ * masters) interleaved with the pipeline's own inputs on its H2D stream, sliced
+ * so each chunk's H2D time matches its D2H time (one copy engine serves all
+ * H2D in submission order); complete when the run completes. h2d_bytes counts them. */
 int tg_mplan_run_host(tg_mplan* p, const uint8_t* const* h_windows, const uint8_t* const* d_windows,
                       uint32_t resident_fields, uint8_t* h_dst, int32_t variant, uint64_t chunk_bytes, int32_t async,
-                      uint64_t* h2d_bytes, uint64_t* d2h_bytes);
+                      const tg_host_copy* prefetch, uint32_t nprefetch, uint64_t* h2d_bytes, uint64_t* d2h_bytes);
 int tg_mplan_wait(tg_mplan* p);
 
 /* Whole score -> select -> merge step on the device for one unit (rank-r shard +

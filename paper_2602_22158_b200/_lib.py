@@ -73,6 +73,10 @@ class GatherSegC(ctypes.Structure):
     _fields_ = [("src", ctypes.c_void_p), ("dst_off", ctypes.c_uint64), ("bytes", ctypes.c_uint64)]
 
 
+class HostCopyC(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_void_p), ("dst", ctypes.c_void_p), ("bytes", ctypes.c_uint64)]
+
+
 class ScoreTileC(ctypes.Structure):
     _fields_ = [("module", ctypes.c_uint32), ("field", ctypes.c_uint32), ("count", ctypes.c_uint32),
                 ("pad", ctypes.c_uint32), ("elem_start", ctypes.c_uint64)]
@@ -147,7 +151,8 @@ SIGNATURES = {
     "tg_mplan_bind": (_I, [_P, _PP]),
     "tg_mplan_bulk_ok": (_I32, [_P]),
     "tg_mplan_run": (_I, [_P, _P, _I32, _P]),
-    "tg_mplan_run_host": (_I, [_P, _PP, _PP, _U32, _P, _I32, _U64, _I32, _c.POINTER(_U64), _c.POINTER(_U64)]),
+    "tg_mplan_run_host": (_I, [_P, _PP, _PP, _U32, _P, _I32, _U64, _I32, _c.POINTER(HostCopyC), _U32,
+                               _c.POINTER(_U64), _c.POINTER(_U64)]),
     "tg_mplan_wait": (_I, [_P]),
     "tg_dstep_create": (_P, [_P, _I32, _I32, _I32, _D]),
     "tg_dstep_destroy": (None, [_P]),

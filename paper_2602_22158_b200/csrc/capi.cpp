@@ -662,7 +662,7 @@ int tg_mplan_run(tg_mplan* p, uint8_t* d_dst, int32_t variant, void* stream) {
 
 int tg_mplan_run_host(tg_mplan* p, const uint8_t* const* h_windows, const uint8_t* const* d_windows,
                       uint32_t resident_fields, uint8_t* h_dst, int32_t variant, uint64_t chunk, int32_t async,
-                      uint64_t* h2d, uint64_t* d2h) {
+                      const tg_host_copy* prefetch, uint32_t nprefetch, uint64_t* h2d, uint64_t* d2h) {
     return guard([&] {
         const PartitionPlan& pp = p->dev->plan();
         if (!d_windows) resident_fields = 0;
@@ -689,8 +689,10 @@ int tg_mplan_run_host(tg_mplan* p, const uint8_t* const* h_windows, const uint8_
         }
         std::vector<const std::uint8_t*> dw(pp.windows.size(), nullptr);
         if (d_windows) dw.assign(d_windows, d_windows + pp.windows.size());
+        std::vector<HostCopy> pf;
+        for (uint32_t i = 0; prefetch && i < nprefetch; ++i) pf.push_back({prefetch[i].src, prefetch[i].dst, prefetch[i].bytes});
         p->host->run(std::vector<const std::uint8_t*>(h_windows, h_windows + pp.windows.size()), dw, h_dst, variant,
-                     async != 0);
+                     async != 0, pf);
         if (h2d) *h2d = p->host->h2d_bytes();
         if (d2h) *d2h = p->host->d2h_bytes();
     });

@@ -524,6 +524,7 @@ HostMerge::HostMerge(const PartitionPlan& plan, std::uint64_t chunk_bytes, Resid
             at += p.n;
         }
         c.staging = align16(at);
+        for (const auto& rd : c.reads) c.in_bytes += rd.b - rd.a;
         c.pieces = std::move(ps);
         max_staging_ = std::max(max_staging_, c.staging);
         max_out_ = std::max(max_out_, c.hi - c.lo);
@@ -532,43 +533,79 @@ HostMerge::HostMerge(const PartitionPlan& plan, std::uint64_t chunk_bytes, Resid
 }
 
 HostMerge::~HostMerge() {
-    for (auto& s : stream_)
+    for (cudaStream_t s : {h2d_s_, gather_s_, d2h_s_})
         if (s) {
             cudaStreamSynchronize(s);
             cudaStreamDestroy(s);
         }
+    for (auto* evs : {loaded_, consumed_})
+        for (int i = 0; i < kInSlots; ++i)
+            if (evs[i]) cudaEventDestroy(evs[i]);
+    for (auto* evs : {gathered_, drained_})
+        for (int i = 0; i < kOutSlots; ++i)
+            if (evs[i]) cudaEventDestroy(evs[i]);
 }
 
 void HostMerge::wait() {
-    for (auto& s : stream_)
+    for (cudaStream_t s : {h2d_s_, gather_s_, d2h_s_})
         if (s) cuda_check(cudaStreamSynchronize(s), "sync");
 }
 
 void HostMerge::run(const std::vector<const std::uint8_t*>& h_windows, const std::vector<const std::uint8_t*>& d_windows,
-                    std::uint8_t* h_dst, int variant, bool async) {
+                    std::uint8_t* h_dst, int variant, bool async, const std::vector<HostCopy>& prefetch) {
     if (h_windows.size() != plan_.windows.size()) fail(ErrorKind::Geometry, "window pointer count mismatch");
     wait(); // a previous asynchronous run still owns the staging buffers
     std::size_t max_segs = 1;
     for (const auto& c : chunks_) max_segs = std::max(max_segs, c.pieces.size());
-    for (int i = 0; i < 2; ++i) {
-        if (!stream_[i]) cuda_check(cudaStreamCreateWithFlags(&stream_[i], cudaStreamNonBlocking), "stream");
+    if (!h2d_s_) {
+        for (cudaStream_t* s : {&h2d_s_, &gather_s_, &d2h_s_})
+            cuda_check(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking), "stream");
+        for (auto* evs : {loaded_, consumed_})
+            for (int i = 0; i < kInSlots; ++i) cuda_check(cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming), "event");
+        for (auto* evs : {gathered_, drained_})
+            for (int i = 0; i < kOutSlots; ++i) cuda_check(cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming), "event");
+    }
+    for (int i = 0; i < kInSlots; ++i) {
         stage_[i].resize(std::max<std::uint64_t>(16, max_staging_));
-        out_[i].resize(std::max<std::uint64_t>(16, max_out_));
         segs_[i].resize(max_segs * sizeof(dev::GatherSeg));
     }
-    patched_.assign(chunks_.size(), {});
+    for (int i = 0; i < kOutSlots; ++i) out_[i].resize(std::max<std::uint64_t>(16, max_out_));
+    if (patched_at_.size() != chunks_.size() + 1) {
+        patched_at_.assign(1, 0);
+        for (const auto& c : chunks_) patched_at_.push_back(patched_at_.back() + c.pieces.size());
+        patched_.resize(std::max<std::size_t>(1, patched_at_.back()) * sizeof(dev::GatherSeg));
+    }
     h2d_ = d2h_ = 0;
+    // prefetch cursor: copies are sliced so each chunk's H2D (inputs + slice) matches its D2H
+    std::size_t pf = 0;
+    std::uint64_t pf_off = 0;
+    const auto issue_prefetch = [&](std::uint64_t budget) {
+        while (pf < prefetch.size() && budget > 0) {
+            const HostCopy& c = prefetch[pf];
+            const std::uint64_t n = std::min(budget, c.bytes - pf_off);
+            if (n) cuda_check(cudaMemcpyAsync(c.dst + pf_off, c.src + pf_off, n, cudaMemcpyHostToDevice, h2d_s_), "prefetch");
+            h2d_ += n;
+            budget -= n;
+            pf_off += n;
+            if (pf_off == c.bytes) {
+                ++pf;
+                pf_off = 0;
+            }
+        }
+    };
     for (std::size_t ci = 0; ci < chunks_.size(); ++ci) {
         const Chunk& c = chunks_[ci];
-        const int slot = static_cast<int>(ci & 1);
-        cudaStream_t s = stream_[slot];
+        const int in = static_cast<int>(ci % kInSlots), out = static_cast<int>(ci % kOutSlots);
+        // H2D: the slot's previous gather must be done with its staging and table
+        if (ci >= kInSlots) cuda_check(cudaStreamWaitEvent(h2d_s_, consumed_[in], 0), "wait");
         for (const auto& rd : c.reads) {
-            cuda_check(cudaMemcpyAsync(stage_[slot].get() + rd.at, h_windows[rd.w] + rd.a, rd.b - rd.a,
-                                       cudaMemcpyHostToDevice, s),
+            cuda_check(cudaMemcpyAsync(stage_[in].get() + rd.at, h_windows[rd.w] + rd.a, rd.b - rd.a,
+                                       cudaMemcpyHostToDevice, h2d_s_),
                        "H2D");
             h2d_ += rd.b - rd.a;
         }
-        auto& segs = patched_[ci];
+        dev::GatherSeg* segs = reinterpret_cast<dev::GatherSeg*>(patched_.get()) + patched_at_[ci];
+        std::size_t nseg = 0;
         bool bulk = true;
         std::uint64_t expect = c.lo;
         for (const auto& p : c.pieces) {
@@ -577,23 +614,34 @@ void HostMerge::run(const std::vector<const std::uint8_t*>& h_windows, const std
                 if (d_windows.size() <= p.w || !d_windows[p.w]) fail(ErrorKind::Geometry, "resident window without a device pointer");
                 src = d_windows[p.w] + p.src;
             } else {
-                src = stage_[slot].get() + p.stage;
+                src = stage_[in].get() + p.stage;
             }
-            segs.push_back({src, p.dst - c.lo, p.n});
+            segs[nseg++] = {src, p.dst - c.lo, p.n};
             bulk = bulk && p.dst == expect && reinterpret_cast<std::uintptr_t>(src) % 16 == 0 && p.n % 16 == 0 &&
                    (p.dst - c.lo) % 16 == 0;
             expect = p.dst + p.n;
         }
         bulk = bulk && expect == c.hi;
-        cuda_check(cudaMemcpyAsync(segs_[slot].get(), segs.data(), segs.size() * sizeof(dev::GatherSeg),
-                                   cudaMemcpyHostToDevice, s),
+        cuda_check(cudaMemcpyAsync(segs_[in].get(), segs, nseg * sizeof(dev::GatherSeg), cudaMemcpyHostToDevice, h2d_s_),
                    "segs");
-        cuda_check(dev::launch_gather(segs_[slot].get<dev::GatherSeg>(), static_cast<std::uint32_t>(segs.size()),
-                                      out_[slot].get(), c.hi - c.lo, variant, bulk, s),
+        cuda_check(cudaEventRecord(loaded_[in], h2d_s_), "event");
+        const std::uint64_t out_bytes = c.hi - c.lo;
+        issue_prefetch(out_bytes > c.in_bytes ? out_bytes - c.in_bytes : 0);
+        // gather: inputs loaded, output slot drained by its previous D2H
+        cuda_check(cudaStreamWaitEvent(gather_s_, loaded_[in], 0), "wait");
+        if (ci >= kOutSlots) cuda_check(cudaStreamWaitEvent(gather_s_, drained_[out], 0), "wait");
+        cuda_check(dev::launch_gather(segs_[in].get<dev::GatherSeg>(), static_cast<std::uint32_t>(nseg), out_[out].get(),
+                                      out_bytes, variant, bulk, gather_s_),
                    "gather");
-        cuda_check(cudaMemcpyAsync(h_dst + c.lo, out_[slot].get(), c.hi - c.lo, cudaMemcpyDeviceToHost, s), "D2H");
-        d2h_ += c.hi - c.lo;
+        cuda_check(cudaEventRecord(consumed_[in], gather_s_), "event");
+        cuda_check(cudaEventRecord(gathered_[out], gather_s_), "event");
+        // D2H
+        cuda_check(cudaStreamWaitEvent(d2h_s_, gathered_[out], 0), "wait");
+        cuda_check(cudaMemcpyAsync(h_dst + c.lo, out_[out].get(), out_bytes, cudaMemcpyDeviceToHost, d2h_s_), "D2H");
+        cuda_check(cudaEventRecord(drained_[out], d2h_s_), "event");
+        d2h_ += out_bytes;
     }
+    issue_prefetch(~0ull);
     if (!async) wait();
 }
 

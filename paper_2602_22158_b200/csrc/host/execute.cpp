@@ -93,9 +93,9 @@ class FileAssembler {
             d_in_[i].resize(std::max<std::uint64_t>(16, plan.max_staging));
             d_out_[i].resize(std::max<std::uint64_t>(16, plan.max_out));
             d_segs_[i].resize(std::max<std::size_t>(1, plan.max_segs) * sizeof(dev::GatherSeg));
+            pin_segs_[i].resize(std::max<std::size_t>(1, plan.max_segs) * sizeof(dev::GatherSeg));
         }
         int pending[2] = {-1, -1};
-        std::vector<std::vector<dev::GatherSeg>> patched(plan.chunks.size());
         const auto flush = [&](int slot) {
             if (pending[slot] < 0) return;
             cuda_check(cudaStreamSynchronize(stream_[slot]), "sync");
@@ -133,13 +133,17 @@ class FileAssembler {
             run_reads(jobs, workers_, out_path.string());
             cudaStream_t s = stream_[slot];
             cuda_check(cudaMemcpyAsync(d_in_[slot].get(), pin_in_[slot].get(), c.staging, cudaMemcpyHostToDevice, s), "H2D");
-            patched[ci] = c.segs;
-            for (auto& g : patched[ci]) g.src = d_in_[slot].get() + reinterpret_cast<std::uintptr_t>(g.src);
-            cuda_check(cudaMemcpyAsync(d_segs_[slot].get(), patched[ci].data(), patched[ci].size() * sizeof(dev::GatherSeg),
+            // (the slot's previous chunk has been flushed, so its pinned table is free)
+            auto* segs = reinterpret_cast<dev::GatherSeg*>(pin_segs_[slot].get());
+            for (std::size_t i = 0; i < c.segs.size(); ++i) {
+                segs[i] = c.segs[i];
+                segs[i].src = d_in_[slot].get() + reinterpret_cast<std::uintptr_t>(c.segs[i].src);
+            }
+            cuda_check(cudaMemcpyAsync(d_segs_[slot].get(), segs, c.segs.size() * sizeof(dev::GatherSeg),
                                        cudaMemcpyHostToDevice, s),
                        "segs");
             cuda_check(cudaEventRecord(ev0_[slot], s), "event");
-            cuda_check(dev::launch_gather(d_segs_[slot].get<dev::GatherSeg>(), static_cast<std::uint32_t>(patched[ci].size()),
+            cuda_check(dev::launch_gather(d_segs_[slot].get<dev::GatherSeg>(), static_cast<std::uint32_t>(c.segs.size()),
                                           d_out_[slot].get(), c.hi - c.lo, dev::kGatherAuto, c.bulk_ok, s),
                        "gather");
             cuda_check(cudaEventRecord(ev1_[slot], s), "event");
@@ -237,7 +241,7 @@ class FileAssembler {
     bool uncached_;
     cudaStream_t stream_[2]{};
     cudaEvent_t ev0_[2]{}, ev1_[2]{};
-    PinnedBuffer pin_in_[2], pin_out_[2];
+    PinnedBuffer pin_in_[2], pin_out_[2], pin_segs_[2]; // pinned: async uploads never sync the stream
     DeviceBuffer d_in_[2], d_out_[2], d_segs_[2];
     std::map<std::string, std::uint64_t> payload_off_;
 };

@@ -196,10 +196,23 @@ class DeviceSelectStep {
 
 // Pipelined host->device->host assembly of one partition from host (pinned)
 // source windows into a host destination: per chunk, only the bytes the
-// chunk needs are copied in, gathered on the device and copied out, on two
-// streams so H2D, the gather and D2H of consecutive chunks overlap. Source
+// chunk needs are copied in, gathered on the device and copied out. Source
 // byte ranges listed as `resident` (window-relative) are read straight from
 // device copies instead (e.g. masters already staged for scoring).
+//
+// All host->device copies of a GPU go through one copy engine in submission
+// order (measured: a 1 MB H2D on another stream waits behind a 2 GB one,
+// tools/pcie_ce_probe.cu), so the pipeline owns the order: one H2D stream
+// carries the chunk inputs and, between them, slices of the caller's
+// `prefetch` copies (e.g. the next unit's masters), sized so that each chunk's
+// H2D time matches its D2H time; a gather stream and a D2H stream follow via
+// events. The link then stays busy in both directions.
+struct HostCopy {
+    const std::uint8_t* src; // pinned host
+    std::uint8_t* dst;       // device
+    std::uint64_t bytes;
+};
+
 class HostMerge {
   public:
     using Resident = std::vector<std::vector<std::pair<std::uint64_t, std::uint64_t>>>;
@@ -208,12 +221,13 @@ class HostMerge {
     // h_windows[w] = host address of window w's first byte; d_windows[w] = device
     // address (only needed for windows with resident ranges); h_dst = output byte dst_lo.
     void run(const std::vector<const std::uint8_t*>& h_windows, const std::vector<const std::uint8_t*>& d_windows,
-             std::uint8_t* h_dst, int variant, bool async = false);
+             std::uint8_t* h_dst, int variant, bool async = false, const std::vector<HostCopy>& prefetch = {});
     void wait();
     std::uint64_t h2d_bytes() const { return h2d_; }
     std::uint64_t d2h_bytes() const { return d2h_; }
 
   private:
+    static constexpr int kInSlots = 3, kOutSlots = 2;
     struct Piece {
         std::uint32_t w;
         std::uint64_t src, dst, n;
@@ -228,15 +242,17 @@ class HostMerge {
         std::uint64_t lo, hi; // output range (relative to dst_lo)
         std::vector<Piece> pieces;
         std::vector<Read> reads;
-        std::uint64_t staging = 0;
+        std::uint64_t staging = 0, in_bytes = 0;
     };
     PartitionPlan plan_;
     Resident resident_;
     std::vector<Chunk> chunks_;
     std::uint64_t max_staging_ = 0, max_out_ = 0;
-    DeviceBuffer stage_[2], out_[2], segs_[2];
-    cudaStream_t stream_[2]{};
-    std::vector<std::vector<dev::GatherSeg>> patched_;
+    DeviceBuffer stage_[kInSlots], segs_[kInSlots], out_[kOutSlots];
+    cudaStream_t h2d_s_ = nullptr, gather_s_ = nullptr, d2h_s_ = nullptr;
+    cudaEvent_t loaded_[kInSlots]{}, consumed_[kInSlots]{}, gathered_[kOutSlots]{}, drained_[kOutSlots]{};
+    PinnedBuffer patched_;                 // per-chunk segment tables (pinned: the async
+    std::vector<std::size_t> patched_at_;  // uploads must not sync the stream)
     std::uint64_t h2d_ = 0, d2h_ = 0;
 };
 

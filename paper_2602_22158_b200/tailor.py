@@ -21,7 +21,7 @@ import json
 import os
 from typing import Dict, List, Optional, Sequence
 
-from ._lib import (ErrorKind, GatherSegC, MergeOptionsC, MergeStatsC, ModelSpecC, TailorError, check,
+from ._lib import (ErrorKind, GatherSegC, HostCopyC, MergeOptionsC, MergeStatsC, ModelSpecC, TailorError, check,
                    check_handle, lib, ptr_array, text_call)
 
 __all__ = ["ErrorKind", "TailorError", "ModelSpec", "RecipeSlice", "MergeRecipe", "MergeOptions", "MergeStats",
@@ -373,13 +373,17 @@ class MergePartition:
         check(lib().tg_mplan_run(self._h, d_dst, variant, stream))
 
     def run_host(self, h_windows: Sequence[int], h_dst: int, variant: int = 0, chunk_bytes: int = 0,
-                 d_windows: Optional[Sequence[int]] = None, resident_fields: int = 0, async_: bool = False):
+                 d_windows: Optional[Sequence[int]] = None, resident_fields: int = 0, async_: bool = False,
+                 prefetch: Optional[Sequence[tuple]] = None):
         """Shard pipeline from pinned host windows; `resident_fields` (1 exp_avg, 2 exp_avg_sq,
-        4 master) are read from `d_windows` instead of crossing PCIe."""
+        4 master) are read from `d_windows` instead of crossing PCIe. `prefetch`: extra
+        (host_src, device_dst, bytes) copies interleaved on the pipeline's H2D stream."""
         h2d, d2h = ctypes.c_uint64(), ctypes.c_uint64()
         dw = ptr_array(d_windows) if d_windows is not None else None
+        pf = (HostCopyC * max(1, len(prefetch or ())))(*[HostCopyC(int(s), int(d), int(n)) for s, d, n in prefetch or ()])
         check(lib().tg_mplan_run_host(self._h, ptr_array(h_windows), dw, resident_fields if dw else 0, h_dst, variant,
-                                      chunk_bytes, 1 if async_ else 0, ctypes.byref(h2d), ctypes.byref(d2h)))
+                                      chunk_bytes, 1 if async_ else 0, pf, len(prefetch or ()), ctypes.byref(h2d),
+                                      ctypes.byref(d2h)))
         return h2d.value, d2h.value
 
     def wait(self) -> None:
