@@ -55,12 +55,16 @@ WORKLOADS = {
              "tiny Llama-style 4-layer (hidden 256), 2 sources half-layer merge, 1 ZeRO rank"),
     "cfg4": (32, 4096, 14336, 128256, False, 8, 16, 0.5,
              "Llama-3.1-8B-shaped update-norm scoring sweep over 16 consecutive snapshots (scorer only)"),
+    "cfg5": (80, 8192, 28672, 128256, False, 8, 4, 0.5,
+             "Llama-3-70B-shaped ZeRO-3 8-rank merge of 4 sources with pinned host staging "
+             "(partitions exceed single-pass HBM budget)"),
 }
 # Reference-arm / cpu_baseline sample: cfg3's merge, shrunk to fit a few
 # seconds of CPU work per step (same layout rules, 8 ranks, 4 snapshots).
 SAMPLE = (1, 1024, 3584, 4096, False, 8, 4, 0.5)
 MODEL_NAMES = {"cfg1": "tiny Llama-style (reference ModelSpec)", "cfg2": "Qwen2.5-7B-shaped (reference ModelSpec)",
-               "cfg3": "Llama-3.1-8B-shaped (reference ModelSpec)", "cfg4": "Llama-3.1-8B-shaped (reference ModelSpec)"}
+               "cfg3": "Llama-3.1-8B-shaped (reference ModelSpec)", "cfg4": "Llama-3.1-8B-shaped (reference ModelSpec)",
+               "cfg5": "Llama-3-70B-shaped (reference ModelSpec)"}
 SCORE_VARIANTS = {0: "auto", 1: "register", 2: "staged", 3: "register-128b", 4: "register-64b"}
 
 
@@ -491,6 +495,38 @@ def our_arm(args, rank, world, local_rank):
     return 0
 
 
+def pcie_rates(torch, dev):
+    """Measured pinned copy bandwidth (GB/s) H2D alone, D2H alone and each way while both
+    stream at once (1 GiB, best of 3; tools/pcie_probe.py). Under bidirectional load each
+    direction gets less than alone (B200 box: ~48 vs ~56 GB/s), so host-link floors are:
+    the smaller direction overlapped at the concurrent rate, the rest of the larger alone."""
+    n = 1 << 30
+    probe = [torch.empty(n, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    probe_d = [torch.empty(n, dtype=torch.uint8, device=dev) for _ in range(2)]
+    s_up, s_dn = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def probe_time(up, dn):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record()
+        s_up.wait_event(e0)
+        s_dn.wait_event(e0)
+        if up:
+            with torch.cuda.stream(s_up):
+                probe_d[0].copy_(probe[0], non_blocking=True)
+        if dn:
+            with torch.cuda.stream(s_dn):
+                probe[1].copy_(probe_d[1], non_blocking=True)
+        torch.cuda.current_stream(dev).wait_stream(s_up)
+        torch.cuda.current_stream(dev).wait_stream(s_dn)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / 1e3
+
+    return {name: max(n / probe_time(*flags) / 1e9 for _ in range(3))
+            for name, flags in {"h2d": (True, False), "d2h": (False, True), "bidir_each": (True, True)}.items()}
+
+
 def e2e_run(args, t, torch, fam, scorer, shards, wbufs, wlo, yaml, r, N, world, dev, sp, K, M, rho):
     """The same step with HOST (pinned) sources and destination, through the C ABI:
     per unit, the K snapshots' master fields go H2D into a device staging set and
@@ -594,35 +630,7 @@ def e2e_run(args, t, torch, fam, scorer, shards, wbufs, wlo, yaml, r, N, world, 
         all_reduce(tt, dist.ReduceOp.MAX)
         dt = float(tt.item())
     comp = spl.bytes + wpl.bytes
-    # PCIe roofline: measured pinned copy bandwidth each way alone and both ways at once
-    # (1 GiB, best of 3; tools/pcie_probe.py). While both directions stream, each gets
-    # less than alone (B200 box: ~46 vs ~56 GB/s), so the floor is: the smaller
-    # direction overlapped at the concurrent rate, the rest of the larger one alone.
-    n = 1 << 30
-    probe = [torch.empty(n, dtype=torch.uint8).pin_memory() for _ in range(2)]
-    probe_d = [torch.empty(n, dtype=torch.uint8, device=dev) for _ in range(2)]
-    s_up, s_dn = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-
-    def probe_time(up, dn):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize(dev)
-        e0.record()
-        s_up.wait_event(e0)
-        s_dn.wait_event(e0)
-        if up:
-            with torch.cuda.stream(s_up):
-                probe_d[0].copy_(probe[0], non_blocking=True)
-        if dn:
-            with torch.cuda.stream(s_dn):
-                probe[1].copy_(probe_d[1], non_blocking=True)
-        torch.cuda.current_stream(dev).wait_stream(s_up)
-        torch.cuda.current_stream(dev).wait_stream(s_dn)
-        e1.record()
-        torch.cuda.synchronize(dev)
-        return e0.elapsed_time(e1) / 1e3
-
-    bw = {name: max(n / probe_time(*flags) / 1e9 for _ in range(3))
-          for name, flags in {"h2d": (True, False), "d2h": (False, True), "bidir_each": (True, True)}.items()}
+    bw = pcie_rates(torch, dev)
     H, D = counters["h2d"] / 1e9, counters["d2h"] / 1e9
     both = min(H, D) / bw["bidir_each"]
     rest = (H - min(H, D)) / bw["h2d"] + (D - min(H, D)) / bw["d2h"]
@@ -733,6 +741,164 @@ def scorer_arm(args, rank, world, local_rank):
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": scorer.bytes_read, "traffic": traffic, "traffic_source": src},
         "gpu_launches": args.steps * 2, "clocks": clocks.summary()}))
+    return 0
+
+
+def hoststaged_arm(args, rank, world, local_rank):
+    """cfg5 (Llama-3-70B-shaped, 8 ZeRO ranks, 4 sources): one rank partition per GPU
+    is 4 x 120 GB of source shards + 4 x 20 GB of weights — more than HBM (180 GB) and
+    than this box's host RAM (196 GB), so sources live in pinned host memory one
+    window at a time. The timed work per step is the host-staged pipeline itself:
+      A. masters of the 4 snapshots (4 x 40 GB, packed) H2D, scored pair by pair as
+         they arrive (two device slots, K3/K4 per consecutive pair);
+      B. selection (all-gathered partials), then the composite shard partition in
+         tensor-aligned sub-units (tg_mplan sub-ranges) and the weights share in
+         pieces, each through tg_mplan_run_host (H2D of the needed bytes -> K2 -> D2H).
+    Between timed pieces the next window's source bytes are materialised (K5 on the
+    device -> D2H into pinned host buffers; untimed, like every other workload's
+    input generation). Every sub-unit's host output is checked against a device
+    gather of the same windows."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_22158_b200 as t
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    L, h, f, v, tied, N, K, rho, desc = WORKLOADS[args.workload]
+    if world > N:
+        raise SystemExit(f"cfg5 has {N} rank partitions; cannot run on {world} GPUs")
+    fam = t.SynthFamily(t.ModelSpec(L, h, f, v, tied, 42), N, K, 100)
+    M, r = fam.num_modules, rank
+    sp = torch.cuda.current_stream(dev).cuda_stream
+    U, UW = env_int("TAILOR_CFG5_UNITS", 8), 2  # shard sub-units, weights pieces per share
+
+    def sync_time(fn):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize(dev)
+        return time.perf_counter() - t0
+
+    def pass_a():
+        """Masters H2D + pairwise scoring; returns (seconds timed, bytes H2D, partials)."""
+        pm = fam.packed_master_bytes(r)
+        slots = [torch.empty(pm, dtype=torch.uint8, device=dev) for _ in range(2)]
+        host = torch.empty(pm, dtype=torch.uint8, pin_memory=True)
+        partials = torch.zeros((K - 1) * M * 2, dtype=torch.float64, device=dev)
+        scorers = {k: t.Scorer(fam, r, k - 1, k, packed=True) for k in range(2, K + 1)}
+        secs = 0.0
+        for k in range(1, K + 1):
+            slot = slots[(k - 1) % 2]
+            fam.gen_masters(r, k, k, [slot.data_ptr()], sp)  # materialise snapshot k's masters ...
+            host.copy_(slot)                                    # ... into pinned host memory
+            slot.zero_()
+            secs += sync_time(lambda: slot.copy_(host, non_blocking=True))  # timed: H2D
+            if k >= 2:
+                p = k - 2
+                out = partials[p * M * 2:(p + 1) * M * 2]
+                secs += sync_time(lambda: scorers[k].run([slots[(k - 2) % 2].data_ptr(), slot.data_ptr()],
+                                                         out.data_ptr(), sp))
+        del slots, host
+        return secs, K * pm, partials
+
+    def pass_b(yaml):
+        """Composite shard partition in sub-units + weights share in pieces, host-staged."""
+        plans = [t.MergePartition(fam, yaml, r, u, U) for u in range(U)]
+        plans += [t.MergePartition(fam, yaml, -1, r * UW + j, N * UW) for j in range(UW)]
+        win_bytes = max(sum(hi - lo for _, _, lo, hi in p.windows()) for p in plans)
+        out_bytes = max(p.bytes for p in plans)
+        hwin = torch.empty(win_bytes, dtype=torch.uint8, pin_memory=True)
+        hout = torch.empty(out_bytes, dtype=torch.uint8, pin_memory=True)
+        dwin = torch.empty(win_bytes, dtype=torch.uint8, device=dev)
+        dref = torch.empty(out_bytes, dtype=torch.uint8, device=dev)
+        secs, h2d, d2h, comp, ok = 0.0, 0, 0, 0, True
+        piece_s.clear()
+        for p in plans:
+            offs, at = [], 0
+            for k, c, lo, hi in p.windows():   # materialise this piece's source windows
+                if c >= 0:
+                    fam.gen_shard_range(c, k, lo, hi, dwin.data_ptr() + at, sp)
+                else:
+                    fam.gen_weights(k, k, lo, hi, [dwin.data_ptr() + at], sp)
+                offs.append(at)
+                at += hi - lo
+            hwin[:at].copy_(dwin[:at])
+            p.bind([dwin.data_ptr() + o for o in offs])  # device reference of the same windows
+            p.run(dref.data_ptr(), args.variant, sp)
+            res = {}
+
+            def run():
+                res["io"] = p.run_host([hwin.data_ptr() + o for o in offs], hout.data_ptr(), args.variant)
+
+            dt = sync_time(run)
+            secs += dt
+            piece_s.append((round(dt, 4), round(p.bytes / 1e9, 2), len(offs)))
+            if os.environ.get("TAILOR_CFG5_REPEAT"):  # diagnostics: steady-state time of the same piece
+                piece_s[-1] += (round(sync_time(run), 4),)
+            h2d += res["io"][0]
+            d2h += res["io"][1]
+            comp += p.bytes
+            ok = ok and bool(torch.equal(hout[:p.bytes].to(dev), dref[:p.bytes]))
+        del hwin, hout, dwin, dref
+        return secs, h2d, d2h, comp, ok
+
+    piece_s = []
+
+    def step():
+        sa, ha, partials = pass_a()
+        if world > 1:
+            gathered = torch.zeros(world * partials.numel(), dtype=torch.float64, device=dev)
+            all_gather(gathered, partials)
+            parts = gathered
+        else:
+            parts = partials
+        t0 = time.perf_counter()
+        yaml, src, _, gap = fam.select(parts.cpu().tolist(), world, rho)
+        sel = time.perf_counter() - t0
+        sb, hb, db, comp, ok = pass_b(yaml)
+        return {"secs": sa + sel + sb, "score_s": sa, "merge_s": sb, "h2d": ha + hb, "d2h": db + parts.numel() * 8,
+                "comp": comp, "ok": ok, "gap": gap, "sources": src}
+
+    with ClockSampler(local_rank) as clocks:
+        rec = [step() for _ in range(max(1, args.steps))]
+    secs = sum(x["secs"] for x in rec)
+    if world > 1:
+        tt = torch.tensor([secs], dtype=torch.float64, device=dev)
+        all_reduce(tt, dist.ReduceOp.MAX)
+        secs = float(tt.item())
+    last = rec[-1]
+    n = len(rec)
+    value = last["comp"] * world * n / secs / 1e9
+    # host-link roofline of the same bytes (bidirectional model as in e2e_run)
+    H, D = last["h2d"] / 1e9, last["d2h"] / 1e9
+    probe = pcie_rates(torch, dev)
+    both = min(H, D) / probe["bidir_each"]
+    floor = both + (H - min(H, D)) / probe["h2d"] + (D - min(H, D)) / probe["d2h"]
+    if rank != 0:
+        return 0
+    line = {
+        "metric": "composite-checkpoint merge GB/s (score+select+merge), host-staged", "value": round(value, 3),
+        "unit": "GB/s", "n_gpus": world, "steps": n, "warmup": 0, "ms_per_step": round(secs / n * 1e3, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8 (payload bytes) / f32->f64 (scores)", "data": "synthetic",
+        "config": {"workload": "cfg5", "description": desc, "model": MODEL_NAMES["cfg5"],
+                   "params": fam.parameter_count, "zero_ranks": N, "snapshots": K, "rho": rho,
+                   "unit_of_work": "one ZeRO rank partition per GPU, host-staged in sub-units",
+                   "shard_sub_units": U, "weights_pieces": UW, "composite_bytes_per_gpu_step": last["comp"],
+                   "min_boundary_gap": last["gap"], "score_s": round(last["score_s"], 3),
+                   "merge_s": round(last["merge_s"], 3), "merge_piece_s": piece_s,
+                   "source_materialisation": "K5 window by window into pinned host buffers, untimed"},
+        "host_output_matches_device_gather": all(x["ok"] for x in rec),
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": last["h2d"],
+                "d2h_bytes_per_step": last["d2h"],
+                "note": "the measurement itself is end to end (pinned host sources and destination)"},
+        "roofline": {"bound": "pcie (host link)", "achieved": round((H + D) / (secs / n), 2), "unit": "GB/s",
+                     "floor_ms_per_step": round(floor * 1e3, 1), "frac": round(floor / (secs / n), 4),
+                     "h2d_gbs_measured": round(probe["h2d"], 1), "d2h_gbs_measured": round(probe["d2h"], 1),
+                     "bidir_gbs_each_measured": round(probe["bidir_each"], 1)},
+        "gpu_launches": None, "clocks": clocks.summary()}
+    print(json.dumps(line))
     return 0
 
 
@@ -883,6 +1049,8 @@ def main():
         return reference_arm(args, rank, world)
     if args.workload == "cfg4":
         return init_and(scorer_arm, args, rank, world, local_rank)
+    if args.workload == "cfg5":
+        return init_and(hoststaged_arm, args, rank, world, local_rank)
     if args.workload == "files":
         return files_arm(args) if rank == 0 else 0
     if args.workload == "train":

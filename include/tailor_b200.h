@@ -183,6 +183,9 @@ int tg_family_gen_shard(tg_family* f, int32_t rank, int32_t k0, int32_t k1, uint
 int tg_family_gen_weights(tg_family* f, int32_t k0, int32_t k1, uint64_t lo, uint64_t hi, uint8_t* const* outs,
                           void* stream);
 int tg_family_gen_masters(tg_family* f, int32_t rank, int32_t k0, int32_t k1, uint8_t* const* outs, void* stream);
+/* Bytes [lo, hi) of snapshot k's rank shard payload (tensor-aligned; e.g. one merge window). */
+int tg_family_gen_shard_range(tg_family* f, int32_t rank, int32_t k, uint64_t lo, uint64_t hi, uint8_t* out,
+                              void* stream);
 int tg_family_write_dir(tg_family* f, int32_t k, const char* dir);
 /* Combine per-rank partials [nranks][K-1][M][2] in rank order, select (a14),
  * emit the recipe over the family's snapshot ids. */
@@ -200,7 +203,8 @@ int tg_scorer_set_variant(tg_scorer* s, int32_t variant);
 int tg_scorer_run(tg_scorer* s, const uint8_t* const* bases, double* d_out, void* stream);
 
 /* Merge plan of one output partition of a recipe over family snapshots:
- * container = -1 -> weights bytes of share unit/units, r >= 0 -> rank r shard. */
+ * container = -1 -> weights bytes of share unit/units, r >= 0 -> rank r shard
+ * (units > 1: its unit-th tensor-aligned byte sub-range, for host-staged units). */
 tg_mplan* tg_mplan_create(tg_family* f, const char* recipe_yaml, int32_t container, int32_t unit, int32_t units);
 void tg_mplan_destroy(tg_mplan* p);
 uint64_t tg_mplan_bytes(const tg_mplan* p);

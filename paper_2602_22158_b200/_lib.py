@@ -132,6 +132,7 @@ SIGNATURES = {
     "tg_family_gen_shard": (_I, [_P, _I32, _I32, _I32, _PP, _P]),
     "tg_family_gen_weights": (_I, [_P, _I32, _I32, _U64, _U64, _PP, _P]),
     "tg_family_gen_masters": (_I, [_P, _I32, _I32, _I32, _PP, _P]),
+    "tg_family_gen_shard_range": (_I, [_P, _I32, _I32, _U64, _U64, _P, _P]),
     "tg_family_write_dir": (_I, [_P, _I32, _S]),
     "tg_family_select": (_I, [_P, _c.POINTER(_D), _I32, _D, _c.c_char_p, _SZ, _PSZ, _c.POINTER(_I32),
                               _c.POINTER(_D), _c.POINTER(_D)]),

@@ -502,6 +502,10 @@ int tg_family_gen_masters(tg_family* f, int32_t rank, int32_t k0, int32_t k1, ui
     return guard([&] { f->fam->gen_masters_packed(rank, k0, k1, outs, static_cast<cudaStream_t>(stream)); });
 }
 
+int tg_family_gen_shard_range(tg_family* f, int32_t rank, int32_t k, uint64_t lo, uint64_t hi, uint8_t* out, void* stream) {
+    return guard([&] { f->fam->gen_shard_range(rank, k, lo, hi, out, static_cast<cudaStream_t>(stream)); });
+}
+
 int tg_family_write_dir(tg_family* f, int32_t k, const char* dir) {
     return guard([&] { f->fam->write_dir(k, dir ? dir : ""); });
 }
@@ -602,6 +606,10 @@ tg_mplan* tg_mplan_create(tg_family* f, const char* yaml, int32_t container, int
         } else {
             if (container >= plan.num_ranks) fail(ErrorKind::Geometry, "rank out of range");
             pp = plan_shard(plan, lay_of, container);
+            if (units > 1) { // sub-unit of the rank partition, split at tensor boundaries
+                const auto [lo, hi] = weights_share(pp.out, unit, units);
+                pp = plan_shard(plan, lay_of, container, lo, hi);
+            }
         }
         auto* p = new tg_mplan{};
         for (const auto& w : pp.windows) {

@@ -308,6 +308,56 @@ void SynthFamily::gen_masters_packed(int rank, int k0, int k1, std::uint8_t* con
                "synth masters");
 }
 
+void SynthFamily::gen_shard_range(int rank, int k, std::uint64_t lo, std::uint64_t hi, std::uint8_t* out,
+                                  cudaStream_t s) {
+    if (rank < 0 || rank >= num_ranks_) fail(ErrorKind::Geometry, "rank out of range");
+    if (k < 1 || k > K_) fail(ErrorKind::Geometry, "snapshot out of bounds");
+    ensure_sigma(k);
+    const ShardGeometry geom{num_ranks_};
+    const ContainerLayout& c = layout(k).shards[static_cast<std::size_t>(rank)];
+    std::vector<dev::SynthGroup> groups;
+    std::vector<dev::SynthSlice> slices;
+    std::uint64_t begin = 0;
+    for (int g : layout(k).groups) {
+        dev::SynthGroup sg{};
+        bool any = false;
+        int f = 0;
+        for (const char* field : {".exp_avg", ".exp_avg_sq", ".master"}) {
+            const Entry* e = c.find(shard_key(g, field));
+            sg.off[f] = ~0ull;
+            if (e->end > lo && e->begin < hi) {
+                if (e->begin < lo || e->end > hi) fail(ErrorKind::Geometry, "shard window must be tensor-aligned");
+                sg.off[f] = e->begin - lo;
+                any = true;
+            }
+            ++f;
+        }
+        const GroupInfo& info = model_.table().groups[static_cast<std::size_t>(g)];
+        const std::int64_t chunk = geom.shard_length(info.element_count);
+        if (!any || chunk <= 0) continue;
+        sg.begin = begin;
+        sg.chunk = static_cast<std::uint64_t>(chunk);
+        sg.group_first = static_cast<std::uint64_t>(rank) * static_cast<std::uint64_t>(chunk);
+        sg.true_len = static_cast<std::uint64_t>(info.element_count);
+        sg.slice_begin = static_cast<std::uint32_t>(slices.size());
+        for (const auto& sl : model_.slices(g)) slices.push_back({sl.group_offset, sl.model_offset, sl.decl.numel()});
+        sg.slice_count = static_cast<std::uint32_t>(model_.slices(g).size());
+        sg.module = static_cast<std::uint32_t>(model_.owner_index(g));
+        groups.push_back(sg);
+        begin += static_cast<std::uint64_t>(chunk);
+    }
+    if (groups.empty()) return;
+    if (s) cuda_check(cudaStreamSynchronize(s), "sync");
+    DeviceBuffer dg, ds;
+    dg.upload(groups.data(), groups.size() * sizeof(dev::SynthGroup));
+    ds.upload(slices.data(), slices.size() * sizeof(dev::SynthSlice));
+    cuda_check(dev::launch_synth_shard(dg.get<dev::SynthGroup>(), static_cast<std::uint32_t>(groups.size()),
+                                       ds.get<dev::SynthSlice>(), sigma_.get<float>(), model_.module_count(),
+                                       model_.spec().seed, k, k, out_ptrs(&out, 1), begin, s),
+               "synth shard range");
+    cuda_check(s ? cudaStreamSynchronize(s) : cudaDeviceSynchronize(), "sync"); // tables are freed on return
+}
+
 void SynthFamily::gen_weights(int k0, int k1, std::uint64_t lo, std::uint64_t hi, std::uint8_t* const* outs,
                               cudaStream_t s) {
     if (k0 < 1 || k1 > K_ || k0 > k1) fail(ErrorKind::Geometry, "snapshot range out of bounds");

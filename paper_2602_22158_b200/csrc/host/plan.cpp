@@ -202,7 +202,7 @@ PartitionPlan plan_weights(const MergePlan& plan, const LayoutLookup& layouts, s
     return pp;
 }
 
-PartitionPlan plan_shard(const MergePlan& plan, const LayoutLookup& layouts, int rank) {
+PartitionPlan plan_shard(const MergePlan& plan, const LayoutLookup& layouts, int rank, std::uint64_t lo, std::uint64_t hi) {
     const ShardGeometry geom{plan.num_ranks};
     std::vector<EntryDecl> decls;
     std::vector<Piece> pending; // dst offsets filled after layout
@@ -236,10 +236,14 @@ PartitionPlan plan_shard(const MergePlan& plan, const LayoutLookup& layouts, int
     PartitionPlan pp;
     pp.out = layout_for(std::move(decls),
                         {{"num_ranks", std::to_string(plan.num_ranks)}, {"rank", std::to_string(rank)}});
-    pp.dst_lo = 0;
-    pp.dst_hi = pp.out.payload_bytes;
+    pp.dst_lo = std::min(lo, pp.out.payload_bytes);
+    pp.dst_hi = std::min(hi, pp.out.payload_bytes);
     std::vector<Piece> pieces;
-    for (const auto& w : wants) pieces.push_back({w.source, rank, w.src_off, pp.out.find(w.dst)->begin, w.bytes});
+    for (const auto& w : wants) {
+        const std::uint64_t d0 = pp.out.find(w.dst)->begin, d1 = d0 + w.bytes;
+        const std::uint64_t a = std::max(d0, pp.dst_lo), b = std::min(d1, pp.dst_hi);
+        if (a < b) pieces.push_back({w.source, rank, w.src_off + (a - d0), a, b - a});
+    }
     finish_plan(pp, std::move(pieces));
     return pp;
 }

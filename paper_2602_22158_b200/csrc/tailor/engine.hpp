@@ -84,6 +84,8 @@ class SynthFamily {
     void gen_weights(int k0, int k1, std::uint64_t lo, std::uint64_t hi, std::uint8_t* const* outs, cudaStream_t s);
     // Masters only, packed per field in score-field order (for scorer-only sweeps).
     void gen_masters_packed(int rank, int k0, int k1, std::uint8_t* const* outs, cudaStream_t s);
+    // bytes [lo, hi) of snapshot k's rank shard payload; entry-aligned (synchronous table upload)
+    void gen_shard_range(int rank, int k, std::uint64_t lo, std::uint64_t hi, std::uint8_t* out, cudaStream_t s);
     std::uint64_t packed_master_bytes(int rank) const;
     // GPU-generate snapshot k and write it as a checkpoint directory.
     void write_dir(int k, const std::string& dir);

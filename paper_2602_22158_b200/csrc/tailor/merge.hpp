@@ -141,9 +141,12 @@ void finalize_partition(PartitionPlan& pp, std::vector<CopyPiece> pieces);
 PartitionPlan plan_weights(const MergePlan& plan, const LayoutLookup& layouts, std::uint64_t lo = 0,
                            std::uint64_t hi = UINT64_MAX);
 // Rank-r shard container plan (checks as copy_shard_entries, R/src/merge.cpp:207-222).
-PartitionPlan plan_shard(const MergePlan& plan, const LayoutLookup& layouts, int rank);
-// Byte range of the composite weights payload owned by unit u of n: split at
-// tensor boundaries, balanced by bytes.
+// [lo, hi): a byte sub-range of the composite shard payload (host-staged units of
+// partitions that exceed one pass through HBM, e.g. cfg5).
+PartitionPlan plan_shard(const MergePlan& plan, const LayoutLookup& layouts, int rank, std::uint64_t lo = 0,
+                         std::uint64_t hi = UINT64_MAX);
+// Byte range of a container payload owned by unit u of n: split at tensor
+// boundaries, balanced by bytes (weights shares; shard sub-units).
 std::pair<std::uint64_t, std::uint64_t> weights_share(const ContainerLayout& out, int unit, int units);
 
 OptimMeta merged_optim_meta(const MergePlan& plan, const SummaryLookup& lookup);

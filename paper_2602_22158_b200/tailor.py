@@ -278,6 +278,10 @@ class SynthFamily:
     def gen_masters(self, rank: int, k0: int, k1: int, outs: Sequence[int], stream: int = 0) -> None:
         check(lib().tg_family_gen_masters(self._h, rank, k0, k1, ptr_array(outs), stream))
 
+    def gen_shard_range(self, rank: int, k: int, lo: int, hi: int, out: int, stream: int = 0) -> None:
+        """Bytes [lo, hi) of snapshot k's rank shard payload (tensor-aligned window)."""
+        check(lib().tg_family_gen_shard_range(self._h, rank, k, lo, hi, out, stream))
+
     def write_dir(self, k: int, path: str) -> None:
         check(lib().tg_family_write_dir(self._h, k, _b(str(path))))
 
@@ -321,7 +325,8 @@ class Scorer:
 
 
 class MergePartition:
-    """K2 plan for one output partition: container=-1 -> weights share unit/units, r -> rank-r shard."""
+    """K2 plan for one output partition: container=-1 -> weights share unit/units, r -> rank-r shard
+    (units > 1: its unit-th tensor-aligned byte sub-range)."""
 
     def __init__(self, family: SynthFamily, recipe_yaml: str, container: int, unit: int = 0, units: int = 1):
         self._fam = family

@@ -239,6 +239,71 @@ def test_host_pipeline_matches_device():
             assert h2d2 == mp.bytes * frac // 3 or (fields == 4 and 0 < h2d2 < mp.bytes)
 
 
+def test_host_pipeline_prefetch_copies():
+    """tg_mplan_run_host's prefetch list: extra H2D copies land intact, the composite is unchanged."""
+    need_gpu()
+    spec = t.ModelSpec(3, 64, 172, 512, False, 8)
+    N, K = 2, 2
+    fam = t.SynthFamily(spec, N, K)
+    yaml = t.MergeRecipe(num_ranks=N, base_checkpoint="S2", slices=[t.RecipeSlice("S1", [1])]).to_yaml()
+    bufs = [dev(fam.shard_bytes(k, 0)) for k in range(1, K + 1)]
+    fam.gen_shard(0, 1, K, [b.data_ptr() for b in bufs])
+    mp = t.MergePartition(fam, yaml, 0)
+    mp.bind([bufs[k - 1].data_ptr() + lo for k, c, lo, hi in mp.windows()])
+    out = dev(mp.bytes)
+    mp.run(out.data_ptr())
+    hsrc = [b.cpu().pin_memory() for b in bufs]
+    extra = [torch.randint(0, 256, (n,), dtype=torch.uint8).pin_memory() for n in (1, 4097, 300000, 0, 12345)]
+    dsts = [dev(max(1, x.numel())) for x in extra]
+    hdst = torch.empty(mp.bytes, dtype=torch.uint8).pin_memory()
+    h2d, _ = mp.run_host([hsrc[k - 1].data_ptr() + lo for k, c, lo, hi in mp.windows()], hdst.data_ptr(),
+                         chunk_bytes=1 << 13, async_=True,
+                         prefetch=[(x.data_ptr(), d.data_ptr(), x.numel()) for x, d in zip(extra, dsts)])
+    mp.wait()
+    assert bytes(hdst.numpy()) == host_bytes(out, mp.bytes)
+    assert h2d == mp.bytes + sum(x.numel() for x in extra)
+    for x, d in zip(extra, dsts):
+        assert torch.equal(d[:x.numel()].cpu(), x)
+
+
+def test_shard_sub_units_host_staged():
+    """cfg5-style units: a rank partition assembled as tensor-aligned sub-ranges whose source
+    windows are materialised one at a time (tg_family_gen_shard_range) == the whole partition."""
+    need_gpu()
+    spec = t.ModelSpec(4, 64, 172, 512, False, 21)
+    N, K = 2, 3
+    fam = t.SynthFamily(spec, N, K)
+    yaml = t.MergeRecipe(num_ranks=N, base_checkpoint="S3", slices=[t.RecipeSlice("S1", [0, 2]),
+                                                                    t.RecipeSlice("S2", [3])],
+                         aux={"norm": "S1"}).to_yaml()
+    r = 1
+    bufs = [dev(fam.shard_bytes(k, r)) for k in range(1, K + 1)]
+    fam.gen_shard(r, 1, K, [b.data_ptr() for b in bufs])
+    full = t.MergePartition(fam, yaml, r)
+    full.bind([bufs[k - 1].data_ptr() + lo for k, c, lo, hi in full.windows()])
+    out = dev(full.bytes)
+    full.run(out.data_ptr())
+    torch.cuda.synchronize()
+    expect = host_bytes(out, full.bytes)
+    for units in (2, 5):
+        got = b""
+        for u in range(units):
+            mp = t.MergePartition(fam, yaml, r, u, units)
+            hwin = []
+            for k, c, lo, hi in mp.windows():
+                d = dev(hi - lo)
+                fam.gen_shard_range(r, k, lo, hi, d.data_ptr())
+                torch.cuda.synchronize()
+                assert torch.equal(d, bufs[k - 1][lo:hi])
+                hwin.append(d.cpu().pin_memory())
+            hdst = torch.empty(max(1, mp.bytes), dtype=torch.uint8).pin_memory()
+            mp.run_host([h.data_ptr() for h in hwin], hdst.data_ptr(), chunk_bytes=1 << 12)
+            got += bytes(hdst.numpy()[:mp.bytes])
+        assert got == expect
+    with pytest.raises(t.TailorError):  # windows must be tensor-aligned
+        fam.gen_shard_range(r, 1, 4, 64, dev(64).data_ptr())
+
+
 @pytest.mark.parametrize("seed", range(4))
 def test_gather_variants_random_segments(seed):
     """Raw K2 (tg_gather): LSU and bulk paths vs a torch reference copy."""

@@ -152,6 +152,21 @@ def test_partition_plans_headers_and_coverage(spec, N):
             covered.append((lo, hi))
         assert covered[0][0] == 0 and covered[-1][1] == wsize
         assert all(a[1] == b[0] for a, b in zip(covered, covered[1:]))
+    # shard sub-units (host-staged cfg5 units): tile the rank payload at tensor boundaries,
+    # windows shrink to what the sub-range reads
+    full = t.MergePartition(fam, yaml, 0)
+    fl, fh, ftot = full.range()
+    assert (fl, fh) == (0, ftot)
+    for units in (2, 3, 7):
+        parts = [t.MergePartition(fam, yaml, 0, u, units) for u in range(units)]
+        rs = [p.range() for p in parts]
+        assert rs[0][0] == 0 and rs[-1][1] == ftot and all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+        assert sum(p.bytes for p in parts) == full.bytes
+        assert all(p.prefix() == full.prefix() for p in parts)
+        assert sum(p.num_segments for p in parts) >= full.num_segments
+        for p, (lo, hi, _) in zip(parts, rs):
+            for k, c, wlo, whi in p.windows():
+                assert c == 0 and whi - wlo <= hi - lo
 
 
 def test_plan_errors_match_reference_kinds():
