@@ -906,7 +906,7 @@ def trainer_arm(args, rank, world, local_rank):
     """SURVEY §8 f4 at scale: the device-resident trainer step (bit-exact AdamW on a
     Llama-3.1-8B-shaped ZeRO rank partition, one partition per GPU). Algorithmic bytes
     per element: grad pass 4 (w) + 4 (g out); update pass 12 + 4 (w,m,v + g in) read,
-    12 written = 36 B. Each step synchronizes once (the non-finite check precedes any
+    12 written = 36 B (both passes stream host-built TrainTile runs as float4). Each step synchronizes once (the non-finite check precedes any
     state change, as apply_step requires) and once more for the norm partials; timed by
     wall clock around synchronized steps, max over ranks."""
     import torch

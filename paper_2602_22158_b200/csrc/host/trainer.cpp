@@ -66,8 +66,8 @@ std::vector<ModuleId> modules_to_save(const StrategyConfig& cfg, const ModelSpec
 }
 
 struct DeviceTrainer::Rank {
-    DeviceBuffer part, groups, slices, grad, grad_part, delta_part;
-    std::uint32_t ngroups = 0;
+    DeviceBuffer part, groups, slices, tiles, grad, grad_part, delta_part;
+    std::uint32_t ngroups = 0, ntiles = 0;
     std::uint64_t total = 0;
     unsigned grid = 0;
     // in-situ scorer state
@@ -112,9 +112,10 @@ DeviceTrainer::DeviceTrainer(const ModelSpec& spec, int num_ranks, const AdamHyp
         rk->part.resize(std::max<std::uint64_t>(16, lay.payload_bytes));
         cuda_check(cudaMemsetAsync(rk->part.get(), 0, lay.payload_bytes, stream_), "memset");
         std::vector<dev::TrainGroup> tg;
+        std::vector<dev::TrainTile> tiles;
         std::vector<dev::SynthGroup> sg;
         std::vector<dev::SynthSlice> sl;
-        std::uint64_t begin = 0;
+        std::uint64_t begin = 0, vbegin = 0; // generator / gradient-scratch element spaces
         for (int g = 0; g < model_.table().group_count(); ++g) {
             const std::int64_t len = model_.table().groups[static_cast<std::size_t>(g)].element_count;
             const std::uint64_t chunk = static_cast<std::uint64_t>(geom.shard_length(len));
@@ -127,6 +128,30 @@ DeviceTrainer::DeviceTrainer(const ModelSpec& spec, int num_ranks, const AdamHyp
                                                                              static_cast<std::int64_t>(chunk)));
             tg.push_back({begin, chunk, static_cast<std::uint64_t>(r) * chunk, static_cast<std::uint64_t>(len), om, ov, ow, sb,
                           static_cast<std::uint32_t>(model_.slices(g).size()), static_cast<std::uint32_t>(g), 0});
+            // tiles: non-padding elements of this rank's chunk, split at tensor slices
+            // and at field-index multiples of kTrainTileElems (4-aligned runs)
+            const std::int64_t first = static_cast<std::int64_t>(r) * static_cast<std::int64_t>(chunk);
+            const std::int64_t valid_end = std::min<std::int64_t>(len, first + static_cast<std::int64_t>(chunk));
+            const bool fields16 = om % 16 == 0 && ov % 16 == 0 && ow % 16 == 0;
+            for (const auto& sc : model_.slices(g)) {
+                std::int64_t a = std::max<std::int64_t>(sc.group_offset, first);
+                const std::int64_t b = std::min<std::int64_t>(sc.group_offset + sc.decl.numel(), valid_end);
+                while (a < b) {
+                    const std::uint64_t i0 = static_cast<std::uint64_t>(a - first);
+                    const std::uint64_t next = (i0 / dev::kTrainTileElems + 1) * dev::kTrainTileElems;
+                    const std::uint64_t n = std::min<std::uint64_t>(next - i0, static_cast<std::uint64_t>(b - a));
+                    dev::TrainTile t{};
+                    t.v0 = vbegin + i0;
+                    t.i0 = i0;
+                    t.e0 = static_cast<std::uint64_t>(sc.model_offset + (a - sc.group_offset));
+                    t.count = static_cast<std::uint32_t>(n);
+                    t.group = static_cast<std::uint16_t>(tg.size() - 1);
+                    t.vec = fields16 && i0 % 4 == 0 && n % 4 == 0 ? 1 : 0;
+                    tiles.push_back(t);
+                    a += static_cast<std::int64_t>(n);
+                }
+            }
+            vbegin = (vbegin + chunk + 3) & ~3ull;
             dev::SynthGroup s{};
             s.begin = begin;
             s.chunk = chunk;
@@ -143,11 +168,14 @@ DeviceTrainer::DeviceTrainer(const ModelSpec& spec, int num_ranks, const AdamHyp
         }
         rk->ngroups = static_cast<std::uint32_t>(tg.size());
         rk->total = begin;
+        if (tg.size() > 0xFFFF) fail(ErrorKind::Geometry, "too many optimizer groups for the trainer tile table");
         rk->groups.upload(tg.data(), tg.size() * sizeof(dev::TrainGroup));
         rk->slices.upload(sl.data(), sl.size() * sizeof(dev::SynthSlice));
-        rk->grid = dev::adamw_grid(begin);
+        rk->ntiles = static_cast<std::uint32_t>(tiles.size());
+        rk->tiles.upload(tiles.data(), std::max<std::size_t>(1, tiles.size()) * sizeof(dev::TrainTile));
+        rk->grid = dev::train_grid(rk->ntiles);
         rk->grad_part.resize(rk->grid * sizeof(double));
-        rk->grad.resize(std::max<std::uint64_t>(16, begin * sizeof(float)));
+        rk->grad.resize(std::max<std::uint64_t>(16, vbegin * sizeof(float)));
         rk->delta_part.resize(rk->grid * sizeof(double));
         // W_0 = 0.02 * u(seed, 0, e) (init_state, R/src/gradients.cpp:51-66): the
         // generator with k1 = 0 writes exactly the initial masters.
@@ -178,8 +206,8 @@ std::pair<double, double> DeviceTrainer::step(std::int64_t s) {
     const dev::TrainParams p{dev::noise_prefix(model_.spec().seed, static_cast<std::uint64_t>(s)), 0.05f, 0.01f};
     cuda_check(cudaMemsetAsync(flag_.get(), 0, sizeof(unsigned int), stream_), "memset");
     for (auto& rk : ranks_)
-        cuda_check(dev::launch_grad_check(rk->groups.get<dev::TrainGroup>(), rk->ngroups, rk->slices.get<dev::SynthSlice>(),
-                                          rk->part.get(), rk->total, p, rk->grad.get<float>(), rk->grad_part.get<double>(),
+        cuda_check(dev::launch_grad_check(rk->tiles.get<dev::TrainTile>(), rk->ntiles, rk->groups.get<dev::TrainGroup>(),
+                                          rk->part.get(), p, rk->grad.get<float>(), rk->grad_part.get<double>(),
                                           flag_.get<unsigned int>(), stream_),
                    "grad check");
     unsigned int bad = 0;
@@ -204,8 +232,9 @@ std::pair<double, double> DeviceTrainer::step(std::int64_t s) {
     cuda_check(cudaMemcpyAsync(coef_.get(), coef.data(), coef.size() * sizeof(dev::AdamCoef), cudaMemcpyHostToDevice, stream_),
                "coef");
     for (auto& rk : ranks_)
-        cuda_check(dev::launch_adamw(rk->groups.get<dev::TrainGroup>(), rk->ngroups, coef_.get<dev::AdamCoef>(), rk->part.get(),
-                                     rk->grad.get<float>(), rk->total, rk->delta_part.get<double>(), stream_),
+        cuda_check(dev::launch_adamw(rk->tiles.get<dev::TrainTile>(), rk->ntiles, rk->groups.get<dev::TrainGroup>(),
+                                     coef_.get<dev::AdamCoef>(), rk->part.get(), rk->grad.get<float>(),
+                                     rk->delta_part.get<double>(), stream_),
                    "adamw");
     double g2 = 0.0, d2 = 0.0;
     std::vector<double> h;

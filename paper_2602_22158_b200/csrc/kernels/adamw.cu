@@ -32,39 +32,15 @@ __device__ __forceinline__ std::uint64_t mix64(std::uint64_t z) {
     return z;
 }
 
+// float(2 * ((h >> 11) * 2^-53) - 1) of the reference (R/src/gradients.cpp:17-23).
+// With x = h >> 11 (< 2^53), 2u - 1 = (x - 2^52) * 2^-52 exactly in double, so the
+// float result is the round-to-nearest float of the integer x - 2^52, scaled by 2^-52
+// (scaling by a power of two commutes with rounding here): one I2F instead of an
+// I2F.F64 + three FP64 ops + F2F, bit-identical.
 __device__ __forceinline__ float unit_noise_from(std::uint64_t prefix, std::uint64_t e) {
     const std::uint64_t h = mix64(prefix ^ (e * 0x8CB92BA72F3D8DD7ULL));
-    const double unit = __dmul_rn(__ull2double_rn(h >> 11), 0x1.0p-53);
-    return __double2float_rn(__dadd_rn(__dmul_rn(2.0, unit), -1.0));
-}
-
-__device__ __forceinline__ int find_group(const TrainGroup* __restrict__ g, std::uint32_t n, std::uint64_t v) {
-    int lo = 0, hi = static_cast<int>(n) - 1, ans = 0;
-    while (lo <= hi) {
-        const int mid = (lo + hi) >> 1;
-        if (g[mid].begin <= v) {
-            ans = mid;
-            lo = mid + 1;
-        } else {
-            hi = mid - 1;
-        }
-    }
-    return ans;
-}
-
-// Resolves virtual element v of a rank partition to (group, chunk index, global
-// element id); returns false for shard padding.
-__device__ __forceinline__ bool locate(const TrainGroup* __restrict__ groups, std::uint32_t ngroups,
-                                       const SynthSlice* __restrict__ slices, std::uint64_t v, const TrainGroup*& g,
-                                       std::uint64_t& i, std::uint64_t& e) {
-    g = &groups[find_group(groups, ngroups, v)];
-    i = v - g->begin;
-    const std::uint64_t go = g->group_first + i;
-    if (go >= g->true_len) return false;
-    std::uint32_t s = g->slice_begin;
-    while (s + 1 < g->slice_begin + g->slice_count && static_cast<std::int64_t>(go) >= slices[s + 1].group_offset) ++s;
-    e = static_cast<std::uint64_t>(slices[s].model_offset + (static_cast<std::int64_t>(go) - slices[s].group_offset));
-    return true;
+    const long long y = static_cast<long long>(h >> 11) - (1LL << 52);
+    return __fmul_rn(__ll2float_rn(y), 0x1.0p-52f);
 }
 
 __device__ __forceinline__ float grad_of(float w, const TrainParams& p, std::uint64_t e) {
@@ -83,58 +59,108 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     return s;
 }
 
-__global__ void __launch_bounds__(kThreads) grad_check_kernel(const TrainGroup* __restrict__ groups, std::uint32_t ngroups,
-                                                              const SynthSlice* __restrict__ slices,
-                                                              const std::uint8_t* __restrict__ part, std::uint64_t total,
-                                                              TrainParams p, float* __restrict__ grad,
-                                                              double* __restrict__ grad_partials,
+// Tiles (host-built, TrainTile) replace per-element group/slice searches: inside a
+// tile the field index, the gradient index and the noise counter are all affine
+// in j, so each thread streams float4 runs with no lookups.
+__global__ void __launch_bounds__(kThreads) grad_check_kernel(const TrainTile* __restrict__ tiles, std::uint32_t ntiles,
+                                                              const TrainGroup* __restrict__ groups,
+                                                              const std::uint8_t* __restrict__ part, TrainParams p,
+                                                              float* __restrict__ grad, double* __restrict__ grad_partials,
                                                               unsigned int* __restrict__ nonfinite) {
     __shared__ double red[kThreads / 32];
     double acc = 0.0;
     bool bad = false;
-    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
-    for (std::uint64_t v = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; v < total; v += stride) {
-        const TrainGroup* g;
-        std::uint64_t i, e;
-        if (!locate(groups, ngroups, slices, v, g, i, e)) continue;
-        const float w = reinterpret_cast<const float*>(part + g->off_w)[i];
-        const float gr = grad_of(w, p, e);
-        grad[v] = gr;
-        bad = bad || !isfinite(gr);
-        acc += static_cast<double>(gr) * static_cast<double>(gr);
+    for (std::uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const TrainTile tile = tiles[t];
+        const float* w = reinterpret_cast<const float*>(part + groups[tile.group].off_w) + tile.i0;
+        float* gout = grad + tile.v0;
+        if (tile.vec) {
+            const std::uint32_t n4 = tile.count >> 2;
+#pragma unroll 2
+            for (std::uint32_t q = threadIdx.x; q < n4; q += kThreads) {
+                const float4 x = __ldcs(reinterpret_cast<const float4*>(w) + q);
+                const std::uint64_t e = tile.e0 + 4ull * q;
+                float4 gr;
+                gr.x = grad_of(x.x, p, e);
+                gr.y = grad_of(x.y, p, e + 1);
+                gr.z = grad_of(x.z, p, e + 2);
+                gr.w = grad_of(x.w, p, e + 3);
+                reinterpret_cast<float4*>(gout)[q] = gr;
+                bad = bad || !isfinite(gr.x) || !isfinite(gr.y) || !isfinite(gr.z) || !isfinite(gr.w);
+                acc = fma(static_cast<double>(gr.x), static_cast<double>(gr.x), acc);
+                acc = fma(static_cast<double>(gr.y), static_cast<double>(gr.y), acc);
+                acc = fma(static_cast<double>(gr.z), static_cast<double>(gr.z), acc);
+                acc = fma(static_cast<double>(gr.w), static_cast<double>(gr.w), acc);
+            }
+        } else {
+            for (std::uint32_t j = threadIdx.x; j < tile.count; j += kThreads) {
+                const float gr = grad_of(w[j], p, tile.e0 + j);
+                gout[j] = gr;
+                bad = bad || !isfinite(gr);
+                acc = fma(static_cast<double>(gr), static_cast<double>(gr), acc);
+            }
+        }
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
     const double s = block_sum(acc, red);
     if (threadIdx.x == 0) grad_partials[blockIdx.x] = s;
 }
 
-__global__ void __launch_bounds__(kThreads) adamw_update_kernel(const TrainGroup* __restrict__ groups, std::uint32_t ngroups,
+__device__ __forceinline__ float adam_one(const AdamCoef& c, float& w, float& m, float& v, float gr) {
+    m = __fadd_rn(__fmul_rn(c.b1, m), __fmul_rn(c.one_minus_b1, gr));
+    v = __fadd_rn(__fmul_rn(c.b2, v), __fmul_rn(c.one_minus_b2, __fmul_rn(gr, gr)));
+    const float m_hat = __fdiv_rn(m, c.bias1);
+    const float v_hat = __fdiv_rn(v, c.bias2);
+    const float update = __fadd_rn(__fdiv_rn(m_hat, __fadd_rn(__fsqrt_rn(v_hat), c.eps)), __fmul_rn(c.wd, w));
+    const float step = __fmul_rn(c.lr, update);
+    w = __fsub_rn(w, step);
+    return step;
+}
+
+__global__ void __launch_bounds__(kThreads) adamw_update_kernel(const TrainTile* __restrict__ tiles, std::uint32_t ntiles,
+                                                                const TrainGroup* __restrict__ groups,
                                                                 const AdamCoef* __restrict__ coef, std::uint8_t* __restrict__ part,
-                                                                const float* __restrict__ grad, std::uint64_t total,
+                                                                const float* __restrict__ grad,
                                                                 double* __restrict__ delta_partials) {
     __shared__ double red[kThreads / 32];
     double acc = 0.0;
-    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
-    for (std::uint64_t v = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; v < total; v += stride) {
-        const TrainGroup* g = &groups[find_group(groups, ngroups, v)];
-        const std::uint64_t i = v - g->begin;
-        if (g->group_first + i >= g->true_len) continue; // shard padding stays zero
-        const AdamCoef c = coef[g->coef];
-        float* wp = reinterpret_cast<float*>(part + g->off_w) + i;
-        float* mp = reinterpret_cast<float*>(part + g->off_m) + i;
-        float* vp = reinterpret_cast<float*>(part + g->off_v) + i;
-        const float w = *wp;
-        const float gr = grad[v];
-        const float m = __fadd_rn(__fmul_rn(c.b1, *mp), __fmul_rn(c.one_minus_b1, gr));
-        const float vv = __fadd_rn(__fmul_rn(c.b2, *vp), __fmul_rn(c.one_minus_b2, __fmul_rn(gr, gr)));
-        const float m_hat = __fdiv_rn(m, c.bias1);
-        const float v_hat = __fdiv_rn(vv, c.bias2);
-        const float update = __fadd_rn(__fdiv_rn(m_hat, __fadd_rn(__fsqrt_rn(v_hat), c.eps)), __fmul_rn(c.wd, w));
-        const float step = __fmul_rn(c.lr, update);
-        *mp = m;
-        *vp = vv;
-        *wp = __fsub_rn(w, step);
-        acc += static_cast<double>(step) * static_cast<double>(step);
+    for (std::uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const TrainTile tile = tiles[t];
+        const TrainGroup& g = groups[tile.group];
+        const AdamCoef c = coef[g.coef];
+        float* wp = reinterpret_cast<float*>(part + g.off_w) + tile.i0;
+        float* mp = reinterpret_cast<float*>(part + g.off_m) + tile.i0;
+        float* vp = reinterpret_cast<float*>(part + g.off_v) + tile.i0;
+        const float* gp = grad + tile.v0;
+        if (tile.vec) {
+            const std::uint32_t n4 = tile.count >> 2;
+            for (std::uint32_t q = threadIdx.x; q < n4; q += kThreads) {
+                float4 w = __ldcs(reinterpret_cast<const float4*>(wp) + q);
+                float4 m = __ldcs(reinterpret_cast<const float4*>(mp) + q);
+                float4 v = __ldcs(reinterpret_cast<const float4*>(vp) + q);
+                const float4 gr = __ldcs(reinterpret_cast<const float4*>(gp) + q);
+                const float s0 = adam_one(c, w.x, m.x, v.x, gr.x);
+                const float s1 = adam_one(c, w.y, m.y, v.y, gr.y);
+                const float s2 = adam_one(c, w.z, m.z, v.z, gr.z);
+                const float s3 = adam_one(c, w.w, m.w, v.w, gr.w);
+                __stcs(reinterpret_cast<float4*>(mp) + q, m);
+                __stcs(reinterpret_cast<float4*>(vp) + q, v);
+                __stcs(reinterpret_cast<float4*>(wp) + q, w);
+                acc = fma(static_cast<double>(s0), static_cast<double>(s0), acc);
+                acc = fma(static_cast<double>(s1), static_cast<double>(s1), acc);
+                acc = fma(static_cast<double>(s2), static_cast<double>(s2), acc);
+                acc = fma(static_cast<double>(s3), static_cast<double>(s3), acc);
+            }
+        } else {
+            for (std::uint32_t j = threadIdx.x; j < tile.count; j += kThreads) {
+                float w = wp[j], m = mp[j], v = vp[j];
+                const float st = adam_one(c, w, m, v, gp[j]);
+                mp[j] = m;
+                vp[j] = v;
+                wp[j] = w;
+                acc = fma(static_cast<double>(st), static_cast<double>(st), acc);
+            }
+        }
     }
     const double s = block_sum(acc, red);
     if (threadIdx.x == 0) delta_partials[blockIdx.x] = s;
@@ -194,20 +220,22 @@ std::uint64_t noise_prefix(std::uint64_t seed, std::uint64_t step) {
     return mix(mix(seed + 0x9E3779B97F4A7C15ULL) ^ (step * 0xD1B54A32D192ED03ULL));
 }
 
-cudaError_t launch_grad_check(const TrainGroup* d_groups, std::uint32_t ngroups, const SynthSlice* d_slices,
-                              const std::uint8_t* d_part, std::uint64_t total, const TrainParams& p, float* d_grad,
-                              double* d_grad_partials, unsigned int* d_nonfinite, cudaStream_t s) {
-    if (total == 0) return cudaSuccess;
-    grad_check_kernel<<<adamw_grid(total), kThreads, 0, s>>>(d_groups, ngroups, d_slices, d_part, total, p, d_grad,
-                                                            d_grad_partials, d_nonfinite);
+unsigned train_grid(std::uint32_t ntiles) {
+    return std::max(1u, std::min(ntiles, static_cast<unsigned>(sm_count()) * 8u));
+}
+
+cudaError_t launch_grad_check(const TrainTile* d_tiles, std::uint32_t ntiles, const TrainGroup* d_groups,
+                              const std::uint8_t* d_part, const TrainParams& p, float* d_grad, double* d_grad_partials,
+                              unsigned int* d_nonfinite, cudaStream_t s) {
+    grad_check_kernel<<<train_grid(ntiles), kThreads, 0, s>>>(d_tiles, ntiles, d_groups, d_part, p, d_grad, d_grad_partials,
+                                                             d_nonfinite);
     return cudaGetLastError();
 }
 
-cudaError_t launch_adamw(const TrainGroup* d_groups, std::uint32_t ngroups, const AdamCoef* d_coef, std::uint8_t* d_part,
-                         const float* d_grad, std::uint64_t total, double* d_delta_partials, cudaStream_t s) {
-    if (total == 0) return cudaSuccess;
-    adamw_update_kernel<<<adamw_grid(total), kThreads, 0, s>>>(d_groups, ngroups, d_coef, d_part, d_grad, total,
-                                                              d_delta_partials);
+cudaError_t launch_adamw(const TrainTile* d_tiles, std::uint32_t ntiles, const TrainGroup* d_groups, const AdamCoef* d_coef,
+                         std::uint8_t* d_part, const float* d_grad, double* d_delta_partials, cudaStream_t s) {
+    adamw_update_kernel<<<train_grid(ntiles), kThreads, 0, s>>>(d_tiles, ntiles, d_groups, d_coef, d_part, d_grad,
+                                                               d_delta_partials);
     return cudaGetLastError();
 }
 

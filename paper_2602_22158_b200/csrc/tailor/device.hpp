@@ -152,13 +152,25 @@ struct TrainParams {
     float noise_coeff; // c2
 };
 std::uint64_t noise_prefix(std::uint64_t seed, std::uint64_t step);
+// A run of consecutive non-padding elements of one group inside one tensor slice
+// (host-built): element j of the tile is field element i0 + j, virtual element
+// v0 + j (gradient scratch index) and global element id e0 + j (noise counter).
+struct TrainTile {
+    std::uint64_t v0, i0, e0;
+    std::uint32_t count;
+    std::uint16_t group; // index into the rank's TrainGroup table
+    std::uint16_t vec;   // 1: i0 and count are multiples of 4 and the fields 16-B aligned
+};
+constexpr std::uint32_t kTrainTileElems = 16384;
 // Pass 1: gradients -> d_grad (one float per virtual element), FP64 sum g^2 per
 // block, non-finite flag. Pass 2 (only if no flag): AdamW from d_grad.
-cudaError_t launch_grad_check(const TrainGroup* d_groups, std::uint32_t ngroups, const SynthSlice* d_slices,
-                              const std::uint8_t* d_part, std::uint64_t total, const TrainParams& p, float* d_grad,
-                              double* d_grad_partials, unsigned int* d_nonfinite, cudaStream_t s);
-cudaError_t launch_adamw(const TrainGroup* d_groups, std::uint32_t ngroups, const AdamCoef* d_coef, std::uint8_t* d_part,
-                         const float* d_grad, std::uint64_t total, double* d_delta_partials, cudaStream_t s);
+cudaError_t launch_grad_check(const TrainTile* d_tiles, std::uint32_t ntiles, const TrainGroup* d_groups,
+                              const std::uint8_t* d_part, const TrainParams& p, float* d_grad, double* d_grad_partials,
+                              unsigned int* d_nonfinite, cudaStream_t s);
+cudaError_t launch_adamw(const TrainTile* d_tiles, std::uint32_t ntiles, const TrainGroup* d_groups, const AdamCoef* d_coef,
+                         std::uint8_t* d_part, const float* d_grad, double* d_delta_partials, cudaStream_t s);
+// blocks of the two passes (one FP64 partial each)
+unsigned train_grid(std::uint32_t ntiles);
 unsigned adamw_grid(std::uint64_t total);
 
 // ---- K8: bf16 weights derived from sharded masters ---------------------------------
