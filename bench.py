@@ -217,7 +217,8 @@ def ncu_traffic(kernel: str, workload: str):
             d = json.loads(p.read_text())
             if d.get("workload") != workload:
                 continue
-            k = d.get("kernels", {}).get(kernel)
+            ks = d.get("kernels", {})
+            k = ks.get(kernel) or next((v for n, v in ks.items() if n.startswith(kernel + "<")), None)
             if k and k.get("dram_bytes_per_launch"):
                 return float(k["dram_bytes_per_launch"]), p.name
         except Exception:
@@ -720,9 +721,9 @@ def scorer_arm(args, rank, world, local_rank):
     kms = statistics.mean(a.elapsed_time(b) for a, b in recs)
     hbm, peak_kind = peaks()
     achieved = scorer.bytes_read / (kms / 1e3) / 1e9
-    traffic, src = ncu_traffic("score_staged_kernel<16>" if args.score_variant == 2 else
-                               "score_partials_kernel<16,2>" if args.score_variant == 4 else "score_partials_kernel<16,4>",
-                               args.workload)
+    kname = ("score_staged_kernel<16>" if args.score_variant in (0, 2) else
+             "score_partials_kernel<16,2>" if args.score_variant == 4 else "score_partials_kernel<16,4>")
+    traffic, src = ncu_traffic(kname, args.workload)
     if rank != 0:
         return 0
     # Units: one rank partition of every module-pair score per GPU per step; all G
@@ -737,7 +738,7 @@ def scorer_arm(args, rank, world, local_rank):
                    "zero_ranks": N, "unit_of_work": "one ZeRO rank partition of 16 snapshots' masters per GPU",
                    "score_variant": SCORE_VARIANTS[args.score_variant],
                    "bytes_per_gpu_step": scorer.bytes_read, "min_boundary_gap": res[3]},
-        "roofline": {"bound": "hbm", "kernel": "K3 score_partials<16>", "achieved": round(achieved, 1), "peak": hbm,
+        "roofline": {"bound": "hbm", "kernel": "K3 " + kname, "achieved": round(achieved, 1), "peak": hbm,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": scorer.bytes_read, "traffic": traffic, "traffic_source": src},
         "gpu_launches": args.steps * 2, "clocks": clocks.summary()}))

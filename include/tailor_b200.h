@@ -197,7 +197,8 @@ int tg_family_select(tg_family* f, const double* rank_partials, int32_t nranks, 
 tg_scorer* tg_scorer_create(tg_family* f, int32_t rank, int32_t k0, int32_t k1, int32_t packed);
 void tg_scorer_destroy(tg_scorer* s);
 uint64_t tg_scorer_bytes(const tg_scorer* s);
-/* 0 auto, 1 register-staged 128-bit loads, 2 TMA-bulk shared-memory ring. */
+/* 0 auto (TMA-bulk ring when the bases are 16-B aligned, else register loads),
+ * 1 register-staged 128-bit loads, 2 TMA-bulk shared-memory ring. */
 int tg_scorer_set_variant(tg_scorer* s, int32_t variant);
 /* d_out: [K-1][M][2] FP64 partial sums for this rank. */
 int tg_scorer_run(tg_scorer* s, const uint8_t* const* bases, double* d_out, void* stream);

@@ -7,10 +7,11 @@
 // over every master element of m's groups; score = sqrt(s_delta)/sqrt(s_ref).
 // Shard padding is zero in every snapshot, so whole rank chunks can be summed.
 //
-// K3 reads each snapshot once (K snapshots -> K-1 pairs in one sweep) with
-// 128-bit non-allocating loads, accumulates FP64 per thread, reduces with warp
-// shuffles and a fixed warp order, and writes one partial per tile (no
-// atomics). K4 sums each module's tile partials in a fixed lane/tree order.
+// K3 reads each snapshot once (K snapshots -> K-1 pairs in one sweep) — by
+// default through a warp-specialised TMA bulk ring (score_staged_kernel), else
+// with 128-bit non-allocating register loads — accumulates FP64 per thread,
+// reduces with warp shuffles and a fixed warp order, and writes one partial per
+// tile (no atomics). K4 sums each module's tile partials in a fixed lane/tree order.
 // Results are bitwise reproducible for a given tile table, independent of the
 // grid size and of scheduling.
 #include <algorithm>
@@ -169,27 +170,30 @@ __global__ void score_combine_kernel(const double* __restrict__ partials, const 
 
 // ---- staged variant: TMA bulk copies into a shared-memory ring ------------------
 // For large K the register-staged kernel above needs K float4 per thread in
-// flight (172 registers at K=16 -> 12.5% occupancy, latency-bound). Here one
-// elected thread streams 1024-element chunks of all K snapshots into smem with
-// cp.async.bulk (completion by mbarrier transaction count), S stages deep, and
-// all threads reduce out of smem rolling over k (two float4 live). Loads in
-// flight are set by the ring depth, not by registers. Same tile -> partial
-// contract (one partial per tile, fixed order); summation order inside a tile
-// differs from the register kernel, so the two variants agree to ~1e-15, not
-// bitwise.
-constexpr int kChunkElems = 4 * kScoreThreads; // one float4 per thread per snapshot row
+// flight (222 registers at K=16 -> one 8-warp CTA per SM, latency-bound: issue
+// 21%, FP64 pipe 25%). Here loads are decoupled from registers: a producer warp
+// (one elected lane) streams 1024-element chunks of all K snapshots into an
+// S-stage shared-memory ring with cp.async.bulk (completion by mbarrier
+// transaction count), and 8 consumer warps reduce out of shared memory rolling
+// over k (two float4 live) and release each stage through an `empty` mbarrier
+// (one arrival per consumer warp) — no CTA-wide barrier in the stream. Same
+// tile -> partial contract (one partial per tile, fixed order); the summation
+// order inside a tile differs from the register kernel, so the two variants
+// agree to ~1e-15, not bitwise.
+constexpr int kChunkElems = 4 * kScoreThreads; // one float4 per consumer thread per snapshot row
 constexpr int kStagedSmem = 192 * 1024;
+constexpr int kStagedThreads = kScoreThreads + 32; // 8 consumer warps + 1 producer warp
 
 template <int K>
 __host__ __device__ constexpr int staged_stages() {
     constexpr int per = K * kChunkElems * 4;
     constexpr int s = kStagedSmem / per;
-    return s < 2 ? 2 : (s > 6 ? 6 : s);
+    return s < 2 ? 2 : (s > 8 ? 8 : s);
 }
 
 template <int K>
 __host__ __device__ constexpr std::size_t staged_smem_bytes() {
-    return static_cast<std::size_t>(staged_stages<K>()) * K * kChunkElems * 4 + 8 * staged_stages<K>();
+    return static_cast<std::size_t>(staged_stages<K>()) * K * kChunkElems * 4 + 16 * staged_stages<K>();
 }
 
 template <int K>
@@ -202,48 +206,52 @@ __device__ __forceinline__ void accumulate4(double (&acc)[2 * (K - 1)], int p, c
 }
 
 template <int K>
-__global__ void __launch_bounds__(kScoreThreads, 1) score_staged_kernel(const ScoreTile* __restrict__ tiles,
-                                                                         std::uint32_t ntiles,
-                                                                         const float* const* __restrict__ field_base,
-                                                                         std::uint32_t nfields, double* __restrict__ out) {
+__global__ void __launch_bounds__(kStagedThreads, 1) score_staged_kernel(const ScoreTile* __restrict__ tiles,
+                                                                          std::uint32_t ntiles,
+                                                                          const float* const* __restrict__ field_base,
+                                                                          std::uint32_t nfields, double* __restrict__ out) {
     using namespace tma;
     constexpr int S = staged_stages<K>();
     constexpr int V = 2 * (K - 1);
     extern __shared__ __align__(128) float ring[];
     std::uint64_t* full = reinterpret_cast<std::uint64_t*>(ring + S * K * kChunkElems);
+    std::uint64_t* empty = full + S;
     __shared__ double red[kWarps][V];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
-        for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
+        for (int st = 0; st < S; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], kWarps);
+        }
         fence_barrier_init();
     }
     __syncthreads();
-
     const std::uint32_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     const auto tile_at = [&](std::uint32_t i) { return blockIdx.x + i * gridDim.x; };
-    // producer cursor (thread 0 only)
-    std::uint32_t p_tile = 0, p_chunk = 0;
-    const auto issue = [&](int stage) {
-        while (p_tile < mine) {
-            const ScoreTile t = tiles[tile_at(p_tile)];
-            if (p_chunk * kChunkElems < t.count) {
-                const std::uint32_t start = p_chunk * kChunkElems;
-                const std::uint32_t n = min(static_cast<std::uint32_t>(kChunkElems), t.count - start);
-                const std::uint32_t nb = (n & ~3u) * 4u;
-                mbar_arrive_expect_tx(&full[stage], nb * K);
-                if (nb)
-                    for (int k = 0; k < K; ++k)
-                        bulk_load(ring + (stage * K + k) * kChunkElems, field_base[k * nfields + t.field] + t.elem_start + start,
-                                  nb, &full[stage]);
-                ++p_chunk;
-                return;
+
+    if (warp == kWarps) { // producer
+        if (lane == 0) {
+            std::uint32_t item = 0;
+            for (std::uint32_t i = 0; i < mine; ++i) {
+                const ScoreTile t = tiles[tile_at(i)];
+                const float* base[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) base[k] = field_base[k * nfields + t.field] + t.elem_start;
+                for (std::uint32_t start = 0; start < t.count; start += kChunkElems, ++item) {
+                    const int stage = static_cast<int>(item % S);
+                    if (item >= static_cast<std::uint32_t>(S)) mbar_wait_parity(&empty[stage], ((item / S) - 1) & 1u);
+                    const std::uint32_t n = min(static_cast<std::uint32_t>(kChunkElems), t.count - start);
+                    const std::uint32_t nb = (n & ~3u) * 4u;
+                    mbar_arrive_expect_tx(&full[stage], nb * K);
+                    if (nb)
+#pragma unroll
+                        for (int k = 0; k < K; ++k)
+                            bulk_load(ring + (stage * K + k) * kChunkElems, base[k] + start, nb, &full[stage]);
+                }
             }
-            ++p_tile;
-            p_chunk = 0;
         }
-    };
-    if (tid == 0)
-        for (int st = 0; st < S; ++st) issue(st);
+        return;
+    }
 
     std::uint32_t item = 0;
     for (std::uint32_t i = 0; i < mine; ++i) {
@@ -251,11 +259,9 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_staged_kernel(const Sc
         double acc[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) acc[v] = 0.0;
-        const std::uint32_t nchunks = (t.count + kChunkElems - 1) / kChunkElems;
-        for (std::uint32_t c = 0; c < nchunks; ++c, ++item) {
+        for (std::uint32_t start = 0; start < t.count; start += kChunkElems, ++item) {
             const int stage = static_cast<int>(item % S);
             mbar_wait_parity(&full[stage], (item / S) & 1u);
-            const std::uint32_t start = c * kChunkElems;
             const std::uint32_t n = min(static_cast<std::uint32_t>(kChunkElems), t.count - start);
             const std::uint32_t n4 = n & ~3u;
             const std::uint32_t e = static_cast<std::uint32_t>(tid) * 4u;
@@ -269,28 +275,28 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_staged_kernel(const Sc
                     prev = cur;
                 }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]); // this warp is done with the stage
             if (static_cast<std::uint32_t>(tid) < n - n4) { // ragged tail straight from global
                 float x[K];
 #pragma unroll
                 for (int k = 0; k < K; ++k) x[k] = __ldg(field_base[k * nfields + t.field] + t.elem_start + start + n4 + tid);
                 accumulate<K>(acc, x);
             }
-            __syncthreads(); // every thread is done with this stage
-            if (tid == 0) issue(stage);
         }
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const double sv = warp_sum(acc[v]);
             if (lane == 0) red[warp][v] = sv;
         }
-        __syncthreads();
+        named_bar_sync(1, kScoreThreads);
         if (tid < V) {
             double sv = 0.0;
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) sv += red[w][tid];
             out[static_cast<std::uint64_t>(tile_at(i)) * V + tid] = sv;
         }
-        __syncthreads();
+        named_bar_sync(1, kScoreThreads);
     }
 }
 
@@ -306,7 +312,7 @@ cudaError_t launch_staged(const ScoreTile* d_tiles, std::uint32_t ntiles, const 
         attr = true;
     }
     const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ntiles, static_cast<std::uint64_t>(sm_count())));
-    score_staged_kernel<K><<<grid, kScoreThreads, smem, stream>>>(d_tiles, ntiles, d_field_base, nfields, d_out);
+    score_staged_kernel<K><<<grid, kStagedThreads, smem, stream>>>(d_tiles, ntiles, d_field_base, nfields, d_out);
     return cudaGetLastError();
 }
 

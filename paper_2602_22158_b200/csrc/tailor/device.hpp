@@ -58,9 +58,12 @@ static_assert(sizeof(ScoreTile) == 24, "ScoreTile is part of the C ABI");
 // auto always uses 128-bit loads.
 enum ScoreVariant : int { kScoreAuto = 0, kScoreRegister = 1, kScoreStaged = 2, kScoreWide = 3, kScoreNarrow = 4 };
 constexpr int kNarrowMinK = 1 << 20;
-// Measured (profiles/r1_*): the staged ring is barrier-bound with one 8-warp CTA
-// per SM (K=16: 88% vs 90% register; K=4: 61% vs 106%), so auto never picks it.
-constexpr int kStagedMinK = 1 << 20;
+// Staged = warp-specialised TMA ring (producer warp + 8 consumer warps, full/empty
+// mbarriers). Measured on B200 (bench events, fraction of the 6543 GB/s copy peak):
+// K=16 1.093 vs register 0.951; K=4 1.075 vs 1.064 -> auto picks it whenever the
+// bases are 16-B aligned. (Its first version, one CTA-wide barrier per chunk, was
+// barrier-bound: 0.88 / 0.61.)
+constexpr int kStagedMinK = 2;
 cudaError_t launch_score_partials(const ScoreTile* d_tiles, std::uint32_t ntiles, const float* const* d_field_base,
                                   std::uint32_t nfields, int K, bool vec_ok, double* d_tile_partials, cudaStream_t stream,
                                   int variant = kScoreAuto);
