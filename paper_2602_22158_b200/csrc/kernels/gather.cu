@@ -178,33 +178,38 @@ __global__ void __launch_bounds__(32) gather_bulk_kernel(const GatherSeg* __rest
 template <int STAGES, std::uint32_t STAGE>
 cudaError_t launch_bulk(const GatherSeg* d_segs, std::uint32_t nseg, std::uint8_t* d_dst, std::uint64_t dst_bytes,
                         int ctas_per_sm, cudaStream_t stream) {
-    static bool attr = false;
+    static std::atomic<std::uint64_t> attr{0};
     const std::size_t smem = STAGES * STAGE + STAGES * sizeof(std::uint64_t);
-    if (!attr) {
-        const cudaError_t e = cudaFuncSetAttribute(gather_bulk_kernel<STAGES, STAGE>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gather_bulk_kernel<STAGES, STAGE>), smem, attr);
+        e != cudaSuccess)
+        return e;
     const std::uint64_t tiles = (dst_bytes + STAGE - 1) / STAGE;
     const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(tiles, static_cast<std::uint64_t>(sm_count()) * ctas_per_sm));
     gather_bulk_kernel<STAGES, STAGE><<<grid, 32, smem, stream>>>(d_segs, nseg, d_dst, dst_bytes);
     return cudaGetLastError();
 }
 
-int g_sms = 0;
-int g_lsu_blocks_per_sm = 0;
 
 } // namespace
 
 int sm_count() {
-    if (g_sms == 0) {
-        int dev = 0;
+    static const int n = [] {
+        int dev = 0, sms = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_sms <= 0) g_sms = 148;
-    }
-    return g_sms;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return sms > 0 ? sms : 148;
+    }();
+    return n;
+}
+
+cudaError_t ensure_smem_attr(const void* fn, std::size_t smem, std::atomic<std::uint64_t>& done) {
+    int dev = 0;
+    if (const cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+    const std::uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
 }
 
 cudaError_t launch_gather(const GatherSeg* d_segs, std::uint32_t nseg, std::uint8_t* d_dst, std::uint64_t dst_bytes,
@@ -221,13 +226,14 @@ cudaError_t launch_gather(const GatherSeg* d_segs, std::uint32_t nseg, std::uint
             default: return launch_bulk<kBulkStages, kBulkStage>(d_segs, nseg, d_dst, dst_bytes, 1, stream);
         }
     }
-    if (g_lsu_blocks_per_sm == 0) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_lsu_blocks_per_sm, gather_lsu_kernel, kLsuThreads, 0);
-        g_lsu_blocks_per_sm = std::max(1, std::min(g_lsu_blocks_per_sm, 4));
-    }
+    static const int lsu_blocks_per_sm = [] {
+        int n = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gather_lsu_kernel, kLsuThreads, 0);
+        return std::max(1, std::min(n, 4));
+    }();
     const std::uint64_t tiles = (dst_bytes + kLsuTile - 1) / kLsuTile;
     const unsigned grid =
-        static_cast<unsigned>(std::min<std::uint64_t>(tiles, static_cast<std::uint64_t>(sms) * g_lsu_blocks_per_sm));
+        static_cast<unsigned>(std::min<std::uint64_t>(tiles, static_cast<std::uint64_t>(sms) * lsu_blocks_per_sm));
     gather_lsu_kernel<<<grid, kLsuThreads, 0, stream>>>(d_segs, nseg, d_dst, dst_bytes);
     return cudaGetLastError();
 }

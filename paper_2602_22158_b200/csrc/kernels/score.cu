@@ -276,7 +276,10 @@ __global__ void __launch_bounds__(kStagedThreads, 1) score_staged_kernel(const S
                 }
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]); // this warp is done with the stage
+            if (lane == 0) { // this warp is done with the stage: order its generic-proxy reads
+                fence_proxy_async_smem(); // before the producer's next async-proxy (TMA) writes
+                mbar_arrive(&empty[stage]);
+            }
             if (static_cast<std::uint32_t>(tid) < n - n4) { // ragged tail straight from global
                 float x[K];
 #pragma unroll
@@ -303,14 +306,11 @@ __global__ void __launch_bounds__(kStagedThreads, 1) score_staged_kernel(const S
 template <int K>
 cudaError_t launch_staged(const ScoreTile* d_tiles, std::uint32_t ntiles, const float* const* d_field_base,
                           std::uint32_t nfields, double* d_out, cudaStream_t stream) {
-    static bool attr = false;
+    static std::atomic<std::uint64_t> attr{0};
     constexpr std::size_t smem = staged_smem_bytes<K>();
-    if (!attr) {
-        const cudaError_t e = cudaFuncSetAttribute(score_staged_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(score_staged_kernel<K>), smem, attr);
+        e != cudaSuccess)
+        return e;
     const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ntiles, static_cast<std::uint64_t>(sm_count())));
     score_staged_kernel<K><<<grid, kStagedThreads, smem, stream>>>(d_tiles, ntiles, d_field_base, nfields, d_out);
     return cudaGetLastError();
@@ -319,11 +319,11 @@ cudaError_t launch_staged(const ScoreTile* d_tiles, std::uint32_t ntiles, const 
 template <int K, int VW>
 cudaError_t launch_kv(const ScoreTile* d_tiles, std::uint32_t ntiles, const float* const* d_field_base,
                       std::uint32_t nfields, bool vec_ok, double* d_out, cudaStream_t stream) {
-    static int per_sm = 0;
-    if (per_sm == 0) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_partials_kernel<K, VW>, kScoreThreads, 0);
-        per_sm = std::max(1, per_sm);
-    }
+    static const int per_sm = [] {
+        int n = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, score_partials_kernel<K, VW>, kScoreThreads, 0);
+        return std::max(1, n);
+    }();
     const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ntiles, static_cast<std::uint64_t>(sm_count()) * per_sm));
     score_partials_kernel<K, VW><<<grid, kScoreThreads, 0, stream>>>(d_tiles, ntiles, d_field_base, nfields, vec_ok ? 1 : 0,
                                                                      d_out);

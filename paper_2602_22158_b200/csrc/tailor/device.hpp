@@ -4,6 +4,7 @@
 // asynchronous on the caller's stream.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 
 #include <cuda_runtime.h>
@@ -206,5 +207,8 @@ cudaError_t launch_select_plan(const double* d_parts, int nranks, int K, int M, 
                                double* d_scores, cudaStream_t s);
 
 int sm_count();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device);
+// `done` is the kernel's per-device bitmask. Thread-safe.
+cudaError_t ensure_smem_attr(const void* fn, std::size_t smem, std::atomic<std::uint64_t>& done);
 
 } // namespace tailor::dev
