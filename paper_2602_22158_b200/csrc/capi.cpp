@@ -140,7 +140,7 @@ void load_packed_masters(const std::vector<std::string>& dirs, int rank, const M
     offs.assign(dirs.size(), {});
     PinnedBuffer stage;
     for (std::size_t k = 0; k < dirs.size(); ++k) {
-        const fs::path p = shard_path(dirs[k], rank);
+        const fs::path p = ckpt_file(CkptFile::Shard, dirs[k], rank);
         const ContainerLayout lay = read_layout(p);
         std::uint64_t total = 0;
         std::vector<std::pair<const Entry*, std::uint64_t>> where;
@@ -376,7 +376,7 @@ int tg_select_recipe(const char* const* dirs, int32_t n, double rho, int32_t dev
 
 int tg_parse_config(const char* text, tg_model_spec* out) {
     return guard([&] {
-        const ModelSpec s = parse_config_json(text ? text : "", "config");
+        const ModelSpec s = sidecar_value<ModelSpec>(text ? text : "", "config");
         if (out) *out = tg_model_spec{s.num_layers, s.hidden_dim, s.ffn_dim, s.vocab_size, s.weight_tied ? 1 : 0, 0, s.seed};
     });
 }

@@ -41,9 +41,9 @@ const OptimGroupMeta* OptimMeta::find(int index) const {
     return nullptr;
 }
 
-std::string checkpoint_dir_name(std::int64_t step) { return "checkpoint-" + std::to_string(step); }
+std::string dir_of_step(std::int64_t step) { return "checkpoint-" + std::to_string(step); }
 
-std::optional<std::int64_t> parse_checkpoint_dir_name(const std::string& name) {
+std::optional<std::int64_t> step_of_dir(const std::string& name) {
     static const std::string kPrefix = "checkpoint-";
     if (name.compare(0, kPrefix.size(), kPrefix) != 0) return std::nullopt;
     std::int64_t step = -1;
@@ -54,12 +54,17 @@ std::optional<std::int64_t> parse_checkpoint_dir_name(const std::string& name) {
     return step;
 }
 
-fs::path weights_path(const fs::path& dir) { return dir / "model.weights"; }
-fs::path shard_path(const fs::path& dir, int rank) { return dir / "optim" / ("rank_" + std::to_string(rank) + ".shard"); }
-fs::path optim_meta_path(const fs::path& dir) { return dir / "optim_meta.json"; }
-fs::path config_path(const fs::path& dir) { return dir / "config.json"; }
-fs::path trainer_state_path(const fs::path& dir) { return dir / "trainer_state.json"; }
-fs::path manifest_path(const fs::path& dir) { return dir / "manifest.json"; }
+fs::path ckpt_file(CkptFile kind, const fs::path& dir, int rank) {
+    switch (kind) {
+    case CkptFile::Weights: return dir / "model.weights";
+    case CkptFile::Shard: return dir / "optim" / ("rank_" + std::to_string(rank) + ".shard");
+    case CkptFile::OptimMeta: return dir / "optim_meta.json";
+    case CkptFile::Config: return dir / "config.json";
+    case CkptFile::TrainerState: return dir / "trainer_state.json";
+    case CkptFile::Manifest: return dir / "manifest.json";
+    }
+    fail(ErrorKind::Consistency, "unknown checkpoint file kind");
+}
 
 std::string read_text_file(const fs::path& path) {
     std::ifstream in(path, std::ios::binary);
@@ -109,7 +114,7 @@ DecayClass decay_from(const std::string& s, const std::string& origin) {
 
 } // namespace
 
-std::string render_config_json(const ModelSpec& s) {
+std::string sidecar_text(const ModelSpec& s) {
     json j = json::object();
     j["num_layers"] = s.num_layers;
     j["hidden_dim"] = s.hidden_dim;
@@ -120,7 +125,8 @@ std::string render_config_json(const ModelSpec& s) {
     return pretty(j);
 }
 
-ModelSpec parse_config_json(const std::string& text, const std::string& origin) {
+template <>
+ModelSpec sidecar_value<ModelSpec>(const std::string& text, const std::string& origin) {
     const json j = parse_json(text, origin);
     exact_keys(j, {"num_layers", "hidden_dim", "ffn_dim", "vocab_size", "weight_tied", "seed"}, {}, origin);
     ModelSpec s;
@@ -134,7 +140,7 @@ ModelSpec parse_config_json(const std::string& text, const std::string& origin) 
     return s;
 }
 
-std::string render_trainer_state_json(const TrainerMeta& m) {
+std::string sidecar_text(const TrainerMeta& m) {
     json strat = json::object();
     strat["kind"] = strategy_kind_name(m.strategy.kind);
     strat["interval"] = m.strategy.interval;
@@ -153,7 +159,8 @@ std::string render_trainer_state_json(const TrainerMeta& m) {
     return pretty(j);
 }
 
-TrainerMeta parse_trainer_state_json(const std::string& text, const std::string& origin) {
+template <>
+TrainerMeta sidecar_value<TrainerMeta>(const std::string& text, const std::string& origin) {
     const json j = parse_json(text, origin);
     exact_keys(j, {"step", "lr", "optimizer_t", "strategy", "checkpoint_counter", "rng_seed"}, {}, origin);
     TrainerMeta m;
@@ -172,7 +179,7 @@ TrainerMeta parse_trainer_state_json(const std::string& text, const std::string&
     return m;
 }
 
-std::string render_manifest_json(const SaveManifest& man) {
+std::string sidecar_text(const SaveManifest& man) {
     json mods = json::array();
     for (const auto& m : man.modules) mods.push_back(module_name(m));
     json j = json::object();
@@ -192,7 +199,8 @@ std::string render_manifest_json(const SaveManifest& man) {
     return pretty(j);
 }
 
-SaveManifest parse_manifest_json(const std::string& text, const std::string& origin) {
+template <>
+SaveManifest sidecar_value<SaveManifest>(const std::string& text, const std::string& origin) {
     const json j = parse_json(text, origin);
     exact_keys(j, {"step", "strategy", "modules"}, {"provenance"}, origin);
     SaveManifest man;
@@ -208,7 +216,7 @@ SaveManifest parse_manifest_json(const std::string& text, const std::string& ori
     return man;
 }
 
-std::string render_optim_meta_json(const OptimMeta& meta) {
+std::string sidecar_text(const OptimMeta& meta) {
     json groups = json::array();
     for (const auto& g : meta.groups) {
         json e = json::object();
@@ -233,7 +241,8 @@ std::string render_optim_meta_json(const OptimMeta& meta) {
     return pretty(j);
 }
 
-OptimMeta parse_optim_meta_json(const std::string& text, const std::string& origin) {
+template <>
+OptimMeta sidecar_value<OptimMeta>(const std::string& text, const std::string& origin) {
     const json j = parse_json(text, origin);
     exact_keys(j, {"grouping", "num_ranks", "step", "groups"}, {}, origin);
     OptimMeta meta;
@@ -291,10 +300,14 @@ CheckpointSummary read_checkpoint_summary(const fs::path& dir) {
     if (!fs::exists(dir)) fail(ErrorKind::MissingArtifact, "checkpoint directory '" + dir.string() + "' does not exist");
     CheckpointSummary s;
     s.dir = dir;
-    s.spec = parse_config_json(read_text_file(config_path(dir)), config_path(dir).string());
-    s.trainer = parse_trainer_state_json(read_text_file(trainer_state_path(dir)), trainer_state_path(dir).string());
-    s.manifest = parse_manifest_json(read_text_file(manifest_path(dir)), manifest_path(dir).string());
-    s.optim = parse_optim_meta_json(read_text_file(optim_meta_path(dir)), optim_meta_path(dir).string());
+    auto load = [&dir]<class T>(CkptFile kind, T& out) {
+        const fs::path f = ckpt_file(kind, dir);
+        out = sidecar_value<T>(read_text_file(f), f.string());
+    };
+    load(CkptFile::Config, s.spec);
+    load(CkptFile::TrainerState, s.trainer);
+    load(CkptFile::Manifest, s.manifest);
+    load(CkptFile::OptimMeta, s.optim);
     const std::string d = dir.string();
     if (s.manifest.step != s.trainer.step) fail(ErrorKind::Consistency, d + ": manifest step disagrees with trainer state");
     if (s.optim.step != s.trainer.optimizer_t) fail(ErrorKind::Consistency, d + ": optim_meta step disagrees with trainer state");

@@ -197,9 +197,9 @@ CheckpointSummary SynthFamily::summary(int k, const std::string& dir) const {
     return s;
 }
 
-std::string SynthFamily::trainer_state_json(int k) const { return render_trainer_state_json(summary(k, "").trainer); }
-std::string SynthFamily::manifest_json(int k) const { return render_manifest_json(summary(k, "").manifest); }
-std::string SynthFamily::optim_meta_json(int k) const { return render_optim_meta_json(summary(k, "").optim); }
+std::string SynthFamily::trainer_state_json(int k) const { return sidecar_text(summary(k, "").trainer); }
+std::string SynthFamily::manifest_json(int k) const { return sidecar_text(summary(k, "").manifest); }
+std::string SynthFamily::optim_meta_json(int k) const { return sidecar_text(summary(k, "").optim); }
 
 void SynthFamily::ensure_sigma(int kmax) {
     if (kmax <= sigma_rows_) return;
@@ -416,18 +416,18 @@ void SynthFamily::write_dir(int k, const std::string& dir) {
     std::uint8_t* outs[1] = {d.get()};
     gen_weights(k, k, 0, lay.weights.payload_bytes, outs, nullptr);
     cuda_check(cudaMemcpy(h.data(), d.get(), lay.weights.payload_bytes, cudaMemcpyDeviceToHost), "D2H");
-    write_bytes_file(weights_path(dir), lay.weights.prefix(), h.data(), lay.weights.payload_bytes);
+    write_bytes_file(ckpt_file(CkptFile::Weights, dir), lay.weights.prefix(), h.data(), lay.weights.payload_bytes);
     for (int r = 0; r < num_ranks_; ++r) {
         gen_shard(r, k, k, outs, nullptr);
         const auto& c = lay.shards[static_cast<std::size_t>(r)];
         cuda_check(cudaMemcpy(h.data(), d.get(), c.payload_bytes, cudaMemcpyDeviceToHost), "D2H");
-        write_bytes_file(shard_path(dir, r), c.prefix(), h.data(), c.payload_bytes);
+        write_bytes_file(ckpt_file(CkptFile::Shard, dir, r), c.prefix(), h.data(), c.payload_bytes);
     }
     const CheckpointSummary s = summary(k, dir);
-    write_text_file(optim_meta_path(dir), render_optim_meta_json(s.optim));
-    write_text_file(config_path(dir), render_config_json(s.spec));
-    write_text_file(trainer_state_path(dir), render_trainer_state_json(s.trainer));
-    write_text_file(manifest_path(dir), render_manifest_json(s.manifest));
+    write_text_file(ckpt_file(CkptFile::OptimMeta, dir), sidecar_text(s.optim));
+    write_text_file(ckpt_file(CkptFile::Config, dir), sidecar_text(s.spec));
+    write_text_file(ckpt_file(CkptFile::TrainerState, dir), sidecar_text(s.trainer));
+    write_text_file(ckpt_file(CkptFile::Manifest, dir), sidecar_text(s.manifest));
     set_id(k, dir);
 }
 
@@ -837,33 +837,33 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
     if (files != static_cast<std::size_t>(s.optim.num_ranks))
         fail(ErrorKind::Geometry, dir.string() + ": found " + std::to_string(files) + " shard files for " +
                                       std::to_string(s.optim.num_ranks) + " ranks");
-    const ContainerLayout wl = read_layout(weights_path(dir));
+    const ContainerLayout wl = read_layout(ckpt_file(CkptFile::Weights, dir));
     std::size_t expect_tensors = 0;
     for (const auto& m : s.manifest.modules)
         for (const auto& t : tensors_of(s.spec, m)) {
             ++expect_tensors;
             const Entry* e = wl.find(t.name);
-            if (!e) fail(ErrorKind::CorruptContainer, weights_path(dir).string() + ": missing tensor '" + t.name + "'");
+            if (!e) fail(ErrorKind::CorruptContainer, ckpt_file(CkptFile::Weights, dir).string() + ": missing tensor '" + t.name + "'");
             if (e->dtype != Dtype::BF16 || e->shape != t.shape)
-                fail(ErrorKind::Geometry, weights_path(dir).string() + ": tensor '" + t.name + "' has unexpected dtype/shape");
+                fail(ErrorKind::Geometry, ckpt_file(CkptFile::Weights, dir).string() + ": tensor '" + t.name + "' has unexpected dtype/shape");
         }
     if (wl.entries.size() != expect_tensors)
-        fail(ErrorKind::CorruptContainer, weights_path(dir).string() + ": contains tensors not in the manifest");
+        fail(ErrorKind::CorruptContainer, ckpt_file(CkptFile::Weights, dir).string() + ": contains tensors not in the manifest");
 
     DeviceBuffer dw, ds, dpairs, dranges, derr(3 * sizeof(unsigned long long));
     PinnedBuffer stage;
     {
         PhaseTimer pt("verify.load_weights");
-        load_payload(weights_path(dir), wl, dw, stage);
+        load_payload(ckpt_file(CkptFile::Weights, dir), wl, dw, stage);
     }
     unsigned long long err[3] = {0, 0, 0};
     cuda_check(cudaMemset(derr.get(), 0, sizeof(err)), "memset");
     for (int r = 0; r < s.optim.num_ranks; ++r) {
-        const ContainerLayout sl = read_layout(shard_path(dir, r));
+        const ContainerLayout sl = read_layout(ckpt_file(CkptFile::Shard, dir, r));
         auto mr = sl.metadata.find("rank");
         if (mr != sl.metadata.end() && mr->second != std::to_string(r))
-            fail(ErrorKind::CorruptContainer, shard_path(dir, r).string() + ": rank metadata mismatch");
-        load_payload(shard_path(dir, r), sl, ds, stage);
+            fail(ErrorKind::CorruptContainer, ckpt_file(CkptFile::Shard, dir, r).string() + ": rank metadata mismatch");
+        load_payload(ckpt_file(CkptFile::Shard, dir, r), sl, ds, stage);
         std::vector<dev::VerifyPair> pairs;
         std::vector<dev::VerifyRange> ranges;
         for (const auto& g : s.optim.groups) {
@@ -873,9 +873,9 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
                 f[i] = sl.find(shard_key(g.index, names[i]));
                 if (!f[i])
                     fail(ErrorKind::CorruptContainer,
-                         shard_path(dir, r).string() + ": missing tensor '" + shard_key(g.index, names[i]) + "'");
+                         ckpt_file(CkptFile::Shard, dir, r).string() + ": missing tensor '" + shard_key(g.index, names[i]) + "'");
                 if (f[i]->dtype != Dtype::F32 || f[i]->shape != std::vector<std::int64_t>{g.shard_length})
-                    fail(ErrorKind::Geometry, shard_path(dir, r).string() + ": tensor '" + shard_key(g.index, names[i]) +
+                    fail(ErrorKind::Geometry, ckpt_file(CkptFile::Shard, dir, r).string() + ": tensor '" + shard_key(g.index, names[i]) +
                                                   "' has unexpected dtype/shape");
             }
             const std::int64_t c = g.shard_length, first = static_cast<std::int64_t>(r) * c;

@@ -269,13 +269,13 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
     for (const auto& [tgt, a] : plan.assignment) {
         if (layouts.count(a.source)) continue;
         SourceLayout sl;
-        sl.weights = read_layout(weights_path(a.source));
+        sl.weights = read_layout(ckpt_file(CkptFile::Weights, a.source));
         stats.weight_files_read += 1;
         layouts.emplace(a.source, std::move(sl));
     }
     for (const auto& src : plan.sources) {
         auto& sl = layouts[src];
-        for (int r = 0; r < plan.num_ranks; ++r) sl.shards.push_back(read_layout(shard_path(src, r)));
+        for (int r = 0; r < plan.num_ranks; ++r) sl.shards.push_back(read_layout(ckpt_file(CkptFile::Shard, src, r)));
     }
     stats.shard_files_read = options.uncached
                                  ? static_cast<std::int64_t>(plan.num_ranks) * static_cast<std::int64_t>(plan.group_copies.size())
@@ -296,18 +296,18 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
     FileAssembler fa(workers, options.uncached);
     {
         std::vector<fs::path> files;
-        for (const auto& w : wplan.windows) files.push_back(weights_path(w.source));
-        fa.assemble(wplan, files, weights_path(out_dir));
+        for (const auto& w : wplan.windows) files.push_back(ckpt_file(CkptFile::Weights, w.source));
+        fa.assemble(wplan, files, ckpt_file(CkptFile::Weights, out_dir));
     }
     for (int r = 0; r < plan.num_ranks; ++r) {
         std::vector<fs::path> files;
-        for (const auto& w : splans[static_cast<std::size_t>(r)].windows) files.push_back(shard_path(w.source, w.container));
-        fa.assemble(splans[static_cast<std::size_t>(r)], files, shard_path(out_dir, r));
+        for (const auto& w : splans[static_cast<std::size_t>(r)].windows) files.push_back(ckpt_file(CkptFile::Shard, w.source, w.container));
+        fa.assemble(splans[static_cast<std::size_t>(r)], files, ckpt_file(CkptFile::Shard, out_dir, r));
     }
-    write_text_file(optim_meta_path(out_dir), render_optim_meta_json(optim));
-    write_text_file(config_path(out_dir), read_text_file(config_path(plan.config_source)));
-    write_text_file(trainer_state_path(out_dir), read_text_file(trainer_state_path(plan.config_source)));
-    write_text_file(manifest_path(out_dir), render_manifest_json(manifest));
+    write_text_file(ckpt_file(CkptFile::OptimMeta, out_dir), sidecar_text(optim));
+    write_text_file(ckpt_file(CkptFile::Config, out_dir), read_text_file(ckpt_file(CkptFile::Config, plan.config_source)));
+    write_text_file(ckpt_file(CkptFile::TrainerState, out_dir), read_text_file(ckpt_file(CkptFile::TrainerState, plan.config_source)));
+    write_text_file(ckpt_file(CkptFile::Manifest, out_dir), sidecar_text(manifest));
 
     phase = std::make_unique<PhaseTimer>("merge.verify");
     if (options.verify) verify_checkpoint_dir(out_dir.string(), options.device);
@@ -350,13 +350,13 @@ MergeStats execute_regroup(const fs::path& src, const fs::path& out_dir, Groupin
         for (const auto& sl : group_tensor_slices(spec, src_table, g)) where[sl.decl.name] = {g, sl.group_offset};
     std::vector<ContainerLayout> shards;
     for (int r = 0; r < N; ++r) {
-        shards.push_back(read_layout(shard_path(src, r)));
+        shards.push_back(read_layout(ckpt_file(CkptFile::Shard, src, r)));
         for (const auto& gm : s.optim.groups)
             for (const char* f : {".master", ".exp_avg", ".exp_avg_sq"}) {
                 const Entry* e = shards.back().find(shard_key(gm.index, f));
-                if (!e) fail(ErrorKind::CorruptContainer, shard_path(src, r).string() + ": missing tensor '" + shard_key(gm.index, f) + "'");
+                if (!e) fail(ErrorKind::CorruptContainer, ckpt_file(CkptFile::Shard, src, r).string() + ": missing tensor '" + shard_key(gm.index, f) + "'");
                 if (e->dtype != Dtype::F32 || e->shape != std::vector<std::int64_t>{gm.shard_length})
-                    fail(ErrorKind::Geometry, shard_path(src, r).string() + ": tensor '" + e->name + "' has unexpected dtype/shape");
+                    fail(ErrorKind::Geometry, ckpt_file(CkptFile::Shard, src, r).string() + ": tensor '" + e->name + "' has unexpected dtype/shape");
             }
     }
     stats.shard_files_read = N;
@@ -423,7 +423,7 @@ MergeStats execute_regroup(const fs::path& src, const fs::path& out_dir, Groupin
     }
     // weights: the tensor set and order do not depend on the grouping
     PartitionPlan wp;
-    wp.out = read_layout(weights_path(src));
+    wp.out = read_layout(ckpt_file(CkptFile::Weights, src));
     stats.weight_files_read = 1;
     wp.dst_lo = 0;
     wp.dst_hi = wp.out.payload_bytes;
@@ -436,15 +436,15 @@ MergeStats execute_regroup(const fs::path& src, const fs::path& out_dir, Groupin
     const auto files_of = [&](const PartitionPlan& pp) {
         std::vector<fs::path> files;
         for (const auto& w : pp.windows)
-            files.push_back(w.container == kZeroContainer ? fs::path() : w.container < 0 ? weights_path(src) : shard_path(src, w.container));
+            files.push_back(w.container == kZeroContainer ? fs::path() : w.container < 0 ? ckpt_file(CkptFile::Weights, src) : ckpt_file(CkptFile::Shard, src, w.container));
         return files;
     };
-    fa.assemble(wp, files_of(wp), weights_path(out_dir));
-    for (int r = 0; r < N; ++r) fa.assemble(plans[static_cast<std::size_t>(r)], files_of(plans[static_cast<std::size_t>(r)]), shard_path(out_dir, r));
-    write_text_file(optim_meta_path(out_dir), render_optim_meta_json(optim));
-    write_text_file(config_path(out_dir), render_config_json(spec));
-    write_text_file(trainer_state_path(out_dir), render_trainer_state_json(s.trainer));
-    write_text_file(manifest_path(out_dir), render_manifest_json(s.manifest));
+    fa.assemble(wp, files_of(wp), ckpt_file(CkptFile::Weights, out_dir));
+    for (int r = 0; r < N; ++r) fa.assemble(plans[static_cast<std::size_t>(r)], files_of(plans[static_cast<std::size_t>(r)]), ckpt_file(CkptFile::Shard, out_dir, r));
+    write_text_file(ckpt_file(CkptFile::OptimMeta, out_dir), sidecar_text(optim));
+    write_text_file(ckpt_file(CkptFile::Config, out_dir), sidecar_text(spec));
+    write_text_file(ckpt_file(CkptFile::TrainerState, out_dir), sidecar_text(s.trainer));
+    write_text_file(ckpt_file(CkptFile::Manifest, out_dir), sidecar_text(s.manifest));
     if (options.verify) verify_checkpoint_dir(out_dir.string(), options.device);
     stats.device_ms = fa.device_ms;
     stats.bytes_moved = fa.bytes;

@@ -314,7 +314,7 @@ std::vector<fs::path> list_checkpoints(const fs::path& run_dir) {
     std::vector<std::pair<std::int64_t, fs::path>> found;
     for (const auto& e : fs::directory_iterator(run_dir)) {
         if (!e.is_directory()) continue;
-        if (auto st = parse_checkpoint_dir_name(e.path().filename().string())) found.emplace_back(*st, e.path());
+        if (auto st = step_of_dir(e.path().filename().string())) found.emplace_back(*st, e.path());
     }
     std::sort(found.begin(), found.end());
     std::vector<fs::path> out;

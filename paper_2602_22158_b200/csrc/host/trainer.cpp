@@ -283,7 +283,7 @@ void DeviceTrainer::save(const fs::path& dir, const TrainerMeta& meta, const std
                "derive weights");
     cuda_check(cudaMemcpyAsync(host.data(), out.get(), lay.weights.payload_bytes, cudaMemcpyDeviceToHost, stream_), "D2H");
     cuda_check(cudaStreamSynchronize(stream_), "sync");
-    write_container_file(weights_path(dir), lay.weights, host);
+    write_container_file(ckpt_file(CkptFile::Weights, dir), lay.weights, host);
     // shards: the kept groups' fields gathered (K2) out of the full partitions
     const bool complete = lay.groups.size() == static_cast<std::size_t>(model_.table().group_count());
     for (int r = 0; r < N_; ++r) {
@@ -302,7 +302,7 @@ void DeviceTrainer::save(const fs::path& dir, const TrainerMeta& meta, const std
             cuda_check(cudaMemcpyAsync(host.data(), out.get(), sl.payload_bytes, cudaMemcpyDeviceToHost, stream_), "D2H");
         }
         cuda_check(cudaStreamSynchronize(stream_), "sync");
-        write_container_file(shard_path(dir, r), sl, host);
+        write_container_file(ckpt_file(CkptFile::Shard, dir, r), sl, host);
     }
     std::map<int, AdamHyperparams> hyp;
     for (int g : lay.groups) hyp[g] = hyper_for_class(base_, model_.table().groups[static_cast<std::size_t>(g)].decay);
@@ -310,10 +310,10 @@ void DeviceTrainer::save(const fs::path& dir, const TrainerMeta& meta, const std
     man.step = meta.step;
     man.strategy = label;
     man.modules = modules;
-    write_text_file(optim_meta_path(dir), render_optim_meta_json(make_optim_meta(model_.table(), hyp, geom, meta.optimizer_t)));
-    write_text_file(config_path(dir), render_config_json(model_.spec()));
-    write_text_file(trainer_state_path(dir), render_trainer_state_json(meta));
-    write_text_file(manifest_path(dir), render_manifest_json(man));
+    write_text_file(ckpt_file(CkptFile::OptimMeta, dir), sidecar_text(make_optim_meta(model_.table(), hyp, geom, meta.optimizer_t)));
+    write_text_file(ckpt_file(CkptFile::Config, dir), sidecar_text(model_.spec()));
+    write_text_file(ckpt_file(CkptFile::TrainerState, dir), sidecar_text(meta));
+    write_text_file(ckpt_file(CkptFile::Manifest, dir), sidecar_text(man));
 }
 
 void DeviceTrainer::keep_masters() {
@@ -405,7 +405,7 @@ std::vector<fs::path> device_train(const DeviceTrainConfig& cfg, const fs::path&
             const Selection sel = select_by_magnitude({row}, M, cfg.rho);
             for (int m : sel.saved[1]) mods.push_back(tr.model().modules()[static_cast<std::size_t>(m)]);
         }
-        const fs::path dir = out_dir / checkpoint_dir_name(s);
+        const fs::path dir = out_dir / dir_of_step(s);
         tr.save(dir, meta, mods, cfg.magnitude ? "magnitude" : strategy_kind_name(cfg.strategy.kind));
         if (cfg.magnitude) tr.keep_masters();
         saved.push_back(dir);
