@@ -3,7 +3,12 @@
 // return code and the message goes to tg_last_error().
 #include "tailor_b200.h"
 
+#include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <cstring>
 #include <filesystem>
 #include <fcntl.h>
@@ -132,13 +137,13 @@ CheckpointSummary family_summary(const SynthFamily& f, const std::string& id) {
 }
 
 // Reads each snapshot's rank-r master fields into one packed device buffer.
+// (Buffers are reused across calls: a lane loads one rank after another.)
 void load_packed_masters(const std::vector<std::string>& dirs, int rank, const ModelLayout& model, int num_ranks,
-                         std::vector<DeviceBuffer>& out, std::vector<std::vector<std::uint64_t>>& offs) {
+                         std::vector<DeviceBuffer>& out, std::vector<std::vector<std::uint64_t>>& offs,
+                         PinnedBuffer& stage, int threads) {
     const auto fields = score_fields(model, num_ranks);
-    out.clear();
     out.resize(dirs.size());
     offs.assign(dirs.size(), {});
-    PinnedBuffer stage;
     for (std::size_t k = 0; k < dirs.size(); ++k) {
         const fs::path p = ckpt_file(CkptFile::Shard, dirs[k], rank);
         const ContainerLayout lay = read_layout(p);
@@ -159,7 +164,7 @@ void load_packed_masters(const std::vector<std::string>& dirs, int rank, const M
         std::vector<ReadJob> jobs;
         for (const auto& [e, at] : where) jobs.push_back({fd, stage.get() + at, e->bytes(), lay.payload_offset() + e->begin});
         try {
-            run_reads(jobs, io_threads(), p.string());
+            run_reads(jobs, threads, p.string());
         } catch (...) {
             ::close(fd);
             throw;
@@ -190,18 +195,63 @@ void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<st
     const int K = static_cast<int>(dirs.size()), M = model.module_count();
     sd.assign(static_cast<std::size_t>(K - 1), std::vector<double>(static_cast<std::size_t>(M), 0.0));
     sr = sd;
-    DeviceBuffer dout(static_cast<std::size_t>(K - 1) * M * 2 * sizeof(double));
-    std::vector<double> h(static_cast<std::size_t>(K - 1) * M * 2);
+    // Ranks are independent: lanes (threads with their own buffers) score one
+    // rank each; the per-rank partials are summed in rank order afterwards, so
+    // the result does not depend on the lane count.
+    std::uint64_t per_rank = 16;
+    for (const auto& f : score_fields(model, N)) per_rank += (static_cast<std::uint64_t>(f.chunk) * 4 + 15) & ~15ull;
+    per_rank *= static_cast<std::uint64_t>(K);
+    std::size_t free_b = 0, total_b = 0;
+    cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    const std::uint64_t budget = free_b > (2ull << 30) ? (free_b - (2ull << 30)) / 2 : 0;
+    const int lanes = std::clamp<int>(static_cast<int>(std::min<std::uint64_t>(budget / per_rank, 8)), 1, std::min(N, 8));
+    const int readers = std::max(1, io_threads() / lanes);
+    const std::size_t nres = static_cast<std::size_t>(K - 1) * M * 2;
+    std::vector<std::vector<double>> res(static_cast<std::size_t>(N), std::vector<double>(nres));
+    std::atomic<int> next{0};
+    std::exception_ptr lane_err;
+    std::mutex mu;
+    const auto lane = [&] {
+        try {
+            cuda_check(cudaSetDevice(device), "cudaSetDevice");
+            cudaStream_t st = nullptr;
+            cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+            std::unique_ptr<CUstream_st, decltype(&cudaStreamDestroy)> own(st, &cudaStreamDestroy);
+            DeviceBuffer dout(nres * sizeof(double));
+            std::vector<DeviceBuffer> bufs;
+            PinnedBuffer stage;
+            for (int r = next.fetch_add(1); r < N; r = next.fetch_add(1)) {
+                {
+                    std::lock_guard<std::mutex> lk(mu);
+                    if (lane_err) break;
+                }
+                std::vector<std::vector<std::uint64_t>> offs;
+                PhaseTimer pt("score.rank");
+                load_packed_masters(dirs, r, model, N, bufs, offs, stage, readers);
+                ScorePlan plan(model, N, offs);
+                std::vector<const std::uint8_t*> bases;
+                for (auto& b : bufs) bases.push_back(b.get());
+                plan.run(bases.data(), dout.get<double>(), st);
+                cuda_check(cudaMemcpyAsync(res[static_cast<std::size_t>(r)].data(), dout.get(), nres * sizeof(double),
+                                           cudaMemcpyDeviceToHost, st),
+                           "D2H");
+                cuda_check(cudaStreamSynchronize(st), "sync");
+            }
+        } catch (...) {
+            std::lock_guard<std::mutex> lk(mu);
+            if (!lane_err) lane_err = std::current_exception();
+        }
+    };
+    if (lanes == 1) {
+        lane();
+    } else {
+        std::vector<std::thread> pool;
+        for (int i = 0; i < lanes; ++i) pool.emplace_back(lane);
+        for (auto& t : pool) t.join();
+    }
+    if (lane_err) std::rethrow_exception(lane_err);
     for (int r = 0; r < N; ++r) {
-        std::vector<DeviceBuffer> bufs;
-        std::vector<std::vector<std::uint64_t>> offs;
-        PhaseTimer pt("score.rank");
-        load_packed_masters(dirs, r, model, N, bufs, offs);
-        ScorePlan plan(model, N, offs);
-        std::vector<const std::uint8_t*> bases;
-        for (auto& b : bufs) bases.push_back(b.get());
-        plan.run(bases.data(), dout.get<double>(), nullptr);
-        cuda_check(cudaMemcpy(h.data(), dout.get(), h.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+        const auto& h = res[static_cast<std::size_t>(r)];
         for (int p = 0; p < K - 1; ++p)
             for (int m = 0; m < M; ++m) {
                 sd[static_cast<std::size_t>(p)][static_cast<std::size_t>(m)] += h[(static_cast<std::size_t>(p) * M + m) * 2];

@@ -3,6 +3,7 @@
 #include "tailor/engine.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <fcntl.h>
@@ -10,6 +11,7 @@
 #include <fstream>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <unistd.h>
 
 #include "tailor/errors.hpp"
@@ -781,13 +783,21 @@ std::vector<double> DeviceSelectStep::scores(cudaStream_t s) {
 // ---- device re-verify --------------------------------------------------------------
 namespace {
 
-void load_payload(const fs::path& path, const ContainerLayout& lay, DeviceBuffer& dst, PinnedBuffer& stage) {
+struct StreamHandle {
+    cudaStream_t s = nullptr;
+    StreamHandle() { cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream"); }
+    ~StreamHandle() { cudaStreamDestroy(s); }
+    StreamHandle(const StreamHandle&) = delete;
+    StreamHandle& operator=(const StreamHandle&) = delete;
+};
+
+void load_payload(const fs::path& path, const ContainerLayout& lay, DeviceBuffer& dst, PinnedBuffer& stage,
+                  int threads = io_threads(), std::uint64_t step = 512ull << 20) {
     dst.resize(std::max<std::uint64_t>(16, lay.payload_bytes));
     const int fd = ::open(path.c_str(), O_RDONLY);
     if (fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + path.string() + "'");
-    // 512 MB windows read by the I/O pool, alternating two halves of the pinned
-    // stage so the H2D of one overlaps the reads of the next.
-    const std::uint64_t step = 512ull << 20;
+    // `step`-byte windows read by the I/O pool, alternating two halves of the
+    // pinned stage so the H2D of one overlaps the reads of the next.
     stage.resize(2 * step);
     cudaStream_t s = nullptr;
     cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
@@ -801,7 +811,7 @@ void load_payload(const fs::path& path, const ContainerLayout& lay, DeviceBuffer
             const std::uint64_t n = std::min(step, lay.payload_bytes - off);
             std::uint8_t* buf = stage.get() + static_cast<std::uint64_t>(half) * step;
             if (used[half]) cuda_check(cudaEventSynchronize(done[half]), "event");
-            run_reads({{fd, buf, n, lay.payload_offset() + off}}, io_threads(), path.string());
+            run_reads({{fd, buf, n, lay.payload_offset() + off}}, threads, path.string());
             cuda_check(cudaMemcpyAsync(dst.get() + off, buf, n, cudaMemcpyHostToDevice, s), "H2D");
             cuda_check(cudaEventRecord(done[half], s), "event");
             used[half] = true;
@@ -850,64 +860,124 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
     if (wl.entries.size() != expect_tensors)
         fail(ErrorKind::CorruptContainer, ckpt_file(CkptFile::Weights, dir).string() + ": contains tensors not in the manifest");
 
-    DeviceBuffer dw, ds, dpairs, dranges, derr(3 * sizeof(unsigned long long));
-    PinnedBuffer stage;
-    {
-        PhaseTimer pt("verify.load_weights");
-        load_payload(ckpt_file(CkptFile::Weights, dir), wl, dw, stage);
-    }
-    unsigned long long err[3] = {0, 0, 0};
-    cuda_check(cudaMemset(derr.get(), 0, sizeof(err)), "memset");
-    for (int r = 0; r < s.optim.num_ranks; ++r) {
-        const ContainerLayout sl = read_layout(ckpt_file(CkptFile::Shard, dir, r));
+    // Structure of every rank file first (rank order), with the verify work of
+    // each rank as offsets into its payload; then the payloads stream to the
+    // device over parallel lanes (one rank file each) and the failure counters
+    // are checked in rank order.
+    const int N = s.optim.num_ranks;
+    std::vector<ContainerLayout> shard_lay;
+    std::vector<std::vector<dev::VerifyPair>> pairs(static_cast<std::size_t>(N));
+    std::vector<std::vector<dev::VerifyRange>> ranges(static_cast<std::size_t>(N));
+    std::uint64_t max_shard = 16;
+    for (int r = 0; r < N; ++r) {
+        const fs::path sp = ckpt_file(CkptFile::Shard, dir, r);
+        shard_lay.push_back(read_layout(sp));
+        const ContainerLayout& sl = shard_lay.back();
+        max_shard = std::max<std::uint64_t>(max_shard, sl.payload_bytes);
         auto mr = sl.metadata.find("rank");
         if (mr != sl.metadata.end() && mr->second != std::to_string(r))
-            fail(ErrorKind::CorruptContainer, ckpt_file(CkptFile::Shard, dir, r).string() + ": rank metadata mismatch");
-        load_payload(ckpt_file(CkptFile::Shard, dir, r), sl, ds, stage);
-        std::vector<dev::VerifyPair> pairs;
-        std::vector<dev::VerifyRange> ranges;
+            fail(ErrorKind::CorruptContainer, sp.string() + ": rank metadata mismatch");
         for (const auto& g : s.optim.groups) {
             const Entry* f[3];
             const char* names[3] = {".master", ".exp_avg", ".exp_avg_sq"};
             for (int i = 0; i < 3; ++i) {
                 f[i] = sl.find(shard_key(g.index, names[i]));
-                if (!f[i])
-                    fail(ErrorKind::CorruptContainer,
-                         ckpt_file(CkptFile::Shard, dir, r).string() + ": missing tensor '" + shard_key(g.index, names[i]) + "'");
+                if (!f[i]) fail(ErrorKind::CorruptContainer, sp.string() + ": missing tensor '" + shard_key(g.index, names[i]) + "'");
                 if (f[i]->dtype != Dtype::F32 || f[i]->shape != std::vector<std::int64_t>{g.shard_length})
-                    fail(ErrorKind::Geometry, ckpt_file(CkptFile::Shard, dir, r).string() + ": tensor '" + shard_key(g.index, names[i]) +
-                                                  "' has unexpected dtype/shape");
+                    fail(ErrorKind::Geometry,
+                         sp.string() + ": tensor '" + shard_key(g.index, names[i]) + "' has unexpected dtype/shape");
             }
+            // pointers below are payload offsets (shard) / weights offsets; rebased per lane
             const std::int64_t c = g.shard_length, first = static_cast<std::int64_t>(r) * c;
             const std::int64_t valid = std::clamp<std::int64_t>(g.true_length - first, 0, c);
+            auto at = [](std::uint64_t off) { return reinterpret_cast<const std::uint32_t*>(off); };
             for (int i = 0; i < 3; ++i)
                 if (valid < c)
-                    ranges.push_back({reinterpret_cast<const std::uint32_t*>(ds.get() + f[i]->begin) + valid,
-                                      static_cast<std::uint64_t>(c - valid), 0, 0});
-            if (valid > 0)
-                ranges.push_back({reinterpret_cast<const std::uint32_t*>(ds.get() + f[2]->begin),
-                                  static_cast<std::uint64_t>(valid), 1, 0});
+                    ranges[static_cast<std::size_t>(r)].push_back(
+                        {at(f[i]->begin + static_cast<std::uint64_t>(valid) * 4), static_cast<std::uint64_t>(c - valid), 0, 0});
+            if (valid > 0) ranges[static_cast<std::size_t>(r)].push_back({at(f[2]->begin), static_cast<std::uint64_t>(valid), 1, 0});
             for (const auto& sl2 : group_slices.at(g.index)) {
                 const std::int64_t a = std::max(first, sl2.group_offset);
                 const std::int64_t b = std::min(first + valid, sl2.group_offset + sl2.decl.numel());
                 if (a >= b) continue;
                 const Entry* we = wl.find(sl2.decl.name);
-                pairs.push_back({reinterpret_cast<const float*>(ds.get() + f[0]->begin) + (a - first),
-                                 reinterpret_cast<const std::uint16_t*>(dw.get() + we->begin) + (a - sl2.group_offset),
-                                 static_cast<std::uint64_t>(b - a)});
+                pairs[static_cast<std::size_t>(r)].push_back(
+                    {reinterpret_cast<const float*>(f[0]->begin + static_cast<std::uint64_t>(a - first) * 4),
+                     reinterpret_cast<const std::uint16_t*>(we->begin + static_cast<std::uint64_t>(a - sl2.group_offset) * 2),
+                     static_cast<std::uint64_t>(b - a)});
             }
         }
-        dpairs.upload(pairs.data(), pairs.size() * sizeof(dev::VerifyPair));
-        dranges.upload(ranges.data(), ranges.size() * sizeof(dev::VerifyRange));
-        cuda_check(dev::launch_verify(dpairs.get<dev::VerifyPair>(), static_cast<std::uint32_t>(pairs.size()),
-                                      dranges.get<dev::VerifyRange>(), static_cast<std::uint32_t>(ranges.size()),
-                                      derr.get<unsigned long long>(), nullptr),
-                   "verify");
-        cuda_check(cudaMemcpy(err, derr.get(), sizeof(err), cudaMemcpyDeviceToHost), "D2H");
-        if (err[1]) fail(ErrorKind::CorruptContainer, dir.string() + ": nonzero padding in rank " + std::to_string(r));
-        if (err[2]) fail(ErrorKind::Consistency, "exp_avg_sq contains a negative or non-finite element");
     }
-    if (err[0]) fail(ErrorKind::Consistency, dir.string() + ": a weight tensor disagrees with its FP32 master");
+
+    DeviceBuffer dw, derr(static_cast<std::size_t>(N) * 3 * sizeof(unsigned long long));
+    cuda_check(cudaMemset(derr.get(), 0, derr.size()), "memset");
+    std::size_t free_b = 0, total_b = 0;
+    cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    const std::uint64_t budget = free_b > wl.payload_bytes + (2ull << 30) ? (free_b - wl.payload_bytes - (2ull << 30)) / 2 : 0;
+    const int lanes = std::clamp<int>(static_cast<int>(std::min<std::uint64_t>(budget / max_shard, 8)), 1, std::max(1, std::min(N, 8)));
+    const int readers = std::max(1, io_threads() / lanes);
+    const std::uint64_t step = lanes > 1 ? (64ull << 20) : (512ull << 20);
+    {
+        PhaseTimer pt("verify.load_weights");
+        PinnedBuffer stage;
+        load_payload(ckpt_file(CkptFile::Weights, dir), wl, dw, stage, io_threads(), step);
+    }
+    std::atomic<int> next{0};
+    std::exception_ptr lane_err;
+    std::mutex mu;
+    const auto lane = [&] {
+        try {
+            cuda_check(cudaSetDevice(device), "cudaSetDevice");
+            DeviceBuffer ds, dpairs, dranges;
+            PinnedBuffer stage;
+            StreamHandle ls;
+            for (int r = next.fetch_add(1); r < N; r = next.fetch_add(1)) {
+                {
+                    std::lock_guard<std::mutex> lk(mu);
+                    if (lane_err) break;
+                }
+                const auto& sl = shard_lay[static_cast<std::size_t>(r)];
+                load_payload(ckpt_file(CkptFile::Shard, dir, r), sl, ds, stage, readers, step);
+                auto pr = pairs[static_cast<std::size_t>(r)];
+                auto rg = ranges[static_cast<std::size_t>(r)];
+                for (auto& x : pr) {
+                    x.master = reinterpret_cast<const float*>(ds.get() + reinterpret_cast<std::uintptr_t>(x.master));
+                    x.weight = reinterpret_cast<const std::uint16_t*>(dw.get() + reinterpret_cast<std::uintptr_t>(x.weight));
+                }
+                for (auto& x : rg) x.words = reinterpret_cast<const std::uint32_t*>(ds.get() + reinterpret_cast<std::uintptr_t>(x.words));
+                dpairs.upload(pr.data(), pr.size() * sizeof(dev::VerifyPair));
+                dranges.upload(rg.data(), rg.size() * sizeof(dev::VerifyRange));
+                cuda_check(dev::launch_verify(dpairs.get<dev::VerifyPair>(), static_cast<std::uint32_t>(pr.size()),
+                                              dranges.get<dev::VerifyRange>(), static_cast<std::uint32_t>(rg.size()),
+                                              derr.get<unsigned long long>() + 3 * r, ls.s),
+                           "verify");
+                cuda_check(cudaStreamSynchronize(ls.s), "verify");
+            }
+        } catch (...) {
+            std::lock_guard<std::mutex> lk(mu);
+            if (!lane_err) lane_err = std::current_exception();
+        }
+    };
+    {
+        PhaseTimer pt("verify.shards");
+        if (lanes == 1) {
+            lane();
+        } else {
+            std::vector<std::thread> pool;
+            for (int i = 0; i < lanes; ++i) pool.emplace_back(lane);
+            for (auto& t : pool) t.join();
+        }
+    }
+    if (lane_err) std::rethrow_exception(lane_err);
+    std::vector<unsigned long long> err(static_cast<std::size_t>(N) * 3);
+    cuda_check(cudaMemcpy(err.data(), derr.get(), derr.size(), cudaMemcpyDeviceToHost), "D2H");
+    bool mismatch = false;
+    for (int r = 0; r < N; ++r) {
+        if (err[3 * r + 1]) fail(ErrorKind::CorruptContainer, dir.string() + ": nonzero padding in rank " + std::to_string(r));
+        if (err[3 * r + 2]) fail(ErrorKind::Consistency, "exp_avg_sq contains a negative or non-finite element");
+        mismatch = mismatch || err[3 * r] != 0;
+    }
+    if (mismatch) fail(ErrorKind::Consistency, dir.string() + ": a weight tensor disagrees with its FP32 master");
 }
 
 } // namespace tailor

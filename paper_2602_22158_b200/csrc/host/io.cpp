@@ -36,6 +36,13 @@ PhaseTimer::~PhaseTimer() {
     if (on_) std::fprintf(stderr, "[tailor] %s %.2f ms\n", name_, now_ms() - t0_);
 }
 
+ScopedAccum::ScopedAccum(double& sink) : sink_(sink), t0_(now_ms()) {}
+ScopedAccum::~ScopedAccum() { sink_ += now_ms() - t0_; }
+
+void trace_value(const char* name, double ms) {
+    if (trace_on()) std::fprintf(stderr, "[tailor] %s %.2f ms\n", name, ms);
+}
+
 int io_threads() {
     const unsigned hw = std::thread::hardware_concurrency();
     return static_cast<int>(std::clamp<unsigned>(hw ? hw : 4u, 1u, 16u));

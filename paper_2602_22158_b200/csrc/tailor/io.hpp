@@ -38,4 +38,19 @@ class PhaseTimer {
     bool on_;
 };
 
+// Adds the scope's wall time (ms) to `sink`.
+class ScopedAccum {
+  public:
+    explicit ScopedAccum(double& sink);
+    ~ScopedAccum();
+    ScopedAccum(const ScopedAccum&) = delete;
+    ScopedAccum& operator=(const ScopedAccum&) = delete;
+
+  private:
+    double& sink_;
+    double t0_;
+};
+// Prints "[tailor] <name> <ms>" when TAILOR_TRACE=1.
+void trace_value(const char* name, double ms);
+
 } // namespace tailor

@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Phase trace of the file-facing drop-in path (TAILOR_TRACE=1): medium shape
+"""Phase trace (usage: files_trace.py [root_dir] [iters]) of the file-facing drop-in path (TAILOR_TRACE=1): medium shape
 L8 h1024 f2752 v32000, N=8, K=4 written to /tmp, then select_recipe + execute_merge."""
 import os
 import pathlib
@@ -13,13 +13,15 @@ ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 import paper_2602_22158_b200 as t  # noqa: E402
 
-work = pathlib.Path(tempfile.mkdtemp(prefix="tailor-trace-"))
+root = sys.argv[1] if len(sys.argv) > 1 else None  # e.g. /dev/shm (default: $TMPDIR or /tmp)
+iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+work = pathlib.Path(tempfile.mkdtemp(prefix="tailor-trace-", dir=root))
 try:
     fam = t.SynthFamily(t.ModelSpec(8, 1024, 2752, 32000, False, 42), 8, 4, 100)
     dirs = [str(work / f"checkpoint-{k * 100}") for k in range(1, 5)]
     for k in range(1, 5):
         fam.write_dir(k, dirs[k - 1])
-    for i in range(3):
+    for i in range(iters):
         t0 = time.perf_counter()
         rec, _, _ = t.select_recipe(dirs, 0.5)
         t1 = time.perf_counter()
