@@ -970,7 +970,7 @@ def files_arm(args):
         dirs = [str(work / "run" / f"checkpoint-{k * 100}") for k in range(1, K + 1)]
         for k in range(1, K + 1):
             fam.write_dir(k, dirs[k - 1])
-        ours, refs, comp = [], [], 0
+        ours, refs, comp, step_ms = [], [], 0, []
         for i in range(args.warmup + args.steps):
             out = work / f"ours-{i}"
             t0 = time.perf_counter()
@@ -984,6 +984,7 @@ def files_arm(args):
             shutil.rmtree(out, ignore_errors=True)
             if i >= args.warmup:
                 ours.append(dt)
+                step_ms.append((phases["select_ms"], phases["merge_ms"]))
         ref_steps = max(1, min(args.steps, 3))
         for i in range(1 + ref_steps):
             out = work / f"ref-{i}"
@@ -1005,7 +1006,8 @@ def files_arm(args):
         "vs_baseline": None, "dtype": "u8/f32/f64", "data": "synthetic (written by the GPU writer, byte-identical "
                                                           "to the reference writer), page cache warm",
         "config": {"workload": "files", "shape": f"L{L} h{h} f{f} v{v} N{N} K{K} rho{rho}",
-                   "composite_bytes": comp, "min_boundary_gap": gap, "last_step_phases": phases},
+                   "composite_bytes": comp, "min_boundary_gap": gap, "last_step_phases": phases,
+                   "steps_select_merge_ms": step_ms},
         "reference": {"value": round(r_v, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
                       "ms_per_step": round(statistics.median(refs) * 1e3, 1)},
         "speedup_vs_reference": round(o_v / r_v, 2)}))

@@ -273,14 +273,14 @@ struct AssembleTotals {
     std::uint64_t bytes = 0;
 };
 
-// Runs the output files over up to 8 lanes (largest file first, pulled from a
+// Runs the output files over up to 16 lanes (largest file first, pulled from a
 // shared queue). Output bytes do not depend on the lane count or timing: each
 // file is produced by exactly one lane, in chunk order.
 AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool uncached, int device) {
     std::sort(jobs.begin(), jobs.end(), [](const OutputJob& a, const OutputJob& b) {
         return a.plan->dst_hi - a.plan->dst_lo > b.plan->dst_hi - b.plan->dst_lo;
     });
-    const int lanes = std::clamp<int>(std::min<int>(static_cast<int>(jobs.size()), workers), 1, 8);
+    const int lanes = std::clamp<int>(std::min<int>(static_cast<int>(jobs.size()), workers), 1, 16);
     const int readers = std::max(1, workers / lanes);
     const std::uint64_t chunk = lanes > 1 ? (32ull << 20) : (128ull << 20);
     std::vector<AssembleTotals> part(static_cast<std::size_t>(lanes));
