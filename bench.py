@@ -906,8 +906,10 @@ def hoststaged_arm(args, rank, world, local_rank):
 def trainer_arm(args, rank, world, local_rank):
     """SURVEY §8 f4 at scale: the device-resident trainer step (bit-exact AdamW on a
     Llama-3.1-8B-shaped ZeRO rank partition, one partition per GPU). Algorithmic bytes
-    per element: grad pass 4 (w) + 4 (g out); update pass 12 + 4 (w,m,v + g in) read,
-    12 written = 36 B (both passes stream host-built TrainTile runs as float4). Each step synchronizes once (the non-finite check precedes any
+    per element: grad pass 4 (w read); update pass 12 (w,m,v) read + 12 written, the
+    gradient recomputed from w = 28 B (TAILOR_TRAIN_STORE_GRAD=1: the gradient goes
+    through a scratch buffer, 4 + 4 + 16 + 12 = 36 B). Both passes stream host-built
+    TrainTile runs as float4. Each step synchronizes once (the non-finite check precedes any
     state change, as apply_step requires) and once more for the norm partials; timed by
     wall clock around synchronized steps, max over ranks."""
     import torch
@@ -934,7 +936,8 @@ def trainer_arm(args, rank, world, local_rank):
         all_reduce(tt, dist.ReduceOp.MAX)
         dt = float(tt.item())
     hbm, kind = peaks()
-    gbs = 36 * n * args.steps / dt / 1e9
+    bpe = 36 if os.environ.get("TAILOR_TRAIN_STORE_GRAD", "0") not in ("", "0") else 28
+    gbs = bpe * n * args.steps / dt / 1e9
     if rank == 0:
         print(json.dumps({
             "metric": "device trainer steps: optimizer elements updated per second (bit-exact AdamW)",
@@ -945,7 +948,8 @@ def trainer_arm(args, rank, world, local_rank):
             "config": {"workload": "train", "model": "Llama-3.1-8B-shaped", "zero_ranks": N,
                        "elements_per_gpu": n, "unit_of_work": "one rank partition per GPU"},
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
-                         "frac": round(gbs / hbm, 4), "peak_kind": kind, "bytes_per_element": 36},
+                         "frac": round(gbs / hbm, 4), "peak_kind": kind, "bytes_per_element": bpe,
+                         "gradient": "scratch buffer" if bpe == 36 else "recomputed in the update pass"},
             "last_norms": {"grad": gn, "update": un}, "gpu_launches": 2 * args.steps, "clocks": clocks.summary()}))
     return 0
 

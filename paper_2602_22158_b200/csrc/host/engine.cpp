@@ -56,19 +56,31 @@ struct PinnedPool {
     std::multimap<std::size_t, void*> free_; // size -> block
     std::size_t pooled = 0;
 
+    // Size classes (2^k x {1, 1.25, 1.5, 1.75}, >= 2 MB), matched exactly: a request never takes a block
+    // of another class, so the staging buffers of different phases (16-32 MB
+    // assemble slots, 64-128 MB verify / scorer stages) each keep their own
+    // blocks, and a warm process never pins again (cudaMallocHost holds a
+    // driver lock that stalls every other thread's CUDA calls).
+    static std::size_t size_class(std::size_t n) {
+        std::size_t base = 2u << 20;
+        while (base * 2 <= n) base <<= 1;
+        for (std::size_t q = 4; q <= 8; ++q)
+            if (base / 4 * q >= n) return base / 4 * q;
+        return base * 2;
+    }
     void* take(std::size_t n, std::size_t* got) {
+        const std::size_t sz = size_class(n);
         {
             std::lock_guard<std::mutex> lk(mu);
-            auto it = free_.lower_bound(n);
-            if (it != free_.end() && it->first <= 4 * n + (64u << 20)) {
+            auto it = free_.find(sz);
+            if (it != free_.end()) {
                 void* p = it->second;
-                *got = it->first;
-                pooled -= it->first;
+                *got = sz;
+                pooled -= sz;
                 free_.erase(it);
                 return p;
             }
         }
-        const std::size_t sz = (n + (2u << 20) - 1) & ~((2ull << 20) - 1); // 2 MB granules
         void* p = nullptr;
         cuda_check(cudaMallocHost(&p, sz), "cudaMallocHost");
         *got = sz;

@@ -12,6 +12,7 @@
 #include <atomic>
 #include <exception>
 #include <chrono>
+#include <condition_variable>
 #include <cstring>
 #include <fcntl.h>
 #include <filesystem>
@@ -50,24 +51,27 @@ void pwrite_all(int fd, const std::uint8_t* src, std::uint64_t n, std::uint64_t 
 std::uint64_t align16(std::uint64_t x) { return (x + 15) & ~15ull; }
 
 // One lane of the file pipeline: assembles whole output container files, one
-// chunk at a time through two slots (pread -> H2D -> K2 -> D2H -> pwrite), the
-// GPU work of one slot overlapping the host I/O of the other. Lanes run on their
-// own threads, each writing a different file: buffered writes to ONE file
-// serialise on its inode lock (tools/write_probe.cpp: 8 threads on one file
-// 1.8-2.5 GB/s, on 8 files 10-12 GB/s), so the parallelism is across files.
+// chunk at a time through kSlots slots: the lane thread preads chunk i while the
+// GPU runs chunk i-1 (H2D -> K2 -> D2H on the slot's stream) and the lane's
+// writer thread pwrites chunk i-2. Lanes run on their own threads, each writing
+// a different file: buffered writes to ONE file serialise on its inode lock
+// (tools/write_probe.cpp: 8 threads on one file ~4.7 GB/s, on 8 files 20-30 GB/s
+// on the B200 host), so the parallelism is across files.
 class FileAssembler {
   public:
+    static constexpr int kSlots = 3;
+
     FileAssembler(int read_threads, bool uncached, std::uint64_t chunk)
         : workers_(std::max(1, read_threads)), uncached_(uncached), chunk_(chunk) {
         for (auto& s : stream_) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kSlots; ++i) {
             cuda_check(cudaEventCreate(&ev0_[i]), "event");
             cuda_check(cudaEventCreate(&ev1_[i]), "event");
         }
     }
     ~FileAssembler() {
         for (auto& s : stream_) cudaStreamDestroy(s);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kSlots; ++i) {
             cudaEventDestroy(ev0_[i]);
             cudaEventDestroy(ev1_[i]);
         }
@@ -77,7 +81,6 @@ class FileAssembler {
     std::uint64_t bytes = 0;
 
     void assemble(const PartitionPlan& pp, const std::vector<fs::path>& window_files, const fs::path& out_path) {
-        const std::uint64_t chunk = chunk_;
         Fd out(out_path, O_WRONLY | O_CREAT | O_TRUNC);
         if (out.fd < 0) fail(ErrorKind::Storage, "cannot create '" + out_path.string() + "'");
         const std::string prefix = pp.out.prefix();
@@ -94,8 +97,8 @@ class FileAssembler {
                 if (fds[w]->fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + window_files[w].string() + "'");
             }
         }
-        HostMergeChunks plan(pp, chunk);
-        for (int i = 0; i < 2; ++i) {
+        HostMergeChunks plan(pp, chunk_);
+        for (int i = 0; i < kSlots; ++i) {
             pin_in_[i].resize(std::max<std::uint64_t>(16, plan.max_staging));
             pin_out_[i].resize(std::max<std::uint64_t>(16, plan.max_out));
             d_in_[i].resize(std::max<std::uint64_t>(16, plan.max_staging));
@@ -103,75 +106,121 @@ class FileAssembler {
             d_segs_[i].resize(std::max<std::size_t>(1, plan.max_segs) * sizeof(dev::GatherSeg));
             pin_segs_[i].resize(std::max<std::size_t>(1, plan.max_segs) * sizeof(dev::GatherSeg));
         }
-        int pending[2] = {-1, -1};
-        const auto flush = [&](int slot) {
-            if (pending[slot] < 0) return;
-            {
-                ScopedAccum acc(wait_ms);
-                cuda_check(cudaStreamSynchronize(stream_[slot]), "sync");
-            }
-            ScopedAccum acc(write_ms);
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, ev0_[slot], ev1_[slot]);
-            device_ms += ms;
-            const auto& c = plan.chunks[static_cast<std::size_t>(pending[slot])];
-            pwrite_all(out.fd, pin_out_[slot].get(), c.hi - c.lo, base + c.lo, out_path.string());
-            pending[slot] = -1;
-        };
-        for (std::size_t ci = 0; ci < plan.chunks.size(); ++ci) {
-            const int slot = static_cast<int>(ci & 1);
-            flush(slot);
-            const auto& c = plan.chunks[ci];
-            // This chunk's source ranges -> pinned staging, via the parallel pread pool
-            // (uncached mode re-opens the source file per read, as the reference
-            // reloads a shard per group copy).
-            std::vector<std::unique_ptr<Fd>> opened;
-            std::vector<ReadJob> jobs;
-            for (const auto& rd : c.reads) {
-                int fd;
-                if (pp.windows[rd.w].container == kZeroContainer) {
-                    std::memset(pin_in_[slot].get() + rd.at, 0, rd.b - rd.a);
-                    continue;
+
+        // Writer: takes chunks in order, waits for the slot's stream, pwrites,
+        // frees the slot. `written` counts chunks fully on disk (page cache).
+        std::mutex mu;
+        std::condition_variable cv;
+        std::size_t issued = 0, written = 0;
+        std::exception_ptr werr;
+        std::thread writer([&] {
+            try {
+                for (std::size_t ci = 0; ci < plan.chunks.size(); ++ci) {
+                    {
+                        std::unique_lock<std::mutex> lk(mu);
+                        cv.wait(lk, [&] { return issued > ci || werr; });
+                        if (werr) return;
+                    }
+                    const int slot = static_cast<int>(ci % kSlots);
+                    {
+                        ScopedAccum acc(wait_ms);
+                        cuda_check(cudaStreamSynchronize(stream_[slot]), "sync");
+                    }
+                    float ms = 0.f;
+                    cudaEventElapsedTime(&ms, ev0_[slot], ev1_[slot]);
+                    device_ms += ms;
+                    const auto& c = plan.chunks[ci];
+                    {
+                        ScopedAccum acc(write_ms);
+                        pwrite_all(out.fd, pin_out_[slot].get(), c.hi - c.lo, base + c.lo, out_path.string());
+                    }
+                    std::lock_guard<std::mutex> lk(mu);
+                    written = ci + 1;
+                    cv.notify_all();
                 }
-                if (uncached_) {
-                    opened.push_back(std::make_unique<Fd>(window_files[rd.w], O_RDONLY));
-                    if (opened.back()->fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + window_files[rd.w].string() + "'");
-                    fd = opened.back()->fd;
-                } else {
-                    fd = fds[rd.w]->fd;
+            } catch (...) {
+                std::lock_guard<std::mutex> lk(mu);
+                werr = std::current_exception();
+                cv.notify_all();
+            }
+        });
+        std::exception_ptr rerr;
+        try {
+            for (std::size_t ci = 0; ci < plan.chunks.size(); ++ci) {
+                const int slot = static_cast<int>(ci % kSlots);
+                {
+                    std::unique_lock<std::mutex> lk(mu); // the slot's previous chunk is written
+                    cv.wait(lk, [&] { return written + kSlots > ci || werr; });
+                    if (werr) break;
                 }
-                jobs.push_back({fd, pin_in_[slot].get() + rd.at, rd.b - rd.a, file_off[rd.w] + rd.a});
+                stage_chunk(plan.chunks[ci], pp, window_files, file_off, fds, slot, out_path);
+                std::lock_guard<std::mutex> lk(mu);
+                issued = ci + 1;
+                cv.notify_all();
             }
-            {
-                ScopedAccum acc(read_ms);
-                run_reads(jobs, workers_, out_path.string());
-            }
-            cudaStream_t s = stream_[slot];
-            cuda_check(cudaMemcpyAsync(d_in_[slot].get(), pin_in_[slot].get(), c.staging, cudaMemcpyHostToDevice, s), "H2D");
-            // (the slot's previous chunk has been flushed, so its pinned table is free)
-            auto* segs = reinterpret_cast<dev::GatherSeg*>(pin_segs_[slot].get());
-            for (std::size_t i = 0; i < c.segs.size(); ++i) {
-                segs[i] = c.segs[i];
-                segs[i].src = d_in_[slot].get() + reinterpret_cast<std::uintptr_t>(c.segs[i].src);
-            }
-            cuda_check(cudaMemcpyAsync(d_segs_[slot].get(), segs, c.segs.size() * sizeof(dev::GatherSeg),
-                                       cudaMemcpyHostToDevice, s),
-                       "segs");
-            cuda_check(cudaEventRecord(ev0_[slot], s), "event");
-            cuda_check(dev::launch_gather(d_segs_[slot].get<dev::GatherSeg>(), static_cast<std::uint32_t>(c.segs.size()),
-                                          d_out_[slot].get(), c.hi - c.lo, dev::kGatherAuto, c.bulk_ok, s),
-                       "gather");
-            cuda_check(cudaEventRecord(ev1_[slot], s), "event");
-            cuda_check(cudaMemcpyAsync(pin_out_[slot].get(), d_out_[slot].get(), c.hi - c.lo, cudaMemcpyDeviceToHost, s), "D2H");
-            pending[slot] = static_cast<int>(ci);
-            bytes += c.hi - c.lo;
+        } catch (...) {
+            rerr = std::current_exception();
         }
-        flush(0);
-        flush(1);
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (rerr && !werr) werr = rerr; // stops the writer
+            cv.notify_all();
+        }
+        writer.join();
+        for (auto& st : stream_) cudaStreamSynchronize(st);
+        if (rerr) std::rethrow_exception(rerr);
+        if (werr) std::rethrow_exception(werr);
         if (plan.chunks.empty() && pp.out.payload_bytes != 0) fail(ErrorKind::Consistency, "empty merge plan");
     }
 
   private:
+    struct ChunkPlan;
+
+    // Reads one chunk's source ranges into the slot's pinned staging (parallel
+    // pread; uncached mode re-opens the source file per read, as the reference
+    // reloads a shard per group copy), then queues H2D -> K2 -> D2H on the slot.
+    void stage_chunk(const ChunkPlan& c, const PartitionPlan& pp, const std::vector<fs::path>& window_files,
+                     const std::vector<std::uint64_t>& file_off, const std::vector<std::unique_ptr<Fd>>& fds, int slot,
+                     const fs::path& out_path) {
+        std::vector<std::unique_ptr<Fd>> opened;
+        std::vector<ReadJob> jobs;
+        for (const auto& rd : c.reads) {
+            int fd;
+            if (pp.windows[rd.w].container == kZeroContainer) {
+                std::memset(pin_in_[slot].get() + rd.at, 0, rd.b - rd.a);
+                continue;
+            }
+            if (uncached_) {
+                opened.push_back(std::make_unique<Fd>(window_files[rd.w], O_RDONLY));
+                if (opened.back()->fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + window_files[rd.w].string() + "'");
+                fd = opened.back()->fd;
+            } else {
+                fd = fds[rd.w]->fd;
+            }
+            jobs.push_back({fd, pin_in_[slot].get() + rd.at, rd.b - rd.a, file_off[rd.w] + rd.a});
+        }
+        {
+            ScopedAccum acc(read_ms);
+            run_reads(jobs, workers_, out_path.string());
+        }
+        cudaStream_t s = stream_[slot];
+        cuda_check(cudaMemcpyAsync(d_in_[slot].get(), pin_in_[slot].get(), c.staging, cudaMemcpyHostToDevice, s), "H2D");
+        auto* segs = reinterpret_cast<dev::GatherSeg*>(pin_segs_[slot].get());
+        for (std::size_t i = 0; i < c.segs.size(); ++i) {
+            segs[i] = c.segs[i];
+            segs[i].src = d_in_[slot].get() + reinterpret_cast<std::uintptr_t>(c.segs[i].src);
+        }
+        cuda_check(cudaMemcpyAsync(d_segs_[slot].get(), segs, c.segs.size() * sizeof(dev::GatherSeg), cudaMemcpyHostToDevice, s),
+                   "segs");
+        cuda_check(cudaEventRecord(ev0_[slot], s), "event");
+        cuda_check(dev::launch_gather(d_segs_[slot].get<dev::GatherSeg>(), static_cast<std::uint32_t>(c.segs.size()),
+                                      d_out_[slot].get(), c.hi - c.lo, dev::kGatherAuto, c.bulk_ok, s),
+                   "gather");
+        cuda_check(cudaEventRecord(ev1_[slot], s), "event");
+        cuda_check(cudaMemcpyAsync(pin_out_[slot].get(), d_out_[slot].get(), c.hi - c.lo, cudaMemcpyDeviceToHost, s), "D2H");
+        bytes += c.hi - c.lo;
+    }
+
     struct Read {
         std::uint32_t w;
         std::uint64_t a, b, at;
@@ -255,10 +304,10 @@ class FileAssembler {
     int workers_;
     bool uncached_;
     std::uint64_t chunk_;
-    cudaStream_t stream_[2]{};
-    cudaEvent_t ev0_[2]{}, ev1_[2]{};
-    PinnedBuffer pin_in_[2], pin_out_[2], pin_segs_[2]; // pinned: async uploads never sync the stream
-    DeviceBuffer d_in_[2], d_out_[2], d_segs_[2];
+    cudaStream_t stream_[kSlots]{};
+    cudaEvent_t ev0_[kSlots]{}, ev1_[kSlots]{};
+    PinnedBuffer pin_in_[kSlots], pin_out_[kSlots], pin_segs_[kSlots]; // pinned: async uploads never sync the stream
+    DeviceBuffer d_in_[kSlots], d_out_[kSlots], d_segs_[kSlots];
     std::map<std::string, std::uint64_t> payload_off_;
 };
 
@@ -282,7 +331,7 @@ AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool u
     });
     const int lanes = std::clamp<int>(std::min<int>(static_cast<int>(jobs.size()), workers), 1, 16);
     const int readers = std::max(1, workers / lanes);
-    const std::uint64_t chunk = lanes > 1 ? (32ull << 20) : (128ull << 20);
+    const std::uint64_t chunk = lanes >= 4 ? (16ull << 20) : lanes > 1 ? (32ull << 20) : (128ull << 20);
     std::vector<AssembleTotals> part(static_cast<std::size_t>(lanes));
     std::atomic<std::size_t> next{0};
     std::exception_ptr err;

@@ -2,6 +2,7 @@
 #include "tailor/trainer.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <fstream>
 #include <map>
@@ -97,6 +98,7 @@ DeviceTrainer::DeviceTrainer(const ModelSpec& spec, int num_ranks, const AdamHyp
                              int rank_end)
     : model_(spec), N_(num_ranks), base_(base) {
     base_.validate();
+    if (const char* v = std::getenv("TAILOR_TRAIN_STORE_GRAD")) store_grad_ = *v && *v != '0';
     if (num_ranks < 1) fail(ErrorKind::Recipe, "num_ranks must be >= 1");
     r0_ = rank_begin;
     r1_ = rank_end < 0 ? num_ranks : rank_end;
@@ -175,7 +177,7 @@ DeviceTrainer::DeviceTrainer(const ModelSpec& spec, int num_ranks, const AdamHyp
         rk->tiles.upload(tiles.data(), std::max<std::size_t>(1, tiles.size()) * sizeof(dev::TrainTile));
         rk->grid = dev::train_grid(rk->ntiles);
         rk->grad_part.resize(rk->grid * sizeof(double));
-        rk->grad.resize(std::max<std::uint64_t>(16, vbegin * sizeof(float)));
+        if (store_grad_) rk->grad.resize(std::max<std::uint64_t>(16, vbegin * sizeof(float)));
         rk->delta_part.resize(rk->grid * sizeof(double));
         // W_0 = 0.02 * u(seed, 0, e) (init_state, R/src/gradients.cpp:51-66): the
         // generator with k1 = 0 writes exactly the initial masters.
@@ -207,7 +209,8 @@ std::pair<double, double> DeviceTrainer::step(std::int64_t s) {
     cuda_check(cudaMemsetAsync(flag_.get(), 0, sizeof(unsigned int), stream_), "memset");
     for (auto& rk : ranks_)
         cuda_check(dev::launch_grad_check(rk->tiles.get<dev::TrainTile>(), rk->ntiles, rk->groups.get<dev::TrainGroup>(),
-                                          rk->part.get(), p, rk->grad.get<float>(), rk->grad_part.get<double>(),
+                                          rk->part.get(), p, store_grad_ ? rk->grad.get<float>() : nullptr,
+                                          rk->grad_part.get<double>(),
                                           flag_.get<unsigned int>(), stream_),
                    "grad check");
     unsigned int bad = 0;
@@ -233,8 +236,8 @@ std::pair<double, double> DeviceTrainer::step(std::int64_t s) {
                "coef");
     for (auto& rk : ranks_)
         cuda_check(dev::launch_adamw(rk->tiles.get<dev::TrainTile>(), rk->ntiles, rk->groups.get<dev::TrainGroup>(),
-                                     coef_.get<dev::AdamCoef>(), rk->part.get(), rk->grad.get<float>(),
-                                     rk->delta_part.get<double>(), stream_),
+                                     coef_.get<dev::AdamCoef>(), rk->part.get(),
+                                     store_grad_ ? rk->grad.get<float>() : nullptr, p, rk->delta_part.get<double>(), stream_),
                    "adamw");
     double g2 = 0.0, d2 = 0.0;
     std::vector<double> h;

@@ -62,6 +62,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // Tiles (host-built, TrainTile) replace per-element group/slice searches: inside a
 // tile the field index, the gradient index and the noise counter are all affine
 // in j, so each thread streams float4 runs with no lookups.
+template <bool kStore>
 __global__ void __launch_bounds__(kThreads) grad_check_kernel(const TrainTile* __restrict__ tiles, std::uint32_t ntiles,
                                                               const TrainGroup* __restrict__ groups,
                                                               const std::uint8_t* __restrict__ part, TrainParams p,
@@ -85,7 +86,7 @@ __global__ void __launch_bounds__(kThreads) grad_check_kernel(const TrainTile* _
                 gr.y = grad_of(x.y, p, e + 1);
                 gr.z = grad_of(x.z, p, e + 2);
                 gr.w = grad_of(x.w, p, e + 3);
-                reinterpret_cast<float4*>(gout)[q] = gr;
+                if constexpr (kStore) reinterpret_cast<float4*>(gout)[q] = gr;
                 bad = bad || !isfinite(gr.x) || !isfinite(gr.y) || !isfinite(gr.z) || !isfinite(gr.w);
                 acc = fma(static_cast<double>(gr.x), static_cast<double>(gr.x), acc);
                 acc = fma(static_cast<double>(gr.y), static_cast<double>(gr.y), acc);
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(kThreads) grad_check_kernel(const TrainTile* _
         } else {
             for (std::uint32_t j = threadIdx.x; j < tile.count; j += kThreads) {
                 const float gr = grad_of(w[j], p, tile.e0 + j);
-                gout[j] = gr;
+                if constexpr (kStore) gout[j] = gr;
                 bad = bad || !isfinite(gr);
                 acc = fma(static_cast<double>(gr), static_cast<double>(gr), acc);
             }
@@ -117,10 +118,14 @@ __device__ __forceinline__ float adam_one(const AdamCoef& c, float& w, float& m,
     return step;
 }
 
+// kRecompute: the gradient is recomputed from the pre-update master (the same
+// _rn expression as pass 1, so the same bits) instead of being read back from a
+// scratch buffer: 28 B per element for the step instead of 36.
+template <bool kRecompute>
 __global__ void __launch_bounds__(kThreads) adamw_update_kernel(const TrainTile* __restrict__ tiles, std::uint32_t ntiles,
                                                                 const TrainGroup* __restrict__ groups,
                                                                 const AdamCoef* __restrict__ coef, std::uint8_t* __restrict__ part,
-                                                                const float* __restrict__ grad,
+                                                                const float* __restrict__ grad, TrainParams p,
                                                                 double* __restrict__ delta_partials) {
     __shared__ double red[kThreads / 32];
     double acc = 0.0;
@@ -138,7 +143,13 @@ __global__ void __launch_bounds__(kThreads) adamw_update_kernel(const TrainTile*
                 float4 w = __ldcs(reinterpret_cast<const float4*>(wp) + q);
                 float4 m = __ldcs(reinterpret_cast<const float4*>(mp) + q);
                 float4 v = __ldcs(reinterpret_cast<const float4*>(vp) + q);
-                const float4 gr = __ldcs(reinterpret_cast<const float4*>(gp) + q);
+                float4 gr;
+                if constexpr (kRecompute) {
+                    const std::uint64_t e = tile.e0 + 4ull * q;
+                    gr = make_float4(grad_of(w.x, p, e), grad_of(w.y, p, e + 1), grad_of(w.z, p, e + 2), grad_of(w.w, p, e + 3));
+                } else {
+                    gr = __ldcs(reinterpret_cast<const float4*>(gp) + q);
+                }
                 const float s0 = adam_one(c, w.x, m.x, v.x, gr.x);
                 const float s1 = adam_one(c, w.y, m.y, v.y, gr.y);
                 const float s2 = adam_one(c, w.z, m.z, v.z, gr.z);
@@ -154,7 +165,8 @@ __global__ void __launch_bounds__(kThreads) adamw_update_kernel(const TrainTile*
         } else {
             for (std::uint32_t j = threadIdx.x; j < tile.count; j += kThreads) {
                 float w = wp[j], m = mp[j], v = vp[j];
-                const float st = adam_one(c, w, m, v, gp[j]);
+                const float gr = kRecompute ? grad_of(w, p, tile.e0 + j) : gp[j];
+                const float st = adam_one(c, w, m, v, gr);
                 mp[j] = m;
                 vp[j] = v;
                 wp[j] = w;
@@ -227,15 +239,24 @@ unsigned train_grid(std::uint32_t ntiles) {
 cudaError_t launch_grad_check(const TrainTile* d_tiles, std::uint32_t ntiles, const TrainGroup* d_groups,
                               const std::uint8_t* d_part, const TrainParams& p, float* d_grad, double* d_grad_partials,
                               unsigned int* d_nonfinite, cudaStream_t s) {
-    grad_check_kernel<<<train_grid(ntiles), kThreads, 0, s>>>(d_tiles, ntiles, d_groups, d_part, p, d_grad, d_grad_partials,
-                                                             d_nonfinite);
+    if (d_grad)
+        grad_check_kernel<true><<<train_grid(ntiles), kThreads, 0, s>>>(d_tiles, ntiles, d_groups, d_part, p, d_grad,
+                                                                       d_grad_partials, d_nonfinite);
+    else
+        grad_check_kernel<false><<<train_grid(ntiles), kThreads, 0, s>>>(d_tiles, ntiles, d_groups, d_part, p, nullptr,
+                                                                        d_grad_partials, d_nonfinite);
     return cudaGetLastError();
 }
 
 cudaError_t launch_adamw(const TrainTile* d_tiles, std::uint32_t ntiles, const TrainGroup* d_groups, const AdamCoef* d_coef,
-                         std::uint8_t* d_part, const float* d_grad, double* d_delta_partials, cudaStream_t s) {
-    adamw_update_kernel<<<train_grid(ntiles), kThreads, 0, s>>>(d_tiles, ntiles, d_groups, d_coef, d_part, d_grad,
-                                                               d_delta_partials);
+                         std::uint8_t* d_part, const float* d_grad, const TrainParams& p, double* d_delta_partials,
+                         cudaStream_t s) {
+    if (d_grad)
+        adamw_update_kernel<false><<<train_grid(ntiles), kThreads, 0, s>>>(d_tiles, ntiles, d_groups, d_coef, d_part, d_grad, p,
+                                                                          d_delta_partials);
+    else
+        adamw_update_kernel<true><<<train_grid(ntiles), kThreads, 0, s>>>(d_tiles, ntiles, d_groups, d_coef, d_part, nullptr, p,
+                                                                         d_delta_partials);
     return cudaGetLastError();
 }
 

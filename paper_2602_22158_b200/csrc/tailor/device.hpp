@@ -166,13 +166,15 @@ struct TrainTile {
     std::uint16_t vec;   // 1: i0 and count are multiples of 4 and the fields 16-B aligned
 };
 constexpr std::uint32_t kTrainTileElems = 16384;
-// Pass 1: gradients -> d_grad (one float per virtual element), FP64 sum g^2 per
-// block, non-finite flag. Pass 2 (only if no flag): AdamW from d_grad.
+// Pass 1: gradients (stored to d_grad, one float per virtual element, unless
+// d_grad is null), FP64 sum g^2 per block, non-finite flag. Pass 2 (only if no
+// flag): AdamW, reading d_grad or (null) recomputing the gradient from p.
 cudaError_t launch_grad_check(const TrainTile* d_tiles, std::uint32_t ntiles, const TrainGroup* d_groups,
                               const std::uint8_t* d_part, const TrainParams& p, float* d_grad, double* d_grad_partials,
                               unsigned int* d_nonfinite, cudaStream_t s);
 cudaError_t launch_adamw(const TrainTile* d_tiles, std::uint32_t ntiles, const TrainGroup* d_groups, const AdamCoef* d_coef,
-                         std::uint8_t* d_part, const float* d_grad, double* d_delta_partials, cudaStream_t s);
+                         std::uint8_t* d_part, const float* d_grad, const TrainParams& p, double* d_delta_partials,
+                         cudaStream_t s);
 // blocks of the two passes (one FP64 partial each)
 unsigned train_grid(std::uint32_t ntiles);
 unsigned adamw_grid(std::uint64_t total);

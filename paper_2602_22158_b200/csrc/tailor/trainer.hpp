@@ -67,6 +67,9 @@ class DeviceTrainer {
     DeviceBuffer coef_, part_ptrs_, flag_;
     std::int64_t t_ = 0;
     cudaStream_t stream_ = nullptr;
+    // Pass 2 recomputes the gradient (28 B/element) unless TAILOR_TRAIN_STORE_GRAD=1
+    // selects the scratch-buffer variant (36 B/element; kept for comparison).
+    bool store_grad_ = false;
 };
 
 // The reference's train() (R/src/trainer.cpp:109-123) on the device: same run

@@ -8,6 +8,7 @@ Bar: bit-exact bytes for every payload, header and sidecar; scores within
 """
 import json
 import os
+import pathlib
 import random
 
 import numpy as np
@@ -556,3 +557,76 @@ def test_scorer_variants_agree(K):
         torch.cuda.synchronize()
         for o_ in outs[1:]:
             assert torch.allclose(outs[0], o_, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("N", [1, 2, 4, 8])
+def test_execute_merge_lane_count_independent_and_sources_untouched(tmp_path, N):
+    """Acceptance c9/c10 + R/tests/test_merge.cpp:370-385 shape: the composite does not
+    depend on the host worker (lane) count, equals the reference's, and the source files
+    are byte-for-byte untouched."""
+    need_gpu()
+    import hashlib
+
+    spec = t.ModelSpec(5, 16, 40, 64, False, 6060 + N)
+    d = _gen_ref(tmp_path, spec, N, 3)
+
+    def digest():
+        return {str(p): hashlib.sha256(p.read_bytes()).hexdigest() for k in d for p in sorted(pathlib.Path(k).rglob("*"))
+                if p.is_file()}
+
+    before = digest()
+    recipe = t.MergeRecipe(num_ranks=N, base_checkpoint=d[2],
+                           slices=[t.RecipeSlice(d[0], [0, 3]), t.RecipeSlice(d[1], [1, 4], [2, 1])],
+                           aux={"embed_tokens": d[0], "lm_head": d[1]})
+    _both_merge(tmp_path, recipe, name="w1", workers=1)
+    for w in (3, 16):
+        t.execute_merge(recipe, str(tmp_path / f"w{w}"), t.MergeOptions(workers=w))
+        _assert_same_tree(tmp_path / "w1_ours", tmp_path / f"w{w}")
+    assert digest() == before
+    # identity round trip at this rank count (c9): merged base == source base
+    t.execute_merge(t.MergeRecipe(num_ranks=N, base_checkpoint=d[1]), str(tmp_path / "ident"))
+    for r in range(N):
+        rel = f"optim/rank_{r}.shard"
+        assert (tmp_path / "ident" / rel).read_bytes() == (pathlib.Path(d[1]) / rel).read_bytes()
+
+
+@pytest.mark.parametrize("damage", ["padding", "negative_v", "weight_bit"])
+def test_verify_lanes_report_the_damaged_rank(tmp_path, damage):
+    """Device re-verify runs the rank files over parallel lanes; a defect in one rank
+    file of eight is still found with the reference's error kind."""
+    need_gpu()
+    import shutil
+    import struct
+
+    spec = t.ModelSpec(3, 4, 16, 31, False, 99)  # h=4 norm over 8 ranks: ranks 4-7 hold only padding
+    d = _gen_ref(tmp_path, spec, 8, 1)
+    t.verify_checkpoint(d[0])
+    bad = tmp_path / "bad"
+    shutil.copytree(d[0], bad)
+    r = 5
+    if damage == "weight_bit":
+        w = bytearray((bad / "model.weights").read_bytes())
+        w[-3] ^= 0x40
+        (bad / "model.weights").write_bytes(bytes(w))
+        kind, ref_name = t.ErrorKind.Consistency, "ConsistencyError"
+    else:
+        p = bad / "optim" / f"rank_{r}.shard" if damage == "negative_v" else bad / "optim" / "rank_7.shard"
+        b = bytearray(p.read_bytes())
+        hlen = int.from_bytes(b[:8], "little")
+        hdr = json.loads(b[8:8 + hlen])
+        base = 8 + hlen
+        g = spec.num_layers + 1  # embed group: 124 elements, chunk 16, rank 5 fully valid
+        if damage == "padding":
+            lo, hi = hdr["g0.master"]["data_offsets"]  # norm group: rank 7's one element is padding
+            b[base + hi - 4:base + hi] = struct.pack("<f", 1.0)
+            kind, ref_name = t.ErrorKind.CorruptContainer, "CorruptContainer"
+        else:
+            lo, hi = hdr[f"g{g}.exp_avg_sq"]["data_offsets"]
+            b[base + lo:base + lo + 4] = struct.pack("<f", -1.0)
+            kind, ref_name = t.ErrorKind.Consistency, "ConsistencyError"
+        p.write_bytes(bytes(b))
+    with pytest.raises(t.TailorError) as e:
+        t.verify_checkpoint(str(bad))
+    assert e.value.kind == kind
+    rc, _, err = ref_tool("read", "--dir", bad, check=False)
+    assert rc != 0 and ref_name in err
