@@ -9,6 +9,7 @@
 #include <exception>
 #include <mutex>
 #include <thread>
+#include <cstdio>
 #include <cstring>
 #include <filesystem>
 #include <fcntl.h>
@@ -140,7 +141,7 @@ CheckpointSummary family_summary(const SynthFamily& f, const std::string& id) {
 // (Buffers are reused across calls: a lane loads one rank after another.)
 void load_packed_masters(const std::vector<std::string>& dirs, int rank, const ModelLayout& model, int num_ranks,
                          std::vector<DeviceBuffer>& out, std::vector<std::vector<std::uint64_t>>& offs,
-                         PinnedBuffer& stage, int threads) {
+                         PinnedBuffer& stage, int threads, double* phase_ms = nullptr) {
     const auto fields = score_fields(model, num_ranks);
     out.resize(dirs.size());
     offs.assign(dirs.size(), {});
@@ -159,6 +160,7 @@ void load_packed_masters(const std::vector<std::string>& dirs, int rank, const M
             total = (total + e->bytes() + 15) & ~15ull;
         }
         stage.resize(std::max<std::uint64_t>(16, total));
+        const double t0 = clock_ms();
         const int fd = ::open(p.c_str(), O_RDONLY);
         if (fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + p.string() + "'");
         std::vector<ReadJob> jobs;
@@ -170,8 +172,15 @@ void load_packed_masters(const std::vector<std::string>& dirs, int rank, const M
             throw;
         }
         ::close(fd);
+        const double t1 = clock_ms();
         out[k].resize(std::max<std::uint64_t>(16, total));
+        const double t2 = clock_ms();
         cuda_check(cudaMemcpy(out[k].get(), stage.get(), total, cudaMemcpyHostToDevice), "H2D");
+        if (phase_ms) {
+            phase_ms[0] += t1 - t0;
+            phase_ms[1] += t2 - t1;
+            phase_ms[2] += clock_ms() - t2;
+        }
     }
 }
 
@@ -227,7 +236,10 @@ void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<st
                 }
                 std::vector<std::vector<std::uint64_t>> offs;
                 PhaseTimer pt("score.rank");
-                load_packed_masters(dirs, r, model, N, bufs, offs, stage, readers);
+                double ph[3] = {0, 0, 0};
+                const double t0 = clock_ms();
+                load_packed_masters(dirs, r, model, N, bufs, offs, stage, readers, ph);
+                const double t1 = clock_ms();
                 ScorePlan plan(model, N, offs);
                 std::vector<const std::uint8_t*> bases;
                 for (auto& b : bufs) bases.push_back(b.get());
@@ -236,6 +248,9 @@ void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<st
                                            cudaMemcpyDeviceToHost, st),
                            "D2H");
                 cuda_check(cudaStreamSynchronize(st), "sync");
+                if (trace_enabled())
+                    std::fprintf(stderr, "[tailor] score.rank %d: load %.1f (read %.1f alloc %.1f h2d %.1f) plan+run %.1f ms\n", r,
+                                 t1 - t0, ph[0], ph[1], ph[2], clock_ms() - t1);
             }
         } catch (...) {
             std::lock_guard<std::mutex> lk(mu);

@@ -25,17 +25,89 @@ void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(ErrorKind::Device, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// cudaMalloc of a large block can take 10-350 ms on a busy process (measured in
+// the file scorer lanes: tools/files_trace.py), so released device blocks up to
+// 2 GB are kept per device in size classes (cap 8 GB per device) and reused.
+// Release keeps cudaFree's implicit device synchronisation, so a block is never
+// handed out while a kernel launched before the release may still use it.
+namespace {
+std::size_t pool_size_class(std::size_t n) {
+    std::size_t base = 2u << 20;
+    while (base * 2 <= n) base <<= 1;
+    for (std::size_t q = 4; q <= 8; ++q)
+        if (base / 4 * q >= n) return base / 4 * q;
+    return base * 2;
+}
+
+struct DevicePool {
+    static constexpr std::size_t kCap = 8ull << 30, kMaxBlock = 2ull << 30;
+    std::mutex mu;
+    std::map<int, std::multimap<std::size_t, void*>> free_; // device -> size class -> block
+    std::map<int, std::size_t> pooled;
+
+    void* take(int dev, std::size_t n, std::size_t* got) {
+        const std::size_t sz = n <= kMaxBlock ? pool_size_class(n) : n;
+        if (sz <= kMaxBlock) {
+            std::lock_guard<std::mutex> lk(mu);
+            auto& f = free_[dev];
+            auto it = f.find(sz);
+            if (it != f.end()) {
+                void* p = it->second;
+                pooled[dev] -= sz;
+                f.erase(it);
+                *got = sz;
+                return p;
+            }
+        }
+        void* p = nullptr;
+        cuda_check(cudaMalloc(&p, sz), "cudaMalloc");
+        *got = sz;
+        return p;
+    }
+    void give(int dev, void* p, std::size_t sz) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cur != dev) cudaSetDevice(dev);
+        if (sz > kMaxBlock) {
+            cudaFree(p);
+        } else {
+            cudaDeviceSynchronize();
+            std::lock_guard<std::mutex> lk(mu);
+            free_[dev].emplace(sz, p);
+            pooled[dev] += sz;
+            auto& f = free_[dev];
+            while (pooled[dev] > kCap && !f.empty()) {
+                auto it = std::prev(f.end());
+                pooled[dev] -= it->first;
+                cudaFree(it->second);
+                f.erase(it);
+            }
+        }
+        if (cur != dev) cudaSetDevice(cur);
+    }
+};
+DevicePool& device_pool() {
+    static DevicePool* pool = new DevicePool(); // intentionally leaked: lives for the process
+    return *pool;
+}
+} // namespace
+
 DeviceBuffer::~DeviceBuffer() {
-    if (p_) cudaFree(p_);
+    if (p_) device_pool().give(dev_, p_, cap_);
 }
 
 void DeviceBuffer::resize(std::size_t n) {
     if (n <= n_ && p_) return;
-    if (p_) cudaFree(p_);
+    if (p_ && n <= cap_) {
+        n_ = n;
+        return;
+    }
+    if (p_) device_pool().give(dev_, p_, cap_);
     p_ = nullptr;
-    n_ = 0;
+    n_ = cap_ = 0;
     if (n == 0) return;
-    cuda_check(cudaMalloc(&p_, n), "cudaMalloc");
+    cuda_check(cudaGetDevice(&dev_), "cudaGetDevice");
+    p_ = device_pool().take(dev_, n, &cap_);
     n_ = n;
 }
 

@@ -39,6 +39,9 @@ PhaseTimer::~PhaseTimer() {
 ScopedAccum::ScopedAccum(double& sink) : sink_(sink), t0_(now_ms()) {}
 ScopedAccum::~ScopedAccum() { sink_ += now_ms() - t0_; }
 
+bool trace_enabled() { return trace_on(); }
+double clock_ms() { return now_ms(); }
+
 void trace_value(const char* name, double ms) {
     if (trace_on()) std::fprintf(stderr, "[tailor] %s %.2f ms\n", name, ms);
 }

@@ -29,7 +29,10 @@ class DeviceBuffer {
     ~DeviceBuffer();
     DeviceBuffer(const DeviceBuffer&) = delete;
     DeviceBuffer& operator=(const DeviceBuffer&) = delete;
-    DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+    DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_), cap_(o.cap_), dev_(o.dev_) {
+        o.p_ = nullptr;
+        o.n_ = o.cap_ = 0;
+    }
     void resize(std::size_t n); // discards contents
     template <typename T = std::uint8_t>
     T* get() const { return static_cast<T*>(p_); }
@@ -38,7 +41,9 @@ class DeviceBuffer {
 
   private:
     void* p_ = nullptr;
-    std::size_t n_ = 0;
+    std::size_t n_ = 0;   // bytes requested (largest so far)
+    std::size_t cap_ = 0; // bytes allocated (pool size class)
+    int dev_ = 0;
 };
 
 class PinnedBuffer {

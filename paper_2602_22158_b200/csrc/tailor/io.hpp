@@ -52,5 +52,8 @@ class ScopedAccum {
 };
 // Prints "[tailor] <name> <ms>" when TAILOR_TRACE=1.
 void trace_value(const char* name, double ms);
+bool trace_enabled();
+// Monotonic clock in ms (for phase breakdowns).
+double clock_ms();
 
 } // namespace tailor

@@ -21,7 +21,13 @@ try:
     dirs = [str(work / f"checkpoint-{k * 100}") for k in range(1, 5)]
     for k in range(1, 5):
         fam.write_dir(k, dirs[k - 1])
+    def dirty():
+        with open("/proc/meminfo") as f:
+            kv = dict(line.split(":", 1) for line in f)
+        return {k: kv[k].strip() for k in ("Dirty", "Writeback")}
+
     for i in range(iters):
+        print(f"iter {i} start: {dirty()}", file=sys.stderr, flush=True)
         t0 = time.perf_counter()
         rec, _, _ = t.select_recipe(dirs, 0.5)
         t1 = time.perf_counter()
