@@ -137,14 +137,21 @@ CheckpointSummary family_summary(const SynthFamily& f, const std::string& id) {
     return f.summary(k, id);
 }
 
-// Reads each snapshot's rank-r master fields into one packed device buffer.
-// (Buffers are reused across calls: a lane loads one rank after another.)
+// Reads each snapshot's rank-r master fields into one packed device buffer,
+// streamed through two 16 MB pinned halves (pread of one half overlaps the H2D
+// of the other on the lane's stream). Buffers are reused across calls: a lane
+// loads one rank after another.
 void load_packed_masters(const std::vector<std::string>& dirs, int rank, const ModelLayout& model, int num_ranks,
                          std::vector<DeviceBuffer>& out, std::vector<std::vector<std::uint64_t>>& offs,
-                         PinnedBuffer& stage, int threads, double* phase_ms = nullptr) {
+                         PinnedBuffer& stage, int threads, cudaStream_t st, cudaEvent_t* half_done,
+                         double* phase_ms = nullptr) {
+    constexpr std::uint64_t kHalf = 16ull << 20;
     const auto fields = score_fields(model, num_ranks);
     out.resize(dirs.size());
     offs.assign(dirs.size(), {});
+    stage.resize(2 * kHalf);
+    bool used[2] = {false, false};
+    int half = 0;
     for (std::size_t k = 0; k < dirs.size(); ++k) {
         const fs::path p = ckpt_file(CkptFile::Shard, dirs[k], rank);
         const ContainerLayout lay = read_layout(p);
@@ -159,25 +166,38 @@ void load_packed_masters(const std::vector<std::string>& dirs, int rank, const M
             offs[k].push_back(total);
             total = (total + e->bytes() + 15) & ~15ull;
         }
-        stage.resize(std::max<std::uint64_t>(16, total));
-        const double t0 = clock_ms();
+        const double t1 = clock_ms();
+        out[k].resize(std::max<std::uint64_t>(16, total));
+        const double t2 = clock_ms();
         const int fd = ::open(p.c_str(), O_RDONLY);
         if (fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + p.string() + "'");
-        std::vector<ReadJob> jobs;
-        for (const auto& [e, at] : where) jobs.push_back({fd, stage.get() + at, e->bytes(), lay.payload_offset() + e->begin});
         try {
-            run_reads(jobs, threads, p.string());
+            std::size_t fi = 0;
+            for (std::uint64_t lo = 0; lo < total; lo += kHalf, half ^= 1) {
+                const std::uint64_t hi = std::min(total, lo + kHalf);
+                std::uint8_t* buf = stage.get() + static_cast<std::uint64_t>(half) * kHalf;
+                if (used[half]) cuda_check(cudaEventSynchronize(half_done[half]), "event");
+                std::vector<ReadJob> jobs;
+                while (fi < where.size() && where[fi].second + where[fi].first->bytes() <= lo) ++fi;
+                for (std::size_t j = fi; j < where.size() && where[j].second < hi; ++j) {
+                    const auto& [e, at] = where[j];
+                    const std::uint64_t a = std::max(lo, at), z = std::min(hi, at + e->bytes());
+                    if (a < z) jobs.push_back({fd, buf + (a - lo), z - a, lay.payload_offset() + e->begin + (a - at)});
+                }
+                const double r0 = clock_ms();
+                run_reads(jobs, threads, p.string());
+                if (phase_ms) phase_ms[0] += clock_ms() - r0;
+                cuda_check(cudaMemcpyAsync(out[k].get() + lo, buf, hi - lo, cudaMemcpyHostToDevice, st), "H2D");
+                cuda_check(cudaEventRecord(half_done[half], st), "event");
+                used[half] = true;
+            }
         } catch (...) {
+            cudaStreamSynchronize(st);
             ::close(fd);
             throw;
         }
         ::close(fd);
-        const double t1 = clock_ms();
-        out[k].resize(std::max<std::uint64_t>(16, total));
-        const double t2 = clock_ms();
-        cuda_check(cudaMemcpy(out[k].get(), stage.get(), total, cudaMemcpyHostToDevice), "H2D");
         if (phase_ms) {
-            phase_ms[0] += t1 - t0;
             phase_ms[1] += t2 - t1;
             phase_ms[2] += clock_ms() - t2;
         }
@@ -229,6 +249,10 @@ void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<st
             DeviceBuffer dout(nres * sizeof(double));
             std::vector<DeviceBuffer> bufs;
             PinnedBuffer stage;
+            cudaEvent_t half_done[2];
+            for (auto& e : half_done) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+            std::unique_ptr<CUevent_st, decltype(&cudaEventDestroy)> own0(half_done[0], &cudaEventDestroy),
+                own1(half_done[1], &cudaEventDestroy);
             for (int r = next.fetch_add(1); r < N; r = next.fetch_add(1)) {
                 {
                     std::lock_guard<std::mutex> lk(mu);
@@ -238,7 +262,7 @@ void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<st
                 PhaseTimer pt("score.rank");
                 double ph[3] = {0, 0, 0};
                 const double t0 = clock_ms();
-                load_packed_masters(dirs, r, model, N, bufs, offs, stage, readers, ph);
+                load_packed_masters(dirs, r, model, N, bufs, offs, stage, readers, st, half_done, ph);
                 const double t1 = clock_ms();
                 ScorePlan plan(model, N, offs);
                 std::vector<const std::uint8_t*> bases;
@@ -249,7 +273,7 @@ void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<st
                            "D2H");
                 cuda_check(cudaStreamSynchronize(st), "sync");
                 if (trace_enabled())
-                    std::fprintf(stderr, "[tailor] score.rank %d: load %.1f (read %.1f alloc %.1f h2d %.1f) plan+run %.1f ms\n", r,
+                    std::fprintf(stderr, "[tailor] score.rank %d: load %.1f (read %.1f alloc %.1f read+h2d %.1f) plan+run %.1f ms\n", r,
                                  t1 - t0, ph[0], ph[1], ph[2], clock_ms() - t1);
             }
         } catch (...) {

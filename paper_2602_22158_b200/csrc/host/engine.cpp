@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <fcntl.h>
 #include <filesystem>
@@ -23,6 +24,25 @@ namespace fs = std::filesystem;
 
 void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(ErrorKind::Device, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+AllocStats& alloc_stats() {
+    static AllocStats* s = new AllocStats();
+    return *s;
+}
+
+void AllocStats::note(bool pinned, std::size_t bytes, double ms) {
+    std::lock_guard<std::mutex> lk(mu);
+    (pinned ? pinned_bytes : device_bytes) += bytes;
+    (pinned ? pinned_ms : device_ms) += ms;
+    (pinned ? pinned_count : device_count) += 1;
+}
+
+void AllocStats::trace(const char* where) {
+    if (!trace_enabled()) return;
+    std::lock_guard<std::mutex> lk(mu);
+    std::fprintf(stderr, "[tailor] %s: new pinned %zu blocks %.1f MB in %.1f ms (thread-sum), new device %zu blocks %.1f MB in %.1f ms\n",
+                 where, pinned_count, pinned_bytes / 1048576.0, pinned_ms, device_count, device_bytes / 1048576.0, device_ms);
 }
 
 // cudaMalloc of a large block can take 10-350 ms on a busy process (measured in
@@ -60,7 +80,9 @@ struct DevicePool {
             }
         }
         void* p = nullptr;
+        const double t0 = clock_ms();
         cuda_check(cudaMalloc(&p, sz), "cudaMalloc");
+        alloc_stats().note(false, sz, clock_ms() - t0);
         *got = sz;
         return p;
     }
@@ -154,7 +176,9 @@ struct PinnedPool {
             }
         }
         void* p = nullptr;
+        const double t0 = clock_ms();
         cuda_check(cudaMallocHost(&p, sz), "cudaMallocHost");
+        alloc_stats().note(true, sz, clock_ms() - t0);
         *got = sz;
         return p;
     }
@@ -875,14 +899,15 @@ struct StreamHandle {
     StreamHandle& operator=(const StreamHandle&) = delete;
 };
 
-void load_payload(const fs::path& path, const ContainerLayout& lay, DeviceBuffer& dst, PinnedBuffer& stage,
+void load_payload(const fs::path& path, const ContainerLayout& lay, DeviceBuffer& dst, PinnedBuffer* stage /* [2] */,
                   int threads = io_threads(), std::uint64_t step = 512ull << 20) {
     dst.resize(std::max<std::uint64_t>(16, lay.payload_bytes));
     const int fd = ::open(path.c_str(), O_RDONLY);
     if (fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + path.string() + "'");
     // `step`-byte windows read by the I/O pool, alternating two halves of the
     // pinned stage so the H2D of one overlaps the reads of the next.
-    stage.resize(2 * step);
+    stage[0].resize(step);
+    stage[1].resize(step);
     cudaStream_t s = nullptr;
     cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
     cudaEvent_t done[2];
@@ -893,7 +918,7 @@ void load_payload(const fs::path& path, const ContainerLayout& lay, DeviceBuffer
         int half = 0;
         for (std::uint64_t off = 0; off < lay.payload_bytes; off += step, half ^= 1) {
             const std::uint64_t n = std::min(step, lay.payload_bytes - off);
-            std::uint8_t* buf = stage.get() + static_cast<std::uint64_t>(half) * step;
+            std::uint8_t* buf = stage[half].get();
             if (used[half]) cuda_check(cudaEventSynchronize(done[half]), "event");
             run_reads({{fd, buf, n, lay.payload_offset() + off}}, threads, path.string());
             cuda_check(cudaMemcpyAsync(dst.get() + off, buf, n, cudaMemcpyHostToDevice, s), "H2D");
@@ -1000,10 +1025,10 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
     const std::uint64_t budget = free_b > wl.payload_bytes + (2ull << 30) ? (free_b - wl.payload_bytes - (2ull << 30)) / 2 : 0;
     const int lanes = std::clamp<int>(static_cast<int>(std::min<std::uint64_t>(budget / max_shard, 8)), 1, std::max(1, std::min(N, 8)));
     const int readers = std::max(1, io_threads() / lanes);
-    const std::uint64_t step = lanes > 1 ? (64ull << 20) : (512ull << 20);
+    const std::uint64_t step = lanes > 1 ? (16ull << 20) : (256ull << 20);
     {
         PhaseTimer pt("verify.load_weights");
-        PinnedBuffer stage;
+        PinnedBuffer stage[2];
         load_payload(ckpt_file(CkptFile::Weights, dir), wl, dw, stage, io_threads(), step);
     }
     std::atomic<int> next{0};
@@ -1013,7 +1038,7 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
         try {
             cuda_check(cudaSetDevice(device), "cudaSetDevice");
             DeviceBuffer ds, dpairs, dranges;
-            PinnedBuffer stage;
+            PinnedBuffer stage[2];
             StreamHandle ls;
             for (int r = next.fetch_add(1); r < N; r = next.fetch_add(1)) {
                 {

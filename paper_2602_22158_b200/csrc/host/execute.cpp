@@ -99,8 +99,9 @@ class FileAssembler {
         }
         HostMergeChunks plan(pp, chunk_);
         for (int i = 0; i < kSlots; ++i) {
-            pin_in_[i].resize(std::max<std::uint64_t>(16, plan.max_staging));
-            pin_out_[i].resize(std::max<std::uint64_t>(16, plan.max_out));
+            // one pinned buffer per slot carries the chunk both ways: the D2H of the
+            // gathered chunk lands in it after its H2D has completed (same stream)
+            pin_io_[i].resize(std::max<std::uint64_t>(16, std::max(plan.max_staging, plan.max_out)));
             d_in_[i].resize(std::max<std::uint64_t>(16, plan.max_staging));
             d_out_[i].resize(std::max<std::uint64_t>(16, plan.max_out));
             d_segs_[i].resize(std::max<std::size_t>(1, plan.max_segs) * sizeof(dev::GatherSeg));
@@ -132,7 +133,7 @@ class FileAssembler {
                     const auto& c = plan.chunks[ci];
                     {
                         ScopedAccum acc(write_ms);
-                        pwrite_all(out.fd, pin_out_[slot].get(), c.hi - c.lo, base + c.lo, out_path.string());
+                        pwrite_all(out.fd, pin_io_[slot].get(), c.hi - c.lo, base + c.lo, out_path.string());
                     }
                     std::lock_guard<std::mutex> lk(mu);
                     written = ci + 1;
@@ -187,7 +188,7 @@ class FileAssembler {
         for (const auto& rd : c.reads) {
             int fd;
             if (pp.windows[rd.w].container == kZeroContainer) {
-                std::memset(pin_in_[slot].get() + rd.at, 0, rd.b - rd.a);
+                std::memset(pin_io_[slot].get() + rd.at, 0, rd.b - rd.a);
                 continue;
             }
             if (uncached_) {
@@ -197,14 +198,14 @@ class FileAssembler {
             } else {
                 fd = fds[rd.w]->fd;
             }
-            jobs.push_back({fd, pin_in_[slot].get() + rd.at, rd.b - rd.a, file_off[rd.w] + rd.a});
+            jobs.push_back({fd, pin_io_[slot].get() + rd.at, rd.b - rd.a, file_off[rd.w] + rd.a});
         }
         {
             ScopedAccum acc(read_ms);
             run_reads(jobs, workers_, out_path.string());
         }
         cudaStream_t s = stream_[slot];
-        cuda_check(cudaMemcpyAsync(d_in_[slot].get(), pin_in_[slot].get(), c.staging, cudaMemcpyHostToDevice, s), "H2D");
+        cuda_check(cudaMemcpyAsync(d_in_[slot].get(), pin_io_[slot].get(), c.staging, cudaMemcpyHostToDevice, s), "H2D");
         auto* segs = reinterpret_cast<dev::GatherSeg*>(pin_segs_[slot].get());
         for (std::size_t i = 0; i < c.segs.size(); ++i) {
             segs[i] = c.segs[i];
@@ -217,7 +218,7 @@ class FileAssembler {
                                       d_out_[slot].get(), c.hi - c.lo, dev::kGatherAuto, c.bulk_ok, s),
                    "gather");
         cuda_check(cudaEventRecord(ev1_[slot], s), "event");
-        cuda_check(cudaMemcpyAsync(pin_out_[slot].get(), d_out_[slot].get(), c.hi - c.lo, cudaMemcpyDeviceToHost, s), "D2H");
+        cuda_check(cudaMemcpyAsync(pin_io_[slot].get(), d_out_[slot].get(), c.hi - c.lo, cudaMemcpyDeviceToHost, s), "D2H");
         bytes += c.hi - c.lo;
     }
 
@@ -306,7 +307,7 @@ class FileAssembler {
     std::uint64_t chunk_;
     cudaStream_t stream_[kSlots]{};
     cudaEvent_t ev0_[kSlots]{}, ev1_[kSlots]{};
-    PinnedBuffer pin_in_[kSlots], pin_out_[kSlots], pin_segs_[kSlots]; // pinned: async uploads never sync the stream
+    PinnedBuffer pin_io_[kSlots], pin_segs_[kSlots]; // pinned: async copies never sync the stream
     DeviceBuffer d_in_[kSlots], d_out_[kSlots], d_segs_[kSlots];
     std::map<std::string, std::uint64_t> payload_off_;
 };
@@ -331,7 +332,10 @@ AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool u
     });
     const int lanes = std::clamp<int>(std::min<int>(static_cast<int>(jobs.size()), workers), 1, 16);
     const int readers = std::max(1, workers / lanes);
-    const std::uint64_t chunk = lanes >= 4 ? (16ull << 20) : lanes > 1 ? (32ull << 20) : (128ull << 20);
+    // Chunks a little under a pool size class (16 / 32 / 128 MB), so a slot's
+    // staging (chunk + <= 31 B of alignment per read) stays in that class and the
+    // verify stages (16 MB halves) reuse the same pinned blocks.
+    const std::uint64_t chunk = lanes >= 4 ? (15ull << 20) : lanes > 1 ? (31ull << 20) : (127ull << 20);
     std::vector<AssembleTotals> part(static_cast<std::size_t>(lanes));
     std::atomic<std::size_t> next{0};
     std::exception_ptr err;
@@ -384,7 +388,11 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
     std::error_code ec;
     if (fs::exists(out_dir) && !fs::is_empty(out_dir, ec))
         fail(ErrorKind::Storage, "refusing to write into non-empty directory '" + out_dir.string() + "'");
-    cuda_check(cudaSetDevice(options.device), "cudaSetDevice");
+    {
+        PhaseTimer pt("merge.cuda_init");
+        cuda_check(cudaSetDevice(options.device), "cudaSetDevice");
+        cuda_check(cudaFree(nullptr), "cuda init");
+    }
 
     auto phase = std::make_unique<PhaseTimer>("merge.headers+plan");
     std::map<std::string, CheckpointSummary> sums;
@@ -441,9 +449,11 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
     write_text_file(ckpt_file(CkptFile::TrainerState, out_dir), read_text_file(ckpt_file(CkptFile::TrainerState, plan.config_source)));
     write_text_file(ckpt_file(CkptFile::Manifest, out_dir), sidecar_text(manifest));
 
+    alloc_stats().trace("merge.assemble allocations");
     phase = std::make_unique<PhaseTimer>("merge.verify");
     if (options.verify) verify_checkpoint_dir(out_dir.string(), options.device);
     phase.reset();
+    alloc_stats().trace("merge.verify allocations (cumulative)");
 
     stats.device_ms = fa.device_ms;
     stats.bytes_moved = fa.bytes;

@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
 #include <map>
 #include <memory>
 #include <string>
@@ -45,6 +46,16 @@ class DeviceBuffer {
     std::size_t cap_ = 0; // bytes allocated (pool size class)
     int dev_ = 0;
 };
+
+// Counters of fresh (non-pooled) allocations, printed by TAILOR_TRACE=1.
+struct AllocStats {
+    std::mutex mu;
+    std::size_t pinned_count = 0, device_count = 0, pinned_bytes = 0, device_bytes = 0;
+    double pinned_ms = 0.0, device_ms = 0.0;
+    void note(bool pinned, std::size_t bytes, double ms);
+    void trace(const char* where);
+};
+AllocStats& alloc_stats();
 
 class PinnedBuffer {
   public:
