@@ -144,6 +144,9 @@ tg_trainer* tg_trainer_create(const tg_model_spec* spec, int32_t num_ranks, int3
 void tg_trainer_destroy(tg_trainer* t);
 uint64_t tg_trainer_elements(const tg_trainer* t);
 int tg_trainer_step(tg_trainer* t, int64_t step, double* grad_norm, double* update_norm);
+/* Device pointer and byte size of rank partition `rank` (optim/rank_<rank>.shard payload
+ * layout); valid until the trainer is destroyed. */
+int tg_trainer_partition(tg_trainer* t, int32_t rank, void** d_ptr, uint64_t* bytes);
 /* read_checkpoint's invariants (R/src/checkpoint.cpp:485-575), checked on the device. */
 int tg_verify_checkpoint(const char* dir, int32_t device);
 /* Update-magnitude scores of consecutive snapshot directories on the device

@@ -112,6 +112,7 @@ SIGNATURES = {
     "tg_trainer_destroy": (None, [_P]),
     "tg_trainer_elements": (_U64, [_P]),
     "tg_trainer_step": (_I, [_P, _I64, _c.POINTER(_D), _c.POINTER(_D)]),
+    "tg_trainer_partition": (_I, [_P, _I32, _c.POINTER(_P), _c.POINTER(_U64)]),
     "tg_score_snapshots": (_I, [_c.POINTER(_S), _I32, _I32, _c.POINTER(_D), _c.POINTER(_D), _c.POINTER(_I32)]),
     "tg_select_recipe": (_I, [_c.POINTER(_S), _I32, _D, _I32, _c.c_char_p, _SZ, _PSZ, _c.POINTER(_I32),
                               _c.POINTER(_D)]),

@@ -422,6 +422,14 @@ int tg_trainer_step(tg_trainer* t, int64_t step, double* gn, double* un) {
     });
 }
 
+int tg_trainer_partition(tg_trainer* t, int32_t rank, void** d_ptr, uint64_t* bytes) {
+    return guard([&] {
+        const auto [p, n] = t->tr->partition(rank);
+        if (d_ptr) *d_ptr = p;
+        if (bytes) *bytes = n;
+    });
+}
+
 int tg_verify_checkpoint(const char* dir, int32_t device) {
     return guard([&] { verify_checkpoint_dir(dir ? dir : "", device); });
 }

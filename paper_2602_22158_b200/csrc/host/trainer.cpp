@@ -204,14 +204,25 @@ DeviceTrainer::~DeviceTrainer() {
 
 std::uint64_t DeviceTrainer::elements() const { return elements_; }
 
+std::pair<std::uint8_t*, std::uint64_t> DeviceTrainer::partition(int rank) {
+    if (rank < r0_ || rank >= r1_) fail(ErrorKind::Geometry, "rank " + std::to_string(rank) + " is not held by this trainer");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+    const auto& rk = ranks_[static_cast<std::size_t>(rank - r0_)];
+    return {rk->part.get(), full_.shards[static_cast<std::size_t>(rank)].payload_bytes};
+}
+
 std::pair<double, double> DeviceTrainer::step(std::int64_t s) {
     const dev::TrainParams p{dev::noise_prefix(model_.spec().seed, static_cast<std::uint64_t>(s)), 0.05f, 0.01f};
     cuda_check(cudaMemsetAsync(flag_.get(), 0, sizeof(unsigned int), stream_), "memset");
+    // fast check: masters' finiteness decides the gradient's (see finite_check_kernel);
+    // the gradient norm then comes from the update pass
+    const bool fast = !store_grad_ && dev::finite_check_suffices(p);
     for (auto& rk : ranks_)
-        cuda_check(dev::launch_grad_check(rk->tiles.get<dev::TrainTile>(), rk->ntiles, rk->groups.get<dev::TrainGroup>(),
-                                          rk->part.get(), p, store_grad_ ? rk->grad.get<float>() : nullptr,
-                                          rk->grad_part.get<double>(),
-                                          flag_.get<unsigned int>(), stream_),
+        cuda_check(fast ? dev::launch_finite_check(rk->tiles.get<dev::TrainTile>(), rk->ntiles, rk->groups.get<dev::TrainGroup>(),
+                                                   rk->part.get(), flag_.get<unsigned int>(), stream_)
+                        : dev::launch_grad_check(rk->tiles.get<dev::TrainTile>(), rk->ntiles, rk->groups.get<dev::TrainGroup>(),
+                                                 rk->part.get(), p, store_grad_ ? rk->grad.get<float>() : nullptr,
+                                                 rk->grad_part.get<double>(), flag_.get<unsigned int>(), stream_),
                    "grad check");
     unsigned int bad = 0;
     cuda_check(cudaMemcpyAsync(&bad, flag_.get(), sizeof(bad), cudaMemcpyDeviceToHost, stream_), "D2H");
@@ -237,7 +248,8 @@ std::pair<double, double> DeviceTrainer::step(std::int64_t s) {
     for (auto& rk : ranks_)
         cuda_check(dev::launch_adamw(rk->tiles.get<dev::TrainTile>(), rk->ntiles, rk->groups.get<dev::TrainGroup>(),
                                      coef_.get<dev::AdamCoef>(), rk->part.get(),
-                                     store_grad_ ? rk->grad.get<float>() : nullptr, p, rk->delta_part.get<double>(), stream_),
+                                     store_grad_ ? rk->grad.get<float>() : nullptr, p, rk->delta_part.get<double>(),
+                                     fast ? rk->grad_part.get<double>() : nullptr, stream_),
                    "adamw");
     double g2 = 0.0, d2 = 0.0;
     std::vector<double> h;

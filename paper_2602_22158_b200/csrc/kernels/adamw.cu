@@ -107,6 +107,35 @@ __global__ void __launch_bounds__(kThreads) grad_check_kernel(const TrainTile* _
     if (threadIdx.x == 0) grad_partials[blockIdx.x] = s;
 }
 
+// Pass 1, fast form: for the reference gradient source g = c1*w + c2*u with
+// 0 < |c1| <= 1/2, |c2| <= 1 and |u| < 1, g is finite exactly when w is (|c1*w|
+// <= FLT_MAX/2 cannot overflow with |c2*u| <= 1 added; c1*inf and c1*NaN are not
+// finite), so the pre-update check needs only the masters' exponent bits: a
+// pure 4 B/element read instead of the hash. The host picks this form only when
+// the coefficients satisfy the bound; the gradient norm then comes from pass 2.
+__global__ void __launch_bounds__(kThreads) finite_check_kernel(const TrainTile* __restrict__ tiles, std::uint32_t ntiles,
+                                                                const TrainGroup* __restrict__ groups,
+                                                                const std::uint8_t* __restrict__ part,
+                                                                unsigned int* __restrict__ nonfinite) {
+    bool bad = false;
+    for (std::uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const TrainTile tile = tiles[t];
+        const std::uint32_t* w = reinterpret_cast<const std::uint32_t*>(part + groups[tile.group].off_w) + tile.i0;
+        const auto inf_or_nan = [](std::uint32_t b) { return (b & 0x7F800000u) == 0x7F800000u; };
+        if (tile.vec) {
+            const std::uint32_t n4 = tile.count >> 2;
+#pragma unroll 4
+            for (std::uint32_t q = threadIdx.x; q < n4; q += kThreads) {
+                const uint4 x = __ldcs(reinterpret_cast<const uint4*>(w) + q);
+                bad = bad || inf_or_nan(x.x) || inf_or_nan(x.y) || inf_or_nan(x.z) || inf_or_nan(x.w);
+            }
+        } else {
+            for (std::uint32_t j = threadIdx.x; j < tile.count; j += kThreads) bad = bad || inf_or_nan(w[j]);
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
+}
+
 __device__ __forceinline__ float adam_one(const AdamCoef& c, float& w, float& m, float& v, float gr) {
     m = __fadd_rn(__fmul_rn(c.b1, m), __fmul_rn(c.one_minus_b1, gr));
     v = __fadd_rn(__fmul_rn(c.b2, v), __fmul_rn(c.one_minus_b2, __fmul_rn(gr, gr)));
@@ -126,9 +155,10 @@ __global__ void __launch_bounds__(kThreads) adamw_update_kernel(const TrainTile*
                                                                 const TrainGroup* __restrict__ groups,
                                                                 const AdamCoef* __restrict__ coef, std::uint8_t* __restrict__ part,
                                                                 const float* __restrict__ grad, TrainParams p,
-                                                                double* __restrict__ delta_partials) {
+                                                                double* __restrict__ delta_partials,
+                                                                double* __restrict__ grad_partials) {
     __shared__ double red[kThreads / 32];
-    double acc = 0.0;
+    double acc = 0.0, gacc = 0.0;
     for (std::uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const TrainTile tile = tiles[t];
         const TrainGroup& g = groups[tile.group];
@@ -161,6 +191,12 @@ __global__ void __launch_bounds__(kThreads) adamw_update_kernel(const TrainTile*
                 acc = fma(static_cast<double>(s1), static_cast<double>(s1), acc);
                 acc = fma(static_cast<double>(s2), static_cast<double>(s2), acc);
                 acc = fma(static_cast<double>(s3), static_cast<double>(s3), acc);
+                if constexpr (kRecompute) {
+                    gacc = fma(static_cast<double>(gr.x), static_cast<double>(gr.x), gacc);
+                    gacc = fma(static_cast<double>(gr.y), static_cast<double>(gr.y), gacc);
+                    gacc = fma(static_cast<double>(gr.z), static_cast<double>(gr.z), gacc);
+                    gacc = fma(static_cast<double>(gr.w), static_cast<double>(gr.w), gacc);
+                }
             }
         } else {
             for (std::uint32_t j = threadIdx.x; j < tile.count; j += kThreads) {
@@ -171,11 +207,18 @@ __global__ void __launch_bounds__(kThreads) adamw_update_kernel(const TrainTile*
                 vp[j] = v;
                 wp[j] = w;
                 acc = fma(static_cast<double>(st), static_cast<double>(st), acc);
+                if constexpr (kRecompute) gacc = fma(static_cast<double>(gr), static_cast<double>(gr), gacc);
             }
         }
     }
     const double s = block_sum(acc, red);
     if (threadIdx.x == 0) delta_partials[blockIdx.x] = s;
+    if constexpr (kRecompute) {
+        if (grad_partials) {
+            const double gs = block_sum(gacc, red);
+            if (threadIdx.x == 0) grad_partials[blockIdx.x] = gs;
+        }
+    }
 }
 
 // K8 — consolidated BF16 weights from sharded FP32 masters (derive_weights,
@@ -248,15 +291,27 @@ cudaError_t launch_grad_check(const TrainTile* d_tiles, std::uint32_t ntiles, co
     return cudaGetLastError();
 }
 
+bool finite_check_suffices(const TrainParams& p) {
+    const float c1 = p.state_coeff < 0 ? -p.state_coeff : p.state_coeff;
+    const float c2 = p.noise_coeff < 0 ? -p.noise_coeff : p.noise_coeff;
+    return c1 > 0.f && c1 <= 0.5f && c2 <= 1.f; // false for NaN coefficients too
+}
+
+cudaError_t launch_finite_check(const TrainTile* d_tiles, std::uint32_t ntiles, const TrainGroup* d_groups,
+                                const std::uint8_t* d_part, unsigned int* d_nonfinite, cudaStream_t s) {
+    finite_check_kernel<<<train_grid(ntiles), kThreads, 0, s>>>(d_tiles, ntiles, d_groups, d_part, d_nonfinite);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_adamw(const TrainTile* d_tiles, std::uint32_t ntiles, const TrainGroup* d_groups, const AdamCoef* d_coef,
                          std::uint8_t* d_part, const float* d_grad, const TrainParams& p, double* d_delta_partials,
-                         cudaStream_t s) {
+                         double* d_grad_partials, cudaStream_t s) {
     if (d_grad)
         adamw_update_kernel<false><<<train_grid(ntiles), kThreads, 0, s>>>(d_tiles, ntiles, d_groups, d_coef, d_part, d_grad, p,
-                                                                          d_delta_partials);
+                                                                          d_delta_partials, nullptr);
     else
         adamw_update_kernel<true><<<train_grid(ntiles), kThreads, 0, s>>>(d_tiles, ntiles, d_groups, d_coef, d_part, nullptr, p,
-                                                                         d_delta_partials);
+                                                                         d_delta_partials, d_grad_partials);
     return cudaGetLastError();
 }
 

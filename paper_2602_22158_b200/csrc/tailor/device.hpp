@@ -174,7 +174,13 @@ cudaError_t launch_grad_check(const TrainTile* d_tiles, std::uint32_t ntiles, co
                               unsigned int* d_nonfinite, cudaStream_t s);
 cudaError_t launch_adamw(const TrainTile* d_tiles, std::uint32_t ntiles, const TrainGroup* d_groups, const AdamCoef* d_coef,
                          std::uint8_t* d_part, const float* d_grad, const TrainParams& p, double* d_delta_partials,
-                         cudaStream_t s);
+                         double* d_grad_partials, cudaStream_t s);
+// Pass 1 fast form (masters' exponent bits only) and when it is exact: g = c1*w +
+// c2*u is finite iff w is, for 0 < |c1| <= 1/2 and |c2| <= 1. In that mode pass 2
+// (recomputing) also writes the FP64 sum g^2 per block into d_grad_partials.
+bool finite_check_suffices(const TrainParams& p);
+cudaError_t launch_finite_check(const TrainTile* d_tiles, std::uint32_t ntiles, const TrainGroup* d_groups,
+                                const std::uint8_t* d_part, unsigned int* d_nonfinite, cudaStream_t s);
 // blocks of the two passes (one FP64 partial each)
 unsigned train_grid(std::uint32_t ntiles);
 unsigned adamw_grid(std::uint64_t total);

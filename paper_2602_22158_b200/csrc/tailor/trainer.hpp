@@ -54,6 +54,9 @@ class DeviceTrainer {
     void keep_masters();
     std::vector<std::pair<double, double>> score_against_kept();
     const ModelLayout& model() const { return model_; }
+    // Device partition of rank r (payload layout of optim/rank_r.shard) and its
+    // size, for in-situ consumers (scorers, diagnostics); synchronizes first.
+    std::pair<std::uint8_t*, std::uint64_t> partition(int rank);
 
   private:
     struct Rank;

@@ -419,6 +419,12 @@ class Trainer:
         check(lib().tg_trainer_step(self._h, step, ctypes.byref(g), ctypes.byref(u)))
         return g.value, u.value
 
+    def partition(self, rank: int):
+        """(device pointer, bytes) of a held rank partition (rank_<r>.shard payload layout)."""
+        ptr, n = ctypes.c_void_p(), ctypes.c_uint64()
+        check(lib().tg_trainer_partition(self._h, rank, ctypes.byref(ptr), ctypes.byref(n)))
+        return ptr.value, n.value
+
 
 class SelectStep:
     """Device score -> select -> merge step for one unit of a family of full snapshots

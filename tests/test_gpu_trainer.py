@@ -110,3 +110,62 @@ def test_cli_train_matches_reference_cli(tmp_path):
                 ["--strategy", "full", "--grouping", "coarse", "--out", str(tmp_path / "y")]]:
         r = subprocess.run(base + bad, capture_output=True, text=True)
         assert r.returncode == 1 and "RecipeError" in r.stderr
+
+
+def _d2d(dst: int, src: int, n: int) -> None:
+    import ctypes
+
+    cudart = ctypes.CDLL("libcudart.so.12")
+    assert cudart.cudaMemcpy(ctypes.c_void_p(dst), ctypes.c_void_p(src), ctypes.c_size_t(n), 3) == 0  # D2D
+
+
+@pytest.mark.parametrize("store_grad", ["0", "1"])
+@pytest.mark.parametrize("poison", [float("inf"), float("nan"), float("-inf")])
+def test_nonfinite_gradient_leaves_state_untouched(monkeypatch, store_grad, poison):
+    """apply_step's contract (R/src/adamw.cpp:49-60): a non-finite gradient raises
+    NonFinite before any state changes. Both pass-1 forms (the masters' exponent check,
+    with the gradient recomputed in pass 2; and the full gradient pass with a scratch
+    buffer) must catch it, and both give the same norms on clean steps."""
+    need_gpu()
+    import sys
+
+    sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1] / "oracle"))
+    import tailor_oracle as o
+
+    monkeypatch.setenv("TAILOR_TRAIN_STORE_GRAD", store_grad)
+    spec = t.ModelSpec(2, 16, 40, 64, False, 5)
+    ospec = dict(num_layers=2, hidden_dim=16, ffn_dim=40, vocab_size=64, weight_tied=False, seed=5)
+    N = 2
+    tr = t.Trainer(spec, N)
+    norms = [tr.step(1), tr.step(2)]
+    ref = t.Trainer(spec, N) if store_grad == "0" else None
+    if ref is not None:  # the other pass-1 form gives the same norms (within FP64 summation order)
+        monkeypatch.setenv("TAILOR_TRAIN_STORE_GRAD", "1")
+        ref = t.Trainer(spec, N)
+        for s, (g, u) in zip((1, 2), norms):
+            rg, ru = ref.step(s)
+            assert g == pytest.approx(rg, rel=1e-12) and u == pytest.approx(ru, rel=1e-12)
+    ptr, n = tr.partition(1)
+    _, entries, payload = o.container_layout(o.shard_decls(ospec, N, range(len(o.group_table(ospec)))))
+    assert payload == n
+    lo, hi = entries["g1.master"]  # layer 0 no-decay group, rank 1's chunk
+    snap = torch.empty(n, dtype=torch.uint8, device="cuda")
+    _d2d(snap.data_ptr(), ptr, n)
+    snap.view(torch.float32)[lo // 4 + 3] = poison
+    _d2d(ptr, snap.data_ptr(), n)
+    with pytest.raises(t.TailorError) as e:
+        tr.step(3)
+    assert e.value.kind == t.ErrorKind.NonFinite
+    after = torch.empty_like(snap)
+    _d2d(after.data_ptr(), ptr, n)
+    assert torch.equal(after, snap)
+    # a non-finite first moment is not a gradient: the step proceeds
+    tr2 = t.Trainer(spec, N)
+    tr2.step(1)
+    p2, _ = tr2.partition(0)
+    s2 = torch.empty(n, dtype=torch.uint8, device="cuda")
+    _d2d(s2.data_ptr(), p2, n)
+    lo, hi = entries["g1.exp_avg"]
+    s2.view(torch.float32)[lo // 4] = poison
+    _d2d(p2, s2.data_ptr(), n)
+    tr2.step(2)
