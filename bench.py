@@ -113,8 +113,32 @@ def peaks():
         return FALLBACK_HBM, "fallback"
 
 
+_NVML_POLLER = r"""
+import sys, time, pynvml as nv
+nv.nvmlInit()
+bus = sys.argv[1]
+try:
+    h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+except Exception:
+    h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[2]))
+mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+        nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+print("ready", flush=True)
+while True:
+    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+    act = ", ".join("Active" if r & b else "Not Active" for b in bits)
+    print(f"{time.time():.6f} {sys.argv[2]}, {sm}, {mx}, 0, 0, {act}", flush=True)
+    time.sleep(0.002)
+"""
+
+
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML polled every
+    ~2 ms from a separate process (a thread in this process would compete for the GIL
+    with the step loop and can miss a 75 ms region), samples kept by timestamp; falls
+    back to `nvidia-smi -lms 20`."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -124,52 +148,35 @@ class ClockSampler:
         self.gpu = gpu_index
         self.proc = None
         self.lines = []
-        self.nvml = None
+        self.nvml = False
+        self.t0 = self.t1 = 0.0
 
-    def _nvml_handle(self):
-        """NVML handle of the CUDA device (by PCI bus id, so CUDA_VISIBLE_DEVICES is honoured)."""
-        import pynvml
+    def _bus_id(self):
         import torch
 
-        pynvml.nvmlInit()
         p = torch.cuda.get_device_properties(self.gpu)
-        bus = f"{p.pci_domain_id:08X}:{p.pci_bus_id:02X}:{p.pci_device_id:02X}.0"
-        try:
-            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
-        except Exception:
-            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
-
-    def _poll(self):
-        # NVML directly, every ~2 ms: a 75 ms timed region still gets dozens of samples
-        nv, h = self.nvml
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
-                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
-                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
-                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
-        while not self.stop.is_set():
-            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-            act = [n for n, b in bits.items() if r & b]
-            self.lines.append(f"{self.gpu}, {sm}, {mx}, 0, 0, " + ", ".join(
-                "Active" if n in act else "Not Active" for n in bits))
-            self.stop.wait(0.002)
+        return f"{p.pci_domain_id:08X}:{p.pci_bus_id:02X}:{p.pci_device_id:02X}.0"
 
     def __enter__(self):
         try:
-            self.nvml = self._nvml_handle()
-            self.stop = threading.Event()
-            self.reader = threading.Thread(target=self._poll, daemon=True)
-            self.reader.start()
-            return self
-        except Exception:
-            self.nvml = None
-        if shutil.which("nvidia-smi"):
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "20"],
+            self.proc = subprocess.Popen([sys.executable, "-c", _NVML_POLLER, self._bus_id(), str(self.gpu)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            if self.proc.stdout.readline().strip() != "ready":
+                raise RuntimeError("nvml poller did not start")
+            self.nvml = True
+        except Exception:
+            if self.proc:
+                self.proc.kill()
+            self.proc, self.nvml = None, False
+            if shutil.which("nvidia-smi"):
+                self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                              "--format=csv,noheader,nounits", "-lms", "20"],
+                                             stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        if self.proc:
             self.reader = threading.Thread(target=self._read, daemon=True)
             self.reader.start()
+        time.sleep(0.01)  # a few samples before the region starts
+        self.t0 = time.time()
         return self
 
     def _read(self):
@@ -177,9 +184,8 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
-        if self.nvml:
-            self.stop.set()
-            self.reader.join(timeout=2)
+        self.t1 = time.time()
+        time.sleep(0.01)
         if self.proc:
             self.proc.terminate()
             try:
@@ -192,6 +198,13 @@ class ClockSampler:
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
+            if self.nvml:  # "<unix time> idx, sm, max, ..." : keep the samples inside the region
+                ts, _, ln = ln.partition(" ")
+                try:
+                    if not self.t0 <= float(ts) <= self.t1:
+                        continue
+                except ValueError:
+                    continue
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 9:
                 continue
