@@ -76,9 +76,22 @@ def run(spec, N, K, variants=(0, 1, 2)):
                             slices=[t.RecipeSlice(f"{d}/checkpoint-100", [0])])
         t.execute_merge(rec, f"{d}/merged")
         t.verify_checkpoint(f"{d}/merged")
+        # file scorer lanes + multi-lane merge (workers 1 and 8) + regroup both ways
+        dirs = [f"{d}/checkpoint-{k * 100}" for k in range(1, K + 1)]
+        rec2, _, _ = t.select_recipe(dirs, 0.5)
+        t.execute_merge(rec2, f"{d}/sel8", t.MergeOptions(workers=8))
+        t.execute_merge(rec2, f"{d}/sel1", t.MergeOptions(workers=1))
+        t.regroup(f"{d}/sel8", f"{d}/coarse", to_fine=False)
+        t.regroup(f"{d}/coarse", f"{d}/fine", to_fine=True)
 
 
 def run_trainer():
+    import os
+
+    os.environ["TAILOR_TRAIN_STORE_GRAD"] = "1"  # scratch-gradient form
+    with tempfile.TemporaryDirectory() as d:
+        t.train(t.ModelSpec(2, 8, 12, 20, False, 9), f"{d}/full", 10, 10, "full", num_ranks=2)
+    os.environ["TAILOR_TRAIN_STORE_GRAD"] = "0"  # default: exponent-bit check + recomputed gradient
     with tempfile.TemporaryDirectory() as d:
         t.train(t.ModelSpec(3, 8, 12, 20, False, 9), f"{d}/full", 20, 10, "full", num_ranks=2)
         t.train(t.ModelSpec(2, 16, 40, 50, True, 5), f"{d}/mag", 30, 10, "magnitude", num_ranks=3, rho=0.5)
