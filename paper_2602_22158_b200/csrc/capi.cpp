@@ -142,12 +142,21 @@ CheckpointSummary family_summary(const SynthFamily& f, const std::string& id) {
 // of the other on the lane's stream). Buffers are reused across calls: a lane
 // loads one rank after another.
 void load_packed_masters(const std::vector<std::string>& dirs, int rank, const ModelLayout& model, int num_ranks,
-                         std::vector<DeviceBuffer>& out, std::vector<std::vector<std::uint64_t>>& offs,
+                         DeviceBuffer& arena, std::vector<const std::uint8_t*>& bases,
+                         std::vector<std::vector<std::uint64_t>>& offs,
                          PinnedBuffer& stage, int threads, cudaStream_t st, cudaEvent_t* half_done,
                          double* phase_ms = nullptr) {
     constexpr std::uint64_t kHalf = 16ull << 20;
     const auto fields = score_fields(model, num_ranks);
-    out.resize(dirs.size());
+    // one device arena holds the K packed snapshots (same layout each): one allocation
+    std::uint64_t stride = 0;
+    for (const auto& f : fields) stride = (stride + static_cast<std::uint64_t>(f.chunk) * 4 + 15) & ~15ull;
+    stride = std::max<std::uint64_t>(256, (stride + 255) & ~255ull);
+    const double ta = clock_ms();
+    arena.resize(stride * dirs.size());
+    if (phase_ms) phase_ms[1] += clock_ms() - ta;
+    bases.clear();
+    for (std::size_t k = 0; k < dirs.size(); ++k) bases.push_back(arena.get() + k * stride);
     offs.assign(dirs.size(), {});
     stage.resize(2 * kHalf);
     bool used[2] = {false, false};
@@ -166,9 +175,8 @@ void load_packed_masters(const std::vector<std::string>& dirs, int rank, const M
             offs[k].push_back(total);
             total = (total + e->bytes() + 15) & ~15ull;
         }
-        const double t1 = clock_ms();
-        out[k].resize(std::max<std::uint64_t>(16, total));
         const double t2 = clock_ms();
+        std::uint8_t* dst = arena.get() + k * stride;
         const int fd = ::open(p.c_str(), O_RDONLY);
         if (fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + p.string() + "'");
         try {
@@ -187,7 +195,7 @@ void load_packed_masters(const std::vector<std::string>& dirs, int rank, const M
                 const double r0 = clock_ms();
                 run_reads(jobs, threads, p.string());
                 if (phase_ms) phase_ms[0] += clock_ms() - r0;
-                cuda_check(cudaMemcpyAsync(out[k].get() + lo, buf, hi - lo, cudaMemcpyHostToDevice, st), "H2D");
+                cuda_check(cudaMemcpyAsync(dst + lo, buf, hi - lo, cudaMemcpyHostToDevice, st), "H2D");
                 cuda_check(cudaEventRecord(half_done[half], st), "event");
                 used[half] = true;
             }
@@ -197,10 +205,7 @@ void load_packed_masters(const std::vector<std::string>& dirs, int rank, const M
             throw;
         }
         ::close(fd);
-        if (phase_ms) {
-            phase_ms[1] += t2 - t1;
-            phase_ms[2] += clock_ms() - t2;
-        }
+        if (phase_ms) phase_ms[2] += clock_ms() - t2;
     }
 }
 
@@ -246,8 +251,8 @@ void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<st
             cudaStream_t st = nullptr;
             cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
             std::unique_ptr<CUstream_st, decltype(&cudaStreamDestroy)> own(st, &cudaStreamDestroy);
-            DeviceBuffer dout(nres * sizeof(double));
-            std::vector<DeviceBuffer> bufs;
+            DeviceBuffer dout(nres * sizeof(double)), arena;
+            std::vector<const std::uint8_t*> bases;
             PinnedBuffer stage;
             cudaEvent_t half_done[2];
             for (auto& e : half_done) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -262,11 +267,9 @@ void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<st
                 PhaseTimer pt("score.rank");
                 double ph[3] = {0, 0, 0};
                 const double t0 = clock_ms();
-                load_packed_masters(dirs, r, model, N, bufs, offs, stage, readers, st, half_done, ph);
+                load_packed_masters(dirs, r, model, N, arena, bases, offs, stage, readers, st, half_done, ph);
                 const double t1 = clock_ms();
                 ScorePlan plan(model, N, offs);
-                std::vector<const std::uint8_t*> bases;
-                for (auto& b : bufs) bases.push_back(b.get());
                 plan.run(bases.data(), dout.get<double>(), st);
                 cuda_check(cudaMemcpyAsync(res[static_cast<std::size_t>(r)].data(), dout.get(), nres * sizeof(double),
                                            cudaMemcpyDeviceToHost, st),
