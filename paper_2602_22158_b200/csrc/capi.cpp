@@ -10,6 +10,7 @@
 #include <mutex>
 #include <thread>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <filesystem>
 #include <fcntl.h>
@@ -137,46 +138,52 @@ CheckpointSummary family_summary(const SynthFamily& f, const std::string& id) {
     return f.summary(k, id);
 }
 
-// Reads each snapshot's rank-r master fields into one packed device buffer,
-// streamed through two 16 MB pinned halves (pread of one half overlaps the H2D
-// of the other on the lane's stream). Buffers are reused across calls: a lane
-// loads one rank after another.
-void load_packed_masters(const std::vector<std::string>& dirs, int rank, const ModelLayout& model, int num_ranks,
-                         DeviceBuffer& arena, std::vector<const std::uint8_t*>& bases,
-                         std::vector<std::vector<std::uint64_t>>& offs,
-                         PinnedBuffer& stage, int threads, cudaStream_t st, cudaEvent_t* half_done,
-                         double* phase_ms = nullptr) {
-    constexpr std::uint64_t kHalf = 16ull << 20;
-    const auto fields = score_fields(model, num_ranks);
-    // one device arena holds the K packed snapshots (same layout each): one allocation
-    std::uint64_t stride = 0;
-    for (const auto& f : fields) stride = (stride + static_cast<std::uint64_t>(f.chunk) * 4 + 15) & ~15ull;
-    stride = std::max<std::uint64_t>(256, (stride + 255) & ~255ull);
-    const double ta = clock_ms();
-    arena.resize(stride * dirs.size());
-    if (phase_ms) phase_ms[1] += clock_ms() - ta;
-    bases.clear();
-    for (std::size_t k = 0; k < dirs.size(); ++k) bases.push_back(arena.get() + k * stride);
-    offs.assign(dirs.size(), {});
-    stage.resize(2 * kHalf);
+// Packed layout of one snapshot's rank-r master fields: 16-B aligned, in
+// score_fields order; `stride` rounds the total to 256 B (the slot size).
+std::uint64_t packed_stride(const std::vector<ScoreField>& fields) {
+    std::uint64_t total = 0;
+    for (const auto& f : fields) total = (total + static_cast<std::uint64_t>(f.chunk) * 4 + 15) & ~15ull;
+    return std::max<std::uint64_t>(256, (total + 255) & ~255ull);
+}
+
+// Streams one snapshot's rank-r master fields into `dst` (packed layout) through
+// two 16 MB pinned halves: the pread of one half overlaps the H2D of the other on
+// the lane's stream. `offs` receives the field offsets inside `dst`.
+struct PackedLoader {
+    PinnedBuffer stage;
+    cudaStream_t st = nullptr;
+    cudaEvent_t half_done[2]{};
     bool used[2] = {false, false};
-    int half = 0;
-    for (std::size_t k = 0; k < dirs.size(); ++k) {
-        const fs::path p = ckpt_file(CkptFile::Shard, dirs[k], rank);
+    int half = 0, threads = 1;
+    double read_ms = 0.0, load_ms = 0.0;
+    static constexpr std::uint64_t kHalf = 16ull << 20;
+
+    PackedLoader(cudaStream_t s, int reader_threads) : st(s), threads(reader_threads) {
+        for (auto& e : half_done) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        stage.resize(2 * kHalf);
+    }
+    ~PackedLoader() {
+        if (st) cudaStreamSynchronize(st);
+        for (auto& e : half_done) cudaEventDestroy(e);
+    }
+    PackedLoader(const PackedLoader&) = delete;
+    PackedLoader& operator=(const PackedLoader&) = delete;
+
+    void load(const fs::path& p, const std::vector<ScoreField>& fields, std::uint8_t* dst, std::vector<std::uint64_t>& offs) {
+        const double t0 = clock_ms();
         const ContainerLayout lay = read_layout(p);
         std::uint64_t total = 0;
         std::vector<std::pair<const Entry*, std::uint64_t>> where;
+        offs.clear();
         for (const auto& f : fields) {
             const Entry* e = lay.find(shard_key(f.group, ".master"));
             if (!e) fail(ErrorKind::MissingModules, p.string() + ": scoring needs every module; missing '" + shard_key(f.group, ".master") + "'");
             if (e->dtype != Dtype::F32 || e->shape != std::vector<std::int64_t>{f.chunk})
                 fail(ErrorKind::Geometry, p.string() + ": master '" + e->name + "' has unexpected dtype/shape");
             where.push_back({e, total});
-            offs[k].push_back(total);
+            offs.push_back(total);
             total = (total + e->bytes() + 15) & ~15ull;
         }
-        const double t2 = clock_ms();
-        std::uint8_t* dst = arena.get() + k * stride;
         const int fd = ::open(p.c_str(), O_RDONLY);
         if (fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + p.string() + "'");
         try {
@@ -194,7 +201,7 @@ void load_packed_masters(const std::vector<std::string>& dirs, int rank, const M
                 }
                 const double r0 = clock_ms();
                 run_reads(jobs, threads, p.string());
-                if (phase_ms) phase_ms[0] += clock_ms() - r0;
+                read_ms += clock_ms() - r0;
                 cuda_check(cudaMemcpyAsync(dst + lo, buf, hi - lo, cudaMemcpyHostToDevice, st), "H2D");
                 cuda_check(cudaEventRecord(half_done[half], st), "event");
                 used[half] = true;
@@ -205,9 +212,9 @@ void load_packed_masters(const std::vector<std::string>& dirs, int rank, const M
             throw;
         }
         ::close(fd);
-        if (phase_ms) phase_ms[2] += clock_ms() - t2;
+        load_ms += clock_ms() - t0;
     }
-}
+};
 
 // Device scores over snapshot directories: per rank, packed masters -> K3/K4;
 // ranks combined in rank order on the host (FP64, fixed order).
@@ -231,15 +238,22 @@ void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<st
     sr = sd;
     // Ranks are independent: lanes (threads with their own buffers) score one
     // rank each; the per-rank partials are summed in rank order afterwards, so
-    // the result does not depend on the lane count.
-    std::uint64_t per_rank = 16;
-    for (const auto& f : score_fields(model, N)) per_rank += (static_cast<std::uint64_t>(f.chunk) * 4 + 15) & ~15ull;
-    per_rank *= static_cast<std::uint64_t>(K);
-    std::size_t free_b = 0, total_b = 0;
-    cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-    const std::uint64_t budget = free_b > (2ull << 30) ? (free_b - (2ull << 30)) / 2 : 0;
-    const int lanes = std::clamp<int>(static_cast<int>(std::min<std::uint64_t>(budget / per_rank, 8)), 1, std::min(N, 8));
+    // the result does not depend on the lane count. A lane holds the K packed
+    // snapshots of its rank when they fit the device budget; otherwise it streams
+    // the snapshots through two slots and scores consecutive pairs (K3 with K=2 over
+    // the same tiles in the same order gives each pair's sums), e.g. a 70B-shaped
+    // rank partition (4 x 40 GB of masters).
+    const auto fields = score_fields(model, N);
+    const std::uint64_t stride = packed_stride(fields);
+    const std::uint64_t budget = device_budget();
+    const bool pairwise = stride * static_cast<std::uint64_t>(K) > budget;
+    const std::uint64_t per_lane = stride * (pairwise ? 2u : static_cast<std::uint64_t>(K));
+    if (per_lane > budget && !std::getenv("TAILOR_DEVICE_BUDGET"))
+        fail(ErrorKind::Device, "scoring needs " + std::to_string(per_lane) + " B of device memory for two snapshots of one rank; " +
+                                    std::to_string(budget) + " B available");
+    const int lanes = std::clamp<int>(static_cast<int>(std::min<std::uint64_t>(budget / per_lane, 8)), 1, std::min(N, 8));
     const int readers = std::max(1, io_threads() / lanes);
+    trace_value(pairwise ? "score.lanes (pairwise)" : "score.lanes", lanes);
     const std::size_t nres = static_cast<std::size_t>(K - 1) * M * 2;
     std::vector<std::vector<double>> res(static_cast<std::size_t>(N), std::vector<double>(nres));
     std::atomic<int> next{0};
@@ -251,33 +265,48 @@ void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<st
             cudaStream_t st = nullptr;
             cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
             std::unique_ptr<CUstream_st, decltype(&cudaStreamDestroy)> own(st, &cudaStreamDestroy);
-            DeviceBuffer dout(nres * sizeof(double)), arena;
-            std::vector<const std::uint8_t*> bases;
-            PinnedBuffer stage;
-            cudaEvent_t half_done[2];
-            for (auto& e : half_done) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-            std::unique_ptr<CUevent_st, decltype(&cudaEventDestroy)> own0(half_done[0], &cudaEventDestroy),
-                own1(half_done[1], &cudaEventDestroy);
+            DeviceBuffer dout(nres * sizeof(double)), arena(per_lane);
+            PackedLoader loader(st, readers);
             for (int r = next.fetch_add(1); r < N; r = next.fetch_add(1)) {
                 {
                     std::lock_guard<std::mutex> lk(mu);
                     if (lane_err) break;
                 }
-                std::vector<std::vector<std::uint64_t>> offs;
                 PhaseTimer pt("score.rank");
-                double ph[3] = {0, 0, 0};
+                loader.read_ms = loader.load_ms = 0.0;
                 const double t0 = clock_ms();
-                load_packed_masters(dirs, r, model, N, arena, bases, offs, stage, readers, st, half_done, ph);
-                const double t1 = clock_ms();
-                ScorePlan plan(model, N, offs);
-                plan.run(bases.data(), dout.get<double>(), st);
+                std::vector<std::vector<std::uint64_t>> offs(static_cast<std::size_t>(K));
+                if (!pairwise) {
+                    std::vector<const std::uint8_t*> bases;
+                    for (int k = 0; k < K; ++k) {
+                        std::uint8_t* slot = arena.get() + static_cast<std::uint64_t>(k) * stride;
+                        loader.load(ckpt_file(CkptFile::Shard, dirs[static_cast<std::size_t>(k)], r), fields, slot,
+                                    offs[static_cast<std::size_t>(k)]);
+                        bases.push_back(slot);
+                    }
+                    ScorePlan plan(model, N, offs);
+                    plan.run(bases.data(), dout.get<double>(), st);
+                } else {
+                    loader.load(ckpt_file(CkptFile::Shard, dirs[0], r), fields, arena.get(), offs[0]);
+                    std::unique_ptr<ScorePlan> plan;
+                    for (int k = 1; k < K; ++k) {
+                        std::uint8_t* prev = arena.get() + static_cast<std::uint64_t>((k - 1) % 2) * stride;
+                        std::uint8_t* cur = arena.get() + static_cast<std::uint64_t>(k % 2) * stride;
+                        // the slot is free once the previous pair's scoring has run (same stream)
+                        loader.load(ckpt_file(CkptFile::Shard, dirs[static_cast<std::size_t>(k)], r), fields, cur,
+                                    offs[static_cast<std::size_t>(k)]);
+                        if (!plan) plan = std::make_unique<ScorePlan>(model, N, std::vector<std::vector<std::uint64_t>>{offs[0], offs[1]});
+                        const std::uint8_t* bases[2] = {prev, cur};
+                        plan->run(bases, dout.get<double>() + static_cast<std::size_t>(k - 1) * M * 2, st);
+                    }
+                }
                 cuda_check(cudaMemcpyAsync(res[static_cast<std::size_t>(r)].data(), dout.get(), nres * sizeof(double),
                                            cudaMemcpyDeviceToHost, st),
                            "D2H");
                 cuda_check(cudaStreamSynchronize(st), "sync");
                 if (trace_enabled())
-                    std::fprintf(stderr, "[tailor] score.rank %d: load %.1f (read %.1f alloc %.1f read+h2d %.1f) plan+run %.1f ms\n", r,
-                                 t1 - t0, ph[0], ph[1], ph[2], clock_ms() - t1);
+                    std::fprintf(stderr, "[tailor] score.rank %d: load %.1f (read %.1f) total %.1f ms\n", r, loader.load_ms,
+                                 loader.read_ms, clock_ms() - t0);
             }
         } catch (...) {
             std::lock_guard<std::mutex> lk(mu);

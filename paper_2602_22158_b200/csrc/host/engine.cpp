@@ -6,10 +6,12 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fcntl.h>
 #include <filesystem>
 #include <fstream>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <thread>
@@ -113,6 +115,14 @@ DevicePool& device_pool() {
     return *pool;
 }
 } // namespace
+
+std::uint64_t device_budget() {
+    std::size_t free_b = 0, total_b = 0;
+    cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    std::uint64_t b = free_b > (2ull << 30) ? (free_b - (2ull << 30)) / 2 : 0;
+    if (const char* v = std::getenv("TAILOR_DEVICE_BUDGET"); v && *v) b = std::min<std::uint64_t>(b, std::strtoull(v, nullptr, 10));
+    return b;
+}
 
 DeviceBuffer::~DeviceBuffer() {
     if (p_) device_pool().give(dev_, p_, cap_);
@@ -899,45 +909,81 @@ struct StreamHandle {
     StreamHandle& operator=(const StreamHandle&) = delete;
 };
 
-void load_payload(const fs::path& path, const ContainerLayout& lay, DeviceBuffer& dst, PinnedBuffer* stage /* [2] */,
-                  int threads = io_threads(), std::uint64_t step = 512ull << 20) {
-    dst.resize(std::max<std::uint64_t>(16, lay.payload_bytes));
+struct FileRange {
+    std::uint64_t file_off, bytes;
+    std::uint8_t* dst; // device
+};
+
+// Streams byte ranges of one file to device memory in `step`-byte pieces read by
+// the I/O pool, alternating two pinned halves so the H2D of one piece overlaps
+// the reads of the next. Returns after the copies complete.
+void load_ranges(const fs::path& path, const std::vector<FileRange>& ranges, PinnedBuffer* stage /* [2] */, int threads,
+                 std::uint64_t step, cudaStream_t s) {
     const int fd = ::open(path.c_str(), O_RDONLY);
     if (fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + path.string() + "'");
-    // `step`-byte windows read by the I/O pool, alternating two halves of the
-    // pinned stage so the H2D of one overlaps the reads of the next.
     stage[0].resize(step);
     stage[1].resize(step);
-    cudaStream_t s = nullptr;
-    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
     cudaEvent_t done[2];
     cuda_check(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming), "event");
     cuda_check(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming), "event");
     bool used[2] = {false, false};
-    try {
-        int half = 0;
-        for (std::uint64_t off = 0; off < lay.payload_bytes; off += step, half ^= 1) {
-            const std::uint64_t n = std::min(step, lay.payload_bytes - off);
-            std::uint8_t* buf = stage[half].get();
-            if (used[half]) cuda_check(cudaEventSynchronize(done[half]), "event");
-            run_reads({{fd, buf, n, lay.payload_offset() + off}}, threads, path.string());
-            cuda_check(cudaMemcpyAsync(dst.get() + off, buf, n, cudaMemcpyHostToDevice, s), "H2D");
-            cuda_check(cudaEventRecord(done[half], s), "event");
-            used[half] = true;
-        }
-        cuda_check(cudaStreamSynchronize(s), "sync");
-    } catch (...) {
+    const auto cleanup = [&] {
         cudaStreamSynchronize(s);
-        cudaStreamDestroy(s);
         cudaEventDestroy(done[0]);
         cudaEventDestroy(done[1]);
         ::close(fd);
+    };
+    try {
+        int half = 0;
+        std::size_t ri = 0;
+        std::uint64_t at = 0; // progress inside ranges[ri]
+        while (ri < ranges.size()) {
+            // fill one half with up to `step` bytes drawn from consecutive ranges
+            std::uint8_t* buf = stage[half].get();
+            if (used[half]) cuda_check(cudaEventSynchronize(done[half]), "event");
+            std::vector<ReadJob> jobs;
+            std::vector<std::pair<std::uint64_t, const FileRange*>> pieces; // (bytes, range) with in-range offsets
+            std::vector<std::uint64_t> starts;
+            std::uint64_t fill = 0;
+            while (ri < ranges.size() && fill < step) {
+                const FileRange& r = ranges[ri];
+                const std::uint64_t n = std::min(step - fill, r.bytes - at);
+                if (n > 0) {
+                    jobs.push_back({fd, buf + fill, n, r.file_off + at});
+                    pieces.push_back({n, &r});
+                    starts.push_back(at);
+                }
+                fill += n;
+                at += n;
+                if (at == r.bytes) {
+                    ++ri;
+                    at = 0;
+                }
+            }
+            run_reads(jobs, threads, path.string());
+            std::uint64_t off = 0;
+            for (std::size_t i = 0; i < pieces.size(); ++i) {
+                cuda_check(cudaMemcpyAsync(pieces[i].second->dst + starts[i], buf + off, pieces[i].first, cudaMemcpyHostToDevice, s),
+                           "H2D");
+                off += pieces[i].first;
+            }
+            cuda_check(cudaEventRecord(done[half], s), "event");
+            used[half] = true;
+            half ^= 1;
+        }
+        cuda_check(cudaStreamSynchronize(s), "sync");
+    } catch (...) {
+        cleanup();
         throw;
     }
-    cudaStreamDestroy(s);
-    cudaEventDestroy(done[0]);
-    cudaEventDestroy(done[1]);
-    ::close(fd);
+    cleanup();
+}
+
+void load_payload(const fs::path& path, const ContainerLayout& lay, DeviceBuffer& dst, PinnedBuffer* stage /* [2] */,
+                  int threads = io_threads(), std::uint64_t step = 512ull << 20) {
+    dst.resize(std::max<std::uint64_t>(16, lay.payload_bytes));
+    StreamHandle sh;
+    load_ranges(path, {{lay.payload_offset(), lay.payload_bytes, dst.get()}}, stage, threads, step, sh.s);
 }
 
 } // namespace
@@ -1020,54 +1066,16 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
 
     DeviceBuffer dw, derr(static_cast<std::size_t>(N) * 3 * sizeof(unsigned long long));
     cuda_check(cudaMemset(derr.get(), 0, derr.size()), "memset");
-    std::size_t free_b = 0, total_b = 0;
-    cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-    const std::uint64_t budget = free_b > wl.payload_bytes + (2ull << 30) ? (free_b - wl.payload_bytes - (2ull << 30)) / 2 : 0;
-    const int lanes = std::clamp<int>(static_cast<int>(std::min<std::uint64_t>(budget / max_shard, 8)), 1, std::max(1, std::min(N, 8)));
-    const int readers = std::max(1, io_threads() / lanes);
-    const std::uint64_t step = lanes > 1 ? (16ull << 20) : (256ull << 20);
-    {
-        PhaseTimer pt("verify.load_weights");
-        PinnedBuffer stage[2];
-        load_payload(ckpt_file(CkptFile::Weights, dir), wl, dw, stage, io_threads(), step);
-    }
+    const std::uint64_t budget = device_budget();
+    // Resident form: the weights payload stays on the device and each lane holds one
+    // whole rank payload. Streaming form (a 70B-shaped checkpoint: 160 GB of weights,
+    // 120 GB per rank): each lane walks its rank payload in windows and loads, per
+    // window, only the weight bytes its masters pair with (every byte read once).
+    const bool resident = wl.payload_bytes + max_shard <= budget;
     std::atomic<int> next{0};
     std::exception_ptr lane_err;
     std::mutex mu;
-    const auto lane = [&] {
-        try {
-            cuda_check(cudaSetDevice(device), "cudaSetDevice");
-            DeviceBuffer ds, dpairs, dranges;
-            PinnedBuffer stage[2];
-            StreamHandle ls;
-            for (int r = next.fetch_add(1); r < N; r = next.fetch_add(1)) {
-                {
-                    std::lock_guard<std::mutex> lk(mu);
-                    if (lane_err) break;
-                }
-                const auto& sl = shard_lay[static_cast<std::size_t>(r)];
-                load_payload(ckpt_file(CkptFile::Shard, dir, r), sl, ds, stage, readers, step);
-                auto pr = pairs[static_cast<std::size_t>(r)];
-                auto rg = ranges[static_cast<std::size_t>(r)];
-                for (auto& x : pr) {
-                    x.master = reinterpret_cast<const float*>(ds.get() + reinterpret_cast<std::uintptr_t>(x.master));
-                    x.weight = reinterpret_cast<const std::uint16_t*>(dw.get() + reinterpret_cast<std::uintptr_t>(x.weight));
-                }
-                for (auto& x : rg) x.words = reinterpret_cast<const std::uint32_t*>(ds.get() + reinterpret_cast<std::uintptr_t>(x.words));
-                dpairs.upload(pr.data(), pr.size() * sizeof(dev::VerifyPair));
-                dranges.upload(rg.data(), rg.size() * sizeof(dev::VerifyRange));
-                cuda_check(dev::launch_verify(dpairs.get<dev::VerifyPair>(), static_cast<std::uint32_t>(pr.size()),
-                                              dranges.get<dev::VerifyRange>(), static_cast<std::uint32_t>(rg.size()),
-                                              derr.get<unsigned long long>() + 3 * r, ls.s),
-                           "verify");
-                cuda_check(cudaStreamSynchronize(ls.s), "verify");
-            }
-        } catch (...) {
-            std::lock_guard<std::mutex> lk(mu);
-            if (!lane_err) lane_err = std::current_exception();
-        }
-    };
-    {
+    const auto run_lanes = [&](int lanes, const std::function<void()>& lane) {
         PhaseTimer pt("verify.shards");
         if (lanes == 1) {
             lane();
@@ -1076,6 +1084,125 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
             for (int i = 0; i < lanes; ++i) pool.emplace_back(lane);
             for (auto& t : pool) t.join();
         }
+    };
+    const auto launch = [&](std::vector<dev::VerifyPair>& pr, std::vector<dev::VerifyRange>& rg, DeviceBuffer& dpairs,
+                            DeviceBuffer& dranges, int r, cudaStream_t st) {
+        dpairs.upload(pr.data(), pr.size() * sizeof(dev::VerifyPair));
+        dranges.upload(rg.data(), rg.size() * sizeof(dev::VerifyRange));
+        cuda_check(dev::launch_verify(dpairs.get<dev::VerifyPair>(), static_cast<std::uint32_t>(pr.size()),
+                                      dranges.get<dev::VerifyRange>(), static_cast<std::uint32_t>(rg.size()),
+                                      derr.get<unsigned long long>() + 3 * r, st),
+                   "verify");
+        cuda_check(cudaStreamSynchronize(st), "verify");
+    };
+    if (resident) {
+        const int lanes = std::clamp<int>(static_cast<int>(std::min<std::uint64_t>((budget - wl.payload_bytes) / max_shard, 8)), 1,
+                                          std::max(1, std::min(N, 8)));
+        const int readers = std::max(1, io_threads() / lanes);
+        const std::uint64_t step = lanes > 1 ? (16ull << 20) : (256ull << 20);
+        {
+            PhaseTimer pt("verify.load_weights");
+            PinnedBuffer stage[2];
+            load_payload(ckpt_file(CkptFile::Weights, dir), wl, dw, stage, io_threads(), step);
+        }
+        run_lanes(lanes, [&] {
+            try {
+                cuda_check(cudaSetDevice(device), "cudaSetDevice");
+                DeviceBuffer ds, dpairs, dranges;
+                PinnedBuffer stage[2];
+                StreamHandle ls;
+                for (int r = next.fetch_add(1); r < N; r = next.fetch_add(1)) {
+                    {
+                        std::lock_guard<std::mutex> lk(mu);
+                        if (lane_err) break;
+                    }
+                    const auto& sl = shard_lay[static_cast<std::size_t>(r)];
+                    load_payload(ckpt_file(CkptFile::Shard, dir, r), sl, ds, stage, readers, step);
+                    auto pr = pairs[static_cast<std::size_t>(r)];
+                    auto rg = ranges[static_cast<std::size_t>(r)];
+                    for (auto& x : pr) {
+                        x.master = reinterpret_cast<const float*>(ds.get() + reinterpret_cast<std::uintptr_t>(x.master));
+                        x.weight = reinterpret_cast<const std::uint16_t*>(dw.get() + reinterpret_cast<std::uintptr_t>(x.weight));
+                    }
+                    for (auto& x : rg)
+                        x.words = reinterpret_cast<const std::uint32_t*>(ds.get() + reinterpret_cast<std::uintptr_t>(x.words));
+                    launch(pr, rg, dpairs, dranges, r, ls.s);
+                }
+            } catch (...) {
+                std::lock_guard<std::mutex> lk(mu);
+                if (!lane_err) lane_err = std::current_exception();
+            }
+        });
+    } else {
+        // window W of shard bytes + up to W/2 of weight bytes per lane
+        const int want = std::max(1, std::min(N, 8));
+        std::uint64_t W = std::min<std::uint64_t>(256ull << 20, budget / (3 * static_cast<std::uint64_t>(want)) * 2);
+        W = std::max<std::uint64_t>(4096, W & ~4095ull);
+        const int lanes = std::clamp<int>(static_cast<int>(budget / (W + W / 2)), 1, want);
+        const int readers = std::max(1, io_threads() / lanes);
+        trace_value("verify.streaming window (MB)", static_cast<double>(W >> 20));
+        run_lanes(lanes, [&] {
+            try {
+                cuda_check(cudaSetDevice(device), "cudaSetDevice");
+                DeviceBuffer A(W), B(W / 2 + 16), dpairs, dranges;
+                PinnedBuffer stage[2];
+                StreamHandle ls;
+                for (int r = next.fetch_add(1); r < N; r = next.fetch_add(1)) {
+                    {
+                        std::lock_guard<std::mutex> lk(mu);
+                        if (lane_err) break;
+                    }
+                    // items by shard payload offset: pairs (master 4 B/elt, weight 2 B/elt) and word ranges
+                    struct Item {
+                        std::uint64_t soff, count, woff;
+                        std::uint32_t kind; // 0 pair, 1 must-be-zero words, 2 must-be-nonnegative floats
+                    };
+                    std::vector<Item> items;
+                    for (const auto& x : pairs[static_cast<std::size_t>(r)])
+                        items.push_back({reinterpret_cast<std::uintptr_t>(x.master), x.count, reinterpret_cast<std::uintptr_t>(x.weight), 0});
+                    for (const auto& x : ranges[static_cast<std::size_t>(r)])
+                        items.push_back({reinterpret_cast<std::uintptr_t>(x.words), x.count, 0, 1 + x.kind});
+                    std::sort(items.begin(), items.end(), [](const Item& a, const Item& b) { return a.soff < b.soff; });
+                    const ContainerLayout& sl = shard_lay[static_cast<std::size_t>(r)];
+                    const fs::path sp = ckpt_file(CkptFile::Shard, dir, r), wp = ckpt_file(CkptFile::Weights, dir);
+                    std::size_t first = 0;
+                    for (std::uint64_t lo = 0; lo < sl.payload_bytes; lo += W) {
+                        const std::uint64_t hi = std::min(sl.payload_bytes, lo + W);
+                        std::vector<dev::VerifyPair> pr;
+                        std::vector<dev::VerifyRange> rg;
+                        std::vector<FileRange> wr;
+                        std::uint64_t bpos = 0;
+                        while (first < items.size() && items[first].soff + 4 * items[first].count <= lo) ++first;
+                        for (std::size_t i = first; i < items.size() && items[i].soff < hi; ++i) {
+                            const Item& it = items[i];
+                            const std::uint64_t a = std::max(lo, it.soff), z = std::min(hi, it.soff + 4 * it.count);
+                            if (a >= z) continue;
+                            const std::uint64_t j0 = (a - it.soff) / 4, n = (z - a) / 4;
+                            if (it.kind == 0) {
+                                const std::uint64_t wo = it.woff + 2 * j0;
+                                if (!wr.empty() && wr.back().file_off + wr.back().bytes == wl.payload_offset() + wo &&
+                                    wr.back().dst + wr.back().bytes == B.get() + bpos) {
+                                    wr.back().bytes += 2 * n;
+                                } else {
+                                    wr.push_back({wl.payload_offset() + wo, 2 * n, B.get() + bpos});
+                                }
+                                pr.push_back({reinterpret_cast<const float*>(A.get() + (a - lo)),
+                                              reinterpret_cast<const std::uint16_t*>(B.get() + bpos), n});
+                                bpos += 2 * n;
+                            } else {
+                                rg.push_back({reinterpret_cast<const std::uint32_t*>(A.get() + (a - lo)), n, it.kind - 1, 0});
+                            }
+                        }
+                        load_ranges(sp, {{sl.payload_offset() + lo, hi - lo, A.get()}}, stage, readers, 16ull << 20, ls.s);
+                        if (!wr.empty()) load_ranges(wp, wr, stage, readers, 16ull << 20, ls.s);
+                        launch(pr, rg, dpairs, dranges, r, ls.s);
+                    }
+                }
+            } catch (...) {
+                std::lock_guard<std::mutex> lk(mu);
+                if (!lane_err) lane_err = std::current_exception();
+            }
+        });
     }
     if (lane_err) std::rethrow_exception(lane_err);
     std::vector<unsigned long long> err(static_cast<std::size_t>(N) * 3);

@@ -47,6 +47,10 @@ class DeviceBuffer {
     int dev_ = 0;
 };
 
+// Device bytes the file-facing paths may plan for: half of (free - 2 GB), capped by
+// TAILOR_DEVICE_BUDGET (bytes; tests use it to force the streaming forms).
+std::uint64_t device_budget();
+
 // Counters of fresh (non-pooled) allocations, printed by TAILOR_TRACE=1.
 struct AllocStats {
     std::mutex mu;

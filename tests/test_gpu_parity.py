@@ -630,3 +630,59 @@ def test_verify_lanes_report_the_damaged_rank(tmp_path, damage):
     assert e.value.kind == kind
     rc, _, err = ref_tool("read", "--dir", bad, check=False)
     assert rc != 0 and ref_name in err
+
+
+KIND_NAMES = {t.ErrorKind.Consistency: "ConsistencyError", t.ErrorKind.CorruptContainer: "CorruptContainer"}
+
+
+@pytest.mark.parametrize("budget", [None, 1 << 14])
+def test_file_paths_stream_under_a_small_device_budget(tmp_path, monkeypatch, budget):
+    """The file-facing paths must not need a whole rank (or the whole weights payload)
+    resident: a 70B-shaped rank partition is 4 x 40 GB of masters for the scorer and
+    160 GB of weights + 120 GB of shard for the re-verify. TAILOR_DEVICE_BUDGET forces
+    the streaming forms at a small shape (pairwise scoring through two slots; verify in
+    4 KB windows with only the paired weight bytes loaded). Scores, selection, merged
+    bytes and error kinds must be those of the resident forms and of the reference."""
+    need_gpu()
+    import shutil
+    import struct
+
+    spec = t.ModelSpec(3, 16, 40, 61, False, 4242)
+    N = 3
+    d = _gen_ref(tmp_path, spec, N, 4)
+    if budget is not None:
+        monkeypatch.setenv("TAILOR_DEVICE_BUDGET", str(budget))
+    rec, src, gap = t.select_recipe(d, 0.5)
+    ref = ref_tool("score", "--snapshots", ",".join(d), "--rho", "0.5")[1]
+    _, scores = t.score_snapshots(d)
+    for p, row in enumerate(ref["scores"]):
+        for m, v in enumerate(row):
+            assert scores[p][m] == pytest.approx(v, rel=SCORE_RTOL)
+    assert rec == t.MergeRecipe.from_json(json.dumps(ref["recipe"]))
+    _both_merge(tmp_path, rec)  # includes the device re-verify in the forced form
+    t.verify_checkpoint(str(tmp_path / "m_ours"))
+    # damage one element of each kind; the verify must name the reference's error kind
+    cases = {"weight": t.ErrorKind.Consistency, "padding": t.ErrorKind.CorruptContainer,
+             "negative_v": t.ErrorKind.Consistency}
+    for damage, kind in cases.items():
+        bad = tmp_path / f"bad_{damage}"
+        shutil.copytree(tmp_path / "m_ours", bad)
+        if damage == "weight":
+            w = bytearray((bad / "model.weights").read_bytes())
+            w[-5] ^= 0x20
+            (bad / "model.weights").write_bytes(bytes(w))
+        else:  # N=3: norm (16 elements) -> chunk 6, rank 2 holds 2 padding elements
+            p = bad / "optim" / ("rank_2.shard" if damage == "padding" else "rank_1.shard")
+            b = bytearray(p.read_bytes())
+            hlen = int.from_bytes(b[:8], "little")
+            hdr = json.loads(b[8:8 + hlen])
+            key = "g0.master" if damage == "padding" else f"g{spec.num_layers + 1}.exp_avg_sq"
+            lo, hi = hdr[key]["data_offsets"]
+            at = 8 + hlen + (hi - 4 if damage == "padding" else lo + 4 * 7)
+            b[at:at + 4] = struct.pack("<f", -2.0 if damage == "negative_v" else 3.0)
+            p.write_bytes(bytes(b))
+        with pytest.raises(t.TailorError) as e:
+            t.verify_checkpoint(str(bad))
+        rc, _, err = ref_tool("read", "--dir", bad, check=False)
+        assert rc != 0 and KIND_NAMES[kind] in err, (damage, err)
+        assert e.value.kind == kind, (damage, err)
