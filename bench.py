@@ -222,6 +222,32 @@ class ClockSampler:
                 "source": "nvml 2 ms" if self.nvml else "nvidia-smi -lms 20"}
 
 
+def read_stream_probe(torch, dev, gib: int = 8, reps: int = 5):
+    """Read-only HBM stream reference for the scorer (which only reads): the library's
+    read probe (tg_read_probe: 8 x 16-B streaming loads in flight per thread, persistent
+    grid) over a buffer far larger than L2, timed with CUDA events, best of `reps`. The
+    measured copy peak counts read+write and is the right denominator for the gather;
+    a read-only kernel can exceed it, so the scorer is also reported against this."""
+    import paper_2602_22158_b200 as t
+
+    x = torch.empty(gib << 30, dtype=torch.uint8, device=dev)
+    sink = torch.zeros(1, dtype=torch.int32, device=dev)
+    s = torch.cuda.current_stream(dev)
+    best = None
+    for _ in range(reps + 1):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        t.read_probe(x.data_ptr(), x.numel(), sink.data_ptr(), s.cuda_stream)
+        b.record(s)
+        torch.cuda.synchronize(dev)
+        ms = a.elapsed_time(b)
+        best = ms if best is None else min(best, ms)
+    gbs = x.numel() / (best / 1e3) / 1e9
+    del x
+    torch.cuda.empty_cache()
+    return round(gbs, 1)
+
+
 def ncu_traffic(kernel: str, workload: str):
     """dram read+write bytes per launch of `kernel` from the committed ncu capture of the
     same workload (profiles/*ncu_summary*.json), or None."""
@@ -453,6 +479,7 @@ def our_arm(args, rank, world, local_rank):
 
     # ---- roofline of the dominant kernel ----------------------------------------------
     hbm, peak_kind = peaks()
+    read_gbs = read_stream_probe(torch, dev) if not args.no_read_probe else None
     g_ms = statistics.mean(kt["gather_shard"])
     s_ms = statistics.mean(kt["score"])
     gather_achieved = 2 * sp0.bytes / (g_ms / 1e3) / 1e9
@@ -487,7 +514,9 @@ def our_arm(args, rank, world, local_rank):
                      "algorithmic_bytes_per_launch": 2 * sp0.bytes,
                      "traffic": traffic, "traffic_source": traffic_src},
         "scorer_roofline": {"achieved": round(score_achieved, 1), "peak": hbm, "unit": "GB/s",
-                            "frac": round(score_achieved / hbm, 4), "bytes_per_launch": scorer.bytes_read},
+                            "frac": round(score_achieved / hbm, 4), "bytes_per_launch": scorer.bytes_read,
+                            "read_stream_probe_gbs": read_gbs,
+                            "frac_of_read_stream": round(score_achieved / read_gbs, 4) if read_gbs else None},
         "gpu_launches": args.steps * (4 if args.host_select else 5),
         "clocks": clocks.summary(),
     }
@@ -734,6 +763,7 @@ def scorer_arm(args, rank, world, local_rank):
     kms = statistics.mean(a.elapsed_time(b) for a, b in recs)
     hbm, peak_kind = peaks()
     achieved = scorer.bytes_read / (kms / 1e3) / 1e9
+    read_gbs = read_stream_probe(torch, dev) if not args.no_read_probe else None
     kname = ("score_staged_kernel<16>" if args.score_variant in (0, 2) else
              "score_partials_kernel<16,2>" if args.score_variant == 4 else "score_partials_kernel<16,4>")
     traffic, src = ncu_traffic(kname, args.workload)
@@ -753,7 +783,9 @@ def scorer_arm(args, rank, world, local_rank):
                    "bytes_per_gpu_step": scorer.bytes_read, "min_boundary_gap": res[3]},
         "roofline": {"bound": "hbm", "kernel": "K3 " + kname, "achieved": round(achieved, 1), "peak": hbm,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_launch": scorer.bytes_read, "traffic": traffic, "traffic_source": src},
+                     "algorithmic_bytes_per_launch": scorer.bytes_read, "traffic": traffic, "traffic_source": src,
+                     "read_stream_probe_gbs": read_gbs,
+                     "frac_of_read_stream": round(achieved / read_gbs, 4) if read_gbs else None},
         "gpu_launches": args.steps * 2, "clocks": clocks.summary()}))
     return 0
 
@@ -1063,6 +1095,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-select", action="store_true", help="select + plan on the host instead of K9")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-read-probe", action="store_true", help="skip the read-only HBM stream probe")
     args = ap.parse_args()
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":

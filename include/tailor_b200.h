@@ -167,6 +167,9 @@ int tg_layer_map(const tg_model_spec* spec, int32_t num_ranks, char* json_out, s
 /* variant: 0 auto, 1 LSU vector path, 2 TMA bulk path (requires bulk_ok). */
 int tg_gather(const tg_gather_seg* d_segs, uint32_t nseg, uint8_t* d_dst, uint64_t dst_bytes, int32_t variant,
               int32_t bulk_ok, void* stream);
+/* Measurement only: a read-only HBM stream over a 16-B aligned device buffer (the
+ * denominator bench.py reports read-only kernels against), XOR-folded into *d_sink. */
+int tg_read_probe(const void* d_src, uint64_t bytes, uint32_t* d_sink, void* stream);
 int tg_score_partials(const tg_score_tile* d_tiles, uint32_t ntiles, const float* const* d_field_base,
                       uint32_t nfields, int32_t K, int32_t vec_ok, double* d_tile_partials, void* stream);
 int tg_score_combine(const double* d_tile_partials, const uint32_t* d_module_tile_begin, int32_t M, int32_t K,

@@ -119,6 +119,7 @@ SIGNATURES = {
     "tg_layer_map": (_I, [_c.POINTER(ModelSpecC), _I32, _c.c_char_p, _SZ, _PSZ]),
     "tg_parse_config": (_I, [_S, _c.POINTER(ModelSpecC)]),
     "tg_gather": (_I, [_P, _U32, _P, _U64, _I32, _I32, _P]),
+    "tg_read_probe": (_I, [_P, _U64, _P, _P]),
     "tg_score_partials": (_I, [_P, _U32, _P, _U32, _I32, _I32, _P, _P]),
     "tg_score_combine": (_I, [_P, _P, _I32, _I32, _P, _P]),
     "tg_family_create": (_P, [_c.POINTER(ModelSpecC), _I32, _I32, _I64]),

@@ -547,6 +547,13 @@ int tg_gather(const tg_gather_seg* d_segs, uint32_t nseg, uint8_t* d_dst, uint64
     });
 }
 
+int tg_read_probe(const void* d_src, uint64_t bytes, uint32_t* d_sink, void* stream) {
+    return guard([&] {
+        cuda_check(dev::launch_read_probe(static_cast<const std::uint8_t*>(d_src), bytes, d_sink, static_cast<cudaStream_t>(stream)),
+                   "tg_read_probe");
+    });
+}
+
 int tg_score_partials(const tg_score_tile* d_tiles, uint32_t ntiles, const float* const* d_field_base, uint32_t nfields,
                       int32_t K, int32_t vec_ok, double* d_tile_partials, void* stream) {
     return guard([&] {

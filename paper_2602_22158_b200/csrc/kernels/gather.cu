@@ -190,7 +190,48 @@ cudaError_t launch_bulk(const GatherSeg* d_segs, std::uint32_t nseg, std::uint8_
 }
 
 
+// Read-only HBM stream reference (measurement only): persistent grid, 8 x 16-B
+// streaming loads in flight per thread, XOR-folded into one word per block so
+// the loads cannot be elided. Gives the denominator for read-only kernels (the
+// scorer), for which the read+write copy peak understates what HBM delivers.
+__global__ void __launch_bounds__(kLsuThreads) read_probe_kernel(const int4* __restrict__ src, std::uint64_t n16,
+                                                                 unsigned int* __restrict__ sink) {
+    int4 acc = make_int4(0, 0, 0, 0);
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * kLsuThreads;
+    std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(kLsuThreads) + threadIdx.x;
+    for (; i + 7 * stride < n16; i += 8 * stride) {
+        int4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = ld_stream(src + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            acc.x ^= v[u].x;
+            acc.y ^= v[u].y;
+            acc.z ^= v[u].z;
+            acc.w ^= v[u].w;
+        }
+    }
+    for (; i < n16; i += stride) {
+        const int4 v = ld_stream(src + i);
+        acc.x ^= v.x;
+        acc.y ^= v.y;
+        acc.z ^= v.z;
+        acc.w ^= v.w;
+    }
+    unsigned int x = static_cast<unsigned int>(acc.x ^ acc.y ^ acc.z ^ acc.w);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0) atomicXor(sink, x);
+}
+
 } // namespace
+
+cudaError_t launch_read_probe(const std::uint8_t* d_src, std::uint64_t bytes, unsigned int* d_sink, cudaStream_t stream) {
+    if (bytes < 16) return cudaSuccess;
+    read_probe_kernel<<<static_cast<unsigned>(sm_count()) * 4, kLsuThreads, 0, stream>>>(reinterpret_cast<const int4*>(d_src),
+                                                                                           bytes / 16, d_sink);
+    return cudaGetLastError();
+}
 
 int sm_count() {
     static const int n = [] {

@@ -37,6 +37,9 @@ enum GatherVariant : int {
 // the segments tile [0, dst_bytes) exactly — the TMA bulk path's contract.
 cudaError_t launch_gather(const GatherSeg* d_segs, std::uint32_t nseg, std::uint8_t* d_dst, std::uint64_t dst_bytes,
                           int variant, bool bulk_ok, cudaStream_t stream);
+// Measurement only: read-only HBM stream over [d_src, d_src + bytes) (16-B aligned),
+// XOR-folded into *d_sink.
+cudaError_t launch_read_probe(const std::uint8_t* d_src, std::uint64_t bytes, unsigned int* d_sink, cudaStream_t stream);
 
 // ---- K3/K4: update-magnitude scorer -----------------------------------------
 // A tile covers `count` consecutive master elements of one field (one group's

@@ -27,7 +27,7 @@ from ._lib import (ErrorKind, GatherSegC, HostCopyC, MergeOptionsC, MergeStatsC,
 __all__ = ["ErrorKind", "TailorError", "ModelSpec", "RecipeSlice", "MergeRecipe", "MergeOptions", "MergeStats",
            "parse_recipe", "recipe_to_yaml", "resolve_plan", "execute_merge", "recipe_from_manifests",
            "verify_checkpoint", "regroup", "train", "score_snapshots", "select_recipe", "layer_map", "SynthFamily", "Scorer",
-           "MergePartition", "SelectStep", "Trainer", "STRATEGIES", "gather"]
+           "MergePartition", "SelectStep", "Trainer", "STRATEGIES", "gather", "read_probe"]
 
 
 @dataclasses.dataclass
@@ -226,6 +226,11 @@ def gather(d_segs_ptr: int, nseg: int, d_dst: int, dst_bytes: int, variant: int 
            stream: int = 0) -> None:
     """Raw K2 launch over a device segment table (tg_gather)."""
     check(lib().tg_gather(d_segs_ptr, nseg, d_dst, dst_bytes, variant, 1 if bulk_ok else 0, stream))
+
+
+def read_probe(d_src: int, nbytes: int, d_sink: int, stream: int = 0) -> None:
+    """Read-only HBM stream over a device buffer (measurement; tg_read_probe)."""
+    check(lib().tg_read_probe(d_src, nbytes, d_sink, stream))
 
 
 class SynthFamily:
