@@ -69,6 +69,9 @@ int guard(F&& f) {
     } catch (const std::exception& e) {
         g_err = std::string("internal error: ") + e.what();
         g_kind = TG_E_INTERNAL;
+    } catch (...) { // nothing may unwind across the C ABI
+        g_err = "internal error: unknown exception";
+        g_kind = TG_E_INTERNAL;
     }
     return g_kind;
 }
