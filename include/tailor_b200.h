@@ -136,6 +136,11 @@ typedef struct tg_train_config {
 } tg_train_config;
 int tg_train(const tg_model_spec* spec, const tg_train_config* config, const char* out_dir,
              int32_t* checkpoints_written);
+/* resume (R/src/trainer.cpp:125-152) on the device: verify a complete fine checkpoint,
+ * continue `additional_steps` steps with its strategy, rank count and per-group
+ * hyperparameters, writing checkpoints + log.jsonl into a fresh out_dir. */
+int tg_resume(const char* checkpoint_dir, int64_t additional_steps, const char* out_dir, int32_t device,
+              int32_t* checkpoints_written);
 /* A resident trainer over rank partitions [rank_begin, rank_end) of a num_ranks layout
  * (one per GPU in a ZeRO job): train_step (R/src/trainer.cpp:26-35) on the device. */
 typedef struct tg_trainer tg_trainer;

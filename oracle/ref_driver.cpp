@@ -288,6 +288,14 @@ json cmd_plan(const Args& a) {
     return {{"recipe", recipe_to_json(recipe_from_manifests(a.str("run"), a.i64("failure-step", 0)))}};
 }
 
+// resume (R/src/trainer.cpp:125-152): continue a complete checkpoint for --steps steps.
+json cmd_resume(const Args& a) {
+    const TrainResult res = resume(a.str("ckpt"), static_cast<int>(a.i64("steps", 0)), a.str("out"));
+    json cks = json::array();
+    for (const auto& c : res.checkpoints) cks.push_back(c.string());
+    return {{"checkpoints", cks}, {"step", res.meta.step}};
+}
+
 json cmd_train(const Args& a) {
     TrainRunConfig cfg;
     cfg.spec = spec_from(a);
@@ -488,7 +496,7 @@ json cmd_read(const Args& a) {
 
 int main(int argc, char** argv) {
     if (argc < 2) {
-        std::cerr << "usage: ref_tool <gen|merge|resolve|plan|train|score|select-merge|verify|read> [--k v ...]\n";
+        std::cerr << "usage: ref_tool <gen|merge|resolve|plan|train|resume|score|select-merge|verify|read|regroup> [--k v ...]\n";
         return 1;
     }
     const std::string cmd = argv[1];
@@ -500,6 +508,7 @@ int main(int argc, char** argv) {
         else if (cmd == "resolve") out = cmd_resolve(a);
         else if (cmd == "plan") out = cmd_plan(a);
         else if (cmd == "train") out = cmd_train(a);
+        else if (cmd == "resume") out = cmd_resume(a);
         else if (cmd == "score") out = cmd_score(a);
         else if (cmd == "select-merge") out = cmd_select_merge(a);
         else if (cmd == "verify") out = cmd_verify(a);

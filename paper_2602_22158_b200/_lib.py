@@ -108,6 +108,7 @@ SIGNATURES = {
     "tg_verify_checkpoint": (_I, [_S, _I32]),
     "tg_regroup": (_I, [_S, _S, _I32, _c.POINTER(MergeOptionsC), _c.POINTER(MergeStatsC)]),
     "tg_train": (_I, [_c.POINTER(ModelSpecC), _c.POINTER(TrainConfigC), _S, _c.POINTER(_I32)]),
+    "tg_resume": (_I, [_S, _I64, _S, _I32, _c.POINTER(_I32)]),
     "tg_trainer_create": (_P, [_c.POINTER(ModelSpecC), _I32, _I32, _I32, _D, _D, _I32]),
     "tg_trainer_destroy": (None, [_P]),
     "tg_trainer_elements": (_U64, [_P]),

@@ -449,6 +449,13 @@ tg_trainer* tg_trainer_create(const tg_model_spec* spec, int32_t num_ranks, int3
 void tg_trainer_destroy(tg_trainer* t) { delete t; }
 uint64_t tg_trainer_elements(const tg_trainer* t) { return t->tr->elements(); }
 
+int tg_resume(const char* checkpoint_dir, int64_t additional_steps, const char* out_dir, int32_t device, int32_t* written) {
+    return guard([&] {
+        const auto dirs = device_resume(checkpoint_dir ? checkpoint_dir : "", additional_steps, out_dir ? out_dir : "", device);
+        if (written) *written = static_cast<int32_t>(dirs.size());
+    });
+}
+
 int tg_trainer_step(tg_trainer* t, int64_t step, double* gn, double* un) {
     return guard([&] {
         const auto [g, u] = t->tr->step(step);

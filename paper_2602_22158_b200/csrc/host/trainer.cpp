@@ -5,12 +5,15 @@
 #include <cstdlib>
 #include <cmath>
 #include <fstream>
+#include <unistd.h>
+#include <fcntl.h>
 #include <map>
 #include <set>
 
 #include <json.hpp>
 
 #include "tailor/errors.hpp"
+#include "tailor/io.hpp"
 
 namespace tailor {
 
@@ -103,6 +106,7 @@ DeviceTrainer::DeviceTrainer(const ModelSpec& spec, int num_ranks, const AdamHyp
     r0_ = rank_begin;
     r1_ = rank_end < 0 ? num_ranks : rank_end;
     if (r0_ < 0 || r1_ > num_ranks || r0_ >= r1_) fail(ErrorKind::Geometry, "bad rank range for the trainer");
+    for (const auto& g : model_.table().groups) hyper_.push_back(hyper_for_class(base_, g.decay));
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
     cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
     full_ = checkpoint_layout(model_, N_, model_.modules());
@@ -204,6 +208,41 @@ DeviceTrainer::~DeviceTrainer() {
 
 std::uint64_t DeviceTrainer::elements() const { return elements_; }
 
+void DeviceTrainer::load(const fs::path& dir, const CheckpointSummary& s) {
+    if (s.optim.grouping != Grouping::Fine)
+        fail(ErrorKind::Geometry, "the device trainer resumes fine-grouped checkpoints; convert with `tailor regroup --to fine`");
+    if (s.optim.num_ranks != N_ || !s.spec.same_geometry(model_.spec()))
+        fail(ErrorKind::Geometry, "checkpoint geometry does not match the trainer");
+    for (const auto& g : s.optim.groups) hyper_.at(static_cast<std::size_t>(g.index)) = g.hyper;
+    PinnedBuffer stage;
+    for (int r = r0_; r < r1_; ++r) {
+        const fs::path p = ckpt_file(CkptFile::Shard, dir, r);
+        const ContainerLayout lay = read_layout(p);
+        const ContainerLayout& want = full_.shards[static_cast<std::size_t>(r)];
+        if (lay.payload_bytes != want.payload_bytes || lay.entries.size() != want.entries.size())
+            fail(ErrorKind::Geometry, p.string() + ": shard layout does not match a complete fine checkpoint");
+        for (std::size_t i = 0; i < lay.entries.size(); ++i)
+            if (lay.entries[i].name != want.entries[i].name || lay.entries[i].begin != want.entries[i].begin ||
+                lay.entries[i].bytes() != want.entries[i].bytes())
+                fail(ErrorKind::Geometry, p.string() + ": shard layout does not match a complete fine checkpoint");
+        // the rank partition IS the file payload (same keys, same order)
+        stage.resize(std::max<std::uint64_t>(16, lay.payload_bytes));
+        const int fd = ::open(p.c_str(), O_RDONLY);
+        if (fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + p.string() + "'");
+        try {
+            run_reads({{fd, stage.get(), lay.payload_bytes, lay.payload_offset()}}, io_threads(), p.string());
+        } catch (...) {
+            ::close(fd);
+            throw;
+        }
+        ::close(fd);
+        auto& rk = ranks_[static_cast<std::size_t>(r - r0_)];
+        cuda_check(cudaMemcpyAsync(rk->part.get(), stage.get(), lay.payload_bytes, cudaMemcpyHostToDevice, stream_), "H2D");
+        cuda_check(cudaStreamSynchronize(stream_), "sync");
+    }
+    t_ = s.trainer.optimizer_t;
+}
+
 std::pair<std::uint8_t*, std::uint64_t> DeviceTrainer::partition(int rank) {
     if (rank < r0_ || rank >= r1_) fail(ErrorKind::Geometry, "rank " + std::to_string(rank) + " is not held by this trainer");
     cuda_check(cudaStreamSynchronize(stream_), "sync");
@@ -231,7 +270,7 @@ std::pair<double, double> DeviceTrainer::step(std::int64_t s) {
     t_ += 1;
     std::vector<dev::AdamCoef> coef(static_cast<std::size_t>(model_.table().group_count()));
     for (const auto& g : model_.table().groups) {
-        const AdamHyperparams h = hyper_for_class(base_, g.decay);
+        const AdamHyperparams& h = hyper_[static_cast<std::size_t>(g.index)];
         dev::AdamCoef& c = coef[static_cast<std::size_t>(g.index)];
         c.b1 = static_cast<float>(h.beta1);
         c.one_minus_b1 = static_cast<float>(1.0 - h.beta1);
@@ -320,7 +359,7 @@ void DeviceTrainer::save(const fs::path& dir, const TrainerMeta& meta, const std
         write_container_file(ckpt_file(CkptFile::Shard, dir, r), sl, host);
     }
     std::map<int, AdamHyperparams> hyp;
-    for (int g : lay.groups) hyp[g] = hyper_for_class(base_, model_.table().groups[static_cast<std::size_t>(g)].decay);
+    for (int g : lay.groups) hyp[g] = hyper_[static_cast<std::size_t>(g)];
     SaveManifest man;
     man.step = meta.step;
     man.strategy = label;
@@ -423,6 +462,48 @@ std::vector<fs::path> device_train(const DeviceTrainConfig& cfg, const fs::path&
         const fs::path dir = out_dir / dir_of_step(s);
         tr.save(dir, meta, mods, cfg.magnitude ? "magnitude" : strategy_kind_name(cfg.strategy.kind));
         if (cfg.magnitude) tr.keep_masters();
+        saved.push_back(dir);
+    }
+    log.flush();
+    if (!log) fail(ErrorKind::Storage, "log write failed");
+    return saved;
+}
+
+std::vector<fs::path> device_resume(const fs::path& checkpoint_dir, std::int64_t additional_steps, const fs::path& out_dir,
+                                    int device) {
+    if (additional_steps < 0) fail(ErrorKind::Recipe, "additional_steps must be >= 0");
+    // read_checkpoint: the full structural + payload verification, on the device
+    verify_checkpoint_dir(checkpoint_dir.string(), device);
+    const CheckpointSummary s = read_checkpoint_summary(checkpoint_dir);
+    std::string missing;
+    for (const auto& m : enumerate_modules(s.spec))
+        if (!s.manifest.contains(m)) missing += (missing.empty() ? "" : ", ") + module_name(m);
+    if (!missing.empty())
+        fail(ErrorKind::MissingModules, "checkpoint '" + checkpoint_dir.string() + "' is partial (missing " + missing +
+                                            "); assemble a complete checkpoint with the merge command first");
+    if (s.trainer.rng_seed != s.spec.seed) fail(ErrorKind::Consistency, "trainer rng_seed disagrees with the model config seed");
+    std::error_code ec;
+    if (fs::exists(out_dir) && !fs::is_empty(out_dir, ec))
+        fail(ErrorKind::Storage, "refusing to write into non-empty directory '" + out_dir.string() + "'");
+    DeviceTrainer tr(s.spec, s.optim.num_ranks, AdamHyperparams{}, device);
+    tr.load(checkpoint_dir, s);
+    fs::create_directories(out_dir, ec);
+    if (ec) fail(ErrorKind::Storage, "cannot create '" + out_dir.string() + "': " + ec.message());
+    std::ofstream log(out_dir / "log.jsonl", std::ios::binary);
+    if (!log) fail(ErrorKind::Storage, "cannot create log in '" + out_dir.string() + "'");
+    TrainerMeta meta = s.trainer;
+    const StrategyConfig strategy = s.trainer.strategy;
+    std::vector<fs::path> saved;
+    for (std::int64_t st = s.trainer.step + 1; st <= s.trainer.step + additional_steps; ++st) {
+        const auto [gn, un] = tr.step(st);
+        log << nlohmann::json{{"grad_norm", gn}, {"step", st}, {"update_norm", un}}.dump() << "\n";
+        meta.step = st;
+        meta.optimizer_t = tr.optimizer_t();
+        if (st % strategy.interval != 0) continue;
+        meta.checkpoint_counter = st / strategy.interval;
+        const auto mods = modules_to_save(strategy, s.spec, meta.checkpoint_counter);
+        const fs::path dir = out_dir / dir_of_step(st);
+        tr.save(dir, meta, mods, strategy_kind_name(strategy.kind));
         saved.push_back(dir);
     }
     log.flush();

@@ -54,6 +54,10 @@ class DeviceTrainer {
     void keep_masters();
     std::vector<std::pair<double, double>> score_against_kept();
     const ModelLayout& model() const { return model_; }
+    // resume (R/src/trainer.cpp:125-152): replace the state with a complete fine
+    // checkpoint's (rank payloads byte for byte, per-group hyperparameters from its
+    // optim_meta, the optimizer step counter); the caller has verified it.
+    void load(const std::filesystem::path& dir, const CheckpointSummary& s);
     // Device partition of rank r (payload layout of optim/rank_r.shard) and its
     // size, for in-situ consumers (scorers, diagnostics); synchronizes first.
     std::pair<std::uint8_t*, std::uint64_t> partition(int rank);
@@ -73,10 +77,17 @@ class DeviceTrainer {
     // Pass 2 recomputes the gradient (28 B/element) unless TAILOR_TRAIN_STORE_GRAD=1
     // selects the scratch-buffer variant (36 B/element; kept for comparison).
     bool store_grad_ = false;
+    std::vector<AdamHyperparams> hyper_; // per group (GroupState::hyper)
 };
 
 // The reference's train() (R/src/trainer.cpp:109-123) on the device: same run
 // directory layout, checkpoints byte-identical for full/parity/filter.
 std::vector<std::filesystem::path> device_train(const DeviceTrainConfig& cfg, const std::filesystem::path& out_dir);
+
+// The reference's resume() (R/src/trainer.cpp:125-152) on the device: read + verify a
+// complete fine checkpoint, continue `additional_steps` steps with its strategy and
+// rank count, writing checkpoints and log.jsonl into a fresh out_dir.
+std::vector<std::filesystem::path> device_resume(const std::filesystem::path& checkpoint_dir, std::int64_t additional_steps,
+                                                 const std::filesystem::path& out_dir, int device);
 
 } // namespace tailor

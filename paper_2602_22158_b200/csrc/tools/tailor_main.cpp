@@ -9,6 +9,7 @@
 //   tailor score  --snapshots A,B,... [--device D]
 //   tailor check  --ckpt DIR [--device D]
 //   tailor regroup --ckpt DIR --out DIR [--to fine|coarse] [--device D] [--no-verify]
+//   tailor resume --ckpt DIR --steps S --out RUN [--device D]
 //   tailor train  --config c.json --steps S --interval I --strategy full|parity|filter|magnitude
 //                 --ranks N --out RUN [--lr --weight-decay --head --tail --sparse-multiple --rho --device]
 // Exit codes: 0 success, 1 user error, 2 internal/consistency error.
@@ -213,6 +214,18 @@ int cmd_train(const Args& a) {
     return 0;
 }
 
+// R/tools/tailor_main.cpp:105-110 (`resume --ckpt --steps --out`), on the device.
+int cmd_resume(const Args& a) {
+    if (!require(a, {"ckpt", "steps", "out"})) return 1;
+    const int device = a.kv.count("device") ? std::stoi(a.kv.at("device")) : 0;
+    const int steps = std::stoi(a.kv.at("steps"));
+    int32_t written = 0;
+    if (int rc = tg_resume(a.kv.at("ckpt").c_str(), steps, a.kv.at("out").c_str(), device, &written); rc != TG_OK)
+        return report(rc);
+    std::cout << "resumed from " << a.kv.at("ckpt") << " for " << steps << " steps\n";
+    return 0;
+}
+
 int cmd_regroup(const Args& a) {
     if (!require(a, {"ckpt", "out"})) return 1;
     const std::string to = a.kv.count("to") ? a.kv.at("to") : "fine";
@@ -244,7 +257,7 @@ int cmd_check(const Args& a) {
 
 int main(int argc, char** argv) {
     if (argc < 2) {
-        std::cerr << "usage: tailor <merge|plan|select|score|check> [options]\n";
+        std::cerr << "usage: tailor <merge|plan|select|score|check|regroup|train|resume> [options]\n";
         return 1;
     }
     Args a;
@@ -267,6 +280,7 @@ int main(int argc, char** argv) {
         if (cmd == "check") return cmd_check(a);
         if (cmd == "regroup") return cmd_regroup(a);
         if (cmd == "train") return cmd_train(a);
+        if (cmd == "resume") return cmd_resume(a);
     } catch (const std::exception& e) {
         std::cerr << "error: " << e.what() << "\n";
         return 1;

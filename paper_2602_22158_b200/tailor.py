@@ -26,7 +26,7 @@ from ._lib import (ErrorKind, GatherSegC, HostCopyC, MergeOptionsC, MergeStatsC,
 
 __all__ = ["ErrorKind", "TailorError", "ModelSpec", "RecipeSlice", "MergeRecipe", "MergeOptions", "MergeStats",
            "parse_recipe", "recipe_to_yaml", "resolve_plan", "execute_merge", "recipe_from_manifests",
-           "verify_checkpoint", "regroup", "train", "score_snapshots", "select_recipe", "layer_map", "SynthFamily", "Scorer",
+           "verify_checkpoint", "regroup", "train", "resume", "score_snapshots", "select_recipe", "layer_map", "SynthFamily", "Scorer",
            "MergePartition", "SelectStep", "Trainer", "STRATEGIES", "gather", "read_probe"]
 
 
@@ -175,6 +175,14 @@ def train(spec: ModelSpec, out_dir: str, steps: int, interval: int = 50, strateg
                        weight_decay, rho)
     n = ctypes.c_int32(0)
     check(lib().tg_train(ctypes.byref(c), ctypes.byref(cfg), _b(str(out_dir)), ctypes.byref(n)))
+    return n.value
+
+
+def resume(checkpoint_dir: str, steps: int, out_dir: str, device: int = 0) -> int:
+    """Device resume() (R/src/trainer.cpp:125-152) from a complete fine checkpoint ->
+    number of checkpoints written into out_dir."""
+    n = ctypes.c_int32(0)
+    check(lib().tg_resume(_b(str(checkpoint_dir)), steps, _b(str(out_dir)), device, ctypes.byref(n)))
     return n.value
 
 

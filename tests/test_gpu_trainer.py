@@ -169,3 +169,60 @@ def test_nonfinite_gradient_leaves_state_untouched(monkeypatch, store_grad, pois
     s2.view(torch.float32)[lo // 4] = poison
     _d2d(p2, s2.data_ptr(), n)
     tr2.step(2)
+
+
+@pytest.mark.parametrize("strategy,ranks", [("parity", 2), ("filter", 3), ("full", 1)])
+def test_resume_from_merged_composite_matches_reference(tmp_path, strategy, ranks):
+    """Acceptance c5 (R/tests/acceptance.cpp:256-303) on the device: the reference trains
+    with a partial-checkpoint strategy and fails at 110; the composite is planned
+    (recipe_from_manifests) and merged (our execute_merge); then `resume` continues 100
+    steps from it — our device resume and the reference's resume write byte-identical
+    checkpoints (log norms within 1e-9), and the CLI does the same."""
+    need_gpu()
+    import subprocess
+
+    spec = dict(num_layers=4, hidden_dim=8, ffn_dim=16, vocab_size=32, weight_tied=False, seed=31415)
+    extra = ["--head", 1, "--tail", 1, "--sparse-multiple", 2] if strategy == "filter" else []
+    ref_tool("train", *spec_args(spec), "--strategy", strategy, "--steps", 100, "--interval", 25, "--ranks", ranks,
+             *extra, "--out", tmp_path / "run", "--fail-at", 110)
+    recipe = t.recipe_from_manifests(str(tmp_path / "run"), 110)
+    t.execute_merge(recipe, str(tmp_path / "merged"))
+    ref_tool("resume", "--ckpt", tmp_path / "merged", "--steps", 100, "--out", tmp_path / "ref_res")
+    n = t.resume(str(tmp_path / "merged"), 100, str(tmp_path / "our_res"))
+    assert n == 4
+    same_tree(tmp_path / "ref_res", tmp_path / "our_res")
+    logs_close(tmp_path / "ref_res", tmp_path / "our_res")
+    r = subprocess.run([str(t._lib.CLI_PATH), "resume", "--ckpt", str(tmp_path / "merged"), "--steps", "100", "--out",
+                        str(tmp_path / "cli_res")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    same_tree(tmp_path / "ref_res", tmp_path / "cli_res")
+
+
+def test_resume_errors_match_reference(tmp_path):
+    """resume's contract: partial checkpoints -> MissingModules (exit 1), a non-empty output
+    directory -> StorageError (exit 2), negative steps -> RecipeError."""
+    need_gpu()
+    import subprocess
+
+    spec = dict(num_layers=2, hidden_dim=8, ffn_dim=16, vocab_size=32, weight_tied=False, seed=7)
+    ref_tool("train", *spec_args(spec), "--strategy", "parity", "--steps", 50, "--interval", 25, "--ranks", 2,
+             "--out", tmp_path / "run")
+    partial = tmp_path / "run" / "checkpoint-50"
+    rc, _, err = ref_tool("resume", "--ckpt", partial, "--steps", 10, "--out", tmp_path / "r1", check=False)
+    with pytest.raises(t.TailorError) as e:
+        t.resume(str(partial), 10, str(tmp_path / "o1"))
+    assert e.value.kind == t.ErrorKind.MissingModules and rc == 1 and "MissingModules" in err
+    full = tmp_path / "full"
+    ref_tool("train", *spec_args(spec), "--strategy", "full", "--steps", 25, "--interval", 25, "--ranks", 2,
+             "--out", full)
+    (tmp_path / "busy").mkdir()
+    (tmp_path / "busy" / "x").write_text("x")
+    with pytest.raises(t.TailorError) as e:
+        t.resume(str(full / "checkpoint-25"), 10, str(tmp_path / "busy"))
+    assert e.value.kind == t.ErrorKind.Storage
+    r = subprocess.run([str(t._lib.CLI_PATH), "resume", "--ckpt", str(full / "checkpoint-25"), "--steps", "5", "--out",
+                        str(tmp_path / "busy")], capture_output=True, text=True)
+    assert r.returncode == 2 and "StorageError" in r.stderr
+    with pytest.raises(t.TailorError) as e:
+        t.resume(str(full / "checkpoint-25"), -1, str(tmp_path / "o2"))
+    assert e.value.kind == t.ErrorKind.Recipe
