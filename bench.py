@@ -195,31 +195,43 @@ class ClockSampler:
             self.reader.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            if self.nvml:  # "<unix time> idx, sm, max, ..." : keep the samples inside the region
-                ts, _, ln = ln.partition(" ")
-                try:
-                    if not self.t0 <= float(ts) <= self.t1:
+
+        def collect(lo, hi):
+            sm, mx, reasons = [], [], set()
+            for ln in self.lines:
+                if self.nvml:  # "<unix time> idx, sm, max, ..." : keep the samples inside [lo, hi]
+                    ts, _, ln = ln.partition(" ")
+                    try:
+                        if not lo <= float(ts) <= hi:
+                            continue
+                    except ValueError:
                         continue
+                parts = [x.strip() for x in ln.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx.append(float(parts[2]))
                 except ValueError:
                     continue
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx.append(float(parts[2]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
+                for n, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+            return sm, mx, reasons
+
+        sm, mx, reasons = collect(self.t0, self.t1)
+        widened = False
+        if not sm and self.nvml:  # region shorter than the poll period: nearest samples around it
+            sm, mx, reasons = collect(self.t0 - 0.01, self.t1 + 0.01)
+            widened = True
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm),
-                "source": "nvml 2 ms" if self.nvml else "nvidia-smi -lms 20"}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm),
+               "source": "nvml 2 ms" if self.nvml else "nvidia-smi -lms 20"}
+        if widened:
+            out["window"] = f"timed region {1e3 * (self.t1 - self.t0):.2f} ms < poll period: samples within 10 ms of it"
+        return out
 
 
 def read_stream_probe(torch, dev, gib: int = 8, reps: int = 5):
