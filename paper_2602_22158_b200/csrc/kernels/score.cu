@@ -180,20 +180,30 @@ __global__ void score_combine_kernel(const double* __restrict__ partials, const 
 // tile -> partial contract (one partial per tile, fixed order); the summation
 // order inside a tile differs from the register kernel, so the two variants
 // agree to ~1e-15, not bitwise.
-constexpr int kChunkElems = 4 * kScoreThreads; // one float4 per consumer thread per snapshot row
 constexpr int kStagedSmem = 192 * 1024;
 constexpr int kStagedThreads = kScoreThreads + 32; // 8 consumer warps + 1 producer warp
 
+// float4 per consumer thread per snapshot row in one stage: small K gets wider
+// stages (>= 16 KB), so the single producer lane issues few enough of them.
+template <int K>
+__host__ __device__ constexpr int staged_rows() {
+    return K >= 4 ? 1 : (K == 3 ? 2 : 4);
+}
+template <int K>
+__host__ __device__ constexpr int chunk_elems() {
+    return 4 * kScoreThreads * staged_rows<K>();
+}
+
 template <int K>
 __host__ __device__ constexpr int staged_stages() {
-    constexpr int per = K * kChunkElems * 4;
+    constexpr int per = K * chunk_elems<K>() * 4;
     constexpr int s = kStagedSmem / per;
     return s < 2 ? 2 : (s > 8 ? 8 : s);
 }
 
 template <int K>
 __host__ __device__ constexpr std::size_t staged_smem_bytes() {
-    return static_cast<std::size_t>(staged_stages<K>()) * K * kChunkElems * 4 + 16 * staged_stages<K>();
+    return static_cast<std::size_t>(staged_stages<K>()) * K * chunk_elems<K>() * 4 + 16 * staged_stages<K>();
 }
 
 template <int K>
@@ -213,6 +223,8 @@ __global__ void __launch_bounds__(kStagedThreads, 1) score_staged_kernel(const S
     using namespace tma;
     constexpr int S = staged_stages<K>();
     constexpr int V = 2 * (K - 1);
+    constexpr int kChunkElems = chunk_elems<K>();
+    constexpr int R = staged_rows<K>();
     extern __shared__ __align__(128) float ring[];
     std::uint64_t* full = reinterpret_cast<std::uint64_t*>(ring + S * K * kChunkElems);
     std::uint64_t* empty = full + S;
@@ -264,15 +276,18 @@ __global__ void __launch_bounds__(kStagedThreads, 1) score_staged_kernel(const S
             mbar_wait_parity(&full[stage], (item / S) & 1u);
             const std::uint32_t n = min(static_cast<std::uint32_t>(kChunkElems), t.count - start);
             const std::uint32_t n4 = n & ~3u;
-            const std::uint32_t e = static_cast<std::uint32_t>(tid) * 4u;
-            if (e < n4) {
-                const float* row = ring + stage * K * kChunkElems + e;
-                float4 prev = *reinterpret_cast<const float4*>(row);
 #pragma unroll
-                for (int k = 1; k < K; ++k) {
-                    const float4 cur = *reinterpret_cast<const float4*>(row + k * kChunkElems);
-                    accumulate4<K>(acc, k - 1, prev, cur);
-                    prev = cur;
+            for (int rr = 0; rr < R; ++rr) {
+                const std::uint32_t e = (static_cast<std::uint32_t>(rr) * kScoreThreads + static_cast<std::uint32_t>(tid)) * 4u;
+                if (e < n4) {
+                    const float* row = ring + stage * K * kChunkElems + e;
+                    float4 prev = *reinterpret_cast<const float4*>(row);
+#pragma unroll
+                    for (int k = 1; k < K; ++k) {
+                        const float4 cur = *reinterpret_cast<const float4*>(row + k * kChunkElems);
+                        accumulate4<K>(acc, k - 1, prev, cur);
+                        prev = cur;
+                    }
                 }
             }
             __syncwarp();

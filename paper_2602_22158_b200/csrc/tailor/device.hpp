@@ -64,11 +64,12 @@ enum ScoreVariant : int { kScoreAuto = 0, kScoreRegister = 1, kScoreStaged = 2, 
 constexpr int kNarrowMinK = 1 << 20;
 // Staged = warp-specialised TMA ring (producer warp + 8 consumer warps, full/empty
 // mbarriers). Measured on B200 (bench events, fraction of the 6543 GB/s copy peak):
-// K=16 1.093 vs register 0.951; K=4 1.075 vs 1.064; but K=2 0.71 vs 1.00 (cfg2: 1.83 vs
-// 1.28 ms — 8 KB stages need ~6 stages/us per SM from one producer lane, more than
-// it issues; a deeper ring did not help) -> auto picks it for K >= 4 when the bases
-// are 16-B aligned. (Its first version, one CTA-wide barrier per chunk, was
-// barrier-bound: 0.88 / 0.61.)
+// K=16 1.093 vs register 0.951; K=4 1.075 vs 1.064. At K=2 its first form lost (cfg2:
+// 1.83 vs 1.28 ms: 8 KB stages need ~6 stages/us per SM from one producer lane; a deeper
+// ring did not help); with 4 float4 rows per thread per stage (32 KB stages) it ties the
+// register kernel (1.30 vs 1.27 ms) -> auto picks it for K >= 4 when the bases are 16-B
+// aligned. (Its very first version, one CTA-wide barrier per chunk, was barrier-bound:
+// 0.88 / 0.61.)
 constexpr int kStagedMinK = 4;
 cudaError_t launch_score_partials(const ScoreTile* d_tiles, std::uint32_t ntiles, const float* const* d_field_base,
                                   std::uint32_t nfields, int K, bool vec_ok, double* d_tile_partials, cudaStream_t stream,
