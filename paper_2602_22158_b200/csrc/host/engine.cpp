@@ -67,8 +67,13 @@ struct DevicePool {
     std::map<int, std::multimap<std::size_t, void*>> free_; // device -> size class -> block
     std::map<int, std::size_t> pooled;
 
+    // TAILOR_DEVICE_POOL=0 turns pooling off (plain cudaMalloc / cudaFree), for comparisons
+    const bool enabled = [] {
+        const char* v = std::getenv("TAILOR_DEVICE_POOL");
+        return !(v && *v == '0');
+    }();
     void* take(int dev, std::size_t n, std::size_t* got) {
-        const std::size_t sz = n <= kMaxBlock ? pool_size_class(n) : n;
+        const std::size_t sz = enabled && n <= kMaxBlock ? pool_size_class(n) : n;
         if (sz <= kMaxBlock) {
             std::lock_guard<std::mutex> lk(mu);
             auto& f = free_[dev];
@@ -92,7 +97,7 @@ struct DevicePool {
         int cur = 0;
         cudaGetDevice(&cur);
         if (cur != dev) cudaSetDevice(dev);
-        if (sz > kMaxBlock) {
+        if (sz > kMaxBlock || !enabled) {
             cudaFree(p);
         } else {
             cudaDeviceSynchronize();
