@@ -1041,6 +1041,7 @@ def files_arm(args):
         dirs = [str(work / "run" / f"checkpoint-{k * 100}") for k in range(1, K + 1)]
         for k in range(1, K + 1):
             fam.write_dir(k, dirs[k - 1])
+        os.sync()  # flush the sources now: background writeback of them would land inside timed steps
         ours, refs, comp, step_ms = [], [], 0, []
         for i in range(args.warmup + args.steps):
             out = work / f"ours-{i}"

@@ -21,6 +21,7 @@ try:
     dirs = [str(work / f"checkpoint-{k * 100}") for k in range(1, 5)]
     for k in range(1, 5):
         fam.write_dir(k, dirs[k - 1])
+    os.sync()
     def dirty():
         with open("/proc/meminfo") as f:
             kv = dict(line.split(":", 1) for line in f)
