@@ -306,6 +306,11 @@ def run_reference_sample(workdir: pathlib.Path, workers: int):
     return dt, composite, detail
 
 
+# The headline metric (BASELINE.json: composite-checkpoint merge GB/s vs HBM roofline);
+# both arms print the same string so the driver pairs them.
+MERGE_METRIC = "composite-checkpoint merge GB/s (score+select+merge) vs HBM roofline"
+
+
 def reference_arm(args, rank, world):
     if rank != 0:
         return 0
@@ -329,7 +334,7 @@ def reference_arm(args, rank, world):
     L, h, f, v, tied, N, K, rho = SAMPLE
     sample = (f"reference select-merge (read_checkpoint + FP64 scorer + resolve_plan + execute_merge with re-verify, "
               f"files in /tmp) on L{L} h{h} f{f} v{v} N{N} K{K} rho{rho}: {comp / 1e9:.3f} GB composite per step")
-    line = {"metric": "composite-checkpoint merge GB/s (score+select+merge)", "value": round(value, 4),
+    line = {"metric": MERGE_METRIC, "value": round(value, 4),
             "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8/f32/f64", "data": "synthetic",
@@ -502,7 +507,7 @@ def our_arm(args, rank, world, local_rank):
     if rank != 0:
         return 0
     line = {
-        "metric": "composite-checkpoint merge GB/s (score+select+merge) vs HBM roofline",
+        "metric": MERGE_METRIC,
         "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8 (payload bytes) / f32->f64 (scores)", "data": "synthetic",
