@@ -256,7 +256,7 @@ void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<st
                                     std::to_string(budget) + " B available");
     const int lanes = std::clamp<int>(static_cast<int>(std::min<std::uint64_t>(budget / per_lane, 8)), 1, std::min(N, 8));
     const int readers = std::max(1, io_threads() / lanes);
-    trace_value(pairwise ? "score.lanes (pairwise)" : "score.lanes", lanes);
+    trace_count(pairwise ? "score.lanes (pairwise)" : "score.lanes", lanes);
     const std::size_t nres = static_cast<std::size_t>(K - 1) * M * 2;
     std::vector<std::vector<double>> res(static_cast<std::size_t>(N), std::vector<double>(nres));
     std::atomic<int> next{0};

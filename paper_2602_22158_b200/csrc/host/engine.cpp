@@ -1145,7 +1145,7 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
         W = std::max<std::uint64_t>(4096, W & ~4095ull);
         const int lanes = std::clamp<int>(static_cast<int>(budget / (W + W / 2)), 1, want);
         const int readers = std::max(1, io_threads() / lanes);
-        trace_value("verify.streaming window (MB)", static_cast<double>(W >> 20));
+        trace_count("verify.streaming window (MB)", static_cast<double>(W >> 20));
         run_lanes(lanes, [&] {
             try {
                 cuda_check(cudaSetDevice(device), "cudaSetDevice");

@@ -373,7 +373,7 @@ AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool u
         tot.write_ms += x.write_ms;
         tot.bytes += x.bytes;
     }
-    trace_value("assemble.lanes", lanes);
+    trace_count("assemble.lanes", lanes);
     trace_value("assemble.read (sum over lanes)", tot.read_ms);
     trace_value("assemble.wait (sum over lanes)", tot.wait_ms);
     trace_value("assemble.write (sum over lanes)", tot.write_ms);

@@ -42,6 +42,10 @@ ScopedAccum::~ScopedAccum() { sink_ += now_ms() - t0_; }
 bool trace_enabled() { return trace_on(); }
 double clock_ms() { return now_ms(); }
 
+void trace_count(const char* name, double count) {
+    if (trace_on()) std::fprintf(stderr, "[tailor] %s %g\n", name, count);
+}
+
 void trace_value(const char* name, double ms) {
     if (trace_on()) std::fprintf(stderr, "[tailor] %s %.2f ms\n", name, ms);
 }

@@ -50,8 +50,9 @@ class ScopedAccum {
     double& sink_;
     double t0_;
 };
-// Prints "[tailor] <name> <ms>" when TAILOR_TRACE=1.
+// Prints "[tailor] <name> <ms> ms" / "[tailor] <name> <count>" when TAILOR_TRACE=1.
 void trace_value(const char* name, double ms);
+void trace_count(const char* name, double count);
 bool trace_enabled();
 // Monotonic clock in ms (for phase breakdowns).
 double clock_ms();
