@@ -443,18 +443,50 @@ def our_arm(args, rank, world, local_rank):
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    recs = []
-    with ClockSampler(local_rank) as clocks:
+
+    # One step as a CUDA graph (score -> K9 select/plan -> shard gather -> weights gather:
+    # 5 kernel nodes, no host work), replayed per step: the launch gaps of the eager
+    # step disappear (they matter at cfg1, where a step is ~0.17 ms). Single-GPU only
+    # (the all-gather stays eager); the eager pass below still gives the per-kernel times.
+    graph, graph_note = None, None
+    if world == 1 and not args.host_select and not args.no_graph:
+        try:
+            cs = torch.cuda.Stream(dev)
+            cs.wait_stream(stream)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cs):
+                scorer.run(bases, partials.data_ptr(), cs.cuda_stream)
+                for ph in (1, 2, 4):
+                    dstep.run(partials.data_ptr(), 1, out_shard.data_ptr(), out_w.data_ptr(), args.variant,
+                              cs.cuda_stream, phases=ph)
+            torch.cuda.synchronize(dev)
+            graph = g
+        except Exception as exc:  # capture unsupported here: the eager step is the measurement
+            graph_note = f"graph capture failed ({type(exc).__name__}: {exc}); eager step timed"
+            torch.cuda.synchronize(dev)
+
+    def timed(fn):
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
         start, end = ev(), ev()
         start.record(stream)
         for _ in range(args.steps):
-            step(recs)
+            fn()
         end.record(stream)
         torch.cuda.synchronize(dev)
-    total_ms = start.elapsed_time(end)
+        return start.elapsed_time(end)
+
+    recs = []
+    eager_ms = None
+    if graph is not None:
+        graph.replay()  # warm replay
+        eager_ms = timed(lambda: step(recs))  # per-kernel breakdown (events need the eager step)
+        with ClockSampler(local_rank) as clocks:
+            total_ms = timed(graph.replay)
+    else:
+        with ClockSampler(local_rank) as clocks:
+            total_ms = timed(lambda: step(recs))
     for e0, e1, e2, e3, e4 in recs:
         kt["score"].append(e0.elapsed_time(e1))
         kt["gather_shard"].append(e2.elapsed_time(e3))
@@ -522,7 +554,10 @@ def our_arm(args, rank, world, local_rank):
                    "score_variant": SCORE_VARIANTS[args.score_variant],
                    "plan_ms_uncached": round(plan_ms, 3), "min_boundary_gap": state["gap"],
                    "selection": "host (D2H partials)" if args.host_select else "device (K9, no host round trip)",
-                   "device_selection_matches_host": select_check},
+                   "device_selection_matches_host": select_check,
+                   "step_launch": ("CUDA graph replay (5 kernel nodes per step)" if graph is not None
+                                   else (graph_note or "eager (5 launches per step)")),
+                   "eager_ms_per_step": round(eager_ms / args.steps, 4) if eager_ms else None},
         "layers_scored_per_s": round(scores_per_s, 1),
         "kernels_ms": {k: round(statistics.mean(x), 4) for k, x in kt.items()},
         "roofline": {"bound": "hbm", "kernel": "K2 gather (rank shard partition)",
@@ -1124,6 +1159,7 @@ def main():
     ap.add_argument("--host-select", action="store_true", help="select + plan on the host instead of K9")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-read-probe", action="store_true", help="skip the read-only HBM stream probe")
+    ap.add_argument("--no-graph", action="store_true", help="time the eager step instead of its CUDA graph")
     args = ap.parse_args()
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
