@@ -580,10 +580,13 @@ def our_arm(args, rank, world, local_rank):
             cores = os.cpu_count() or 1
             dt, comp, _ = run_reference_sample(work, cores)
             L2, h2, f2, v2, _, N2, K2, rho2 = SAMPLE
+            dt1, comp1, _ = run_reference_sample(work, 1)  # also a workers=1 run
             line["cpu_baseline"] = {"value": round(comp / dt / 1e9, 4), "unit": "GB/s", "cores": cores,
                                     "kind": "reference",
                                     "sample": f"reference select-merge on L{L2} h{h2} f{f2} v{v2} N{N2} K{K2}, "
-                                              f"{comp / 1e9:.3f} GB composite, {dt:.1f} s, files in /tmp"}
+                                              f"{comp / 1e9:.3f} GB composite, {dt:.1f} s, files in /tmp",
+                                    "workers_1": {"value": round(comp1 / dt1 / 1e9, 4), "unit": "GB/s", "cores": 1,
+                                                  "seconds": round(dt1, 2)}}
         finally:
             shutil.rmtree(work, ignore_errors=True)
     print(json.dumps(line))
