@@ -224,6 +224,10 @@ int tg_mplan_range(const tg_mplan* p, uint64_t* lo, uint64_t* hi, uint64_t* payl
 int32_t tg_mplan_num_windows(const tg_mplan* p);
 int tg_mplan_window(const tg_mplan* p, int32_t i, int32_t* snapshot, int32_t* container, uint64_t* lo, uint64_t* hi);
 uint32_t tg_mplan_num_segments(const tg_mplan* p);
+/* Segment i of the plan: bytes [src_off, src_off + bytes) of window `window` (offsets
+ * relative to the window's lo) land at payload offset dst_off - range lo of the output. */
+int tg_mplan_segment(const tg_mplan* p, uint32_t i, uint32_t* window, uint64_t* src_off, uint64_t* dst_off,
+                     uint64_t* bytes);
 int tg_mplan_prefix(const tg_mplan* p, char* out, size_t cap, size_t* needed); /* 8-B length + header */
 int tg_mplan_bind(tg_mplan* p, const uint8_t* const* window_ptrs);
 int32_t tg_mplan_bulk_ok(const tg_mplan* p);

@@ -151,6 +151,7 @@ SIGNATURES = {
     "tg_mplan_num_windows": (_I32, [_P]),
     "tg_mplan_window": (_I, [_P, _I32, _c.POINTER(_I32), _c.POINTER(_I32), _c.POINTER(_U64), _c.POINTER(_U64)]),
     "tg_mplan_num_segments": (_U32, [_P]),
+    "tg_mplan_segment": (_I, [_P, _U32, _c.POINTER(_U32), _c.POINTER(_U64), _c.POINTER(_U64), _c.POINTER(_U64)]),
     "tg_mplan_prefix": (_I, [_P, _c.c_char_p, _SZ, _PSZ]),
     "tg_mplan_bind": (_I, [_P, _PP]),
     "tg_mplan_bulk_ok": (_I32, [_P]),

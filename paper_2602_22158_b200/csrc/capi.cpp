@@ -795,6 +795,17 @@ int tg_mplan_window(const tg_mplan* p, int32_t i, int32_t* k, int32_t* container
 
 uint32_t tg_mplan_num_segments(const tg_mplan* p) { return static_cast<uint32_t>(p->dev->plan().segments.size()); }
 
+int tg_mplan_segment(const tg_mplan* p, uint32_t i, uint32_t* window, uint64_t* src_off, uint64_t* dst_off, uint64_t* bytes) {
+    return guard([&] {
+        const PartitionPlan& pp = p->dev->plan();
+        const CopySegment& s = pp.segments.at(i);
+        if (window) *window = s.window;
+        if (src_off) *src_off = s.src_off;
+        if (dst_off) *dst_off = s.dst_off - pp.dst_lo;
+        if (bytes) *bytes = s.bytes;
+    });
+}
+
 int tg_mplan_prefix(const tg_mplan* p, char* out, size_t cap, size_t* needed) {
     return guard([&] {
         const std::string s = p->dev->plan().out.prefix();

@@ -359,6 +359,15 @@ class MergePartition:
     def num_segments(self) -> int:
         return lib().tg_mplan_num_segments(self._h)
 
+    def segments(self):
+        """[(window, src_off, dst_off, bytes)]: the byte copies of this plan (host view)."""
+        out = []
+        for i in range(self.num_segments):
+            w, so, do, n = ctypes.c_uint32(), ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+            check(lib().tg_mplan_segment(self._h, i, ctypes.byref(w), ctypes.byref(so), ctypes.byref(do), ctypes.byref(n)))
+            out.append((w.value, so.value, do.value, n.value))
+        return out
+
     @property
     def bulk_ok(self) -> bool:
         return bool(lib().tg_mplan_bulk_ok(self._h))

@@ -4,6 +4,8 @@ selection — each against the oracle or the reference binary."""
 import json
 import random
 
+import numpy as np
+
 import pytest
 
 import paper_2602_22158_b200 as t
@@ -284,3 +286,78 @@ def test_selection_matches_oracle(seed):
     got.update(rec.aux)
     for i, m in enumerate(mods):
         assert got.get(m, f"S{K}") == f"S{ref_src[i] + 1}"
+
+
+# ---- acceptance c4 on the planning layer (R/tests/acceptance.cpp:244-254), no device ---------------
+def _random_recipe(rng, spec, K):
+    """Random recipe over sources S1..SK: every layer from a random source, optionally
+    moved to a permuted target position; every non-layer module from a random source."""
+    mods = o.modules(ospec(spec))
+    L = spec.num_layers
+    targets = list(range(L))
+    if rng.random() < 0.4:
+        rng.shuffle(targets)
+    assign, slices = {}, {}
+    for i in range(L):
+        k = rng.randrange(1, K + 1)
+        assign[f"layers.{targets[i]}"] = (f"S{k}", f"layers.{i}")
+        slices.setdefault(k, ([], []))
+        slices[k][0].append(i)
+        slices[k][1].append(targets[i])
+    recipe = t.MergeRecipe(num_ranks=0)
+    for k, (ls, ts) in sorted(slices.items()):
+        recipe.slices.append(t.RecipeSlice(f"S{k}", ls, ts))
+    for m in mods:
+        if not m.startswith("layers."):
+            k = rng.randrange(1, K + 1)
+            assign[m] = (f"S{k}", m)
+            recipe.aux[m] = f"S{k}"
+    return recipe, assign
+
+
+@pytest.mark.parametrize("case", range(200))
+def test_plan_segments_reassemble_the_reference_composite(case):
+    """200 random merges (random L<=8, h, f, v, tied, N<=5, K<=3, layer moves): applying the
+    plan's byte segments (what K2 copies) to random source payloads gives exactly the
+    composite the reference assembly produces (oracle merge_payloads restates
+    R/src/merge.cpp:244-303), for every rank partition and for the weights payload split
+    into 1 and 3 tensor-aligned shares; headers equal the reference's."""
+    rng = random.Random(7000 + case)
+    spec = t.ModelSpec(1 + rng.randrange(8), 4 << rng.randrange(2), 4 << rng.randrange(3), 8 << rng.randrange(3),
+                       rng.random() < 0.5, 100 + case)
+    N, K = 1 + rng.randrange(5), 1 + rng.randrange(3)
+    s = ospec(spec)
+    fam = t.SynthFamily(spec, N, K)
+    recipe, assign = _random_recipe(rng, spec, K)
+    recipe.num_ranks = N
+    if rng.random() < 0.3:
+        recipe.base_checkpoint = f"S{K}"
+    yaml = recipe.to_yaml()
+    nprng = np.random.default_rng(case)
+    mods = o.modules(s)
+    sources = {f"S{k}": (nprng.integers(0, 256, fam.weights_bytes(k), dtype=np.uint8).tobytes(),
+                         [nprng.integers(0, 256, fam.shard_bytes(k, r), dtype=np.uint8).tobytes() for r in range(N)],
+                         mods) for k in range(1, K + 1)}
+    exp_w, exp_r, wprefix, rprefixes = o.merge_payloads(s, N, assign, sources)
+
+    def apply(mp):
+        out = bytearray(mp.bytes)
+        wins = mp.windows()
+        for w, so, do, n in mp.segments():
+            k, c, lo, hi = wins[w]
+            assert lo + so + n <= hi
+            src = sources[f"S{k}"][0] if c < 0 else sources[f"S{k}"][1][c]
+            out[do:do + n] = src[lo + so:lo + so + n]
+        return bytes(out)
+
+    for r in range(N):
+        mp = t.MergePartition(fam, yaml, r)
+        assert mp.prefix() == rprefixes[r]
+        assert apply(mp) == exp_r[r], f"rank {r}"
+    for units in (1, 3):
+        got = b""
+        for u in range(units):
+            mp = t.MergePartition(fam, yaml, -1, u, units)
+            assert mp.prefix() == wprefix
+            got += apply(mp)
+        assert got == exp_w, f"weights in {units} shares"
