@@ -1016,9 +1016,11 @@ def hoststaged_arm(args, rank, world, local_rank):
 def trainer_arm(args, rank, world, local_rank):
     """SURVEY §8 f4 at scale: the device-resident trainer step (bit-exact AdamW on a
     Llama-3.1-8B-shaped ZeRO rank partition, one partition per GPU). Algorithmic bytes
-    per element: grad pass 4 (w read); update pass 12 (w,m,v) read + 12 written, the
-    gradient recomputed from w = 28 B (TAILOR_TRAIN_STORE_GRAD=1: the gradient goes
-    through a scratch buffer, 4 + 4 + 16 + 12 = 36 B). Both passes stream host-built
+    per element: the update pass reads w,m,v (12 B) and writes them (12 B), recomputing
+    the gradient from w and checking the new masters' exponents, which is the next
+    step's pre-update finiteness check = 24 B (a standalone 4 B check runs only when the
+    state was written by someone else, e.g. on the first step). TAILOR_TRAIN_STORE_GRAD=1:
+    the gradient goes through a scratch buffer, 4 + 4 + 16 + 12 = 36 B. Both passes stream host-built
     TrainTile runs as float4. Each step synchronizes once (the non-finite check precedes any
     state change, as apply_step requires) and once more for the norm partials; timed by
     wall clock around synchronized steps, max over ranks."""
@@ -1046,7 +1048,7 @@ def trainer_arm(args, rank, world, local_rank):
         all_reduce(tt, dist.ReduceOp.MAX)
         dt = float(tt.item())
     hbm, kind = peaks()
-    bpe = 36 if os.environ.get("TAILOR_TRAIN_STORE_GRAD", "0") not in ("", "0") else 28
+    bpe = 36 if os.environ.get("TAILOR_TRAIN_STORE_GRAD", "0") not in ("", "0") else 24
     gbs = bpe * n * args.steps / dt / 1e9
     if rank == 0:
         print(json.dumps({
@@ -1059,8 +1061,9 @@ def trainer_arm(args, rank, world, local_rank):
                        "elements_per_gpu": n, "unit_of_work": "one rank partition per GPU"},
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(gbs / hbm, 4), "peak_kind": kind, "bytes_per_element": bpe,
-                         "gradient": "scratch buffer" if bpe == 36 else "recomputed in the update pass"},
-            "last_norms": {"grad": gn, "update": un}, "gpu_launches": 2 * args.steps, "clocks": clocks.summary()}))
+                         "gradient": "scratch buffer" if bpe == 36 else
+                         "recomputed in the update pass, which also checks the next step's masters"},
+            "last_norms": {"grad": gn, "update": un}, "gpu_launches": (1 if bpe == 24 else 2) * args.steps, "clocks": clocks.summary()}))
     return 0
 
 

@@ -214,6 +214,7 @@ void DeviceTrainer::load(const fs::path& dir, const CheckpointSummary& s) {
     if (s.optim.num_ranks != N_ || !s.spec.same_geometry(model_.spec()))
         fail(ErrorKind::Geometry, "checkpoint geometry does not match the trainer");
     for (const auto& g : s.optim.groups) hyper_.at(static_cast<std::size_t>(g.index)) = g.hyper;
+    masters_checked_ = masters_bad_ = false; // new state: the next step checks it
     PinnedBuffer stage;
     for (int r = r0_; r < r1_; ++r) {
         const fs::path p = ckpt_file(CkptFile::Shard, dir, r);
@@ -246,6 +247,7 @@ void DeviceTrainer::load(const fs::path& dir, const CheckpointSummary& s) {
 std::pair<std::uint8_t*, std::uint64_t> DeviceTrainer::partition(int rank) {
     if (rank < r0_ || rank >= r1_) fail(ErrorKind::Geometry, "rank " + std::to_string(rank) + " is not held by this trainer");
     cuda_check(cudaStreamSynchronize(stream_), "sync");
+    masters_checked_ = masters_bad_ = false; // the caller may write the state
     const auto& rk = ranks_[static_cast<std::size_t>(rank - r0_)];
     return {rk->part.get(), full_.shards[static_cast<std::size_t>(rank)].payload_bytes};
 }
@@ -256,17 +258,27 @@ std::pair<double, double> DeviceTrainer::step(std::int64_t s) {
     // fast check: masters' finiteness decides the gradient's (see finite_check_kernel);
     // the gradient norm then comes from the update pass
     const bool fast = !store_grad_ && dev::finite_check_suffices(p);
-    for (auto& rk : ranks_)
-        cuda_check(fast ? dev::launch_finite_check(rk->tiles.get<dev::TrainTile>(), rk->ntiles, rk->groups.get<dev::TrainGroup>(),
-                                                   rk->part.get(), flag_.get<unsigned int>(), stream_)
-                        : dev::launch_grad_check(rk->tiles.get<dev::TrainTile>(), rk->ntiles, rk->groups.get<dev::TrainGroup>(),
-                                                 rk->part.get(), p, store_grad_ ? rk->grad.get<float>() : nullptr,
-                                                 rk->grad_part.get<double>(), flag_.get<unsigned int>(), stream_),
-                   "grad check");
-    unsigned int bad = 0;
-    cuda_check(cudaMemcpyAsync(&bad, flag_.get(), sizeof(bad), cudaMemcpyDeviceToHost, stream_), "D2H");
-    cuda_check(cudaStreamSynchronize(stream_), "sync");
-    if (bad) fail(ErrorKind::NonFinite, "non-finite gradient at step " + std::to_string(s));
+    if (fast && masters_bad_) fail(ErrorKind::NonFinite, "non-finite gradient at step " + std::to_string(s));
+    if (!(fast && masters_checked_)) { // otherwise the previous update pass already checked these masters
+        for (auto& rk : ranks_)
+            cuda_check(fast ? dev::launch_finite_check(rk->tiles.get<dev::TrainTile>(), rk->ntiles, rk->groups.get<dev::TrainGroup>(),
+                                                       rk->part.get(), flag_.get<unsigned int>(), stream_)
+                            : dev::launch_grad_check(rk->tiles.get<dev::TrainTile>(), rk->ntiles, rk->groups.get<dev::TrainGroup>(),
+                                                     rk->part.get(), p, store_grad_ ? rk->grad.get<float>() : nullptr,
+                                                     rk->grad_part.get<double>(), flag_.get<unsigned int>(), stream_),
+                       "grad check");
+        unsigned int bad = 0;
+        cuda_check(cudaMemcpyAsync(&bad, flag_.get(), sizeof(bad), cudaMemcpyDeviceToHost, stream_), "D2H");
+        cuda_check(cudaStreamSynchronize(stream_), "sync");
+        if (bad) {
+            masters_bad_ = fast;
+            fail(ErrorKind::NonFinite, "non-finite gradient at step " + std::to_string(s));
+        }
+    }
+    if (fast) {
+        next_flag_.resize(sizeof(unsigned int));
+        cuda_check(cudaMemsetAsync(next_flag_.get(), 0, sizeof(unsigned int), stream_), "memset");
+    }
     t_ += 1;
     std::vector<dev::AdamCoef> coef(static_cast<std::size_t>(model_.table().group_count()));
     for (const auto& g : model_.table().groups) {
@@ -288,7 +300,8 @@ std::pair<double, double> DeviceTrainer::step(std::int64_t s) {
         cuda_check(dev::launch_adamw(rk->tiles.get<dev::TrainTile>(), rk->ntiles, rk->groups.get<dev::TrainGroup>(),
                                      coef_.get<dev::AdamCoef>(), rk->part.get(),
                                      store_grad_ ? rk->grad.get<float>() : nullptr, p, rk->delta_part.get<double>(),
-                                     fast ? rk->grad_part.get<double>() : nullptr, stream_),
+                                     fast ? rk->grad_part.get<double>() : nullptr,
+                                     fast ? next_flag_.get<unsigned int>() : nullptr, stream_),
                    "adamw");
     double g2 = 0.0, d2 = 0.0;
     std::vector<double> h;
@@ -303,6 +316,14 @@ std::pair<double, double> DeviceTrainer::step(std::int64_t s) {
             g2 += h[b];
             d2 += h[rk->grid + b];
         }
+    }
+    if (fast) { // the stream is synchronized: the flag of the masters just written is final
+        unsigned int next_bad = 0;
+        cuda_check(cudaMemcpy(&next_bad, next_flag_.get(), sizeof(next_bad), cudaMemcpyDeviceToHost), "D2H");
+        masters_checked_ = next_bad == 0;
+        masters_bad_ = next_bad != 0;
+    } else {
+        masters_checked_ = masters_bad_ = false;
     }
     return {std::sqrt(g2), std::sqrt(d2)};
 }

@@ -156,9 +156,12 @@ __global__ void __launch_bounds__(kThreads) adamw_update_kernel(const TrainTile*
                                                                 const AdamCoef* __restrict__ coef, std::uint8_t* __restrict__ part,
                                                                 const float* __restrict__ grad, TrainParams p,
                                                                 double* __restrict__ delta_partials,
-                                                                double* __restrict__ grad_partials) {
+                                                                double* __restrict__ grad_partials,
+                                                                unsigned int* __restrict__ next_nonfinite) {
     __shared__ double red[kThreads / 32];
     double acc = 0.0, gacc = 0.0;
+    bool next_bad = false; // a new master is inf/NaN: the next step's gradient is not finite
+    const auto inf_or_nan = [](float x) { return (__float_as_uint(x) & 0x7F800000u) == 0x7F800000u; };
     for (std::uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const TrainTile tile = tiles[t];
         const TrainGroup& g = groups[tile.group];
@@ -187,6 +190,8 @@ __global__ void __launch_bounds__(kThreads) adamw_update_kernel(const TrainTile*
                 __stcs(reinterpret_cast<float4*>(mp) + q, m);
                 __stcs(reinterpret_cast<float4*>(vp) + q, v);
                 __stcs(reinterpret_cast<float4*>(wp) + q, w);
+                if constexpr (kRecompute)
+                    next_bad = next_bad || inf_or_nan(w.x) || inf_or_nan(w.y) || inf_or_nan(w.z) || inf_or_nan(w.w);
                 acc = fma(static_cast<double>(s0), static_cast<double>(s0), acc);
                 acc = fma(static_cast<double>(s1), static_cast<double>(s1), acc);
                 acc = fma(static_cast<double>(s2), static_cast<double>(s2), acc);
@@ -207,9 +212,15 @@ __global__ void __launch_bounds__(kThreads) adamw_update_kernel(const TrainTile*
                 vp[j] = v;
                 wp[j] = w;
                 acc = fma(static_cast<double>(st), static_cast<double>(st), acc);
-                if constexpr (kRecompute) gacc = fma(static_cast<double>(gr), static_cast<double>(gr), gacc);
+                if constexpr (kRecompute) {
+                    gacc = fma(static_cast<double>(gr), static_cast<double>(gr), gacc);
+                    next_bad = next_bad || inf_or_nan(w);
+                }
             }
         }
+    }
+    if constexpr (kRecompute) {
+        if (next_nonfinite && __any_sync(0xffffffffu, next_bad) && (threadIdx.x & 31) == 0) atomicOr(next_nonfinite, 1u);
     }
     const double s = block_sum(acc, red);
     if (threadIdx.x == 0) delta_partials[blockIdx.x] = s;
@@ -305,13 +316,13 @@ cudaError_t launch_finite_check(const TrainTile* d_tiles, std::uint32_t ntiles, 
 
 cudaError_t launch_adamw(const TrainTile* d_tiles, std::uint32_t ntiles, const TrainGroup* d_groups, const AdamCoef* d_coef,
                          std::uint8_t* d_part, const float* d_grad, const TrainParams& p, double* d_delta_partials,
-                         double* d_grad_partials, cudaStream_t s) {
+                         double* d_grad_partials, unsigned int* d_next_nonfinite, cudaStream_t s) {
     if (d_grad)
         adamw_update_kernel<false><<<train_grid(ntiles), kThreads, 0, s>>>(d_tiles, ntiles, d_groups, d_coef, d_part, d_grad, p,
-                                                                          d_delta_partials, nullptr);
+                                                                          d_delta_partials, nullptr, nullptr);
     else
         adamw_update_kernel<true><<<train_grid(ntiles), kThreads, 0, s>>>(d_tiles, ntiles, d_groups, d_coef, d_part, nullptr, p,
-                                                                         d_delta_partials, d_grad_partials);
+                                                                         d_delta_partials, d_grad_partials, d_next_nonfinite);
     return cudaGetLastError();
 }
 

@@ -180,7 +180,9 @@ cudaError_t launch_grad_check(const TrainTile* d_tiles, std::uint32_t ntiles, co
                               unsigned int* d_nonfinite, cudaStream_t s);
 cudaError_t launch_adamw(const TrainTile* d_tiles, std::uint32_t ntiles, const TrainGroup* d_groups, const AdamCoef* d_coef,
                          std::uint8_t* d_part, const float* d_grad, const TrainParams& p, double* d_delta_partials,
-                         double* d_grad_partials, cudaStream_t s);
+                         double* d_grad_partials, unsigned int* d_next_nonfinite, cudaStream_t s);
+// (recomputing form) d_next_nonfinite, if set, is OR-ed with 1 when a new master is
+// inf/NaN: the exponent check of the NEXT step, done on the values as they are written.
 // Pass 1 fast form (masters' exponent bits only) and when it is exact: g = c1*w +
 // c2*u is finite iff w is, for 0 < |c1| <= 1/2 and |c2| <= 1. In that mode pass 2
 // (recomputing) also writes the FP64 sum g^2 per block into d_grad_partials.

@@ -78,6 +78,12 @@ class DeviceTrainer {
     // selects the scratch-buffer variant (36 B/element; kept for comparison).
     bool store_grad_ = false;
     std::vector<AdamHyperparams> hyper_; // per group (GroupState::hyper)
+    // The fast pre-update check of step s+1 is folded into step s's update pass (it sees
+    // every new master as it writes it): masters_checked_ = the current masters are known
+    // finite, masters_bad_ = known not finite. Any other writer of the state (load,
+    // partition() access) clears both, and the next step runs the standalone check.
+    DeviceBuffer next_flag_;
+    bool masters_checked_ = false, masters_bad_ = false;
 };
 
 // The reference's train() (R/src/trainer.cpp:109-123) on the device: same run
