@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1105,11 +1106,31 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
                                           std::max(1, std::min(N, 8)));
         const int readers = std::max(1, io_threads() / lanes);
         const std::uint64_t step = lanes > 1 ? (16ull << 20) : (256ull << 20);
-        {
-            PhaseTimer pt("verify.load_weights");
-            PinnedBuffer stage[2];
-            load_payload(ckpt_file(CkptFile::Weights, dir), wl, dw, stage, io_threads(), step);
-        }
+        // the weights payload loads on its own thread while the lanes load rank payloads;
+        // a lane waits for it only before its first duality kernel
+        dw.resize(std::max<std::uint64_t>(16, wl.payload_bytes));
+        std::mutex wmu;
+        std::condition_variable wcv;
+        bool weights_ready = false;
+        std::exception_ptr werr;
+        std::thread wloader([&] {
+            try {
+                cuda_check(cudaSetDevice(device), "cudaSetDevice");
+                PhaseTimer pt("verify.load_weights");
+                PinnedBuffer stage[2];
+                load_payload(ckpt_file(CkptFile::Weights, dir), wl, dw, stage, std::max(1, io_threads() / 2), step);
+            } catch (...) {
+                werr = std::current_exception();
+            }
+            std::lock_guard<std::mutex> lk(wmu);
+            weights_ready = true;
+            wcv.notify_all();
+        });
+        const auto wait_weights = [&] {
+            std::unique_lock<std::mutex> lk(wmu);
+            wcv.wait(lk, [&] { return weights_ready; });
+            if (werr) std::rethrow_exception(werr);
+        };
         run_lanes(lanes, [&] {
             try {
                 cuda_check(cudaSetDevice(device), "cudaSetDevice");
@@ -1131,6 +1152,7 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
                     }
                     for (auto& x : rg)
                         x.words = reinterpret_cast<const std::uint32_t*>(ds.get() + reinterpret_cast<std::uintptr_t>(x.words));
+                    wait_weights();
                     launch(pr, rg, dpairs, dranges, r, ls.s);
                 }
             } catch (...) {
@@ -1138,6 +1160,8 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
                 if (!lane_err) lane_err = std::current_exception();
             }
         });
+        wloader.join();
+        if (werr && !lane_err) std::rethrow_exception(werr);
     } else {
         // window W of shard bytes + up to W/2 of weight bytes per lane
         const int want = std::max(1, std::min(N, 8));
