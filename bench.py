@@ -900,10 +900,13 @@ def hoststaged_arm(args, rank, world, local_rank):
                 out = partials[p * M * 2:(p + 1) * M * 2]
                 secs += sync_time(lambda: scorers[k].run([slots[(k - 2) % 2].data_ptr(), slot.data_ptr()],
                                                          out.data_ptr(), sp))
-        del slots, host
-        return secs, K * pm, partials
+        del host
+        # the two slots now hold the packed masters of S_{K-1} and S_K: pass B reads those
+        # masters from HBM instead of re-uploading them
+        resident = {k: slots[(k - 1) % 2] for k in (K - 1, K)}
+        return secs, K * pm, partials, resident
 
-    def pass_b(yaml):
+    def pass_b(yaml, resident):
         """Composite shard partition in sub-units + weights share in pieces, host-staged.
         Each piece's plan is destroyed after it runs, so its pipeline buffers go back to the
         pinned/device pools and the next piece reuses them; the first piece runs once untimed
@@ -936,8 +939,11 @@ def hoststaged_arm(args, rank, world, local_rank):
             p.run(dref.data_ptr(), args.variant, sp)
             res = {}
 
+            dres = [resident[k].data_ptr() if (c >= 0 and k in resident) else None for k, c, lo, hi in p.windows()]
+
             def run():
-                res["io"] = p.run_host([hwin.data_ptr() + o for o in offs], hout.data_ptr(), args.variant)
+                res["io"] = p.run_host([hwin.data_ptr() + o for o in offs], hout.data_ptr(), args.variant,
+                                       d_windows=dres, resident_fields=8 if any(dres) else 0)
 
             if i == 0:
                 sync_time(run)  # untimed: fills the pools with this pipeline's staging buffers
@@ -957,7 +963,7 @@ def hoststaged_arm(args, rank, world, local_rank):
     piece_s = []
 
     def step():
-        sa, ha, partials = pass_a()
+        sa, ha, partials, resident = pass_a()
         if world > 1:
             gathered = torch.zeros(world * partials.numel(), dtype=torch.float64, device=dev)
             all_gather(gathered, partials)
@@ -967,7 +973,8 @@ def hoststaged_arm(args, rank, world, local_rank):
         t0 = time.perf_counter()
         yaml, src, _, gap = fam.select(parts.cpu().tolist(), world, rho)
         sel = time.perf_counter() - t0
-        sb, hb, db, comp, ok = pass_b(yaml)
+        sb, hb, db, comp, ok = pass_b(yaml, resident)
+        del resident
         return {"secs": sa + sel + sb, "score_s": sa, "merge_s": sb, "h2d": ha + hb, "d2h": db + parts.numel() * 8,
                 "comp": comp, "ok": ok, "gap": gap, "sources": src}
 

@@ -235,7 +235,9 @@ int tg_mplan_run(tg_mplan* p, uint8_t* d_dst, int32_t variant, void* stream);
 /* Shard pipeline: host windows -> H2D (needed bytes only) -> K2 -> D2H into h_dst.
  * Fields in `resident_fields` (bit0 exp_avg, bit1 exp_avg_sq, bit2 master) are read
  * from d_windows[w] (device copies of shard windows, e.g. masters staged for
- * scoring) instead of crossing PCIe again. async=1 returns before completion;
+ * scoring) instead of crossing PCIe again; bit3 reads the masters from d_windows[w] =
+ * the packed masters of the window's snapshot for this rank (the scorer's packed
+ * layout). A null d_windows[w] keeps window w on PCIe. async=1 returns before completion;
  * tg_mplan_wait() (or the next run) synchronizes. */
 typedef struct {
     const uint8_t* src; /* pinned host */

@@ -216,5 +216,5 @@ def text_call(fn, *args) -> str:
 def ptr_array(ptrs) -> ctypes.Array:
     arr = (ctypes.c_void_p * max(1, len(ptrs)))()
     for i, p in enumerate(ptrs):
-        arr[i] = int(p)
+        arr[i] = int(p) if p is not None else 0
     return arr

@@ -46,7 +46,8 @@ struct tg_mplan {
     std::unique_ptr<DeviceMerge> dev;
     std::unique_ptr<HostMerge> host;
     std::uint64_t host_chunk = 0;
-    std::uint32_t host_fields = 0;
+    HostMerge::Resident host_resident; // the resident map the host pipeline was built for
+    const SynthFamily* fam = nullptr;
     std::vector<int> window_k;
     std::vector<ContainerLayout> window_layout; // source container of each window
 };
@@ -758,6 +759,7 @@ tg_mplan* tg_mplan_create(tg_family* f, const char* yaml, int32_t container, int
             }
         }
         auto* p = new tg_mplan{};
+        p->fam = &fam;
         for (const auto& w : pp.windows) {
             p->window_k.push_back(fam.index_of(w.source));
             const SourceLayout& sl = lay_of(w.source);
@@ -831,26 +833,47 @@ int tg_mplan_run_host(tg_mplan* p, const uint8_t* const* h_windows, const uint8_
     return guard([&] {
         const PartitionPlan& pp = p->dev->plan();
         if (!d_windows) resident_fields = 0;
-        if (!p->host || p->host_chunk != chunk || p->host_fields != resident_fields) {
-            HostMerge::Resident res(pp.windows.size());
-            static const char* kField[3] = {".exp_avg", ".exp_avg_sq", ".master"};
-            for (std::size_t w = 0; w < pp.windows.size(); ++w) {
-                if (pp.windows[w].container < 0) continue; // weights are never resident
-                for (const auto& e : p->window_layout[w].entries)
-                    for (int f = 0; f < 3; ++f) {
-                        if (!(resident_fields & (1u << f))) continue;
-                        const std::string& n = e.name;
-                        const std::string suf = kField[f];
-                        if (n.size() < suf.size() || n.compare(n.size() - suf.size(), suf.size(), suf) != 0) continue;
-                        if (f == 0 && n.size() >= 11 && n.compare(n.size() - 11, 11, ".exp_avg_sq") == 0) continue;
-                        const std::uint64_t a = std::max(e.begin, pp.windows[w].lo), b = std::min(e.end, pp.windows[w].hi);
-                        if (a < b) res[w].push_back({a - pp.windows[w].lo, b - pp.windows[w].lo});
-                    }
-                std::sort(res[w].begin(), res[w].end());
+        // Resident ranges: bits 0-2 read exp_avg / exp_avg_sq / master from d_windows[w], a
+        // device copy of the window in shard layout; bit 3 reads the masters from
+        // d_windows[w] = the window snapshot's packed masters of this rank (the scorer's
+        // layout, SynthFamily::gen_masters). Windows with a null d_windows entry stay on PCIe.
+        HostMerge::Resident res(pp.windows.size());
+        static const char* kField[3] = {".exp_avg", ".exp_avg_sq", ".master"};
+        std::map<int, std::uint64_t> packed_off; // group -> offset in the packed masters
+        if (resident_fields & 8u) {
+            std::uint64_t off = 0;
+            for (const auto& f : score_fields(p->fam->model(), p->fam->num_ranks())) {
+                packed_off[f.group] = off;
+                off = (off + static_cast<std::uint64_t>(f.chunk) * 4 + 15) & ~15ull;
             }
-            p->host = std::make_unique<HostMerge>(pp, chunk ? chunk : (256ull << 20), std::move(res));
+        }
+        for (std::size_t w = 0; resident_fields && w < pp.windows.size(); ++w) {
+            if (pp.windows[w].container < 0 || !d_windows[w]) continue; // weights are never resident
+            const std::uint64_t wlo = pp.windows[w].lo, whi = pp.windows[w].hi;
+            for (const auto& e : p->window_layout[w].entries) {
+                const std::uint64_t a = std::max(e.begin, wlo), b = std::min(e.end, whi);
+                if (a >= b) continue;
+                const std::string& n = e.name;
+                const auto ends = [&](const char* suf) {
+                    const std::size_t k = std::strlen(suf);
+                    return n.size() >= k && n.compare(n.size() - k, k, suf) == 0;
+                };
+                const int f = ends(kField[1]) ? 1 : ends(kField[0]) ? 0 : ends(kField[2]) ? 2 : -1;
+                if (f < 0) continue;
+                if ((resident_fields & 8u) && f == 2) {
+                    const int g = std::stoi(n.substr(1, n.find('.') - 1));
+                    res[w].push_back({a - wlo, b - wlo, packed_off.at(g) + (a - e.begin)});
+                } else if (resident_fields & (1u << f)) {
+                    res[w].push_back({a - wlo, b - wlo, a - wlo});
+                }
+            }
+            std::sort(res[w].begin(), res[w].end(),
+                      [](const HostMerge::ResidentRange& x, const HostMerge::ResidentRange& y) { return x.lo < y.lo; });
+        }
+        if (!p->host || p->host_chunk != chunk || p->host_resident != res) {
+            p->host = std::make_unique<HostMerge>(pp, chunk ? chunk : (256ull << 20), res);
             p->host_chunk = chunk;
-            p->host_fields = resident_fields;
+            p->host_resident = std::move(res);
         }
         std::vector<const std::uint8_t*> dw(pp.windows.size(), nullptr);
         if (d_windows) dw.assign(d_windows, d_windows + pp.windows.size());

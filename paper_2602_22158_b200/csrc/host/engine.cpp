@@ -666,15 +666,17 @@ HostMerge::HostMerge(const PartitionPlan& plan, std::uint64_t chunk_bytes, Resid
                 const std::uint64_t src = s.src_off + (a - d0);
                 std::uint64_t n = b - a;
                 bool dev_side = false;
-                for (const auto& [r0, r1] : resident_[s.window]) {
-                    if (src >= r0 && src < r1) {
+                std::uint64_t dev_at = 0;
+                for (const auto& rr : resident_[s.window]) {
+                    if (src >= rr.lo && src < rr.hi) {
                         dev_side = true;
-                        n = std::min(n, r1 - src);
+                        dev_at = rr.dev_off + (src - rr.lo);
+                        n = std::min(n, rr.hi - src);
                         break;
                     }
-                    if (r0 > src) n = std::min(n, r0 - src);
+                    if (rr.lo > src) n = std::min(n, rr.lo - src);
                 }
-                ps.push_back({s.window, src, a, n, dev_side});
+                ps.push_back({s.window, src, a, n, dev_side, dev_at});
                 a += n;
             }
         }
@@ -788,7 +790,7 @@ void HostMerge::run(const std::vector<const std::uint8_t*>& h_windows, const std
             const std::uint8_t* src;
             if (p.dev) {
                 if (d_windows.size() <= p.w || !d_windows[p.w]) fail(ErrorKind::Geometry, "resident window without a device pointer");
-                src = d_windows[p.w] + p.src;
+                src = d_windows[p.w] + p.stage;
             } else {
                 src = stage_[in].get() + p.stage;
             }

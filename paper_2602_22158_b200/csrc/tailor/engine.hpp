@@ -237,7 +237,14 @@ struct HostCopy {
 
 class HostMerge {
   public:
-    using Resident = std::vector<std::vector<std::pair<std::uint64_t, std::uint64_t>>>;
+    // Per window: byte ranges [lo, hi) (window-relative) that are read from device
+    // memory instead of crossing PCIe; byte x lives at d_windows[w] + dev_off + (x - lo)
+    // (dev_off = lo: a device copy in the window's own layout).
+    struct ResidentRange {
+        std::uint64_t lo, hi, dev_off;
+        bool operator==(const ResidentRange&) const = default;
+    };
+    using Resident = std::vector<std::vector<ResidentRange>>;
     explicit HostMerge(const PartitionPlan& plan, std::uint64_t chunk_bytes = 256ull << 20, Resident resident = {});
     ~HostMerge();
     // h_windows[w] = host address of window w's first byte; d_windows[w] = device
@@ -254,7 +261,7 @@ class HostMerge {
         std::uint32_t w;
         std::uint64_t src, dst, n;
         bool dev;
-        std::uint64_t stage = 0;
+        std::uint64_t stage = 0; // host pieces: offset in the staging slot; device pieces: offset from d_windows[w]
     };
     struct Read {
         std::uint32_t w;

@@ -238,6 +238,20 @@ def test_host_pipeline_matches_device():
             mp.wait()
             assert bytes(hdst2.numpy()) == host_bytes(out, mp.bytes)
             assert h2d2 == mp.bytes * frac // 3 or (fields == 4 and 0 < h2d2 < mp.bytes)
+        # masters read from the scorer's packed buffers (cfg5's staged snapshots), only for
+        # some windows' snapshots: same composite, fewer H2D bytes
+        packed = [dev(fam.packed_master_bytes(r)) for _ in range(K)]
+        for k in range(1, K + 1):
+            fam.gen_masters(r, k, k, [packed[k - 1].data_ptr()])
+        for keep in ({1, 2, 3}, {3}, {2}):
+            hdst3 = torch.zeros(mp.bytes, dtype=torch.uint8).pin_memory()
+            h2d3, _ = mp.run_host([hsrc[k - 1].data_ptr() + lo for k, c, lo, hi in mp.windows()], hdst3.data_ptr(),
+                                  chunk_bytes=1 << 14,
+                                  d_windows=[packed[k - 1].data_ptr() if k in keep else None for k, c, lo, hi in mp.windows()],
+                                  resident_fields=8)
+            torch.cuda.synchronize()
+            assert bytes(hdst3.numpy()) == host_bytes(out, mp.bytes), keep
+            assert h2d3 < mp.bytes
 
 
 def test_host_pipeline_prefetch_copies():
