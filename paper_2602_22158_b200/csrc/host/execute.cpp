@@ -6,8 +6,9 @@
 // full re-verify before returning, MergeStats counting files read. Different
 // mechanism: only the byte ranges the composite needs are read from each
 // source (the reference loads every shard file whole), staged through pinned
-// memory, assembled by the device gather kernel, and streamed back out in
-// chunks on two CUDA streams; the re-verify is the device kernel K6.
+// memory, assembled by the device gather kernel, and streamed back out — the
+// output files in parallel lanes (one file per lane, 3-slot pipeline each); the
+// re-verify is the device kernel K6.
 #include <algorithm>
 #include <atomic>
 #include <exception>

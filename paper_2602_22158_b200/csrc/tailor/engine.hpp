@@ -3,7 +3,8 @@
 //   ScorePlan    — K3/K4 tile tables for one rank partition of K snapshots
 //   DeviceMerge  — K2 segment table for one output partition, bound to device windows
 //   HostMerge    — the shard pipeline: pinned host sources -> H2D -> K2 -> D2H, chunked,
-//                  on two streams so transfers overlap the gather
+//                  on three streams (H2D / gather / D2H, event-ordered) so transfers
+//                  overlap the gather
 #pragma once
 
 #include <cstdint>
