@@ -996,21 +996,15 @@ void load_payload(const fs::path& path, const ContainerLayout& lay, DeviceBuffer
 
 } // namespace
 
-void verify_checkpoint_dir(const std::string& dir_s, int device) {
-    cuda_check(cudaSetDevice(device), "cudaSetDevice");
-    const fs::path dir(dir_s);
-    const CheckpointSummary s = read_checkpoint_summary(dir);
+VerifyPlan verify_plan(const fs::path& dir, const CheckpointSummary& s, ContainerLayout weights,
+                       std::vector<ContainerLayout> shards) {
+    VerifyPlan out;
+    out.weights = std::move(weights);
+    out.shards = std::move(shards);
     const GroupTable table = s.optim.grouping == Grouping::Fine ? build_group_table(s.spec) : build_coarse_table(s.spec);
     std::map<int, std::vector<TensorSlice>> group_slices;
     for (const auto& g : s.optim.groups) group_slices[g.index] = group_tensor_slices(s.spec, table, g.index);
-    const fs::path optim = dir / "optim";
-    if (!fs::exists(optim)) fail(ErrorKind::MissingArtifact, "'" + optim.string() + "' does not exist");
-    std::size_t files = 0;
-    for ([[maybe_unused]] const auto& e : fs::directory_iterator(optim)) ++files;
-    if (files != static_cast<std::size_t>(s.optim.num_ranks))
-        fail(ErrorKind::Geometry, dir.string() + ": found " + std::to_string(files) + " shard files for " +
-                                      std::to_string(s.optim.num_ranks) + " ranks");
-    const ContainerLayout wl = read_layout(ckpt_file(CkptFile::Weights, dir));
+    const ContainerLayout& wl = out.weights;
     std::size_t expect_tensors = 0;
     for (const auto& m : s.manifest.modules)
         for (const auto& t : tensors_of(s.spec, m)) {
@@ -1028,15 +1022,15 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
     // device over parallel lanes (one rank file each) and the failure counters
     // are checked in rank order.
     const int N = s.optim.num_ranks;
-    std::vector<ContainerLayout> shard_lay;
-    std::vector<std::vector<dev::VerifyPair>> pairs(static_cast<std::size_t>(N));
-    std::vector<std::vector<dev::VerifyRange>> ranges(static_cast<std::size_t>(N));
-    std::uint64_t max_shard = 16;
+    if (out.shards.size() != static_cast<std::size_t>(N)) fail(ErrorKind::Geometry, "shard layout count mismatch");
+    auto& pairs = out.pairs;
+    auto& ranges = out.ranges;
+    pairs.assign(static_cast<std::size_t>(N), {});
+    ranges.assign(static_cast<std::size_t>(N), {});
     for (int r = 0; r < N; ++r) {
         const fs::path sp = ckpt_file(CkptFile::Shard, dir, r);
-        shard_lay.push_back(read_layout(sp));
-        const ContainerLayout& sl = shard_lay.back();
-        max_shard = std::max<std::uint64_t>(max_shard, sl.payload_bytes);
+        const ContainerLayout& sl = out.shards[static_cast<std::size_t>(r)];
+        out.max_shard = std::max<std::uint64_t>(out.max_shard, sl.payload_bytes);
         auto mr = sl.metadata.find("rank");
         if (mr != sl.metadata.end() && mr->second != std::to_string(r))
             fail(ErrorKind::CorruptContainer, sp.string() + ": rank metadata mismatch");
@@ -1072,6 +1066,68 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
         }
     }
 
+    return out;
+}
+
+void verify_rank_resident(const VerifyPlan& plan, int r, const fs::path& shard_file, const std::uint8_t* dw, DeviceBuffer& ds,
+                          DeviceBuffer& dpairs, DeviceBuffer& dranges, PinnedBuffer* stage, int readers, std::uint64_t step,
+                          unsigned long long* d_err, cudaStream_t st, const std::function<void()>& before_kernel) {
+    const auto& sl = plan.shards.at(static_cast<std::size_t>(r));
+    load_payload(shard_file, sl, ds, stage, readers, step);
+    auto pr = plan.pairs[static_cast<std::size_t>(r)];
+    auto rg = plan.ranges[static_cast<std::size_t>(r)];
+    for (auto& x : pr) {
+        x.master = reinterpret_cast<const float*>(ds.get() + reinterpret_cast<std::uintptr_t>(x.master));
+        x.weight = reinterpret_cast<const std::uint16_t*>(dw + reinterpret_cast<std::uintptr_t>(x.weight));
+    }
+    for (auto& x : rg) x.words = reinterpret_cast<const std::uint32_t*>(ds.get() + reinterpret_cast<std::uintptr_t>(x.words));
+    if (before_kernel) before_kernel();
+    dpairs.upload(pr.data(), pr.size() * sizeof(dev::VerifyPair));
+    dranges.upload(rg.data(), rg.size() * sizeof(dev::VerifyRange));
+    cuda_check(dev::launch_verify(dpairs.get<dev::VerifyPair>(), static_cast<std::uint32_t>(pr.size()),
+                                  dranges.get<dev::VerifyRange>(), static_cast<std::uint32_t>(rg.size()), d_err + 3 * r, st),
+               "verify");
+    cuda_check(cudaStreamSynchronize(st), "verify");
+}
+
+void load_payload_to(const fs::path& path, const ContainerLayout& lay, DeviceBuffer& dst, PinnedBuffer* stage, int threads,
+                     std::uint64_t step) {
+    load_payload(path, lay, dst, stage, threads, step);
+}
+
+void verify_counters(const fs::path& dir, int num_ranks, const unsigned long long* d_err) {
+    std::vector<unsigned long long> err(static_cast<std::size_t>(num_ranks) * 3);
+    cuda_check(cudaMemcpy(err.data(), d_err, err.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "D2H");
+    bool mismatch = false;
+    for (int r = 0; r < num_ranks; ++r) {
+        if (err[3 * r + 1]) fail(ErrorKind::CorruptContainer, dir.string() + ": nonzero padding in rank " + std::to_string(r));
+        if (err[3 * r + 2]) fail(ErrorKind::Consistency, "exp_avg_sq contains a negative or non-finite element");
+        mismatch = mismatch || err[3 * r] != 0;
+    }
+    if (mismatch) fail(ErrorKind::Consistency, dir.string() + ": a weight tensor disagrees with its FP32 master");
+}
+
+void verify_checkpoint_dir(const std::string& dir_s, int device) {
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    const fs::path dir(dir_s);
+    const CheckpointSummary s = read_checkpoint_summary(dir);
+    const fs::path optim = dir / "optim";
+    if (!fs::exists(optim)) fail(ErrorKind::MissingArtifact, "'" + optim.string() + "' does not exist");
+    std::size_t files = 0;
+    for ([[maybe_unused]] const auto& e : fs::directory_iterator(optim)) ++files;
+    if (files != static_cast<std::size_t>(s.optim.num_ranks))
+        fail(ErrorKind::Geometry, dir.string() + ": found " + std::to_string(files) + " shard files for " +
+                                      std::to_string(s.optim.num_ranks) + " ranks");
+    ContainerLayout wl_file = read_layout(ckpt_file(CkptFile::Weights, dir));
+    std::vector<ContainerLayout> shard_files;
+    for (int r = 0; r < s.optim.num_ranks; ++r) shard_files.push_back(read_layout(ckpt_file(CkptFile::Shard, dir, r)));
+    const VerifyPlan plan = verify_plan(dir, s, std::move(wl_file), std::move(shard_files));
+    const ContainerLayout& wl = plan.weights;
+    const int N = s.optim.num_ranks;
+    const std::uint64_t max_shard = plan.max_shard;
+    const auto& pairs = plan.pairs;
+    const auto& ranges = plan.ranges;
+    const auto& shard_lay = plan.shards;
     DeviceBuffer dw, derr(static_cast<std::size_t>(N) * 3 * sizeof(unsigned long long));
     cuda_check(cudaMemset(derr.get(), 0, derr.size()), "memset");
     const std::uint64_t budget = device_budget();
@@ -1144,18 +1200,8 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
                         std::lock_guard<std::mutex> lk(mu);
                         if (lane_err) break;
                     }
-                    const auto& sl = shard_lay[static_cast<std::size_t>(r)];
-                    load_payload(ckpt_file(CkptFile::Shard, dir, r), sl, ds, stage, readers, step);
-                    auto pr = pairs[static_cast<std::size_t>(r)];
-                    auto rg = ranges[static_cast<std::size_t>(r)];
-                    for (auto& x : pr) {
-                        x.master = reinterpret_cast<const float*>(ds.get() + reinterpret_cast<std::uintptr_t>(x.master));
-                        x.weight = reinterpret_cast<const std::uint16_t*>(dw.get() + reinterpret_cast<std::uintptr_t>(x.weight));
-                    }
-                    for (auto& x : rg)
-                        x.words = reinterpret_cast<const std::uint32_t*>(ds.get() + reinterpret_cast<std::uintptr_t>(x.words));
-                    wait_weights();
-                    launch(pr, rg, dpairs, dranges, r, ls.s);
+                    verify_rank_resident(plan, r, ckpt_file(CkptFile::Shard, dir, r), dw.get(), ds, dpairs, dranges, stage, readers,
+                                         step, derr.get<unsigned long long>(), ls.s, wait_weights);
                 }
             } catch (...) {
                 std::lock_guard<std::mutex> lk(mu);
@@ -1236,15 +1282,7 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
         });
     }
     if (lane_err) std::rethrow_exception(lane_err);
-    std::vector<unsigned long long> err(static_cast<std::size_t>(N) * 3);
-    cuda_check(cudaMemcpy(err.data(), derr.get(), derr.size(), cudaMemcpyDeviceToHost), "D2H");
-    bool mismatch = false;
-    for (int r = 0; r < N; ++r) {
-        if (err[3 * r + 1]) fail(ErrorKind::CorruptContainer, dir.string() + ": nonzero padding in rank " + std::to_string(r));
-        if (err[3 * r + 2]) fail(ErrorKind::Consistency, "exp_avg_sq contains a negative or non-finite element");
-        mismatch = mismatch || err[3 * r] != 0;
-    }
-    if (mismatch) fail(ErrorKind::Consistency, dir.string() + ": a weight tensor disagrees with its FP32 master");
+    verify_counters(dir, N, derr.get<unsigned long long>());
 }
 
 } // namespace tailor

@@ -17,6 +17,7 @@
 #include <cstring>
 #include <fcntl.h>
 #include <filesystem>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <thread>
@@ -80,6 +81,7 @@ class FileAssembler {
 
     double device_ms = 0.0, read_ms = 0.0, wait_ms = 0.0, write_ms = 0.0;
     std::uint64_t bytes = 0;
+    void set_read_threads(int n) { workers_ = std::max(1, n); }
 
     void assemble(const PartitionPlan& pp, const std::vector<fs::path>& window_files, const fs::path& out_path) {
         Fd out(out_path, O_WRONLY | O_CREAT | O_TRUNC);
@@ -317,6 +319,7 @@ struct OutputJob {
     const PartitionPlan* plan;
     std::vector<fs::path> window_files;
     fs::path out;
+    int tag = 0; // passed to on_done: -1 = weights, r >= 0 = rank-r shard file
 };
 
 struct AssembleTotals {
@@ -324,11 +327,17 @@ struct AssembleTotals {
     std::uint64_t bytes = 0;
 };
 
-// Runs the output files over up to 16 lanes (largest file first, pulled from a
-// shared queue). Output bytes do not depend on the lane count or timing: each
+// Runs the output files over up to 16 lanes (weights first, then largest first,
+// pulled from a shared queue). Output bytes do not depend on the lane count or timing: each
 // file is produced by exactly one lane, in chunk order.
-AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool uncached, int device) {
-    std::sort(jobs.begin(), jobs.end(), [](const OutputJob& a, const OutputJob& b) {
+// on_done(tag), if set, runs on the lane's thread right after a file is complete (the
+// pipelined re-verify of execute_merge hooks in here).
+AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool uncached, int device,
+                                const std::function<void(int)>& on_done = {}) {
+    // the weights file first (a lane verifying a rank file waits for it: with fewer lanes
+    // than files, taking it last could block every lane), then largest first
+    std::stable_sort(jobs.begin(), jobs.end(), [](const OutputJob& a, const OutputJob& b) {
+        if ((a.tag < 0) != (b.tag < 0)) return a.tag < 0;
         return a.plan->dst_hi - a.plan->dst_lo > b.plan->dst_hi - b.plan->dst_lo;
     });
     const int lanes = std::clamp<int>(std::min<int>(static_cast<int>(jobs.size()), workers), 1, 16);
@@ -350,7 +359,10 @@ AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool u
                     std::lock_guard<std::mutex> lk(mu);
                     if (err) break;
                 }
+                // the weights file is the longest job and the one everything waits for: more readers
+                fa.set_read_threads(jobs[j].tag < 0 ? std::max(readers, 4) : readers);
                 fa.assemble(*jobs[j].plan, jobs[j].window_files, jobs[j].out);
+                if (on_done) on_done(jobs[j].tag);
             }
             part[static_cast<std::size_t>(li)] = {fa.device_ms, fa.read_ms, fa.wait_ms, fa.write_ms, fa.bytes};
         } catch (...) {
@@ -432,27 +444,108 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
     if (ec) fail(ErrorKind::Storage, "cannot create '" + out_dir.string() + "': " + ec.message());
     const int workers = options.workers > 0 ? options.workers : std::max(plan.num_ranks, io_threads());
     phase = std::make_unique<PhaseTimer>("merge.assemble");
-    std::vector<OutputJob> jobs;
-    {
-        OutputJob j{&wplan, {}, ckpt_file(CkptFile::Weights, out_dir)};
-        for (const auto& w : wplan.windows) j.window_files.push_back(ckpt_file(CkptFile::Weights, w.source));
-        jobs.push_back(std::move(j));
-    }
-    for (int r = 0; r < plan.num_ranks; ++r) {
-        const PartitionPlan& sp = splans[static_cast<std::size_t>(r)];
-        OutputJob j{&sp, {}, ckpt_file(CkptFile::Shard, out_dir, r)};
-        for (const auto& w : sp.windows) j.window_files.push_back(ckpt_file(CkptFile::Shard, w.source, w.container));
-        jobs.push_back(std::move(j));
-    }
-    const AssembleTotals fa = assemble_outputs(std::move(jobs), workers, options.uncached, options.device);
+    // Sidecars first: the re-verify reads them back, and it starts while the payload
+    // files are still being assembled.
     write_text_file(ckpt_file(CkptFile::OptimMeta, out_dir), sidecar_text(optim));
     write_text_file(ckpt_file(CkptFile::Config, out_dir), read_text_file(ckpt_file(CkptFile::Config, plan.config_source)));
     write_text_file(ckpt_file(CkptFile::TrainerState, out_dir), read_text_file(ckpt_file(CkptFile::TrainerState, plan.config_source)));
     write_text_file(ckpt_file(CkptFile::Manifest, out_dir), sidecar_text(manifest));
 
+    std::vector<OutputJob> jobs;
+    {
+        OutputJob j{&wplan, {}, ckpt_file(CkptFile::Weights, out_dir), -1};
+        for (const auto& w : wplan.windows) j.window_files.push_back(ckpt_file(CkptFile::Weights, w.source));
+        jobs.push_back(std::move(j));
+    }
+    for (int r = 0; r < plan.num_ranks; ++r) {
+        const PartitionPlan& sp = splans[static_cast<std::size_t>(r)];
+        OutputJob j{&sp, {}, ckpt_file(CkptFile::Shard, out_dir, r), r};
+        for (const auto& w : sp.windows) j.window_files.push_back(ckpt_file(CkptFile::Shard, w.source, w.container));
+        jobs.push_back(std::move(j));
+    }
+
+    // Pipelined re-verify (resident form, when weights + one rank payload per lane fit the
+    // device budget): the lane that finished the weights file loads it to the device; a
+    // lane that finished a rank file re-reads it and runs K6 (after the weights are in).
+    // The on-disk headers are compared with the planned layouts afterwards. Otherwise the
+    // whole directory is verified after assembly (verify_checkpoint_dir).
+    const int N = plan.num_ranks;
+    std::uint64_t max_shard = 16;
+    for (const auto& sp : splans) max_shard = std::max<std::uint64_t>(max_shard, sp.out.payload_bytes);
+    const int lanes_est = std::clamp<int>(std::min<int>(N + 1, workers), 1, 16);
+    const bool pipelined = options.verify && wplan.out.payload_bytes + static_cast<std::uint64_t>(lanes_est) * max_shard <= device_budget();
+    VerifyPlan vplan;
+    DeviceBuffer dw, derr;
+    std::mutex wmu;
+    std::condition_variable wcv;
+    bool weights_in = false;
+    std::exception_ptr werr;
+    std::function<void(int)> on_done;
+    if (pipelined) {
+        const CheckpointSummary vs = read_checkpoint_summary(out_dir);
+        std::vector<ContainerLayout> sl;
+        for (const auto& sp : splans) sl.push_back(sp.out);
+        vplan = verify_plan(out_dir, vs, wplan.out, std::move(sl));
+        dw.resize(std::max<std::uint64_t>(16, wplan.out.payload_bytes));
+        derr.resize(static_cast<std::size_t>(N) * 3 * sizeof(unsigned long long));
+        cuda_check(cudaMemset(derr.get(), 0, derr.size()), "memset");
+        const int readers = std::max(1, io_threads() / lanes_est);
+        on_done = [&](int tag) {
+            PinnedBuffer stage[2];
+            if (tag < 0) {
+                try {
+                    DeviceBuffer& d = dw;
+                    load_payload_to(ckpt_file(CkptFile::Weights, out_dir), wplan.out, d, stage, std::max(readers, 8),
+                                    16ull << 20);
+                } catch (...) {
+                    werr = std::current_exception();
+                }
+                std::lock_guard<std::mutex> lk(wmu);
+                weights_in = true;
+                wcv.notify_all();
+                if (werr) std::rethrow_exception(werr);
+                return;
+            }
+            DeviceBuffer ds, dpairs, dranges;
+            cudaStream_t st = nullptr;
+            cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+            std::unique_ptr<CUstream_st, decltype(&cudaStreamDestroy)> own(st, &cudaStreamDestroy);
+            verify_rank_resident(vplan, tag, ckpt_file(CkptFile::Shard, out_dir, tag), dw.get(), ds, dpairs, dranges, stage,
+                                 readers, 16ull << 20, derr.get<unsigned long long>(), st, [&] {
+                                     std::unique_lock<std::mutex> lk(wmu);
+                                     wcv.wait(lk, [&] { return weights_in; });
+                                     if (werr) std::rethrow_exception(werr);
+                                 });
+        };
+    }
+    const AssembleTotals fa = assemble_outputs(std::move(jobs), workers, options.uncached, options.device, on_done);
     alloc_stats().trace("merge.assemble allocations");
     phase = std::make_unique<PhaseTimer>("merge.verify");
-    if (options.verify) verify_checkpoint_dir(out_dir.string(), options.device);
+    if (pipelined) {
+        // structure on disk == the planned layouts (what read_checkpoint's deserialize checks)
+        const auto same = [](const ContainerLayout& a, const ContainerLayout& b) {
+            if (a.payload_offset() != b.payload_offset() || a.payload_bytes != b.payload_bytes ||
+                a.entries.size() != b.entries.size() || a.metadata != b.metadata)
+                return false;
+            for (std::size_t i = 0; i < a.entries.size(); ++i)
+                if (a.entries[i].name != b.entries[i].name || a.entries[i].begin != b.entries[i].begin ||
+                    a.entries[i].end != b.entries[i].end || a.entries[i].dtype != b.entries[i].dtype ||
+                    a.entries[i].shape != b.entries[i].shape)
+                    return false;
+            return true;
+        };
+        std::size_t files = 0;
+        for ([[maybe_unused]] const auto& e : fs::directory_iterator(out_dir / "optim")) ++files;
+        if (files != static_cast<std::size_t>(N)) fail(ErrorKind::Consistency, out_dir.string() + ": unexpected shard file count");
+        if (!same(read_layout(ckpt_file(CkptFile::Weights, out_dir)), wplan.out))
+            fail(ErrorKind::CorruptContainer, out_dir.string() + ": weights header differs from the plan");
+        for (int r = 0; r < N; ++r)
+            if (!same(read_layout(ckpt_file(CkptFile::Shard, out_dir, r)), splans[static_cast<std::size_t>(r)].out))
+                fail(ErrorKind::CorruptContainer, out_dir.string() + ": shard " + std::to_string(r) + " header differs from the plan");
+        verify_counters(out_dir, N, derr.get<unsigned long long>());
+    } else if (options.verify) {
+        verify_checkpoint_dir(out_dir.string(), options.device);
+    }
     phase.reset();
     alloc_stats().trace("merge.verify allocations (cumulative)");
 
@@ -582,9 +675,9 @@ MergeStats execute_regroup(const fs::path& src, const fs::path& out_dir, Groupin
         return files;
     };
     std::vector<OutputJob> jobs;
-    jobs.push_back({&wp, files_of(wp), ckpt_file(CkptFile::Weights, out_dir)});
+    jobs.push_back({&wp, files_of(wp), ckpt_file(CkptFile::Weights, out_dir), -1});
     for (int r = 0; r < N; ++r)
-        jobs.push_back({&plans[static_cast<std::size_t>(r)], files_of(plans[static_cast<std::size_t>(r)]), ckpt_file(CkptFile::Shard, out_dir, r)});
+        jobs.push_back({&plans[static_cast<std::size_t>(r)], files_of(plans[static_cast<std::size_t>(r)]), ckpt_file(CkptFile::Shard, out_dir, r), r});
     const AssembleTotals fa = assemble_outputs(std::move(jobs), workers, false, options.device);
     write_text_file(ckpt_file(CkptFile::OptimMeta, out_dir), sidecar_text(optim));
     write_text_file(ckpt_file(CkptFile::Config, out_dir), sidecar_text(spec));

@@ -9,6 +9,7 @@
 
 #include <cstdint>
 #include <mutex>
+#include <functional>
 #include <map>
 #include <memory>
 #include <string>
@@ -289,5 +290,28 @@ class HostMerge {
 // Device re-verify of a checkpoint directory (duality, zero padding,
 // exp_avg_sq >= 0) plus the structural checks of read_checkpoint.
 void verify_checkpoint_dir(const std::string& dir, int device);
+
+// The pieces of the device re-verify (read_checkpoint's checks), reusable by callers
+// that already hold the layouts (execute_merge verifies files as its lanes finish them):
+// verify_plan = structural checks + per-rank work lists as payload offsets;
+// verify_rank_resident = load one rank payload, run K6 against a device weights payload
+// (counters at d_err[3r..3r+2]; `before_kernel` may block, e.g. until the weights are in);
+// verify_counters = the errors, in rank order.
+struct VerifyPlan {
+    ContainerLayout weights;
+    std::vector<ContainerLayout> shards;
+    std::vector<std::vector<dev::VerifyPair>> pairs;   // master / weight offsets
+    std::vector<std::vector<dev::VerifyRange>> ranges; // payload offsets
+    std::uint64_t max_shard = 16;
+};
+VerifyPlan verify_plan(const std::filesystem::path& dir, const CheckpointSummary& s, ContainerLayout weights,
+                       std::vector<ContainerLayout> shards);
+void verify_rank_resident(const VerifyPlan& plan, int r, const std::filesystem::path& shard_file, const std::uint8_t* dw,
+                          DeviceBuffer& ds, DeviceBuffer& dpairs, DeviceBuffer& dranges, PinnedBuffer* stage, int readers,
+                          std::uint64_t step, unsigned long long* d_err, cudaStream_t st,
+                          const std::function<void()>& before_kernel);
+void verify_counters(const std::filesystem::path& dir, int num_ranks, const unsigned long long* d_err);
+void load_payload_to(const std::filesystem::path& path, const ContainerLayout& lay, DeviceBuffer& dst, PinnedBuffer* stage,
+                     int threads, std::uint64_t step);
 
 } // namespace tailor
