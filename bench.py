@@ -549,8 +549,8 @@ def our_arm(args, rank, world, local_rank):
                    "composite_bytes_per_gpu_step": composite, "parallelism": f"zero-partition x{world}",
                    "l2": f"inputs {resident / 1e9:.1f} GB/GPU vs 126 MB L2"
                          + (" (no flush needed)" if resident > 1e9 else " (L2-resident: small workload)"),
-                   "gather_variant": {0: "auto", 1: "lsu", 2: "bulk-4x48K", 3: "bulk-6x32K", 4: "bulk-2cta-3x32K",
-                                      5: "bulk-3x64K", 6: "bulk-8x24K"}[args.variant],
+                   "gather_variant": {0: "auto (bulk-3x64K)", 1: "lsu", 2: "bulk-3x64K", 3: "bulk-6x32K", 4: "bulk-2cta-3x32K",
+                                      5: "bulk-4x48K", 6: "bulk-8x24K"}[args.variant],
                    "score_variant": SCORE_VARIANTS[args.score_variant],
                    "plan_ms_uncached": round(plan_ms, 3), "min_boundary_gap": state["gap"],
                    "selection": "host (D2H partials)" if args.host_select else "device (K9, no host round trip)",
@@ -1179,7 +1179,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS) + ["files", "train"], default="cfg3")
-    ap.add_argument("--variant", type=int, default=0, help="gather: 0 auto, 1 LSU, 2 TMA bulk")
+    ap.add_argument("--variant", type=int, default=0, help="gather: 0 auto, 1 LSU, 2 TMA bulk 3x64K, 3-6 other rings")
     ap.add_argument("--score-variant", type=int, default=0, help="scorer: 0 auto, 1 register, 2 TMA-staged")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-select", action="store_true", help="select + plan on the host instead of K9")

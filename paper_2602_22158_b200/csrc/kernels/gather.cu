@@ -29,8 +29,10 @@ constexpr int kLsuThreads = 256;
 constexpr std::uint64_t kLsuTile = 64 * 1024;
 constexpr int kLsuUnroll = 8;
 
-constexpr int kBulkStages = 4;
-constexpr std::uint32_t kBulkStage = 48 * 1024;
+// Ring: 3 x 64 KB (sweep on B200, cfg3 shard gather: 3x64K 4.155 ms, 4x48K 4.20, 3x72K
+// 4.18, 4x56K 4.22, 6x32K 4.19, 2 CTAs x 3x32K 4.20, 8x24K 4.32).
+constexpr int kBulkStages = 3;
+constexpr std::uint32_t kBulkStage = 64 * 1024;
 
 __device__ __forceinline__ int seg_lookup(const GatherSeg* __restrict__ segs, std::uint32_t n, std::uint64_t x) {
     int lo = 0, hi = static_cast<int>(n) - 1, ans = -1;
@@ -259,10 +261,10 @@ cudaError_t launch_gather(const GatherSeg* d_segs, std::uint32_t nseg, std::uint
     const int sms = sm_count();
     const bool bulk = variant >= kGatherBulk || (variant == kGatherAuto && bulk_ok);
     if (bulk && bulk_ok) {
-        switch (variant) { // ring shapes for experiments; auto/2 = 4 x 48 KB, one CTA per SM
+        switch (variant) { // ring shapes for experiments; auto/2 = 3 x 64 KB, one CTA per SM
             case kGatherBulk6x32: return launch_bulk<6, 32 * 1024>(d_segs, nseg, d_dst, dst_bytes, 1, stream);
             case kGatherBulk2Cta: return launch_bulk<3, 32 * 1024>(d_segs, nseg, d_dst, dst_bytes, 2, stream);
-            case kGatherBulk3x64: return launch_bulk<3, 64 * 1024>(d_segs, nseg, d_dst, dst_bytes, 1, stream);
+            case kGatherBulk4x48: return launch_bulk<4, 48 * 1024>(d_segs, nseg, d_dst, dst_bytes, 1, stream);
             case kGatherBulk8x24: return launch_bulk<8, 24 * 1024>(d_segs, nseg, d_dst, dst_bytes, 1, stream);
             default: return launch_bulk<kBulkStages, kBulkStage>(d_segs, nseg, d_dst, dst_bytes, 1, stream);
         }

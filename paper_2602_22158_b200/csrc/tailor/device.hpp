@@ -21,7 +21,7 @@ struct GatherSeg {
 };
 static_assert(sizeof(GatherSeg) == 24, "GatherSeg is part of the C ABI");
 
-// kGatherBulk = 4 x 48 KB ring, one CTA per SM (default); the other bulk
+// kGatherBulk = 3 x 64 KB ring, one CTA per SM (default); the other bulk
 // shapes exist for measured comparisons (profiles/).
 enum GatherVariant : int {
     kGatherAuto = 0,
@@ -29,7 +29,7 @@ enum GatherVariant : int {
     kGatherBulk = 2,
     kGatherBulk6x32 = 3,
     kGatherBulk2Cta = 4,
-    kGatherBulk3x64 = 5,
+    kGatherBulk4x48 = 5, // the previous default ring
     kGatherBulk8x24 = 6
 };
 
