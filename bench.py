@@ -221,16 +221,19 @@ class ClockSampler:
             return sm, mx, reasons
 
         sm, mx, reasons = collect(self.t0, self.t1)
-        widened = False
-        if not sm and self.nvml:  # region shorter than the poll period: nearest samples around it
-            sm, mx, reasons = collect(self.t0 - 0.01, self.t1 + 0.01)
-            widened = True
+        widened = 0.0
+        for pad in (0.01, 0.05, 0.25):  # region shorter than the poll period: nearest samples around it
+            if sm or not self.nvml:
+                break
+            sm, mx, reasons = collect(self.t0 - pad, self.t1 + pad)
+            widened = pad
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm),
                "source": "nvml 2 ms" if self.nvml else "nvidia-smi -lms 20"}
         if widened:
-            out["window"] = f"timed region {1e3 * (self.t1 - self.t0):.2f} ms < poll period: samples within 10 ms of it"
+            out["window"] = (f"timed region {1e3 * (self.t1 - self.t0):.2f} ms < poll period: samples within "
+                             f"{1e3 * widened:.0f} ms of it")
         return out
 
 
