@@ -3,7 +3,7 @@
 # drives K2 bulk + LSU, K3 staged + register, K5, K6, K7/K8, K9 on small shapes).
 mkdir -p gpurun_out
 for tool in memcheck racecheck synccheck; do
-    timeout 2400 compute-sanitizer --tool $tool --error-exitcode 9 python tools/sanitize_run.py \
+    TAILOR_SANITIZE_TOOL=$tool timeout 2400 compute-sanitizer --tool $tool --error-exitcode 9 python tools/sanitize_run.py \
         > gpurun_out/san_$tool.txt 2>&1
     echo "$tool rc=$?" >> gpurun_out/san_$tool.txt
     tail -3 gpurun_out/san_$tool.txt
