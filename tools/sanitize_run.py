@@ -5,6 +5,7 @@ Covers K5 generator (shards, weights, packed masters, tensor-aligned windows), K
 (TMA ring + register + scalar paths), K9 device selection, K2 gather (bulk + LSU, aligned +
 misaligned shapes, host pipeline with prefetch copies), K6 verify (through execute_merge),
 K7/K8 trainer (through train, magnitude strategy)."""
+import os
 import pathlib
 import sys
 import tempfile
