@@ -15,11 +15,13 @@
 //   merge    resolve_plan + execute_merge (R/src/merge.cpp:39-357) on a JSON recipe
 //   plan     recipe_from_manifests (R/src/merge.cpp:359-418)
 //   train    the reference toy trainer (R/src/trainer.cpp:109-123) + optional inject_failure
+//   resume   resume from a complete checkpoint (R/src/trainer.cpp:125-152)
 //   score    CPU restatement of the update-magnitude scorer and the
 //            magnitude selection → recipe mapping (a14) over read_checkpoint output
 //   select-merge   score → select → resolve_plan → execute_merge, timed (reference arm)
 //   verify   verify_checkpoints (R/src/verify.cpp:46-112)
 //   read     read_checkpoint (R/src/checkpoint.cpp:485-575) — full validation
+//   regroup  read_checkpoint -> coarse_to_fine / fine_to_coarse -> write_checkpoint
 #include <algorithm>
 #include <chrono>
 #include <cmath>
