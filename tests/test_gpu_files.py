@@ -198,3 +198,35 @@ def test_regroup_cli_and_errors(tmp_path):
     with pytest.raises(t.TailorError) as e:
         t.regroup(str(tmp_path / "part" / "checkpoint-100"), str(tmp_path / "x"))
     assert e.value.kind == t.ErrorKind.MissingModules
+
+
+@pytest.mark.parametrize("damage", ["negative_v", "weight_bit"])
+def test_merge_reverify_catches_bad_source_data(tmp_path, damage):
+    """A source with valid structure but bad payload data (a negative exp_avg_sq, a weight
+    that no longer matches its master) merges into a bad composite; the re-verify inside
+    execute_merge — pipelined into the file lanes — must refuse it with the reference's
+    error kind (ConsistencyError, exit 2)."""
+    need_gpu()
+    import struct
+
+    d = gen(tmp_path, SPEC, 2, 2)
+    bad = tmp_path / "bad"
+    shutil.copytree(d[0], bad)
+    if damage == "weight_bit":
+        w = bytearray((bad / "model.weights").read_bytes())
+        w[-7] ^= 0x10
+        (bad / "model.weights").write_bytes(bytes(w))
+    else:
+        p = bad / "optim" / "rank_1.shard"
+        b = bytearray(p.read_bytes())
+        hlen = int.from_bytes(b[:8], "little")
+        hdr = json.loads(b[8:8 + hlen])
+        lo, _ = hdr["g0.exp_avg_sq"]["data_offsets"]
+        b[8 + hlen + lo:8 + hlen + lo + 4] = struct.pack("<f", -3.0)
+        p.write_bytes(bytes(b))
+    # the damaged source provides everything (base), so the composite carries the defect
+    recipe = t.MergeRecipe(num_ranks=2, base_checkpoint=str(bad), slices=[t.RecipeSlice(d[1], [1])])
+    rc, err = ref_error(recipe, tmp_path / "ref_out")
+    e = our_error(recipe, tmp_path / "our_out")
+    assert rc == 2 and err == "ConsistencyError", (rc, err)
+    assert e is not None and e.kind == t.ErrorKind.Consistency, e
