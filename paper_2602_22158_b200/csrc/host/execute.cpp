@@ -393,6 +393,105 @@ AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool u
     return tot;
 }
 
+// Pipelined re-verify (resident form, when weights + one rank payload per lane fit the
+// device budget): the lane that finished the weights file loads it to the device; a
+// lane that finished a rank file re-reads it and runs K6 (after the weights are in).
+// The on-disk headers are compared with the planned layouts afterwards. Otherwise the
+// whole directory is verified after assembly (verify_checkpoint_dir). The sidecars must
+// be written before the assembly starts.
+class LaneVerifier {
+  public:
+    LaneVerifier(const fs::path& out_dir, const PartitionPlan* wplan, const std::vector<PartitionPlan>& splans, int workers,
+                 bool verify)
+        : out_(out_dir), wplan_(wplan), splans_(splans), verify_(verify), N_(static_cast<int>(splans.size())) {
+        std::uint64_t max_shard = 16;
+        for (const auto& sp : splans) max_shard = std::max<std::uint64_t>(max_shard, sp.out.payload_bytes);
+        lanes_ = std::clamp<int>(std::min<int>(N_ + 1, workers), 1, 16);
+        pipelined_ = verify && wplan->out.payload_bytes + static_cast<std::uint64_t>(lanes_) * max_shard <= device_budget();
+        if (!pipelined_) return;
+        const CheckpointSummary vs = read_checkpoint_summary(out_dir);
+        std::vector<ContainerLayout> sl;
+        for (const auto& sp : splans) sl.push_back(sp.out);
+        vplan_ = verify_plan(out_dir, vs, wplan->out, std::move(sl));
+        dw_.resize(std::max<std::uint64_t>(16, wplan->out.payload_bytes));
+        derr_.resize(static_cast<std::size_t>(N_) * 3 * sizeof(unsigned long long));
+        cuda_check(cudaMemset(derr_.get(), 0, derr_.size()), "memset");
+    }
+
+    // on_done hook for assemble_outputs (empty when not pipelined)
+    std::function<void(int)> hook() {
+        if (!pipelined_) return {};
+        const int readers = std::max(1, io_threads() / lanes_);
+        return [this, readers](int tag) {
+            PinnedBuffer stage[2];
+            if (tag < 0) {
+                try {
+                    load_payload_to(ckpt_file(CkptFile::Weights, out_), wplan_->out, dw_, stage, std::max(readers, 8), 16ull << 20);
+                } catch (...) {
+                    werr_ = std::current_exception();
+                }
+                std::lock_guard<std::mutex> lk(mu_);
+                weights_in_ = true;
+                cv_.notify_all();
+                if (werr_) std::rethrow_exception(werr_);
+                return;
+            }
+            DeviceBuffer ds, dpairs, dranges;
+            cudaStream_t st = nullptr;
+            cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+            std::unique_ptr<CUstream_st, decltype(&cudaStreamDestroy)> own(st, &cudaStreamDestroy);
+            verify_rank_resident(vplan_, tag, ckpt_file(CkptFile::Shard, out_, tag), dw_.get(), ds, dpairs, dranges, stage, readers,
+                                 16ull << 20, derr_.get<unsigned long long>(), st, [this] {
+                                     std::unique_lock<std::mutex> lk(mu_);
+                                     cv_.wait(lk, [this] { return weights_in_; });
+                                     if (werr_) std::rethrow_exception(werr_);
+                                 });
+        };
+    }
+
+    // after assembly: headers on disk == the planned layouts (what read_checkpoint's
+    // deserialize checks) and the counters, or the whole post-assembly verify
+    void finish(int device) {
+        if (!pipelined_) {
+            if (verify_) verify_checkpoint_dir(out_.string(), device);
+            return;
+        }
+        const auto same = [](const ContainerLayout& a, const ContainerLayout& b) {
+            if (a.payload_offset() != b.payload_offset() || a.payload_bytes != b.payload_bytes ||
+                a.entries.size() != b.entries.size() || a.metadata != b.metadata)
+                return false;
+            for (std::size_t i = 0; i < a.entries.size(); ++i)
+                if (a.entries[i].name != b.entries[i].name || a.entries[i].begin != b.entries[i].begin ||
+                    a.entries[i].end != b.entries[i].end || a.entries[i].dtype != b.entries[i].dtype ||
+                    a.entries[i].shape != b.entries[i].shape)
+                    return false;
+            return true;
+        };
+        std::size_t files = 0;
+        for ([[maybe_unused]] const auto& e : fs::directory_iterator(out_ / "optim")) ++files;
+        if (files != static_cast<std::size_t>(N_)) fail(ErrorKind::Consistency, out_.string() + ": unexpected shard file count");
+        if (!same(read_layout(ckpt_file(CkptFile::Weights, out_)), wplan_->out))
+            fail(ErrorKind::CorruptContainer, out_.string() + ": weights header differs from the plan");
+        for (int r = 0; r < N_; ++r)
+            if (!same(read_layout(ckpt_file(CkptFile::Shard, out_, r)), splans_[static_cast<std::size_t>(r)].out))
+                fail(ErrorKind::CorruptContainer, out_.string() + ": shard " + std::to_string(r) + " header differs from the plan");
+        verify_counters(out_, N_, derr_.get<unsigned long long>());
+    }
+
+  private:
+    fs::path out_;
+    const PartitionPlan* wplan_;
+    const std::vector<PartitionPlan>& splans_;
+    bool verify_, pipelined_ = false;
+    int N_, lanes_ = 1;
+    VerifyPlan vplan_;
+    DeviceBuffer dw_, derr_;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    bool weights_in_ = false;
+    std::exception_ptr werr_;
+};
+
 } // namespace
 
 MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const MergeOptions& options) {
@@ -464,88 +563,11 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
         jobs.push_back(std::move(j));
     }
 
-    // Pipelined re-verify (resident form, when weights + one rank payload per lane fit the
-    // device budget): the lane that finished the weights file loads it to the device; a
-    // lane that finished a rank file re-reads it and runs K6 (after the weights are in).
-    // The on-disk headers are compared with the planned layouts afterwards. Otherwise the
-    // whole directory is verified after assembly (verify_checkpoint_dir).
-    const int N = plan.num_ranks;
-    std::uint64_t max_shard = 16;
-    for (const auto& sp : splans) max_shard = std::max<std::uint64_t>(max_shard, sp.out.payload_bytes);
-    const int lanes_est = std::clamp<int>(std::min<int>(N + 1, workers), 1, 16);
-    const bool pipelined = options.verify && wplan.out.payload_bytes + static_cast<std::uint64_t>(lanes_est) * max_shard <= device_budget();
-    VerifyPlan vplan;
-    DeviceBuffer dw, derr;
-    std::mutex wmu;
-    std::condition_variable wcv;
-    bool weights_in = false;
-    std::exception_ptr werr;
-    std::function<void(int)> on_done;
-    if (pipelined) {
-        const CheckpointSummary vs = read_checkpoint_summary(out_dir);
-        std::vector<ContainerLayout> sl;
-        for (const auto& sp : splans) sl.push_back(sp.out);
-        vplan = verify_plan(out_dir, vs, wplan.out, std::move(sl));
-        dw.resize(std::max<std::uint64_t>(16, wplan.out.payload_bytes));
-        derr.resize(static_cast<std::size_t>(N) * 3 * sizeof(unsigned long long));
-        cuda_check(cudaMemset(derr.get(), 0, derr.size()), "memset");
-        const int readers = std::max(1, io_threads() / lanes_est);
-        on_done = [&](int tag) {
-            PinnedBuffer stage[2];
-            if (tag < 0) {
-                try {
-                    DeviceBuffer& d = dw;
-                    load_payload_to(ckpt_file(CkptFile::Weights, out_dir), wplan.out, d, stage, std::max(readers, 8),
-                                    16ull << 20);
-                } catch (...) {
-                    werr = std::current_exception();
-                }
-                std::lock_guard<std::mutex> lk(wmu);
-                weights_in = true;
-                wcv.notify_all();
-                if (werr) std::rethrow_exception(werr);
-                return;
-            }
-            DeviceBuffer ds, dpairs, dranges;
-            cudaStream_t st = nullptr;
-            cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
-            std::unique_ptr<CUstream_st, decltype(&cudaStreamDestroy)> own(st, &cudaStreamDestroy);
-            verify_rank_resident(vplan, tag, ckpt_file(CkptFile::Shard, out_dir, tag), dw.get(), ds, dpairs, dranges, stage,
-                                 readers, 16ull << 20, derr.get<unsigned long long>(), st, [&] {
-                                     std::unique_lock<std::mutex> lk(wmu);
-                                     wcv.wait(lk, [&] { return weights_in; });
-                                     if (werr) std::rethrow_exception(werr);
-                                 });
-        };
-    }
-    const AssembleTotals fa = assemble_outputs(std::move(jobs), workers, options.uncached, options.device, on_done);
+    LaneVerifier lv(out_dir, &wplan, splans, workers, options.verify);
+    const AssembleTotals fa = assemble_outputs(std::move(jobs), workers, options.uncached, options.device, lv.hook());
     alloc_stats().trace("merge.assemble allocations");
     phase = std::make_unique<PhaseTimer>("merge.verify");
-    if (pipelined) {
-        // structure on disk == the planned layouts (what read_checkpoint's deserialize checks)
-        const auto same = [](const ContainerLayout& a, const ContainerLayout& b) {
-            if (a.payload_offset() != b.payload_offset() || a.payload_bytes != b.payload_bytes ||
-                a.entries.size() != b.entries.size() || a.metadata != b.metadata)
-                return false;
-            for (std::size_t i = 0; i < a.entries.size(); ++i)
-                if (a.entries[i].name != b.entries[i].name || a.entries[i].begin != b.entries[i].begin ||
-                    a.entries[i].end != b.entries[i].end || a.entries[i].dtype != b.entries[i].dtype ||
-                    a.entries[i].shape != b.entries[i].shape)
-                    return false;
-            return true;
-        };
-        std::size_t files = 0;
-        for ([[maybe_unused]] const auto& e : fs::directory_iterator(out_dir / "optim")) ++files;
-        if (files != static_cast<std::size_t>(N)) fail(ErrorKind::Consistency, out_dir.string() + ": unexpected shard file count");
-        if (!same(read_layout(ckpt_file(CkptFile::Weights, out_dir)), wplan.out))
-            fail(ErrorKind::CorruptContainer, out_dir.string() + ": weights header differs from the plan");
-        for (int r = 0; r < N; ++r)
-            if (!same(read_layout(ckpt_file(CkptFile::Shard, out_dir, r)), splans[static_cast<std::size_t>(r)].out))
-                fail(ErrorKind::CorruptContainer, out_dir.string() + ": shard " + std::to_string(r) + " header differs from the plan");
-        verify_counters(out_dir, N, derr.get<unsigned long long>());
-    } else if (options.verify) {
-        verify_checkpoint_dir(out_dir.string(), options.device);
-    }
+    lv.finish(options.device);
     phase.reset();
     alloc_stats().trace("merge.verify allocations (cumulative)");
 
@@ -678,12 +700,14 @@ MergeStats execute_regroup(const fs::path& src, const fs::path& out_dir, Groupin
     jobs.push_back({&wp, files_of(wp), ckpt_file(CkptFile::Weights, out_dir), -1});
     for (int r = 0; r < N; ++r)
         jobs.push_back({&plans[static_cast<std::size_t>(r)], files_of(plans[static_cast<std::size_t>(r)]), ckpt_file(CkptFile::Shard, out_dir, r), r});
-    const AssembleTotals fa = assemble_outputs(std::move(jobs), workers, false, options.device);
+    // sidecars first: the pipelined re-verify reads them back while the files assemble
     write_text_file(ckpt_file(CkptFile::OptimMeta, out_dir), sidecar_text(optim));
     write_text_file(ckpt_file(CkptFile::Config, out_dir), sidecar_text(spec));
     write_text_file(ckpt_file(CkptFile::TrainerState, out_dir), sidecar_text(s.trainer));
     write_text_file(ckpt_file(CkptFile::Manifest, out_dir), sidecar_text(s.manifest));
-    if (options.verify) verify_checkpoint_dir(out_dir.string(), options.device);
+    LaneVerifier lv(out_dir, &wp, plans, workers, options.verify);
+    const AssembleTotals fa = assemble_outputs(std::move(jobs), workers, false, options.device, lv.hook());
+    lv.finish(options.device);
     stats.device_ms = fa.device_ms;
     stats.bytes_moved = fa.bytes;
     stats.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
