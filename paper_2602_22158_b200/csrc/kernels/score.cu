@@ -181,6 +181,11 @@ __global__ void score_combine_kernel(const double* __restrict__ partials, const 
 // order inside a tile differs from the register kernel, so the two variants
 // agree to ~1e-15, not bitwise.
 constexpr int kStagedSmem = 192 * 1024;
+// CTAs per SM: small K runs two (each with half the ring) for more independent streams
+template <int K>
+__host__ __device__ constexpr int staged_ctas() {
+    return K < 4 ? 2 : 1;
+}
 constexpr int kStagedThreads = kScoreThreads + 32; // 8 consumer warps + 1 producer warp
 
 // float4 per consumer thread per snapshot row in one stage: small K gets wider
@@ -197,7 +202,7 @@ __host__ __device__ constexpr int chunk_elems() {
 template <int K>
 __host__ __device__ constexpr int staged_stages() {
     constexpr int per = K * chunk_elems<K>() * 4;
-    constexpr int s = kStagedSmem / per;
+    constexpr int s = kStagedSmem / staged_ctas<K>() / per;
     return s < 2 ? 2 : (s > 8 ? 8 : s);
 }
 
@@ -326,7 +331,8 @@ cudaError_t launch_staged(const ScoreTile* d_tiles, std::uint32_t ntiles, const 
     if (const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(score_staged_kernel<K>), smem, attr);
         e != cudaSuccess)
         return e;
-    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ntiles, static_cast<std::uint64_t>(sm_count())));
+    const unsigned grid = static_cast<unsigned>(
+        std::min<std::uint64_t>(ntiles, static_cast<std::uint64_t>(sm_count()) * staged_ctas<K>()));
     score_staged_kernel<K><<<grid, kStagedThreads, smem, stream>>>(d_tiles, ntiles, d_field_base, nfields, d_out);
     return cudaGetLastError();
 }

@@ -66,11 +66,12 @@ constexpr int kNarrowMinK = 1 << 20;
 // mbarriers). Measured on B200 (bench events, fraction of the 6543 GB/s copy peak):
 // K=16 1.093 vs register 0.951; K=4 1.075 vs 1.064. At K=2 its first form lost (cfg2:
 // 1.83 vs 1.28 ms: 8 KB stages need ~6 stages/us per SM from one producer lane; a deeper
-// ring did not help); with 4 float4 rows per thread per stage (32 KB stages) it ties the
-// register kernel (1.30 vs 1.27 ms) -> auto picks it for K >= 4 when the bases are 16-B
-// aligned. (Its very first version, one CTA-wide barrier per chunk, was barrier-bound:
-// 0.88 / 0.61.)
-constexpr int kStagedMinK = 4;
+// ring did not help); with 4 float4 rows per thread per stage (32 KB stages) it tied the
+// register kernel (1.30 vs 1.27 ms), and with two CTAs per SM for K < 4 (half the ring
+// each: more independent streams) it wins (1.23 ms; at K=4 two CTAs lose: 2.65 vs 2.47)
+// -> auto picks it whenever the bases are 16-B aligned. (Its very first version, one
+// CTA-wide barrier per chunk, was barrier-bound: 0.88 / 0.61.)
+constexpr int kStagedMinK = 2;
 cudaError_t launch_score_partials(const ScoreTile* d_tiles, std::uint32_t ntiles, const float* const* d_field_base,
                                   std::uint32_t nfields, int K, bool vec_ok, double* d_tile_partials, cudaStream_t stream,
                                   int variant = kScoreAuto);
