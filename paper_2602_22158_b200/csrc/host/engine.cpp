@@ -562,6 +562,7 @@ ScorePlan::ScorePlan(const ModelLayout& model, int num_ranks, std::vector<std::v
                      std::uint32_t tile_elems)
     : K_(static_cast<int>(field_offsets.size())), M_(model.module_count()), offs_(std::move(field_offsets)) {
     if (K_ < 2 || K_ > dev::kMaxSnapshots) fail(ErrorKind::Geometry, "scoring needs 2..16 snapshots");
+    if (const char* v = std::getenv("TAILOR_SCORE_VARIANT"); v && *v) variant_ = std::atoi(v);
     tile_elems = std::max<std::uint32_t>(4, tile_elems & ~3u);
     fields_ = score_fields(model, num_ranks);
     for (const auto& o : offs_) {

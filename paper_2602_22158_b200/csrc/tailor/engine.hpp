@@ -157,7 +157,7 @@ class ScorePlan {
     void set_variant(int v) { variant_ = v; }
 
   private:
-    int variant_ = dev::kScoreAuto;
+    int variant_ = dev::kScoreAuto; // TAILOR_SCORE_VARIANT (diagnostics) sets the default; set_variant overrides
     int K_, M_;
     std::vector<ScoreField> fields_;
     std::vector<std::vector<std::uint64_t>> offs_;
