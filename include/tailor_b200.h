@@ -56,12 +56,18 @@ typedef struct tg_model_spec {
 } tg_model_spec;
 
 /* MergeOptions / MergeStats (R/include/tailor/merge.hpp:46-55), extended with
- * device timing and the composite byte count. */
+ * device timing, the composite byte count and the devices the output lanes run on.
+ * A zero-initialised struct means: workers = default, cached, device 0, re-verify on
+ * (the reference always re-verifies, R/src/merge.cpp:353). */
 typedef struct tg_merge_options {
-    int32_t workers;  /* host read threads; 0 = num_ranks */
-    int32_t uncached; /* reload source shard per group copy (benchmark mode) */
-    int32_t device;
-    int32_t verify; /* device re-verify of the output (reference always re-verifies) */
+    int32_t workers;        /* output/IO lanes; 0 = max(num_ranks, host threads) */
+    int32_t uncached;       /* reload source shard per group copy (benchmark mode) */
+    int32_t device;         /* the device of every lane when num_devices == 0 */
+    int32_t skip_verify;    /* 1 = skip the device re-verify of the written composite */
+    const int32_t* devices; /* num_devices > 0: lanes spread round-robin over devices[0..num_devices);
+                               output bytes do not depend on the devices (R/tests/acceptance.cpp:442-458) */
+    int32_t num_devices;
+    int32_t reserved;
 } tg_merge_options;
 
 typedef struct tg_merge_stats {
@@ -156,13 +162,15 @@ int tg_trainer_partition(tg_trainer* t, int32_t rank, void** d_ptr, uint64_t* by
 int tg_verify_checkpoint(const char* dir, int32_t device);
 /* Update-magnitude scores of consecutive snapshot directories on the device
  * (SURVEY §8 a13): sums[(p*M + m)*2 + {0,1}] = (sum delta^2, sum ref^2) of
- * pair p = (dirs[p], dirs[p+1]); scores[p*M + m]. Capacity: (n-1)*M. */
-int tg_score_snapshots(const char* const* dirs, int32_t n, int32_t device, double* sums, double* scores,
-                       int32_t* num_modules);
+ * pair p = (dirs[p], dirs[p+1]); scores[p*M + m]. Capacity: (n-1)*M. Any n >= 2.
+ * Rank partitions are scored by lanes spread over devices[0..num_devices)
+ * (NULL / 0 = device 0) and combined in rank order: results do not depend on the devices. */
+int tg_score_snapshots(const char* const* dirs, int32_t n, const int32_t* devices, int32_t num_devices, double* sums,
+                       double* scores, int32_t* num_modules);
 /* Score -> magnitude selection (a14) -> recipe (latest-version rule,
  * R/src/merge.cpp:375-417). source_of[m] = index into dirs. */
-int tg_select_recipe(const char* const* dirs, int32_t n, double rho, int32_t device, char* yaml_out, size_t cap,
-                     size_t* needed, int32_t* source_of, double* min_boundary_gap);
+int tg_select_recipe(const char* const* dirs, int32_t n, double rho, const int32_t* devices, int32_t num_devices,
+                     char* yaml_out, size_t cap, size_t* needed, int32_t* source_of, double* min_boundary_gap);
 /* parse_config_json (R/src/checkpoint.cpp:123-136): model config.json text -> spec. */
 int tg_parse_config(const char* config_json, tg_model_spec* spec);
 /* Layer map (R/src/model.cpp, R/src/groups.cpp, R/src/shard.cpp) as JSON. */

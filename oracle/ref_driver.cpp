@@ -30,9 +30,11 @@
 #include <filesystem>
 #include <iostream>
 #include <map>
+#include <mutex>
 #include <optional>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <json.hpp>
@@ -421,11 +423,28 @@ MergeRecipe recipe_from_selection(const std::vector<CheckpointSummary>& snaps,
 
 json score_and_select(const Args& a, MergeRecipe* recipe_out, double* score_ms) {
     const auto t0 = Clock::now();
-    std::vector<CheckpointData> snaps;
-    std::vector<CheckpointSummary> sums;
-    for (const auto& p : split(a.str("snapshots"), ',')) {
-        snaps.push_back(read_checkpoint(p));
-        sums.push_back(read_checkpoint_summary(p));
+    // Snapshots are independent: each is read (read_checkpoint, full validation) on its
+    // own thread, as the reference's ShardLoader spreads file loads over std::threads
+    // (R/src/merge.cpp:157-205); the first error is rethrown after the join.
+    const auto paths = split(a.str("snapshots"), ',');
+    std::vector<CheckpointData> snaps(paths.size());
+    std::vector<CheckpointSummary> sums(paths.size());
+    {
+        std::exception_ptr err;
+        std::mutex mu;
+        std::vector<std::thread> pool;
+        for (std::size_t i = 0; i < paths.size(); ++i)
+            pool.emplace_back([&, i] {
+                try {
+                    snaps[i] = read_checkpoint(paths[i]);
+                    sums[i] = read_checkpoint_summary(paths[i]);
+                } catch (...) {
+                    std::lock_guard<std::mutex> lk(mu);
+                    if (!err) err = std::current_exception();
+                }
+            });
+        for (auto& th : pool) th.join();
+        if (err) std::rethrow_exception(err);
     }
     if (snaps.size() < 2) fail(ErrorKind::Recipe, "scoring needs at least two snapshots");
     const ScoreResult sr = score_snapshots(snaps);

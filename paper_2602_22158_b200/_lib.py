@@ -54,7 +54,8 @@ class ModelSpecC(ctypes.Structure):
 
 class MergeOptionsC(ctypes.Structure):
     _fields_ = [("workers", ctypes.c_int32), ("uncached", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("verify", ctypes.c_int32)]
+                ("skip_verify", ctypes.c_int32), ("devices", ctypes.POINTER(ctypes.c_int32)),
+                ("num_devices", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class MergeStatsC(ctypes.Structure):
@@ -114,9 +115,10 @@ SIGNATURES = {
     "tg_trainer_elements": (_U64, [_P]),
     "tg_trainer_step": (_I, [_P, _I64, _c.POINTER(_D), _c.POINTER(_D)]),
     "tg_trainer_partition": (_I, [_P, _I32, _c.POINTER(_P), _c.POINTER(_U64)]),
-    "tg_score_snapshots": (_I, [_c.POINTER(_S), _I32, _I32, _c.POINTER(_D), _c.POINTER(_D), _c.POINTER(_I32)]),
-    "tg_select_recipe": (_I, [_c.POINTER(_S), _I32, _D, _I32, _c.c_char_p, _SZ, _PSZ, _c.POINTER(_I32),
-                              _c.POINTER(_D)]),
+    "tg_score_snapshots": (_I, [_c.POINTER(_S), _I32, _c.POINTER(_I32), _I32, _c.POINTER(_D), _c.POINTER(_D),
+                                _c.POINTER(_I32)]),
+    "tg_select_recipe": (_I, [_c.POINTER(_S), _I32, _D, _c.POINTER(_I32), _I32, _c.c_char_p, _SZ, _PSZ,
+                              _c.POINTER(_I32), _c.POINTER(_D)]),
     "tg_layer_map": (_I, [_c.POINTER(ModelSpecC), _I32, _c.c_char_p, _SZ, _PSZ]),
     "tg_parse_config": (_I, [_S, _c.POINTER(ModelSpecC)]),
     "tg_gather": (_I, [_P, _U32, _P, _U64, _I32, _I32, _P]),

@@ -222,11 +222,10 @@ struct PackedLoader {
 
 // Device scores over snapshot directories: per rank, packed masters -> K3/K4;
 // ranks combined in rank order on the host (FP64, fixed order).
-void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<std::vector<double>>& sd,
+void score_dirs(const std::vector<std::string>& dirs, const std::vector<int>& devices, std::vector<std::vector<double>>& sd,
                 std::vector<std::vector<double>>& sr, std::vector<CheckpointSummary>& sums) {
     if (dirs.size() < 2) fail(ErrorKind::Recipe, "scoring needs at least two snapshots");
-    if (dirs.size() > 16) fail(ErrorKind::Geometry, "at most 16 snapshots per scoring sweep");
-    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cuda_check(cudaSetDevice(devices.front()), "cudaSetDevice");
     sums.clear();
     for (const auto& d : dirs) sums.push_back(read_checkpoint_summary(d));
     const ModelSpec& spec = sums.front().spec;
@@ -240,37 +239,49 @@ void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<st
     const int K = static_cast<int>(dirs.size()), M = model.module_count();
     sd.assign(static_cast<std::size_t>(K - 1), std::vector<double>(static_cast<std::size_t>(M), 0.0));
     sr = sd;
-    // Ranks are independent: lanes (threads with their own buffers) score one
-    // rank each; the per-rank partials are summed in rank order afterwards, so
-    // the result does not depend on the lane count. A lane holds the K packed
-    // snapshots of its rank when they fit the device budget; otherwise it streams
-    // the snapshots through two slots and scores consecutive pairs (K3 with K=2 over
-    // the same tiles in the same order gives each pair's sums), e.g. a 70B-shaped
-    // rank partition (4 x 40 GB of masters).
+    // Ranks are independent: lanes (threads with their own buffers, spread round-robin
+    // over the devices) score one rank each; the per-rank partials are summed in rank
+    // order afterwards, so the result depends on neither the lane count nor the devices.
+    // A lane holds all K packed snapshots of its rank when they fit the device budget;
+    // otherwise it rolls through `slots` device slots (>= 2) in windows of up to
+    // min(slots, 16) consecutive snapshots that overlap by one (snapshot k lives in slot
+    // k % slots; every pair is scored once, inside one window), e.g. a 70B-shaped rank
+    // partition (4 x 40 GB of masters) in pairs, or a 35-snapshot sweep.
     const auto fields = score_fields(model, N);
     const std::uint64_t stride = packed_stride(fields);
-    const std::uint64_t budget = device_budget();
-    const bool pairwise = stride * static_cast<std::uint64_t>(K) > budget;
-    const std::uint64_t per_lane = stride * (pairwise ? 2u : static_cast<std::uint64_t>(K));
+    std::uint64_t budget = ~0ull;
+    for (int d : devices) {
+        cuda_check(cudaSetDevice(d), "cudaSetDevice");
+        budget = std::min(budget, device_budget());
+    }
+    cuda_check(cudaSetDevice(devices.front()), "cudaSetDevice");
+    const bool all_resident = stride * static_cast<std::uint64_t>(K) <= budget;
+    const int slots = all_resident ? K
+                                   : static_cast<int>(std::clamp<std::uint64_t>(budget / stride, 2, static_cast<std::uint64_t>(dev::kMaxSnapshots)));
+    const std::uint64_t per_lane = stride * static_cast<std::uint64_t>(slots);
     if (per_lane > budget && !std::getenv("TAILOR_DEVICE_BUDGET"))
         fail(ErrorKind::Device, "scoring needs " + std::to_string(per_lane) + " B of device memory for two snapshots of one rank; " +
                                     std::to_string(budget) + " B available");
-    const int lanes = std::clamp<int>(static_cast<int>(std::min<std::uint64_t>(budget / per_lane, 8)), 1, std::min(N, 8));
+    const int nd = static_cast<int>(devices.size());
+    const int per_dev = std::clamp<int>(static_cast<int>(std::min<std::uint64_t>(budget / per_lane, 8)), 1, 8);
+    const int lanes = std::clamp<int>(per_dev * nd, 1, N);
     const int readers = std::max(1, io_threads() / lanes);
-    trace_count(pairwise ? "score.lanes (pairwise)" : "score.lanes", lanes);
+    trace_count(all_resident ? "score.lanes" : "score.lanes (rolling windows)", lanes);
+    trace_count("score.slots", slots);
     const std::size_t nres = static_cast<std::size_t>(K - 1) * M * 2;
     std::vector<std::vector<double>> res(static_cast<std::size_t>(N), std::vector<double>(nres));
     std::atomic<int> next{0};
     std::exception_ptr lane_err;
     std::mutex mu;
-    const auto lane = [&] {
+    const auto lane = [&](int li) {
         try {
-            cuda_check(cudaSetDevice(device), "cudaSetDevice");
+            cuda_check(cudaSetDevice(devices[static_cast<std::size_t>(li % nd)]), "cudaSetDevice");
             cudaStream_t st = nullptr;
             cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
             std::unique_ptr<CUstream_st, decltype(&cudaStreamDestroy)> own(st, &cudaStreamDestroy);
             DeviceBuffer dout(nres * sizeof(double)), arena(per_lane);
             PackedLoader loader(st, readers);
+            std::map<int, std::unique_ptr<ScorePlan>> plans; // by window length (offsets are rank-independent)
             for (int r = next.fetch_add(1); r < N; r = next.fetch_add(1)) {
                 {
                     std::lock_guard<std::mutex> lk(mu);
@@ -279,29 +290,32 @@ void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<st
                 PhaseTimer pt("score.rank");
                 loader.read_ms = loader.load_ms = 0.0;
                 const double t0 = clock_ms();
-                std::vector<std::vector<std::uint64_t>> offs(static_cast<std::size_t>(K));
-                if (!pairwise) {
+                std::vector<std::uint64_t> offs;
+                const auto slot_of = [&](int k) { return arena.get() + static_cast<std::uint64_t>(k % slots) * stride; };
+                const auto load = [&](int k) {
+                    loader.load(ckpt_file(CkptFile::Shard, dirs[static_cast<std::size_t>(k)], r), fields, slot_of(k), offs);
+                };
+                const auto score = [&](int k0, int k1) { // snapshots k0..k1 resident, pairs k0..k1-1
+                    const int n = k1 - k0 + 1;
+                    auto& plan = plans[n];
+                    if (!plan) plan = std::make_unique<ScorePlan>(model, N, std::vector<std::vector<std::uint64_t>>(static_cast<std::size_t>(n), offs));
                     std::vector<const std::uint8_t*> bases;
-                    for (int k = 0; k < K; ++k) {
-                        std::uint8_t* slot = arena.get() + static_cast<std::uint64_t>(k) * stride;
-                        loader.load(ckpt_file(CkptFile::Shard, dirs[static_cast<std::size_t>(k)], r), fields, slot,
-                                    offs[static_cast<std::size_t>(k)]);
-                        bases.push_back(slot);
-                    }
-                    ScorePlan plan(model, N, offs);
-                    plan.run(bases.data(), dout.get<double>(), st);
+                    for (int k = k0; k <= k1; ++k) bases.push_back(slot_of(k));
+                    plan->run(bases.data(), dout.get<double>() + static_cast<std::size_t>(k0) * M * 2, st);
+                };
+                if (all_resident) {
+                    for (int k = 0; k < K; ++k) load(k);
+                    score(0, K - 1); // windows of <= 16 inside ScorePlan
                 } else {
-                    loader.load(ckpt_file(CkptFile::Shard, dirs[0], r), fields, arena.get(), offs[0]);
-                    std::unique_ptr<ScorePlan> plan;
-                    for (int k = 1; k < K; ++k) {
-                        std::uint8_t* prev = arena.get() + static_cast<std::uint64_t>((k - 1) % 2) * stride;
-                        std::uint8_t* cur = arena.get() + static_cast<std::uint64_t>(k % 2) * stride;
-                        // the slot is free once the previous pair's scoring has run (same stream)
-                        loader.load(ckpt_file(CkptFile::Shard, dirs[static_cast<std::size_t>(k)], r), fields, cur,
-                                    offs[static_cast<std::size_t>(k)]);
-                        if (!plan) plan = std::make_unique<ScorePlan>(model, N, std::vector<std::vector<std::uint64_t>>{offs[0], offs[1]});
-                        const std::uint8_t* bases[2] = {prev, cur};
-                        plan->run(bases, dout.get<double>() + static_cast<std::size_t>(k - 1) * M * 2, st);
+                    // the slot a load overwrites was last read by a window scored earlier on
+                    // this stream, so stream order keeps the reuse safe
+                    const int win = std::min(slots, static_cast<int>(dev::kMaxSnapshots));
+                    load(0);
+                    for (int k0 = 0; k0 < K - 1;) {
+                        const int k1 = std::min(K - 1, k0 + win - 1);
+                        for (int k = k0 + 1; k <= k1; ++k) load(k);
+                        score(k0, k1);
+                        k0 = k1;
                     }
                 }
                 cuda_check(cudaMemcpyAsync(res[static_cast<std::size_t>(r)].data(), dout.get(), nres * sizeof(double),
@@ -318,12 +332,13 @@ void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<st
         }
     };
     if (lanes == 1) {
-        lane();
+        lane(0);
     } else {
         std::vector<std::thread> pool;
-        for (int i = 0; i < lanes; ++i) pool.emplace_back(lane);
+        for (int i = 0; i < lanes; ++i) pool.emplace_back(lane, i);
         for (auto& t : pool) t.join();
     }
+    cuda_check(cudaSetDevice(devices.front()), "cudaSetDevice");
     if (lane_err) std::rethrow_exception(lane_err);
     for (int r = 0; r < N; ++r) {
         const auto& h = res[static_cast<std::size_t>(r)];
@@ -333,6 +348,25 @@ void score_dirs(const std::vector<std::string>& dirs, int device, std::vector<st
                 sr[static_cast<std::size_t>(p)][static_cast<std::size_t>(m)] += h[(static_cast<std::size_t>(p) * M + m) * 2 + 1];
             }
     }
+}
+
+MergeOptions merge_options(const tg_merge_options* o) {
+    MergeOptions opt;
+    if (!o) return opt;
+    opt.workers = o->workers;
+    opt.uncached = o->uncached != 0;
+    opt.device = o->device;
+    opt.verify = o->skip_verify == 0;
+    if (o->num_devices > 0) {
+        if (!o->devices) fail(ErrorKind::Recipe, "tg_merge_options: num_devices > 0 with a null device list");
+        opt.devices.assign(o->devices, o->devices + o->num_devices);
+    }
+    return opt;
+}
+
+std::vector<int> device_list(const int32_t* devices, int32_t n) {
+    if (n <= 0 || !devices) return {0};
+    return std::vector<int>(devices, devices + n);
 }
 
 } // namespace
@@ -363,13 +397,7 @@ int tg_resolve_plan(const char* yaml, char* out, size_t cap, size_t* needed) {
 int tg_execute_merge(const char* yaml, const char* out_dir, const tg_merge_options* o, tg_merge_stats* st) {
     return guard([&] {
         const MergePlan plan = resolve_plan(parse_recipe(yaml ? yaml : ""));
-        MergeOptions opt;
-        if (o) {
-            opt.workers = o->workers;
-            opt.uncached = o->uncached != 0;
-            opt.device = o->device;
-            opt.verify = o->verify != 0;
-        }
+        const MergeOptions opt = merge_options(o);
         const MergeStats s = execute_merge(plan, out_dir ? out_dir : "", opt);
         if (st) {
             st->shard_files_read = s.shard_files_read;
@@ -387,12 +415,8 @@ int tg_recipe_from_manifests(const char* run_dir, int64_t failure_step, char* ou
 
 int tg_regroup(const char* src_dir, const char* out_dir, int32_t to_fine, const tg_merge_options* o, tg_merge_stats* st) {
     return guard([&] {
-        MergeOptions opt;
-        if (o) {
-            opt.workers = o->workers;
-            opt.device = o->device;
-            opt.verify = o->verify != 0;
-        }
+        MergeOptions opt = merge_options(o);
+        opt.uncached = false;
         const MergeStats s = execute_regroup(src_dir ? src_dir : "", out_dir ? out_dir : "",
                                              to_fine ? Grouping::Fine : Grouping::Coarse, opt);
         if (st) {
@@ -477,12 +501,13 @@ int tg_verify_checkpoint(const char* dir, int32_t device) {
     return guard([&] { verify_checkpoint_dir(dir ? dir : "", device); });
 }
 
-int tg_score_snapshots(const char* const* dirs, int32_t n, int32_t device, double* sums, double* scores, int32_t* nm) {
+int tg_score_snapshots(const char* const* dirs, int32_t n, const int32_t* devices, int32_t num_devices, double* sums,
+                       double* scores, int32_t* nm) {
     return guard([&] {
         std::vector<std::string> ds(dirs, dirs + n);
         std::vector<std::vector<double>> sd, sr;
         std::vector<CheckpointSummary> summ;
-        score_dirs(ds, device, sd, sr, summ);
+        score_dirs(ds, device_list(devices, num_devices), sd, sr, summ);
         const int M = static_cast<int>(sd.front().size());
         if (nm) *nm = M;
         for (std::size_t p = 0; p < sd.size(); ++p)
@@ -496,13 +521,13 @@ int tg_score_snapshots(const char* const* dirs, int32_t n, int32_t device, doubl
     });
 }
 
-int tg_select_recipe(const char* const* dirs, int32_t n, double rho, int32_t device, char* out, size_t cap,
+int tg_select_recipe(const char* const* dirs, int32_t n, double rho, const int32_t* devices, int32_t num_devices, char* out, size_t cap,
                      size_t* needed, int32_t* source_of, double* min_gap) {
     return guard([&] {
         std::vector<std::string> ds(dirs, dirs + n);
         std::vector<std::vector<double>> sd, sr;
         std::vector<CheckpointSummary> summ;
-        score_dirs(ds, device, sd, sr, summ);
+        score_dirs(ds, device_list(devices, num_devices), sd, sr, summ);
         std::vector<std::vector<double>> sc = sd;
         for (std::size_t p = 0; p < sd.size(); ++p)
             for (std::size_t m = 0; m < sd[p].size(); ++m) sc[p][m] = magnitude_score(sd[p][m], sr[p][m]);

@@ -417,10 +417,13 @@ void SynthFamily::gen_shard(int rank, int k0, int k1, std::uint8_t* const* outs,
             fail(ErrorKind::Geometry, "snapshots generated together must share one layout");
     ensure_sigma(k1);
     ShardTables& t = shard_tables(k0, rank, false);
-    cuda_check(dev::launch_synth_shard(t.groups.get<dev::SynthGroup>(), t.ngroups, t.slices.get<dev::SynthSlice>(),
-                                       sigma_.get<float>(), model_.module_count(), model_.spec().seed, k0, k1,
-                                       out_ptrs(outs, k1 - k0 + 1), t.total, s),
-               "synth shard");
+    for (int a = k0; a <= k1; a += dev::kMaxSnapshots) { // <= 16 snapshots per launch
+        const int b = std::min(k1, a + dev::kMaxSnapshots - 1);
+        cuda_check(dev::launch_synth_shard(t.groups.get<dev::SynthGroup>(), t.ngroups, t.slices.get<dev::SynthSlice>(),
+                                           sigma_.get<float>(), model_.module_count(), model_.spec().seed, a, b,
+                                           out_ptrs(outs + (a - k0), b - a + 1), t.total, s),
+                   "synth shard");
+    }
 }
 
 void SynthFamily::gen_masters_packed(int rank, int k0, int k1, std::uint8_t* const* outs, cudaStream_t s) {
@@ -428,10 +431,13 @@ void SynthFamily::gen_masters_packed(int rank, int k0, int k1, std::uint8_t* con
     if (k0 < 1 || k1 > K_ || k0 > k1) fail(ErrorKind::Geometry, "snapshot range out of bounds");
     ensure_sigma(k1);
     ShardTables& t = shard_tables(0, rank, true);
-    cuda_check(dev::launch_synth_shard(t.groups.get<dev::SynthGroup>(), t.ngroups, t.slices.get<dev::SynthSlice>(),
-                                       sigma_.get<float>(), model_.module_count(), model_.spec().seed, k0, k1,
-                                       out_ptrs(outs, k1 - k0 + 1), t.total, s),
-               "synth masters");
+    for (int a = k0; a <= k1; a += dev::kMaxSnapshots) {
+        const int b = std::min(k1, a + dev::kMaxSnapshots - 1);
+        cuda_check(dev::launch_synth_shard(t.groups.get<dev::SynthGroup>(), t.ngroups, t.slices.get<dev::SynthSlice>(),
+                                           sigma_.get<float>(), model_.module_count(), model_.spec().seed, a, b,
+                                           out_ptrs(outs + (a - k0), b - a + 1), t.total, s),
+                   "synth masters");
+    }
 }
 
 void SynthFamily::gen_shard_range(int rank, int k, std::uint64_t lo, std::uint64_t hi, std::uint8_t* out,
@@ -510,10 +516,13 @@ void SynthFamily::gen_weights(int k0, int k1, std::uint64_t lo, std::uint64_t hi
     if (tabs.empty()) return;
     if (s) cuda_check(cudaStreamSynchronize(s), "sync");
     wtab_.upload(tabs.data(), tabs.size() * sizeof(dev::SynthTensor));
-    cuda_check(dev::launch_synth_weights(wtab_.get<dev::SynthTensor>(), static_cast<std::uint32_t>(tabs.size()),
-                                         sigma_.get<float>(), model_.module_count(), model_.spec().seed, k0, k1,
-                                         out_ptrs(outs, k1 - k0 + 1), begin, s),
-               "synth weights");
+    for (int a = k0; a <= k1; a += dev::kMaxSnapshots) {
+        const int b = std::min(k1, a + dev::kMaxSnapshots - 1);
+        cuda_check(dev::launch_synth_weights(wtab_.get<dev::SynthTensor>(), static_cast<std::uint32_t>(tabs.size()),
+                                             sigma_.get<float>(), model_.module_count(), model_.spec().seed, a, b,
+                                             out_ptrs(outs + (a - k0), b - a + 1), begin, s),
+                   "synth weights");
+    }
     cuda_check(cudaStreamSynchronize(s), "sync");
 }
 
@@ -561,7 +570,11 @@ void SynthFamily::write_dir(int k, const std::string& dir) {
 ScorePlan::ScorePlan(const ModelLayout& model, int num_ranks, std::vector<std::vector<std::uint64_t>> field_offsets,
                      std::uint32_t tile_elems)
     : K_(static_cast<int>(field_offsets.size())), M_(model.module_count()), offs_(std::move(field_offsets)) {
-    if (K_ < 2 || K_ > dev::kMaxSnapshots) fail(ErrorKind::Geometry, "scoring needs 2..16 snapshots");
+    if (K_ < 2) fail(ErrorKind::Geometry, "scoring needs at least 2 snapshots");
+    // K3 holds up to 16 snapshots per launch; longer sweeps run as windows of <= 16
+    // snapshots that overlap by one (pairs never straddle a window)
+    for (int s0 = 0; s0 < K_ - 1; s0 += dev::kMaxSnapshots - 1)
+        windows_.push_back({s0, std::min(K_ - 1, s0 + dev::kMaxSnapshots - 1)});
     if (const char* v = std::getenv("TAILOR_SCORE_VARIANT"); v && *v) variant_ = std::atoi(v);
     tile_elems = std::max<std::uint32_t>(4, tile_elems & ~3u);
     fields_ = score_fields(model, num_ranks);
@@ -579,12 +592,13 @@ ScorePlan::ScorePlan(const ModelLayout& model, int num_ranks, std::vector<std::v
             tiles_.push_back({static_cast<std::uint32_t>(sf.module), static_cast<std::uint32_t>(f), n, 0,
                               static_cast<std::uint64_t>(s)});
         }
-        bytes_ += static_cast<std::uint64_t>(sf.chunk) * 4 * static_cast<std::uint64_t>(K_);
+        for (const auto& w : windows_) bytes_ += static_cast<std::uint64_t>(sf.chunk) * 4 * static_cast<std::uint64_t>(w.second - w.first + 1);
     }
     while (cur < M_) begin_[static_cast<std::size_t>(++cur)] = static_cast<std::uint32_t>(tiles_.size());
     d_tiles_.upload(tiles_.data(), tiles_.size() * sizeof(dev::ScoreTile));
     d_begin_.upload(begin_.data(), begin_.size() * sizeof(std::uint32_t));
-    d_partials_.resize(std::max<std::size_t>(1, tiles_.size()) * 2 * static_cast<std::size_t>(K_ - 1) * sizeof(double));
+    d_partials_.resize(std::max<std::size_t>(1, tiles_.size()) * 2 *
+                       static_cast<std::size_t>(std::min(K_, static_cast<int>(dev::kMaxSnapshots)) - 1) * sizeof(double));
     h_bases_.resize(static_cast<std::size_t>(K_) * fields_.size() * sizeof(void*) + 8);
     d_bases_.resize(static_cast<std::size_t>(K_) * fields_.size() * sizeof(void*) + 8);
 }
@@ -605,12 +619,17 @@ void ScorePlan::run(const std::uint8_t* const* snap_bases, double* d_out, cudaSt
         cuda_check(cudaStreamSynchronize(s), "sync");
         bound_ = want;
     }
-    cuda_check(dev::launch_score_partials(d_tiles_.get<dev::ScoreTile>(), static_cast<std::uint32_t>(tiles_.size()),
-                                          d_bases_.get<const float*>(), static_cast<std::uint32_t>(fields_.size()), K_,
-                                          vec, d_partials_.get<double>(), s, variant_),
-               "score partials");
-    cuda_check(dev::launch_score_combine(d_partials_.get<double>(), d_begin_.get<std::uint32_t>(), M_, K_, d_out, s),
-               "score combine");
+    for (const auto& [w0, w1] : windows_) { // pairs w0..w1-1 of the sweep
+        const int Kw = w1 - w0 + 1;
+        cuda_check(dev::launch_score_partials(d_tiles_.get<dev::ScoreTile>(), static_cast<std::uint32_t>(tiles_.size()),
+                                              d_bases_.get<const float*>() + static_cast<std::size_t>(w0) * fields_.size(),
+                                              static_cast<std::uint32_t>(fields_.size()), Kw, vec, d_partials_.get<double>(), s,
+                                              variant_),
+                   "score partials");
+        cuda_check(dev::launch_score_combine(d_partials_.get<double>(), d_begin_.get<std::uint32_t>(), M_, Kw,
+                                             d_out + static_cast<std::size_t>(w0) * M_ * 2, s),
+                   "score combine");
+    }
 }
 
 // ---- device merge -----------------------------------------------------------------
@@ -827,7 +846,7 @@ void HostMerge::run(const std::vector<const std::uint8_t*>& h_windows, const std
 // ---- device select + plan step ---------------------------------------------------------
 DeviceSelectStep::DeviceSelectStep(const SynthFamily& fam, int rank, int unit, int units, double rho)
     : K_(fam.snapshots()), M_(fam.model().module_count()) {
-    if (K_ < 2 || K_ > dev::kMaxSnapshots) fail(ErrorKind::Geometry, "device selection needs 2..16 snapshots");
+    if (K_ < 2 || K_ > dev::kMaxSelectSnapshots) fail(ErrorKind::Geometry, "device selection needs 2..64 snapshots");
     if (!(rho > 0.0 && rho <= 1.0)) fail(ErrorKind::Recipe, "selection ratio rho must lie in (0, 1]");
     if (rank < 0 || rank >= fam.num_ranks()) fail(ErrorKind::Geometry, "rank out of range");
     n_save_ = std::max(1, std::min(M_, static_cast<int>(std::ceil(rho * M_))));
@@ -1058,7 +1077,11 @@ VerifyPlan verify_plan(const fs::path& dir, const CheckpointSummary& s, Containe
                 const std::int64_t a = std::max(first, sl2.group_offset);
                 const std::int64_t b = std::min(first + valid, sl2.group_offset + sl2.decl.numel());
                 if (a >= b) continue;
+                // derive_weights (R/src/checkpoint.cpp:287-312) pairs only tensors of manifest
+                // modules: a coarse checkpoint with a partial manifest has group slices
+                // without a weights entry, and those are not checked
                 const Entry* we = wl.find(sl2.decl.name);
+                if (!we) continue;
                 pairs[static_cast<std::size_t>(r)].push_back(
                     {reinterpret_cast<const float*>(f[0]->begin + static_cast<std::uint64_t>(a - first) * 4),
                      reinterpret_cast<const std::uint16_t*>(we->begin + static_cast<std::uint64_t>(a - sl2.group_offset) * 2),
@@ -1070,11 +1093,12 @@ VerifyPlan verify_plan(const fs::path& dir, const CheckpointSummary& s, Containe
     return out;
 }
 
-void verify_rank_resident(const VerifyPlan& plan, int r, const fs::path& shard_file, const std::uint8_t* dw, DeviceBuffer& ds,
-                          DeviceBuffer& dpairs, DeviceBuffer& dranges, PinnedBuffer* stage, int readers, std::uint64_t step,
-                          unsigned long long* d_err, cudaStream_t st, const std::function<void()>& before_kernel) {
+void verify_rank_resident(const VerifyPlan& plan, int r, const fs::path& shard_file, DeviceBuffer& ds, DeviceBuffer& dpairs,
+                          DeviceBuffer& dranges, PinnedBuffer* stage, int readers, std::uint64_t step, unsigned long long* d_err,
+                          cudaStream_t st, const std::function<const std::uint8_t*()>& weights) {
     const auto& sl = plan.shards.at(static_cast<std::size_t>(r));
     load_payload(shard_file, sl, ds, stage, readers, step);
+    const std::uint8_t* dw = weights(); // may block (e.g. until the weights file is in)
     auto pr = plan.pairs[static_cast<std::size_t>(r)];
     auto rg = plan.ranges[static_cast<std::size_t>(r)];
     for (auto& x : pr) {
@@ -1082,7 +1106,6 @@ void verify_rank_resident(const VerifyPlan& plan, int r, const fs::path& shard_f
         x.weight = reinterpret_cast<const std::uint16_t*>(dw + reinterpret_cast<std::uintptr_t>(x.weight));
     }
     for (auto& x : rg) x.words = reinterpret_cast<const std::uint32_t*>(ds.get() + reinterpret_cast<std::uintptr_t>(x.words));
-    if (before_kernel) before_kernel();
     dpairs.upload(pr.data(), pr.size() * sizeof(dev::VerifyPair));
     dranges.upload(rg.data(), rg.size() * sizeof(dev::VerifyRange));
     cuda_check(dev::launch_verify(dpairs.get<dev::VerifyPair>(), static_cast<std::uint32_t>(pr.size()),
@@ -1096,9 +1119,7 @@ void load_payload_to(const fs::path& path, const ContainerLayout& lay, DeviceBuf
     load_payload(path, lay, dst, stage, threads, step);
 }
 
-void verify_counters(const fs::path& dir, int num_ranks, const unsigned long long* d_err) {
-    std::vector<unsigned long long> err(static_cast<std::size_t>(num_ranks) * 3);
-    cuda_check(cudaMemcpy(err.data(), d_err, err.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "D2H");
+void verify_counters_host(const fs::path& dir, int num_ranks, const unsigned long long* err) {
     bool mismatch = false;
     for (int r = 0; r < num_ranks; ++r) {
         if (err[3 * r + 1]) fail(ErrorKind::CorruptContainer, dir.string() + ": nonzero padding in rank " + std::to_string(r));
@@ -1106,6 +1127,12 @@ void verify_counters(const fs::path& dir, int num_ranks, const unsigned long lon
         mismatch = mismatch || err[3 * r] != 0;
     }
     if (mismatch) fail(ErrorKind::Consistency, dir.string() + ": a weight tensor disagrees with its FP32 master");
+}
+
+void verify_counters(const fs::path& dir, int num_ranks, const unsigned long long* d_err) {
+    std::vector<unsigned long long> err(static_cast<std::size_t>(num_ranks) * 3);
+    cuda_check(cudaMemcpy(err.data(), d_err, err.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "D2H");
+    verify_counters_host(dir, num_ranks, err.data());
 }
 
 void verify_checkpoint_dir(const std::string& dir_s, int device) {
@@ -1201,8 +1228,11 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
                         std::lock_guard<std::mutex> lk(mu);
                         if (lane_err) break;
                     }
-                    verify_rank_resident(plan, r, ckpt_file(CkptFile::Shard, dir, r), dw.get(), ds, dpairs, dranges, stage, readers,
-                                         step, derr.get<unsigned long long>(), ls.s, wait_weights);
+                    verify_rank_resident(plan, r, ckpt_file(CkptFile::Shard, dir, r), ds, dpairs, dranges, stage, readers,
+                                         step, derr.get<unsigned long long>(), ls.s, [&] {
+                                             wait_weights();
+                                             return static_cast<const std::uint8_t*>(dw.get());
+                                         });
                 }
             } catch (...) {
                 std::lock_guard<std::mutex> lk(mu);

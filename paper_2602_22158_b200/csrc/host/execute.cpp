@@ -315,6 +315,16 @@ class FileAssembler {
     std::map<std::string, std::uint64_t> payload_off_;
 };
 
+// Failure injection for tests (TAILOR_FAULT = comma-separated point names), in the
+// spirit of the reference's inject_failure (R/src/trainer.cpp:170-193): lets a test
+// make one output lane fail and check that the others are released.
+bool fault_injected(const char* point) {
+    const char* v = std::getenv("TAILOR_FAULT");
+    if (!v || !*v) return false;
+    const std::string s = std::string(",") + v + ",";
+    return s.find(std::string(",") + point + ",") != std::string::npos;
+}
+
 struct OutputJob {
     const PartitionPlan* plan;
     std::vector<fs::path> window_files;
@@ -332,15 +342,20 @@ struct AssembleTotals {
 // file is produced by exactly one lane, in chunk order.
 // on_done(tag), if set, runs on the lane's thread right after a file is complete (the
 // pipelined re-verify of execute_merge hooks in here).
-AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool uncached, int device,
-                                const std::function<void(int)>& on_done = {}) {
+// on_error, if set, runs once on the thread of the first lane that fails (before the pool
+// joins), so that lanes blocked on a hook's condition can be released.
+// Lane li runs on devices[li % devices.size()] (the reference's loader pool,
+// R/src/merge.cpp:156-205, spread over GPUs; which lane writes a file never changes its bytes).
+AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool uncached, const std::vector<int>& devices,
+                                const std::function<void(int)>& on_done = {}, const std::function<void()>& on_error = {}) {
     // the weights file first (a lane verifying a rank file waits for it: with fewer lanes
     // than files, taking it last could block every lane), then largest first
     std::stable_sort(jobs.begin(), jobs.end(), [](const OutputJob& a, const OutputJob& b) {
         if ((a.tag < 0) != (b.tag < 0)) return a.tag < 0;
         return a.plan->dst_hi - a.plan->dst_lo > b.plan->dst_hi - b.plan->dst_lo;
     });
-    const int lanes = std::clamp<int>(std::min<int>(static_cast<int>(jobs.size()), workers), 1, 16);
+    const int lanes = std::clamp<int>(std::min<int>(static_cast<int>(jobs.size()), std::max<int>(workers, static_cast<int>(devices.size()))),
+                                      1, 16 * static_cast<int>(devices.size()));
     const int readers = std::max(1, workers / lanes);
     // Chunks a little under a pool size class (16 / 32 / 128 MB), so a slot's
     // staging (chunk + <= 31 B of alignment per read) stays in that class and the
@@ -352,7 +367,7 @@ AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool u
     std::mutex mu;
     const auto lane = [&](int li) {
         try {
-            cuda_check(cudaSetDevice(device), "cudaSetDevice");
+            cuda_check(cudaSetDevice(devices[static_cast<std::size_t>(li) % devices.size()]), "cudaSetDevice");
             FileAssembler fa(readers, uncached, chunk);
             for (std::size_t j = next.fetch_add(1); j < jobs.size(); j = next.fetch_add(1)) {
                 {
@@ -361,13 +376,22 @@ AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool u
                 }
                 // the weights file is the longest job and the one everything waits for: more readers
                 fa.set_read_threads(jobs[j].tag < 0 ? std::max(readers, 4) : readers);
+                if (jobs[j].tag < 0 && fault_injected("assemble-weights"))
+                    fail(ErrorKind::Storage, "injected fault (TAILOR_FAULT=assemble-weights): " + jobs[j].out.string());
                 fa.assemble(*jobs[j].plan, jobs[j].window_files, jobs[j].out);
                 if (on_done) on_done(jobs[j].tag);
             }
             part[static_cast<std::size_t>(li)] = {fa.device_ms, fa.read_ms, fa.wait_ms, fa.write_ms, fa.bytes};
         } catch (...) {
-            std::lock_guard<std::mutex> lk(mu);
-            if (!err) err = std::current_exception();
+            bool first = false;
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                if (!err) {
+                    err = std::current_exception();
+                    first = true;
+                }
+            }
+            if (first && on_error) on_error();
         }
     };
     if (lanes == 1) {
@@ -387,6 +411,7 @@ AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool u
         tot.bytes += x.bytes;
     }
     trace_count("assemble.lanes", lanes);
+    trace_count("assemble.devices", static_cast<long long>(devices.size()));
     trace_value("assemble.read (sum over lanes)", tot.read_ms);
     trace_value("assemble.wait (sum over lanes)", tot.wait_ms);
     trace_value("assemble.write (sum over lanes)", tot.write_ms);
@@ -394,41 +419,63 @@ AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool u
 }
 
 // Pipelined re-verify (resident form, when weights + one rank payload per lane fit the
-// device budget): the lane that finished the weights file loads it to the device; a
-// lane that finished a rank file re-reads it and runs K6 (after the weights are in).
-// The on-disk headers are compared with the planned layouts afterwards. Otherwise the
-// whole directory is verified after assembly (verify_checkpoint_dir). The sidecars must
-// be written before the assembly starts.
+// budget of every device): the lane that finished the weights file loads it to its
+// device; a lane that finished a rank file re-reads it and runs K6 on its own device
+// (after the weights are in; a device's first such lane loads its own copy of the
+// weights payload). The on-disk headers are compared with the planned layouts
+// afterwards. Otherwise the whole directory is verified after assembly
+// (verify_checkpoint_dir). The sidecars must be written before the assembly starts.
 class LaneVerifier {
   public:
     LaneVerifier(const fs::path& out_dir, const PartitionPlan* wplan, const std::vector<PartitionPlan>& splans, int workers,
-                 bool verify)
-        : out_(out_dir), wplan_(wplan), splans_(splans), verify_(verify), N_(static_cast<int>(splans.size())) {
+                 bool verify, const std::vector<int>& devices)
+        : out_(out_dir), wplan_(wplan), splans_(splans), verify_(verify), devices_(devices), N_(static_cast<int>(splans.size())) {
         std::uint64_t max_shard = 16;
         for (const auto& sp : splans) max_shard = std::max<std::uint64_t>(max_shard, sp.out.payload_bytes);
-        lanes_ = std::clamp<int>(std::min<int>(N_ + 1, workers), 1, 16);
-        pipelined_ = verify && wplan->out.payload_bytes + static_cast<std::uint64_t>(lanes_) * max_shard <= device_budget();
+        const int nd = static_cast<int>(devices_.size());
+        lanes_ = std::clamp<int>(std::min<int>(N_ + 1, std::max(workers, nd)), 1, 16 * nd);
+        const std::uint64_t lanes_per_dev = static_cast<std::uint64_t>((lanes_ + nd - 1) / nd);
+        pipelined_ = verify;
+        for (int d : devices_) {
+            if (!pipelined_) break;
+            cuda_check(cudaSetDevice(d), "cudaSetDevice");
+            pipelined_ = wplan->out.payload_bytes + lanes_per_dev * max_shard <= device_budget();
+        }
+        cuda_check(cudaSetDevice(devices_.front()), "cudaSetDevice");
         if (!pipelined_) return;
         const CheckpointSummary vs = read_checkpoint_summary(out_dir);
         std::vector<ContainerLayout> sl;
         for (const auto& sp : splans) sl.push_back(sp.out);
         vplan_ = verify_plan(out_dir, vs, wplan->out, std::move(sl));
-        dw_.resize(std::max<std::uint64_t>(16, wplan->out.payload_bytes));
-        derr_.resize(static_cast<std::size_t>(N_) * 3 * sizeof(unsigned long long));
-        cuda_check(cudaMemset(derr_.get(), 0, derr_.size()), "memset");
+        for (int d : devices_) {
+            if (dev_.count(d)) continue;
+            cuda_check(cudaSetDevice(d), "cudaSetDevice");
+            auto st = std::make_unique<DevState>();
+            st->derr.resize(static_cast<std::size_t>(N_) * 3 * sizeof(unsigned long long));
+            cuda_check(cudaMemset(st->derr.get(), 0, st->derr.size()), "memset");
+            dev_.emplace(d, std::move(st));
+        }
+        cuda_check(cudaSetDevice(devices_.front()), "cudaSetDevice");
     }
 
-    // on_done hook for assemble_outputs (empty when not pipelined)
+    // on_done hook for assemble_outputs (empty when not pipelined); runs on the lane's
+    // thread, with the lane's device current
     std::function<void(int)> hook() {
         if (!pipelined_) return {};
         const int readers = std::max(1, io_threads() / lanes_);
         return [this, readers](int tag) {
+            int d = 0;
+            cuda_check(cudaGetDevice(&d), "cudaGetDevice");
+            DevState& ds_ = *dev_.at(d);
             PinnedBuffer stage[2];
             if (tag < 0) {
                 try {
-                    load_payload_to(ckpt_file(CkptFile::Weights, out_), wplan_->out, dw_, stage, std::max(readers, 8), 16ull << 20);
+                    std::lock_guard<std::mutex> dl(ds_.mu);
+                    load_payload_to(ckpt_file(CkptFile::Weights, out_), wplan_->out, ds_.dw, stage, std::max(readers, 8), 16ull << 20);
+                    ds_.loaded = true;
                 } catch (...) {
-                    werr_ = std::current_exception();
+                    std::lock_guard<std::mutex> lk(mu_);
+                    if (!werr_) werr_ = std::current_exception();
                 }
                 std::lock_guard<std::mutex> lk(mu_);
                 weights_in_ = true;
@@ -440,20 +487,47 @@ class LaneVerifier {
             cudaStream_t st = nullptr;
             cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
             std::unique_ptr<CUstream_st, decltype(&cudaStreamDestroy)> own(st, &cudaStreamDestroy);
-            verify_rank_resident(vplan_, tag, ckpt_file(CkptFile::Shard, out_, tag), dw_.get(), ds, dpairs, dranges, stage, readers,
-                                 16ull << 20, derr_.get<unsigned long long>(), st, [this] {
-                                     std::unique_lock<std::mutex> lk(mu_);
-                                     cv_.wait(lk, [this] { return weights_in_; });
-                                     if (werr_) std::rethrow_exception(werr_);
+            // the last argument blocks until the weights file is complete and loaded on this
+            // device, and returns its device address
+            verify_rank_resident(vplan_, tag, ckpt_file(CkptFile::Shard, out_, tag), ds, dpairs, dranges, stage, readers,
+                                 16ull << 20, ds_.derr.get<unsigned long long>(), st, [this, &ds_, readers] {
+                                     {
+                                         std::unique_lock<std::mutex> lk(mu_);
+                                         cv_.wait(lk, [this] { return weights_in_; });
+                                         if (werr_) std::rethrow_exception(werr_);
+                                     }
+                                     std::lock_guard<std::mutex> dl(ds_.mu);
+                                     if (!ds_.loaded) { // first lane of a device other than the weights lane's
+                                         PinnedBuffer st2[2];
+                                         load_payload_to(ckpt_file(CkptFile::Weights, out_), wplan_->out, ds_.dw, st2,
+                                                         std::max(readers, 8), 16ull << 20);
+                                         ds_.loaded = true;
+                                     }
+                                     return static_cast<const std::uint8_t*>(ds_.dw.get());
                                  });
+        };
+    }
+
+    // on_error hook for assemble_outputs: a lane failed (e.g. while assembling the weights
+    // file, before it could release the others), so lanes waiting for the weights must not
+    // wait forever; they fail with this error (the first lane's error is the one reported).
+    std::function<void()> abort_hook() {
+        if (!pipelined_) return {};
+        return [this] {
+            std::lock_guard<std::mutex> lk(mu_);
+            if (!werr_)
+                werr_ = std::make_exception_ptr(TailorError(ErrorKind::Storage, "merge aborted: another output lane failed"));
+            weights_in_ = true;
+            cv_.notify_all();
         };
     }
 
     // after assembly: headers on disk == the planned layouts (what read_checkpoint's
     // deserialize checks) and the counters, or the whole post-assembly verify
-    void finish(int device) {
+    void finish() {
+        cuda_check(cudaSetDevice(devices_.front()), "cudaSetDevice");
         if (!pipelined_) {
-            if (verify_) verify_checkpoint_dir(out_.string(), device);
+            if (verify_) verify_checkpoint_dir(out_.string(), devices_.front());
             return;
         }
         const auto same = [](const ContainerLayout& a, const ContainerLayout& b) {
@@ -475,17 +549,31 @@ class LaneVerifier {
         for (int r = 0; r < N_; ++r)
             if (!same(read_layout(ckpt_file(CkptFile::Shard, out_, r)), splans_[static_cast<std::size_t>(r)].out))
                 fail(ErrorKind::CorruptContainer, out_.string() + ": shard " + std::to_string(r) + " header differs from the plan");
-        verify_counters(out_, N_, derr_.get<unsigned long long>());
+        // each rank was verified on exactly one device; the others' counters for it stay 0
+        std::vector<unsigned long long> err(static_cast<std::size_t>(N_) * 3, 0), part(err.size());
+        for (auto& [d, st] : dev_) {
+            cuda_check(cudaSetDevice(d), "cudaSetDevice");
+            cuda_check(cudaMemcpy(part.data(), st->derr.get(), part.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "D2H");
+            for (std::size_t i = 0; i < err.size(); ++i) err[i] += part[i];
+        }
+        cuda_check(cudaSetDevice(devices_.front()), "cudaSetDevice");
+        verify_counters_host(out_, N_, err.data());
     }
 
   private:
+    struct DevState {
+        std::mutex mu;
+        bool loaded = false;
+        DeviceBuffer dw, derr;
+    };
     fs::path out_;
     const PartitionPlan* wplan_;
     const std::vector<PartitionPlan>& splans_;
     bool verify_, pipelined_ = false;
+    std::vector<int> devices_;
     int N_, lanes_ = 1;
     VerifyPlan vplan_;
-    DeviceBuffer dw_, derr_;
+    std::map<int, std::unique_ptr<DevState>> dev_;
     std::mutex mu_;
     std::condition_variable cv_;
     bool weights_in_ = false;
@@ -497,13 +585,17 @@ class LaneVerifier {
 MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const MergeOptions& options) {
     const auto t0 = std::chrono::steady_clock::now();
     MergeStats stats;
+    const std::vector<int> devices = lane_devices(options);
     std::error_code ec;
     if (fs::exists(out_dir) && !fs::is_empty(out_dir, ec))
         fail(ErrorKind::Storage, "refusing to write into non-empty directory '" + out_dir.string() + "'");
     {
         PhaseTimer pt("merge.cuda_init");
-        cuda_check(cudaSetDevice(options.device), "cudaSetDevice");
-        cuda_check(cudaFree(nullptr), "cuda init");
+        for (int d : devices) {
+            cuda_check(cudaSetDevice(d), "cudaSetDevice");
+            cuda_check(cudaFree(nullptr), "cuda init");
+        }
+        cuda_check(cudaSetDevice(devices.front()), "cudaSetDevice");
     }
 
     auto phase = std::make_unique<PhaseTimer>("merge.headers+plan");
@@ -563,11 +655,11 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
         jobs.push_back(std::move(j));
     }
 
-    LaneVerifier lv(out_dir, &wplan, splans, workers, options.verify);
-    const AssembleTotals fa = assemble_outputs(std::move(jobs), workers, options.uncached, options.device, lv.hook());
+    LaneVerifier lv(out_dir, &wplan, splans, workers, options.verify, devices);
+    const AssembleTotals fa = assemble_outputs(std::move(jobs), workers, options.uncached, devices, lv.hook(), lv.abort_hook());
     alloc_stats().trace("merge.assemble allocations");
     phase = std::make_unique<PhaseTimer>("merge.verify");
-    lv.finish(options.device);
+    lv.finish();
     phase.reset();
     alloc_stats().trace("merge.verify allocations (cumulative)");
 
@@ -589,7 +681,8 @@ MergeStats execute_regroup(const fs::path& src, const fs::path& out_dir, Groupin
     std::error_code ec;
     if (fs::exists(out_dir) && !fs::is_empty(out_dir, ec))
         fail(ErrorKind::Storage, "refusing to write into non-empty directory '" + out_dir.string() + "'");
-    cuda_check(cudaSetDevice(options.device), "cudaSetDevice");
+    const std::vector<int> devices = lane_devices(options);
+    cuda_check(cudaSetDevice(devices.front()), "cudaSetDevice");
     const CheckpointSummary s = read_checkpoint_summary(src);
     const ModelSpec& spec = s.spec;
     const int N = s.optim.num_ranks;
@@ -687,6 +780,12 @@ MergeStats execute_regroup(const fs::path& src, const fs::path& out_dir, Groupin
     wp.dst_hi = wp.out.payload_bytes;
     finalize_partition(wp, {{key, -1, 0, 0, wp.out.payload_bytes}});
 
+    // The reference regroups what read_checkpoint returned (R/src/checkpoint.cpp:485-575):
+    // a source with nonzero shard padding, a negative exp_avg_sq or a weight that
+    // disagrees with its master fails before anything is written. Same here: the
+    // device re-verify of the source directory runs before out_dir is created.
+    verify_checkpoint_dir(src.string(), devices.front());
+
     fs::create_directories(out_dir / "optim", ec);
     if (ec) fail(ErrorKind::Storage, "cannot create '" + out_dir.string() + "': " + ec.message());
     const int workers = options.workers > 0 ? options.workers : std::max(N, io_threads());
@@ -705,9 +804,9 @@ MergeStats execute_regroup(const fs::path& src, const fs::path& out_dir, Groupin
     write_text_file(ckpt_file(CkptFile::Config, out_dir), sidecar_text(spec));
     write_text_file(ckpt_file(CkptFile::TrainerState, out_dir), sidecar_text(s.trainer));
     write_text_file(ckpt_file(CkptFile::Manifest, out_dir), sidecar_text(s.manifest));
-    LaneVerifier lv(out_dir, &wp, plans, workers, options.verify);
-    const AssembleTotals fa = assemble_outputs(std::move(jobs), workers, false, options.device, lv.hook());
-    lv.finish(options.device);
+    LaneVerifier lv(out_dir, &wp, plans, workers, options.verify, devices);
+    const AssembleTotals fa = assemble_outputs(std::move(jobs), workers, false, devices, lv.hook(), lv.abort_hook());
+    lv.finish();
     stats.device_ms = fa.device_ms;
     stats.bytes_moved = fa.bytes;
     stats.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

@@ -320,15 +320,43 @@ std::string scalar_of(const Node& n, const std::string& path) {
     return n.text;
 }
 
+// node.as<int>() of the reference (R/src/recipe.cpp:28-35) goes through yaml-cpp's
+// convert<int>::decode: operator>> on a stringstream with std::ios::dec unset, so the
+// base comes from the prefix like strtol(.., 0) ("010" is 8, "0x10" is 16, "08" fails),
+// an optional sign, no leading whitespace, trailing whitespace allowed, the whole scalar
+// consumed, overflow fails. Restated without iostreams (numeric stream extraction is not
+// safe in this statically linked libstdc++ once the host process loaded another one).
 int int_of(const Node& n, const std::string& path) {
     if (n.kind != Node::Scalar) bad(path, "expected an integer");
     const std::string& s = n.text;
-    std::size_t i = (!s.empty() && (s[0] == '-' || s[0] == '+')) ? 1 : 0;
-    bool ok = i < s.size();
-    for (std::size_t j = i; j < s.size(); ++j) ok = ok && std::isdigit(static_cast<unsigned char>(s[j]));
-    if (!ok || s.size() > 11) bad(path, "expected an integer, got '" + s + "'");
-    const long long v = std::stoll(s);
-    if (v < INT32_MIN || v > INT32_MAX) bad(path, "expected an integer, got '" + s + "'");
+    const auto fail_int = [&] { bad(path, "expected an integer, got '" + s + "'"); };
+    std::size_t i = 0;
+    bool neg = false;
+    if (i < s.size() && (s[i] == '+' || s[i] == '-')) neg = s[i++] == '-';
+    int base = 10;
+    if (i + 1 < s.size() && s[i] == '0' && (s[i + 1] == 'x' || s[i + 1] == 'X')) {
+        base = 16;
+        i += 2;
+    } else if (i < s.size() && s[i] == '0') {
+        base = 8;
+    }
+    const std::size_t first = i;
+    long long v = 0;
+    for (; i < s.size(); ++i) {
+        const char c = s[i];
+        int d = -1;
+        if (c >= '0' && c <= '9') d = c - '0';
+        else if (base == 16 && c >= 'a' && c <= 'f') d = c - 'a' + 10;
+        else if (base == 16 && c >= 'A' && c <= 'F') d = c - 'A' + 10;
+        if (d < 0 || d >= base) break;
+        v = v * base + d;
+        if (v > 2147483648LL) fail_int();
+    }
+    if (i == first) fail_int();
+    for (; i < s.size(); ++i)
+        if (!std::isspace(static_cast<unsigned char>(s[i]))) fail_int();
+    if (neg) v = -v;
+    if (v < INT32_MIN || v > INT32_MAX) fail_int();
     return static_cast<int>(v);
 }
 

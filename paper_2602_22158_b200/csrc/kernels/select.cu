@@ -17,7 +17,7 @@ namespace {
 
 constexpr int kSelThreads = 256;
 constexpr int kMaxModules = 1024;
-constexpr int kMaxPairs = kMaxSnapshots - 1;
+constexpr int kMaxPairs = kMaxSelectSnapshots - 1;
 
 __global__ void __launch_bounds__(kSelThreads) select_plan_kernel(const double* __restrict__ parts, int nranks, int P, int M,
                                                                    int n_save, const PlanEntry* __restrict__ shard_entries,

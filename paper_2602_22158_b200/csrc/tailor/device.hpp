@@ -214,9 +214,11 @@ struct PlanEntry {
     std::uint64_t dst_off;
     std::uint64_t bytes;
 };
+// K9 takes the snapshot bases by value (1 KB of launch parameters at 64 snapshots).
+constexpr int kMaxSelectSnapshots = 64;
 struct SnapshotBases {
-    const std::uint8_t* shard[kMaxSnapshots];
-    const std::uint8_t* weights[kMaxSnapshots];
+    const std::uint8_t* shard[kMaxSelectSnapshots];
+    const std::uint8_t* weights[kMaxSelectSnapshots];
 };
 cudaError_t launch_select_plan(const double* d_parts, int nranks, int K, int M, int n_save, const PlanEntry* d_shard_entries,
                                std::uint32_t n_shard, const PlanEntry* d_w_entries, std::uint32_t n_w,

@@ -152,7 +152,9 @@ class ScorePlan {
     int K() const { return K_; }
     int M() const { return M_; }
     std::uint64_t bytes_read() const { return bytes_; }
-    // out: device [K-1][M][2] FP64 (sum delta^2, sum ref^2) for this rank.
+    // out: device [K-1][M][2] FP64 (sum delta^2, sum ref^2) for this rank. Any K >= 2:
+    // sweeps longer than 16 snapshots run as K3 launches over windows of <= 16
+    // snapshots overlapping by one (bytes_read counts the overlap snapshot twice).
     void run(const std::uint8_t* const* snap_bases, double* d_out, cudaStream_t s);
     void set_variant(int v) { variant_ = v; }
 
@@ -160,6 +162,7 @@ class ScorePlan {
     int variant_ = dev::kScoreAuto; // TAILOR_SCORE_VARIANT (diagnostics) sets the default; set_variant overrides
     int K_, M_;
     std::vector<ScoreField> fields_;
+    std::vector<std::pair<int, int>> windows_; // [first, last] snapshot of each K3 launch (<= 16, overlapping by one)
     std::vector<std::vector<std::uint64_t>> offs_;
     std::vector<dev::ScoreTile> tiles_;
     std::vector<std::uint32_t> begin_;
@@ -294,8 +297,9 @@ void verify_checkpoint_dir(const std::string& dir, int device);
 // The pieces of the device re-verify (read_checkpoint's checks), reusable by callers
 // that already hold the layouts (execute_merge verifies files as its lanes finish them):
 // verify_plan = structural checks + per-rank work lists as payload offsets;
-// verify_rank_resident = load one rank payload, run K6 against a device weights payload
-// (counters at d_err[3r..3r+2]; `before_kernel` may block, e.g. until the weights are in);
+// verify_rank_resident = load one rank payload, run K6 against the device weights payload
+// that `weights` returns (counters at d_err[3r..3r+2]; `weights` may block, e.g. until the
+// weights are in);
 // verify_counters = the errors, in rank order.
 struct VerifyPlan {
     ContainerLayout weights;
@@ -306,11 +310,11 @@ struct VerifyPlan {
 };
 VerifyPlan verify_plan(const std::filesystem::path& dir, const CheckpointSummary& s, ContainerLayout weights,
                        std::vector<ContainerLayout> shards);
-void verify_rank_resident(const VerifyPlan& plan, int r, const std::filesystem::path& shard_file, const std::uint8_t* dw,
-                          DeviceBuffer& ds, DeviceBuffer& dpairs, DeviceBuffer& dranges, PinnedBuffer* stage, int readers,
-                          std::uint64_t step, unsigned long long* d_err, cudaStream_t st,
-                          const std::function<void()>& before_kernel);
+void verify_rank_resident(const VerifyPlan& plan, int r, const std::filesystem::path& shard_file, DeviceBuffer& ds,
+                          DeviceBuffer& dpairs, DeviceBuffer& dranges, PinnedBuffer* stage, int readers, std::uint64_t step,
+                          unsigned long long* d_err, cudaStream_t st, const std::function<const std::uint8_t*()>& weights);
 void verify_counters(const std::filesystem::path& dir, int num_ranks, const unsigned long long* d_err);
+void verify_counters_host(const std::filesystem::path& dir, int num_ranks, const unsigned long long* err);
 void load_payload_to(const std::filesystem::path& path, const ContainerLayout& lay, DeviceBuffer& dst, PinnedBuffer* stage,
                      int threads, std::uint64_t step);
 

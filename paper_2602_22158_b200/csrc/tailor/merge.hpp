@@ -67,7 +67,13 @@ struct MergeOptions {
     bool uncached = false; // re-read the source shard per group copy (benchmark mode)
     int device = 0;
     bool verify = true;    // device re-verify of the written composite
+    // Lanes (one output file at a time each) spread round-robin over these devices;
+    // empty = {device}. Output bytes do not depend on the devices or the lane count.
+    std::vector<int> devices;
 };
+inline std::vector<int> lane_devices(const MergeOptions& o) {
+    return o.devices.empty() ? std::vector<int>{o.device} : o.devices;
+}
 
 struct MergeStats {
     std::int64_t shard_files_read = 0;

@@ -3,12 +3,12 @@
 // (R/tools/tailor_main.cpp:66-103, :291-299, :351-357) and adds the
 // update-magnitude `select` / `score` subcommands.
 //
-//   tailor merge  --recipe r.yaml --out DIR [--workers W] [--uncached] [--json] [--device D] [--no-verify]
+//   tailor merge  --recipe r.yaml --out DIR [--workers W] [--uncached] [--json] [--device D | --devices 0,1,..] [--no-verify]
 //   tailor plan   --run RUN --failure-step S --out r.yaml
-//   tailor select --snapshots A,B,... [--rho 0.5] --out r.yaml [--device D] [--json]
-//   tailor score  --snapshots A,B,... [--device D]
+//   tailor select --snapshots A,B,... [--rho 0.5] --out r.yaml [--device D | --devices 0,1,..] [--json]
+//   tailor score  --snapshots A,B,... [--device D | --devices 0,1,..]
 //   tailor check  --ckpt DIR [--device D]
-//   tailor regroup --ckpt DIR --out DIR [--to fine|coarse] [--device D] [--no-verify]
+//   tailor regroup --ckpt DIR --out DIR [--to fine|coarse] [--device D | --devices 0,1,..] [--no-verify]
 //   tailor resume --ckpt DIR --steps S --out RUN [--device D]
 //   tailor train  --config c.json --steps S --interval I --strategy full|parity|filter|magnitude
 //                 --ranks N --out RUN [--lr --weight-decay --head --tail --sparse-multiple --rho --device]
@@ -67,6 +67,16 @@ int text_call(F&& f, std::string& out) {
     return rc;
 }
 
+// --devices 0,1,... (lanes spread over these GPUs; output bytes do not depend on them),
+// else --device D, else device 0
+std::vector<int32_t> devices_of(const Args& a) {
+    std::vector<int32_t> out;
+    if (a.kv.count("devices"))
+        for (const auto& x : split_csv(a.kv.at("devices"))) out.push_back(static_cast<int32_t>(std::stoi(x)));
+    if (out.empty()) out.push_back(a.kv.count("device") ? static_cast<int32_t>(std::stoi(a.kv.at("device"))) : 0);
+    return out;
+}
+
 bool require(const Args& a, std::initializer_list<const char*> keys) {
     for (const char* k : keys)
         if (!a.kv.count(k)) {
@@ -85,10 +95,13 @@ int cmd_merge(const Args& a) {
         return 1;
     }
     tg_merge_options opt{};
+    const std::vector<int32_t> devs = devices_of(a);
     opt.workers = a.kv.count("workers") ? std::stoi(a.kv.at("workers")) : 0;
     opt.uncached = a.flags.count("uncached") ? 1 : 0;
-    opt.device = a.kv.count("device") ? std::stoi(a.kv.at("device")) : 0;
-    opt.verify = a.flags.count("no-verify") ? 0 : 1;
+    opt.device = devs.front();
+    opt.skip_verify = a.flags.count("no-verify") ? 1 : 0;
+    opt.devices = devs.data();
+    opt.num_devices = static_cast<int32_t>(devs.size());
     tg_merge_stats st{};
     const int rc = tg_execute_merge(yaml.c_str(), a.kv.at("out").c_str(), &opt, &st);
     if (rc != TG_OK) return report(rc);
@@ -133,13 +146,14 @@ int cmd_select(const Args& a) {
     std::vector<const char*> ptrs;
     for (const auto& d : dirs) ptrs.push_back(d.c_str());
     const double rho = a.kv.count("rho") ? std::stod(a.kv.at("rho")) : 0.5;
-    const int device = a.kv.count("device") ? std::stoi(a.kv.at("device")) : 0;
+    const std::vector<int32_t> devs = devices_of(a);
     std::vector<int32_t> src(4096);
     double gap = 0.0;
     std::string yaml;
     const int rc = text_call(
         [&](char* b, size_t c, size_t* n) {
-            return tg_select_recipe(ptrs.data(), static_cast<int32_t>(ptrs.size()), rho, device, b, c, n, src.data(), &gap);
+            return tg_select_recipe(ptrs.data(), static_cast<int32_t>(ptrs.size()), rho, devs.data(),
+                                    static_cast<int32_t>(devs.size()), b, c, n, src.data(), &gap);
         },
         yaml);
     if (rc != TG_OK) return report(rc);
@@ -153,10 +167,11 @@ int cmd_score(const Args& a) {
     const auto dirs = split_csv(a.kv.at("snapshots"));
     std::vector<const char*> ptrs;
     for (const auto& d : dirs) ptrs.push_back(d.c_str());
-    const int device = a.kv.count("device") ? std::stoi(a.kv.at("device")) : 0;
+    const std::vector<int32_t> devs = devices_of(a);
     std::vector<double> scores(dirs.size() * 4096);
     int32_t M = 0;
-    const int rc = tg_score_snapshots(ptrs.data(), static_cast<int32_t>(ptrs.size()), device, nullptr, scores.data(), &M);
+    const int rc = tg_score_snapshots(ptrs.data(), static_cast<int32_t>(ptrs.size()), devs.data(), static_cast<int32_t>(devs.size()),
+                                       nullptr, scores.data(), &M);
     if (rc != TG_OK) return report(rc);
     std::printf("{\"scores\":[");
     for (size_t p = 0; p + 1 < dirs.size(); ++p) {
@@ -234,8 +249,11 @@ int cmd_regroup(const Args& a) {
         return 1;
     }
     tg_merge_options opt{};
-    opt.device = a.kv.count("device") ? std::stoi(a.kv.at("device")) : 0;
-    opt.verify = a.flags.count("no-verify") ? 0 : 1;
+    const std::vector<int32_t> devs = devices_of(a);
+    opt.device = devs.front();
+    opt.skip_verify = a.flags.count("no-verify") ? 1 : 0;
+    opt.devices = devs.data();
+    opt.num_devices = static_cast<int32_t>(devs.size());
     tg_merge_stats st{};
     const int rc = tg_regroup(a.kv.at("ckpt").c_str(), a.kv.at("out").c_str(), to == "fine" ? 1 : 0, &opt, &st);
     if (rc != TG_OK) return report(rc);

@@ -97,12 +97,22 @@ class MergeRecipe:
 
 @dataclasses.dataclass
 class MergeOptions:
-    """R/include/tailor/merge.hpp:46-49 (+ device, verify)."""
+    """R/include/tailor/merge.hpp:46-49 (+ device, verify, devices: the output lanes
+    spread round-robin over these GPUs; the bytes written do not depend on them)."""
 
     workers: int = 0
     uncached: bool = False
     device: int = 0
     verify: bool = True
+    devices: Optional[Sequence[int]] = None
+
+    def to_c(self):
+        devs = list(self.devices or [])
+        arr = (ctypes.c_int32 * max(1, len(devs)))(*devs)
+        c = MergeOptionsC(self.workers, 1 if self.uncached else 0, self.device, 0 if self.verify else 1,
+                          ctypes.cast(arr, ctypes.POINTER(ctypes.c_int32)), len(devs), 0)
+        c._keep = arr  # the array must outlive the call
+        return c
 
 
 @dataclasses.dataclass
@@ -139,7 +149,7 @@ def resolve_plan(recipe) -> dict:
 
 def execute_merge(recipe, out_dir: str, options: Optional[MergeOptions] = None) -> MergeStats:
     o = options or MergeOptions()
-    copt = MergeOptionsC(o.workers, 1 if o.uncached else 0, o.device, 1 if o.verify else 0)
+    copt = o.to_c()
     st = MergeStatsC()
     check(lib().tg_execute_merge(_yaml_of(recipe), _b(str(out_dir)), ctypes.byref(copt), ctypes.byref(st)))
     return MergeStats(st.shard_files_read, st.weight_files_read, st.wall_ms, st.device_ms, st.bytes_moved)
@@ -152,7 +162,7 @@ def recipe_from_manifests(run_dir: str, failure_step: int) -> MergeRecipe:
 def regroup(src_dir: str, out_dir: str, to_fine: bool = True, options: Optional[MergeOptions] = None) -> MergeStats:
     """coarse_to_fine / fine_to_coarse of a checkpoint directory on the device (R/src/groups.cpp:152-220)."""
     o = options or MergeOptions()
-    copt = MergeOptionsC(o.workers, 0, o.device, 1 if o.verify else 0)
+    copt = dataclasses.replace(o, uncached=False).to_c()
     st = MergeStatsC()
     check(lib().tg_regroup(_b(str(src_dir)), _b(str(out_dir)), 1 if to_fine else 0, ctypes.byref(copt),
                            ctypes.byref(st)))
@@ -197,24 +207,32 @@ def _dirs_arg(dirs: Sequence[str]):
     return arr
 
 
-def score_snapshots(dirs: Sequence[str], device: int = 0):
-    """Device scores over consecutive snapshot dirs -> (sums[p][m][2], scores[p][m])."""
+def _devices_arg(device: int, devices):
+    devs = list(devices) if devices else [device]
+    return (ctypes.c_int32 * len(devs))(*devs), len(devs)
+
+
+def score_snapshots(dirs: Sequence[str], device: int = 0, devices: Optional[Sequence[int]] = None):
+    """Device scores over consecutive snapshot dirs (any number >= 2) -> (sums[p][m][2], scores[p][m]).
+    `devices`: rank partitions are scored by lanes spread over these GPUs (same result)."""
     n = len(dirs)
     cap = max(1, (n - 1)) * 8192
     sums = (ctypes.c_double * (cap * 2))()
     scores = (ctypes.c_double * cap)()
     m = ctypes.c_int32(0)
-    check(lib().tg_score_snapshots(_dirs_arg(dirs), n, device, sums, scores, ctypes.byref(m)))
+    darr, nd = _devices_arg(device, devices)
+    check(lib().tg_score_snapshots(_dirs_arg(dirs), n, darr, nd, sums, scores, ctypes.byref(m)))
     M = m.value
     return ([[[sums[(p * M + i) * 2], sums[(p * M + i) * 2 + 1]] for i in range(M)] for p in range(n - 1)],
             [[scores[p * M + i] for i in range(M)] for p in range(n - 1)])
 
 
-def select_recipe(dirs: Sequence[str], rho: float = 0.5, device: int = 0):
+def select_recipe(dirs: Sequence[str], rho: float = 0.5, device: int = 0, devices: Optional[Sequence[int]] = None):
     """Score -> magnitude selection -> recipe. Returns (recipe, source_of, min_boundary_gap)."""
     src = (ctypes.c_int32 * 8192)()
     gap = ctypes.c_double(0)
-    yaml = text_call(lambda b, c, n: lib().tg_select_recipe(_dirs_arg(dirs), len(dirs), rho, device, b, c, n, src,
+    darr, nd = _devices_arg(device, devices)
+    yaml = text_call(lambda b, c, n: lib().tg_select_recipe(_dirs_arg(dirs), len(dirs), rho, darr, nd, b, c, n, src,
                                                              ctypes.byref(gap)))
     rec = parse_recipe(yaml)
     M = None

@@ -38,6 +38,7 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.ScoreTileC) == 24
     assert ctypes.sizeof(_lib.ModelSpecC) == 32
     assert ctypes.sizeof(_lib.MergeStatsC) == 40
+    assert ctypes.sizeof(_lib.MergeOptionsC) == 32
 
 
 def test_errors_are_codes_not_exceptions():

@@ -2,6 +2,7 @@
 missing / incompatible sources, the CLI (exit codes, --json), hyperparameter and
 config provenance, tied models. Every successful merge is compared file by file."""
 import json
+import pathlib
 import os
 import shutil
 import subprocess
@@ -230,3 +231,73 @@ def test_merge_reverify_catches_bad_source_data(tmp_path, damage):
     e = our_error(recipe, tmp_path / "our_out")
     assert rc == 2 and err == "ConsistencyError", (rc, err)
     assert e is not None and e.kind == t.ErrorKind.Consistency, e
+
+
+def test_regroup_refuses_a_source_with_bad_padding_before_writing(tmp_path):
+    """read_checkpoint validates the source before the reference regroups it
+    (R/src/checkpoint.cpp:515-553): nonzero shard padding is a CorruptContainer and
+    nothing is written. The device path re-verifies the source first."""
+    need_gpu()
+    import struct
+
+    spec = dict(SPEC, num_layers=3, hidden_dim=4, ffn_dim=16, vocab_size=31)
+    ref_tool("train", *spec_args(spec), "--strategy", "full", "--steps", 10, "--interval", 10, "--ranks", 8,
+             "--grouping", "coarse", "--out", tmp_path / "run")
+    src = tmp_path / "run" / "checkpoint-10"
+    p = src / "optim" / "rank_7.shard"
+    b = bytearray(p.read_bytes())
+    hlen = int.from_bytes(b[:8], "little")
+    hdr = json.loads(b[8:8 + hlen])
+    _, hi = hdr["g0.master"]["data_offsets"]  # coarse group 0 ends in rank 7's padding
+    b[8 + hlen + hi - 4:8 + hlen + hi] = struct.pack("<f", 1.0)
+    p.write_bytes(bytes(b))
+    rc, _, err = ref_tool("regroup", "--dir", src, "--out", tmp_path / "ref", check=False)
+    assert rc != 0 and "CorruptContainer" in err
+    with pytest.raises(t.TailorError) as e:
+        t.regroup(str(src), str(tmp_path / "ours"))
+    assert e.value.kind == t.ErrorKind.CorruptContainer
+    assert not (tmp_path / "ours").exists()
+
+
+@pytest.mark.parametrize("strategy", ["parity", "filter"])
+def test_coarse_partial_checkpoints_verify_like_the_reference(tmp_path, strategy):
+    """A coarse checkpoint stores every group but its manifest (and weights) may cover
+    only some modules; derive_weights pairs only the manifest's tensors
+    (R/src/checkpoint.cpp:287-312), so read_checkpoint accepts it. So must the device
+    re-verify (it used to dereference the missing weights entries)."""
+    need_gpu()
+    spec = dict(SPEC, num_layers=6)
+    cks = ref_tool("train", *spec_args(spec), "--strategy", strategy, "--steps", 40, "--interval", 10, "--ranks", 2,
+                   "--grouping", "coarse", "--out", tmp_path / "run")[1]["checkpoints"]
+    partial = 0
+    for c in cks:
+        man = json.loads((pathlib.Path(c) / "manifest.json").read_text())
+        partial += len(man["modules"]) < spec["num_layers"] + 3
+        ref_tool("read", "--dir", c)
+        t.verify_checkpoint(c)
+    assert partial > 0
+
+
+def test_lane_failure_does_not_hang_the_pipelined_reverify(tmp_path, monkeypatch):
+    """when assembling the weights output fails, lanes that finished a rank
+    file wait for the weights before their re-verify; they must be released and the
+    merge must fail with a Storage error instead of hanging."""
+    need_gpu()
+    import threading
+
+    d = gen(tmp_path, SPEC, 4, 2)
+    monkeypatch.setenv("TAILOR_FAULT", "assemble-weights")
+    recipe = t.MergeRecipe(num_ranks=4, base_checkpoint=d[1], slices=[t.RecipeSlice(d[0], [0, 2])])
+    res = {}
+
+    def run():
+        try:
+            t.execute_merge(recipe, str(tmp_path / "out"), t.MergeOptions(workers=5))
+        except t.TailorError as e:
+            res["e"] = e
+
+    th = threading.Thread(target=run, daemon=True)
+    th.start()
+    th.join(timeout=120)
+    assert not th.is_alive(), "execute_merge hung after a lane failure"
+    assert res.get("e") is not None and res["e"].kind == t.ErrorKind.Storage, res

@@ -483,6 +483,43 @@ def test_verify_detects_corruption(tmp_path):
     assert rc == 2 and "ConsistencyError" in err
 
 
+@pytest.mark.parametrize("K", [17, 20, 35])
+def test_select_recipe_beyond_16_snapshots_matches_reference(tmp_path, K):
+    """The paper merges from 18 and 35 checkpoints and
+    recipe_from_manifests takes any number (R/src/merge.cpp:359-418): sweeps longer than
+    one 16-snapshot K3 launch run as overlapping windows. Scores, selection and recipe
+    equal the reference-side restatement; the merge equals the reference's bytes."""
+    need_gpu()
+    spec = t.ModelSpec(3, 8, 24, 40, False, 4200 + K)
+    d = _gen_ref(tmp_path, spec, 2, K)
+    ref = ref_tool("score", "--snapshots", ",".join(d), "--rho", "0.5")[1]
+    devs = list(range(torch.cuda.device_count())) * 2
+    for kw in (dict(), dict(devices=devs)):
+        rec, src, gap = t.select_recipe(d, 0.5, **kw)
+        _, scores = t.score_snapshots(d, **kw)
+        assert len(scores) == K - 1
+        for p, row in enumerate(ref["scores"]):
+            for m, v in enumerate(row):
+                assert scores[p][m] == pytest.approx(v, rel=SCORE_RTOL)
+        assert rec == t.MergeRecipe.from_json(json.dumps(ref["recipe"]))
+        assert gap == pytest.approx(ref["min_boundary_gap"], rel=1e-6)
+    _both_merge(tmp_path, rec)
+
+
+def test_scoring_rolls_through_two_slots_beyond_16_snapshots(tmp_path, monkeypatch):
+    """Under a device budget of two snapshots per rank, a 20-snapshot sweep rolls
+    through two slots (every pair scored once); same scores as the resident sweep."""
+    need_gpu()
+    spec = t.ModelSpec(2, 8, 24, 40, False, 77)
+    d = _gen_ref(tmp_path, spec, 2, 20)
+    _, full = t.score_snapshots(d)
+    monkeypatch.setenv("TAILOR_DEVICE_BUDGET", str(2 * 4096))
+    _, rolled = t.score_snapshots(d)
+    assert len(rolled) == len(full) == 19
+    for a, b in zip(rolled, full):  # K3 at K=2 vs K=16 tiles: same sums up to FP64 reassociation
+        assert a == pytest.approx(b, rel=1e-12)
+
+
 def test_select_recipe_matches_reference_scorer(tmp_path):
     need_gpu()
     spec = t.ModelSpec(4, 16, 40, 64, False, 42)
@@ -596,6 +633,10 @@ def test_execute_merge_lane_count_independent_and_sources_untouched(tmp_path, N)
     for w in (3, 16):
         t.execute_merge(recipe, str(tmp_path / f"w{w}"), t.MergeOptions(workers=w))
         _assert_same_tree(tmp_path / "w1_ours", tmp_path / f"w{w}")
+    # lanes spread over a device list (every GPU of the box, each listed twice): same bytes
+    devs = list(range(torch.cuda.device_count())) * 2
+    t.execute_merge(recipe, str(tmp_path / "devs"), t.MergeOptions(workers=len(devs), devices=devs))
+    _assert_same_tree(tmp_path / "w1_ours", tmp_path / "devs")
     assert digest() == before
     # identity round trip at this rank count (c9): merged base == source base
     t.execute_merge(t.MergeRecipe(num_ranks=N, base_checkpoint=d[1]), str(tmp_path / "ident"))

@@ -55,6 +55,21 @@ def test_ranges_half_open_and_targets():
     assert r.slices[0].targets == [2, 3]
 
 
+@pytest.mark.parametrize("text,layers", [("010", [8]), ("0x10", [16]), ("+4", [4]), ("0", [0]), ("12", [12])])
+def test_integers_convert_like_yaml_cpp(text, layers):
+    """node.as<int>() (R/src/recipe.cpp:28-35) is yaml-cpp's stream conversion with
+    std::ios::dec unset: a leading 0 means octal and 0x hexadecimal."""
+    r = t.parse_recipe(f"merge_method: passthrough\nnum_ranks: 1\nslices:\n  - source: c\n    layers: [{text}]\n")
+    assert r.slices[0].layers == layers
+
+
+@pytest.mark.parametrize("text", ["08", "0x", "1.0", "4294967296", "1e3"])
+def test_non_integers_are_recipe_errors_like_yaml_cpp(text):
+    with pytest.raises(t.TailorError) as e:
+        t.parse_recipe(f"merge_method: passthrough\nnum_ranks: 1\nslices:\n  - source: c\n    layers: [{text}]\n")
+    assert e.value.kind == t.ErrorKind.Recipe
+
+
 @pytest.mark.parametrize("text", [
     "merge_method: passthrough\nnum_ranks: 2\nextra_key: 1\n",
     "num_ranks: 2\n",
