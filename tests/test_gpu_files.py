@@ -259,23 +259,54 @@ def test_regroup_refuses_a_source_with_bad_padding_before_writing(tmp_path):
     assert not (tmp_path / "ours").exists()
 
 
-@pytest.mark.parametrize("strategy", ["parity", "filter"])
-def test_coarse_partial_checkpoints_verify_like_the_reference(tmp_path, strategy):
-    """A coarse checkpoint stores every group but its manifest (and weights) may cover
-    only some modules; derive_weights pairs only the manifest's tensors
-    (R/src/checkpoint.cpp:287-312), so read_checkpoint accepts it. So must the device
-    re-verify (it used to dereference the missing weights entries)."""
+def _restrict_to_modules(ckpt: pathlib.Path, keep):
+    """Rewrites a checkpoint's manifest and model.weights to cover only `keep` (the
+    optimizer shards keep every group): a container in the reference's own layout —
+    compact sorted JSON header padded with spaces to 8 B, payload in key order."""
+    man = json.loads((ckpt / "manifest.json").read_text())
+    man["modules"] = [m for m in man["modules"] if m in keep]
+    (ckpt / "manifest.json").write_text(json.dumps(man, indent=2) + "\n")
+    b = (ckpt / "model.weights").read_bytes()
+    n = int.from_bytes(b[:8], "little")
+    hdr = json.loads(b[8:8 + n])
+    base = 8 + n
+    mod = lambda name: ".".join(name.split(".")[:2]) if name.startswith("layers.") else name.split(".")[0]  # noqa: E731
+    out_hdr, payload, at = {}, bytearray(), 0
+    for name in sorted(hdr):
+        if mod(name) not in keep:
+            continue
+        lo, hi = hdr[name]["data_offsets"]
+        out_hdr[name] = dict(hdr[name], data_offsets=[at, at + hi - lo])
+        payload += b[base + lo:base + hi]
+        at += hi - lo
+    text = json.dumps(out_hdr, sort_keys=True, separators=(",", ":")).encode()
+    text += b" " * ((-(8 + len(text))) % 8)
+    (ckpt / "model.weights").write_bytes(len(text).to_bytes(8, "little") + text + bytes(payload))
+
+
+def test_coarse_partial_checkpoint_verifies_like_the_reference(tmp_path):
+    """A coarse checkpoint stores every group, but its manifest (and weights) may cover
+    only some modules: group_indices_for_modules returns all coarse groups and
+    derive_weights pairs only the manifest's tensors (R/src/checkpoint.cpp:272-312), so
+    read_checkpoint accepts it. So must the device re-verify (it dereferenced
+    the missing weights entries)."""
     need_gpu()
-    spec = dict(SPEC, num_layers=6)
-    cks = ref_tool("train", *spec_args(spec), "--strategy", strategy, "--steps", 40, "--interval", 10, "--ranks", 2,
-                   "--grouping", "coarse", "--out", tmp_path / "run")[1]["checkpoints"]
-    partial = 0
-    for c in cks:
-        man = json.loads((pathlib.Path(c) / "manifest.json").read_text())
-        partial += len(man["modules"]) < spec["num_layers"] + 3
-        ref_tool("read", "--dir", c)
-        t.verify_checkpoint(c)
-    assert partial > 0
+    spec = dict(SPEC, num_layers=4)
+    ref_tool("train", *spec_args(spec), "--strategy", "full", "--steps", 10, "--interval", 10, "--ranks", 2,
+             "--grouping", "coarse", "--out", tmp_path / "run")
+    ck = tmp_path / "run" / "checkpoint-10"
+    _restrict_to_modules(ck, {"embed_tokens", "layers.1", "layers.3", "norm"})
+    ref_tool("read", "--dir", ck)
+    t.verify_checkpoint(str(ck))
+    # and a damaged kept tensor is still found, with the reference's kind
+    w = bytearray((ck / "model.weights").read_bytes())
+    w[-3] ^= 0x40
+    (ck / "model.weights").write_bytes(bytes(w))
+    rc, _, err = ref_tool("read", "--dir", ck, check=False)
+    assert rc == 2 and "ConsistencyError" in err
+    with pytest.raises(t.TailorError) as e:
+        t.verify_checkpoint(str(ck))
+    assert e.value.kind == t.ErrorKind.Consistency
 
 
 def test_lane_failure_does_not_hang_the_pipelined_reverify(tmp_path, monkeypatch):
