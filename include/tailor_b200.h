@@ -94,6 +94,7 @@ typedef struct tg_score_tile {
     uint64_t elem_start;
 } tg_score_tile;
 
+typedef struct tg_layout tg_layout;
 typedef struct tg_family tg_family;
 typedef struct tg_scorer tg_scorer;
 typedef struct tg_mplan tg_mplan;
@@ -188,16 +189,39 @@ int tg_score_partials(const tg_score_tile* d_tiles, uint32_t ntiles, const float
 int tg_score_combine(const double* d_tile_partials, const uint32_t* d_module_tile_begin, int32_t M, int32_t K,
                      double* d_out, void* stream);
 
-/* ---- synthetic snapshot families S_1..S_K --------------------------- */
+/* ---- snapshot layouts S_1..S_K ----------------------------------------------------
+ * What the device plans below (scorer tiles, merge segments, K9 tables) are built
+ * from: the model (R/include/tailor/model.hpp:14-30), the ZeRO rank count, and each
+ * snapshot's module set (its manifest) and id. The caller owns the payload bytes (a
+ * trainer's resident rank partitions, buffers loaded from files, or the synthetic
+ * generator's output) in the rank-shard / weights payload layout of the files
+ * (R/src/container.cpp:62-100) and binds them to the plans. */
+/* Synthetic set: every snapshot complete, ids "S1".."SK", step k*interval. */
+tg_layout* tg_layout_create(const tg_model_spec* spec, int32_t num_ranks, int32_t snapshots, int64_t interval);
+/* From checkpoint directories (read_checkpoint_summary, R/src/checkpoint.cpp:439-483, of
+ * each): snapshot k = dirs[k-1], id = the path; same geometry, rank count, fine grouping. */
+tg_layout* tg_layout_from_checkpoints(const char* const* dirs, int32_t n);
+void tg_layout_destroy(tg_layout* l); /* no-op on a family's layout (tg_family_layout) */
+int tg_layout_set_partial(tg_layout* l, int32_t k, const char* modules_csv);
+int tg_layout_set_id(tg_layout* l, int32_t k, const char* id);
+int32_t tg_layout_num_modules(const tg_layout* l);
+int32_t tg_layout_num_ranks(const tg_layout* l);
+int32_t tg_layout_snapshots(const tg_layout* l);
+uint64_t tg_layout_shard_bytes(const tg_layout* l, int32_t k, int32_t rank);
+uint64_t tg_layout_weights_bytes(const tg_layout* l, int32_t k);
+uint64_t tg_layout_packed_master_bytes(const tg_layout* l, int32_t rank);
+uint64_t tg_layout_parameter_count(const tg_layout* l);
+/* Combine per-rank partials [nranks][K-1][M][2] in rank order, select (a14), emit the
+ * recipe over the snapshot ids (latest-version rule, R/src/merge.cpp:375-417). */
+int tg_layout_select(const tg_layout* l, const double* rank_partials, int32_t nranks, double rho, char* yaml_out,
+                     size_t cap, size_t* needed, int32_t* source_of, double* scores, double* min_boundary_gap);
+
+/* ---- synthetic snapshot generator -------------------------------------
+ * A layout (tg_family_layout: owned by the family) plus the K5 kernels that write its
+ * payloads: bit-exact with the reference-side generator (oracle/ref_driver.cpp). */
 tg_family* tg_family_create(const tg_model_spec* spec, int32_t num_ranks, int32_t snapshots, int64_t interval);
 void tg_family_destroy(tg_family* f);
-int tg_family_set_partial(tg_family* f, int32_t k, const char* modules_csv);
-int tg_family_set_id(tg_family* f, int32_t k, const char* id);
-int32_t tg_family_num_modules(const tg_family* f);
-uint64_t tg_family_shard_bytes(tg_family* f, int32_t k, int32_t rank);
-uint64_t tg_family_weights_bytes(tg_family* f, int32_t k);
-uint64_t tg_family_packed_master_bytes(tg_family* f, int32_t rank);
-uint64_t tg_family_parameter_count(tg_family* f);
+tg_layout* tg_family_layout(tg_family* f);
 int tg_family_gen_shard(tg_family* f, int32_t rank, int32_t k0, int32_t k1, uint8_t* const* outs, void* stream);
 int tg_family_gen_weights(tg_family* f, int32_t k0, int32_t k1, uint64_t lo, uint64_t hi, uint8_t* const* outs,
                           void* stream);
@@ -206,14 +230,11 @@ int tg_family_gen_masters(tg_family* f, int32_t rank, int32_t k0, int32_t k1, ui
 int tg_family_gen_shard_range(tg_family* f, int32_t rank, int32_t k, uint64_t lo, uint64_t hi, uint8_t* out,
                               void* stream);
 int tg_family_write_dir(tg_family* f, int32_t k, const char* dir);
-/* Combine per-rank partials [nranks][K-1][M][2] in rank order, select (a14),
- * emit the recipe over the family's snapshot ids. */
-int tg_family_select(tg_family* f, const double* rank_partials, int32_t nranks, double rho, char* yaml_out,
-                     size_t cap, size_t* needed, int32_t* source_of, double* scores, double* min_boundary_gap);
 
-/* Scorer over snapshots k0..k1 of a family, rank partition `rank`; packed=1 reads
- * tg_family_gen_masters buffers, packed=0 full shard payloads. */
-tg_scorer* tg_scorer_create(tg_family* f, int32_t rank, int32_t k0, int32_t k1, int32_t packed);
+/* Scorer over snapshots k0..k1 of a layout, rank partition `rank` (any k1 - k0 >= 1);
+ * packed=1 reads masters in the packed layout (tg_family_gen_masters), packed=0 full
+ * shard payloads. */
+tg_scorer* tg_scorer_create(const tg_layout* l, int32_t rank, int32_t k0, int32_t k1, int32_t packed);
 void tg_scorer_destroy(tg_scorer* s);
 uint64_t tg_scorer_bytes(const tg_scorer* s);
 /* 0 auto (TMA-bulk ring when the bases are 16-B aligned, else register loads),
@@ -222,10 +243,10 @@ int tg_scorer_set_variant(tg_scorer* s, int32_t variant);
 /* d_out: [K-1][M][2] FP64 partial sums for this rank. */
 int tg_scorer_run(tg_scorer* s, const uint8_t* const* bases, double* d_out, void* stream);
 
-/* Merge plan of one output partition of a recipe over family snapshots:
+/* Merge plan of one output partition of a recipe over a layout's snapshots (by id):
  * container = -1 -> weights bytes of share unit/units, r >= 0 -> rank r shard
  * (units > 1: its unit-th tensor-aligned byte sub-range, for host-staged units). */
-tg_mplan* tg_mplan_create(tg_family* f, const char* recipe_yaml, int32_t container, int32_t unit, int32_t units);
+tg_mplan* tg_mplan_create(const tg_layout* l, const char* recipe_yaml, int32_t container, int32_t unit, int32_t units);
 void tg_mplan_destroy(tg_mplan* p);
 uint64_t tg_mplan_bytes(const tg_mplan* p);
 int tg_mplan_range(const tg_mplan* p, uint64_t* lo, uint64_t* hi, uint64_t* payload_bytes);
@@ -262,11 +283,11 @@ int tg_mplan_run_host(tg_mplan* p, const uint8_t* const* h_windows, const uint8_
 int tg_mplan_wait(tg_mplan* p);
 
 /* Whole score -> select -> merge step on the device for one unit (rank-r shard +
- * weights share unit/units) of a family of full snapshots: selection (a14) and both
+ * weights share unit/units) of a layout of full snapshots (2..64): selection (a14) and both
  * segment tables are built by a device kernel from the all-gathered per-rank partials
  * [nranks][K-1][M][2]; no host synchronization (graph-capturable). */
 typedef struct tg_dstep tg_dstep;
-tg_dstep* tg_dstep_create(tg_family* f, int32_t rank, int32_t unit, int32_t units, double rho);
+tg_dstep* tg_dstep_create(const tg_layout* l, int32_t rank, int32_t unit, int32_t units, double rho);
 void tg_dstep_destroy(tg_dstep* s);
 int tg_dstep_range(const tg_dstep* s, uint64_t* shard_bytes, uint64_t* weights_lo, uint64_t* weights_hi);
 int tg_dstep_bind(tg_dstep* s, const uint8_t* const* shard_bases, const uint8_t* const* weights_window_bases);

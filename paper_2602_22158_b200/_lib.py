@@ -125,22 +125,28 @@ SIGNATURES = {
     "tg_read_probe": (_I, [_P, _U64, _P, _P]),
     "tg_score_partials": (_I, [_P, _U32, _P, _U32, _I32, _I32, _P, _P]),
     "tg_score_combine": (_I, [_P, _P, _I32, _I32, _P, _P]),
+    "tg_layout_create": (_P, [_c.POINTER(ModelSpecC), _I32, _I32, _I64]),
+    "tg_layout_from_checkpoints": (_P, [_c.POINTER(_S), _I32]),
+    "tg_layout_destroy": (None, [_P]),
+    "tg_layout_set_partial": (_I, [_P, _I32, _S]),
+    "tg_layout_set_id": (_I, [_P, _I32, _S]),
+    "tg_layout_num_modules": (_I32, [_P]),
+    "tg_layout_num_ranks": (_I32, [_P]),
+    "tg_layout_snapshots": (_I32, [_P]),
+    "tg_layout_shard_bytes": (_U64, [_P, _I32, _I32]),
+    "tg_layout_weights_bytes": (_U64, [_P, _I32]),
+    "tg_layout_packed_master_bytes": (_U64, [_P, _I32]),
+    "tg_layout_parameter_count": (_U64, [_P]),
+    "tg_layout_select": (_I, [_P, _c.POINTER(_D), _I32, _D, _c.c_char_p, _SZ, _PSZ, _c.POINTER(_I32),
+                              _c.POINTER(_D), _c.POINTER(_D)]),
     "tg_family_create": (_P, [_c.POINTER(ModelSpecC), _I32, _I32, _I64]),
     "tg_family_destroy": (None, [_P]),
-    "tg_family_set_partial": (_I, [_P, _I32, _S]),
-    "tg_family_set_id": (_I, [_P, _I32, _S]),
-    "tg_family_num_modules": (_I32, [_P]),
-    "tg_family_shard_bytes": (_U64, [_P, _I32, _I32]),
-    "tg_family_weights_bytes": (_U64, [_P, _I32]),
-    "tg_family_packed_master_bytes": (_U64, [_P, _I32]),
-    "tg_family_parameter_count": (_U64, [_P]),
+    "tg_family_layout": (_P, [_P]),
     "tg_family_gen_shard": (_I, [_P, _I32, _I32, _I32, _PP, _P]),
     "tg_family_gen_weights": (_I, [_P, _I32, _I32, _U64, _U64, _PP, _P]),
     "tg_family_gen_masters": (_I, [_P, _I32, _I32, _I32, _PP, _P]),
     "tg_family_gen_shard_range": (_I, [_P, _I32, _I32, _U64, _U64, _P, _P]),
     "tg_family_write_dir": (_I, [_P, _I32, _S]),
-    "tg_family_select": (_I, [_P, _c.POINTER(_D), _I32, _D, _c.c_char_p, _SZ, _PSZ, _c.POINTER(_I32),
-                              _c.POINTER(_D), _c.POINTER(_D)]),
     "tg_scorer_create": (_P, [_P, _I32, _I32, _I32, _I32]),
     "tg_scorer_destroy": (None, [_P]),
     "tg_scorer_bytes": (_U64, [_P]),

@@ -30,8 +30,15 @@ using nlohmann::json;
 using namespace tailor;
 namespace fs = std::filesystem;
 
+// A layout handle either owns its SnapshotSet (tg_layout_create / _from_checkpoints)
+// or views a family's (tg_family_layout; owned by the family, never destroyed by the caller).
+struct tg_layout {
+    SnapshotSet* set = nullptr;
+    std::unique_ptr<SnapshotSet> owned;
+};
 struct tg_family {
     std::unique_ptr<SynthFamily> fam;
+    tg_layout view;
 };
 struct tg_scorer {
     std::unique_ptr<ScorePlan> plan;
@@ -47,7 +54,7 @@ struct tg_mplan {
     std::unique_ptr<HostMerge> host;
     std::uint64_t host_chunk = 0;
     HostMerge::Resident host_resident; // the resident map the host pipeline was built for
-    const SynthFamily* fam = nullptr;
+    const SnapshotSet* fam = nullptr;
     std::vector<int> window_k;
     std::vector<ContainerLayout> window_layout; // source container of each window
 };
@@ -136,7 +143,7 @@ json plan_json(const MergePlan& p) {
             {"group_copies", copies}, {"assignment", assign}};
 }
 
-CheckpointSummary family_summary(const SynthFamily& f, const std::string& id) {
+CheckpointSummary family_summary(const SnapshotSet& f, const std::string& id) {
     const int k = f.index_of(id);
     if (k == 0) fail(ErrorKind::MissingArtifact, "checkpoint directory '" + id + "' does not exist");
     return f.summary(k, id);
@@ -609,13 +616,41 @@ int tg_score_combine(const double* d_tile_partials, const uint32_t* d_begin, int
 
 tg_family* tg_family_create(const tg_model_spec* spec, int32_t num_ranks, int32_t snapshots, int64_t interval) {
     tg_family* out = nullptr;
-    guard([&] { out = new tg_family{std::make_unique<SynthFamily>(to_spec(spec), num_ranks, snapshots, interval)}; });
+    guard([&] {
+        out = new tg_family{std::make_unique<SynthFamily>(to_spec(spec), num_ranks, snapshots, interval), {}};
+        out->view.set = out->fam.get();
+    });
     return out;
 }
 
 void tg_family_destroy(tg_family* f) { delete f; }
 
-int tg_family_set_partial(tg_family* f, int32_t k, const char* csv) {
+tg_layout* tg_family_layout(tg_family* f) { return f ? &f->view : nullptr; }
+
+tg_layout* tg_layout_create(const tg_model_spec* spec, int32_t num_ranks, int32_t snapshots, int64_t interval) {
+    tg_layout* out = nullptr;
+    guard([&] {
+        auto set = std::make_unique<SnapshotSet>(to_spec(spec), num_ranks, snapshots, interval);
+        out = new tg_layout{set.get(), std::move(set)};
+    });
+    return out;
+}
+
+tg_layout* tg_layout_from_checkpoints(const char* const* dirs, int32_t n) {
+    tg_layout* out = nullptr;
+    guard([&] {
+        if (!dirs || n < 1) fail(ErrorKind::Recipe, "no checkpoint directories");
+        auto set = SnapshotSet::from_checkpoints(std::vector<std::string>(dirs, dirs + n));
+        out = new tg_layout{set.get(), std::move(set)};
+    });
+    return out;
+}
+
+void tg_layout_destroy(tg_layout* l) {
+    if (l && l->owned) delete l; // a family's view belongs to the family
+}
+
+int tg_layout_set_partial(tg_layout* l, int32_t k, const char* csv) {
     return guard([&] {
         std::vector<ModuleId> mods;
         std::string cur;
@@ -628,38 +663,40 @@ int tg_family_set_partial(tg_family* f, int32_t k, const char* csv) {
             }
         }
         if (!cur.empty()) mods.push_back(parse_module_name(cur));
-        f->fam->set_partial(k, mods);
+        l->set->set_partial(k, mods);
     });
 }
 
-int tg_family_set_id(tg_family* f, int32_t k, const char* id) {
+int tg_layout_set_id(tg_layout* l, int32_t k, const char* id) {
     return guard([&] {
-        if (k < 1 || k > f->fam->snapshots()) fail(ErrorKind::Geometry, "snapshot index out of range");
-        f->fam->set_id(k, id ? id : "");
+        if (k < 1 || k > l->set->snapshots()) fail(ErrorKind::Geometry, "snapshot index out of range");
+        l->set->set_id(k, id ? id : "");
     });
 }
 
-int32_t tg_family_num_modules(const tg_family* f) { return f->fam->model().module_count(); }
+int32_t tg_layout_num_modules(const tg_layout* l) { return l->set->model().module_count(); }
+int32_t tg_layout_num_ranks(const tg_layout* l) { return l->set->num_ranks(); }
+int32_t tg_layout_snapshots(const tg_layout* l) { return l->set->snapshots(); }
 
-uint64_t tg_family_shard_bytes(tg_family* f, int32_t k, int32_t rank) {
+uint64_t tg_layout_shard_bytes(const tg_layout* l, int32_t k, int32_t rank) {
     uint64_t n = 0;
-    guard([&] { n = f->fam->layout(k).shards.at(static_cast<std::size_t>(rank)).payload_bytes; });
+    guard([&] { n = l->set->layout(k).shards.at(static_cast<std::size_t>(rank)).payload_bytes; });
     return n;
 }
 
-uint64_t tg_family_weights_bytes(tg_family* f, int32_t k) {
+uint64_t tg_layout_weights_bytes(const tg_layout* l, int32_t k) {
     uint64_t n = 0;
-    guard([&] { n = f->fam->layout(k).weights.payload_bytes; });
+    guard([&] { n = l->set->layout(k).weights.payload_bytes; });
     return n;
 }
 
-uint64_t tg_family_packed_master_bytes(tg_family* f, int32_t rank) {
+uint64_t tg_layout_packed_master_bytes(const tg_layout* l, int32_t rank) {
     uint64_t n = 0;
-    guard([&] { n = f->fam->packed_master_bytes(rank); });
+    guard([&] { n = l->set->packed_master_bytes(rank); });
     return n;
 }
 
-uint64_t tg_family_parameter_count(tg_family* f) { return static_cast<uint64_t>(f->fam->model().parameter_count()); }
+uint64_t tg_layout_parameter_count(const tg_layout* l) { return static_cast<uint64_t>(l->set->model().parameter_count()); }
 
 int tg_family_gen_shard(tg_family* f, int32_t rank, int32_t k0, int32_t k1, uint8_t* const* outs, void* stream) {
     return guard([&] { f->fam->gen_shard(rank, k0, k1, outs, static_cast<cudaStream_t>(stream)); });
@@ -682,10 +719,10 @@ int tg_family_write_dir(tg_family* f, int32_t k, const char* dir) {
     return guard([&] { f->fam->write_dir(k, dir ? dir : ""); });
 }
 
-int tg_family_select(tg_family* f, const double* parts, int32_t nranks, double rho, char* out, size_t cap,
+int tg_layout_select(const tg_layout* l, const double* parts, int32_t nranks, double rho, char* out, size_t cap,
                      size_t* needed, int32_t* source_of, double* scores, double* min_gap) {
     return guard([&] {
-        const SynthFamily& fam = *f->fam;
+        const SnapshotSet& fam = *l->set;
         const int K = fam.snapshots(), M = fam.model().module_count();
         std::vector<std::vector<double>> sc(static_cast<std::size_t>(K - 1), std::vector<double>(static_cast<std::size_t>(M)));
         for (int p = 0; p < K - 1; ++p)
@@ -709,10 +746,12 @@ int tg_family_select(tg_family* f, const double* parts, int32_t nranks, double r
     });
 }
 
-tg_scorer* tg_scorer_create(tg_family* f, int32_t rank, int32_t k0, int32_t k1, int32_t packed) {
+tg_scorer* tg_scorer_create(const tg_layout* l, int32_t rank, int32_t k0, int32_t k1, int32_t packed) {
     tg_scorer* out = nullptr;
     guard([&] {
-        const SynthFamily& fam = *f->fam;
+        const SnapshotSet& fam = *l->set;
+        if (rank < 0 || rank >= fam.num_ranks()) fail(ErrorKind::Geometry, "rank out of range");
+        if (k0 < 1 || k1 > fam.snapshots() || k1 - k0 < 1) fail(ErrorKind::Geometry, "snapshot range out of bounds");
         const auto fields = score_fields(fam.model(), fam.num_ranks());
         std::vector<std::vector<std::uint64_t>> offs;
         for (int k = k0; k <= k1; ++k) {
@@ -753,10 +792,10 @@ int tg_scorer_run(tg_scorer* s, const uint8_t* const* bases, double* d_out, void
     return guard([&] { s->plan->run(bases, d_out, static_cast<cudaStream_t>(stream)); });
 }
 
-tg_mplan* tg_mplan_create(tg_family* f, const char* yaml, int32_t container, int32_t unit, int32_t units) {
+tg_mplan* tg_mplan_create(const tg_layout* l, const char* yaml, int32_t container, int32_t unit, int32_t units) {
     tg_mplan* out = nullptr;
     guard([&] {
-        const SynthFamily& fam = *f->fam;
+        const SnapshotSet& fam = *l->set;
         const MergePlan plan =
             resolve_plan_with(parse_recipe(yaml ? yaml : ""), [&](const std::string& id) { return family_summary(fam, id); });
         std::map<std::string, SourceLayout> lays;
@@ -917,9 +956,9 @@ int tg_mplan_wait(tg_mplan* p) {
     });
 }
 
-tg_dstep* tg_dstep_create(tg_family* f, int32_t rank, int32_t unit, int32_t units, double rho) {
+tg_dstep* tg_dstep_create(const tg_layout* l, int32_t rank, int32_t unit, int32_t units, double rho) {
     tg_dstep* out = nullptr;
-    guard([&] { out = new tg_dstep{std::make_unique<DeviceSelectStep>(*f->fam, rank, unit, units, rho)}; });
+    guard([&] { out = new tg_dstep{std::make_unique<DeviceSelectStep>(*l->set, rank, unit, units, rho)}; });
     return out;
 }
 

@@ -267,7 +267,7 @@ std::vector<float> synth_sigma(std::uint64_t seed, int M, int j) {
     return s;
 }
 
-SynthFamily::SynthFamily(const ModelSpec& spec, int num_ranks, int snapshots, std::int64_t interval)
+SnapshotSet::SnapshotSet(const ModelSpec& spec, int num_ranks, int snapshots, std::int64_t interval)
     : model_(spec), num_ranks_(num_ranks), K_(snapshots), interval_(interval) {
     if (num_ranks < 1) fail(ErrorKind::Geometry, "num_ranks must be >= 1");
     if (snapshots < 1) fail(ErrorKind::Geometry, "need at least one snapshot");
@@ -277,32 +277,65 @@ SynthFamily::SynthFamily(const ModelSpec& spec, int num_ranks, int snapshots, st
     for (int k = 1; k <= K_; ++k) ids_.push_back("S" + std::to_string(k));
 }
 
-void SynthFamily::set_partial(int k, const std::vector<ModuleId>& modules) {
+std::unique_ptr<SnapshotSet> SnapshotSet::from_checkpoints(const std::vector<std::string>& dirs) {
+    if (dirs.empty()) fail(ErrorKind::Recipe, "no checkpoint directories");
+    std::vector<CheckpointSummary> sums;
+    for (const auto& d : dirs) sums.push_back(read_checkpoint_summary(d));
+    const CheckpointSummary& s0 = sums.front();
+    for (const auto& s : sums) {
+        if (!s.spec.same_geometry(s0.spec)) fail(ErrorKind::Geometry, "checkpoints disagree on model geometry");
+        if (s.optim.num_ranks != s0.optim.num_ranks) fail(ErrorKind::Geometry, "checkpoints disagree on the rank count");
+        if (s.optim.grouping != Grouping::Fine) fail(ErrorKind::Geometry, "device plans need the fine grouping");
+    }
+    auto set = std::make_unique<SnapshotSet>(s0.spec, s0.optim.num_ranks, static_cast<int>(dirs.size()), 1);
+    for (std::size_t i = 0; i < dirs.size(); ++i) {
+        set->modules_[i] = sums[i].manifest.modules;
+        set->ids_[i] = dirs[i];
+    }
+    set->real_ = std::move(sums);
+    return set;
+}
+
+std::int64_t SnapshotSet::step(int k) const {
+    return real_.empty() ? interval_ * k : real_.at(static_cast<std::size_t>(k - 1)).trainer.step;
+}
+
+void SnapshotSet::set_partial(int k, const std::vector<ModuleId>& modules) {
     if (k < 1 || k > K_) fail(ErrorKind::Geometry, "snapshot index out of range");
+    if (!real_.empty()) fail(ErrorKind::Consistency, "the module set of a checkpoint on disk comes from its manifest");
     std::vector<ModuleId> sorted;
     for (const auto& m : model_.modules())
         if (std::find(modules.begin(), modules.end(), m) != modules.end()) sorted.push_back(m);
     if (sorted.empty()) fail(ErrorKind::Consistency, "manifest module list is empty");
     modules_[static_cast<std::size_t>(k - 1)] = sorted;
     layouts_[static_cast<std::size_t>(k - 1)].reset();
+}
+
+void SynthFamily::set_partial(int k, const std::vector<ModuleId>& modules) {
+    SnapshotSet::set_partial(k, modules);
     for (auto it = tables_.begin(); it != tables_.end();)
         it = std::get<0>(it->first) == k ? tables_.erase(it) : std::next(it);
 }
 
-const CheckpointLayout& SynthFamily::layout(int k) const {
+const CheckpointLayout& SnapshotSet::layout(int k) const {
     if (k < 1 || k > K_) fail(ErrorKind::Geometry, "snapshot index out of range");
     auto& slot = const_cast<std::unique_ptr<CheckpointLayout>&>(layouts_[static_cast<std::size_t>(k - 1)]);
     if (!slot) slot = std::make_unique<CheckpointLayout>(checkpoint_layout(model_, num_ranks_, modules_[static_cast<std::size_t>(k - 1)]));
     return *slot;
 }
 
-int SynthFamily::index_of(const std::string& id) const {
+int SnapshotSet::index_of(const std::string& id) const {
     for (int k = 1; k <= K_; ++k)
         if (ids_[static_cast<std::size_t>(k - 1)] == id) return k;
     return 0;
 }
 
-CheckpointSummary SynthFamily::summary(int k, const std::string& dir) const {
+CheckpointSummary SnapshotSet::summary(int k, const std::string& dir) const {
+    if (!real_.empty()) {
+        CheckpointSummary s = real_.at(static_cast<std::size_t>(k - 1));
+        s.dir = dir;
+        return s;
+    }
     const CheckpointLayout& lay = layout(k);
     CheckpointSummary s;
     s.dir = dir;
@@ -323,9 +356,12 @@ CheckpointSummary SynthFamily::summary(int k, const std::string& dir) const {
     return s;
 }
 
-std::string SynthFamily::trainer_state_json(int k) const { return sidecar_text(summary(k, "").trainer); }
-std::string SynthFamily::manifest_json(int k) const { return sidecar_text(summary(k, "").manifest); }
-std::string SynthFamily::optim_meta_json(int k) const { return sidecar_text(summary(k, "").optim); }
+SynthFamily::SynthFamily(const ModelSpec& spec, int num_ranks, int snapshots, std::int64_t interval)
+    : SnapshotSet(spec, num_ranks, snapshots, interval) {}
+
+std::string SnapshotSet::trainer_state_json(int k) const { return sidecar_text(summary(k, "").trainer); }
+std::string SnapshotSet::manifest_json(int k) const { return sidecar_text(summary(k, "").manifest); }
+std::string SnapshotSet::optim_meta_json(int k) const { return sidecar_text(summary(k, "").optim); }
 
 void SynthFamily::ensure_sigma(int kmax) {
     if (kmax <= sigma_rows_) return;
@@ -348,7 +384,7 @@ std::vector<ScoreField> score_fields(const ModelLayout& model, int num_ranks) {
     return out;
 }
 
-std::uint64_t SynthFamily::packed_master_bytes(int /*rank*/) const {
+std::uint64_t SnapshotSet::packed_master_bytes(int /*rank*/) const {
     std::uint64_t off = 0;
     for (const auto& f : score_fields(model_, num_ranks_)) off = align16(off + static_cast<std::uint64_t>(f.chunk) * 4);
     return off;
@@ -844,7 +880,7 @@ void HostMerge::run(const std::vector<const std::uint8_t*>& h_windows, const std
 }
 
 // ---- device select + plan step ---------------------------------------------------------
-DeviceSelectStep::DeviceSelectStep(const SynthFamily& fam, int rank, int unit, int units, double rho)
+DeviceSelectStep::DeviceSelectStep(const SnapshotSet& fam, int rank, int unit, int units, double rho)
     : K_(fam.snapshots()), M_(fam.model().module_count()) {
     if (K_ < 2 || K_ > dev::kMaxSelectSnapshots) fail(ErrorKind::Geometry, "device selection needs 2..64 snapshots");
     if (!(rho > 0.0 && rho <= 1.0)) fail(ErrorKind::Recipe, "selection ratio rho must lie in (0, 1]");

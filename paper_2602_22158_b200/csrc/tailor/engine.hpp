@@ -1,5 +1,6 @@
 // Host-side engine binding layer-map plans to the device kernels:
-//   SynthFamily  — synthetic snapshots S_1..S_K (layouts, sidecars, K5 launches)
+//   SnapshotSet  — layouts of snapshots S_1..S_K (synthetic, or read from checkpoint dirs)
+//   SynthFamily  — a SnapshotSet plus the K5 generator of its payloads (synthetic sources)
 //   ScorePlan    — K3/K4 tile tables for one rank partition of K snapshots
 //   DeviceMerge  — K2 segment table for one output partition, bound to device windows
 //   HostMerge    — the shard pipeline: pinned host sources -> H2D -> K2 -> D2H, chunked,
@@ -82,15 +83,25 @@ class PinnedBuffer {
 // sigma_j(m) = 1e-6 * g^{pi_j(m)}, g = 1000^{1/(M-1)} (SURVEY §8d ladder).
 std::vector<float> synth_sigma(std::uint64_t seed, int M, int j);
 
-class SynthFamily {
+// The layouts of K snapshots S_1..S_K of one model over N ZeRO ranks — what the
+// device plans (scorer tiles, merge segments, K9 tables) are built from. Either
+// synthetic (every snapshot full unless set_partial; ids "S1".."SK", step k*interval)
+// or read from real checkpoint directories (read_checkpoint_summary of each: spec,
+// rank count, manifest module set, step; ids = the directory paths). It owns no
+// payload bytes: callers (a trainer, a loader, the generator below) own the device
+// buffers and bind them to the plans.
+class SnapshotSet {
   public:
-    SynthFamily(const ModelSpec& spec, int num_ranks, int snapshots, std::int64_t interval);
-    void set_partial(int k, const std::vector<ModuleId>& modules);
+    SnapshotSet(const ModelSpec& spec, int num_ranks, int snapshots, std::int64_t interval);
+    // Snapshot k = dirs[k-1]; all must share geometry, rank count and the fine grouping.
+    static std::unique_ptr<SnapshotSet> from_checkpoints(const std::vector<std::string>& dirs);
+    virtual ~SnapshotSet() = default;
+    virtual void set_partial(int k, const std::vector<ModuleId>& modules);
 
     const ModelLayout& model() const { return model_; }
     int num_ranks() const { return num_ranks_; }
     int snapshots() const { return K_; }
-    std::int64_t step(int k) const { return interval_ * k; }
+    std::int64_t step(int k) const;
     const CheckpointLayout& layout(int k) const;
     CheckpointSummary summary(int k, const std::string& dir) const;
     std::string trainer_state_json(int k) const;
@@ -99,6 +110,24 @@ class SynthFamily {
     const std::string& id(int k) const { return ids_[static_cast<std::size_t>(k - 1)]; }
     void set_id(int k, const std::string& id) { ids_[static_cast<std::size_t>(k - 1)] = id; }
     int index_of(const std::string& id) const; // 1-based; 0 if unknown
+    // Masters only, packed per field in score-field order (the scorer's packed layout).
+    std::uint64_t packed_master_bytes(int rank) const;
+
+  protected:
+    ModelLayout model_;
+    int num_ranks_;
+    int K_;
+    std::int64_t interval_;
+    std::vector<std::vector<ModuleId>> modules_;
+    std::vector<std::unique_ptr<CheckpointLayout>> layouts_;
+    std::vector<std::string> ids_;
+    std::vector<CheckpointSummary> real_; // from_checkpoints: the on-disk summaries
+};
+
+class SynthFamily : public SnapshotSet {
+  public:
+    SynthFamily(const ModelSpec& spec, int num_ranks, int snapshots, std::int64_t interval);
+    void set_partial(int k, const std::vector<ModuleId>& modules) override;
 
     // Device generation. Snapshots k0..k1 must share one layout.
     void gen_shard(int rank, int k0, int k1, std::uint8_t* const* outs, cudaStream_t s);
@@ -108,7 +137,6 @@ class SynthFamily {
     void gen_masters_packed(int rank, int k0, int k1, std::uint8_t* const* outs, cudaStream_t s);
     // bytes [lo, hi) of snapshot k's rank shard payload; entry-aligned (synchronous table upload)
     void gen_shard_range(int rank, int k, std::uint64_t lo, std::uint64_t hi, std::uint8_t* out, cudaStream_t s);
-    std::uint64_t packed_master_bytes(int rank) const;
     // GPU-generate snapshot k and write it as a checkpoint directory.
     void write_dir(int k, const std::string& dir);
 
@@ -121,13 +149,6 @@ class SynthFamily {
     ShardTables& shard_tables(int k, int rank, bool packed);
     void ensure_sigma(int kmax);
 
-    ModelLayout model_;
-    int num_ranks_;
-    int K_;
-    std::int64_t interval_;
-    std::vector<std::vector<ModuleId>> modules_;
-    std::vector<std::unique_ptr<CheckpointLayout>> layouts_;
-    std::vector<std::string> ids_;
     std::map<std::tuple<int, int, bool>, std::unique_ptr<ShardTables>> tables_;
     DeviceBuffer sigma_;
     int sigma_rows_ = 0;
@@ -198,7 +219,7 @@ class DeviceMerge {
 // selection is bitwise the host's (select_by_magnitude).
 class DeviceSelectStep {
   public:
-    DeviceSelectStep(const SynthFamily& fam, int rank, int unit, int units, double rho);
+    DeviceSelectStep(const SnapshotSet& snaps, int rank, int unit, int units, double rho);
     std::uint64_t shard_bytes() const { return shard_bytes_; }
     std::uint64_t weights_lo() const { return wlo_; }
     std::uint64_t weights_hi() const { return whi_; }

@@ -26,7 +26,7 @@ from ._lib import (ErrorKind, GatherSegC, HostCopyC, MergeOptionsC, MergeStatsC,
 
 __all__ = ["ErrorKind", "TailorError", "ModelSpec", "RecipeSlice", "MergeRecipe", "MergeOptions", "MergeStats",
            "parse_recipe", "recipe_to_yaml", "resolve_plan", "execute_merge", "recipe_from_manifests",
-           "verify_checkpoint", "regroup", "train", "resume", "score_snapshots", "select_recipe", "layer_map", "SynthFamily", "Scorer",
+           "verify_checkpoint", "regroup", "train", "resume", "score_snapshots", "select_recipe", "layer_map", "SnapshotLayout", "SynthFamily", "Scorer",
            "MergePartition", "SelectStep", "Trainer", "STRATEGIES", "gather", "read_probe"]
 
 
@@ -259,62 +259,70 @@ def read_probe(d_src: int, nbytes: int, d_sink: int, stream: int = 0) -> None:
     check(lib().tg_read_probe(d_src, nbytes, d_sink, stream))
 
 
-class SynthFamily:
-    """Synthetic snapshots S_1..S_K of SURVEY §8(d), generated on the device."""
+class SnapshotLayout:
+    """Layouts of snapshots S_1..S_K (tg_layout_*): what the scorer, merge plans and the
+    device select step are built from. Synthetic (`SnapshotLayout(spec, N, K)`: complete
+    snapshots, ids "S1".."SK") or read from checkpoint directories
+    (`SnapshotLayout.from_checkpoints(dirs)`: ids are the paths). It holds no payload
+    bytes; the caller binds its own device buffers (rank-shard / weights payload layout)."""
 
-    def __init__(self, spec: ModelSpec, num_ranks: int, snapshots: int, interval: int = 100):
-        self.spec, self.num_ranks, self.snapshots, self.interval = spec, num_ranks, snapshots, interval
-        c = spec.to_c()
-        self._h = check_handle(lib().tg_family_create(ctypes.byref(c), num_ranks, snapshots, interval))
+    def __init__(self, spec: Optional[ModelSpec] = None, num_ranks: int = 1, snapshots: int = 1, interval: int = 100,
+                 _handle=None, _owner=None):
+        self._owner = _owner  # a SynthFamily whose layout this is (keeps it alive; not destroyed here)
+        if _handle is not None:
+            self._h, self._owned = _handle, False
+        else:
+            c = spec.to_c()
+            self._h, self._owned = check_handle(lib().tg_layout_create(ctypes.byref(c), num_ranks, snapshots,
+                                                                       interval)), True
+
+    @classmethod
+    def from_checkpoints(cls, dirs: Sequence[str]) -> "SnapshotLayout":
+        h = check_handle(lib().tg_layout_from_checkpoints(_dirs_arg(dirs), len(dirs)))
+        obj = cls(_handle=h)
+        obj._owned = True
+        return obj
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
-            lib().tg_family_destroy(h)
-            self._h = None
+        if h and getattr(self, "_owned", False):
+            lib().tg_layout_destroy(h)
+        self._h = None
 
     @property
-    def handle(self):
+    def layout_handle(self):
         return self._h
 
     @property
     def num_modules(self) -> int:
-        return lib().tg_family_num_modules(self._h)
+        return lib().tg_layout_num_modules(self._h)
+
+    @property
+    def num_ranks(self) -> int:
+        return lib().tg_layout_num_ranks(self._h)
+
+    @property
+    def snapshots(self) -> int:
+        return lib().tg_layout_snapshots(self._h)
 
     @property
     def parameter_count(self) -> int:
-        return lib().tg_family_parameter_count(self._h)
+        return lib().tg_layout_parameter_count(self._h)
 
     def set_partial(self, k: int, modules: Sequence[str]) -> None:
-        check(lib().tg_family_set_partial(self._h, k, ",".join(modules).encode()))
+        check(lib().tg_layout_set_partial(self._h, k, ",".join(modules).encode()))
 
     def set_id(self, k: int, ident: str) -> None:
-        check(lib().tg_family_set_id(self._h, k, ident.encode()))
+        check(lib().tg_layout_set_id(self._h, k, ident.encode()))
 
     def shard_bytes(self, k: int, rank: int) -> int:
-        return lib().tg_family_shard_bytes(self._h, k, rank)
+        return lib().tg_layout_shard_bytes(self._h, k, rank)
 
     def weights_bytes(self, k: int) -> int:
-        return lib().tg_family_weights_bytes(self._h, k)
+        return lib().tg_layout_weights_bytes(self._h, k)
 
     def packed_master_bytes(self, rank: int) -> int:
-        return lib().tg_family_packed_master_bytes(self._h, rank)
-
-    def gen_shard(self, rank: int, k0: int, k1: int, outs: Sequence[int], stream: int = 0) -> None:
-        check(lib().tg_family_gen_shard(self._h, rank, k0, k1, ptr_array(outs), stream))
-
-    def gen_weights(self, k0: int, k1: int, lo: int, hi: int, outs: Sequence[int], stream: int = 0) -> None:
-        check(lib().tg_family_gen_weights(self._h, k0, k1, lo, hi, ptr_array(outs), stream))
-
-    def gen_masters(self, rank: int, k0: int, k1: int, outs: Sequence[int], stream: int = 0) -> None:
-        check(lib().tg_family_gen_masters(self._h, rank, k0, k1, ptr_array(outs), stream))
-
-    def gen_shard_range(self, rank: int, k: int, lo: int, hi: int, out: int, stream: int = 0) -> None:
-        """Bytes [lo, hi) of snapshot k's rank shard payload (tensor-aligned window)."""
-        check(lib().tg_family_gen_shard_range(self._h, rank, k, lo, hi, out, stream))
-
-    def write_dir(self, k: int, path: str) -> None:
-        check(lib().tg_family_write_dir(self._h, k, _b(str(path))))
+        return lib().tg_layout_packed_master_bytes(self._h, rank)
 
     def select(self, rank_partials: Sequence[float], nranks: int, rho: float = 0.5):
         """Combine [nranks][K-1][M][2] partials in rank order -> (recipe_yaml, source_of, scores, gap)."""
@@ -323,18 +331,60 @@ class SynthFamily:
         src = (ctypes.c_int32 * M)()
         scores = (ctypes.c_double * max(1, (K - 1) * M))()
         gap = ctypes.c_double(0)
-        yaml = text_call(lambda b, c, n: lib().tg_family_select(self._h, arr, nranks, rho, b, c, n, src, scores,
+        yaml = text_call(lambda b, c, n: lib().tg_layout_select(self._h, arr, nranks, rho, b, c, n, src, scores,
                                                                  ctypes.byref(gap)))
         return (yaml, [src[i] for i in range(M)],
                 [[scores[p * M + m] for m in range(M)] for p in range(K - 1)], gap.value)
 
 
-class Scorer:
-    """K3/K4 scorer plan for one rank partition of snapshots k0..k1 of a family."""
+class SynthFamily(SnapshotLayout):
+    """Synthetic snapshots S_1..S_K of SURVEY §8(d): a SnapshotLayout plus the device
+    generator (K5) of their payloads."""
 
-    def __init__(self, family: SynthFamily, rank: int, k0: int, k1: int, packed: bool = False):
-        self._fam = family
-        self._h = check_handle(lib().tg_scorer_create(family.handle, rank, k0, k1, 1 if packed else 0))
+    def __init__(self, spec: ModelSpec, num_ranks: int, snapshots: int, interval: int = 100):
+        self.spec, self.interval = spec, interval
+        c = spec.to_c()
+        self._fh = check_handle(lib().tg_family_create(ctypes.byref(c), num_ranks, snapshots, interval))
+        super().__init__(_handle=lib().tg_family_layout(self._fh))
+
+    def __del__(self):
+        self._h = None  # the layout view belongs to the family
+        h = getattr(self, "_fh", None)
+        if h:
+            lib().tg_family_destroy(h)
+            self._fh = None
+
+    @property
+    def handle(self):
+        return self._fh
+
+    @property
+    def layout(self) -> SnapshotLayout:
+        return SnapshotLayout(_handle=self._h, _owner=self)
+
+    def gen_shard(self, rank: int, k0: int, k1: int, outs: Sequence[int], stream: int = 0) -> None:
+        check(lib().tg_family_gen_shard(self._fh, rank, k0, k1, ptr_array(outs), stream))
+
+    def gen_weights(self, k0: int, k1: int, lo: int, hi: int, outs: Sequence[int], stream: int = 0) -> None:
+        check(lib().tg_family_gen_weights(self._fh, k0, k1, lo, hi, ptr_array(outs), stream))
+
+    def gen_masters(self, rank: int, k0: int, k1: int, outs: Sequence[int], stream: int = 0) -> None:
+        check(lib().tg_family_gen_masters(self._fh, rank, k0, k1, ptr_array(outs), stream))
+
+    def gen_shard_range(self, rank: int, k: int, lo: int, hi: int, out: int, stream: int = 0) -> None:
+        """Bytes [lo, hi) of snapshot k's rank shard payload (tensor-aligned window)."""
+        check(lib().tg_family_gen_shard_range(self._fh, rank, k, lo, hi, out, stream))
+
+    def write_dir(self, k: int, path: str) -> None:
+        check(lib().tg_family_write_dir(self._fh, k, _b(str(path))))
+
+
+class Scorer:
+    """K3/K4 scorer plan for one rank partition of snapshots k0..k1 of a layout (or family)."""
+
+    def __init__(self, layout: SnapshotLayout, rank: int, k0: int, k1: int, packed: bool = False):
+        self._fam = layout
+        self._h = check_handle(lib().tg_scorer_create(layout.layout_handle, rank, k0, k1, 1 if packed else 0))
         self.K = k1 - k0 + 1
 
     def __del__(self):
@@ -359,9 +409,10 @@ class MergePartition:
     """K2 plan for one output partition: container=-1 -> weights share unit/units, r -> rank-r shard
     (units > 1: its unit-th tensor-aligned byte sub-range)."""
 
-    def __init__(self, family: SynthFamily, recipe_yaml: str, container: int, unit: int = 0, units: int = 1):
-        self._fam = family
-        self._h = check_handle(lib().tg_mplan_create(family.handle, recipe_yaml.encode(), container, unit, units))
+    def __init__(self, layout: SnapshotLayout, recipe_yaml: str, container: int, unit: int = 0, units: int = 1):
+        self._fam = layout
+        self._h = check_handle(lib().tg_mplan_create(layout.layout_handle, recipe_yaml.encode(), container, unit,
+                                                     units))
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -470,10 +521,10 @@ class SelectStep:
     """Device score -> select -> merge step for one unit of a family of full snapshots
     (tg_dstep_*): selection and segment tables built on the device, no host sync."""
 
-    def __init__(self, family: SynthFamily, rank: int, unit: int, units: int, rho: float = 0.5):
-        self._fam = family
-        self.K, self.M = family.snapshots, family.num_modules
-        self._h = check_handle(lib().tg_dstep_create(family.handle, rank, unit, units, rho))
+    def __init__(self, layout: SnapshotLayout, rank: int, unit: int, units: int, rho: float = 0.5):
+        self._fam = layout
+        self.K, self.M = layout.snapshots, layout.num_modules
+        self._h = check_handle(lib().tg_dstep_create(layout.layout_handle, rank, unit, units, rho))
 
     def __del__(self):
         h = getattr(self, "_h", None)
