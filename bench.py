@@ -664,6 +664,7 @@ def our_arm(args, rank, world, local_rank):
         ref_w = torch.empty(max(16, wpl.bytes), dtype=torch.uint8, device=dev)
         spl.run(ref_s.data_ptr(), args.variant, sp)
         wpl.run(ref_w.data_ptr(), args.variant, sp)
+        bulk = spl.bulk_ok  # bound plan: its segments and bases decide the K2 path
         torch.cuda.synchronize(dev)
         ok = (src_d == src_h and chunked_equal(torch, ref_s, out_shard[:spl.bytes])
               and chunked_equal(torch, ref_w[:wpl.bytes], out_w[:wpl.bytes]))
@@ -699,7 +700,6 @@ def our_arm(args, rank, world, local_rank):
     s_ms = statistics.mean(kt["score"])
     gather_achieved = 2 * out_shard.numel() / (g_ms / 1e3) / 1e9
     score_achieved = scorers[mine[0]].bytes_read / (s_ms / 1e3) / 1e9
-    bulk = t.MergePartition(fam, base_yaml, mine[0]).bulk_ok
     traffic, traffic_src = ncu_traffic("gather_bulk_kernel" if bulk and args.variant != 1 else "gather_lsu_kernel",
                                        args.workload)
     resident = res.resident_bytes()

@@ -1,4 +1,4 @@
-// Parallel pread (see tailor/io.hpp).
+// Parallel pread, buffered or O_DIRECT (see tailor/io.hpp).
 #include "tailor/io.hpp"
 
 #include <algorithm>
@@ -6,9 +6,14 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <fcntl.h>
+#include <memory>
+#include <sys/mman.h>
 #include <exception>
 #include <mutex>
 #include <thread>
+#include <vector>
 #include <unistd.h>
 
 #include "tailor/errors.hpp"
@@ -55,19 +60,143 @@ int io_threads() {
     return static_cast<int>(std::clamp<unsigned>(hw ? hw : 4u, 1u, 16u));
 }
 
+AlignedBuffer::AlignedBuffer(std::uint64_t bytes) : n(bytes) {
+    void* q = nullptr;
+    if (posix_memalign(&q, kDirectAlign, std::max<std::uint64_t>(bytes, kDirectAlign)) != 0)
+        fail(ErrorKind::Storage, "out of host memory");
+    p = static_cast<std::uint8_t*>(q);
+}
+AlignedBuffer::~AlignedBuffer() { std::free(p); }
+
+IoMode io_mode_from_env(IoMode requested) {
+    const char* v = std::getenv("TAILOR_IO");
+    if (!v || !*v) return requested;
+    const std::string s(v);
+    if (s == "auto") return IoMode::Auto;
+    if (s == "buffered") return IoMode::Buffered;
+    if (s == "direct") return IoMode::DirectRead;
+    if (s == "direct-rw") return IoMode::DirectRW;
+    return requested;
+}
+
+const char* io_mode_name(IoMode m) {
+    switch (m) {
+        case IoMode::Auto: return "auto";
+        case IoMode::Buffered: return "buffered";
+        case IoMode::DirectRead: return "direct";
+        case IoMode::DirectRW: return "direct-rw";
+    }
+    return "?";
+}
+
+double page_cache_fraction(int fd, std::uint64_t off, std::uint64_t len) {
+    if (len == 0) return 1.0;
+    const std::uint64_t pg = static_cast<std::uint64_t>(::sysconf(_SC_PAGESIZE));
+    const std::uint64_t a = off / pg * pg, b = off + len;
+    void* m = ::mmap(nullptr, b - a, PROT_READ, MAP_SHARED, fd, static_cast<off_t>(a));
+    if (m == MAP_FAILED) return 1.0; // unknown: keep the page cache
+    std::vector<unsigned char> v((b - a + pg - 1) / pg);
+    double frac = 1.0;
+    if (::mincore(m, b - a, v.data()) == 0) {
+        std::size_t in = 0;
+        for (unsigned char c : v) in += c & 1u;
+        frac = static_cast<double>(in) / static_cast<double>(v.size());
+    }
+    ::munmap(m, b - a);
+    return frac;
+}
+
+bool want_direct_read(IoMode mode, int fd, std::uint64_t off, std::uint64_t len) {
+    switch (mode) {
+        case IoMode::Buffered: return false;
+        case IoMode::DirectRead:
+        case IoMode::DirectRW: return true;
+        case IoMode::Auto: return page_cache_fraction(fd, off, len) < 0.5;
+    }
+    return false;
+}
+
+int open_direct_read(const std::string& path) { return ::open(path.c_str(), O_RDONLY | O_DIRECT); }
+
+namespace {
+
+// Bounce buffers of the direct path, reused across calls (a 16 MB piece plus the
+// two partial blocks around it).
+constexpr std::uint64_t kPiece = 16ull << 20;
+constexpr std::uint64_t kBounce = kPiece + 2 * kDirectAlign;
+
+struct BouncePool {
+    std::mutex mu;
+    std::vector<std::unique_ptr<AlignedBuffer>> free;
+    std::unique_ptr<AlignedBuffer> take() {
+        std::lock_guard<std::mutex> lk(mu);
+        if (free.empty()) return std::make_unique<AlignedBuffer>(kBounce);
+        auto b = std::move(free.back());
+        free.pop_back();
+        return b;
+    }
+    void give(std::unique_ptr<AlignedBuffer> b) {
+        std::lock_guard<std::mutex> lk(mu);
+        free.push_back(std::move(b));
+    }
+};
+BouncePool& bounce_pool() {
+    static BouncePool* p = new BouncePool(); // process lifetime
+    return *p;
+}
+
+// pread of n bytes, stopping early only at EOF; returns the bytes read
+std::uint64_t pread_full(int fd, std::uint8_t* dst, std::uint64_t n, std::uint64_t off, const std::string& what) {
+    std::uint64_t got = 0;
+    while (got < n) {
+        const ssize_t r = ::pread(fd, dst + got, n - got, static_cast<off_t>(off + got));
+        if (r < 0) fail(ErrorKind::Storage, "read failed for '" + what + "'");
+        if (r == 0) break;
+        got += static_cast<std::uint64_t>(r);
+    }
+    return got;
+}
+
+void read_buffered(const ReadJob& p, const std::string& what) {
+    if (pread_full(p.fd, p.dst, p.bytes, p.offset, what) != p.bytes) fail(ErrorKind::Storage, "read failed for '" + what + "'");
+}
+
+// O_DIRECT read of [offset, offset+bytes) into dst (either may be unaligned).
+void read_direct(const ReadJob& p, const std::string& what) {
+    constexpr std::uint64_t A = kDirectAlign;
+    const std::uint64_t lo = p.offset, hi = p.offset + p.bytes;
+    const std::uint64_t a0 = lo / A * A, a1 = (hi + A - 1) / A * A;
+    std::unique_ptr<AlignedBuffer> bounce;
+    const auto via_bounce = [&](std::uint64_t blo, std::uint64_t bhi) { // aligned blocks -> copy the overlap
+        if (!bounce) bounce = bounce_pool().take();
+        const std::uint64_t got = pread_full(p.dfd, bounce->p, bhi - blo, blo, what);
+        const std::uint64_t x = std::max(lo, blo), y = std::min(hi, bhi);
+        if (got < y - blo) fail(ErrorKind::Storage, "read failed for '" + what + "' (short direct read)");
+        std::memcpy(p.dst + (x - lo), bounce->p + (x - blo), y - x);
+    };
+    const bool congruent = (reinterpret_cast<std::uintptr_t>(p.dst) - lo) % A == 0;
+    const std::uint64_t m0 = (lo + A - 1) / A * A, m1 = hi / A * A; // whole blocks inside [lo, hi)
+    if (congruent && m0 < m1) {
+        if (lo < m0) via_bounce(a0, m0);
+        if (pread_full(p.dfd, p.dst + (m0 - lo), m1 - m0, m0, what) != m1 - m0)
+            fail(ErrorKind::Storage, "read failed for '" + what + "' (short direct read)");
+        if (m1 < hi) via_bounce(m1, a1);
+    } else {
+        for (std::uint64_t b = a0; b < a1; b += kPiece) via_bounce(b, std::min(a1, b + kPiece));
+    }
+    if (bounce) bounce_pool().give(std::move(bounce));
+}
+
+} // namespace
+
 void run_reads(const std::vector<ReadJob>& jobs, int threads, const std::string& what) {
-    constexpr std::uint64_t kPiece = 16ull << 20;
     std::vector<ReadJob> pieces;
     for (const auto& j : jobs)
         for (std::uint64_t at = 0; at < j.bytes; at += kPiece)
-            pieces.push_back({j.fd, j.dst + at, std::min(kPiece, j.bytes - at), j.offset + at});
+            pieces.push_back({j.fd, j.dst + at, std::min(kPiece, j.bytes - at), j.offset + at, j.dfd});
     const auto read_one = [&](const ReadJob& p) {
-        std::uint64_t got = 0;
-        while (got < p.bytes) {
-            const ssize_t r = ::pread(p.fd, p.dst + got, p.bytes - got, static_cast<off_t>(p.offset + got));
-            if (r <= 0) fail(ErrorKind::Storage, "read failed for '" + what + "'");
-            got += static_cast<std::uint64_t>(r);
-        }
+        if (p.dfd >= 0) read_direct(p, what);
+        else read_buffered(p, what);
     };
     const int n = std::max(1, std::min<int>(threads, static_cast<int>(pieces.size())));
     if (n == 1) {

@@ -16,10 +16,50 @@ struct ReadJob {
     std::uint8_t* dst;
     std::uint64_t bytes;
     std::uint64_t offset;
+    int dfd = -1; // O_DIRECT descriptor of the same file (-1: buffered pread on fd)
 };
 
 // Executes all jobs (any order); the first failure is rethrown as StorageError.
+// Jobs with a direct descriptor read with O_DIRECT: whole 4 KB blocks straight into
+// `dst` where dst and the file offset are congruent mod 4 KB (the staging layouts
+// of the merge lanes arrange that), the partial head/tail blocks and any
+// incongruent job through an aligned bounce buffer.
 void run_reads(const std::vector<ReadJob>& jobs, int threads, const std::string& what);
+
+// ---- direct I/O ------------------------------------------------
+// The reference reads every byte through the page cache with an istreambuf loop
+// (R/src/container.cpp:193-207). Sources that are not in the page cache (a
+// recovery reading checkpoints written long ago or elsewhere) are read here with
+// O_DIRECT: deep parallel queues straight into pinned staging, no page-cache
+// insertion, no readahead limits. Warm sources keep buffered reads (a memcpy from
+// the page cache beats the device).
+enum class IoMode : int {
+    Auto = 0,        // O_DIRECT reads for source files mostly absent from the page cache
+    Buffered = 1,    // everything through the page cache (the reference's behaviour)
+    DirectRead = 2,  // O_DIRECT reads of every source file
+    DirectRW = 3,    // + O_DIRECT writes of the output files (and direct re-verify reads)
+};
+constexpr std::uint64_t kDirectAlign = 4096;
+// TAILOR_IO=auto|buffered|direct|direct-rw overrides `requested` when set.
+IoMode io_mode_from_env(IoMode requested);
+const char* io_mode_name(IoMode m);
+// Fraction of the file's pages [off, off+len) resident in the page cache (mincore).
+double page_cache_fraction(int fd, std::uint64_t off, std::uint64_t len);
+// Whether a source read of [off, off+len) of `fd` should use O_DIRECT under `mode`.
+bool want_direct_read(IoMode mode, int fd, std::uint64_t off, std::uint64_t len);
+// open(path, O_RDONLY | O_DIRECT), -1 if the filesystem refuses O_DIRECT.
+int open_direct_read(const std::string& path);
+
+// Aligned host memory for O_DIRECT bounce buffers (page-aligned, freed with free()).
+struct AlignedBuffer {
+    std::uint8_t* p = nullptr;
+    std::uint64_t n = 0;
+    AlignedBuffer() = default;
+    explicit AlignedBuffer(std::uint64_t bytes);
+    ~AlignedBuffer();
+    AlignedBuffer(const AlignedBuffer&) = delete;
+    AlignedBuffer& operator=(const AlignedBuffer&) = delete;
+};
 // Default worker count for host I/O: hardware threads, capped at 16.
 int io_threads();
 
