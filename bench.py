@@ -1330,13 +1330,47 @@ def trainer_arm(args, rank, world, local_rank):
 FILES_SPEC = (8, 1024, 2752, 32000, False, 8, 4, 0.5)  # BASELINE.md §2 "medium" shape
 
 
+def disk_probe(work: pathlib.Path, gib: float = 1.0):
+    """tools/disk_probe on the work directory's filesystem (compiled on first use):
+    the files line's rooflines (device read bandwidth with O_DIRECT, page-cache read and
+    write rates)."""
+    exe = ROOT / "tools" / "disk_probe"
+    src = ROOT / "tools" / "disk_probe.cpp"
+    try:
+        if not exe.exists() or exe.stat().st_mtime < src.stat().st_mtime:
+            subprocess.run(["g++", "-O2", "-std=c++17", "-pthread", str(src), "-o", str(exe)], check=True,
+                           capture_output=True)
+        p = subprocess.run([str(exe), str(work), str(gib), "8", "4"], capture_output=True, text=True, check=True)
+        return json.loads(p.stdout.strip().splitlines()[-1])
+    except Exception as e:  # the line still prints, without its disk roofline
+        return {"error": str(e)[:200]}
+
+
+def evict_files(paths):
+    """Drops the files' pages from the page cache (fsync first: only clean pages go)."""
+    for p in paths:
+        fd = os.open(p, os.O_RDONLY)
+        try:
+            os.fsync(fd)
+            os.posix_fadvise(fd, 0, 0, os.POSIX_FADV_DONTNEED)
+        finally:
+            os.close(fd)
+
+
 def files_arm(args):
-    """Drop-in comparison on files (the reference's own definition of a merge:
-    file reads, assembly, writes and the mandatory re-verify): our select+merge
-    (device scorer on the snapshot files -> selection -> execute_merge with the
-    device gather and device re-verify) vs the reference's (ref_tool select-merge:
-    read_checkpoint scorer restatement + resolve_plan + execute_merge) on the same
-    synthetic snapshot directories (page cache warm, /tmp)."""
+    """The reference's own definition of a merge, on files (reads, assembly, writes and
+    the mandatory re-verify): our select+merge (device scorer on the snapshot files ->
+    selection -> execute_merge with the device gather and device re-verify) vs the
+    reference's (ref_tool select-merge: read_checkpoint scorer restatement +
+    resolve_plan + execute_merge) on the same synthetic snapshot directories, in two
+    page-cache states:
+      warm — sources in the page cache (both arms), io auto -> buffered reads;
+      cold — the sources' pages dropped before every step (fsync + POSIX_FADV_DONTNEED),
+             io auto -> O_DIRECT source reads (and, for comparison, one buffered-read step).
+    Rooflines from tools/disk_probe on the same filesystem: cold against the device's
+    O_DIRECT read bandwidth (the bytes that must come off the device: every snapshot's
+    masters for the scorer + the composite's source bytes), warm against the host's
+    page-cache copy rates (reads: scorer + merge + re-verify; writes: the composite)."""
     import paper_2602_22158_b200 as t
 
     L, h, f, v, tied, N, K, rho = FILES_SPEC
@@ -1348,22 +1382,38 @@ def files_arm(args):
         for k in range(1, K + 1):
             fam.write_dir(k, dirs[k - 1])
         os.sync()  # flush the sources now: background writeback of them would land inside timed steps
-        ours, refs, comp, step_ms = [], [], 0, []
-        for i in range(args.warmup + args.steps):
-            out = work / f"ours-{i}"
+        src_files = [str(p) for d in dirs for p in sorted(pathlib.Path(d).rglob("*")) if p.is_file()]
+        master_bytes = K * sum(hi - lo for r in range(N) for lo, hi in master_byte_ranges(fam, r, K))
+        probe = disk_probe(work)
+
+        def one(i, tag, io="auto", cold=False):
+            if cold:
+                evict_files(src_files)
+            out = work / f"ours-{tag}-{i}"
             t0 = time.perf_counter()
             rec, _, gap = t.select_recipe(dirs, rho)
             t1 = time.perf_counter()
-            st = t.execute_merge(rec, str(out), t.MergeOptions(workers=cores))
+            st = t.execute_merge(rec, str(out), t.MergeOptions(workers=cores, io_mode=io))
             dt = time.perf_counter() - t0
-            phases = {"select_ms": round((t1 - t0) * 1e3, 1), "merge_ms": round(st.wall_ms, 1),
-                      "gather_device_ms": round(st.device_ms, 2)}
-            comp = st.bytes_moved
             shutil.rmtree(out, ignore_errors=True)
+            os.sync()  # the composite's writeback stays out of the next step
+            return dt, st, gap, {"select_ms": round((t1 - t0) * 1e3, 1), "merge_ms": round(st.wall_ms, 1),
+                                 "gather_device_ms": round(st.device_ms, 2)}
+
+        warm, cold, comp, gap, phases, cold_st = [], [], 0, None, None, None
+        for i in range(args.warmup + args.steps):
+            dt, st, gap, ph = one(i, "warm")
+            comp = st.bytes_moved
             if i >= args.warmup:
-                ours.append(dt)
-                step_ms.append((phases["select_ms"], phases["merge_ms"]))
+                warm.append(dt)
+                phases = ph
+        cold_steps = max(1, min(args.steps, 3))
+        for i in range(cold_steps):
+            dt, cold_st, _, cph = one(i, "cold", cold=True)
+            cold.append(dt)
+        cold_buf, _, _, _ = one(0, "coldbuf", io="buffered", cold=True)
         ref_steps = max(1, min(args.steps, 3))
+        refs = []
         for i in range(1 + ref_steps):
             out = work / f"ref-{i}"
             t0 = time.perf_counter()
@@ -1375,19 +1425,45 @@ def files_arm(args):
                 refs.append(dt)
     finally:
         shutil.rmtree(work, ignore_errors=True)
-    o_v = comp / statistics.median(ours) / 1e9
+    w_s, c_s = statistics.median(warm), statistics.median(cold)
+    o_v, c_v = comp / w_s / 1e9, comp / c_s / 1e9
     r_v = comp / statistics.median(refs) / 1e9
+    # cold bound: bytes that must come off the device / its O_DIRECT read bandwidth
+    disk_bytes = master_bytes + comp
+    rd = probe.get("read_direct_gbs")
+    cold_roof = None
+    if rd:
+        floor = disk_bytes / (rd * 1e9)
+        cold_roof = {"bound": "device read (O_DIRECT, tools/disk_probe)", "achieved": round(disk_bytes / c_s / 1e9, 3),
+                     "peak": rd, "unit": "GB/s", "frac": round(floor / c_s, 4), "bytes_per_step": disk_bytes,
+                     "floor_ms": round(floor * 1e3, 1)}
+    # warm bound: page-cache copies (reads: scorer masters + merge sources + re-verify; writes: composite)
+    rw, wc = probe.get("read_warm_gbs"), probe.get("write_cached_gbs")
+    warm_roof = None
+    if rw and wc:
+        floor = (master_bytes + 2 * comp) / (rw * 1e9) + comp / (wc * 1e9)
+        warm_roof = {"bound": "host page-cache copies (tools/disk_probe, 32 threads): reads/read_warm + writes/write_cached",
+                     "achieved_gbs_composite": round(o_v, 3), "read_bytes_per_step": master_bytes + 2 * comp,
+                     "write_bytes_per_step": comp, "peak_read_gbs": rw, "peak_write_gbs": wc,
+                     "floor_ms": round(floor * 1e3, 1), "frac": round(floor / w_s, 4)}
     print(json.dumps({
         "metric": "composite-checkpoint merge GB/s on files (score+select+merge+re-verify)",
         "value": round(o_v, 4), "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(statistics.median(ours) * 1e3, 2), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(w_s * 1e3, 2), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8/f32/f64", "data": "synthetic (written by the GPU writer, byte-identical "
                                                           "to the reference writer), page cache warm",
         "config": {"workload": "files", "shape": f"L{L} h{h} f{f} v{v} N{N} K{K} rho{rho}",
-                   "composite_bytes": comp, "min_boundary_gap": gap, "last_step_phases": phases,
-                   "steps_select_merge_ms": step_ms},
+                   "composite_bytes": comp, "scorer_master_bytes": master_bytes, "min_boundary_gap": gap,
+                   "last_step_phases": phases},
+        "roofline": warm_roof,
+        "cold": {"value": round(c_v, 4), "unit": "GB/s", "ms_per_step": round(c_s * 1e3, 1), "steps": cold_steps,
+                 "io": "auto (O_DIRECT source reads; the sources' pages dropped before every step)",
+                 "direct_read_bytes": cold_st.direct_read_bytes if cold_st else None, "last_step_phases": cph,
+                 "roofline": cold_roof,
+                 "buffered_reads_same_state": {"value": round(comp / cold_buf / 1e9, 4), "ms_per_step": round(cold_buf * 1e3, 1)}},
+        "disk_probe": probe,
         "reference": {"value": round(r_v, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
-                      "ms_per_step": round(statistics.median(refs) * 1e3, 1)},
+                      "ms_per_step": round(statistics.median(refs) * 1e3, 1), "page_cache": "warm"},
         "speedup_vs_reference": round(o_v / r_v, 2)}))
     return 0
 

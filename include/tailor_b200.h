@@ -56,9 +56,16 @@ typedef struct tg_model_spec {
 } tg_model_spec;
 
 /* MergeOptions / MergeStats (R/include/tailor/merge.hpp:46-55), extended with
- * device timing, the composite byte count and the devices the output lanes run on.
- * A zero-initialised struct means: workers = default, cached, device 0, re-verify on
- * (the reference always re-verifies, R/src/merge.cpp:353). */
+ * device timing, the composite byte count, the devices the output lanes run on and
+ * the file I/O mode. A zero-initialised struct means: workers = default, cached,
+ * device 0, re-verify on (the reference always re-verifies, R/src/merge.cpp:353),
+ * io_mode auto. */
+enum {
+    TG_IO_AUTO = 0,        /* O_DIRECT reads of source files mostly absent from the page cache */
+    TG_IO_BUFFERED = 1,    /* everything through the page cache (the reference's behaviour) */
+    TG_IO_DIRECT = 2,      /* O_DIRECT reads of every source file */
+    TG_IO_DIRECT_RW = 3    /* + O_DIRECT writes of the output files */
+};
 typedef struct tg_merge_options {
     int32_t workers;        /* output/IO lanes; 0 = max(num_ranks, host threads) */
     int32_t uncached;       /* reload source shard per group copy (benchmark mode) */
@@ -67,7 +74,7 @@ typedef struct tg_merge_options {
     const int32_t* devices; /* num_devices > 0: lanes spread round-robin over devices[0..num_devices);
                                output bytes do not depend on the devices (R/tests/acceptance.cpp:442-458) */
     int32_t num_devices;
-    int32_t reserved;
+    int32_t io_mode;        /* TG_IO_*; the TAILOR_IO environment variable overrides it */
 } tg_merge_options;
 
 typedef struct tg_merge_stats {
@@ -76,6 +83,8 @@ typedef struct tg_merge_stats {
     double wall_ms;
     double device_ms;
     uint64_t bytes_moved;
+    uint64_t direct_read_bytes;  /* source bytes read with O_DIRECT */
+    uint64_t direct_write_bytes; /* output bytes written with O_DIRECT (whole 4 KB blocks) */
 } tg_merge_stats;
 
 /* K2 segment: dst[dst_off, dst_off+bytes) <- src[0, bytes). */

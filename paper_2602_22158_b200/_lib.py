@@ -55,12 +55,13 @@ class ModelSpecC(ctypes.Structure):
 class MergeOptionsC(ctypes.Structure):
     _fields_ = [("workers", ctypes.c_int32), ("uncached", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("skip_verify", ctypes.c_int32), ("devices", ctypes.POINTER(ctypes.c_int32)),
-                ("num_devices", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("num_devices", ctypes.c_int32), ("io_mode", ctypes.c_int32)]
 
 
 class MergeStatsC(ctypes.Structure):
     _fields_ = [("shard_files_read", ctypes.c_int64), ("weight_files_read", ctypes.c_int64),
-                ("wall_ms", ctypes.c_double), ("device_ms", ctypes.c_double), ("bytes_moved", ctypes.c_uint64)]
+                ("wall_ms", ctypes.c_double), ("device_ms", ctypes.c_double), ("bytes_moved", ctypes.c_uint64),
+                ("direct_read_bytes", ctypes.c_uint64), ("direct_write_bytes", ctypes.c_uint64)]
 
 
 class TrainConfigC(ctypes.Structure):

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <filesystem>
 #include <fcntl.h>
+#include <future>
 #include <memory>
 #include <string>
 #include <unistd.h>
@@ -167,6 +168,7 @@ struct PackedLoader {
     bool used[2] = {false, false};
     int half = 0, threads = 1;
     double read_ms = 0.0, load_ms = 0.0;
+    std::uint64_t direct_bytes = 0;
     static constexpr std::uint64_t kHalf = 16ull << 20;
 
     PackedLoader(cudaStream_t s, int reader_threads) : st(s), threads(reader_threads) {
@@ -197,6 +199,10 @@ struct PackedLoader {
         }
         const int fd = ::open(p.c_str(), O_RDONLY);
         if (fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + p.string() + "'");
+        // snapshots not in the page cache are read with O_DIRECT (tailor/io.hpp; TAILOR_IO overrides)
+        const int dfd = want_direct_read(io_mode_from_env(IoMode::Auto), fd, lay.payload_offset(), lay.payload_bytes)
+                            ? open_direct_read(p.string())
+                            : -1;
         try {
             std::size_t fi = 0;
             for (std::uint64_t lo = 0; lo < total; lo += kHalf, half ^= 1) {
@@ -208,7 +214,7 @@ struct PackedLoader {
                 for (std::size_t j = fi; j < where.size() && where[j].second < hi; ++j) {
                     const auto& [e, at] = where[j];
                     const std::uint64_t a = std::max(lo, at), z = std::min(hi, at + e->bytes());
-                    if (a < z) jobs.push_back({fd, buf + (a - lo), z - a, lay.payload_offset() + e->begin + (a - at)});
+                    if (a < z) jobs.push_back({fd, buf + (a - lo), z - a, lay.payload_offset() + e->begin + (a - at), dfd});
                 }
                 const double r0 = clock_ms();
                 run_reads(jobs, threads, p.string());
@@ -220,9 +226,12 @@ struct PackedLoader {
         } catch (...) {
             cudaStreamSynchronize(st);
             ::close(fd);
+            if (dfd >= 0) ::close(dfd);
             throw;
         }
         ::close(fd);
+        if (dfd >= 0) ::close(dfd);
+        if (dfd >= 0) direct_bytes += total;
         load_ms += clock_ms() - t0;
     }
 };
@@ -232,9 +241,23 @@ struct PackedLoader {
 void score_dirs(const std::vector<std::string>& dirs, const std::vector<int>& devices, std::vector<std::vector<double>>& sd,
                 std::vector<std::vector<double>>& sr, std::vector<CheckpointSummary>& sums) {
     if (dirs.size() < 2) fail(ErrorKind::Recipe, "scoring needs at least two snapshots");
-    cuda_check(cudaSetDevice(devices.front()), "cudaSetDevice");
+    // the CUDA context comes up while the sidecars are parsed (a fresh process pays
+    // hundreds of ms for it)
+    auto cuda_ready = std::async(std::launch::async, [&devices] {
+        for (int d : devices) {
+            cuda_check(cudaSetDevice(d), "cudaSetDevice");
+            cuda_check(cudaFree(nullptr), "cuda init");
+        }
+    });
     sums.clear();
-    for (const auto& d : dirs) sums.push_back(read_checkpoint_summary(d));
+    try {
+        for (const auto& d : dirs) sums.push_back(read_checkpoint_summary(d));
+    } catch (...) {
+        cuda_ready.wait();
+        throw;
+    }
+    cuda_ready.get();
+    cuda_check(cudaSetDevice(devices.front()), "cudaSetDevice");
     const ModelSpec& spec = sums.front().spec;
     const int N = sums.front().optim.num_ranks;
     for (const auto& s : sums) {
@@ -364,11 +387,24 @@ MergeOptions merge_options(const tg_merge_options* o) {
     opt.uncached = o->uncached != 0;
     opt.device = o->device;
     opt.verify = o->skip_verify == 0;
+    if (o->io_mode < TG_IO_AUTO || o->io_mode > TG_IO_DIRECT_RW)
+        fail(ErrorKind::Recipe, "tg_merge_options: unknown io_mode " + std::to_string(o->io_mode));
+    opt.io = static_cast<IoMode>(o->io_mode);
     if (o->num_devices > 0) {
         if (!o->devices) fail(ErrorKind::Recipe, "tg_merge_options: num_devices > 0 with a null device list");
         opt.devices.assign(o->devices, o->devices + o->num_devices);
     }
     return opt;
+}
+
+void put_stats(const MergeStats& s, tg_merge_stats* st) {
+    st->shard_files_read = s.shard_files_read;
+    st->weight_files_read = s.weight_files_read;
+    st->wall_ms = s.wall_ms;
+    st->device_ms = s.device_ms;
+    st->bytes_moved = s.bytes_moved;
+    st->direct_read_bytes = s.direct_read_bytes;
+    st->direct_write_bytes = s.direct_write_bytes;
 }
 
 std::vector<int> device_list(const int32_t* devices, int32_t n) {
@@ -406,13 +442,7 @@ int tg_execute_merge(const char* yaml, const char* out_dir, const tg_merge_optio
         const MergePlan plan = resolve_plan(parse_recipe(yaml ? yaml : ""));
         const MergeOptions opt = merge_options(o);
         const MergeStats s = execute_merge(plan, out_dir ? out_dir : "", opt);
-        if (st) {
-            st->shard_files_read = s.shard_files_read;
-            st->weight_files_read = s.weight_files_read;
-            st->wall_ms = s.wall_ms;
-            st->device_ms = s.device_ms;
-            st->bytes_moved = s.bytes_moved;
-        }
+        if (st) put_stats(s, st);
     });
 }
 
@@ -426,13 +456,7 @@ int tg_regroup(const char* src_dir, const char* out_dir, int32_t to_fine, const 
         opt.uncached = false;
         const MergeStats s = execute_regroup(src_dir ? src_dir : "", out_dir ? out_dir : "",
                                              to_fine ? Grouping::Fine : Grouping::Coarse, opt);
-        if (st) {
-            st->shard_files_read = s.shard_files_read;
-            st->weight_files_read = s.weight_files_read;
-            st->wall_ms = s.wall_ms;
-            st->device_ms = s.device_ms;
-            st->bytes_moved = s.bytes_moved;
-        }
+        if (st) put_stats(s, st);
     });
 }
 

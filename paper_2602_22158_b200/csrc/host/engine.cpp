@@ -985,6 +985,15 @@ void load_ranges(const fs::path& path, const std::vector<FileRange>& ranges, Pin
                  std::uint64_t step, cudaStream_t s) {
     const int fd = ::open(path.c_str(), O_RDONLY);
     if (fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + path.string() + "'");
+    // a file not in the page cache (e.g. written with O_DIRECT) is read with O_DIRECT
+    std::uint64_t span_lo = ~0ull, span_hi = 0;
+    for (const auto& r : ranges) {
+        span_lo = std::min(span_lo, r.file_off);
+        span_hi = std::max(span_hi, r.file_off + r.bytes);
+    }
+    const int dfd = span_hi > span_lo && want_direct_read(io_mode_from_env(IoMode::Auto), fd, span_lo, span_hi - span_lo)
+                        ? open_direct_read(path.string())
+                        : -1;
     stage[0].resize(step);
     stage[1].resize(step);
     cudaEvent_t done[2];
@@ -996,6 +1005,7 @@ void load_ranges(const fs::path& path, const std::vector<FileRange>& ranges, Pin
         cudaEventDestroy(done[0]);
         cudaEventDestroy(done[1]);
         ::close(fd);
+        if (dfd >= 0) ::close(dfd);
     };
     try {
         int half = 0;
@@ -1013,7 +1023,7 @@ void load_ranges(const fs::path& path, const std::vector<FileRange>& ranges, Pin
                 const FileRange& r = ranges[ri];
                 const std::uint64_t n = std::min(step - fill, r.bytes - at);
                 if (n > 0) {
-                    jobs.push_back({fd, buf + fill, n, r.file_off + at});
+                    jobs.push_back({fd, buf + fill, n, r.file_off + at, dfd});
                     pieces.push_back({n, &r});
                     starts.push_back(at);
                 }

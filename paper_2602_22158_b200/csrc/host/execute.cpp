@@ -18,6 +18,7 @@
 #include <fcntl.h>
 #include <filesystem>
 #include <functional>
+#include <future>
 #include <map>
 #include <mutex>
 #include <thread>
@@ -51,6 +52,8 @@ void pwrite_all(int fd, const std::uint8_t* src, std::uint64_t n, std::uint64_t 
 }
 
 std::uint64_t align16(std::uint64_t x) { return (x + 15) & ~15ull; }
+std::uint64_t floor_blk(std::uint64_t x) { return x / kDirectAlign * kDirectAlign; }
+std::uint64_t ceil_blk(std::uint64_t x) { return (x + kDirectAlign - 1) / kDirectAlign * kDirectAlign; }
 
 // One lane of the file pipeline: assembles whole output container files, one
 // chunk at a time through kSlots slots: the lane thread preads chunk i while the
@@ -59,12 +62,16 @@ std::uint64_t align16(std::uint64_t x) { return (x + 15) & ~15ull; }
 // a different file: buffered writes to ONE file serialise on its inode lock
 // (tools/write_probe.cpp: 8 threads on one file ~4.7 GB/s, on 8 files 20-30 GB/s
 // on the B200 host), so the parallelism is across files.
+// Direct I/O (IoMode): a source window read with O_DIRECT is staged at a pinned
+// offset congruent to its file offset mod 4 KB, so whole blocks land in place;
+// with O_DIRECT writes the chunk grid follows the output file's 4 KB blocks
+// (chunk 0 carries the tail of the header) and the file is truncated to size.
 class FileAssembler {
   public:
     static constexpr int kSlots = 3;
 
-    FileAssembler(int read_threads, bool uncached, std::uint64_t chunk)
-        : workers_(std::max(1, read_threads)), uncached_(uncached), chunk_(chunk) {
+    FileAssembler(int read_threads, bool uncached, std::uint64_t chunk, IoMode io = IoMode::Buffered)
+        : workers_(std::max(1, read_threads)), uncached_(uncached), chunk_(chunk), io_(io) {
         for (auto& s : stream_) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
         for (int i = 0; i < kSlots; ++i) {
             cuda_check(cudaEventCreate(&ev0_[i]), "event");
@@ -80,35 +87,59 @@ class FileAssembler {
     }
 
     double device_ms = 0.0, read_ms = 0.0, wait_ms = 0.0, write_ms = 0.0;
-    std::uint64_t bytes = 0;
+    std::uint64_t bytes = 0, direct_read_bytes = 0, direct_write_bytes = 0;
     void set_read_threads(int n) { workers_ = std::max(1, n); }
 
     void assemble(const PartitionPlan& pp, const std::vector<fs::path>& window_files, const fs::path& out_path) {
         Fd out(out_path, O_WRONLY | O_CREAT | O_TRUNC);
         if (out.fd < 0) fail(ErrorKind::Storage, "cannot create '" + out_path.string() + "'");
         const std::string prefix = pp.out.prefix();
-        pwrite_all(out.fd, reinterpret_cast<const std::uint8_t*>(prefix.data()), prefix.size(), 0, out_path.string());
         const std::uint64_t base = pp.out.payload_offset();
-        // Payload offsets of each window inside its source file.
+        // Payload offsets of each window inside its source file; which windows read direct.
         std::vector<std::uint64_t> file_off(pp.windows.size());
-        std::vector<std::unique_ptr<Fd>> fds(pp.windows.size());
+        std::vector<std::unique_ptr<Fd>> fds(pp.windows.size()), dfds(pp.windows.size());
+        std::vector<char> direct(pp.windows.size(), 0);
         for (std::size_t w = 0; w < pp.windows.size(); ++w) {
             if (pp.windows[w].container == kZeroContainer) continue; // zero fill: no source file
             file_off[w] = source_payload_offset(window_files[w]) + pp.windows[w].lo;
             if (!uncached_) {
                 fds[w] = std::make_unique<Fd>(window_files[w], O_RDONLY);
                 if (fds[w]->fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + window_files[w].string() + "'");
+                if (io_ != IoMode::Buffered &&
+                    want_direct_read(io_, fds[w]->fd, file_off[w], pp.windows[w].hi - pp.windows[w].lo)) {
+                    dfds[w] = std::make_unique<Fd>(window_files[w], O_RDONLY | O_DIRECT);
+                    direct[w] = dfds[w]->fd >= 0; // the filesystem may refuse O_DIRECT: buffered then
+                }
             }
         }
-        HostMergeChunks plan(pp, chunk_);
+        // O_DIRECT output: a second descriptor on the same file; every write is whole blocks
+        std::unique_ptr<Fd> dout;
+        bool dwrite = io_ == IoMode::DirectRW && pp.dst_hi > pp.dst_lo;
+        if (dwrite) {
+            dout = std::make_unique<Fd>(out_path, O_WRONLY | O_DIRECT);
+            dwrite = dout->fd >= 0;
+        }
+        const std::uint64_t head = dwrite ? base % kDirectAlign : 0; // header bytes that ride in chunk 0
+        HostMergeChunks plan(pp, chunk_, dwrite ? chunk_ - head : chunk_, file_off, direct);
         for (int i = 0; i < kSlots; ++i) {
             // one pinned buffer per slot carries the chunk both ways: the D2H of the
             // gathered chunk lands in it after its H2D has completed (same stream)
-            pin_io_[i].resize(std::max<std::uint64_t>(16, std::max(plan.max_staging, plan.max_out)));
+            pin_io_[i].resize(std::max<std::uint64_t>(16, std::max(plan.max_staging, ceil_blk(plan.max_out + head))));
+            dwrite = dwrite && reinterpret_cast<std::uintptr_t>(pin_io_[i].get()) % kDirectAlign == 0;
             d_in_[i].resize(std::max<std::uint64_t>(16, plan.max_staging));
             d_out_[i].resize(std::max<std::uint64_t>(16, plan.max_out));
             d_segs_[i].resize(std::max<std::size_t>(1, plan.max_segs) * sizeof(dev::GatherSeg));
             pin_segs_[i].resize(std::max<std::size_t>(1, plan.max_segs) * sizeof(dev::GatherSeg));
+        }
+        if (dwrite) { // the header's whole blocks now; its tail goes out with chunk 0
+            const std::uint64_t whole = floor_blk(base);
+            if (whole) {
+                AlignedBuffer hb(whole);
+                std::memcpy(hb.p, prefix.data(), whole);
+                pwrite_all(dout->fd, hb.p, whole, 0, out_path.string());
+            }
+        } else {
+            pwrite_all(out.fd, reinterpret_cast<const std::uint8_t*>(prefix.data()), prefix.size(), 0, out_path.string());
         }
 
         // Writer: takes chunks in order, waits for the slot's stream, pwrites,
@@ -136,7 +167,15 @@ class FileAssembler {
                     const auto& c = plan.chunks[ci];
                     {
                         ScopedAccum acc(write_ms);
-                        pwrite_all(out.fd, pin_io_[slot].get(), c.hi - c.lo, base + c.lo, out_path.string());
+                        if (dwrite) {
+                            const std::uint64_t h = ci == 0 ? head : 0;
+                            if (h) std::memcpy(pin_io_[slot].get(), prefix.data() + (base - head), h);
+                            const std::uint64_t n = ceil_blk(h + c.hi - c.lo);
+                            pwrite_all(dout->fd, pin_io_[slot].get(), n, base + c.lo - h, out_path.string());
+                            direct_write_bytes += n;
+                        } else {
+                            pwrite_all(out.fd, pin_io_[slot].get(), c.hi - c.lo, base + c.lo, out_path.string());
+                        }
                     }
                     std::lock_guard<std::mutex> lk(mu);
                     written = ci + 1;
@@ -157,7 +196,7 @@ class FileAssembler {
                     cv.wait(lk, [&] { return written + kSlots > ci || werr; });
                     if (werr) break;
                 }
-                stage_chunk(plan.chunks[ci], pp, window_files, file_off, fds, slot, out_path);
+                stage_chunk(plan.chunks[ci], pp, window_files, file_off, fds, dfds, slot, ci == 0 ? head : 0, out_path);
                 std::lock_guard<std::mutex> lk(mu);
                 issued = ci + 1;
                 cv.notify_all();
@@ -175,6 +214,8 @@ class FileAssembler {
         if (rerr) std::rethrow_exception(rerr);
         if (werr) std::rethrow_exception(werr);
         if (plan.chunks.empty() && pp.out.payload_bytes != 0) fail(ErrorKind::Consistency, "empty merge plan");
+        if (dwrite && ::ftruncate(out.fd, static_cast<off_t>(base + pp.out.payload_bytes)) != 0) // drop the last block's tail
+            fail(ErrorKind::Storage, "cannot truncate '" + out_path.string() + "'");
     }
 
   private:
@@ -184,8 +225,8 @@ class FileAssembler {
     // pread; uncached mode re-opens the source file per read, as the reference
     // reloads a shard per group copy), then queues H2D -> K2 -> D2H on the slot.
     void stage_chunk(const ChunkPlan& c, const PartitionPlan& pp, const std::vector<fs::path>& window_files,
-                     const std::vector<std::uint64_t>& file_off, const std::vector<std::unique_ptr<Fd>>& fds, int slot,
-                     const fs::path& out_path) {
+                     const std::vector<std::uint64_t>& file_off, const std::vector<std::unique_ptr<Fd>>& fds,
+                     const std::vector<std::unique_ptr<Fd>>& dfds, int slot, std::uint64_t d2h_shift, const fs::path& out_path) {
         std::vector<std::unique_ptr<Fd>> opened;
         std::vector<ReadJob> jobs;
         for (const auto& rd : c.reads) {
@@ -201,7 +242,9 @@ class FileAssembler {
             } else {
                 fd = fds[rd.w]->fd;
             }
-            jobs.push_back({fd, pin_io_[slot].get() + rd.at, rd.b - rd.a, file_off[rd.w] + rd.a});
+            const int dfd = !uncached_ && dfds[rd.w] && dfds[rd.w]->fd >= 0 ? dfds[rd.w]->fd : -1;
+            if (dfd >= 0) direct_read_bytes += rd.b - rd.a;
+            jobs.push_back({fd, pin_io_[slot].get() + rd.at, rd.b - rd.a, file_off[rd.w] + rd.a, dfd});
         }
         {
             ScopedAccum acc(read_ms);
@@ -221,7 +264,8 @@ class FileAssembler {
                                       d_out_[slot].get(), c.hi - c.lo, dev::kGatherAuto, c.bulk_ok, s),
                    "gather");
         cuda_check(cudaEventRecord(ev1_[slot], s), "event");
-        cuda_check(cudaMemcpyAsync(pin_io_[slot].get(), d_out_[slot].get(), c.hi - c.lo, cudaMemcpyDeviceToHost, s), "D2H");
+        cuda_check(cudaMemcpyAsync(pin_io_[slot].get() + d2h_shift, d_out_[slot].get(), c.hi - c.lo, cudaMemcpyDeviceToHost, s),
+                   "D2H");
         bytes += c.hi - c.lo;
     }
 
@@ -239,13 +283,18 @@ class FileAssembler {
         std::vector<ChunkPlan> chunks;
         std::uint64_t max_staging = 0, max_out = 0;
         std::size_t max_segs = 0;
-        HostMergeChunks(const PartitionPlan& pp, std::uint64_t chunk) {
+        // first: the size of chunk 0 (chunk, or less so that later chunks start on
+        // 4 KB blocks of the output file); direct[w]: window w is read with O_DIRECT,
+        // so its reads are staged congruent to file_off[w] + src mod 4 KB
+        HostMergeChunks(const PartitionPlan& pp, std::uint64_t chunk, std::uint64_t first,
+                        const std::vector<std::uint64_t>& file_off, const std::vector<char>& direct) {
             const std::uint64_t total = pp.dst_hi - pp.dst_lo;
+            first = std::max<std::uint64_t>(1, first);
             std::size_t si = 0;
-            for (std::uint64_t lo = 0; lo < total; lo += chunk) {
+            for (std::uint64_t lo = 0; lo < total; lo = lo == 0 ? first : lo + chunk) {
                 ChunkPlan c;
                 c.lo = lo;
-                c.hi = std::min(total, lo + chunk);
+                c.hi = std::min(total, lo == 0 ? first : lo + chunk);
                 struct P {
                     std::uint32_t w;
                     std::uint64_t src, dst, n;
@@ -268,10 +317,21 @@ class FileAssembler {
                 std::uint64_t at = 0;
                 for (std::size_t i : order) {
                     const P& p = ps[i];
-                    if (!c.reads.empty() && c.reads.back().w == p.w && c.reads.back().b == p.src) {
+                    const bool dw = direct[p.w] != 0;
+                    // contiguous (buffered) or within one block of the previous read
+                    // (direct: the gap is read along; its block is read anyway)
+                    if (!c.reads.empty() && c.reads.back().w == p.w && p.src >= c.reads.back().b &&
+                        p.src - c.reads.back().b <= (dw ? kDirectAlign : 0)) {
                         at_of[i] = c.reads.back().at + (p.src - c.reads.back().a);
-                        c.reads.back().b += p.n;
+                        c.reads.back().b = p.src + p.n;
                         at = c.reads.back().at + (c.reads.back().b - c.reads.back().a);
+                        continue;
+                    }
+                    if (dw) { // whole blocks straight into place: congruent to the file offset mod 4 KB
+                        at = ceil_blk(at) + (file_off[p.w] + p.src) % kDirectAlign;
+                        c.reads.push_back({p.w, p.src, p.src + p.n, at});
+                        at_of[i] = at;
+                        at += p.n;
                         continue;
                     }
                     // keep src/dst congruent mod 16 so the vector path applies
@@ -280,7 +340,7 @@ class FileAssembler {
                     at_of[i] = at;
                     at += p.n;
                 }
-                c.staging = align16(at);
+                c.staging = ceil_blk(at);
                 std::uint64_t expect = c.lo;
                 for (std::size_t i = 0; i < ps.size(); ++i) {
                     c.segs.push_back({reinterpret_cast<const std::uint8_t*>(at_of[i]), ps[i].dst - c.lo, ps[i].n});
@@ -308,6 +368,7 @@ class FileAssembler {
     int workers_;
     bool uncached_;
     std::uint64_t chunk_;
+    IoMode io_;
     cudaStream_t stream_[kSlots]{};
     cudaEvent_t ev0_[kSlots]{}, ev1_[kSlots]{};
     PinnedBuffer pin_io_[kSlots], pin_segs_[kSlots]; // pinned: async copies never sync the stream
@@ -334,7 +395,7 @@ struct OutputJob {
 
 struct AssembleTotals {
     double device_ms = 0.0, read_ms = 0.0, wait_ms = 0.0, write_ms = 0.0;
-    std::uint64_t bytes = 0;
+    std::uint64_t bytes = 0, direct_read_bytes = 0, direct_write_bytes = 0;
 };
 
 // Runs the output files over up to 16 lanes (weights first, then largest first,
@@ -347,7 +408,8 @@ struct AssembleTotals {
 // Lane li runs on devices[li % devices.size()] (the reference's loader pool,
 // R/src/merge.cpp:156-205, spread over GPUs; which lane writes a file never changes its bytes).
 AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool uncached, const std::vector<int>& devices,
-                                const std::function<void(int)>& on_done = {}, const std::function<void()>& on_error = {}) {
+                                IoMode io, const std::function<void(int)>& on_done = {},
+                                const std::function<void()>& on_error = {}) {
     // the weights file first (a lane verifying a rank file waits for it: with fewer lanes
     // than files, taking it last could block every lane), then largest first
     std::stable_sort(jobs.begin(), jobs.end(), [](const OutputJob& a, const OutputJob& b) {
@@ -368,7 +430,7 @@ AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool u
     const auto lane = [&](int li) {
         try {
             cuda_check(cudaSetDevice(devices[static_cast<std::size_t>(li) % devices.size()]), "cudaSetDevice");
-            FileAssembler fa(readers, uncached, chunk);
+            FileAssembler fa(readers, uncached, chunk, io);
             for (std::size_t j = next.fetch_add(1); j < jobs.size(); j = next.fetch_add(1)) {
                 {
                     std::lock_guard<std::mutex> lk(mu);
@@ -381,7 +443,8 @@ AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool u
                 fa.assemble(*jobs[j].plan, jobs[j].window_files, jobs[j].out);
                 if (on_done) on_done(jobs[j].tag);
             }
-            part[static_cast<std::size_t>(li)] = {fa.device_ms, fa.read_ms, fa.wait_ms, fa.write_ms, fa.bytes};
+            part[static_cast<std::size_t>(li)] = {fa.device_ms, fa.read_ms,  fa.wait_ms,           fa.write_ms,
+                                                  fa.bytes,     fa.direct_read_bytes, fa.direct_write_bytes};
         } catch (...) {
             bool first = false;
             {
@@ -409,12 +472,16 @@ AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool u
         tot.wait_ms += x.wait_ms;
         tot.write_ms += x.write_ms;
         tot.bytes += x.bytes;
+        tot.direct_read_bytes += x.direct_read_bytes;
+        tot.direct_write_bytes += x.direct_write_bytes;
     }
     trace_count("assemble.lanes", lanes);
     trace_count("assemble.devices", static_cast<long long>(devices.size()));
     trace_value("assemble.read (sum over lanes)", tot.read_ms);
     trace_value("assemble.wait (sum over lanes)", tot.wait_ms);
     trace_value("assemble.write (sum over lanes)", tot.write_ms);
+    trace_count("assemble.direct_read_bytes", static_cast<double>(tot.direct_read_bytes));
+    trace_count("assemble.direct_write_bytes", static_cast<double>(tot.direct_write_bytes));
     return tot;
 }
 
@@ -589,14 +656,21 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
     std::error_code ec;
     if (fs::exists(out_dir) && !fs::is_empty(out_dir, ec))
         fail(ErrorKind::Storage, "refusing to write into non-empty directory '" + out_dir.string() + "'");
-    {
-        PhaseTimer pt("merge.cuda_init");
+    // CUDA context creation (hundreds of ms in a fresh process) overlaps the header
+    // parsing and planning below; joined before the first device allocation.
+    auto cuda_ready = std::async(std::launch::async, [&devices] {
+        PhaseTimer pt("merge.cuda_init (overlapped)");
         for (int d : devices) {
             cuda_check(cudaSetDevice(d), "cudaSetDevice");
             cuda_check(cudaFree(nullptr), "cuda init");
         }
-        cuda_check(cudaSetDevice(devices.front()), "cudaSetDevice");
-    }
+    });
+    struct JoinOnExit { // a validation error below must not leave the init running past the call
+        std::future<void>& f;
+        ~JoinOnExit() {
+            if (f.valid()) f.wait();
+        }
+    } join_on_exit{cuda_ready};
 
     auto phase = std::make_unique<PhaseTimer>("merge.headers+plan");
     std::map<std::string, CheckpointSummary> sums;
@@ -631,6 +705,8 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
     const SaveManifest manifest = merged_manifest(plan, sum_of);
 
     // All inputs validated; write.
+    cuda_ready.get(); // rethrows a device error
+    cuda_check(cudaSetDevice(devices.front()), "cudaSetDevice");
     fs::create_directories(out_dir / "optim", ec);
     if (ec) fail(ErrorKind::Storage, "cannot create '" + out_dir.string() + "': " + ec.message());
     const int workers = options.workers > 0 ? options.workers : std::max(plan.num_ranks, io_threads());
@@ -656,7 +732,10 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
     }
 
     LaneVerifier lv(out_dir, &wplan, splans, workers, options.verify, devices);
-    const AssembleTotals fa = assemble_outputs(std::move(jobs), workers, options.uncached, devices, lv.hook(), lv.abort_hook());
+    const IoMode io = io_mode_from_env(options.io);
+    trace_count(("merge.io_mode " + std::string(io_mode_name(io))).c_str(), static_cast<double>(io));
+    const AssembleTotals fa =
+        assemble_outputs(std::move(jobs), workers, options.uncached, devices, io, lv.hook(), lv.abort_hook());
     alloc_stats().trace("merge.assemble allocations");
     phase = std::make_unique<PhaseTimer>("merge.verify");
     lv.finish();
@@ -665,6 +744,8 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
 
     stats.device_ms = fa.device_ms;
     stats.bytes_moved = fa.bytes;
+    stats.direct_read_bytes = fa.direct_read_bytes;
+    stats.direct_write_bytes = fa.direct_write_bytes;
     stats.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return stats;
 }
@@ -805,7 +886,8 @@ MergeStats execute_regroup(const fs::path& src, const fs::path& out_dir, Groupin
     write_text_file(ckpt_file(CkptFile::TrainerState, out_dir), sidecar_text(s.trainer));
     write_text_file(ckpt_file(CkptFile::Manifest, out_dir), sidecar_text(s.manifest));
     LaneVerifier lv(out_dir, &wp, plans, workers, options.verify, devices);
-    const AssembleTotals fa = assemble_outputs(std::move(jobs), workers, false, devices, lv.hook(), lv.abort_hook());
+    const AssembleTotals fa =
+        assemble_outputs(std::move(jobs), workers, false, devices, io_mode_from_env(options.io), lv.hook(), lv.abort_hook());
     lv.finish();
     stats.device_ms = fa.device_ms;
     stats.bytes_moved = fa.bytes;

@@ -91,19 +91,24 @@ const char* io_mode_name(IoMode m) {
 
 double page_cache_fraction(int fd, std::uint64_t off, std::uint64_t len) {
     if (len == 0) return 1.0;
+    // sampled: up to 256 pages spread over the range (mincore of a whole 15 GB
+    // window would walk ~4 M page-cache entries)
     const std::uint64_t pg = static_cast<std::uint64_t>(::sysconf(_SC_PAGESIZE));
     const std::uint64_t a = off / pg * pg, b = off + len;
-    void* m = ::mmap(nullptr, b - a, PROT_READ, MAP_SHARED, fd, static_cast<off_t>(a));
+    const std::uint64_t pages = (b - a + pg - 1) / pg;
+    const std::uint64_t probes = std::min<std::uint64_t>(pages, 256);
+    void* m = ::mmap(nullptr, b - a, PROT_READ, MAP_SHARED, fd, static_cast<off_t>(a)); // lazy: no page touched
     if (m == MAP_FAILED) return 1.0; // unknown: keep the page cache
-    std::vector<unsigned char> v((b - a + pg - 1) / pg);
-    double frac = 1.0;
-    if (::mincore(m, b - a, v.data()) == 0) {
-        std::size_t in = 0;
-        for (unsigned char c : v) in += c & 1u;
-        frac = static_cast<double>(in) / static_cast<double>(v.size());
+    std::size_t in = 0, seen = 0;
+    for (std::uint64_t i = 0; i < probes; ++i) {
+        unsigned char v = 0;
+        if (::mincore(static_cast<std::uint8_t*>(m) + (pages * i / probes) * pg, pg, &v) == 0) {
+            in += v & 1u;
+            ++seen;
+        }
     }
     ::munmap(m, b - a);
-    return frac;
+    return seen ? static_cast<double>(in) / static_cast<double>(seen) : 1.0;
 }
 
 bool want_direct_read(IoMode mode, int fd, std::uint64_t off, std::uint64_t len) {

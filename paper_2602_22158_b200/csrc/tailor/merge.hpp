@@ -6,6 +6,8 @@
 // kernel; there is no host copy path.
 #pragma once
 
+#include "tailor/io.hpp"
+
 #include <cstdint>
 #include <filesystem>
 #include <functional>
@@ -70,6 +72,9 @@ struct MergeOptions {
     // Lanes (one output file at a time each) spread round-robin over these devices;
     // empty = {device}. Output bytes do not depend on the devices or the lane count.
     std::vector<int> devices;
+    // Source reads / output writes through the page cache or O_DIRECT (tailor/io.hpp);
+    // the bytes written do not depend on it.
+    IoMode io = IoMode::Auto;
 };
 inline std::vector<int> lane_devices(const MergeOptions& o) {
     return o.devices.empty() ? std::vector<int>{o.device} : o.devices;
@@ -81,6 +86,8 @@ struct MergeStats {
     double wall_ms = 0.0;
     double device_ms = 0.0;        // gather kernels, CUDA events
     std::uint64_t bytes_moved = 0; // composite payload bytes
+    std::uint64_t direct_read_bytes = 0;  // source bytes read with O_DIRECT
+    std::uint64_t direct_write_bytes = 0; // output bytes written with O_DIRECT (whole blocks)
 };
 
 MergeStats execute_merge(const MergePlan& plan, const std::filesystem::path& out_dir, const MergeOptions& options = {});

@@ -4,6 +4,7 @@
 // update-magnitude `select` / `score` subcommands.
 //
 //   tailor merge  --recipe r.yaml --out DIR [--workers W] [--uncached] [--json] [--device D | --devices 0,1,..] [--no-verify]
+//                [--io auto|buffered|direct|direct-rw]
 //   tailor plan   --run RUN --failure-step S --out r.yaml
 //   tailor select --snapshots A,B,... [--rho 0.5] --out r.yaml [--device D | --devices 0,1,..] [--json]
 //   tailor score  --snapshots A,B,... [--device D | --devices 0,1,..]
@@ -102,6 +103,15 @@ int cmd_merge(const Args& a) {
     opt.skip_verify = a.flags.count("no-verify") ? 1 : 0;
     opt.devices = devs.data();
     opt.num_devices = static_cast<int32_t>(devs.size());
+    if (a.kv.count("io")) { // --io auto|buffered|direct|direct-rw (source reads / output writes)
+        const std::string m = a.kv.at("io");
+        opt.io_mode = m == "buffered" ? TG_IO_BUFFERED : m == "direct" ? TG_IO_DIRECT : m == "direct-rw" ? TG_IO_DIRECT_RW
+                      : m == "auto"   ? TG_IO_AUTO : -1;
+        if (opt.io_mode < 0) {
+            std::cerr << "error: unknown --io mode '" << m << "' (auto, buffered, direct, direct-rw)\n";
+            return 1;
+        }
+    }
     tg_merge_stats st{};
     const int rc = tg_execute_merge(yaml.c_str(), a.kv.at("out").c_str(), &opt, &st);
     if (rc != TG_OK) return report(rc);

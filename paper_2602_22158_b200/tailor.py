@@ -105,14 +105,18 @@ class MergeOptions:
     device: int = 0
     verify: bool = True
     devices: Optional[Sequence[int]] = None
+    io_mode: str = "auto"  # auto | buffered | direct | direct-rw (tailor/io.hpp; TAILOR_IO overrides)
 
     def to_c(self):
         devs = list(self.devices or [])
         arr = (ctypes.c_int32 * max(1, len(devs)))(*devs)
         c = MergeOptionsC(self.workers, 1 if self.uncached else 0, self.device, 0 if self.verify else 1,
-                          ctypes.cast(arr, ctypes.POINTER(ctypes.c_int32)), len(devs), 0)
+                          ctypes.cast(arr, ctypes.POINTER(ctypes.c_int32)), len(devs), IO_MODES[self.io_mode])
         c._keep = arr  # the array must outlive the call
         return c
+
+
+IO_MODES = {"auto": 0, "buffered": 1, "direct": 2, "direct-rw": 3}
 
 
 @dataclasses.dataclass
@@ -124,6 +128,13 @@ class MergeStats:
     wall_ms: float
     device_ms: float
     bytes_moved: int
+    direct_read_bytes: int = 0
+    direct_write_bytes: int = 0
+
+    @classmethod
+    def from_c(cls, st) -> "MergeStats":
+        return cls(st.shard_files_read, st.weight_files_read, st.wall_ms, st.device_ms, st.bytes_moved,
+                   st.direct_read_bytes, st.direct_write_bytes)
 
 
 def _b(s: str) -> bytes:
@@ -152,7 +163,7 @@ def execute_merge(recipe, out_dir: str, options: Optional[MergeOptions] = None) 
     copt = o.to_c()
     st = MergeStatsC()
     check(lib().tg_execute_merge(_yaml_of(recipe), _b(str(out_dir)), ctypes.byref(copt), ctypes.byref(st)))
-    return MergeStats(st.shard_files_read, st.weight_files_read, st.wall_ms, st.device_ms, st.bytes_moved)
+    return MergeStats.from_c(st)
 
 
 def recipe_from_manifests(run_dir: str, failure_step: int) -> MergeRecipe:
@@ -166,7 +177,7 @@ def regroup(src_dir: str, out_dir: str, to_fine: bool = True, options: Optional[
     st = MergeStatsC()
     check(lib().tg_regroup(_b(str(src_dir)), _b(str(out_dir)), 1 if to_fine else 0, ctypes.byref(copt),
                            ctypes.byref(st)))
-    return MergeStats(st.shard_files_read, st.weight_files_read, st.wall_ms, st.device_ms, st.bytes_moved)
+    return MergeStats.from_c(st)
 
 
 STRATEGIES = {"full": 0, "parity": 1, "filter": 2, "magnitude": 3}

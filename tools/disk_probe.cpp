@@ -4,7 +4,8 @@
 //   disk_probe <dir> [gib_per_file=2] [files=8] [threads_per_file=4]
 //
 // Writes `files` files of `gib_per_file` GiB in <dir> and prints one JSON line:
-//   write_buffered_gbs  pwrite into the page cache (+ fsync, so the number includes writeback)
+//   write_cached_gbs    pwrite into the page cache (no fsync)
+//   write_buffered_gbs  the same + fsync (includes the writeback to the device)
 //   write_direct_gbs    O_DIRECT pwrite (null if the filesystem refuses O_DIRECT)
 //   read_direct_gbs     O_DIRECT pread (the device's read bandwidth)
 //   read_cold_gbs       buffered pread after POSIX_FADV_DONTNEED (cold page cache)
@@ -104,9 +105,9 @@ int main(int argc, char** argv) {
         return 1;
     }
     double t0 = now();
-    double wb = run(fds, bytes, tpf, pw);
+    const double wc = run(fds, bytes, tpf, pw); // into the page cache
     for (int f : fds) ::fsync(f);
-    if (wb > 0) wb = static_cast<double>(bytes) * fds.size() / (now() - t0) / 1e9;
+    double wb = wc > 0 ? static_cast<double>(bytes) * fds.size() / (now() - t0) / 1e9 : -1.0; // incl. writeback
     close_all(fds);
 
     // O_DIRECT write (overwrites in place)
@@ -142,10 +143,10 @@ int main(int argc, char** argv) {
     struct statvfs sv {};
     statvfs(dir.c_str(), &sv);
     std::printf("{\"dir\": \"%s\", \"files\": %d, \"gib_per_file\": %.2f, \"threads_per_file\": %d, \"free_gb\": %.1f, "
-                "\"write_buffered_gbs\": %s, \"write_direct_gbs\": %s, \"read_direct_gbs\": %s, \"read_cold_gbs\": %s, "
+                "\"write_cached_gbs\": %s, \"write_buffered_gbs\": %s, \"write_direct_gbs\": %s, \"read_direct_gbs\": %s, \"read_cold_gbs\": %s, "
                 "\"read_warm_gbs\": %s, \"o_direct\": %s}\n",
                 dir.c_str(), nfiles, static_cast<double>(bytes) / (1ull << 30), tpf,
-                static_cast<double>(sv.f_bavail) * sv.f_frsize / 1e9, num(wb).c_str(), num(wd).c_str(), num(rd).c_str(),
+                static_cast<double>(sv.f_bavail) * sv.f_frsize / 1e9, num(wc).c_str(), num(wb).c_str(), num(wd).c_str(), num(rd).c_str(),
                 num(rc).c_str(), num(rw).c_str(), direct_ok ? "true" : "false");
     for (const auto& p : paths) ::unlink(p.c_str());
     return 0;
