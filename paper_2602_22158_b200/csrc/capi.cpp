@@ -294,7 +294,9 @@ void score_dirs(const std::vector<std::string>& dirs, const std::vector<int>& de
                                     std::to_string(budget) + " B available");
     const int nd = static_cast<int>(devices.size());
     const int per_dev = std::clamp<int>(static_cast<int>(std::min<std::uint64_t>(budget / per_lane, 8)), 1, 8);
-    const int lanes = std::clamp<int>(per_dev * nd, 1, N);
+    int lanes = std::clamp<int>(per_dev * nd, 1, N);
+    if (const char* v = std::getenv("TAILOR_SCORE_LANES"); v && std::atoi(v) > 0) // diagnostics (racecheck: one lane)
+        lanes = std::min(lanes, std::atoi(v));
     const int readers = std::max(1, io_threads() / lanes);
     trace_count(all_resident ? "score.lanes" : "score.lanes (rolling windows)", lanes);
     trace_count("score.slots", slots);

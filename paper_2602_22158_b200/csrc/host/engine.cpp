@@ -612,6 +612,8 @@ ScorePlan::ScorePlan(const ModelLayout& model, int num_ranks, std::vector<std::v
     for (int s0 = 0; s0 < K_ - 1; s0 += dev::kMaxSnapshots - 1)
         windows_.push_back({s0, std::min(K_ - 1, s0 + dev::kMaxSnapshots - 1)});
     if (const char* v = std::getenv("TAILOR_SCORE_VARIANT"); v && *v) variant_ = std::atoi(v);
+    if (const char* v = std::getenv("TAILOR_SCORE_STATIC"); v && *v == '1') dynamic_ = false; // diagnostics
+    d_counter_.resize(16);
     tile_elems = std::max<std::uint32_t>(4, tile_elems & ~3u);
     fields_ = score_fields(model, num_ranks);
     for (const auto& o : offs_) {
@@ -660,7 +662,7 @@ void ScorePlan::run(const std::uint8_t* const* snap_bases, double* d_out, cudaSt
         cuda_check(dev::launch_score_partials(d_tiles_.get<dev::ScoreTile>(), static_cast<std::uint32_t>(tiles_.size()),
                                               d_bases_.get<const float*>() + static_cast<std::size_t>(w0) * fields_.size(),
                                               static_cast<std::uint32_t>(fields_.size()), Kw, vec, d_partials_.get<double>(), s,
-                                              variant_),
+                                              variant_, dynamic_ ? d_counter_.get<unsigned int>() : nullptr),
                    "score partials");
         cuda_check(dev::launch_score_combine(d_partials_.get<double>(), d_begin_.get<std::uint32_t>(), M_, Kw,
                                              d_out + static_cast<std::size_t>(w0) * M_ * 2, s),

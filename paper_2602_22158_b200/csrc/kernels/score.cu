@@ -220,11 +220,27 @@ __device__ __forceinline__ void accumulate4(double (&acc)[2 * (K - 1)], int p, c
     acc[2 * p + 1] = fma(aw, aw, fma(az, az, fma(ay, ay, fma(ax, ax, acc[2 * p + 1]))));
 }
 
+// Which tile and chunk a ring stage holds (written by the producer before the
+// stage's bulk copies; published to the consumers by the full barrier's arrive).
+struct StageDesc {
+    std::uint32_t tile;  // ~0u: end of the stream
+    std::uint32_t start; // first element of the chunk within the tile
+    std::uint32_t n;     // elements in the chunk
+    std::uint32_t last;  // last chunk of the tile: the consumers reduce and write its partial
+};
+constexpr std::uint32_t kNoTile = ~0u;
+
+// Tiles are claimed dynamically (counter != nullptr: atomicAdd on a per-launch counter
+// zeroed on the stream before the launch) — SMs do not stream at equal rates (ncu, cfg2
+// K=2 with the static split: SM active 89.6% of elapsed, the rest a tail of CTAs still
+// working) — or statically (b, b+G, ...) without a counter. Either way tile t's partial
+// lands at out[t]: the results do not depend on which CTA ran which tile.
 template <int K>
 __global__ void __launch_bounds__(kStagedThreads, 1) score_staged_kernel(const ScoreTile* __restrict__ tiles,
                                                                           std::uint32_t ntiles,
                                                                           const float* const* __restrict__ field_base,
-                                                                          std::uint32_t nfields, double* __restrict__ out) {
+                                                                          std::uint32_t nfields, double* __restrict__ out,
+                                                                          unsigned int* __restrict__ counter) {
     using namespace tma;
     constexpr int S = staged_stages<K>();
     constexpr int V = 2 * (K - 1);
@@ -234,6 +250,7 @@ __global__ void __launch_bounds__(kStagedThreads, 1) score_staged_kernel(const S
     std::uint64_t* full = reinterpret_cast<std::uint64_t*>(ring + S * K * kChunkElems);
     std::uint64_t* empty = full + S;
     __shared__ double red[kWarps][V];
+    __shared__ StageDesc desc[S];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
         for (int st = 0; st < S; ++st) {
@@ -243,97 +260,120 @@ __global__ void __launch_bounds__(kStagedThreads, 1) score_staged_kernel(const S
         fence_barrier_init();
     }
     __syncthreads();
-    const std::uint32_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    const auto tile_at = [&](std::uint32_t i) { return blockIdx.x + i * gridDim.x; };
 
     if (warp == kWarps) { // producer
         if (lane == 0) {
-            std::uint32_t item = 0;
-            for (std::uint32_t i = 0; i < mine; ++i) {
-                const ScoreTile t = tiles[tile_at(i)];
+            std::uint32_t item = 0, claimed = 0;
+            const auto claim = [&]() -> std::uint32_t {
+                return counter ? atomicAdd(counter, 1u) : blockIdx.x + (claimed++) * gridDim.x;
+            };
+            const auto next_stage = [&]() { // wait until the stage of `item` is free
+                const int stage = static_cast<int>(item % S);
+                if (item >= static_cast<std::uint32_t>(S)) mbar_wait_parity(&empty[stage], ((item / S) - 1) & 1u);
+                return stage;
+            };
+            std::uint32_t t = claim();
+            while (t < ntiles) {
+                const ScoreTile tl = tiles[t];
+                const std::uint32_t t_next = claim(); // in flight while this tile's chunks are issued
                 const float* base[K];
 #pragma unroll
-                for (int k = 0; k < K; ++k) base[k] = field_base[k * nfields + t.field] + t.elem_start;
-                for (std::uint32_t start = 0; start < t.count; start += kChunkElems, ++item) {
-                    const int stage = static_cast<int>(item % S);
-                    if (item >= static_cast<std::uint32_t>(S)) mbar_wait_parity(&empty[stage], ((item / S) - 1) & 1u);
-                    const std::uint32_t n = min(static_cast<std::uint32_t>(kChunkElems), t.count - start);
+                for (int k = 0; k < K; ++k) base[k] = field_base[k * nfields + tl.field] + tl.elem_start;
+                for (std::uint32_t start = 0;; start += kChunkElems, ++item) {
+                    const int stage = next_stage();
+                    const std::uint32_t n = tl.count > start ? min(static_cast<std::uint32_t>(kChunkElems), tl.count - start) : 0u;
+                    const bool last = start + kChunkElems >= tl.count;
+                    desc[stage] = {t, start, n, last ? 1u : 0u};
                     const std::uint32_t nb = (n & ~3u) * 4u;
-                    mbar_arrive_expect_tx(&full[stage], nb * K);
-                    if (nb)
+                    if (nb) {
+                        mbar_arrive_expect_tx(&full[stage], nb * K); // releases desc[stage] too
 #pragma unroll
                         for (int k = 0; k < K; ++k)
                             bulk_load(ring + (stage * K + k) * kChunkElems, base[k] + start, nb, &full[stage]);
+                    } else {
+                        mbar_arrive(&full[stage]);
+                    }
+                    if (last) {
+                        ++item;
+                        break;
+                    }
                 }
+                t = t_next;
             }
+            const int stage = next_stage(); // end of stream
+            desc[stage] = {kNoTile, 0u, 0u, 1u};
+            mbar_arrive(&full[stage]);
         }
         return;
     }
 
-    std::uint32_t item = 0;
-    for (std::uint32_t i = 0; i < mine; ++i) {
-        const ScoreTile t = tiles[tile_at(i)];
-        double acc[V];
+    double acc[V];
 #pragma unroll
-        for (int v = 0; v < V; ++v) acc[v] = 0.0;
-        for (std::uint32_t start = 0; start < t.count; start += kChunkElems, ++item) {
-            const int stage = static_cast<int>(item % S);
-            mbar_wait_parity(&full[stage], (item / S) & 1u);
-            const std::uint32_t n = min(static_cast<std::uint32_t>(kChunkElems), t.count - start);
-            const std::uint32_t n4 = n & ~3u;
+    for (int v = 0; v < V; ++v) acc[v] = 0.0;
+    for (std::uint32_t item = 0;; ++item) {
+        const int stage = static_cast<int>(item % S);
+        mbar_wait_parity(&full[stage], (item / S) & 1u);
+        const StageDesc d = desc[stage];
+        if (d.tile == kNoTile) break;
+        const std::uint32_t n4 = d.n & ~3u;
 #pragma unroll
-            for (int rr = 0; rr < R; ++rr) {
-                const std::uint32_t e = (static_cast<std::uint32_t>(rr) * kScoreThreads + static_cast<std::uint32_t>(tid)) * 4u;
-                if (e < n4) {
-                    const float* row = ring + stage * K * kChunkElems + e;
-                    float4 prev = *reinterpret_cast<const float4*>(row);
+        for (int rr = 0; rr < R; ++rr) {
+            const std::uint32_t e = (static_cast<std::uint32_t>(rr) * kScoreThreads + static_cast<std::uint32_t>(tid)) * 4u;
+            if (e < n4) {
+                const float* row = ring + stage * K * kChunkElems + e;
+                float4 prev = *reinterpret_cast<const float4*>(row);
 #pragma unroll
-                    for (int k = 1; k < K; ++k) {
-                        const float4 cur = *reinterpret_cast<const float4*>(row + k * kChunkElems);
-                        accumulate4<K>(acc, k - 1, prev, cur);
-                        prev = cur;
-                    }
+                for (int k = 1; k < K; ++k) {
+                    const float4 cur = *reinterpret_cast<const float4*>(row + k * kChunkElems);
+                    accumulate4<K>(acc, k - 1, prev, cur);
+                    prev = cur;
                 }
             }
-            __syncwarp();
-            if (lane == 0) { // this warp is done with the stage: order its generic-proxy reads
-                fence_proxy_async_smem(); // before the producer's next async-proxy (TMA) writes
-                mbar_arrive(&empty[stage]);
+        }
+        __syncwarp();
+        if (lane == 0) { // this warp is done with the stage: order its generic-proxy reads
+            fence_proxy_async_smem(); // before the producer's next async-proxy (TMA) writes
+            mbar_arrive(&empty[stage]);
+        }
+        if (static_cast<std::uint32_t>(tid) < d.n - n4) { // ragged tail straight from global
+            const ScoreTile tl = tiles[d.tile];
+            float x[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) x[k] = __ldg(field_base[k * nfields + tl.field] + tl.elem_start + d.start + n4 + tid);
+            accumulate<K>(acc, x);
+        }
+        if (d.last) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const double sv = warp_sum(acc[v]);
+                if (lane == 0) red[warp][v] = sv;
+                acc[v] = 0.0;
             }
-            if (static_cast<std::uint32_t>(tid) < n - n4) { // ragged tail straight from global
-                float x[K];
+            named_bar_sync(1, kScoreThreads);
+            if (tid < V) {
+                double sv = 0.0;
 #pragma unroll
-                for (int k = 0; k < K; ++k) x[k] = __ldg(field_base[k * nfields + t.field] + t.elem_start + start + n4 + tid);
-                accumulate<K>(acc, x);
+                for (int w = 0; w < kWarps; ++w) sv += red[w][tid];
+                out[static_cast<std::uint64_t>(d.tile) * V + tid] = sv;
             }
+            named_bar_sync(1, kScoreThreads);
         }
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-            const double sv = warp_sum(acc[v]);
-            if (lane == 0) red[warp][v] = sv;
-        }
-        named_bar_sync(1, kScoreThreads);
-        if (tid < V) {
-            double sv = 0.0;
-#pragma unroll
-            for (int w = 0; w < kWarps; ++w) sv += red[w][tid];
-            out[static_cast<std::uint64_t>(tile_at(i)) * V + tid] = sv;
-        }
-        named_bar_sync(1, kScoreThreads);
     }
 }
 
 template <int K>
 cudaError_t launch_staged(const ScoreTile* d_tiles, std::uint32_t ntiles, const float* const* d_field_base,
-                          std::uint32_t nfields, double* d_out, cudaStream_t stream) {
+                          std::uint32_t nfields, double* d_out, unsigned int* d_counter, cudaStream_t stream) {
     static std::atomic<std::uint64_t> attr{0};
     constexpr std::size_t smem = staged_smem_bytes<K>();
     if (const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(score_staged_kernel<K>), smem, attr);
         e != cudaSuccess)
         return e;
+    if (d_counter)
+        if (const cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(unsigned int), stream); e != cudaSuccess) return e;
     const unsigned grid = static_cast<unsigned>(
         std::min<std::uint64_t>(ntiles, static_cast<std::uint64_t>(sm_count()) * staged_ctas<K>()));
-    score_staged_kernel<K><<<grid, kStagedThreads, smem, stream>>>(d_tiles, ntiles, d_field_base, nfields, d_out);
+    score_staged_kernel<K><<<grid, kStagedThreads, smem, stream>>>(d_tiles, ntiles, d_field_base, nfields, d_out, d_counter);
     return cudaGetLastError();
 }
 
@@ -363,13 +403,13 @@ cudaError_t launch_k(const ScoreTile* d_tiles, std::uint32_t ntiles, const float
 
 cudaError_t launch_score_partials(const ScoreTile* d_tiles, std::uint32_t ntiles, const float* const* d_field_base,
                                   std::uint32_t nfields, int K, bool vec_ok, double* d_out, cudaStream_t stream,
-                                  int variant) {
+                                  int variant, unsigned int* d_counter) {
     if (ntiles == 0) return cudaSuccess;
     const bool staged = vec_ok && (variant == kScoreStaged || (variant == kScoreAuto && K >= kStagedMinK));
     switch (K) {
 #define TG_K(k)                                                                                           \
     case k:                                                                                               \
-        return staged ? launch_staged<k>(d_tiles, ntiles, d_field_base, nfields, d_out, stream)           \
+        return staged ? launch_staged<k>(d_tiles, ntiles, d_field_base, nfields, d_out, d_counter, stream) \
                       : launch_k<k>(d_tiles, ntiles, d_field_base, nfields, vec_ok, d_out, stream, variant);
         TG_K(2) TG_K(3) TG_K(4) TG_K(5) TG_K(6) TG_K(7) TG_K(8) TG_K(9) TG_K(10) TG_K(11) TG_K(12) TG_K(13) TG_K(14)
             TG_K(15) TG_K(16)

@@ -72,9 +72,11 @@ constexpr int kNarrowMinK = 1 << 20;
 // -> auto picks it whenever the bases are 16-B aligned. (Its very first version, one
 // CTA-wide barrier per chunk, was barrier-bound: 0.88 / 0.61.)
 constexpr int kStagedMinK = 2;
+// d_counter (optional, one word): the staged kernel claims tiles dynamically through it
+// (zeroed on `stream` first); null = static tile split. Results do not depend on it.
 cudaError_t launch_score_partials(const ScoreTile* d_tiles, std::uint32_t ntiles, const float* const* d_field_base,
                                   std::uint32_t nfields, int K, bool vec_ok, double* d_tile_partials, cudaStream_t stream,
-                                  int variant = kScoreAuto);
+                                  int variant = kScoreAuto, unsigned int* d_counter = nullptr);
 // out[p][m][0|1] = fixed-order sum over module m's tiles [tile_begin[m], tile_begin[m+1]).
 cudaError_t launch_score_combine(const double* d_tile_partials, const std::uint32_t* d_module_tile_begin, int M, int K,
                                  double* d_out, cudaStream_t stream);

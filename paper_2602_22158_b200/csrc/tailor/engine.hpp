@@ -188,6 +188,8 @@ class ScorePlan {
     std::vector<dev::ScoreTile> tiles_;
     std::vector<std::uint32_t> begin_;
     DeviceBuffer d_tiles_, d_begin_, d_bases_, d_partials_;
+    DeviceBuffer d_counter_; // K3's dynamic tile counter (zeroed before each launch)
+    bool dynamic_ = true;    // TAILOR_SCORE_STATIC=1: static tile split (diagnostics)
     PinnedBuffer h_bases_;
     std::vector<const std::uint8_t*> bound_;
     std::uint64_t bytes_ = 0;

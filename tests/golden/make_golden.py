@@ -8,7 +8,8 @@ Fixtures (small, content-addressed):
                        set of recipes over reference-written synthetic sources
   score_golden.json  — reference-side scorer restatement (a13) + selection (a14) +
                        recipe over reference-written snapshots
-  plan_golden.json   — reference resolve_plan / recipe_from_manifests results
+(resolve_plan / recipe_from_manifests are pinned by live comparisons with the reference
+binary in tests/test_host.py and tests/test_gpu_parity.py, not by a fixture.)
 Paths inside fixtures are made relative (<SRC>/...) so they are location-free.
 """
 import hashlib

@@ -610,6 +610,40 @@ def test_scorer_variants_agree(K):
             assert torch.allclose(outs[0], o_, rtol=1e-12, atol=0)
 
 
+@pytest.mark.parametrize("K", [2, 3, 4, 9, 16])
+def test_staged_scorer_dynamic_tiles_are_bitwise_the_static_split(K, monkeypatch):
+    """The TMA-ring scorer claims tiles dynamically (atomic counter); each tile's partial
+    still lands in its own slot, so the result must be bitwise the static split's
+    (TAILOR_SCORE_STATIC=1), repeat after repeat. Big enough for many tiles per CTA and
+    ragged field tails (not multiples of 4 or of the chunk)."""
+    need_gpu()
+    spec = t.ModelSpec(3, 256, 690, 1001, False, 17)
+    N = 2
+    fam = t.SynthFamily(spec, N, K)
+    M = fam.num_modules
+    bufs = [dev(fam.packed_master_bytes(0)) for _ in range(K)]
+    fam.gen_masters(0, 1, K, [b.data_ptr() for b in bufs])
+
+    def score(static):
+        if static:
+            monkeypatch.setenv("TAILOR_SCORE_STATIC", "1")
+        else:
+            monkeypatch.delenv("TAILOR_SCORE_STATIC", raising=False)
+        sc = t.Scorer(fam, 0, 1, K, packed=True)
+        sc.set_variant(2)
+        outs = []
+        for _ in range(3):
+            out = torch.zeros((K - 1) * M * 2, dtype=torch.float64, device="cuda")
+            sc.run([b.data_ptr() for b in bufs], out.data_ptr())
+            outs.append(out)
+        torch.cuda.synchronize()
+        return outs
+
+    ref = score(True)[0]
+    for o_ in score(False) + score(True):
+        assert torch.equal(ref, o_)
+
+
 @pytest.mark.parametrize("N", [1, 2, 4, 8])
 def test_execute_merge_lane_count_independent_and_sources_untouched(tmp_path, N):
     """Acceptance c9/c10 + R/tests/test_merge.cpp:370-385 shape: the composite does not

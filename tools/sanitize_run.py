@@ -75,9 +75,21 @@ def run(spec, N, K, variants=(0, 1, 2)):
     step.result()
     torch.cuda.synchronize()
     if os.environ.get("TAILOR_SANITIZE_TOOL") == "racecheck":
-        # racecheck looks for shared-memory races inside kernels; the file paths below launch
-        # the same kernels from many host threads (lanes), which racecheck tracks badly
-        # ("failure to track a kernel launch", then hours) — they run under memcheck/synccheck
+        # racecheck looks for shared-memory races inside kernels; with many host threads
+        # (lanes) launching kernels it tracks badly ("failure to track a kernel launch",
+        # then hours), so under racecheck the file paths run with ONE lane: select (one
+        # scorer lane), merge and regroup with workers=1 (assembly + pipelined re-verify
+        # on the calling thread), both io modes
+        os.environ["TAILOR_SCORE_LANES"] = "1"
+        with tempfile.TemporaryDirectory() as d:
+            for k in range(1, K + 1):
+                fam.write_dir(k, f"{d}/checkpoint-{k * 100}")
+            dirs = [f"{d}/checkpoint-{k * 100}" for k in range(1, K + 1)]
+            rec2, _, _ = t.select_recipe(dirs, 0.5)
+            t.execute_merge(rec2, f"{d}/sel1", t.MergeOptions(workers=1))
+            t.execute_merge(rec2, f"{d}/sel1d", t.MergeOptions(workers=1, io_mode="direct-rw"))
+            t.regroup(f"{d}/sel1", f"{d}/coarse", to_fine=False, options=t.MergeOptions(workers=1))
+            t.verify_checkpoint(f"{d}/coarse")
         return
     with tempfile.TemporaryDirectory() as d:
         for k in range(1, K + 1):
@@ -91,6 +103,7 @@ def run(spec, N, K, variants=(0, 1, 2)):
         rec2, _, _ = t.select_recipe(dirs, 0.5)
         t.execute_merge(rec2, f"{d}/sel8", t.MergeOptions(workers=8))
         t.execute_merge(rec2, f"{d}/sel1", t.MergeOptions(workers=1))
+        t.execute_merge(rec2, f"{d}/sel8d", t.MergeOptions(workers=8, io_mode="direct-rw"))
         t.regroup(f"{d}/sel8", f"{d}/coarse", to_fine=False)
         t.regroup(f"{d}/coarse", f"{d}/fine", to_fine=True)
 
