@@ -73,7 +73,11 @@ def full(path):
                          "dram_pct_peak": val(r, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
                          "registers": val(r, "launch__registers_per_thread"),
                          "warps_active_pct": val(r, "sm__warps_active.avg.pct_of_peak_sustained_active"),
-                         "grid": val(r, "launch__grid_size")})
+                         "grid": val(r, "launch__grid_size"),
+                         # SM active / elapsed: below 1 = SMs idle for part of the kernel (tail, imbalance)
+                         "sm_active_frac": (lambda a_, e_: a_ / e_ if a_ and e_ else None)(
+                             val(r, "sm__cycles_active.avg") or val(r, "TPC.TriageCompute.sm__cycles_active.avg"),
+                             val(r, "sm__cycles_elapsed.avg") or val(r, "gpc__cycles_elapsed.max"))})
     out = {}
     for k, v in ks.items():
         big = max(v, key=lambda x: x["dram_read_bytes"] + x["dram_write_bytes"])
