@@ -79,7 +79,8 @@ SAMPLE_EXTRAPOLATION = {"cfg3": "~35 min for the 123.7 GB job at the sampled rat
 MODEL_NAMES = {"cfg1": "tiny Llama-style (reference ModelSpec)", "cfg2": "Qwen2.5-7B-shaped (reference ModelSpec)",
                "cfg3": "Llama-3.1-8B-shaped (reference ModelSpec)", "cfg4": "Llama-3.1-8B-shaped (reference ModelSpec)",
                "cfg5": "Llama-3-70B-shaped (reference ModelSpec)", "tiny8": "tiny Llama-style (reference ModelSpec)"}
-SCORE_VARIANTS = {0: "auto", 1: "register", 2: "staged", 3: "register-128b", 4: "register-64b"}
+SCORE_VARIANTS = {0: "auto", 1: "register", 2: "staged", 3: "register-128b", 4: "register-64b", 5: "staged-half-rows",
+                  6: "staged-2-ctas"}
 
 
 def shared_gpu() -> bool:
@@ -1008,6 +1009,7 @@ def scorer_arm(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     L, h, f, v, tied, N, K, rho, desc = WORKLOADS[args.workload]
+    K = args.snapshots or K  # --snapshots: the same sweep over K snapshots (scorer geometry studies)
     fam = t.SynthFamily(t.ModelSpec(L, h, f, v, tied, 42), N, K, 100)
     M, r = fam.num_modules, rank
     stream = torch.cuda.current_stream(dev)
@@ -1496,7 +1498,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS) + ["files", "train"], default="cfg3")
     ap.add_argument("--variant", type=int, default=0, help="gather: 0 auto, 1 LSU, 2 TMA bulk 3x64K, 3-6 other rings")
-    ap.add_argument("--score-variant", type=int, default=0, help="scorer: 0 auto, 1 register, 2 TMA-staged")
+    ap.add_argument("--score-variant", type=int, default=0, help="scorer: 0 auto, 1 register, 2 TMA-staged, 5 staged half rows, 6 staged 2 CTAs/SM")
+    ap.add_argument("--snapshots", type=int, default=0, help="cfg4 only: sweep over this many snapshots instead of 16")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2, help="timed e2e steps (each is the whole job)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

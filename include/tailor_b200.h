@@ -247,7 +247,8 @@ tg_scorer* tg_scorer_create(const tg_layout* l, int32_t rank, int32_t k0, int32_
 void tg_scorer_destroy(tg_scorer* s);
 uint64_t tg_scorer_bytes(const tg_scorer* s);
 /* 0 auto (TMA-bulk ring when the bases are 16-B aligned, else register loads),
- * 1 register-staged 128-bit loads, 2 TMA-bulk shared-memory ring. */
+ * 1 register-staged 128-bit loads, 2 TMA-bulk shared-memory ring, 3/4 register loads
+ * 128/64-bit, 5/6 the ring with half the rows per stage / two CTAs per SM (K <= 8). */
 int tg_scorer_set_variant(tg_scorer* s, int32_t variant);
 /* d_out: [K-1][M][2] FP64 partial sums for this rank. */
 int tg_scorer_run(tg_scorer* s, const uint8_t* const* bases, double* d_out, void* stream);

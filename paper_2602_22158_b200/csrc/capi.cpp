@@ -807,8 +807,9 @@ void tg_scorer_destroy(tg_scorer* s) { delete s; }
 
 int tg_scorer_set_variant(tg_scorer* s, int32_t variant) {
     return guard([&] {
-        if (variant < 0 || variant > 4)
-            fail(ErrorKind::Geometry, "scorer variant: 0 auto, 1 register, 2 staged, 3 register-128b, 4 register-64b");
+        if (variant < 0 || variant > 6)
+            fail(ErrorKind::Geometry, "scorer variant: 0 auto, 1 register, 2 staged, 3 register-128b, 4 register-64b, "
+                                          "5 staged half rows, 6 staged 2 CTAs/SM");
         s->plan->set_variant(variant);
     });
 }

@@ -181,34 +181,39 @@ __global__ void score_combine_kernel(const double* __restrict__ partials, const 
 // order inside a tile differs from the register kernel, so the two variants
 // agree to ~1e-15, not bitwise.
 constexpr int kStagedSmem = 192 * 1024;
-// CTAs per SM: small K runs two (each with half the ring) for more independent streams
-template <int K>
+// Ring geometry: G = 0 default, 1 half the rows per stage (smaller bulk copies, more
+// stages; the round-1 default for K >= 4), 2 two CTAs per SM (each half the ring).
+// CTAs per SM: small K runs two (each with half the ring) for more independent streams.
+template <int K, int G = 0>
 __host__ __device__ constexpr int staged_ctas() {
-    return K < 4 ? 2 : 1;
+    return G == 2 ? 2 : (K < 4 ? 2 : 1);
 }
 constexpr int kStagedThreads = kScoreThreads + 32; // 8 consumer warps + 1 producer warp
 
-// float4 per consumer thread per snapshot row in one stage: small K gets wider
-// stages (>= 16 KB), so the single producer lane issues few enough of them.
-template <int K>
+// float4 per consumer thread per snapshot row in one stage: 8 KB per snapshot row for
+// 3 <= K <= 8 (K=4: 32 KB stages x 6 = 192 KB in flight per SM; with 4 KB rows, 8 x 16 KB
+// stages, B200 measured 0.90 of the read stream vs 1.00), 16 KB for K = 2, 4 KB for K >= 9
+// (the stage must fit twice in shared memory).
+template <int K, int G = 0>
 __host__ __device__ constexpr int staged_rows() {
-    return K >= 4 ? 1 : (K == 3 ? 2 : 4);
+    constexpr int r = K >= 9 ? 1 : (K >= 3 ? 2 : 4);
+    return G == 1 ? (r > 1 ? r / 2 : 1) : r;
 }
-template <int K>
+template <int K, int G = 0>
 __host__ __device__ constexpr int chunk_elems() {
-    return 4 * kScoreThreads * staged_rows<K>();
+    return 4 * kScoreThreads * staged_rows<K, G>();
 }
 
-template <int K>
+template <int K, int G = 0>
 __host__ __device__ constexpr int staged_stages() {
-    constexpr int per = K * chunk_elems<K>() * 4;
-    constexpr int s = kStagedSmem / staged_ctas<K>() / per;
+    constexpr int per = K * chunk_elems<K, G>() * 4;
+    constexpr int s = kStagedSmem / staged_ctas<K, G>() / per;
     return s < 2 ? 2 : (s > 8 ? 8 : s);
 }
 
-template <int K>
+template <int K, int G = 0>
 __host__ __device__ constexpr std::size_t staged_smem_bytes() {
-    return static_cast<std::size_t>(staged_stages<K>()) * K * chunk_elems<K>() * 4 + 16 * staged_stages<K>();
+    return static_cast<std::size_t>(staged_stages<K, G>()) * K * chunk_elems<K, G>() * 4 + 16 * staged_stages<K, G>();
 }
 
 template <int K>
@@ -235,17 +240,17 @@ constexpr std::uint32_t kNoTile = ~0u;
 // K=2 with the static split: SM active 89.6% of elapsed, the rest a tail of CTAs still
 // working) — or statically (b, b+G, ...) without a counter. Either way tile t's partial
 // lands at out[t]: the results do not depend on which CTA ran which tile.
-template <int K>
+template <int K, int G>
 __global__ void __launch_bounds__(kStagedThreads, 1) score_staged_kernel(const ScoreTile* __restrict__ tiles,
                                                                           std::uint32_t ntiles,
                                                                           const float* const* __restrict__ field_base,
                                                                           std::uint32_t nfields, double* __restrict__ out,
                                                                           unsigned int* __restrict__ counter) {
     using namespace tma;
-    constexpr int S = staged_stages<K>();
+    constexpr int S = staged_stages<K, G>();
     constexpr int V = 2 * (K - 1);
-    constexpr int kChunkElems = chunk_elems<K>();
-    constexpr int R = staged_rows<K>();
+    constexpr int kChunkElems = chunk_elems<K, G>();
+    constexpr int R = staged_rows<K, G>();
     extern __shared__ __align__(128) float ring[];
     std::uint64_t* full = reinterpret_cast<std::uint64_t*>(ring + S * K * kChunkElems);
     std::uint64_t* empty = full + S;
@@ -361,20 +366,34 @@ __global__ void __launch_bounds__(kStagedThreads, 1) score_staged_kernel(const S
     }
 }
 
-template <int K>
-cudaError_t launch_staged(const ScoreTile* d_tiles, std::uint32_t ntiles, const float* const* d_field_base,
-                          std::uint32_t nfields, double* d_out, unsigned int* d_counter, cudaStream_t stream) {
+template <int K, int G>
+cudaError_t launch_staged_g(const ScoreTile* d_tiles, std::uint32_t ntiles, const float* const* d_field_base,
+                            std::uint32_t nfields, double* d_out, unsigned int* d_counter, cudaStream_t stream) {
     static std::atomic<std::uint64_t> attr{0};
-    constexpr std::size_t smem = staged_smem_bytes<K>();
-    if (const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(score_staged_kernel<K>), smem, attr);
+    constexpr std::size_t smem = staged_smem_bytes<K, G>();
+    if (const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(score_staged_kernel<K, G>), smem, attr);
         e != cudaSuccess)
         return e;
     if (d_counter)
         if (const cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(unsigned int), stream); e != cudaSuccess) return e;
     const unsigned grid = static_cast<unsigned>(
-        std::min<std::uint64_t>(ntiles, static_cast<std::uint64_t>(sm_count()) * staged_ctas<K>()));
-    score_staged_kernel<K><<<grid, kStagedThreads, smem, stream>>>(d_tiles, ntiles, d_field_base, nfields, d_out, d_counter);
+        std::min<std::uint64_t>(ntiles, static_cast<std::uint64_t>(sm_count()) * staged_ctas<K, G>()));
+    score_staged_kernel<K, G><<<grid, kStagedThreads, smem, stream>>>(d_tiles, ntiles, d_field_base, nfields, d_out,
+                                                                      d_counter);
     return cudaGetLastError();
+}
+
+// geometry: 0 default; kScoreStagedWide / kScoreStaged2Cta (K <= 8; larger K keep the default)
+template <int K>
+cudaError_t launch_staged(const ScoreTile* d_tiles, std::uint32_t ntiles, const float* const* d_field_base,
+                          std::uint32_t nfields, double* d_out, unsigned int* d_counter, cudaStream_t stream, int variant) {
+    if constexpr (K <= 8) {
+        if (variant == kScoreStagedWide)
+            return launch_staged_g<K, 1>(d_tiles, ntiles, d_field_base, nfields, d_out, d_counter, stream);
+        if (variant == kScoreStaged2Cta)
+            return launch_staged_g<K, 2>(d_tiles, ntiles, d_field_base, nfields, d_out, d_counter, stream);
+    }
+    return launch_staged_g<K, 0>(d_tiles, ntiles, d_field_base, nfields, d_out, d_counter, stream);
 }
 
 template <int K, int VW>
@@ -405,11 +424,12 @@ cudaError_t launch_score_partials(const ScoreTile* d_tiles, std::uint32_t ntiles
                                   std::uint32_t nfields, int K, bool vec_ok, double* d_out, cudaStream_t stream,
                                   int variant, unsigned int* d_counter) {
     if (ntiles == 0) return cudaSuccess;
-    const bool staged = vec_ok && (variant == kScoreStaged || (variant == kScoreAuto && K >= kStagedMinK));
+    const bool staged = vec_ok && (variant == kScoreStaged || variant == kScoreStagedWide || variant == kScoreStaged2Cta ||
+                                   (variant == kScoreAuto && K >= kStagedMinK));
     switch (K) {
 #define TG_K(k)                                                                                           \
     case k:                                                                                               \
-        return staged ? launch_staged<k>(d_tiles, ntiles, d_field_base, nfields, d_out, d_counter, stream) \
+        return staged ? launch_staged<k>(d_tiles, ntiles, d_field_base, nfields, d_out, d_counter, stream, variant) \
                       : launch_k<k>(d_tiles, ntiles, d_field_base, nfields, vec_ok, d_out, stream, variant);
         TG_K(2) TG_K(3) TG_K(4) TG_K(5) TG_K(6) TG_K(7) TG_K(8) TG_K(9) TG_K(10) TG_K(11) TG_K(12) TG_K(13) TG_K(14)
             TG_K(15) TG_K(16)

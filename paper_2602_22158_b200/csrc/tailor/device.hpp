@@ -60,7 +60,15 @@ static_assert(sizeof(ScoreTile) == 24, "ScoreTile is part of the C ABI");
 // Register variants: 3 forces 128-bit loads, 4 forces 64-bit loads. Measured
 // at K=16: 128-bit 0.938, 64-bit 0.675 (spills at the 2-CTA register cap), so
 // auto always uses 128-bit loads.
-enum ScoreVariant : int { kScoreAuto = 0, kScoreRegister = 1, kScoreStaged = 2, kScoreWide = 3, kScoreNarrow = 4 };
+enum ScoreVariant : int {
+    kScoreAuto = 0,
+    kScoreRegister = 1,
+    kScoreStaged = 2,
+    kScoreWide = 3,
+    kScoreNarrow = 4,
+    kScoreStagedWide = 5, // staged ring, half the rows per stage (K <= 8; the round-1 geometry for K >= 4)
+    kScoreStaged2Cta = 6  // staged ring, two CTAs per SM (K <= 8)
+};
 constexpr int kNarrowMinK = 1 << 20;
 // Staged = warp-specialised TMA ring (producer warp + 8 consumer warps, full/empty
 // mbarriers). Measured on B200 (bench events, fraction of the 6543 GB/s copy peak):
