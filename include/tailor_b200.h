@@ -187,7 +187,8 @@ int tg_parse_config(const char* config_json, tg_model_spec* spec);
 int tg_layer_map(const tg_model_spec* spec, int32_t num_ranks, char* json_out, size_t cap, size_t* needed);
 
 /* ---- device primitives (caller-owned buffers) ---------------------------------- */
-/* variant: 0 auto, 1 LSU vector path, 2 TMA bulk path (requires bulk_ok). */
+/* variant: 0 auto, 1 LSU vector path, 2 TMA bulk path (requires bulk_ok). The raw
+ * primitive splits tiles statically (no counter), so concurrent launches are safe. */
 int tg_gather(const tg_gather_seg* d_segs, uint32_t nseg, uint8_t* d_dst, uint64_t dst_bytes, int32_t variant,
               int32_t bulk_ok, void* stream);
 /* Measurement only: a read-only HBM stream over a 16-B aligned device buffer (the
@@ -270,6 +271,9 @@ int tg_mplan_segment(const tg_mplan* p, uint32_t i, uint32_t* window, uint64_t* 
 int tg_mplan_prefix(const tg_mplan* p, char* out, size_t cap, size_t* needed); /* 8-B length + header */
 int tg_mplan_bind(tg_mplan* p, const uint8_t* const* window_ptrs);
 int32_t tg_mplan_bulk_ok(const tg_mplan* p);
+/* The bulk gather claims its tiles dynamically through a counter the plan owns, so runs
+ * of one plan must be stream-ordered (use one plan per concurrent stream); variant 7
+ * forces the static tile split. */
 int tg_mplan_run(tg_mplan* p, uint8_t* d_dst, int32_t variant, void* stream);
 /* Shard pipeline: host windows -> H2D (needed bytes only) -> K2 -> D2H into h_dst.
  * Fields in `resident_fields` (bit0 exp_avg, bit1 exp_avg_sq, bit2 master) are read
@@ -301,7 +305,9 @@ tg_dstep* tg_dstep_create(const tg_layout* l, int32_t rank, int32_t unit, int32_
 void tg_dstep_destroy(tg_dstep* s);
 int tg_dstep_range(const tg_dstep* s, uint64_t* shard_bytes, uint64_t* weights_lo, uint64_t* weights_hi);
 int tg_dstep_bind(tg_dstep* s, const uint8_t* const* shard_bases, const uint8_t* const* weights_window_bases);
-/* phases: bitmask 1 = select + plan (K9), 2 = gather shard, 4 = gather weights (7 = all). */
+/* phases: bitmask 1 = select + plan (K9), 2 = gather shard, 4 = gather weights (7 = all).
+ * Each gather owns a dynamic tile counter in the step: runs of one step that include the
+ * same gather phase must be stream-ordered. */
 int tg_dstep_run(tg_dstep* s, const double* d_rank_partials, int32_t nranks, uint8_t* d_out_shard, uint8_t* d_out_weights,
                  int32_t variant, int32_t phases, void* stream);
 /* Synchronous reads of the last run's selection: source_of[M] (0-based snapshot), scores[(K-1)*M]. */

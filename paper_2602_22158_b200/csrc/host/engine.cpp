@@ -693,11 +693,16 @@ void DeviceMerge::bind(const std::vector<const std::uint8_t*>& window_ptrs) {
     }
     bulk_ok_ = ok && expect == plan_.dst_hi;
     d_segs_.upload(segs.data(), segs.size() * sizeof(dev::GatherSeg));
+    if (!counter_.size()) { // plans are built without a device; the counter comes with the first bind
+        const unsigned int zero[2] = {0, 0};
+        counter_.upload(zero, sizeof(zero));
+    }
 }
 
 void DeviceMerge::run(std::uint8_t* d_dst, int variant, cudaStream_t s) {
     const bool ok = bulk_ok_ && reinterpret_cast<std::uintptr_t>(d_dst) % 16 == 0;
-    cuda_check(dev::launch_gather(d_segs_.get<dev::GatherSeg>(), nseg_, d_dst, bytes(), variant, ok, s), "gather");
+    cuda_check(dev::launch_gather(d_segs_.get<dev::GatherSeg>(), nseg_, d_dst, bytes(), variant, ok, s, counter_.get<unsigned int>()),
+               "gather");
 }
 
 // ---- host-staged merge (shard pipeline) ------------------------------------------
@@ -919,6 +924,8 @@ DeviceSelectStep::DeviceSelectStep(const SnapshotSet& fam, int rank, int unit, i
     w_segs_.resize(std::max<std::size_t>(1, we.size()) * sizeof(dev::GatherSeg));
     source_.resize(static_cast<std::size_t>(M_) * sizeof(int));
     scores_.resize(static_cast<std::size_t>(M_) * (K_ - 1) * sizeof(double));
+    const unsigned int zero[4] = {0, 0, 0, 0};
+    counters_.upload(zero, sizeof(zero));
 }
 
 void DeviceSelectStep::bind(const std::uint8_t* const* shard_bases, const std::uint8_t* const* wwin_bases) {
@@ -943,10 +950,12 @@ void DeviceSelectStep::run(const double* d_parts, int nranks, std::uint8_t* d_ou
     const bool ok_s = bulk_ && reinterpret_cast<std::uintptr_t>(d_out_shard) % 16 == 0;
     const bool ok_w = bulk_ && reinterpret_cast<std::uintptr_t>(d_out_w) % 16 == 0;
     if (phases & kPhaseShard)
-        cuda_check(dev::launch_gather(shard_segs_.get<dev::GatherSeg>(), n_shard_, d_out_shard, shard_bytes_, variant, ok_s, s),
+        cuda_check(dev::launch_gather(shard_segs_.get<dev::GatherSeg>(), n_shard_, d_out_shard, shard_bytes_, variant, ok_s, s,
+                                      counters_.get<unsigned int>()),
                    "gather shard");
     if (phases & kPhaseWeights)
-        cuda_check(dev::launch_gather(w_segs_.get<dev::GatherSeg>(), n_w_, d_out_w, whi_ - wlo_, variant, ok_w, s),
+        cuda_check(dev::launch_gather(w_segs_.get<dev::GatherSeg>(), n_w_, d_out_w, whi_ - wlo_, variant, ok_w, s,
+                                      counters_.get<unsigned int>() + 2),
                    "gather weights");
 }
 

@@ -129,9 +129,17 @@ __global__ void __launch_bounds__(kLsuThreads) gather_lsu_kernel(const GatherSeg
 // ---- TMA bulk path -----------------------------------------------------------
 using namespace tma;
 
+// Tile assignment: static (counter == nullptr: CTA b copies tiles b, b+G, ...) or
+// dynamic (claimed one at a time from counter[0] with atomicAdd, the next claim in
+// flight while the current tile streams, so faster SMs take more tiles and no SM
+// idles at the tail). Dynamic launches leave the counter as they found it (zero):
+// the last CTA to finish (counter[1] == grid - 1) resets both words, so launches
+// that share a counter must be stream-ordered (each plan owns its counter). The
+// bytes placed never depend on the assignment.
 template <int STAGES, std::uint32_t STAGE>
 __global__ void __launch_bounds__(32) gather_bulk_kernel(const GatherSeg* __restrict__ segs, std::uint32_t nseg,
-                                                          std::uint8_t* __restrict__ dst, std::uint64_t dst_bytes) {
+                                                          std::uint8_t* __restrict__ dst, std::uint64_t dst_bytes,
+                                                          unsigned int* __restrict__ counter) {
     extern __shared__ __align__(128) std::uint8_t smem[];
     std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + STAGES * STAGE);
     if (threadIdx.x != 0) return; // one thread drives the copy engine
@@ -139,12 +147,14 @@ __global__ void __launch_bounds__(32) gather_bulk_kernel(const GatherSeg* __rest
     fence_barrier_init();
 
     const std::uint64_t ntiles = (dst_bytes + STAGE - 1) / STAGE;
-    const std::uint64_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    std::uint64_t claimed = 0; // static: tiles handed out to this CTA so far
+    const auto claim = [&]() -> std::uint64_t {
+        return counter ? static_cast<std::uint64_t>(atomicAdd(counter, 1u)) : blockIdx.x + (claimed++) * gridDim.x;
+    };
+    std::uint64_t tile_of[STAGES];
 
-    const auto tile_lo = [&](std::uint64_t i) { return (blockIdx.x + i * gridDim.x) * static_cast<std::uint64_t>(STAGE); };
-    const auto issue_load = [&](std::uint64_t i) {
-        const int stage = static_cast<int>(i % STAGES);
-        const std::uint64_t lo = tile_lo(i);
+    const auto issue_load = [&](std::uint64_t tile, int stage) {
+        const std::uint64_t lo = tile * STAGE;
         const std::uint64_t hi = min(lo + STAGE, dst_bytes);
         std::uint8_t* buf = smem + stage * STAGE;
         mbar_arrive_expect_tx(&bars[stage], static_cast<std::uint32_t>(hi - lo));
@@ -159,27 +169,42 @@ __global__ void __launch_bounds__(32) gather_bulk_kernel(const GatherSeg* __rest
         }
     };
 
-    const std::uint64_t prologue = mine < STAGES - 1 ? mine : static_cast<std::uint64_t>(STAGES - 1);
-    for (std::uint64_t i = 0; i < prologue; ++i) issue_load(i);
-    for (std::uint64_t i = 0; i < mine; ++i) {
+    std::uint64_t next = claim(); // the claim after the tiles already issued (in flight)
+    std::uint64_t issued = 0;
+    for (; issued < STAGES - 1 && next < ntiles; ++issued) {
+        tile_of[issued] = next;
+        issue_load(next, static_cast<int>(issued));
+        next = claim();
+    }
+    for (std::uint64_t i = 0; i < issued; ++i) {
         const int stage = static_cast<int>(i % STAGES);
         mbar_wait_parity(&bars[stage], static_cast<std::uint32_t>((i / STAGES) & 1));
-        const std::uint64_t lo = tile_lo(i);
+        const std::uint64_t lo = tile_of[stage] * STAGE;
         const std::uint64_t hi = min(lo + STAGE, dst_bytes);
         bulk_store(dst + lo, smem + stage * STAGE, static_cast<std::uint32_t>(hi - lo));
         bulk_commit();
-        const std::uint64_t next = i + STAGES - 1; // lands in tile i-1's stage
-        if (next < mine) {
+        if (next < ntiles) { // lands in tile i-1's stage
+            const int ns = static_cast<int>(issued % STAGES);
             if (i >= 1) bulk_wait_read_1(); // store of tile i-1 has finished reading smem
-            issue_load(next);
+            tile_of[ns] = next;
+            issue_load(next, ns);
+            ++issued;
+            next = claim();
         }
     }
     bulk_wait_all();
+    if (counter) {
+        __threadfence();
+        if (atomicAdd(counter + 1, 1u) == gridDim.x - 1) { // every other CTA has made its last claim
+            counter[0] = 0;
+            counter[1] = 0;
+        }
+    }
 }
 
 template <int STAGES, std::uint32_t STAGE>
 cudaError_t launch_bulk(const GatherSeg* d_segs, std::uint32_t nseg, std::uint8_t* d_dst, std::uint64_t dst_bytes,
-                        int ctas_per_sm, cudaStream_t stream) {
+                        int ctas_per_sm, unsigned int* d_counter, cudaStream_t stream) {
     static std::atomic<std::uint64_t> attr{0};
     const std::size_t smem = STAGES * STAGE + STAGES * sizeof(std::uint64_t);
     if (const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gather_bulk_kernel<STAGES, STAGE>), smem, attr);
@@ -187,7 +212,7 @@ cudaError_t launch_bulk(const GatherSeg* d_segs, std::uint32_t nseg, std::uint8_
         return e;
     const std::uint64_t tiles = (dst_bytes + STAGE - 1) / STAGE;
     const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(tiles, static_cast<std::uint64_t>(sm_count()) * ctas_per_sm));
-    gather_bulk_kernel<STAGES, STAGE><<<grid, 32, smem, stream>>>(d_segs, nseg, d_dst, dst_bytes);
+    gather_bulk_kernel<STAGES, STAGE><<<grid, 32, smem, stream>>>(d_segs, nseg, d_dst, dst_bytes, d_counter);
     return cudaGetLastError();
 }
 
@@ -256,17 +281,21 @@ cudaError_t ensure_smem_attr(const void* fn, std::size_t smem, std::atomic<std::
 }
 
 cudaError_t launch_gather(const GatherSeg* d_segs, std::uint32_t nseg, std::uint8_t* d_dst, std::uint64_t dst_bytes,
-                          int variant, bool bulk_ok, cudaStream_t stream) {
+                          int variant, bool bulk_ok, cudaStream_t stream, unsigned int* d_counter) {
     if (dst_bytes == 0 || nseg == 0) return cudaSuccess;
+    if (variant == kGatherBulkStatic) {
+        variant = kGatherBulk;
+        d_counter = nullptr;
+    }
     const int sms = sm_count();
     const bool bulk = variant >= kGatherBulk || (variant == kGatherAuto && bulk_ok);
     if (bulk && bulk_ok) {
         switch (variant) { // ring shapes for experiments; auto/2 = 3 x 64 KB, one CTA per SM
-            case kGatherBulk6x32: return launch_bulk<6, 32 * 1024>(d_segs, nseg, d_dst, dst_bytes, 1, stream);
-            case kGatherBulk2Cta: return launch_bulk<3, 32 * 1024>(d_segs, nseg, d_dst, dst_bytes, 2, stream);
-            case kGatherBulk4x48: return launch_bulk<4, 48 * 1024>(d_segs, nseg, d_dst, dst_bytes, 1, stream);
-            case kGatherBulk8x24: return launch_bulk<8, 24 * 1024>(d_segs, nseg, d_dst, dst_bytes, 1, stream);
-            default: return launch_bulk<kBulkStages, kBulkStage>(d_segs, nseg, d_dst, dst_bytes, 1, stream);
+            case kGatherBulk6x32: return launch_bulk<6, 32 * 1024>(d_segs, nseg, d_dst, dst_bytes, 1, d_counter, stream);
+            case kGatherBulk2Cta: return launch_bulk<3, 32 * 1024>(d_segs, nseg, d_dst, dst_bytes, 2, d_counter, stream);
+            case kGatherBulk4x48: return launch_bulk<4, 48 * 1024>(d_segs, nseg, d_dst, dst_bytes, 1, d_counter, stream);
+            case kGatherBulk8x24: return launch_bulk<8, 24 * 1024>(d_segs, nseg, d_dst, dst_bytes, 1, d_counter, stream);
+            default: return launch_bulk<kBulkStages, kBulkStage>(d_segs, nseg, d_dst, dst_bytes, 1, d_counter, stream);
         }
     }
     static const int lsu_blocks_per_sm = [] {

@@ -30,13 +30,17 @@ enum GatherVariant : int {
     kGatherBulk6x32 = 3,
     kGatherBulk2Cta = 4,
     kGatherBulk4x48 = 5, // the previous default ring
-    kGatherBulk8x24 = 6
+    kGatherBulk8x24 = 6,
+    kGatherBulkStatic = 7 // the default ring with the static tile split even when a counter is given
 };
 
 // `bulk_ok` (host-checked): every segment has 16-B aligned src/dst/bytes and
 // the segments tile [0, dst_bytes) exactly — the TMA bulk path's contract.
+// `d_counter` (optional, two words, zero between launches): the bulk kernel claims its
+// 64 KB tiles dynamically through it and resets it before it exits; launches sharing
+// one counter must be stream-ordered. Null = static tile split. Bytes never depend on it.
 cudaError_t launch_gather(const GatherSeg* d_segs, std::uint32_t nseg, std::uint8_t* d_dst, std::uint64_t dst_bytes,
-                          int variant, bool bulk_ok, cudaStream_t stream);
+                          int variant, bool bulk_ok, cudaStream_t stream, unsigned int* d_counter = nullptr);
 // Measurement only: read-only HBM stream over [d_src, d_src + bytes) (16-B aligned),
 // XOR-folded into *d_sink.
 cudaError_t launch_read_probe(const std::uint8_t* d_src, std::uint64_t bytes, unsigned int* d_sink, cudaStream_t stream);

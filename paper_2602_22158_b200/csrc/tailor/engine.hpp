@@ -210,6 +210,7 @@ class DeviceMerge {
   private:
     PartitionPlan plan_;
     DeviceBuffer d_segs_;
+    DeviceBuffer counter_; // K2's dynamic tile counter (two words, zero between launches)
     std::uint32_t nseg_ = 0;
     bool bulk_ok_ = false;
 };
@@ -239,6 +240,7 @@ class DeviceSelectStep {
     std::uint64_t shard_bytes_ = 0, wlo_ = 0, whi_ = 0;
     std::uint32_t n_shard_ = 0, n_w_ = 0;
     DeviceBuffer shard_entries_, w_entries_, shard_segs_, w_segs_, source_, scores_;
+    DeviceBuffer counters_; // K2's dynamic tile counters: [0..1] shard gather, [2..3] weights gather
     dev::SnapshotBases bases_{};
     bool entries_aligned_ = false;
     bool bulk_ = false;

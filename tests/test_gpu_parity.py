@@ -319,6 +319,48 @@ def test_shard_sub_units_host_staged():
         fam.gen_shard_range(r, 1, 4, 64, dev(64).data_ptr())
 
 
+def test_dynamic_gather_tiles_are_bitwise_the_static_split():
+    """K2's bulk ring claims its 64 KB tiles from a counter the plan owns and resets it on
+    exit: back-to-back runs (no host sync between them) of the shard gather and of the
+    device step's two gathers give bitwise the static split's bytes every time."""
+    need_gpu()
+    spec, N, K = t.ModelSpec(2, 512, 1376, 4096, False, 7), 2, 3  # ~9.6 MB rank shard: ~150 tiles
+    fam = t.SynthFamily(spec, N, K)
+    r = 1
+    shards = [dev(fam.shard_bytes(k, r)) for k in range(1, K + 1)]
+    fam.gen_shard(r, 1, K, [b.data_ptr() for b in shards])
+    rec = t.MergeRecipe(num_ranks=N, slices=[t.RecipeSlice("S1", [0], [0]), t.RecipeSlice("S2", [1], [1])],
+                        aux={"embed_tokens": "S3", "norm": "S1", "lm_head": "S2"})
+    yaml = rec.to_yaml()
+    mp = t.MergePartition(fam, yaml, r)
+    mp.bind([shards[k - 1].data_ptr() + lo for k, c, lo, hi in mp.windows()])
+    assert mp.bulk_ok
+    ref = dev(mp.bytes)
+    mp.run(ref.data_ptr(), 7)  # static split
+    outs = [dev(mp.bytes) for _ in range(6)]
+    for o_ in outs:
+        mp.run(o_.data_ptr(), 0)
+    torch.cuda.synchronize()
+    for o_ in outs:
+        assert torch.equal(o_[:mp.bytes], ref[:mp.bytes])
+    st = t.SelectStep(fam, r, 0, 1, 0.5)
+    sbytes, wlo, whi = st.range()
+    wb = [dev(whi - wlo) for _ in range(K)]
+    fam.gen_weights(1, K, wlo, whi, [b.data_ptr() for b in wb])
+    st.bind([b.data_ptr() for b in shards], [b.data_ptr() for b in wb])
+    parts = torch.tensor([float((i * 7919) % 97) for i in range(N * (K - 1) * fam.num_modules * 2)],
+                         dtype=torch.float64, device="cuda")
+    s_ref, w_ref = dev(sbytes), dev(whi - wlo)
+    st.run(parts.data_ptr(), N, s_ref.data_ptr(), w_ref.data_ptr(), variant=7)
+    runs = [(dev(sbytes), dev(whi - wlo)) for _ in range(4)]
+    for a, b in runs:
+        st.run(parts.data_ptr(), N, a.data_ptr(), b.data_ptr())
+    torch.cuda.synchronize()
+    for a, b in runs:
+        assert torch.equal(a[:sbytes], s_ref[:sbytes])
+        assert torch.equal(b[:whi - wlo], w_ref[:whi - wlo])
+
+
 @pytest.mark.parametrize("seed", range(4))
 def test_gather_variants_random_segments(seed):
     """Raw K2 (tg_gather): LSU and bulk paths vs a torch reference copy."""

@@ -1,6 +1,7 @@
 #!/usr/bin/env python
-"""Phase trace (usage: files_trace.py [root_dir] [iters]) of the file-facing drop-in path (TAILOR_TRACE=1): medium shape
-L8 h1024 f2752 v32000, N=8, K=4 written to /tmp, then select_recipe + execute_merge."""
+"""Phase trace (usage: files_trace.py [root_dir] [iters] [cold]) of the file-facing drop-in path (TAILOR_TRACE=1):
+medium shape L8 h1024 f2752 v32000, N=8, K=4 written to /tmp, then select_recipe + execute_merge. `cold`: the
+sources' pages are dropped before every iteration (fsync + POSIX_FADV_DONTNEED), as in bench.py's cold files line."""
 import os
 import pathlib
 import shutil
@@ -13,8 +14,9 @@ ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 import paper_2602_22158_b200 as t  # noqa: E402
 
-root = sys.argv[1] if len(sys.argv) > 1 else None  # e.g. /dev/shm (default: $TMPDIR or /tmp)
+root = (sys.argv[1] or None) if len(sys.argv) > 1 else None  # e.g. /dev/shm (default: $TMPDIR or /tmp)
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+cold = len(sys.argv) > 3 and sys.argv[3] == "cold"
 work = pathlib.Path(tempfile.mkdtemp(prefix="tailor-trace-", dir=root))
 try:
     fam = t.SynthFamily(t.ModelSpec(8, 1024, 2752, 32000, False, 42), 8, 4, 100)
@@ -27,7 +29,14 @@ try:
             kv = dict(line.split(":", 1) for line in f)
         return {k: kv[k].strip() for k in ("Dirty", "Writeback")}
 
+    srcs = [p for d in dirs for p in pathlib.Path(d).rglob("*") if p.is_file()]
     for i in range(iters):
+        if cold:
+            for p in srcs:
+                fd = os.open(p, os.O_RDONLY)
+                os.fsync(fd)
+                os.posix_fadvise(fd, 0, 0, os.POSIX_FADV_DONTNEED)
+                os.close(fd)
         print(f"iter {i} start: {dirty()}", file=sys.stderr, flush=True)
         t0 = time.perf_counter()
         rec, _, _ = t.select_recipe(dirs, 0.5)
@@ -37,5 +46,6 @@ try:
         print(f"iter {i}: select {1e3 * (t1 - t0):.1f} ms, merge {1e3 * (t2 - t1):.1f} ms ({st.bytes_moved / 1e9:.2f} GB)",
               file=sys.stderr, flush=True)
         shutil.rmtree(work / f"m{i}")
+        os.sync()
 finally:
     shutil.rmtree(work, ignore_errors=True)
