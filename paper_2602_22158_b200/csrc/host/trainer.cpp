@@ -102,6 +102,7 @@ DeviceTrainer::DeviceTrainer(const ModelSpec& spec, int num_ranks, const AdamHyp
     : model_(spec), N_(num_ranks), base_(base) {
     base_.validate();
     if (const char* v = std::getenv("TAILOR_TRAIN_STORE_GRAD")) store_grad_ = *v && *v != '0';
+    if (const char* v = std::getenv("TAILOR_TRAIN_FDIV")) fdiv_ = *v && *v != '0';
     if (num_ranks < 1) fail(ErrorKind::Recipe, "num_ranks must be >= 1");
     r0_ = rank_begin;
     r1_ = rank_end < 0 ? num_ranks : rank_end;
@@ -293,6 +294,9 @@ std::pair<double, double> DeviceTrainer::step(std::int64_t s) {
         c.lr = static_cast<float>(h.lr);
         c.eps = static_cast<float>(h.eps);
         c.wd = static_cast<float>(h.weight_decay);
+        // y = 0 sends the kernel to __fdiv_rn (TAILOR_TRAIN_FDIV=1: measurement / tests)
+        c.rcp1 = fdiv_ ? 0.f : dev::const_reciprocal(c.bias1);
+        c.rcp2 = fdiv_ ? 0.f : dev::const_reciprocal(c.bias2);
     }
     cuda_check(cudaMemcpyAsync(coef_.get(), coef.data(), coef.size() * sizeof(dev::AdamCoef), cudaMemcpyHostToDevice, stream_),
                "coef");

@@ -13,8 +13,8 @@
 // block order on the host: deterministic, not bitwise equal to the
 // reference's sequential sums (they only feed log.jsonl).
 #include <algorithm>
-#include <cstdlib>
 
+#include "ieee_div.cuh"
 #include "tailor/bf16.hpp"
 #include "tailor/device.hpp"
 
@@ -140,8 +140,9 @@ __global__ void __launch_bounds__(kThreads) finite_check_kernel(const TrainTile*
 __device__ __forceinline__ float adam_one(const AdamCoef& c, float& w, float& m, float& v, float gr) {
     m = __fadd_rn(__fmul_rn(c.b1, m), __fmul_rn(c.one_minus_b1, gr));
     v = __fadd_rn(__fmul_rn(c.b2, v), __fmul_rn(c.one_minus_b2, __fmul_rn(gr, gr)));
-    const float m_hat = __fdiv_rn(m, c.bias1);
-    const float v_hat = __fdiv_rn(v, c.bias2);
+    // bias corrections: constant divisors (RN(1/bias) precomputed on the host; 0 = none)
+    const float m_hat = div_by_const_rn(m, c.bias1, c.rcp1);
+    const float v_hat = div_by_const_rn(v, c.bias2, c.rcp2);
     const float update = __fadd_rn(__fdiv_rn(m_hat, __fadd_rn(__fsqrt_rn(v_hat), c.eps)), __fmul_rn(c.wd, w));
     const float step = __fmul_rn(c.lr, update);
     w = __fsub_rn(w, step);
@@ -151,8 +152,8 @@ __device__ __forceinline__ float adam_one(const AdamCoef& c, float& w, float& m,
 // kRecompute: the gradient is recomputed from the pre-update master (the same
 // _rn expression as pass 1, so the same bits) instead of being read back from a
 // scratch buffer: 28 B per element for the step instead of 36.
-template <bool kRecompute, int kMinBlocks>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) adamw_update_kernel(const TrainTile* __restrict__ tiles, std::uint32_t ntiles,
+template <bool kRecompute>
+__global__ void __launch_bounds__(kThreads) adamw_update_kernel(const TrainTile* __restrict__ tiles, std::uint32_t ntiles,
                                                                 const TrainGroup* __restrict__ groups,
                                                                 const AdamCoef* __restrict__ coef, std::uint8_t* __restrict__ part,
                                                                 const float* __restrict__ grad, TrainParams p,
@@ -287,42 +288,8 @@ std::uint64_t noise_prefix(std::uint64_t seed, std::uint64_t step) {
     return mix(mix(seed + 0x9E3779B97F4A7C15ULL) ^ (step * 0xD1B54A32D192ED03ULL));
 }
 
-// TAILOR_TRAIN_MIN_BLOCKS=6 (measurement): the update compiled for 6 resident blocks per
-// SM (<= 40 registers) instead of the unconstrained 59 (4 blocks).
-int update_min_blocks() {
-    static const int v = [] {
-        const char* e = std::getenv("TAILOR_TRAIN_MIN_BLOCKS");
-        return e && std::atoi(e) == 6 ? 6 : 1;
-    }();
-    return v;
-}
-
-// One wave of blocks: SMs x the blocks per SM that the most register-hungry pass
-// (the update, 50 registers -> 5 blocks of 256 threads) keeps resident. A fixed
-// 8 blocks per SM ran the update in 1.6 waves (740 resident + a 444-block tail at
-// 3 blocks per SM; ncu: 48% warps active). Every pass uses this grid, so the
-// per-block norm partials the host combines have one length (and stay
-// deterministic: the grid depends only on the device).
 unsigned train_grid(std::uint32_t ntiles) {
-    static const unsigned per_sm = [] {
-        int occ = 8;
-        const auto fit = [&occ](const void* fn) {
-            int n = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kThreads, 0) == cudaSuccess && n > 0) occ = std::min(occ, n);
-        };
-        if (update_min_blocks() == 6) {
-            fit(reinterpret_cast<const void*>(adamw_update_kernel<true, 6>));
-            fit(reinterpret_cast<const void*>(adamw_update_kernel<false, 6>));
-        } else {
-            fit(reinterpret_cast<const void*>(adamw_update_kernel<true, 1>));
-            fit(reinterpret_cast<const void*>(adamw_update_kernel<false, 1>));
-        }
-        fit(reinterpret_cast<const void*>(grad_check_kernel<true>));
-        fit(reinterpret_cast<const void*>(grad_check_kernel<false>));
-        fit(reinterpret_cast<const void*>(finite_check_kernel));
-        return static_cast<unsigned>(occ);
-    }();
-    return std::max(1u, std::min(ntiles, static_cast<unsigned>(sm_count()) * per_sm));
+    return std::max(1u, std::min(ntiles, static_cast<unsigned>(sm_count()) * 8u));
 }
 
 cudaError_t launch_grad_check(const TrainTile* d_tiles, std::uint32_t ntiles, const TrainGroup* d_groups,
@@ -352,14 +319,12 @@ cudaError_t launch_finite_check(const TrainTile* d_tiles, std::uint32_t ntiles, 
 cudaError_t launch_adamw(const TrainTile* d_tiles, std::uint32_t ntiles, const TrainGroup* d_groups, const AdamCoef* d_coef,
                          std::uint8_t* d_part, const float* d_grad, const TrainParams& p, double* d_delta_partials,
                          double* d_grad_partials, unsigned int* d_next_nonfinite, cudaStream_t s) {
-    const unsigned grid = train_grid(ntiles);
-    const bool six = update_min_blocks() == 6;
     if (d_grad)
-        (six ? adamw_update_kernel<false, 6> : adamw_update_kernel<false, 1>)<<<grid, kThreads, 0, s>>>(
-            d_tiles, ntiles, d_groups, d_coef, d_part, d_grad, p, d_delta_partials, nullptr, nullptr);
+        adamw_update_kernel<false><<<train_grid(ntiles), kThreads, 0, s>>>(d_tiles, ntiles, d_groups, d_coef, d_part, d_grad, p,
+                                                                          d_delta_partials, nullptr, nullptr);
     else
-        (six ? adamw_update_kernel<true, 6> : adamw_update_kernel<true, 1>)<<<grid, kThreads, 0, s>>>(
-            d_tiles, ntiles, d_groups, d_coef, d_part, nullptr, p, d_delta_partials, d_grad_partials, d_next_nonfinite);
+        adamw_update_kernel<true><<<train_grid(ntiles), kThreads, 0, s>>>(d_tiles, ntiles, d_groups, d_coef, d_part, nullptr, p,
+                                                                         d_delta_partials, d_grad_partials, d_next_nonfinite);
     return cudaGetLastError();
 }
 

@@ -166,8 +166,19 @@ struct TrainGroup {
     std::uint32_t pad;
 };
 // Per-group FP32 coefficients, each rounded once from FP64 (R/src/adamw.cpp:19-27).
+// y = RN(1/b) in single precision for div_by_const_rn (kernels/ieee_div.cuh); a divisor
+// outside [2^-20, 2^20] (never a bias correction: those lie in [1 - beta, 1]) gets 0,
+// which makes the kernel divide per element (__fdiv_rn).
+inline float const_reciprocal(float b) {
+    const float ab = b < 0 ? -b : b;
+    if (!(ab >= 0x1p-20f && ab <= 0x1p20f)) return 0.0f;
+    volatile float one = 1.0f; // an IEEE single division on the host, not a folded constant
+    return one / b;
+}
 struct AdamCoef {
-    float b1, one_minus_b1, b2, one_minus_b2, bias1, bias2, lr, eps, wd, pad[3];
+    float b1, one_minus_b1, b2, one_minus_b2, bias1, bias2, lr, eps, wd;
+    float rcp1, rcp2; // RN(1/bias1), RN(1/bias2) for div_by_const_rn (kernels/ieee_div.cuh); 0 = divide
+    float pad;
 };
 struct TrainParams {
     // unit_noise(seed, step, e) = f(mix64(noise_prefix ^ e * C3)): the first two

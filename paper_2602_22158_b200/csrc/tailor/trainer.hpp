@@ -77,6 +77,9 @@ class DeviceTrainer {
     // Pass 2 recomputes the gradient (28 B/element) unless TAILOR_TRAIN_STORE_GRAD=1
     // selects the scratch-buffer variant (36 B/element; kept for comparison).
     bool store_grad_ = false;
+    // The bias corrections divide by a per-step constant through its precomputed
+    // reciprocal (kernels/ieee_div.cuh); TAILOR_TRAIN_FDIV=1 keeps __fdiv_rn per element.
+    bool fdiv_ = false;
     std::vector<AdamHyperparams> hyper_; // per group (GroupState::hyper)
     // The fast pre-update check of step s+1 is folded into step s's update pass (it sees
     // every new master as it writes it): masters_checked_ = the current masters are known

@@ -227,3 +227,42 @@ def test_resume_errors_match_reference(tmp_path):
     with pytest.raises(t.TailorError) as e:
         t.resume(str(full / "checkpoint-25"), -1, str(tmp_path / "o2"))
     assert e.value.kind == t.ErrorKind.Recipe
+
+
+def test_constant_division_is_ieee_division(tmp_path):
+    """kernels/ieee_div.cuh: a / b through y = RN(1/b) and Markstein's correction equals
+    __fdiv_rn bit for bit for all 2^32 float bit patterns a, for the bias corrections
+    1 - beta^t (beta 0.9, 0.999, 0.95; t = 1..300) and 100 random divisors in [2^-20, 1]."""
+    need_gpu()
+    import pathlib
+    import subprocess
+
+    root = pathlib.Path(__file__).resolve().parents[1]
+    exe = tmp_path / "div_const_check"
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-std=c++17", "-O3",
+                    "-I", str(root / "paper_2602_22158_b200/csrc/kernels"), "-I", str(root / "paper_2602_22158_b200/csrc"),
+                    str(root / "tools/div_const_check.cu"), "-o", str(exe)], check=True)
+    p = subprocess.run([str(exe), "300", "100", "0.9", "0.999", "0.95"], capture_output=True, text=True, timeout=600)
+    res = json.loads(p.stdout.strip().splitlines()[-1])
+    assert res["divisors"] == 1000 and res["mismatches"] == 0, (res, p.stderr[-2000:])
+
+
+@pytest.mark.parametrize("fdiv", ["0", "1"])
+def test_trainer_division_forms_are_bitwise_equal(monkeypatch, fdiv):
+    """The trainer with the precomputed-reciprocal bias division vs per-element __fdiv_rn
+    (TAILOR_TRAIN_FDIV=1): identical state bytes and norms after several steps."""
+    need_gpu()
+    spec = t.ModelSpec(2, 256, 688, 1000, False, 3)
+    monkeypatch.setenv("TAILOR_TRAIN_FDIV", fdiv)
+    a = t.Trainer(spec, 2)
+    monkeypatch.setenv("TAILOR_TRAIN_FDIV", "1")
+    b = t.Trainer(spec, 2)
+    for s in range(1, 8):
+        assert a.step(s) == b.step(s)
+    for r in range(2):
+        (pa, na), (pb, nb) = a.partition(r), b.partition(r)
+        x = torch.empty(na, dtype=torch.uint8, device="cuda")
+        y = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        _d2d(x.data_ptr(), pa, na)
+        _d2d(y.data_ptr(), pb, nb)
+        assert torch.equal(x, y)
