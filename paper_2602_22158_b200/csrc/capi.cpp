@@ -171,7 +171,9 @@ struct PackedLoader {
     std::uint64_t direct_bytes = 0;
     static constexpr std::uint64_t kHalf = 16ull << 20;
 
-    PackedLoader(cudaStream_t s, int reader_threads) : st(s), threads(reader_threads) {
+    ReadPool pool;
+
+    PackedLoader(cudaStream_t s, int reader_threads) : st(s), threads(reader_threads), pool(std::max(1, reader_threads)) {
         for (auto& e : half_done) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
         stage.resize(2 * kHalf);
     }
@@ -203,27 +205,41 @@ struct PackedLoader {
         const int dfd = want_direct_read(io_mode_from_env(IoMode::Auto), fd, lay.payload_offset(), lay.payload_bytes)
                             ? open_direct_read(p.string())
                             : -1;
-        try {
-            std::size_t fi = 0;
-            for (std::uint64_t lo = 0; lo < total; lo += kHalf, half ^= 1) {
-                const std::uint64_t hi = std::min(total, lo + kHalf);
-                std::uint8_t* buf = stage.get() + static_cast<std::uint64_t>(half) * kHalf;
-                if (used[half]) cuda_check(cudaEventSynchronize(half_done[half]), "event");
-                std::vector<ReadJob> jobs;
-                while (fi < where.size() && where[fi].second + where[fi].first->bytes() <= lo) ++fi;
-                for (std::size_t j = fi; j < where.size() && where[j].second < hi; ++j) {
-                    const auto& [e, at] = where[j];
-                    const std::uint64_t a = std::max(lo, at), z = std::min(hi, at + e->bytes());
-                    if (a < z) jobs.push_back({fd, buf + (a - lo), z - a, lay.payload_offset() + e->begin + (a - at), dfd});
-                }
-                const double r0 = clock_ms();
-                run_reads(jobs, threads, p.string());
-                read_ms += clock_ms() - r0;
-                cuda_check(cudaMemcpyAsync(dst + lo, buf, hi - lo, cudaMemcpyHostToDevice, st), "H2D");
-                cuda_check(cudaEventRecord(half_done[half], st), "event");
-                used[half] = true;
+        // half h uses buffer (half + h) & 1; its reads are queued one half ahead on the
+        // reader pool (after the buffer's previous H2D), so the pieces of the next half are
+        // in flight while this half's last ones finish
+        const std::uint64_t nh = (total + kHalf - 1) / kHalf;
+        const auto queue_half = [&](std::uint64_t h) {
+            const int b = static_cast<int>((static_cast<std::uint64_t>(half) + h) & 1);
+            if (used[b]) cuda_check(cudaEventSynchronize(half_done[b]), "event");
+            const std::uint64_t lo = h * kHalf, hi = std::min(total, lo + kHalf);
+            std::uint8_t* buf = stage.get() + static_cast<std::uint64_t>(b) * kHalf;
+            std::vector<ReadJob> jobs;
+            for (const auto& [e, at] : where) {
+                const std::uint64_t a = std::max(lo, at), z = std::min(hi, at + e->bytes());
+                if (a < z) jobs.push_back({fd, buf + (a - lo), z - a, lay.payload_offset() + e->begin + (a - at), dfd});
             }
+            return pool.submit(jobs, p.string());
+        };
+        try {
+            std::uint64_t ticket = nh ? queue_half(0) : 0;
+            for (std::uint64_t h = 0; h < nh; ++h) {
+                const std::uint64_t next = h + 1 < nh ? queue_half(h + 1) : 0;
+                const double r0 = clock_ms();
+                pool.wait(ticket);
+                read_ms += clock_ms() - r0;
+                const int b = static_cast<int>((static_cast<std::uint64_t>(half) + h) & 1);
+                const std::uint64_t lo = h * kHalf, hi = std::min(total, lo + kHalf);
+                cuda_check(cudaMemcpyAsync(dst + lo, stage.get() + static_cast<std::uint64_t>(b) * kHalf, hi - lo,
+                                           cudaMemcpyHostToDevice, st),
+                           "H2D");
+                cuda_check(cudaEventRecord(half_done[b], st), "event");
+                used[b] = true;
+                ticket = next;
+            }
+            half = static_cast<int>((static_cast<std::uint64_t>(half) + nh) & 1);
         } catch (...) {
+            pool.drain();
             cudaStreamSynchronize(st);
             ::close(fd);
             if (dfd >= 0) ::close(dfd);

@@ -71,7 +71,7 @@ class FileAssembler {
     static constexpr int kSlots = 3;
 
     FileAssembler(int read_threads, bool uncached, std::uint64_t chunk, IoMode io = IoMode::Buffered)
-        : workers_(std::max(1, read_threads)), uncached_(uncached), chunk_(chunk), io_(io) {
+        : uncached_(uncached), chunk_(chunk), io_(io), pool_(std::max(1, read_threads)) {
         for (auto& s : stream_) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
         for (int i = 0; i < kSlots; ++i) {
             cuda_check(cudaEventCreate(&ev0_[i]), "event");
@@ -88,7 +88,7 @@ class FileAssembler {
 
     double device_ms = 0.0, read_ms = 0.0, wait_ms = 0.0, write_ms = 0.0;
     std::uint64_t bytes = 0, direct_read_bytes = 0, direct_write_bytes = 0;
-    void set_read_threads(int n) { workers_ = std::max(1, n); }
+    void set_read_threads(int n) { pool_.grow(std::max(1, n)); }
 
     void assemble(const PartitionPlan& pp, const std::vector<fs::path>& window_files, const fs::path& out_path) {
         Fd out(out_path, O_WRONLY | O_CREAT | O_TRUNC);
@@ -187,16 +187,32 @@ class FileAssembler {
                 cv.notify_all();
             }
         });
+        // Reads run one chunk ahead on the lane's reader pool: chunk ci+1's pieces are
+        // queued (its slot free once chunk ci+1-kSlots is written) before chunk ci's
+        // reads are waited for, so the device queue does not drain between chunks.
         std::exception_ptr rerr;
+        std::uint64_t ticket[kSlots] = {};
+        const auto slot_free = [&](std::size_t ci) { // the slot's previous chunk is written
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return written + kSlots > ci || werr; });
+            return !werr;
+        };
         try {
-            for (std::size_t ci = 0; ci < plan.chunks.size(); ++ci) {
+            const std::size_t nchunks = plan.chunks.size();
+            bool go = nchunks > 0 && slot_free(0);
+            if (go) ticket[0] = queue_reads(plan.chunks[0], pp, window_files, file_off, fds, dfds, 0, out_path);
+            for (std::size_t ci = 0; go && ci < nchunks; ++ci) {
                 const int slot = static_cast<int>(ci % kSlots);
-                {
-                    std::unique_lock<std::mutex> lk(mu); // the slot's previous chunk is written
-                    cv.wait(lk, [&] { return written + kSlots > ci || werr; });
-                    if (werr) break;
+                if (ci + 1 < nchunks) {
+                    if (!slot_free(ci + 1)) break;
+                    const int ns = static_cast<int>((ci + 1) % kSlots);
+                    ticket[ns] = queue_reads(plan.chunks[ci + 1], pp, window_files, file_off, fds, dfds, ns, out_path);
                 }
-                stage_chunk(plan.chunks[ci], pp, window_files, file_off, fds, dfds, slot, ci == 0 ? head : 0, out_path);
+                {
+                    ScopedAccum acc(read_ms);
+                    pool_.wait(ticket[slot]);
+                }
+                launch_chunk(plan.chunks[ci], slot, ci == 0 ? head : 0);
                 std::lock_guard<std::mutex> lk(mu);
                 issued = ci + 1;
                 cv.notify_all();
@@ -204,6 +220,8 @@ class FileAssembler {
         } catch (...) {
             rerr = std::current_exception();
         }
+        pool_.drain(); // no read may still target a slot or descriptor of this file
+        for (auto& o : opened_) o.clear();
         {
             std::lock_guard<std::mutex> lk(mu);
             if (rerr && !werr) werr = rerr; // stops the writer
@@ -221,13 +239,15 @@ class FileAssembler {
   private:
     struct ChunkPlan;
 
-    // Reads one chunk's source ranges into the slot's pinned staging (parallel
-    // pread; uncached mode re-opens the source file per read, as the reference
-    // reloads a shard per group copy), then queues H2D -> K2 -> D2H on the slot.
-    void stage_chunk(const ChunkPlan& c, const PartitionPlan& pp, const std::vector<fs::path>& window_files,
-                     const std::vector<std::uint64_t>& file_off, const std::vector<std::unique_ptr<Fd>>& fds,
-                     const std::vector<std::unique_ptr<Fd>>& dfds, int slot, std::uint64_t d2h_shift, const fs::path& out_path) {
-        std::vector<std::unique_ptr<Fd>> opened;
+    // Queues one chunk's source reads into the slot's pinned staging on the lane's
+    // reader pool (uncached mode re-opens the source file per read, as the reference
+    // reloads a shard per group copy; those descriptors live in the slot until its next
+    // use, after the reads were waited for).
+    std::uint64_t queue_reads(const ChunkPlan& c, const PartitionPlan& pp, const std::vector<fs::path>& window_files,
+                              const std::vector<std::uint64_t>& file_off, const std::vector<std::unique_ptr<Fd>>& fds,
+                              const std::vector<std::unique_ptr<Fd>>& dfds, int slot, const fs::path& out_path) {
+        auto& opened = opened_[slot];
+        opened.clear();
         std::vector<ReadJob> jobs;
         for (const auto& rd : c.reads) {
             int fd;
@@ -246,10 +266,11 @@ class FileAssembler {
             if (dfd >= 0) direct_read_bytes += rd.b - rd.a;
             jobs.push_back({fd, pin_io_[slot].get() + rd.at, rd.b - rd.a, file_off[rd.w] + rd.a, dfd});
         }
-        {
-            ScopedAccum acc(read_ms);
-            run_reads(jobs, workers_, out_path.string());
-        }
+        return pool_.submit(jobs, out_path.string());
+    }
+
+    // The slot's reads are complete: H2D -> K2 -> D2H on the slot's stream.
+    void launch_chunk(const ChunkPlan& c, int slot, std::uint64_t d2h_shift) {
         cudaStream_t s = stream_[slot];
         cuda_check(cudaMemcpyAsync(d_in_[slot].get(), pin_io_[slot].get(), c.staging, cudaMemcpyHostToDevice, s), "H2D");
         auto* segs = reinterpret_cast<dev::GatherSeg*>(pin_segs_[slot].get());
@@ -365,7 +386,6 @@ class FileAssembler {
         return off;
     }
 
-    int workers_;
     bool uncached_;
     std::uint64_t chunk_;
     IoMode io_;
@@ -373,7 +393,9 @@ class FileAssembler {
     cudaEvent_t ev0_[kSlots]{}, ev1_[kSlots]{};
     PinnedBuffer pin_io_[kSlots], pin_segs_[kSlots]; // pinned: async copies never sync the stream
     DeviceBuffer d_in_[kSlots], d_out_[kSlots], d_segs_[kSlots];
+    std::vector<std::unique_ptr<Fd>> opened_[kSlots]; // uncached mode: per-read descriptors of the slot's chunk
     std::map<std::string, std::uint64_t> payload_off_;
+    ReadPool pool_; // last: destroyed (joined) before the buffers its reads target
 };
 
 // Failure injection for tests (TAILOR_FAULT = comma-separated point names), in the

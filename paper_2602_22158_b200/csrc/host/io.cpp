@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
+#include <map>
 #include <fcntl.h>
 #include <memory>
 #include <sys/mman.h>
@@ -194,12 +196,13 @@ void read_direct(const ReadJob& p, const std::string& what) {
 
 } // namespace
 
-void run_reads(const std::vector<ReadJob>& jobs, int threads, const std::string& what) {
-    // O_DIRECT reads go to the device, not the page cache: queue depth is what they need
-    // (tools/disk_probe reaches the device's bandwidth with 32 readers), so direct jobs are
-    // cut into 4 MB pieces served by at least 4 threads per call
-    constexpr std::uint64_t kDirectPiece = 4ull << 20;
-    std::vector<ReadJob> pieces;
+namespace {
+// O_DIRECT reads go to the device, not the page cache: queue depth is what they need
+// (tools/disk_probe reaches the device's bandwidth with 32 readers), so direct jobs are
+// cut into 4 MB pieces served by at least 4 threads
+constexpr std::uint64_t kDirectPiece = 4ull << 20;
+
+bool cut_pieces(const std::vector<ReadJob>& jobs, std::vector<ReadJob>& pieces) {
     bool direct = false;
     for (const auto& j : jobs) {
         const std::uint64_t piece = j.dfd >= 0 ? kDirectPiece : kPiece;
@@ -207,11 +210,93 @@ void run_reads(const std::vector<ReadJob>& jobs, int threads, const std::string&
         for (std::uint64_t at = 0; at < j.bytes; at += piece)
             pieces.push_back({j.fd, j.dst + at, std::min(piece, j.bytes - at), j.offset + at, j.dfd});
     }
-    if (direct) threads = std::max(threads, 4);
-    const auto read_one = [&](const ReadJob& p) {
-        if (p.dfd >= 0) read_direct(p, what);
-        else read_buffered(p, what);
-    };
+    return direct;
+}
+
+void read_one(const ReadJob& p, const std::string& what) {
+    if (p.dfd >= 0) read_direct(p, what);
+    else read_buffered(p, what);
+}
+} // namespace
+
+// ---- ReadPool ---------------------------------------------------------------------
+ReadPool::ReadPool(int threads) { grow(threads); }
+
+ReadPool::~ReadPool() {
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        stop_ = true;
+    }
+    work_.notify_all();
+    for (auto& t : threads_) t.join();
+}
+
+void ReadPool::grow(int threads) {
+    std::lock_guard<std::mutex> lk(mu_);
+    while (static_cast<int>(threads_.size()) < threads) threads_.emplace_back([this] { worker(); });
+}
+
+void ReadPool::worker() {
+    for (;;) {
+        Piece pc;
+        {
+            std::unique_lock<std::mutex> lk(mu_);
+            work_.wait(lk, [&] { return stop_ || !queue_.empty(); });
+            if (queue_.empty()) return; // stop_ with nothing left
+            pc = std::move(queue_.front());
+            queue_.pop_front();
+        }
+        std::exception_ptr err;
+        try {
+            read_one(pc.job, *pc.what);
+        } catch (...) {
+            err = std::current_exception();
+        }
+        std::lock_guard<std::mutex> lk(mu_);
+        Batch& b = batches_[pc.ticket];
+        if (err && !b.err) b.err = err;
+        if (--b.remaining == 0) done_.notify_all();
+    }
+}
+
+std::uint64_t ReadPool::submit(const std::vector<ReadJob>& jobs, const std::string& what) {
+    std::vector<ReadJob> pieces;
+    if (cut_pieces(jobs, pieces)) grow(4);
+    std::lock_guard<std::mutex> lk(mu_);
+    const std::uint64_t ticket = next_++;
+    Batch& b = batches_[ticket];
+    b.remaining = pieces.size();
+    b.what = std::make_shared<const std::string>(what);
+    for (auto& p : pieces) queue_.push_back({ticket, p, b.what});
+    work_.notify_all();
+    return ticket;
+}
+
+void ReadPool::wait(std::uint64_t ticket) {
+    std::unique_lock<std::mutex> lk(mu_);
+    auto it = batches_.find(ticket);
+    if (it == batches_.end()) return;
+    done_.wait(lk, [&] { return it->second.remaining == 0; });
+    const std::exception_ptr err = it->second.err;
+    batches_.erase(it);
+    lk.unlock();
+    if (err) std::rethrow_exception(err);
+}
+
+void ReadPool::drain() {
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] {
+        for (const auto& [t, b] : batches_)
+            if (b.remaining) return false;
+        return true;
+    });
+    batches_.clear();
+}
+
+void run_reads(const std::vector<ReadJob>& jobs, int threads, const std::string& what) {
+    std::vector<ReadJob> pieces;
+    if (cut_pieces(jobs, pieces)) threads = std::max(threads, 4);
+    const auto read_one = [&](const ReadJob& p) { tailor::read_one(p, what); };
     const int n = std::max(1, std::min<int>(threads, static_cast<int>(pieces.size())));
     if (n == 1) {
         for (const auto& p : pieces) read_one(p);

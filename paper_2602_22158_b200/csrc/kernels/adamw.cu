@@ -140,7 +140,8 @@ __global__ void __launch_bounds__(kThreads) finite_check_kernel(const TrainTile*
 __device__ __forceinline__ float adam_one(const AdamCoef& c, float& w, float& m, float& v, float gr) {
     m = __fadd_rn(__fmul_rn(c.b1, m), __fmul_rn(c.one_minus_b1, gr));
     v = __fadd_rn(__fmul_rn(c.b2, v), __fmul_rn(c.one_minus_b2, __fmul_rn(gr, gr)));
-    // bias corrections: constant divisors (RN(1/bias) precomputed on the host; 0 = none)
+    // bias corrections: constant divisors through RN(1/bias) precomputed on the host
+    // (kernels/ieee_div.cuh; bitwise __fdiv_rn, checked exhaustively)
     const float m_hat = div_by_const_rn(m, c.bias1, c.rcp1);
     const float v_hat = div_by_const_rn(v, c.bias2, c.rcp2);
     const float update = __fadd_rn(__fdiv_rn(m_hat, __fadd_rn(__fsqrt_rn(v_hat), c.eps)), __fmul_rn(c.wd, w));

@@ -5,8 +5,15 @@
 // with pread, straight into pinned staging buffers.
 #pragma once
 
+#include <condition_variable>
 #include <cstdint>
+#include <deque>
+#include <exception>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace tailor {
@@ -25,6 +32,43 @@ struct ReadJob {
 // of the merge lanes arrange that), the partial head/tail blocks and any
 // incongruent job through an aligned bounce buffer.
 void run_reads(const std::vector<ReadJob>& jobs, int threads, const std::string& what);
+
+// Persistent reader threads over one FIFO of pieces (cut as run_reads cuts them). Each
+// submit() is a batch with its own completion, so a lane can queue the reads of its next
+// chunk while the current chunk's last pieces are still in flight: the device queue never
+// drains at chunk boundaries. Buffers and descriptors of a batch must outlive its wait()
+// (or drain()); the destructor finishes the queued pieces before joining.
+class ReadPool {
+  public:
+    explicit ReadPool(int threads);
+    ~ReadPool();
+    ReadPool(const ReadPool&) = delete;
+    ReadPool& operator=(const ReadPool&) = delete;
+    void grow(int threads); // never shrinks
+    std::uint64_t submit(const std::vector<ReadJob>& jobs, const std::string& what);
+    void wait(std::uint64_t ticket); // rethrows the batch's first failure (StorageError)
+    void drain();                    // waits for every batch, dropping their errors
+
+  private:
+    struct Piece {
+        std::uint64_t ticket = 0;
+        ReadJob job{};
+        std::shared_ptr<const std::string> what;
+    };
+    struct Batch {
+        std::size_t remaining = 0;
+        std::exception_ptr err;
+        std::shared_ptr<const std::string> what;
+    };
+    void worker();
+    std::mutex mu_;
+    std::condition_variable work_, done_;
+    std::deque<Piece> queue_;
+    std::map<std::uint64_t, Batch> batches_;
+    std::vector<std::thread> threads_;
+    std::uint64_t next_ = 0;
+    bool stop_ = false;
+};
 
 // ---- direct I/O ------------------------------------------------
 // The reference reads every byte through the page cache with an istreambuf loop
