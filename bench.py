@@ -92,13 +92,50 @@ def shared_gpu() -> bool:
     return os.environ.get("TAILOR_BENCH_SHARE_GPU") == "1"
 
 
+_COMM = None
+
+
+def lib_comm():
+    """The library's NCCL communicator (tg_comm_*), created on first use on every rank:
+    rank 0's unique id travels over the torch process group (bootstrap only)."""
+    global _COMM
+    if _COMM is None:
+        import torch
+        import torch.distributed as dist
+
+        import paper_2602_22158_b200 as t
+
+        obj = [t.Comm.unique_id() if dist.get_rank() == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        _COMM = t.Comm(obj[0], dist.get_world_size(), dist.get_rank(), torch.cuda.current_device())
+    return _COMM
+
+
+def collective_name():
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return None
+    if dist.get_backend() != "nccl":
+        return "gloo (torch.distributed, host-staged; shared-GPU tests)"
+    if os.environ.get("TAILOR_BENCH_TORCH_ALLGATHER") == "1":
+        return "torch.distributed all_gather_into_tensor (NCCL)"
+    return "tg_comm_allgather (the library's NCCL communicator)"
+
+
 def all_gather(out, inp):
-    """NCCL all-gather of the score partials (gloo: staged through host tensors)."""
+    """All-gather of the FP64 score partials: the library's NCCL communicator
+    (tg_comm_allgather) on the current stream; TAILOR_BENCH_TORCH_ALLGATHER=1 uses torch's
+    NCCL process group instead; gloo (shared-GPU tests) stages through host tensors."""
     import torch
     import torch.distributed as dist
 
     if dist.get_backend() == "nccl":
-        dist.all_gather_into_tensor(out, inp)
+        if os.environ.get("TAILOR_BENCH_TORCH_ALLGATHER") == "1":
+            dist.all_gather_into_tensor(out, inp)
+            return
+        assert inp.dtype == torch.float64 and out.dtype == torch.float64 and inp.is_contiguous() and out.is_contiguous()
+        lib_comm().all_gather(inp.data_ptr(), out.data_ptr(), inp.numel(), torch.cuda.current_stream().cuda_stream)
         return
     parts = [torch.empty(inp.numel(), dtype=inp.dtype) for _ in range(dist.get_world_size())]
     dist.all_gather(parts, inp.cpu())
@@ -761,6 +798,7 @@ def our_arm(args, rank, world, local_rank):
         "detail": {"params": fam.parameter_count, "composite_bytes_per_step": job_bytes,
                    "parallelism": f"zero-partition x{world} (GPU g owns ranks {mine[0]}..{mine[-1]} of {N}"
                                   + (", all-gather of the FP64 partials over NCCL)" if world > 1 else ")"),
+                   "collective": collective_name(),
                    "partitions_per_gpu": len(mine), "resident_partition_slots": res.R,
                    "regenerations_per_step": regen_per_step,
                    "timing": "sum of CUDA-event-timed segments per step (score per partition | all-gather | "

@@ -313,6 +313,18 @@ int tg_dstep_run(tg_dstep* s, const double* d_rank_partials, int32_t nranks, uin
 /* Synchronous reads of the last run's selection: source_of[M] (0-based snapshot), scores[(K-1)*M]. */
 int tg_dstep_result(tg_dstep* s, int32_t* source_of, double* scores, void* stream);
 
+/* ---- the score-partials all-gather across GPUs ------------------------
+ * One NCCL communicator per GPU of a job (libnccl.so.2 is loaded at run time). Rank 0
+ * makes the 128-byte id and the caller ships it to every rank (any bootstrap channel);
+ * tg_comm_create is collective. tg_comm_allgather: d_recv[r * count + i] = rank r's
+ * d_send[i] (FP64), asynchronous on `stream` — the [nranks][K-1][M][2] partials table
+ * that tg_layout_select / tg_dstep_run consume in rank order. */
+typedef struct tg_comm tg_comm;
+int tg_comm_unique_id(uint8_t id_out[128]);
+tg_comm* tg_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device);
+void tg_comm_destroy(tg_comm* c);
+int tg_comm_allgather(tg_comm* c, const double* d_send, double* d_recv, uint64_t count, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -174,6 +174,10 @@ SIGNATURES = {
     "tg_dstep_bind": (_I, [_P, _PP, _PP]),
     "tg_dstep_run": (_I, [_P, _P, _I32, _P, _P, _I32, _I32, _P]),
     "tg_dstep_result": (_I, [_P, _c.POINTER(_I32), _c.POINTER(_D), _P]),
+    "tg_comm_unique_id": (_I, [_c.POINTER(_c.c_uint8)]),
+    "tg_comm_create": (_P, [_c.POINTER(_c.c_uint8), _I32, _I32, _I32]),
+    "tg_comm_destroy": (None, [_P]),
+    "tg_comm_allgather": (_I, [_P, _P, _P, _U64, _P]),
 }
 
 _lib = None

@@ -21,6 +21,7 @@
 
 #include <json.hpp>
 
+#include "tailor/comm.hpp"
 #include "tailor/engine.hpp"
 #include "tailor/errors.hpp"
 #include "tailor/io.hpp"
@@ -49,6 +50,9 @@ struct tg_trainer {
 };
 struct tg_dstep {
     std::unique_ptr<DeviceSelectStep> step;
+};
+struct tg_comm {
+    std::unique_ptr<Comm> comm;
 };
 struct tg_mplan {
     std::unique_ptr<DeviceMerge> dev;
@@ -1034,6 +1038,32 @@ int tg_dstep_result(tg_dstep* s, int32_t* source_of, double* scores, void* strea
             const auto sc = s->step->scores(static_cast<cudaStream_t>(stream));
             std::copy(sc.begin(), sc.end(), scores);
         }
+    });
+}
+
+int tg_comm_unique_id(uint8_t id_out[128]) {
+    return guard([&] {
+        if (!id_out) fail(ErrorKind::Recipe, "tg_comm_unique_id: null output");
+        const auto id = comm_unique_id();
+        std::copy(id.begin(), id.end(), id_out);
+    });
+}
+
+tg_comm* tg_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device) {
+    tg_comm* out = nullptr;
+    guard([&] {
+        if (!id) fail(ErrorKind::Recipe, "tg_comm_create: null id");
+        out = new tg_comm{std::make_unique<Comm>(id, nranks, rank, device)};
+    });
+    return out;
+}
+
+void tg_comm_destroy(tg_comm* c) { delete c; }
+
+int tg_comm_allgather(tg_comm* c, const double* d_send, double* d_recv, uint64_t count, void* stream) {
+    return guard([&] {
+        if (!c) fail(ErrorKind::Recipe, "tg_comm_allgather: null communicator");
+        c->comm->all_gather(d_send, d_recv, count, static_cast<cudaStream_t>(stream));
     });
 }
 

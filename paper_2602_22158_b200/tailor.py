@@ -27,7 +27,7 @@ from ._lib import (ErrorKind, GatherSegC, HostCopyC, MergeOptionsC, MergeStatsC,
 __all__ = ["ErrorKind", "TailorError", "ModelSpec", "RecipeSlice", "MergeRecipe", "MergeOptions", "MergeStats",
            "parse_recipe", "recipe_to_yaml", "resolve_plan", "execute_merge", "recipe_from_manifests",
            "verify_checkpoint", "regroup", "train", "resume", "score_snapshots", "select_recipe", "layer_map", "SnapshotLayout", "SynthFamily", "Scorer",
-           "MergePartition", "SelectStep", "Trainer", "STRATEGIES", "gather", "read_probe"]
+           "MergePartition", "SelectStep", "Trainer", "Comm", "STRATEGIES", "gather", "read_probe"]
 
 
 @dataclasses.dataclass
@@ -561,3 +561,31 @@ class SelectStep:
         sc = (ctypes.c_double * max(1, (self.K - 1) * self.M))()
         check(lib().tg_dstep_result(self._h, src, sc, stream))
         return [src[i] for i in range(self.M)], [[sc[p * self.M + m] for m in range(self.M)] for p in range(self.K - 1)]
+
+
+class Comm:
+    """NCCL communicator of one GPU of a job (tg_comm_*): the score-partials all-gather.
+    Rank 0 calls `Comm.unique_id()` and ships the 128 bytes to every rank (any channel);
+    the constructor is collective."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * 128)()
+        check(lib().tg_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int = 0):
+        if len(uid) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        self._h = check_handle(lib().tg_comm_create(buf, nranks, rank, device))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().tg_comm_destroy(h)
+            self._h = None
+
+    def all_gather(self, d_send: int, d_recv: int, count: int, stream: int = 0) -> None:
+        """d_recv[r * count + i] = rank r's d_send[i] (FP64 device buffers), async on `stream`."""
+        check(lib().tg_comm_allgather(self._h, d_send, d_recv, count, stream))

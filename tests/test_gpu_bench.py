@@ -105,3 +105,24 @@ def test_bench_reference_arm_under_torchrun_rank0_only():
     line = run_bench(2, "--impl", "reference", "--workload", "cfg1", "--steps", "1", "--warmup", "0")
     assert line["impl"] == "reference"
     assert "unavailable" in line or (line["value"] > 0 and line["cpu_baseline"]["kind"] == "reference")
+
+
+def test_library_comm_allgather_single_rank():
+    """tg_comm_* (the library's NCCL communicator, libnccl.so.2 loaded at run time): a
+    one-rank communicator gathers its own FP64 rows unchanged, on a torch stream."""
+    import torch
+
+    import paper_2602_22158_b200 as t
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    uid = t.Comm.unique_id()
+    assert len(uid) == 128
+    c = t.Comm(uid, 1, 0, 0)
+    x = torch.randn(4321, dtype=torch.float64, device="cuda")
+    y = torch.zeros_like(x)
+    c.all_gather(x.data_ptr(), y.data_ptr(), x.numel(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(x, y)
+    with pytest.raises(t.TailorError):
+        t.Comm(uid, 1, 3, 0)  # rank out of range
