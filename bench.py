@@ -1641,6 +1641,8 @@ def init_and(fn, args, rank, world, local_rank):
         if world > 1:
             import torch.distributed as dist
 
+            global _COMM
+            _COMM = None  # ncclCommDestroy while CUDA and the process group are still up
             dist.destroy_process_group()
 
 
