@@ -425,10 +425,12 @@ def composite_bytes_on_disk(out: pathlib.Path) -> int:
     return total
 
 
-def run_files_sample(workdir: pathlib.Path, workload: str, cores: int, reps: int = 2):
-    """The same bounded sample through OUR files drop-in (tg_select_recipe ->
-    tg_execute_merge with the device gather and re-verify), best of `reps` after one
-    warm-up: (seconds, composite bytes)."""
+def run_files_sample(workdir: pathlib.Path, workload: str, cores: int, reps: int = 2, combined: bool = True):
+    """The same bounded sample through OUR files drop-in, best of `reps` after one warm-up:
+    (seconds, composite bytes). combined: tg_select_merge (score, select, merge and
+    re-verify in one call; the scorer's device copies of the masters feed the merge) —
+    the counterpart of the reference's select-merge; else tg_select_recipe then
+    tg_execute_merge."""
     import paper_2602_22158_b200 as t
 
     rho = sample_of(workload)[7]
@@ -437,8 +439,11 @@ def run_files_sample(workdir: pathlib.Path, workload: str, cores: int, reps: int
     for i in range(reps + 1):
         out = workdir / f"ours-{time.time_ns()}"
         t0 = time.perf_counter()
-        rec, _, _ = t.select_recipe(dirs, rho)
-        st = t.execute_merge(rec, str(out), t.MergeOptions(workers=cores))
+        if combined:
+            _, _, _, st = t.select_merge(dirs, str(out), rho, t.MergeOptions(workers=cores))
+        else:
+            rec, _, _ = t.select_recipe(dirs, rho)
+            st = t.execute_merge(rec, str(out), t.MergeOptions(workers=cores))
         dt = time.perf_counter() - t0
         comp = st.bytes_moved
         shutil.rmtree(out, ignore_errors=True)
@@ -841,6 +846,7 @@ def our_arm(args, rank, world, local_rank):
             cores = os.cpu_count() or 1
             dt, comp, _ = run_reference_sample(work, cores, args.workload)
             ours_dt, ours_comp = run_files_sample(work, args.workload, cores)
+            two_dt, _ = run_files_sample(work, args.workload, cores, combined=False)
             line["cpu_baseline"] = {"value": round(comp / dt / 1e9, 4), "unit": "GB/s", "cores": cores,
                                     "kind": "reference",
                                     "sample": f"reference select-merge on {sample_text(args.workload)}, "
@@ -850,11 +856,13 @@ def our_arm(args, rank, world, local_rank):
                 line["cpu_baseline"]["workers_1"] = {"value": round(comp1 / dt1 / 1e9, 4), "unit": "GB/s", "cores": 1,
                                                      "seconds": round(dt1, 2)}
             line["same_sample_files"] = {
-                "what": "the cpu_baseline sample through OUR files drop-in (tg_select_recipe -> tg_execute_merge: "
-                        "device scorer, device gather, device re-verify) on the same snapshot files",
+                "what": "the cpu_baseline sample through OUR files drop-in (tg_select_merge: device scorer whose "
+                        "master copies feed the merge, device gather, device re-verify) on the same snapshot files",
                 "sample": sample_text(args.workload), "value": round(ours_comp / ours_dt / 1e9, 4), "unit": "GB/s",
                 "seconds": round(ours_dt, 3), "reference_value": round(comp / dt / 1e9, 4),
-                "speedup_vs_reference": round((ours_comp / ours_dt) / (comp / dt), 1)}
+                "speedup_vs_reference": round((ours_comp / ours_dt) / (comp / dt), 1),
+                "two_calls": {"what": "tg_select_recipe then tg_execute_merge", "value": round(ours_comp / two_dt / 1e9, 4),
+                              "seconds": round(two_dt, 3)}}
         finally:
             shutil.rmtree(work, ignore_errors=True)
     print(json.dumps(line))
@@ -1475,14 +1483,18 @@ def files_arm(args):
         master_bytes = K * sum(hi - lo for r in range(N) for lo, hi in master_byte_ranges(fam, r, K))
         probe = disk_probe(work)
 
-        def one(i, tag, io="auto", cold=False):
+        def one(i, tag, io="auto", cold=False, combined=False):
             if cold:
                 evict_files(src_files)
             out = work / f"ours-{tag}-{i}"
             t0 = time.perf_counter()
-            rec, _, gap = t.select_recipe(dirs, rho)
-            t1 = time.perf_counter()
-            st = t.execute_merge(rec, str(out), t.MergeOptions(workers=cores, io_mode=io))
+            if combined:  # tg_select_merge: the scorer's master copies feed the merge
+                _, _, gap, st = t.select_merge(dirs, str(out), rho, t.MergeOptions(workers=cores, io_mode=io))
+                t1 = time.perf_counter() - st.wall_ms / 1e3
+            else:
+                rec, _, gap = t.select_recipe(dirs, rho)
+                t1 = time.perf_counter()
+                st = t.execute_merge(rec, str(out), t.MergeOptions(workers=cores, io_mode=io))
             dt = time.perf_counter() - t0
             shutil.rmtree(out, ignore_errors=True)
             os.sync()  # the composite's writeback stays out of the next step
@@ -1496,11 +1508,22 @@ def files_arm(args):
             if i >= args.warmup:
                 warm.append(dt)
                 phases = ph
+        # the combined call while the page cache is still warm (the cold steps below drop it)
+        sm_warm, sm_res = [], 0
+        for i in range(args.warmup + args.steps):
+            dt, st, _, _ = one(i, "smwarm", combined=True)
+            sm_res = st.resident_bytes
+            if i >= args.warmup:
+                sm_warm.append(dt)
         cold_steps = max(1, min(args.steps, 3))
         for i in range(cold_steps):
             dt, cold_st, _, cph = one(i, "cold", cold=True)
             cold.append(dt)
         cold_buf, _, _, _ = one(0, "coldbuf", io="buffered", cold=True)
+        sm_cold = []
+        for i in range(cold_steps):
+            dt, _, _, _ = one(i, "smcold", cold=True, combined=True)
+            sm_cold.append(dt)
         ref_steps = max(1, min(args.steps, 3))
         refs = []
         for i in range(1 + ref_steps):
@@ -1535,6 +1558,17 @@ def files_arm(args):
                      "achieved_gbs_composite": round(o_v, 3), "read_bytes_per_step": master_bytes + 2 * comp,
                      "write_bytes_per_step": comp, "peak_read_gbs": rw, "peak_write_gbs": wc,
                      "floor_ms": round(floor * 1e3, 1), "frac": round(floor / w_s, 4)}
+    sm_w, sm_c = statistics.median(sm_warm), statistics.median(sm_cold)
+    sm_line = {"what": "tg_select_merge (one call; the masters the scorer read stay on the device and feed the "
+                       "merge: resident_bytes are not read again)",
+               "resident_bytes": sm_res,
+               "warm": {"value": round(comp / sm_w / 1e9, 4), "ms_per_step": round(sm_w * 1e3, 1)},
+               "cold": {"value": round(comp / sm_c / 1e9, 4), "ms_per_step": round(sm_c * 1e3, 1)}}
+    if rd:  # what must come off the device now: every snapshot's masters + the composite minus the kept masters
+        sm_bytes = disk_bytes - sm_res
+        sm_line["cold"]["roofline"] = {"bound": "device read (O_DIRECT, tools/disk_probe)", "peak": rd, "unit": "GB/s",
+                                       "bytes_per_step": sm_bytes, "floor_ms": round(sm_bytes / (rd * 1e9) * 1e3, 1),
+                                       "frac": round(sm_bytes / (rd * 1e9) / sm_c, 4)}
     print(json.dumps({
         "metric": "composite-checkpoint merge GB/s on files (score+select+merge+re-verify)",
         "value": round(o_v, 4), "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -1550,6 +1584,7 @@ def files_arm(args):
                  "direct_read_bytes": cold_st.direct_read_bytes if cold_st else None, "last_step_phases": cph,
                  "roofline": cold_roof,
                  "buffered_reads_same_state": {"value": round(comp / cold_buf / 1e9, 4), "ms_per_step": round(cold_buf * 1e3, 1)}},
+        "select_merge": sm_line,
         "disk_probe": probe,
         "reference": {"value": round(r_v, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
                       "ms_per_step": round(statistics.median(refs) * 1e3, 1), "page_cache": "warm"},

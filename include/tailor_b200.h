@@ -85,6 +85,7 @@ typedef struct tg_merge_stats {
     uint64_t bytes_moved;
     uint64_t direct_read_bytes;  /* source bytes read with O_DIRECT */
     uint64_t direct_write_bytes; /* output bytes written with O_DIRECT (whole 4 KB blocks) */
+    uint64_t resident_bytes;     /* source bytes gathered from device copies instead of read (tg_select_merge) */
 } tg_merge_stats;
 
 /* K2 segment: dst[dst_off, dst_off+bytes) <- src[0, bytes). */
@@ -181,6 +182,15 @@ int tg_score_snapshots(const char* const* dirs, int32_t n, const int32_t* device
  * R/src/merge.cpp:375-417). source_of[m] = index into dirs. */
 int tg_select_recipe(const char* const* dirs, int32_t n, double rho, const int32_t* devices, int32_t num_devices,
                      char* yaml_out, size_t cap, size_t* needed, int32_t* source_of, double* min_boundary_gap);
+/* tg_select_recipe + tg_execute_merge in one call: when the snapshots' packed masters
+ * fit the device budget of a single-device run, the scorer keeps them on the device and
+ * the merge gathers the composite's masters from there instead of reading them again
+ * (stats->resident_bytes); otherwise it is exactly the two calls. Same output bytes, same
+ * recipe (yaml_out, copied when it fits `cap`; *needed = its size + 1 either way), same
+ * errors. The options' device list serves both steps. */
+int tg_select_merge(const char* const* dirs, int32_t n, double rho, const char* out_dir, const tg_merge_options* options,
+                    tg_merge_stats* stats, char* yaml_out, size_t cap, size_t* needed, int32_t* source_of,
+                    double* min_boundary_gap);
 /* parse_config_json (R/src/checkpoint.cpp:123-136): model config.json text -> spec. */
 int tg_parse_config(const char* config_json, tg_model_spec* spec);
 /* Layer map (R/src/model.cpp, R/src/groups.cpp, R/src/shard.cpp) as JSON. */

@@ -61,7 +61,8 @@ class MergeOptionsC(ctypes.Structure):
 class MergeStatsC(ctypes.Structure):
     _fields_ = [("shard_files_read", ctypes.c_int64), ("weight_files_read", ctypes.c_int64),
                 ("wall_ms", ctypes.c_double), ("device_ms", ctypes.c_double), ("bytes_moved", ctypes.c_uint64),
-                ("direct_read_bytes", ctypes.c_uint64), ("direct_write_bytes", ctypes.c_uint64)]
+                ("direct_read_bytes", ctypes.c_uint64), ("direct_write_bytes", ctypes.c_uint64),
+                ("resident_bytes", ctypes.c_uint64)]
 
 
 class TrainConfigC(ctypes.Structure):
@@ -120,6 +121,8 @@ SIGNATURES = {
                                 _c.POINTER(_I32)]),
     "tg_select_recipe": (_I, [_c.POINTER(_S), _I32, _D, _c.POINTER(_I32), _I32, _c.c_char_p, _SZ, _PSZ,
                               _c.POINTER(_I32), _c.POINTER(_D)]),
+    "tg_select_merge": (_I, [_c.POINTER(_S), _I32, _D, _S, _c.POINTER(MergeOptionsC), _c.POINTER(MergeStatsC),
+                             _c.c_char_p, _SZ, _PSZ, _c.POINTER(_I32), _c.POINTER(_D)]),
     "tg_layer_map": (_I, [_c.POINTER(ModelSpecC), _I32, _c.c_char_p, _SZ, _PSZ]),
     "tg_parse_config": (_I, [_S, _c.POINTER(ModelSpecC)]),
     "tg_gather": (_I, [_P, _U32, _P, _U64, _I32, _I32, _P]),

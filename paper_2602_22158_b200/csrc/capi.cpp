@@ -174,6 +174,11 @@ struct PackedLoader {
     double read_ms = 0.0, load_ms = 0.0;
     std::uint64_t direct_bytes = 0;
     static constexpr std::uint64_t kHalf = 16ull << 20;
+    struct LoadedEntry {
+        std::uint64_t begin, end; // payload-relative master entry in the file
+        std::uint64_t packed;     // its offset in the packed destination
+    };
+    std::vector<LoadedEntry> last_entries; // of the last load()
 
     ReadPool pool;
 
@@ -203,6 +208,8 @@ struct PackedLoader {
             offs.push_back(total);
             total = (total + e->bytes() + 15) & ~15ull;
         }
+        last_entries.clear();
+        for (const auto& [e, at] : where) last_entries.push_back({e->begin, e->end, at});
         const int fd = ::open(p.c_str(), O_RDONLY);
         if (fd < 0) fail(ErrorKind::MissingArtifact, "cannot open '" + p.string() + "'");
         // snapshots not in the page cache are read with O_DIRECT (tailor/io.hpp; TAILOR_IO overrides)
@@ -226,9 +233,10 @@ struct PackedLoader {
             return pool.submit(jobs, p.string());
         };
         try {
+            const bool ahead = read_lookahead();
             std::uint64_t ticket = nh ? queue_half(0) : 0;
             for (std::uint64_t h = 0; h < nh; ++h) {
-                const std::uint64_t next = h + 1 < nh ? queue_half(h + 1) : 0;
+                const std::uint64_t next = ahead && h + 1 < nh ? queue_half(h + 1) : 0;
                 const double r0 = clock_ms();
                 pool.wait(ticket);
                 read_ms += clock_ms() - r0;
@@ -239,7 +247,7 @@ struct PackedLoader {
                            "H2D");
                 cuda_check(cudaEventRecord(half_done[b], st), "event");
                 used[b] = true;
-                ticket = next;
+                ticket = ahead ? next : (h + 1 < nh ? queue_half(h + 1) : 0);
             }
             half = static_cast<int>((static_cast<std::uint64_t>(half) + nh) & 1);
         } catch (...) {
@@ -258,8 +266,12 @@ struct PackedLoader {
 
 // Device scores over snapshot directories: per rank, packed masters -> K3/K4;
 // ranks combined in rank order on the host (FP64, fixed order).
+// keep (optional): when every snapshot of every rank fits the budget of a single-device
+// run, the packed masters stay in *keep_mem afterwards and *keep maps each (snapshot dir,
+// rank) master entry to its device copy (tg_select_merge hands them to the merge).
 void score_dirs(const std::vector<std::string>& dirs, const std::vector<int>& devices, std::vector<std::vector<double>>& sd,
-                std::vector<std::vector<double>>& sr, std::vector<CheckpointSummary>& sums) {
+                std::vector<std::vector<double>>& sr, std::vector<CheckpointSummary>& sums, ResidentSources* keep = nullptr,
+                DeviceBuffer* keep_mem = nullptr) {
     if (dirs.size() < 2) fail(ErrorKind::Recipe, "scoring needs at least two snapshots");
     // the CUDA context comes up while the sidecars are parsed (a fresh process pays
     // hundreds of ms for it)
@@ -308,7 +320,10 @@ void score_dirs(const std::vector<std::string>& dirs, const std::vector<int>& de
     const bool all_resident = stride * static_cast<std::uint64_t>(K) <= budget;
     const int slots = all_resident ? K
                                    : static_cast<int>(std::clamp<std::uint64_t>(budget / stride, 2, static_cast<std::uint64_t>(dev::kMaxSnapshots)));
-    const std::uint64_t per_lane = stride * static_cast<std::uint64_t>(slots);
+    const std::uint64_t all_bytes = stride * static_cast<std::uint64_t>(K) * static_cast<std::uint64_t>(N);
+    const bool keep_all = keep && keep_mem && devices.size() == 1 && all_resident && all_bytes <= budget;
+    if (keep_all) keep_mem->resize(all_bytes); // one slot per (rank, snapshot), kept after scoring
+    const std::uint64_t per_lane = keep_all ? stride : stride * static_cast<std::uint64_t>(slots);
     if (per_lane > budget && !std::getenv("TAILOR_DEVICE_BUDGET"))
         fail(ErrorKind::Device, "scoring needs " + std::to_string(per_lane) + " B of device memory for two snapshots of one rank; " +
                                     std::to_string(budget) + " B available");
@@ -331,7 +346,7 @@ void score_dirs(const std::vector<std::string>& dirs, const std::vector<int>& de
             cudaStream_t st = nullptr;
             cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
             std::unique_ptr<CUstream_st, decltype(&cudaStreamDestroy)> own(st, &cudaStreamDestroy);
-            DeviceBuffer dout(nres * sizeof(double)), arena(per_lane);
+            DeviceBuffer dout(nres * sizeof(double)), arena(keep_all ? 0 : per_lane);
             PackedLoader loader(st, readers);
             std::map<int, std::unique_ptr<ScorePlan>> plans; // by window length (offsets are rank-independent)
             for (int r = next.fetch_add(1); r < N; r = next.fetch_add(1)) {
@@ -343,9 +358,19 @@ void score_dirs(const std::vector<std::string>& dirs, const std::vector<int>& de
                 loader.read_ms = loader.load_ms = 0.0;
                 const double t0 = clock_ms();
                 std::vector<std::uint64_t> offs;
-                const auto slot_of = [&](int k) { return arena.get() + static_cast<std::uint64_t>(k % slots) * stride; };
+                const auto slot_of = [&](int k) {
+                    return keep_all ? keep_mem->get() + (static_cast<std::uint64_t>(r) * K + static_cast<std::uint64_t>(k)) * stride
+                                    : arena.get() + static_cast<std::uint64_t>(k % slots) * stride;
+                };
                 const auto load = [&](int k) {
                     loader.load(ckpt_file(CkptFile::Shard, dirs[static_cast<std::size_t>(k)], r), fields, slot_of(k), offs);
+                    if (keep_all) {
+                        std::vector<ResidentRange> rr;
+                        for (const auto& e : loader.last_entries) rr.push_back({e.begin, e.end, slot_of(k) + e.packed});
+                        std::sort(rr.begin(), rr.end(), [](const ResidentRange& a, const ResidentRange& b) { return a.lo < b.lo; });
+                        std::lock_guard<std::mutex> lk(mu);
+                        keep->ranges[{fs::path(dirs[static_cast<std::size_t>(k)]).lexically_normal().string(), r}] = std::move(rr);
+                    }
                 };
                 const auto score = [&](int k0, int k1) { // snapshots k0..k1 resident, pairs k0..k1-1
                     const int n = k1 - k0 + 1;
@@ -392,6 +417,7 @@ void score_dirs(const std::vector<std::string>& dirs, const std::vector<int>& de
     }
     cuda_check(cudaSetDevice(devices.front()), "cudaSetDevice");
     if (lane_err) std::rethrow_exception(lane_err);
+    if (keep_all) keep->device = devices.front();
     for (int r = 0; r < N; ++r) {
         const auto& h = res[static_cast<std::size_t>(r)];
         for (int p = 0; p < K - 1; ++p)
@@ -427,6 +453,7 @@ void put_stats(const MergeStats& s, tg_merge_stats* st) {
     st->bytes_moved = s.bytes_moved;
     st->direct_read_bytes = s.direct_read_bytes;
     st->direct_write_bytes = s.direct_write_bytes;
+    st->resident_bytes = s.resident_bytes;
 }
 
 std::vector<int> device_list(const int32_t* devices, int32_t n) {
@@ -589,6 +616,36 @@ int tg_select_recipe(const char* const* dirs, int32_t n, double rho, const int32
             for (std::size_t m = 0; m < sel.source_of.size(); ++m) source_of[m] = sel.source_of[m];
         if (min_gap) *min_gap = sel.min_boundary_gap;
         put_text(recipe_to_yaml(recipe_from_selection(summ, sel)), out, cap, needed);
+    });
+}
+
+int tg_select_merge(const char* const* dirs, int32_t n, double rho, const char* out_dir, const tg_merge_options* o,
+                    tg_merge_stats* st, char* out, size_t cap, size_t* needed, int32_t* source_of, double* min_gap) {
+    return guard([&] {
+        const MergeOptions opt = merge_options(o);
+        const fs::path dst = out_dir ? out_dir : "";
+        std::error_code ec;
+        if (fs::exists(dst) && !fs::is_empty(dst, ec)) // fail before any device work, as execute_merge would
+            fail(ErrorKind::Storage, "refusing to write into non-empty directory '" + dst.string() + "'");
+        std::vector<std::string> ds(dirs, dirs + n);
+        std::vector<std::vector<double>> sd, sr;
+        std::vector<CheckpointSummary> summ;
+        ResidentSources keep;
+        DeviceBuffer keep_mem;
+        score_dirs(ds, lane_devices(opt), sd, sr, summ, &keep, &keep_mem);
+        std::vector<std::vector<double>> sc = sd;
+        for (std::size_t p = 0; p < sd.size(); ++p)
+            for (std::size_t m = 0; m < sd[p].size(); ++m) sc[p][m] = magnitude_score(sd[p][m], sr[p][m]);
+        const Selection sel = select_by_magnitude(sc, static_cast<int>(sd.front().size()), rho);
+        if (source_of)
+            for (std::size_t m = 0; m < sel.source_of.size(); ++m) source_of[m] = sel.source_of[m];
+        if (min_gap) *min_gap = sel.min_boundary_gap;
+        const std::string yaml = recipe_to_yaml(recipe_from_selection(summ, sel));
+        if (needed) *needed = yaml.size() + 1; // the merge runs whether or not the recipe fits yaml_out
+        if (out && cap >= yaml.size() + 1) std::memcpy(out, yaml.c_str(), yaml.size() + 1);
+        const MergePlan plan = resolve_plan(parse_recipe(yaml));
+        const MergeStats s = execute_merge(plan, dst, opt, keep.ranges.empty() ? nullptr : &keep);
+        if (st) put_stats(s, st);
     });
 }
 

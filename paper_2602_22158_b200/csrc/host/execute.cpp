@@ -90,7 +90,10 @@ class FileAssembler {
     std::uint64_t bytes = 0, direct_read_bytes = 0, direct_write_bytes = 0;
     void set_read_threads(int n) { pool_.grow(std::max(1, n)); }
 
-    void assemble(const PartitionPlan& pp, const std::vector<fs::path>& window_files, const fs::path& out_path) {
+    // resident[w] (may be empty): window-relative byte ranges of window w already on the
+    // device (ResidentSources); those bytes are gathered from there, not read.
+    void assemble(const PartitionPlan& pp, const std::vector<fs::path>& window_files, const fs::path& out_path,
+                  const std::vector<std::vector<ResidentRange>>& resident = {}) {
         Fd out(out_path, O_WRONLY | O_CREAT | O_TRUNC);
         if (out.fd < 0) fail(ErrorKind::Storage, "cannot create '" + out_path.string() + "'");
         const std::string prefix = pp.out.prefix();
@@ -120,7 +123,7 @@ class FileAssembler {
             dwrite = dout->fd >= 0;
         }
         const std::uint64_t head = dwrite ? base % kDirectAlign : 0; // header bytes that ride in chunk 0
-        HostMergeChunks plan(pp, chunk_, dwrite ? chunk_ - head : chunk_, file_off, direct);
+        HostMergeChunks plan(pp, chunk_, dwrite ? chunk_ - head : chunk_, file_off, direct, resident);
         for (int i = 0; i < kSlots; ++i) {
             // one pinned buffer per slot carries the chunk both ways: the D2H of the
             // gathered chunk lands in it after its H2D has completed (same stream)
@@ -197,16 +200,28 @@ class FileAssembler {
             cv.wait(lk, [&] { return written + kSlots > ci || werr; });
             return !werr;
         };
+        // A chunk's reads are queued as soon as its slot is free: before the previous chunk's
+        // reads are waited for when the slot is already free then (no blocking for it), else
+        // at the top of its own iteration (as without lookahead).
+        const auto slot_is_free = [&](std::size_t ci) {
+            std::lock_guard<std::mutex> lk(mu);
+            return written + kSlots > ci;
+        };
+        const bool lookahead = read_lookahead();
         try {
             const std::size_t nchunks = plan.chunks.size();
-            bool go = nchunks > 0 && slot_free(0);
-            if (go) ticket[0] = queue_reads(plan.chunks[0], pp, window_files, file_off, fds, dfds, 0, out_path);
-            for (std::size_t ci = 0; go && ci < nchunks; ++ci) {
+            std::size_t queued = 0; // chunks [0, queued) have their reads queued
+            for (std::size_t ci = 0; ci < nchunks; ++ci) {
                 const int slot = static_cast<int>(ci % kSlots);
-                if (ci + 1 < nchunks) {
-                    if (!slot_free(ci + 1)) break;
+                if (queued == ci) {
+                    if (!slot_free(ci)) break;
+                    ticket[slot] = queue_reads(plan.chunks[ci], pp, window_files, file_off, fds, dfds, slot, out_path);
+                    queued = ci + 1;
+                }
+                if (lookahead && ci + 1 < nchunks && queued == ci + 1 && slot_is_free(ci + 1)) {
                     const int ns = static_cast<int>((ci + 1) % kSlots);
                     ticket[ns] = queue_reads(plan.chunks[ci + 1], pp, window_files, file_off, fds, dfds, ns, out_path);
+                    queued = ci + 2;
                 }
                 {
                     ScopedAccum acc(read_ms);
@@ -276,7 +291,7 @@ class FileAssembler {
         auto* segs = reinterpret_cast<dev::GatherSeg*>(pin_segs_[slot].get());
         for (std::size_t i = 0; i < c.segs.size(); ++i) {
             segs[i] = c.segs[i];
-            segs[i].src = d_in_[slot].get() + reinterpret_cast<std::uintptr_t>(c.segs[i].src);
+            if (!c.abs[i]) segs[i].src = d_in_[slot].get() + reinterpret_cast<std::uintptr_t>(c.segs[i].src);
         }
         cuda_check(cudaMemcpyAsync(d_segs_[slot].get(), segs, c.segs.size() * sizeof(dev::GatherSeg), cudaMemcpyHostToDevice, s),
                    "segs");
@@ -297,7 +312,8 @@ class FileAssembler {
     struct ChunkPlan {
         std::uint64_t lo, hi, staging = 0;
         std::vector<Read> reads;
-        std::vector<dev::GatherSeg> segs; // src = staging offset
+        std::vector<dev::GatherSeg> segs; // src = staging offset, or a device address where abs[i]
+        std::vector<std::uint8_t> abs;    // 1: the segment reads resident device bytes
         bool bulk_ok = true;
     };
     struct HostMergeChunks {
@@ -308,7 +324,8 @@ class FileAssembler {
         // 4 KB blocks of the output file); direct[w]: window w is read with O_DIRECT,
         // so its reads are staged congruent to file_off[w] + src mod 4 KB
         HostMergeChunks(const PartitionPlan& pp, std::uint64_t chunk, std::uint64_t first,
-                        const std::vector<std::uint64_t>& file_off, const std::vector<char>& direct) {
+                        const std::vector<std::uint64_t>& file_off, const std::vector<char>& direct,
+                        const std::vector<std::vector<ResidentRange>>& resident) {
             const std::uint64_t total = pp.dst_hi - pp.dst_lo;
             first = std::max<std::uint64_t>(1, first);
             std::size_t si = 0;
@@ -319,22 +336,42 @@ class FileAssembler {
                 struct P {
                     std::uint32_t w;
                     std::uint64_t src, dst, n;
+                    const std::uint8_t* dev = nullptr; // resident: gathered from here, not read
                 };
                 std::vector<P> ps;
+                const auto push = [&](std::uint32_t w, std::uint64_t src, std::uint64_t dst, std::uint64_t n) {
+                    // split at the window's resident ranges (sorted, disjoint)
+                    if (w < resident.size())
+                        for (const auto& r : resident[w]) {
+                            if (r.hi <= src) continue;
+                            if (r.lo >= src + n) break;
+                            if (r.lo > src) { // a non-resident gap first
+                                const std::uint64_t g = r.lo - src;
+                                ps.push_back({w, src, dst, g});
+                                src += g, dst += g, n -= g;
+                            }
+                            const std::uint64_t k = std::min(n, r.hi - src);
+                            ps.push_back({w, src, dst, k, r.dev + (src - r.lo)});
+                            src += k, dst += k, n -= k;
+                            if (!n) return;
+                        }
+                    ps.push_back({w, src, dst, n});
+                };
                 while (si < pp.segments.size() && pp.segments[si].dst_off + pp.segments[si].bytes - pp.dst_lo <= c.lo) ++si;
                 for (std::size_t j = si; j < pp.segments.size(); ++j) {
                     const auto& s = pp.segments[j];
                     const std::uint64_t d0 = s.dst_off - pp.dst_lo, d1 = d0 + s.bytes;
                     if (d0 >= c.hi) break;
                     const std::uint64_t a = std::max(d0, c.lo), b = std::min(d1, c.hi);
-                    if (a < b) ps.push_back({s.window, s.src_off + (a - d0), a, b - a});
+                    if (a < b) push(s.window, s.src_off + (a - d0), a, b - a);
                 }
-                std::vector<std::size_t> order(ps.size());
-                for (std::size_t i = 0; i < ps.size(); ++i) order[i] = i;
+                std::vector<std::size_t> order;
+                for (std::size_t i = 0; i < ps.size(); ++i)
+                    if (!ps[i].dev) order.push_back(i); // only non-resident pieces are read
                 std::sort(order.begin(), order.end(), [&](std::size_t x, std::size_t y) {
                     return ps[x].w != ps[y].w ? ps[x].w < ps[y].w : ps[x].src < ps[y].src;
                 });
-                std::vector<std::uint64_t> at_of(ps.size());
+                std::vector<std::uint64_t> at_of(ps.size(), 0);
                 std::uint64_t at = 0;
                 for (std::size_t i : order) {
                     const P& p = ps[i];
@@ -364,8 +401,11 @@ class FileAssembler {
                 c.staging = ceil_blk(at);
                 std::uint64_t expect = c.lo;
                 for (std::size_t i = 0; i < ps.size(); ++i) {
-                    c.segs.push_back({reinterpret_cast<const std::uint8_t*>(at_of[i]), ps[i].dst - c.lo, ps[i].n});
-                    c.bulk_ok = c.bulk_ok && ps[i].dst == expect && at_of[i] % 16 == 0 && ps[i].n % 16 == 0 &&
+                    const bool res = ps[i].dev != nullptr;
+                    const std::uintptr_t src = res ? reinterpret_cast<std::uintptr_t>(ps[i].dev) : at_of[i];
+                    c.segs.push_back({reinterpret_cast<const std::uint8_t*>(src), ps[i].dst - c.lo, ps[i].n});
+                    c.abs.push_back(res ? 1 : 0);
+                    c.bulk_ok = c.bulk_ok && ps[i].dst == expect && src % 16 == 0 && ps[i].n % 16 == 0 &&
                                 (ps[i].dst - c.lo) % 16 == 0;
                     expect = ps[i].dst + ps[i].n;
                 }
@@ -413,6 +453,7 @@ struct OutputJob {
     std::vector<fs::path> window_files;
     fs::path out;
     int tag = 0; // passed to on_done: -1 = weights, r >= 0 = rank-r shard file
+    std::vector<std::vector<ResidentRange>> resident; // per window, window-relative (may be empty)
 };
 
 struct AssembleTotals {
@@ -462,7 +503,7 @@ AssembleTotals assemble_outputs(std::vector<OutputJob> jobs, int workers, bool u
                 fa.set_read_threads(jobs[j].tag < 0 ? std::max(readers, 4) : readers);
                 if (jobs[j].tag < 0 && fault_injected("assemble-weights"))
                     fail(ErrorKind::Storage, "injected fault (TAILOR_FAULT=assemble-weights): " + jobs[j].out.string());
-                fa.assemble(*jobs[j].plan, jobs[j].window_files, jobs[j].out);
+                fa.assemble(*jobs[j].plan, jobs[j].window_files, jobs[j].out, jobs[j].resident);
                 if (on_done) on_done(jobs[j].tag);
             }
             part[static_cast<std::size_t>(li)] = {fa.device_ms, fa.read_ms,  fa.wait_ms,           fa.write_ms,
@@ -672,6 +713,11 @@ class LaneVerifier {
 } // namespace
 
 MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const MergeOptions& options) {
+    return execute_merge(plan, out_dir, options, nullptr);
+}
+
+MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const MergeOptions& options,
+                         const ResidentSources* resident) {
     const auto t0 = std::chrono::steady_clock::now();
     MergeStats stats;
     const std::vector<int> devices = lane_devices(options);
@@ -742,16 +788,37 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
 
     std::vector<OutputJob> jobs;
     {
-        OutputJob j{&wplan, {}, ckpt_file(CkptFile::Weights, out_dir), -1};
+        OutputJob j{&wplan, {}, ckpt_file(CkptFile::Weights, out_dir), -1, {}};
         for (const auto& w : wplan.windows) j.window_files.push_back(ckpt_file(CkptFile::Weights, w.source));
         jobs.push_back(std::move(j));
     }
+    // resident source bytes are usable when every lane runs on their device
+    const bool use_resident = resident && !resident->ranges.empty() && devices.size() == 1 && devices.front() == resident->device;
+    std::uint64_t resident_bytes = 0;
     for (int r = 0; r < plan.num_ranks; ++r) {
         const PartitionPlan& sp = splans[static_cast<std::size_t>(r)];
-        OutputJob j{&sp, {}, ckpt_file(CkptFile::Shard, out_dir, r), r};
+        OutputJob j{&sp, {}, ckpt_file(CkptFile::Shard, out_dir, r), r, {}};
         for (const auto& w : sp.windows) j.window_files.push_back(ckpt_file(CkptFile::Shard, w.source, w.container));
+        if (use_resident) {
+            j.resident.resize(sp.windows.size());
+            for (std::size_t wi = 0; wi < sp.windows.size(); ++wi) {
+                const SourceWindow& w = sp.windows[wi];
+                const auto it = resident->ranges.find({fs::path(w.source).lexically_normal().string(), w.container});
+                if (it == resident->ranges.end()) continue;
+                for (const ResidentRange& rr : it->second) { // payload-relative -> window-relative
+                    const std::uint64_t lo = std::max(rr.lo, w.lo), hi = std::min(rr.hi, w.hi);
+                    if (lo < hi) j.resident[wi].push_back({lo - w.lo, hi - w.lo, rr.dev + (lo - rr.lo)});
+                }
+            }
+            for (const auto& seg : sp.segments) // bytes the plan will take from the device
+                for (const auto& rr : j.resident[seg.window]) {
+                    const std::uint64_t lo = std::max(rr.lo, seg.src_off), hi = std::min(rr.hi, seg.src_off + seg.bytes);
+                    if (lo < hi) resident_bytes += hi - lo;
+                }
+        }
         jobs.push_back(std::move(j));
     }
+    trace_count("merge.resident_source_bytes", static_cast<double>(resident_bytes));
 
     LaneVerifier lv(out_dir, &wplan, splans, workers, options.verify, devices);
     const IoMode io = io_mode_from_env(options.io);
@@ -766,6 +833,7 @@ MergeStats execute_merge(const MergePlan& plan, const fs::path& out_dir, const M
 
     stats.device_ms = fa.device_ms;
     stats.bytes_moved = fa.bytes;
+    stats.resident_bytes = resident_bytes;
     stats.direct_read_bytes = fa.direct_read_bytes;
     stats.direct_write_bytes = fa.direct_write_bytes;
     stats.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -899,9 +967,10 @@ MergeStats execute_regroup(const fs::path& src, const fs::path& out_dir, Groupin
         return files;
     };
     std::vector<OutputJob> jobs;
-    jobs.push_back({&wp, files_of(wp), ckpt_file(CkptFile::Weights, out_dir), -1});
+    jobs.push_back({&wp, files_of(wp), ckpt_file(CkptFile::Weights, out_dir), -1, {}});
     for (int r = 0; r < N; ++r)
-        jobs.push_back({&plans[static_cast<std::size_t>(r)], files_of(plans[static_cast<std::size_t>(r)]), ckpt_file(CkptFile::Shard, out_dir, r), r});
+        jobs.push_back({&plans[static_cast<std::size_t>(r)], files_of(plans[static_cast<std::size_t>(r)]), ckpt_file(CkptFile::Shard, out_dir, r), r,
+                        {}});
     // sidecars first: the pipelined re-verify reads them back while the files assemble
     write_text_file(ckpt_file(CkptFile::OptimMeta, out_dir), sidecar_text(optim));
     write_text_file(ckpt_file(CkptFile::Config, out_dir), sidecar_text(spec));

@@ -219,6 +219,14 @@ void read_one(const ReadJob& p, const std::string& what) {
 }
 } // namespace
 
+bool read_lookahead() {
+    static const bool on = [] {
+        const char* v = std::getenv("TAILOR_READ_LOOKAHEAD");
+        return !(v && *v == '0');
+    }();
+    return on;
+}
+
 // ---- ReadPool ---------------------------------------------------------------------
 ReadPool::ReadPool(int threads) { grow(threads); }
 

@@ -38,6 +38,9 @@ void run_reads(const std::vector<ReadJob>& jobs, int threads, const std::string&
 // chunk while the current chunk's last pieces are still in flight: the device queue never
 // drains at chunk boundaries. Buffers and descriptors of a batch must outlive its wait()
 // (or drain()); the destructor finishes the queued pieces before joining.
+// TAILOR_READ_LOOKAHEAD=0 (measurement): queue a chunk's reads only when the previous
+// chunk's have completed, as a per-call read pool would.
+bool read_lookahead();
 class ReadPool {
   public:
     explicit ReadPool(int threads);

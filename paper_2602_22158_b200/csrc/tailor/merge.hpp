@@ -88,9 +88,25 @@ struct MergeStats {
     std::uint64_t bytes_moved = 0; // composite payload bytes
     std::uint64_t direct_read_bytes = 0;  // source bytes read with O_DIRECT
     std::uint64_t direct_write_bytes = 0; // output bytes written with O_DIRECT (whole blocks)
+    std::uint64_t resident_bytes = 0;     // source bytes gathered from device copies (ResidentSources), not read
 };
 
 MergeStats execute_merge(const MergePlan& plan, const std::filesystem::path& out_dir, const MergeOptions& options = {});
+
+// Source bytes already on the merge's device (the masters the scorer just read, in a
+// combined select+merge): payload-relative byte ranges of (source, container) that the
+// merge gathers from device memory instead of reading the file again. The output bytes
+// are the same; only fewer bytes come off the disk / cross PCIe.
+struct ResidentRange {
+    std::uint64_t lo = 0, hi = 0;       // payload-relative [lo, hi) in the source container
+    const std::uint8_t* dev = nullptr;  // device address of byte lo
+};
+struct ResidentSources {
+    int device = 0;
+    std::map<std::pair<std::string, int>, std::vector<ResidentRange>> ranges; // sorted by lo, disjoint
+};
+MergeStats execute_merge(const MergePlan& plan, const std::filesystem::path& out_dir, const MergeOptions& options,
+                         const ResidentSources* resident);
 
 // Re-slice a complete checkpoint between the coarse (2-group) and fine
 // (2L+3 / 2L+2) optimizer layouts (R/src/groups.cpp:152-220)

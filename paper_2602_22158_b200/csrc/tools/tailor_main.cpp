@@ -87,16 +87,10 @@ bool require(const Args& a, std::initializer_list<const char*> keys) {
     return true;
 }
 
-int cmd_merge(const Args& a) {
-    if (!require(a, {"recipe", "out"})) return 1;
-    bool ok = false;
-    const std::string yaml = read_file(a.kv.at("recipe"), &ok);
-    if (!ok) {
-        std::cerr << "error: MissingArtifact: cannot open '" << a.kv.at("recipe") << "'\n";
-        return 1;
-    }
-    tg_merge_options opt{};
-    const std::vector<int32_t> devs = devices_of(a);
+// --workers / --uncached / --devices / --no-verify / --io of merge and select-merge;
+// false (after the message) on an unknown --io mode.
+bool merge_options_of(const Args& a, const std::vector<int32_t>& devs, tg_merge_options& opt) {
+    opt = tg_merge_options{};
     opt.workers = a.kv.count("workers") ? std::stoi(a.kv.at("workers")) : 0;
     opt.uncached = a.flags.count("uncached") ? 1 : 0;
     opt.device = devs.front();
@@ -109,9 +103,23 @@ int cmd_merge(const Args& a) {
                       : m == "auto"   ? TG_IO_AUTO : -1;
         if (opt.io_mode < 0) {
             std::cerr << "error: unknown --io mode '" << m << "' (auto, buffered, direct, direct-rw)\n";
-            return 1;
+            return false;
         }
     }
+    return true;
+}
+
+int cmd_merge(const Args& a) {
+    if (!require(a, {"recipe", "out"})) return 1;
+    bool ok = false;
+    const std::string yaml = read_file(a.kv.at("recipe"), &ok);
+    if (!ok) {
+        std::cerr << "error: MissingArtifact: cannot open '" << a.kv.at("recipe") << "'\n";
+        return 1;
+    }
+    const std::vector<int32_t> devs = devices_of(a);
+    tg_merge_options opt{};
+    if (!merge_options_of(a, devs, opt)) return 1;
     tg_merge_stats st{};
     const int rc = tg_execute_merge(yaml.c_str(), a.kv.at("out").c_str(), &opt, &st);
     if (rc != TG_OK) return report(rc);
@@ -169,6 +177,34 @@ int cmd_select(const Args& a) {
     if (rc != TG_OK) return report(rc);
     if (int w = write_out(a.kv.at("out"), yaml)) return w;
     std::cout << yaml << "# min boundary gap " << gap << "\n";
+    return 0;
+}
+
+// select + merge in one call (tg_select_merge): the masters the scorer read stay on the
+// device for the merge when they fit; --recipe-out keeps the recipe it chose.
+int cmd_select_merge(const Args& a) {
+    if (!require(a, {"snapshots", "out"})) return 1;
+    const auto dirs = split_csv(a.kv.at("snapshots"));
+    std::vector<const char*> ptrs;
+    for (const auto& d : dirs) ptrs.push_back(d.c_str());
+    const double rho = a.kv.count("rho") ? std::stod(a.kv.at("rho")) : 0.5;
+    const std::vector<int32_t> devs = devices_of(a);
+    tg_merge_options opt{};
+    if (!merge_options_of(a, devs, opt)) return 1;
+    std::vector<int32_t> src(4096);
+    std::vector<char> yaml(1 << 20);
+    size_t need = 0;
+    double gap = 0.0;
+    tg_merge_stats st{};
+    const int rc = tg_select_merge(ptrs.data(), static_cast<int32_t>(ptrs.size()), rho, a.kv.at("out").c_str(), &opt, &st,
+                                   yaml.data(), yaml.size(), &need, src.data(), &gap);
+    if (rc != TG_OK) return report(rc);
+    if (a.kv.count("recipe-out"))
+        if (int w = write_out(a.kv.at("recipe-out"), std::string(yaml.data()))) return w;
+    std::cout << "merged checkpoint written to " << a.kv.at("out") << "\n";
+    std::cout << "composite bytes: " << st.bytes_moved << " (" << st.resident_bytes
+              << " gathered from the scorer's device copies)\n";
+    std::cout << "min boundary gap " << gap << "; wall time (merge): " << st.wall_ms << " ms\n";
     return 0;
 }
 
@@ -285,7 +321,7 @@ int cmd_check(const Args& a) {
 
 int main(int argc, char** argv) {
     if (argc < 2) {
-        std::cerr << "usage: tailor <merge|plan|select|score|check|regroup|train|resume> [options]\n";
+        std::cerr << "usage: tailor <merge|plan|select|select-merge|score|check|regroup|train|resume> [options]\n";
         return 1;
     }
     Args a;
@@ -304,6 +340,7 @@ int main(int argc, char** argv) {
         if (cmd == "merge") return cmd_merge(a);
         if (cmd == "plan") return cmd_plan(a);
         if (cmd == "select") return cmd_select(a);
+        if (cmd == "select-merge") return cmd_select_merge(a);
         if (cmd == "score") return cmd_score(a);
         if (cmd == "check") return cmd_check(a);
         if (cmd == "regroup") return cmd_regroup(a);

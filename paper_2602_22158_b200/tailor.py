@@ -26,7 +26,7 @@ from ._lib import (ErrorKind, GatherSegC, HostCopyC, MergeOptionsC, MergeStatsC,
 
 __all__ = ["ErrorKind", "TailorError", "ModelSpec", "RecipeSlice", "MergeRecipe", "MergeOptions", "MergeStats",
            "parse_recipe", "recipe_to_yaml", "resolve_plan", "execute_merge", "recipe_from_manifests",
-           "verify_checkpoint", "regroup", "train", "resume", "score_snapshots", "select_recipe", "layer_map", "SnapshotLayout", "SynthFamily", "Scorer",
+           "verify_checkpoint", "regroup", "train", "resume", "score_snapshots", "select_recipe", "select_merge", "layer_map", "SnapshotLayout", "SynthFamily", "Scorer",
            "MergePartition", "SelectStep", "Trainer", "Comm", "STRATEGIES", "gather", "read_probe"]
 
 
@@ -130,11 +130,12 @@ class MergeStats:
     bytes_moved: int
     direct_read_bytes: int = 0
     direct_write_bytes: int = 0
+    resident_bytes: int = 0  # source bytes gathered from device copies (select_merge), not read
 
     @classmethod
     def from_c(cls, st) -> "MergeStats":
         return cls(st.shard_files_read, st.weight_files_read, st.wall_ms, st.device_ms, st.bytes_moved,
-                   st.direct_read_bytes, st.direct_write_bytes)
+                   st.direct_read_bytes, st.direct_write_bytes, st.resident_bytes)
 
 
 def _b(s: str) -> bytes:
@@ -252,6 +253,26 @@ def select_recipe(dirs: Sequence[str], rho: float = 0.5, device: int = 0, device
         cfg = json.load(f)
     M = cfg["num_layers"] + (2 if cfg["weight_tied"] else 3)
     return rec, [src[i] for i in range(M)], gap.value
+
+
+def select_merge(dirs: Sequence[str], out_dir: str, rho: float = 0.5, options: Optional[MergeOptions] = None):
+    """select_recipe + execute_merge in one call (tg_select_merge): the masters the scorer
+    read stay on the device for the merge when they fit. Returns (recipe, source_of,
+    min_boundary_gap, MergeStats)."""
+    o = options or MergeOptions()
+    copt = o.to_c()
+    st = MergeStatsC()
+    src = (ctypes.c_int32 * 8192)()
+    gap = ctypes.c_double(0)
+    cap = 1 << 20
+    buf = ctypes.create_string_buffer(cap)
+    need = ctypes.c_size_t(0)
+    check(lib().tg_select_merge(_dirs_arg(dirs), len(dirs), rho, _b(str(out_dir)), ctypes.byref(copt), ctypes.byref(st),
+                                buf, cap, ctypes.byref(need), src, ctypes.byref(gap)))
+    with open(os.path.join(str(dirs[0]), "config.json")) as f:
+        cfg = json.load(f)
+    M = cfg["num_layers"] + (2 if cfg["weight_tied"] else 3)
+    return parse_recipe(buf.value.decode()), [src[i] for i in range(M)], gap.value, MergeStats.from_c(st)
 
 
 def layer_map(spec: ModelSpec, num_ranks: int = 1) -> dict:

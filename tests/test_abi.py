@@ -37,7 +37,7 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.GatherSegC) == 24
     assert ctypes.sizeof(_lib.ScoreTileC) == 24
     assert ctypes.sizeof(_lib.ModelSpecC) == 32
-    assert ctypes.sizeof(_lib.MergeStatsC) == 56
+    assert ctypes.sizeof(_lib.MergeStatsC) == 64
     assert ctypes.sizeof(_lib.MergeOptionsC) == 32
 
 

@@ -59,6 +59,13 @@ def select_merge_both(tmp: pathlib.Path, dirs, rho=0.5, workers=0):
     assert tree_digest(tmp / "ref_out") == tree_digest(tmp / "our_out")
     assert st.shard_files_read == ref["merge"]["stats"]["shard_files_read"]
     assert st.weight_files_read == ref["merge"]["stats"]["weight_files_read"]
+    # the combined call (tg_select_merge): the composite's masters come from the scorer's
+    # device copies, the bytes written are the reference's
+    rec2, src2, gap2, st2 = t.select_merge(dirs, str(tmp / "our_sm"), rho, t.MergeOptions(workers=workers))
+    assert rec2 == rec and src2 == src and gap2 == gap
+    assert tree_digest(tmp / "ref_out") == tree_digest(tmp / "our_sm")
+    assert st2.resident_bytes > 0
+    assert st2.shard_files_read == st.shard_files_read and st2.weight_files_read == st.weight_files_read
     return ref, rec, src
 
 

@@ -1,7 +1,8 @@
 #!/usr/bin/env python
-"""Phase trace (usage: files_trace.py [root_dir] [iters] [cold]) of the file-facing drop-in path (TAILOR_TRACE=1):
+"""Phase trace (usage: files_trace.py [root_dir] [iters] [cold|warm] [sm|two]) of the file-facing drop-in path (TAILOR_TRACE=1):
 medium shape L8 h1024 f2752 v32000, N=8, K=4 written to /tmp, then select_recipe + execute_merge. `cold`: the
-sources' pages are dropped before every iteration (fsync + POSIX_FADV_DONTNEED), as in bench.py's cold files line."""
+sources' pages are dropped before every iteration (fsync + POSIX_FADV_DONTNEED), as in bench.py's cold files line.
+`sm`: tg_select_merge (one call) instead of select_recipe + execute_merge."""
 import os
 import pathlib
 import shutil
@@ -17,6 +18,7 @@ import paper_2602_22158_b200 as t  # noqa: E402
 root = (sys.argv[1] or None) if len(sys.argv) > 1 else None  # e.g. /dev/shm (default: $TMPDIR or /tmp)
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 cold = len(sys.argv) > 3 and sys.argv[3] == "cold"
+combined = len(sys.argv) > 4 and sys.argv[4] == "sm"  # tg_select_merge instead of the two calls
 work = pathlib.Path(tempfile.mkdtemp(prefix="tailor-trace-", dir=root))
 try:
     fam = t.SynthFamily(t.ModelSpec(8, 1024, 2752, 32000, False, 42), 8, 4, 100)
@@ -39,10 +41,15 @@ try:
                 os.close(fd)
         print(f"iter {i} start: {dirty()}", file=sys.stderr, flush=True)
         t0 = time.perf_counter()
-        rec, _, _ = t.select_recipe(dirs, 0.5)
-        t1 = time.perf_counter()
-        st = t.execute_merge(rec, str(work / f"m{i}"))
-        t2 = time.perf_counter()
+        if combined:
+            _, _, _, st = t.select_merge(dirs, str(work / f"m{i}"), 0.5)
+            t2 = time.perf_counter()
+            t1 = t2 - st.wall_ms / 1e3
+        else:
+            rec, _, _ = t.select_recipe(dirs, 0.5)
+            t1 = time.perf_counter()
+            st = t.execute_merge(rec, str(work / f"m{i}"))
+            t2 = time.perf_counter()
         print(f"iter {i}: select {1e3 * (t1 - t0):.1f} ms, merge {1e3 * (t2 - t1):.1f} ms ({st.bytes_moved / 1e9:.2f} GB)",
               file=sys.stderr, flush=True)
         shutil.rmtree(work / f"m{i}")
