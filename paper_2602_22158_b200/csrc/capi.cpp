@@ -267,11 +267,12 @@ struct PackedLoader {
 // Device scores over snapshot directories: per rank, packed masters -> K3/K4;
 // ranks combined in rank order on the host (FP64, fixed order).
 // keep (optional): when every snapshot of every rank fits the budget of a single-device
-// run, the packed masters stay in *keep_mem afterwards and *keep maps each (snapshot dir,
-// rank) master entry to its device copy (tg_select_merge hands them to the merge).
+// run, the packed masters stay in (*keep_mem)[rank] afterwards (one pooled buffer per rank)
+// and *keep maps each (snapshot dir, rank) master entry to its device copy
+// (tg_select_merge hands them to the merge).
 void score_dirs(const std::vector<std::string>& dirs, const std::vector<int>& devices, std::vector<std::vector<double>>& sd,
                 std::vector<std::vector<double>>& sr, std::vector<CheckpointSummary>& sums, ResidentSources* keep = nullptr,
-                DeviceBuffer* keep_mem = nullptr) {
+                std::vector<DeviceBuffer>* keep_mem = nullptr) {
     if (dirs.size() < 2) fail(ErrorKind::Recipe, "scoring needs at least two snapshots");
     // the CUDA context comes up while the sidecars are parsed (a fresh process pays
     // hundreds of ms for it)
@@ -322,7 +323,7 @@ void score_dirs(const std::vector<std::string>& dirs, const std::vector<int>& de
                                    : static_cast<int>(std::clamp<std::uint64_t>(budget / stride, 2, static_cast<std::uint64_t>(dev::kMaxSnapshots)));
     const std::uint64_t all_bytes = stride * static_cast<std::uint64_t>(K) * static_cast<std::uint64_t>(N);
     const bool keep_all = keep && keep_mem && devices.size() == 1 && all_resident && all_bytes <= budget;
-    if (keep_all) keep_mem->resize(all_bytes); // one slot per (rank, snapshot), kept after scoring
+    if (keep_all) keep_mem->resize(static_cast<std::size_t>(N)); // per rank: K slots, kept after scoring
     const std::uint64_t per_lane = keep_all ? stride : stride * static_cast<std::uint64_t>(slots);
     if (per_lane > budget && !std::getenv("TAILOR_DEVICE_BUDGET"))
         fail(ErrorKind::Device, "scoring needs " + std::to_string(per_lane) + " B of device memory for two snapshots of one rank; " +
@@ -358,8 +359,9 @@ void score_dirs(const std::vector<std::string>& dirs, const std::vector<int>& de
                 loader.read_ms = loader.load_ms = 0.0;
                 const double t0 = clock_ms();
                 std::vector<std::uint64_t> offs;
+                if (keep_all) (*keep_mem)[static_cast<std::size_t>(r)].resize(stride * static_cast<std::uint64_t>(K));
                 const auto slot_of = [&](int k) {
-                    return keep_all ? keep_mem->get() + (static_cast<std::uint64_t>(r) * K + static_cast<std::uint64_t>(k)) * stride
+                    return keep_all ? (*keep_mem)[static_cast<std::size_t>(r)].get() + static_cast<std::uint64_t>(k) * stride
                                     : arena.get() + static_cast<std::uint64_t>(k % slots) * stride;
                 };
                 const auto load = [&](int k) {
@@ -379,6 +381,7 @@ void score_dirs(const std::vector<std::string>& dirs, const std::vector<int>& de
                     std::vector<const std::uint8_t*> bases;
                     for (int k = k0; k <= k1; ++k) bases.push_back(slot_of(k));
                     plan->run(bases.data(), dout.get<double>() + static_cast<std::size_t>(k0) * M * 2, st);
+                    if (sync_check()) cuda_check(cudaStreamSynchronize(st), "score (TAILOR_SYNC_CHECK)");
                 };
                 if (all_resident) {
                     for (int k = 0; k < K; ++k) load(k);
@@ -631,7 +634,7 @@ int tg_select_merge(const char* const* dirs, int32_t n, double rho, const char* 
         std::vector<std::vector<double>> sd, sr;
         std::vector<CheckpointSummary> summ;
         ResidentSources keep;
-        DeviceBuffer keep_mem;
+        std::vector<DeviceBuffer> keep_mem;
         score_dirs(ds, lane_devices(opt), sd, sr, summ, &keep, &keep_mem);
         std::vector<std::vector<double>> sc = sd;
         for (std::size_t p = 0; p < sd.size(); ++p)

@@ -152,8 +152,17 @@ void DeviceBuffer::resize(std::size_t n) {
 void DeviceBuffer::upload(const void* src, std::size_t n, cudaStream_t s) {
     resize(std::max<std::size_t>(n, 1));
     if (n == 0) return;
-    if (s) cuda_check(cudaMemcpyAsync(p_, src, n, cudaMemcpyHostToDevice, s), "upload");
-    else cuda_check(cudaMemcpy(p_, src, n, cudaMemcpyHostToDevice), "upload");
+    if (s) {
+        cuda_check(cudaMemcpyAsync(p_, src, n, cudaMemcpyHostToDevice, s), "upload"); // ordered before s's later work
+    } else {
+        // cudaMemcpy from pageable memory returns once the bytes are staged, before the DMA
+        // has landed, and the legacy stream it uses is not ordered with our non-blocking
+        // streams: without this sync a kernel launched right after on another stream can
+        // read the buffer's previous contents (a verify table with stale pointers -> an
+        // intermittent illegal address).
+        cuda_check(cudaMemcpy(p_, src, n, cudaMemcpyHostToDevice), "upload");
+        cuda_check(cudaStreamSynchronize(cudaStreamLegacy), "upload");
+    }
 }
 
 // Pinning pages costs ~0.4 s per GB, far more than the reads the staging
@@ -1163,8 +1172,8 @@ void verify_rank_resident(const VerifyPlan& plan, int r, const fs::path& shard_f
         x.weight = reinterpret_cast<const std::uint16_t*>(dw + reinterpret_cast<std::uintptr_t>(x.weight));
     }
     for (auto& x : rg) x.words = reinterpret_cast<const std::uint32_t*>(ds.get() + reinterpret_cast<std::uintptr_t>(x.words));
-    dpairs.upload(pr.data(), pr.size() * sizeof(dev::VerifyPair));
-    dranges.upload(rg.data(), rg.size() * sizeof(dev::VerifyRange));
+    dpairs.upload(pr.data(), pr.size() * sizeof(dev::VerifyPair), st); // on the verify stream: ordered before K6
+    dranges.upload(rg.data(), rg.size() * sizeof(dev::VerifyRange), st);
     cuda_check(dev::launch_verify(dpairs.get<dev::VerifyPair>(), static_cast<std::uint32_t>(pr.size()),
                                   dranges.get<dev::VerifyRange>(), static_cast<std::uint32_t>(rg.size()), d_err + 3 * r, st),
                "verify");
@@ -1215,6 +1224,7 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
     const auto& shard_lay = plan.shards;
     DeviceBuffer dw, derr(static_cast<std::size_t>(N) * 3 * sizeof(unsigned long long));
     cuda_check(cudaMemset(derr.get(), 0, derr.size()), "memset");
+    cuda_check(cudaStreamSynchronize(cudaStreamLegacy), "memset"); // cudaMemset is async: done before the verify streams add to it
     const std::uint64_t budget = device_budget();
     // Resident form: the weights payload stays on the device and each lane holds one
     // whole rank payload. Streaming form (a 70B-shaped checkpoint: 160 GB of weights,
@@ -1236,8 +1246,8 @@ void verify_checkpoint_dir(const std::string& dir_s, int device) {
     };
     const auto launch = [&](std::vector<dev::VerifyPair>& pr, std::vector<dev::VerifyRange>& rg, DeviceBuffer& dpairs,
                             DeviceBuffer& dranges, int r, cudaStream_t st) {
-        dpairs.upload(pr.data(), pr.size() * sizeof(dev::VerifyPair));
-        dranges.upload(rg.data(), rg.size() * sizeof(dev::VerifyRange));
+        dpairs.upload(pr.data(), pr.size() * sizeof(dev::VerifyPair), st);
+        dranges.upload(rg.data(), rg.size() * sizeof(dev::VerifyRange), st);
         cuda_check(dev::launch_verify(dpairs.get<dev::VerifyPair>(), static_cast<std::uint32_t>(pr.size()),
                                       dranges.get<dev::VerifyRange>(), static_cast<std::uint32_t>(rg.size()),
                                       derr.get<unsigned long long>() + 3 * r, st),

@@ -300,6 +300,7 @@ class FileAssembler {
                                       d_out_[slot].get(), c.hi - c.lo, dev::kGatherAuto, c.bulk_ok, s),
                    "gather");
         cuda_check(cudaEventRecord(ev1_[slot], s), "event");
+        if (sync_check()) cuda_check(cudaStreamSynchronize(s), "gather (TAILOR_SYNC_CHECK)");
         cuda_check(cudaMemcpyAsync(pin_io_[slot].get() + d2h_shift, d_out_[slot].get(), c.hi - c.lo, cudaMemcpyDeviceToHost, s),
                    "D2H");
         bytes += c.hi - c.lo;
@@ -583,6 +584,7 @@ class LaneVerifier {
             auto st = std::make_unique<DevState>();
             st->derr.resize(static_cast<std::size_t>(N_) * 3 * sizeof(unsigned long long));
             cuda_check(cudaMemset(st->derr.get(), 0, st->derr.size()), "memset");
+            cuda_check(cudaStreamSynchronize(cudaStreamLegacy), "memset"); // cudaMemset is async: done before the verify streams add to it
             dev_.emplace(d, std::move(st));
         }
         cuda_check(cudaSetDevice(devices_.front()), "cudaSetDevice");

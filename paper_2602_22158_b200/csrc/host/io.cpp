@@ -219,6 +219,14 @@ void read_one(const ReadJob& p, const std::string& what) {
 }
 } // namespace
 
+bool sync_check() {
+    static const bool on = [] {
+        const char* v = std::getenv("TAILOR_SYNC_CHECK");
+        return v && *v == '1';
+    }();
+    return on;
+}
+
 bool read_lookahead() {
     static const bool on = [] {
         const char* v = std::getenv("TAILOR_READ_LOOKAHEAD");

@@ -41,6 +41,9 @@ void run_reads(const std::vector<ReadJob>& jobs, int threads, const std::string&
 // TAILOR_READ_LOOKAHEAD=0 (measurement): queue a chunk's reads only when the previous
 // chunk's have completed, as a per-call read pool would.
 bool read_lookahead();
+// TAILOR_SYNC_CHECK=1 (diagnostics): synchronise each device step's stream right after its
+// launch, so an asynchronous fault is reported by the step that caused it.
+bool sync_check();
 class ReadPool {
   public:
     explicit ReadPool(int threads);
