@@ -1,7 +1,7 @@
 #!/bin/bash
 # The files line (two calls and tg_select_merge; warm and cold) twice.
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_select_merge.py -q -x -p no:cacheprovider 2>&1 | tail -2
+
 for rep in 1 2; do
   timeout 1800 python bench.py --workload files --steps 3 --warmup 1 > gpurun_out/bench_files_$rep.json 2> gpurun_out/bench_files_$rep.err; tail -5 gpurun_out/bench_files_$rep.err
   python - $rep <<'PY'
