@@ -110,3 +110,14 @@ def test_device_flow_over_a_layout_from_checkpoints(tmp_path, N, K):
     assert set(ours) == {"model.weights", *(f"optim/rank_{r}.shard" for r in range(N))}
     for name, data in ours.items():
         assert data == theirs[name], name
+
+
+def test_reader_pool_host_reads(tmp_path):
+    """tests/integration/readpool_test.cpp: the file drop-ins' reader pool (lookahead
+    batches, oversize pieces, O_DIRECT congruent and bounce paths, failure isolation,
+    drain, destruction with queued work) — host only, no GPU."""
+    exe = BUILD / "readpool_test"
+    need(exe)
+    p = subprocess.run([str(exe), str(tmp_path / "data.bin")], capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "readpool ok" in p.stdout
