@@ -116,3 +116,16 @@ def test_cli_select_merge_matches_reference(tmp_path):
     bad = subprocess.run([str(t.CLI_PATH), "select-merge", "--snapshots", ",".join(dirs), "--out", str(tmp_path / "ours")],
                          capture_output=True, text=True)
     assert bad.returncode == 2  # Storage (non-empty output directory), as `tailor merge`
+
+
+def test_select_merge_beyond_16_snapshots(tmp_path):
+    """The paper merges from 18 and 35 checkpoints: scoring sweeps windows
+    of <= 16 snapshots; every snapshot's masters are kept for the merge."""
+    need_gpu()
+    spec, N, K = t.ModelSpec(3, 16, 40, 64, False, 21), 2, 20
+    dirs = gen(tmp_path, spec, N, K)
+    ref_tool("select-merge", "--snapshots", ",".join(dirs), "--rho", 0.5, "--out", tmp_path / "ref")
+    rec, src, gap, st = t.select_merge(dirs, str(tmp_path / "ours"), 0.5)
+    assert digest(tmp_path / "ref") == digest(tmp_path / "ours")
+    assert st.resident_bytes > 0
+    assert (rec, src, gap) == t.select_recipe(dirs, 0.5)
