@@ -1554,10 +1554,15 @@ def files_arm(args):
     warm_roof = None
     if rw and wc:
         floor = (master_bytes + 2 * comp) / (rw * 1e9) + comp / (wc * 1e9)
+        overlapped = max((master_bytes + 2 * comp) / (rw * 1e9), comp / (wc * 1e9))
         warm_roof = {"bound": "host page-cache copies (tools/disk_probe, 32 threads): reads/read_warm + writes/write_cached",
                      "achieved_gbs_composite": round(o_v, 3), "read_bytes_per_step": master_bytes + 2 * comp,
                      "write_bytes_per_step": comp, "peak_read_gbs": rw, "peak_write_gbs": wc,
-                     "floor_ms": round(floor * 1e3, 1), "frac": round(floor / w_s, 4)}
+                     "floor_ms": round(floor * 1e3, 1), "frac": round(floor / w_s, 4),
+                     "floor_overlapped_ms": round(overlapped * 1e3, 1), "frac_overlapped": round(overlapped / w_s, 4),
+                     "note": "floor_ms: reads then writes at the probe's rates; the lanes overlap them (the merge "
+                             "writes while the scorer/merge/re-verify read), so frac can exceed 1; frac_overlapped "
+                             "assumes reads and writes fully concurrent at the same rates"}
     sm_w, sm_c = statistics.median(sm_warm), statistics.median(sm_cold)
     sm_line = {"what": "tg_select_merge (one call; the masters the scorer read stay on the device and feed the "
                        "merge: resident_bytes are not read again)",
