@@ -4,6 +4,7 @@
  * checkpoint directories (tg_layout_from_checkpoints) — no synthetic family involved:
  *   load every snapshot's rank-shard and weights payloads into device buffers
  *   -> tg_scorer per rank -> FP64 partials [N][K-1][M][2] (rank order)
+ *   -> tg_comm_allgather (the partials table through the library's NCCL communicator)
  *   -> tg_layout_select (a14: magnitude selection -> recipe over the directories)
  *   -> tg_mplan per output container (bind the device payloads, K2 gather)
  *   -> write the composite payload files (tg_mplan_prefix + gathered payload).
@@ -147,6 +148,26 @@ int main(int argc, char** argv) {
         cuda(cudaMemcpy(parts + per_rank * r, d_out, per_rank * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
         free(bases);
         tg_scorer_destroy(s);
+    }
+    /* the partials table through the library's NCCL all-gather: this process is the one
+     * rank of its job here (a GPU per rank in a real job: rank 0 makes the id, the caller
+     * ships it to the others, every rank contributes its own rows) */
+    {
+        uint8_t id[128];
+        if (tg_comm_unique_id(id) != TG_OK) die("tg_comm_unique_id", tg_last_error_kind());
+        tg_comm* c = tg_comm_create(id, 1, 0, 0);
+        if (!c) die("tg_comm_create", tg_last_error_kind());
+        double *d_rows = NULL, *d_table = NULL;
+        const size_t n = per_rank * (size_t)N;
+        cuda(cudaMalloc((void**)&d_rows, n * sizeof(double)), "cudaMalloc");
+        cuda(cudaMalloc((void**)&d_table, n * sizeof(double)), "cudaMalloc");
+        cuda(cudaMemcpy(d_rows, parts, n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+        int rc = tg_comm_allgather(c, d_rows, d_table, n, NULL);
+        if (rc) die("tg_comm_allgather", rc);
+        cuda(cudaMemcpy(parts, d_table, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+        cudaFree(d_rows);
+        cudaFree(d_table);
+        tg_comm_destroy(c);
     }
     char* yaml = text(tg_layout_select, l, parts, N, rho);
     printf("%s", yaml);
