@@ -171,6 +171,11 @@ int main(int argc, char** argv) {
     }
     char* yaml = text(tg_layout_select, l, parts, N, rho);
     printf("%s", yaml);
+    snprintf(path, sizeof path, "%s.recipe.yaml", out); /* stdout may also carry library banners */
+    FILE* rf = fopen(path, "w");
+    if (!rf) die("fopen recipe", 0);
+    fputs(yaml, rf);
+    fclose(rf);
 
     snprintf(path, sizeof path, "%s/optim", out);
     mkdir(out, 0755);

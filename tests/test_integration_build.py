@@ -102,7 +102,8 @@ def test_device_flow_over_a_layout_from_checkpoints(tmp_path, N, K):
     import paper_2602_22158_b200 as t
 
     ref = ref_tool("score", "--snapshots", ",".join(d), "--rho", "0.5")[1]
-    assert t.parse_recipe(p.stdout) == t.MergeRecipe.from_json(json.dumps(ref["recipe"]))
+    recipe = (tmp_path / "flow.recipe.yaml").read_text()
+    assert t.parse_recipe(recipe) == t.MergeRecipe.from_json(json.dumps(ref["recipe"]))
     (tmp_path / "r.json").write_text(json.dumps(ref["recipe"]))
     ref_tool("merge", "--recipe", tmp_path / "r.json", "--out", tmp_path / "ref")
     ours = tree(tmp_path / "flow")

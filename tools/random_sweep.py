@@ -4,7 +4,8 @@ the reference writes random-shape sources (oracle/_ref/ref_tool gen), a random r
 (layer moves, tied models, N <= 8, K <= 4, optional base) is merged by the reference and
 by execute_merge (random worker count, random device budget forcing the streaming
 re-verify), and every output file must be byte-identical; every 4th case also runs the
-file scorer + selection against the reference scorer.
+file scorer + selection against the reference scorer and tg_select_merge against the
+reference's select-merge.
 usage: random_sweep.py [cases] [seed]"""
 import json
 import os
@@ -85,6 +86,11 @@ def main():
                 r = ref("score", "--snapshots", ",".join(d), "--rho", "0.5")
                 assert rec == t.MergeRecipe.from_json(json.dumps(r["recipe"])), "selection differs"
                 note = f" select ok (gap {gap:.3g})"
+                # the combined call: the reference's select-merge vs tg_select_merge, every file
+                ref("select-merge", "--snapshots", ",".join(d), "--rho", "0.5", "--out", work / "ref_sm")
+                _, _, _, st = t.select_merge(d, str(work / "ours_sm"), 0.5, t.MergeOptions(workers=workers))
+                same_tree(work / "ref_sm", work / "ours_sm")
+                note += f", select-merge ok ({st.resident_bytes} B resident)"
             print(f"case {c}: L{L} h{h} f{f} v{v} tied={tied} N{N} K{K} workers={workers} budget={budget} ok{note}",
                   flush=True)
         except Exception as e:  # keep sweeping; report at the end
