@@ -459,6 +459,23 @@ void put_stats(const MergeStats& s, tg_merge_stats* st) {
     st->resident_bytes = s.resident_bytes;
 }
 
+// A null handle is a caller error reported through tg_last_error, never a crash.
+template <typename T>
+T& need(T* h, const char* fn) {
+    if (!h) fail(ErrorKind::Geometry, std::string(fn) + ": null handle");
+    return *h;
+}
+
+std::vector<std::string> dir_list(const char* const* dirs, int32_t n) {
+    if (n < 0 || (n > 0 && !dirs)) fail(ErrorKind::Recipe, "snapshot directory list is null or has a negative length");
+    std::vector<std::string> ds;
+    for (int32_t i = 0; i < n; ++i) {
+        if (!dirs[i]) fail(ErrorKind::Recipe, "snapshot directory " + std::to_string(i) + " is null");
+        ds.emplace_back(dirs[i]);
+    }
+    return ds;
+}
+
 std::vector<int> device_list(const int32_t* devices, int32_t n) {
     if (n <= 0 || !devices) return {0};
     return std::vector<int>(devices, devices + n);
@@ -555,7 +572,7 @@ tg_trainer* tg_trainer_create(const tg_model_spec* spec, int32_t num_ranks, int3
 }
 
 void tg_trainer_destroy(tg_trainer* t) { delete t; }
-uint64_t tg_trainer_elements(const tg_trainer* t) { return t->tr->elements(); }
+uint64_t tg_trainer_elements(const tg_trainer* t) { return t ? t->tr->elements() : 0; }
 
 int tg_resume(const char* checkpoint_dir, int64_t additional_steps, const char* out_dir, int32_t device, int32_t* written) {
     return guard([&] {
@@ -566,7 +583,7 @@ int tg_resume(const char* checkpoint_dir, int64_t additional_steps, const char* 
 
 int tg_trainer_step(tg_trainer* t, int64_t step, double* gn, double* un) {
     return guard([&] {
-        const auto [g, u] = t->tr->step(step);
+        const auto [g, u] = need(t, "tg_trainer_step").tr->step(step);
         if (gn) *gn = g;
         if (un) *un = u;
     });
@@ -574,7 +591,7 @@ int tg_trainer_step(tg_trainer* t, int64_t step, double* gn, double* un) {
 
 int tg_trainer_partition(tg_trainer* t, int32_t rank, void** d_ptr, uint64_t* bytes) {
     return guard([&] {
-        const auto [p, n] = t->tr->partition(rank);
+        const auto [p, n] = need(t, "tg_trainer_partition").tr->partition(rank);
         if (d_ptr) *d_ptr = p;
         if (bytes) *bytes = n;
     });
@@ -587,7 +604,7 @@ int tg_verify_checkpoint(const char* dir, int32_t device) {
 int tg_score_snapshots(const char* const* dirs, int32_t n, const int32_t* devices, int32_t num_devices, double* sums,
                        double* scores, int32_t* nm) {
     return guard([&] {
-        std::vector<std::string> ds(dirs, dirs + n);
+        std::vector<std::string> ds = dir_list(dirs, n);
         std::vector<std::vector<double>> sd, sr;
         std::vector<CheckpointSummary> summ;
         score_dirs(ds, device_list(devices, num_devices), sd, sr, summ);
@@ -607,7 +624,7 @@ int tg_score_snapshots(const char* const* dirs, int32_t n, const int32_t* device
 int tg_select_recipe(const char* const* dirs, int32_t n, double rho, const int32_t* devices, int32_t num_devices, char* out, size_t cap,
                      size_t* needed, int32_t* source_of, double* min_gap) {
     return guard([&] {
-        std::vector<std::string> ds(dirs, dirs + n);
+        std::vector<std::string> ds = dir_list(dirs, n);
         std::vector<std::vector<double>> sd, sr;
         std::vector<CheckpointSummary> summ;
         score_dirs(ds, device_list(devices, num_devices), sd, sr, summ);
@@ -630,7 +647,7 @@ int tg_select_merge(const char* const* dirs, int32_t n, double rho, const char* 
         std::error_code ec;
         if (fs::exists(dst) && !fs::is_empty(dst, ec)) // fail before any device work, as execute_merge would
             fail(ErrorKind::Storage, "refusing to write into non-empty directory '" + dst.string() + "'");
-        std::vector<std::string> ds(dirs, dirs + n);
+        std::vector<std::string> ds = dir_list(dirs, n);
         std::vector<std::vector<double>> sd, sr;
         std::vector<CheckpointSummary> summ;
         ResidentSources keep;
@@ -746,7 +763,7 @@ tg_layout* tg_layout_from_checkpoints(const char* const* dirs, int32_t n) {
     tg_layout* out = nullptr;
     guard([&] {
         if (!dirs || n < 1) fail(ErrorKind::Recipe, "no checkpoint directories");
-        auto set = SnapshotSet::from_checkpoints(std::vector<std::string>(dirs, dirs + n));
+        auto set = SnapshotSet::from_checkpoints(dir_list(dirs, n));
         out = new tg_layout{set.get(), std::move(set)};
     });
     return out;
@@ -769,67 +786,68 @@ int tg_layout_set_partial(tg_layout* l, int32_t k, const char* csv) {
             }
         }
         if (!cur.empty()) mods.push_back(parse_module_name(cur));
-        l->set->set_partial(k, mods);
+        need(l, "tg_layout_set_partial").set->set_partial(k, mods);
     });
 }
 
 int tg_layout_set_id(tg_layout* l, int32_t k, const char* id) {
     return guard([&] {
-        if (k < 1 || k > l->set->snapshots()) fail(ErrorKind::Geometry, "snapshot index out of range");
+        if (k < 1 || k > need(l, "tg_layout_set_id").set->snapshots()) fail(ErrorKind::Geometry, "snapshot index out of range");
         l->set->set_id(k, id ? id : "");
     });
 }
 
-int32_t tg_layout_num_modules(const tg_layout* l) { return l->set->model().module_count(); }
-int32_t tg_layout_num_ranks(const tg_layout* l) { return l->set->num_ranks(); }
-int32_t tg_layout_snapshots(const tg_layout* l) { return l->set->snapshots(); }
+int32_t tg_layout_num_modules(const tg_layout* l) { return l ? l->set->model().module_count() : 0; }
+int32_t tg_layout_num_ranks(const tg_layout* l) { return l ? l->set->num_ranks() : 0; }
+int32_t tg_layout_snapshots(const tg_layout* l) { return l ? l->set->snapshots() : 0; }
 
 uint64_t tg_layout_shard_bytes(const tg_layout* l, int32_t k, int32_t rank) {
     uint64_t n = 0;
-    guard([&] { n = l->set->layout(k).shards.at(static_cast<std::size_t>(rank)).payload_bytes; });
+    guard([&] { n = need(l, "tg_layout_shard_bytes").set->layout(k).shards.at(static_cast<std::size_t>(rank)).payload_bytes; });
     return n;
 }
 
 uint64_t tg_layout_weights_bytes(const tg_layout* l, int32_t k) {
     uint64_t n = 0;
-    guard([&] { n = l->set->layout(k).weights.payload_bytes; });
+    guard([&] { n = need(l, "tg_layout_weights_bytes").set->layout(k).weights.payload_bytes; });
     return n;
 }
 
 uint64_t tg_layout_packed_master_bytes(const tg_layout* l, int32_t rank) {
     uint64_t n = 0;
-    guard([&] { n = l->set->packed_master_bytes(rank); });
+    guard([&] { n = need(l, "tg_layout_packed_master_bytes").set->packed_master_bytes(rank); });
     return n;
 }
 
-uint64_t tg_layout_parameter_count(const tg_layout* l) { return static_cast<uint64_t>(l->set->model().parameter_count()); }
+uint64_t tg_layout_parameter_count(const tg_layout* l) { return l ? static_cast<uint64_t>(l->set->model().parameter_count()) : 0; }
 
 int tg_family_gen_shard(tg_family* f, int32_t rank, int32_t k0, int32_t k1, uint8_t* const* outs, void* stream) {
-    return guard([&] { f->fam->gen_shard(rank, k0, k1, outs, static_cast<cudaStream_t>(stream)); });
+    return guard([&] { need(f, "tg_family_gen_shard").fam->gen_shard(rank, k0, k1, outs, static_cast<cudaStream_t>(stream)); });
 }
 
 int tg_family_gen_weights(tg_family* f, int32_t k0, int32_t k1, uint64_t lo, uint64_t hi, uint8_t* const* outs,
                           void* stream) {
-    return guard([&] { f->fam->gen_weights(k0, k1, lo, hi, outs, static_cast<cudaStream_t>(stream)); });
+    return guard([&] { need(f, "tg_family_gen_weights").fam->gen_weights(k0, k1, lo, hi, outs, static_cast<cudaStream_t>(stream)); });
 }
 
 int tg_family_gen_masters(tg_family* f, int32_t rank, int32_t k0, int32_t k1, uint8_t* const* outs, void* stream) {
-    return guard([&] { f->fam->gen_masters_packed(rank, k0, k1, outs, static_cast<cudaStream_t>(stream)); });
+    return guard([&] { need(f, "tg_family_gen_masters").fam->gen_masters_packed(rank, k0, k1, outs, static_cast<cudaStream_t>(stream)); });
 }
 
 int tg_family_gen_shard_range(tg_family* f, int32_t rank, int32_t k, uint64_t lo, uint64_t hi, uint8_t* out, void* stream) {
-    return guard([&] { f->fam->gen_shard_range(rank, k, lo, hi, out, static_cast<cudaStream_t>(stream)); });
+    return guard([&] { need(f, "tg_family_gen_shard_range").fam->gen_shard_range(rank, k, lo, hi, out, static_cast<cudaStream_t>(stream)); });
 }
 
 int tg_family_write_dir(tg_family* f, int32_t k, const char* dir) {
-    return guard([&] { f->fam->write_dir(k, dir ? dir : ""); });
+    return guard([&] { need(f, "tg_family_write_dir").fam->write_dir(k, dir ? dir : ""); });
 }
 
 int tg_layout_select(const tg_layout* l, const double* parts, int32_t nranks, double rho, char* out, size_t cap,
                      size_t* needed, int32_t* source_of, double* scores, double* min_gap) {
     return guard([&] {
-        const SnapshotSet& fam = *l->set;
+        const SnapshotSet& fam = *need(l, "tg_layout_select").set;
         const int K = fam.snapshots(), M = fam.model().module_count();
+        if (nranks < 1 || !parts) fail(ErrorKind::Geometry, "tg_layout_select: no score partials");
         std::vector<std::vector<double>> sc(static_cast<std::size_t>(K - 1), std::vector<double>(static_cast<std::size_t>(M)));
         for (int p = 0; p < K - 1; ++p)
             for (int m = 0; m < M; ++m) {
@@ -855,7 +873,7 @@ int tg_layout_select(const tg_layout* l, const double* parts, int32_t nranks, do
 tg_scorer* tg_scorer_create(const tg_layout* l, int32_t rank, int32_t k0, int32_t k1, int32_t packed) {
     tg_scorer* out = nullptr;
     guard([&] {
-        const SnapshotSet& fam = *l->set;
+        const SnapshotSet& fam = *need(l, "tg_scorer_create").set;
         if (rank < 0 || rank >= fam.num_ranks()) fail(ErrorKind::Geometry, "rank out of range");
         if (k0 < 1 || k1 > fam.snapshots() || k1 - k0 < 1) fail(ErrorKind::Geometry, "snapshot range out of bounds");
         const auto fields = score_fields(fam.model(), fam.num_ranks());
@@ -890,19 +908,19 @@ int tg_scorer_set_variant(tg_scorer* s, int32_t variant) {
         if (variant < 0 || variant > 6)
             fail(ErrorKind::Geometry, "scorer variant: 0 auto, 1 register, 2 staged, 3 register-128b, 4 register-64b, "
                                           "5 staged half rows, 6 staged 2 CTAs/SM");
-        s->plan->set_variant(variant);
+        need(s, "tg_scorer_set_variant").plan->set_variant(variant);
     });
 }
-uint64_t tg_scorer_bytes(const tg_scorer* s) { return s->plan->bytes_read(); }
+uint64_t tg_scorer_bytes(const tg_scorer* s) { return s ? s->plan->bytes_read() : 0; }
 
 int tg_scorer_run(tg_scorer* s, const uint8_t* const* bases, double* d_out, void* stream) {
-    return guard([&] { s->plan->run(bases, d_out, static_cast<cudaStream_t>(stream)); });
+    return guard([&] { need(s, "tg_scorer_run").plan->run(bases, d_out, static_cast<cudaStream_t>(stream)); });
 }
 
 tg_mplan* tg_mplan_create(const tg_layout* l, const char* yaml, int32_t container, int32_t unit, int32_t units) {
     tg_mplan* out = nullptr;
     guard([&] {
-        const SnapshotSet& fam = *l->set;
+        const SnapshotSet& fam = *need(l, "tg_mplan_create").set;
         const MergePlan plan =
             resolve_plan_with(parse_recipe(yaml ? yaml : ""), [&](const std::string& id) { return family_summary(fam, id); });
         std::map<std::string, SourceLayout> lays;
@@ -943,22 +961,22 @@ tg_mplan* tg_mplan_create(const tg_layout* l, const char* yaml, int32_t containe
 }
 
 void tg_mplan_destroy(tg_mplan* p) { delete p; }
-uint64_t tg_mplan_bytes(const tg_mplan* p) { return p->dev->bytes(); }
+uint64_t tg_mplan_bytes(const tg_mplan* p) { return p ? p->dev->bytes() : 0; }
 
 int tg_mplan_range(const tg_mplan* p, uint64_t* lo, uint64_t* hi, uint64_t* payload) {
     return guard([&] {
-        const PartitionPlan& pp = p->dev->plan();
+        const PartitionPlan& pp = need(p, "tg_mplan_range").dev->plan();
         if (lo) *lo = pp.dst_lo;
         if (hi) *hi = pp.dst_hi;
         if (payload) *payload = pp.out.payload_bytes;
     });
 }
 
-int32_t tg_mplan_num_windows(const tg_mplan* p) { return static_cast<int32_t>(p->dev->plan().windows.size()); }
+int32_t tg_mplan_num_windows(const tg_mplan* p) { return p ? static_cast<int32_t>(p->dev->plan().windows.size()) : 0; }
 
 int tg_mplan_window(const tg_mplan* p, int32_t i, int32_t* k, int32_t* container, uint64_t* lo, uint64_t* hi) {
     return guard([&] {
-        const auto& w = p->dev->plan().windows.at(static_cast<std::size_t>(i));
+        const auto& w = need(p, "tg_mplan_window").dev->plan().windows.at(static_cast<std::size_t>(i));
         if (k) *k = p->window_k.at(static_cast<std::size_t>(i));
         if (container) *container = w.container;
         if (lo) *lo = w.lo;
@@ -966,11 +984,11 @@ int tg_mplan_window(const tg_mplan* p, int32_t i, int32_t* k, int32_t* container
     });
 }
 
-uint32_t tg_mplan_num_segments(const tg_mplan* p) { return static_cast<uint32_t>(p->dev->plan().segments.size()); }
+uint32_t tg_mplan_num_segments(const tg_mplan* p) { return p ? static_cast<uint32_t>(p->dev->plan().segments.size()) : 0; }
 
 int tg_mplan_segment(const tg_mplan* p, uint32_t i, uint32_t* window, uint64_t* src_off, uint64_t* dst_off, uint64_t* bytes) {
     return guard([&] {
-        const PartitionPlan& pp = p->dev->plan();
+        const PartitionPlan& pp = need(p, "tg_mplan_segment").dev->plan();
         const CopySegment& s = pp.segments.at(i);
         if (window) *window = s.window;
         if (src_off) *src_off = s.src_off;
@@ -981,7 +999,7 @@ int tg_mplan_segment(const tg_mplan* p, uint32_t i, uint32_t* window, uint64_t* 
 
 int tg_mplan_prefix(const tg_mplan* p, char* out, size_t cap, size_t* needed) {
     return guard([&] {
-        const std::string s = p->dev->plan().out.prefix();
+        const std::string s = need(p, "tg_mplan_prefix").dev->plan().out.prefix();
         if (needed) *needed = s.size();
         if (!out || cap < s.size()) fail(ErrorKind::Geometry, "output buffer too small");
         std::memcpy(out, s.data(), s.size());
@@ -989,20 +1007,24 @@ int tg_mplan_prefix(const tg_mplan* p, char* out, size_t cap, size_t* needed) {
 }
 
 int tg_mplan_bind(tg_mplan* p, const uint8_t* const* ptrs) {
-    return guard([&] { p->dev->bind(std::vector<const std::uint8_t*>(ptrs, ptrs + p->dev->plan().windows.size())); });
+    return guard([&] {
+        need(p, "tg_mplan_bind");
+        if (!ptrs && !p->dev->plan().windows.empty()) fail(ErrorKind::Geometry, "tg_mplan_bind: null window list");
+        p->dev->bind(std::vector<const std::uint8_t*>(ptrs, ptrs + p->dev->plan().windows.size())); });
 }
 
-int32_t tg_mplan_bulk_ok(const tg_mplan* p) { return p->dev->bulk_ok() ? 1 : 0; }
+int32_t tg_mplan_bulk_ok(const tg_mplan* p) { return p && p->dev->bulk_ok() ? 1 : 0; }
 
 int tg_mplan_run(tg_mplan* p, uint8_t* d_dst, int32_t variant, void* stream) {
-    return guard([&] { p->dev->run(d_dst, variant, static_cast<cudaStream_t>(stream)); });
+    return guard([&] { need(p, "tg_mplan_run").dev->run(d_dst, variant, static_cast<cudaStream_t>(stream)); });
 }
 
 int tg_mplan_run_host(tg_mplan* p, const uint8_t* const* h_windows, const uint8_t* const* d_windows,
                       uint32_t resident_fields, uint8_t* h_dst, int32_t variant, uint64_t chunk, int32_t async,
                       const tg_host_copy* prefetch, uint32_t nprefetch, uint64_t* h2d, uint64_t* d2h) {
     return guard([&] {
-        const PartitionPlan& pp = p->dev->plan();
+        const PartitionPlan& pp = need(p, "tg_mplan_run_host").dev->plan();
+        if (!h_windows || !h_dst) fail(ErrorKind::Geometry, "tg_mplan_run_host: null host windows or destination");
         if (!d_windows) resident_fields = 0;
         // Resident ranges: bits 0-2 read exp_avg / exp_avg_sq / master from d_windows[w], a
         // device copy of the window in shard layout; bit 3 reads the masters from
@@ -1059,13 +1081,13 @@ int tg_mplan_run_host(tg_mplan* p, const uint8_t* const* h_windows, const uint8_
 
 int tg_mplan_wait(tg_mplan* p) {
     return guard([&] {
-        if (p->host) p->host->wait();
+        if (need(p, "tg_mplan_wait").host) p->host->wait();
     });
 }
 
 tg_dstep* tg_dstep_create(const tg_layout* l, int32_t rank, int32_t unit, int32_t units, double rho) {
     tg_dstep* out = nullptr;
-    guard([&] { out = new tg_dstep{std::make_unique<DeviceSelectStep>(*l->set, rank, unit, units, rho)}; });
+    guard([&] { out = new tg_dstep{std::make_unique<DeviceSelectStep>(*need(l, "tg_dstep_create").set, rank, unit, units, rho)}; });
     return out;
 }
 
@@ -1073,6 +1095,7 @@ void tg_dstep_destroy(tg_dstep* s) { delete s; }
 
 int tg_dstep_range(const tg_dstep* s, uint64_t* shard_bytes, uint64_t* wlo, uint64_t* whi) {
     return guard([&] {
+        need(s, "tg_dstep_range");
         if (shard_bytes) *shard_bytes = s->step->shard_bytes();
         if (wlo) *wlo = s->step->weights_lo();
         if (whi) *whi = s->step->weights_hi();
@@ -1080,19 +1103,19 @@ int tg_dstep_range(const tg_dstep* s, uint64_t* shard_bytes, uint64_t* wlo, uint
 }
 
 int tg_dstep_bind(tg_dstep* s, const uint8_t* const* shard_bases, const uint8_t* const* wwin_bases) {
-    return guard([&] { s->step->bind(shard_bases, wwin_bases); });
+    return guard([&] { need(s, "tg_dstep_bind").step->bind(shard_bases, wwin_bases); });
 }
 
 int tg_dstep_run(tg_dstep* s, const double* d_parts, int32_t nranks, uint8_t* d_out_shard, uint8_t* d_out_w, int32_t variant,
                  int32_t phases, void* stream) {
     return guard([&] {
-        s->step->run(d_parts, nranks, d_out_shard, d_out_w, variant, static_cast<cudaStream_t>(stream), phases);
+        need(s, "tg_dstep_run").step->run(d_parts, nranks, d_out_shard, d_out_w, variant, static_cast<cudaStream_t>(stream), phases);
     });
 }
 
 int tg_dstep_result(tg_dstep* s, int32_t* source_of, double* scores, void* stream) {
     return guard([&] {
-        const auto src = s->step->source_of(static_cast<cudaStream_t>(stream));
+        const auto src = need(s, "tg_dstep_result").step->source_of(static_cast<cudaStream_t>(stream));
         if (source_of) std::copy(src.begin(), src.end(), source_of);
         if (scores) {
             const auto sc = s->step->scores(static_cast<cudaStream_t>(stream));

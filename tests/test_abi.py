@@ -50,6 +50,29 @@ def test_errors_are_codes_not_exceptions():
     assert t.lib().tg_last_error_kind() == t.ErrorKind.Recipe
 
 
+def test_null_handles_are_errors_not_crashes():
+    """Every handle-taking entry point reports a null handle through tg_last_error
+    (no host work, no CUDA needed); getters return 0."""
+    L = t.lib()
+    calls = [
+        lambda: L.tg_scorer_run(None, None, None, None),
+        lambda: L.tg_mplan_run(None, None, 0, None),
+        lambda: L.tg_dstep_run(None, None, 1, None, None, 0, 0, None),
+        lambda: L.tg_family_gen_shard(None, 0, 1, 2, None, None),
+        lambda: L.tg_layout_select(None, None, 1, 0.5, None, 0, None, None, None, None),
+        lambda: L.tg_comm_allgather(None, None, None, 0, None),
+    ]
+    for call in calls:
+        rc = call()
+        assert rc != 0
+        assert b"null" in L.tg_last_error()
+    assert L.tg_layout_num_modules(None) == 0
+    dirs = (ctypes.c_char_p * 2)(b"/nonexistent-a", None)
+    buf = ctypes.create_string_buffer(64)
+    rc = L.tg_select_recipe(dirs, 2, 0.5, None, 0, buf, 64, None, None, None)
+    assert rc == t.ErrorKind.Recipe and b"is null" in L.tg_last_error()
+
+
 def test_version_and_device_count_without_gpu():
     assert b"sm_100a" in t.lib().tg_version()
     assert t.lib().tg_device_count() >= 0
