@@ -12,6 +12,8 @@
  * ErrorKind code below; tg_last_error() holds the message (thread-local).
  * User errors (codes 1..9) are the reference's exit-code-1 class; 10, 11, 12
  * and 100 are internal (exit 2), as R/include/tailor/errors.hpp:51-54.
+ * A null handle passed to an int-returning function is TG_E_GEOMETRY ("<fn>: null
+ * handle"); size/count getters return 0 for a null handle.
  *
  * Device pointers are CUDA global-memory addresses on the current device;
  * `stream` is a cudaStream_t (NULL = legacy default stream). Launches are

@@ -5,8 +5,9 @@ the reference writes random-shape sources (oracle/_ref/ref_tool gen), a random r
 by execute_merge (random worker count, random device budget forcing the streaming
 re-verify), and every output file must be byte-identical; every 4th case also runs the
 file scorer + selection against the reference scorer and tg_select_merge against the
-reference's select-merge.
-usage: random_sweep.py [cases] [seed]"""
+reference's select-merge. `large` draws wider shapes (h 64-384, f 172-1024, v up to
+4096, K up to 6; every 2nd case scores and select-merges).
+usage: random_sweep.py [cases] [seed] [large]"""
 import json
 import os
 import pathlib
@@ -41,16 +42,24 @@ def same_tree(a, b):
 def main():
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 50
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    large = len(sys.argv) > 3 and sys.argv[3] == "large"
     rng = random.Random(seed)
     fails = 0
     for c in range(cases):
         work = pathlib.Path(tempfile.mkdtemp(prefix="sweep-"))
         try:
-            L = 1 + rng.randrange(8)
-            h = rng.choice([4, 8, 12, 16])
-            f, v = rng.choice([4, 8, 20, 40]), rng.choice([8, 16, 31, 64])
-            tied = rng.random() < 0.4
-            N, K = 1 + rng.randrange(8), 1 + rng.randrange(4)
+            if large:
+                L = 1 + rng.randrange(4)
+                h = rng.choice([64, 128, 200, 256, 384])
+                f, v = rng.choice([172, 344, 500, 688, 1024]), rng.choice([256, 1000, 2048, 4096])
+                tied = rng.random() < 0.3
+                N, K = 1 + rng.randrange(8), 2 + rng.randrange(5)
+            else:
+                L = 1 + rng.randrange(8)
+                h = rng.choice([4, 8, 12, 16])
+                f, v = rng.choice([4, 8, 20, 40]), rng.choice([8, 16, 31, 64])
+                tied = rng.random() < 0.4
+                N, K = 1 + rng.randrange(8), 1 + rng.randrange(4)
             spec = ["--layers", L, "--hidden", h, "--ffn", f, "--vocab", v, "--seed", 1000 + c]
             if tied:
                 spec.append("--tied")
@@ -81,7 +90,7 @@ def main():
             t.execute_merge(recipe, str(work / "ours"), t.MergeOptions(workers=workers))
             same_tree(work / "ref", work / "ours")
             note = ""
-            if c % 4 == 0 and K >= 2:
+            if c % (2 if large else 4) == 0 and K >= 2:
                 rec, _, gap = t.select_recipe(d, 0.5)
                 r = ref("score", "--snapshots", ",".join(d), "--rho", "0.5")
                 assert rec == t.MergeRecipe.from_json(json.dumps(r["recipe"])), "selection differs"
