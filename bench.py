@@ -708,11 +708,15 @@ def our_arm(args, rank, world, local_rank):
     scores_per_s = M * (K - 1) * args.steps / sec  # complete module scores (all ranks combined) per second
 
     # ---- per-kernel times: one eager pass with events between the launches ----------------
+    # A spin kernel (torch.cuda._sleep, ~5 ms) holds the stream first, so all four launches
+    # are queued before the GPU reaches e[0]: the events bracket device time, not the host's
+    # launch latency (which dominates at cfg1's microsecond kernels).
     kt = {"score": [], "select": [], "gather_shard": [], "gather_weights": []}
     for i in range(len(mine)):
         res.ensure(i)
         shards, _ = res.slot(i)
         e = [ev() for _ in range(5)]
+        torch.cuda._sleep(10_000_000)
         e[0].record(stream)
         seg_score(i, sp)
         e[1].record(stream)
