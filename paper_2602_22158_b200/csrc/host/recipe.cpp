@@ -1,9 +1,16 @@
 // Strict YAML merge-recipe schema (R/src/recipe.cpp:67-169). yaml-cpp is not
-// in this image, so this file carries a small YAML reader for the subset the
-// schema uses — block maps and sequences, flow [..] / {..}, plain and quoted
-// scalars, comments — and an emitter in yaml-cpp's block style. Schema
-// errors name the offending field, as the reference's do.
+// in this image, so this file carries its own YAML reader for what a recipe may be
+// written with — block maps and sequences, flow [..] / {..} (also across lines, trailing
+// commas), plain scalars (continued on more-indented lines), single- and double-quoted
+// scalars (every YAML escape, line folding), block scalars (| and >, chomping and
+// indentation indicators), comments, anchors and aliases, tags (which do not change the
+// conversions, as in yaml-cpp), %directives, --- / ... markers (the first document, as
+// YAML::Load), BOM and CRLF — and an emitter in yaml-cpp's block style. Schema errors
+// name the offending field, as the reference's do. tests/test_recipe_yaml.py checks the
+// reader against PyYAML on fixed and 400 randomly rendered recipes.
 #include <cctype>
+#include <cstdint>
+#include <map>
 #include <set>
 
 #include "tailor/errors.hpp"
@@ -26,27 +33,18 @@ struct Node {
     }
 };
 
+// &anchor -> node (yaml-cpp resolves *alias to the anchored node)
+using Anchors = std::map<std::string, Node>;
+
 [[noreturn]] void yaml_error(const std::string& what) { fail(ErrorKind::Recipe, "invalid YAML: " + what); }
 
 struct Line {
     int indent;
-    std::string text; // comment-stripped, right-trimmed
+    std::string text; // one logical line: comment-stripped, right-trimmed, continuations folded in
     int number;
 };
 
-std::string strip_comment(const std::string& s) {
-    char quote = 0;
-    for (std::size_t i = 0; i < s.size(); ++i) {
-        const char c = s[i];
-        if (quote) {
-            if (c == quote) quote = 0;
-            continue;
-        }
-        if (c == '"' || c == '\'') quote = c;
-        else if (c == '#' && (i == 0 || s[i - 1] == ' ' || s[i - 1] == '\t')) return s.substr(0, i);
-    }
-    return s;
-}
+bool is_ws(char c) { return c == ' ' || c == '\t'; }
 
 std::string rtrim(std::string s) {
     while (!s.empty() && std::isspace(static_cast<unsigned char>(s.back()))) s.pop_back();
@@ -59,10 +57,98 @@ std::string trim(const std::string& s) {
     return rtrim(s.substr(b));
 }
 
+// A quote opens a quoted scalar only where a node starts (line start, after "- ", ": ",
+// "[", "{", ","); elsewhere ' and " are plain characters ("/runs/bob's/ck-100").
+bool quote_opens(const std::string& s, std::size_t i) {
+    std::size_t j = i;
+    while (j > 0 && is_ws(s[j - 1])) --j;
+    if (j == 0) return true;
+    const char p = s[j - 1];
+    if (p == '[' || p == '{' || p == ',') return true;
+    return (p == ':' || p == '-' || p == '?') && j < i; // "key: 'v'", "- 'v'"
+}
+
+// Scans s from state (quote, depth): returns where a comment starts (npos if none) and
+// leaves the quote / flow-bracket state at the end of the line.
+std::size_t scan(const std::string& s, char& quote, int& depth) {
+    for (std::size_t i = 0; i < s.size(); ++i) {
+        const char c = s[i];
+        if (quote) {
+            if (quote == '"' && c == '\\') {
+                ++i;
+                continue;
+            }
+            if (c == quote) {
+                if (quote == '\'' && i + 1 < s.size() && s[i + 1] == '\'') {
+                    ++i;
+                    continue;
+                }
+                quote = 0;
+            }
+            continue;
+        }
+        if ((c == '"' || c == '\'') && quote_opens(s, i)) quote = c;
+        else if (c == '#' && (i == 0 || is_ws(s[i - 1]))) return i;
+        else if (c == '[' || c == '{') ++depth;
+        else if ((c == ']' || c == '}') && depth > 0) --depth;
+    }
+    return std::string::npos;
+}
+
+std::string strip_comment(const std::string& s) {
+    char q = 0;
+    int d = 0;
+    const std::size_t at = scan(s, q, d);
+    return at == std::string::npos ? s : s.substr(0, at);
+}
+
+void put_utf8(std::string& o, std::uint32_t cp) {
+    if (cp < 0x80) {
+        o.push_back(static_cast<char>(cp));
+    } else if (cp < 0x800) {
+        o.push_back(static_cast<char>(0xC0 | (cp >> 6)));
+        o.push_back(static_cast<char>(0x80 | (cp & 0x3F)));
+    } else if (cp < 0x10000) {
+        o.push_back(static_cast<char>(0xE0 | (cp >> 12)));
+        o.push_back(static_cast<char>(0x80 | ((cp >> 6) & 0x3F)));
+        o.push_back(static_cast<char>(0x80 | (cp & 0x3F)));
+    } else if (cp < 0x110000) {
+        o.push_back(static_cast<char>(0xF0 | (cp >> 18)));
+        o.push_back(static_cast<char>(0x80 | ((cp >> 12) & 0x3F)));
+        o.push_back(static_cast<char>(0x80 | ((cp >> 6) & 0x3F)));
+        o.push_back(static_cast<char>(0x80 | (cp & 0x3F)));
+    } else {
+        yaml_error("escaped code point out of range");
+    }
+}
+
+// A double-quoted scalar's content as yaml-cpp writes it (used for folded block scalars).
+std::string dq(const std::string& v) {
+    std::string o = "\"";
+    for (const char c : v) {
+        if (c == '"' || c == '\\') {
+            o.push_back('\\');
+            o.push_back(c);
+        } else if (c == '\n') {
+            o += "\\n";
+        } else if (c == '\t') {
+            o += "\\t";
+        } else if (static_cast<unsigned char>(c) < 0x20) {
+            static const char* hx = "0123456789abcdef";
+            o += "\\x";
+            o.push_back(hx[(c >> 4) & 0xF]);
+            o.push_back(hx[c & 0xF]);
+        } else {
+            o.push_back(c);
+        }
+    }
+    return o + "\"";
+}
+
 // ---- flow / scalar parsing ----
 class Flow {
   public:
-    explicit Flow(const std::string& s) : s_(s) {}
+    Flow(const std::string& s, Anchors& anchors) : s_(s), anchors_(anchors) {}
     Node parse_all() {
         Node n = value(false);
         ws();
@@ -72,14 +158,79 @@ class Flow {
 
   private:
     void ws() {
-        while (i_ < s_.size() && (s_[i_] == ' ' || s_[i_] == '\t')) ++i_;
+        while (i_ < s_.size() && is_ws(s_[i_])) ++i_;
+    }
+    bool at_end_of_node(bool in_flow) const {
+        return i_ >= s_.size() || (in_flow && (s_[i_] == ',' || s_[i_] == ']' || s_[i_] == '}'));
+    }
+    std::string token() { // anchor / alias / tag name: up to whitespace or a flow indicator
+        const std::size_t b = i_;
+        while (i_ < s_.size() && !is_ws(s_[i_]) && s_[i_] != ',' && s_[i_] != '[' && s_[i_] != ']' && s_[i_] != '{' &&
+               s_[i_] != '}')
+            ++i_;
+        return s_.substr(b, i_ - b);
     }
     Node value(bool in_flow) {
         ws();
-        if (i_ >= s_.size()) return Node{};
-        if (s_[i_] == '[') return seq();
-        if (s_[i_] == '{') return map();
-        return scalar(in_flow, false);
+        std::string anchor;
+        while (i_ < s_.size() && (s_[i_] == '&' || s_[i_] == '!')) { // node properties; tags do not change conversions
+            const bool is_anchor = s_[i_] == '&';
+            ++i_;
+            const std::string name = token();
+            if (is_anchor) {
+                if (name.empty()) yaml_error("empty anchor name");
+                anchor = name;
+            }
+            ws();
+        }
+        Node n;
+        if (i_ < s_.size() && s_[i_] == '*') {
+            if (!anchor.empty()) yaml_error("an alias cannot carry an anchor");
+            ++i_;
+            const std::string name = token();
+            const auto it = anchors_.find(name);
+            if (it == anchors_.end()) yaml_error("unknown anchor '" + name + "'");
+            return it->second;
+        }
+        if (at_end_of_node(in_flow)) n = Node{};
+        else if (s_[i_] == '[') n = seq();
+        else if (s_[i_] == '{') n = map();
+        else n = scalar(in_flow, false);
+        if (!anchor.empty()) anchors_[anchor] = n;
+        return n;
+    }
+    void escape(std::string& out) {
+        if (i_ >= s_.size()) yaml_error("bad escape");
+        const char e = s_[i_++];
+        const auto hex = [&](int digits) {
+            std::uint32_t v = 0;
+            for (int k = 0; k < digits; ++k) {
+                if (i_ >= s_.size() || !std::isxdigit(static_cast<unsigned char>(s_[i_]))) yaml_error("bad escape");
+                const char h = s_[i_++];
+                v = v * 16 + static_cast<std::uint32_t>(std::isdigit(static_cast<unsigned char>(h)) ? h - '0' : (std::tolower(h) - 'a' + 10));
+            }
+            return v;
+        };
+        switch (e) {
+            case '0': out.push_back('\0'); break;
+            case 'a': out.push_back('\a'); break;
+            case 'b': out.push_back('\b'); break;
+            case 't': case '\t': out.push_back('\t'); break;
+            case 'n': out.push_back('\n'); break;
+            case 'v': out.push_back('\v'); break;
+            case 'f': out.push_back('\f'); break;
+            case 'r': out.push_back('\r'); break;
+            case 'e': out.push_back('\x1b'); break;
+            case ' ': case '"': case '/': case '\\': out.push_back(e); break;
+            case 'N': put_utf8(out, 0x85); break;
+            case '_': put_utf8(out, 0xA0); break;
+            case 'L': put_utf8(out, 0x2028); break;
+            case 'P': put_utf8(out, 0x2029); break;
+            case 'x': put_utf8(out, hex(2)); break;
+            case 'u': put_utf8(out, hex(4)); break;
+            case 'U': put_utf8(out, hex(8)); break;
+            default: yaml_error(std::string("unknown escape character '") + e + "'");
+        }
     }
     Node scalar(bool in_flow, bool is_key) {
         ws();
@@ -100,9 +251,7 @@ class Flow {
                     break;
                 }
                 if (q == '"' && c == '\\') {
-                    if (i_ >= s_.size()) yaml_error("bad escape");
-                    const char e = s_[i_++];
-                    n.text.push_back(e == 'n' ? '\n' : e == 't' ? '\t' : e);
+                    escape(n.text);
                     continue;
                 }
                 n.text.push_back(c);
@@ -113,11 +262,12 @@ class Flow {
         while (i_ < s_.size()) {
             const char c = s_[i_];
             if (in_flow && (c == ',' || c == ']' || c == '}')) break;
-            if (is_key && c == ':' && (i_ + 1 == s_.size() || s_[i_ + 1] == ' ')) break;
+            if (is_key && c == ':' && (i_ + 1 == s_.size() || is_ws(s_[i_ + 1]) || (in_flow && (s_[i_ + 1] == ',' || s_[i_ + 1] == '}'))))
+                break;
             ++i_;
         }
         n.text = trim(s_.substr(b, i_ - b));
-        if (n.text.empty() || n.text == "~" || n.text == "null") {
+        if (n.text.empty() || n.text == "~" || n.text == "null" || n.text == "Null" || n.text == "NULL") {
             n.kind = Node::Null;
             n.text.clear();
         }
@@ -138,6 +288,11 @@ class Flow {
             if (i_ >= s_.size()) yaml_error("unterminated flow sequence");
             if (s_[i_] == ',') {
                 ++i_;
+                ws();
+                if (i_ < s_.size() && s_[i_] == ']') { // trailing comma
+                    ++i_;
+                    return n;
+                }
                 continue;
             }
             if (s_[i_] == ']') {
@@ -168,6 +323,11 @@ class Flow {
             if (i_ >= s_.size()) yaml_error("unterminated flow mapping");
             if (s_[i_] == ',') {
                 ++i_;
+                ws();
+                if (i_ < s_.size() && s_[i_] == '}') { // trailing comma
+                    ++i_;
+                    return n;
+                }
                 continue;
             }
             if (s_[i_] == '}') {
@@ -178,6 +338,7 @@ class Flow {
         }
     }
     const std::string& s_;
+    Anchors& anchors_;
     std::size_t i_ = 0;
 };
 
@@ -189,15 +350,28 @@ bool split_key(const std::string& t, std::string& key, std::string& rest) {
     for (std::size_t i = 0; i < t.size(); ++i) {
         const char c = t[i];
         if (quote) {
-            if (c == quote) quote = 0;
+            if (quote == '"' && c == '\\') {
+                ++i;
+                continue;
+            }
+            if (c == quote) {
+                if (quote == '\'' && i + 1 < t.size() && t[i + 1] == '\'') {
+                    ++i;
+                    continue;
+                }
+                quote = 0;
+            }
             continue;
         }
-        if (c == '"' || c == '\'') quote = c;
+        if ((c == '"' || c == '\'') && quote_opens(t, i)) quote = c;
         else if (c == '[' || c == '{') ++depth;
         else if (c == ']' || c == '}') --depth;
-        else if (c == ':' && depth == 0 && (i + 1 == t.size() || t[i + 1] == ' ')) {
+        else if (c == ':' && depth == 0 && (i + 1 == t.size() || is_ws(t[i + 1]))) {
             std::string k = trim(t.substr(0, i));
-            if (k.size() >= 2 && (k.front() == '"' || k.front() == '\'') && k.back() == k.front()) k = k.substr(1, k.size() - 2);
+            if (k.size() >= 2 && (k.front() == '"' || k.front() == '\'') && k.back() == k.front()) {
+                Anchors none;
+                k = Flow(k, none).parse_all().text; // quoted keys: escapes and '' resolved
+            }
             key = k;
             rest = trim(t.substr(i + 1));
             return !key.empty();
@@ -206,9 +380,22 @@ bool split_key(const std::string& t, std::string& key, std::string& rest) {
     return false;
 }
 
+// Leading node properties of a block value ("&a !!map"): returns the anchor (if any) and
+// strips them from `rest`.
+std::string take_properties(std::string& rest) {
+    std::string anchor;
+    while (!rest.empty() && (rest[0] == '&' || rest[0] == '!')) {
+        std::size_t e = 0;
+        while (e < rest.size() && !is_ws(rest[e])) ++e;
+        if (rest[0] == '&') anchor = rest.substr(1, e - 1);
+        rest = trim(rest.substr(e));
+    }
+    return anchor;
+}
+
 class Block {
   public:
-    explicit Block(std::vector<Line> lines) : lines_(std::move(lines)) {}
+    Block(std::vector<Line> lines, Anchors& anchors) : lines_(std::move(lines)), anchors_(anchors) {}
     Node parse() {
         if (lines_.empty()) return Node{};
         Node n = node_at(lines_[0].indent);
@@ -217,7 +404,9 @@ class Block {
     }
 
   private:
-    bool is_item(const Line& l) const { return l.text == "-" || l.text.rfind("- ", 0) == 0; }
+    bool is_item(const Line& l) const { return l.text == "-" || l.text.rfind("- ", 0) == 0 || l.text.rfind("-\t", 0) == 0; }
+
+    Node flow(const std::string& s) { return Flow(s, anchors_).parse_all(); }
 
     Node node_at(int indent) {
         const Line& l = lines_[pos_];
@@ -226,17 +415,21 @@ class Block {
         std::string k, r;
         if (split_key(l.text, k, r)) return map_at(indent);
         ++pos_;
-        return Flow(l.text).parse_all();
+        return flow(l.text);
     }
 
-    Node value_after(const std::string& rest, int indent, bool allow_same_indent_seq) {
-        if (!rest.empty()) return Flow(rest).parse_all();
-        if (pos_ < lines_.size()) {
+    Node value_after(std::string rest, int indent, bool allow_same_indent_seq) {
+        const std::string anchor = take_properties(rest);
+        Node n;
+        if (!rest.empty()) {
+            n = flow(rest);
+        } else if (pos_ < lines_.size()) {
             const Line& nx = lines_[pos_];
-            if (nx.indent > indent) return node_at(nx.indent);
-            if (allow_same_indent_seq && nx.indent == indent && is_item(nx)) return seq_at(indent);
+            if (nx.indent > indent) n = node_at(nx.indent);
+            else if (allow_same_indent_seq && nx.indent == indent && is_item(nx)) n = seq_at(indent);
         }
-        return Node{};
+        if (!anchor.empty()) anchors_[anchor] = n;
+        return n;
     }
 
     Node map_at(int indent) {
@@ -260,56 +453,255 @@ class Block {
         n.kind = Node::Seq;
         while (pos_ < lines_.size() && lines_[pos_].indent == indent && is_item(lines_[pos_])) {
             Line l = lines_[pos_];
-            const std::string rest = l.text.size() > 1 ? trim(l.text.substr(1)) : std::string();
+            std::string rest = l.text.size() > 1 ? trim(l.text.substr(1)) : std::string();
+            const std::string anchor = take_properties(rest);
             if (rest.empty()) {
                 ++pos_;
-                n.items.push_back(value_after("", indent, false));
+                Node v = value_after("", indent, false);
+                if (!anchor.empty()) anchors_[anchor] = v;
+                n.items.push_back(std::move(v));
                 continue;
             }
             // "- key: v" opens a mapping whose keys sit at indent + offset of rest.
-            const int item_indent = indent + static_cast<int>(l.text.find(rest));
+            const int item_indent = indent + static_cast<int>(l.text.rfind(rest));
             std::string k, r;
+            Node v;
             if (split_key(rest, k, r) && rest[0] != '[' && rest[0] != '{') {
                 lines_[pos_].indent = item_indent;
                 lines_[pos_].text = rest;
-                n.items.push_back(map_at(item_indent));
+                v = map_at(item_indent);
             } else {
                 ++pos_;
-                n.items.push_back(Flow(rest).parse_all());
+                v = flow(rest);
             }
+            if (!anchor.empty()) anchors_[anchor] = v;
+            n.items.push_back(std::move(v));
         }
         return n;
     }
 
     std::vector<Line> lines_;
+    Anchors& anchors_;
     std::size_t pos_ = 0;
 };
 
-Node load_yaml(const std::string& text) {
-    std::vector<Line> lines;
-    std::size_t start = 0;
-    int number = 0;
-    while (start <= text.size()) {
+int indent_of(const std::string& raw) {
+    int ind = 0;
+    while (ind < static_cast<int>(raw.size()) && raw[static_cast<std::size_t>(ind)] == ' ') ++ind;
+    return ind;
+}
+
+bool blank(const std::string& raw) { return raw.find_first_not_of(" \t") == std::string::npos; }
+
+// Column of the node a logical line's value belongs to: the indent plus any "- " item
+// prefixes and, for "key: value", the key's column (block scalars and plain-scalar
+// continuation lines must be indented beyond it).
+int owner_column(const Line& l) {
+    int col = l.indent;
+    std::size_t i = 0;
+    while (i + 1 < l.text.size() && l.text[i] == '-' && is_ws(l.text[i + 1])) {
+        i += 2;
+        while (i < l.text.size() && is_ws(l.text[i])) ++i;
+    }
+    return col + static_cast<int>(i);
+}
+
+// The value part of a logical line ("key: v" -> v, "- v" -> v), after properties.
+std::string value_part(const std::string& body) {
+    std::string t = body;
+    while (t.size() >= 2 && t[0] == '-' && is_ws(t[1])) t = trim(t.substr(2));
+    if (t == "-") return "";
+    std::string k, r;
+    if (t.empty() || t[0] == '[' || t[0] == '{' || t[0] == '"' || t[0] == '\'') return t;
+    if (split_key(t, k, r)) t = r;
+    take_properties(t);
+    return t;
+}
+
+bool block_indicator(const std::string& v, char& style, char& chomp, int& explicit_indent) {
+    if (v.empty() || (v[0] != '|' && v[0] != '>')) return false;
+    style = v[0];
+    chomp = 0;
+    explicit_indent = 0;
+    for (std::size_t i = 1; i < v.size(); ++i) {
+        const char c = v[i];
+        if ((c == '+' || c == '-') && !chomp) chomp = c;
+        else if (c >= '1' && c <= '9' && !explicit_indent) explicit_indent = c - '0';
+        else return false;
+    }
+    return true;
+}
+
+// Splits the document into logical lines: BOM, directives and document markers handled
+// (yaml-cpp's Load reads the first document), comments stripped, quoted scalars and flow
+// collections that span lines joined, plain scalars' continuation lines folded, block
+// scalars (| and >, chomping and indentation indicators) turned into one double-quoted
+// scalar. The Block parser then sees one line per node.
+std::vector<Line> logical_lines(const std::string& text_in) {
+    std::string text = text_in;
+    if (text.rfind("\xEF\xBB\xBF", 0) == 0) text = text.substr(3);
+    std::vector<std::string> raw;
+    for (std::size_t start = 0; start <= text.size();) {
         std::size_t end = text.find('\n', start);
         if (end == std::string::npos) end = text.size();
-        std::string raw = text.substr(start, end - start);
-        ++number;
-        start = end + 1;
-        if (!raw.empty() && raw.back() == '\r') raw.pop_back();
-        if (raw.find('\t') != std::string::npos && raw.find_first_not_of(" \t") != std::string::npos &&
-            raw.find('\t') < raw.find_first_not_of(" \t"))
-            yaml_error("tabs are not allowed for indentation (line " + std::to_string(number) + ")");
-        const std::string t = rtrim(strip_comment(raw));
-        if (trim(t).empty() || trim(t) == "---") {
-            if (end == text.size()) break;
-            continue;
-        }
-        int ind = 0;
-        while (ind < static_cast<int>(t.size()) && t[static_cast<std::size_t>(ind)] == ' ') ++ind;
-        lines.push_back({ind, t.substr(static_cast<std::size_t>(ind)), number});
+        std::string r = text.substr(start, end - start);
+        if (!r.empty() && r.back() == '\r') r.pop_back();
+        raw.push_back(std::move(r));
         if (end == text.size()) break;
+        start = end + 1;
     }
-    return Block(std::move(lines)).parse();
+    std::vector<Line> out;
+    bool content = false, in_doc = false;
+    for (std::size_t i = 0; i < raw.size(); ++i) {
+        std::string r = raw[i];
+        const int number = static_cast<int>(i) + 1;
+        const auto marker = [&](const char* m) { return r.rfind(m, 0) == 0 && (r.size() == 3 || is_ws(r[3])); };
+        if (!content && !in_doc && !r.empty() && r[0] == '%') continue; // directive
+        if (marker("---")) {
+            if (content || in_doc) break; // a second document
+            in_doc = true;
+            r = r.substr(3);
+            if (blank(strip_comment(r))) continue;
+            r = trim(r); // "--- value" on the marker line
+        } else if (marker("...")) {
+            break;
+        }
+        if (!blank(r) && r.find('\t') < r.find_first_not_of(" \t"))
+            yaml_error("tabs are not allowed for indentation (line " + std::to_string(number) + ")");
+        char q = 0;
+        int depth = 0;
+        std::size_t cut = scan(r, q, depth);
+        std::string logical = cut == std::string::npos ? r : r.substr(0, cut);
+        if (blank(logical) && !q) continue;
+        const int indent = indent_of(logical);
+        // quoted scalars and flow collections continued on the next lines
+        int pending_breaks = 0;
+        while ((q || depth > 0) && i + 1 < raw.size()) {
+            const std::string nl = raw[++i];
+            if (marker("---") || marker("...")) yaml_error("document marker inside a flow or quoted node");
+            if (q) {
+                std::string c = trim(nl);
+                if (c.empty()) {
+                    ++pending_breaks;
+                    continue;
+                }
+                std::string head = logical;
+                while (!head.empty() && is_ws(head.back())) head.pop_back();
+                std::size_t bs = 0; // an odd run of trailing backslashes escapes the line break
+                while (bs < head.size() && head[head.size() - 1 - bs] == '\\') ++bs;
+                if (q == '"' && bs % 2 == 1 && !pending_breaks) {
+                    head.pop_back();
+                    logical = head;
+                } else {
+                    logical = head + (pending_breaks ? std::string(static_cast<std::size_t>(pending_breaks), '\n') : std::string(" "));
+                }
+                pending_breaks = 0;
+                cut = scan(c, q, depth);
+                logical += cut == std::string::npos ? c : c.substr(0, cut);
+            } else {
+                std::string c = trim(nl);
+                cut = scan(c, q, depth);
+                logical += " " + (cut == std::string::npos ? c : c.substr(0, cut));
+            }
+        }
+        if (q) yaml_error("unterminated quoted scalar starting at line " + std::to_string(number));
+        if (depth > 0) yaml_error("unterminated flow collection starting at line " + std::to_string(number));
+        Line l{indent, rtrim(logical.substr(static_cast<std::size_t>(indent))), number};
+        const int owner = owner_column(l);
+        const std::string v = value_part(l.text);
+        char style = 0, chomp = 0;
+        int ind = 0;
+        if (block_indicator(v, style, chomp, ind)) {
+            // block scalar: the following lines indented beyond the owner (and blank lines)
+            std::vector<std::string> body;
+            int content_indent = ind ? owner + ind : -1;
+            while (i + 1 < raw.size()) {
+                const std::string& nl = raw[i + 1];
+                if (blank(nl)) {
+                    body.push_back(nl);
+                    ++i;
+                    continue;
+                }
+                const int ni = indent_of(nl);
+                if (content_indent < 0) {
+                    if (ni <= owner) break;
+                    content_indent = ni;
+                }
+                if (ni < content_indent) break;
+                body.push_back(nl);
+                ++i;
+            }
+            if (content_indent < 0) content_indent = owner + 1;
+            // trailing blank lines belong to the chomping, not the content
+            std::size_t last = body.size();
+            while (last > 0 && blank(body[last - 1])) --last;
+            std::vector<std::string> ls;
+            for (std::size_t k = 0; k < last; ++k)
+                ls.push_back(static_cast<int>(body[k].size()) > content_indent ? body[k].substr(static_cast<std::size_t>(content_indent)) : std::string());
+            std::string val;
+            if (style == '|') {
+                for (std::size_t k = 0; k < ls.size(); ++k) val += (k ? "\n" : "") + ls[k];
+            } else {
+                int empties = 0;
+                bool have = false, prev_more = false;
+                for (const auto& x : ls) {
+                    if (x.empty()) {
+                        ++empties;
+                        continue;
+                    }
+                    const bool more = is_ws(x[0]);
+                    if (have) val += empties ? std::string(static_cast<std::size_t>(empties) + ((prev_more || more) ? 1 : 0), '\n')
+                                             : std::string((prev_more || more) ? "\n" : " ");
+                    else if (empties) val += std::string(static_cast<std::size_t>(empties), '\n');
+                    val += x;
+                    have = true;
+                    prev_more = more;
+                    empties = 0;
+                }
+            }
+            if (chomp == '-') {
+                // strip: no trailing line break
+            } else if (chomp == '+') {
+                if (!ls.empty()) val += "\n";
+                for (std::size_t k = last; k < body.size(); ++k) val += "\n";
+            } else if (!ls.empty()) {
+                val += "\n";
+            }
+            const std::size_t at = l.text.rfind(v);
+            l.text = l.text.substr(0, at) + dq(val);
+        } else if (!v.empty() && v[0] != '[' && v[0] != '{' && v[0] != '"' && v[0] != '\'' && v[0] != '*') {
+            // plain scalar: more-indented lines that follow continue it (folded with spaces)
+            int breaks = 0;
+            std::string extra;
+            while (i + 1 < raw.size()) {
+                const std::string& nl = raw[i + 1];
+                const std::string c = rtrim(strip_comment(nl));
+                if (blank(c)) {
+                    if (!blank(nl)) break; // a comment line ends a plain scalar
+                    ++breaks;
+                    ++i;
+                    continue;
+                }
+                if (indent_of(nl) <= owner || trim(nl).rfind("#", 0) == 0) break;
+                extra += breaks ? std::string(static_cast<std::size_t>(breaks), '\n') : std::string(" ");
+                extra += trim(c);
+                breaks = 0;
+                ++i;
+            }
+            if (!extra.empty()) {
+                const std::size_t at = l.text.rfind(v);
+                l.text = l.text.substr(0, at) + dq(v + extra);
+            }
+        }
+        content = true;
+        out.push_back(std::move(l));
+    }
+    return out;
+}
+
+Node load_yaml(const std::string& text) {
+    Anchors anchors;
+    return Block(logical_lines(text), anchors).parse();
 }
 
 // ---- schema ----
