@@ -332,7 +332,8 @@ int main(int argc, char** argv) {
             return 1;
         }
         k = k.substr(2);
-        if (i + 1 < argc && std::string(argv[i + 1]).rfind("--", 0) != 0) a.kv[k] = argv[++i];
+        if (const auto eq = k.find('='); eq != std::string::npos) a.kv[k.substr(0, eq)] = k.substr(eq + 1); // --key=value (CLI11)
+        else if (i + 1 < argc && std::string(argv[i + 1]).rfind("--", 0) != 0) a.kv[k] = argv[++i];
         else a.flags.insert(k);
     }
     const std::string cmd = argv[1];

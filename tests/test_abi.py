@@ -87,5 +87,8 @@ def test_cli_exit_codes(tmp_path):
     p = subprocess.run([cli, "merge", "--recipe", str(tmp_path / "r.yaml"), "--out", str(tmp_path / "o")],
                        capture_output=True, text=True)
     assert p.returncode == 1 and "RecipeError" in p.stderr
+    p = subprocess.run([cli, "merge", f"--recipe={tmp_path / 'r.yaml'}", f"--out={tmp_path / 'o'}"],
+                       capture_output=True, text=True)  # CLI11's --key=value form, as the reference CLI accepts
+    assert p.returncode == 1 and "RecipeError" in p.stderr
     p = subprocess.run([cli, "bogus"], capture_output=True, text=True)
     assert p.returncode == 1
