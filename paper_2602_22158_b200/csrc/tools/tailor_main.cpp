@@ -24,6 +24,8 @@
 #include <string>
 #include <vector>
 
+#include <json.hpp>
+
 #include "tailor_b200.h"
 
 namespace {
@@ -123,10 +125,22 @@ int cmd_merge(const Args& a) {
     tg_merge_stats st{};
     const int rc = tg_execute_merge(yaml.c_str(), a.kv.at("out").c_str(), &opt, &st);
     if (rc != TG_OK) return report(rc);
-    if (a.flags.count("json")) {
-        std::printf("{\"bytes_moved\":%llu,\"device_ms\":%.6f,\"out\":\"%s\",\"shard_files_read\":%lld,\"wall_ms\":%.6f,\"weight_files_read\":%lld}\n",
-                    static_cast<unsigned long long>(st.bytes_moved), st.device_ms, a.kv.at("out").c_str(),
-                    static_cast<long long>(st.shard_files_read), st.wall_ms, static_cast<long long>(st.weight_files_read));
+    if (a.flags.count("json")) { // the reference's keys (R/tools/tailor_main.cpp:84-91) plus the device's
+        size_t need = 0;
+        tg_resolve_plan(yaml.c_str(), nullptr, 0, &need);
+        std::string plan(need, '\0');
+        if (tg_resolve_plan(yaml.c_str(), plan.data(), plan.size(), &need) != TG_OK) return report(tg_last_error_kind());
+        const nlohmann::json pj = nlohmann::json::parse(plan.c_str());
+        std::cout << nlohmann::json{{"out", a.kv.at("out")},
+                                    {"num_ranks", pj.at("num_ranks")},
+                                    {"num_sources", pj.at("sources").size()},
+                                    {"shard_files_read", st.shard_files_read},
+                                    {"weight_files_read", st.weight_files_read},
+                                    {"wall_ms", st.wall_ms},
+                                    {"bytes_moved", st.bytes_moved},
+                                    {"device_ms", st.device_ms}}
+                         .dump()
+                  << "\n";
         return 0;
     }
     std::cout << "merged checkpoint written to " << a.kv.at("out") << "\n";

@@ -135,6 +135,9 @@ def test_cli_merge_plan_select(tmp_path):
     assert p.returncode == 0, p.stderr
     js = json.loads(p.stdout)
     assert js["shard_files_read"] == 2 * 3 and js["weight_files_read"] == 3
+    # the reference CLI's --json keys (R/tools/tailor_main.cpp:84-91)
+    assert {"out", "num_ranks", "num_sources", "shard_files_read", "weight_files_read", "wall_ms"} <= set(js)
+    assert js["out"] == str(tmp_path / "cli") and js["num_ranks"] == 2 and js["num_sources"] == 3
     (tmp_path / "r.json").write_text(rec.to_json())
     ref_tool("merge", "--recipe", tmp_path / "r.json", "--out", tmp_path / "ref")
     same_tree(tmp_path / "ref", tmp_path / "cli")
