@@ -125,15 +125,17 @@ int cmd_merge(const Args& a) {
     tg_merge_stats st{};
     const int rc = tg_execute_merge(yaml.c_str(), a.kv.at("out").c_str(), &opt, &st);
     if (rc != TG_OK) return report(rc);
+    size_t need = 0; // plan summary for the report (sidecar reads only)
+    tg_resolve_plan(yaml.c_str(), nullptr, 0, &need);
+    std::string plan(need, '\0');
+    if (tg_resolve_plan(yaml.c_str(), plan.data(), plan.size(), &need) != TG_OK) return report(tg_last_error_kind());
+    const nlohmann::json pj = nlohmann::json::parse(plan.c_str());
+    const int ranks = pj.at("num_ranks").get<int>();
+    const int sources = static_cast<int>(pj.at("sources").size());
     if (a.flags.count("json")) { // the reference's keys (R/tools/tailor_main.cpp:84-91) plus the device's
-        size_t need = 0;
-        tg_resolve_plan(yaml.c_str(), nullptr, 0, &need);
-        std::string plan(need, '\0');
-        if (tg_resolve_plan(yaml.c_str(), plan.data(), plan.size(), &need) != TG_OK) return report(tg_last_error_kind());
-        const nlohmann::json pj = nlohmann::json::parse(plan.c_str());
         std::cout << nlohmann::json{{"out", a.kv.at("out")},
-                                    {"num_ranks", pj.at("num_ranks")},
-                                    {"num_sources", pj.at("sources").size()},
+                                    {"num_ranks", ranks},
+                                    {"num_sources", sources},
                                     {"shard_files_read", st.shard_files_read},
                                     {"weight_files_read", st.weight_files_read},
                                     {"wall_ms", st.wall_ms},
@@ -143,11 +145,14 @@ int cmd_merge(const Args& a) {
                   << "\n";
         return 0;
     }
+    // the reference's report (R/tools/tailor_main.cpp:94-101), then the device's line
     std::cout << "merged checkpoint written to " << a.kv.at("out") << "\n";
-    std::cout << "optimizer shard files read: " << st.shard_files_read << "\n";
+    std::cout << "sources: " << sources << "  ranks: " << ranks << "\n";
+    std::cout << "optimizer shard files read: " << st.shard_files_read << " (bound " << ranks << " x " << sources << " = "
+              << ranks * sources << " cached)\n";
     std::cout << "weight files read: " << st.weight_files_read << "\n";
-    std::cout << "composite bytes: " << st.bytes_moved << " (device gather " << st.device_ms << " ms)\n";
     std::cout << "wall time: " << st.wall_ms << " ms\n";
+    std::cout << "composite bytes: " << st.bytes_moved << " (device gather " << st.device_ms << " ms)\n";
     return 0;
 }
 

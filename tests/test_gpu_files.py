@@ -141,6 +141,15 @@ def test_cli_merge_plan_select(tmp_path):
     (tmp_path / "r.json").write_text(rec.to_json())
     ref_tool("merge", "--recipe", tmp_path / "r.json", "--out", tmp_path / "ref")
     same_tree(tmp_path / "ref", tmp_path / "cli")
+    # text report: the reference's lines (R/tools/tailor_main.cpp:94-101)
+    p = subprocess.run([cli, "merge", "--recipe", str(tmp_path / "r.yaml"), "--out", str(tmp_path / "cli_text")],
+                       capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr
+    lines = p.stdout.splitlines()
+    assert lines[0] == f"merged checkpoint written to {tmp_path / 'cli_text'}"
+    assert lines[1] == "sources: 3  ranks: 2"
+    assert lines[2] == "optimizer shard files read: 6 (bound 2 x 3 = 6 cached)"
+    assert lines[3] == "weight files read: 3" and lines[4].startswith("wall time: ")
     # non-empty output directory -> StorageError -> exit 2
     p = subprocess.run([cli, "merge", "--recipe", str(tmp_path / "r.yaml"), "--out", str(tmp_path / "cli")],
                        capture_output=True, text=True)
