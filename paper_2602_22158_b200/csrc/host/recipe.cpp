@@ -497,13 +497,16 @@ bool blank(const std::string& raw) { return raw.find_first_not_of(" \t") == std:
 // prefixes and, for "key: value", the key's column (block scalars and plain-scalar
 // continuation lines must be indented beyond it).
 int owner_column(const Line& l) {
-    int col = l.indent;
-    std::size_t i = 0;
+    std::size_t i = 0, dash = std::string::npos;
     while (i + 1 < l.text.size() && l.text[i] == '-' && is_ws(l.text[i + 1])) {
+        dash = i;
         i += 2;
         while (i < l.text.size() && is_ws(l.text[i])) ++i;
     }
-    return col + static_cast<int>(i);
+    std::string k, r;
+    if (dash != std::string::npos && !split_key(l.text.substr(i), k, r)) // "- value": the item's dash
+        return l.indent + static_cast<int>(dash);
+    return l.indent + static_cast<int>(i); // "key: value" / "- key: value": the key
 }
 
 // The value part of a logical line ("key: v" -> v, "- v" -> v), after properties.

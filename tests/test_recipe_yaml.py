@@ -68,6 +68,12 @@ CASES = {
     "quoted_keys": "\"merge_method\": passthrough\n'num_ranks': 2\nbase_checkpoint: /a/ck-1\n",
     "hash_in_plain": "merge_method: passthrough\nnum_ranks: 2\nbase_checkpoint: /a/ck#1\n",
     "url_like": "merge_method: passthrough\nnum_ranks: 2\nbase_checkpoint: s3://bucket/ck-1\n",
+    "item_block_scalar": "merge_method: passthrough\nnum_ranks: 2\nslices:\n- source: |-\n    /a/ck-1\n  layers:\n  - 3\n"
+                         "aux:\n  norm:\n    >-\n     x\n",
+    "item_plain_continued": "merge_method: passthrough\nnum_ranks: 2\nslices:\n- source: /a/ck\n    -1\n  layers: [0]\n"
+                            "aux:\n  norm: x\n    y\n",
+    "seq_item_scalars": "merge_method: passthrough\nnum_ranks: 2\nslices:\n- source: a\n  layers:\n  - 1\n  - 2\n"
+                        "aux:\n  norm: >-\n   a\n   b\n",
     "indentless_range": "merge_method: passthrough\nnum_ranks: 2\nslices:\n- source: /a/ck-100\n  layers:\n    start: 0\n    end: 2\n",
 }
 
@@ -75,6 +81,14 @@ CASES = {
 @pytest.mark.parametrize("name", sorted(CASES))
 def test_yaml_styles_parse_like_a_yaml_reader(name):
     check(CASES[name])
+
+
+def test_integers_from_any_scalar_style_like_yaml_cpp():
+    """yaml-cpp's as<int>() converts the scalar's text whatever its style (PyYAML would
+    keep a quoted or block scalar a string), R/src/recipe.cpp:28-35."""
+    text = "merge_method: passthrough\nnum_ranks: '2'\nslices:\n- source: a\n  layers:\n  - |-\n    1\n  - \"2\"\n"
+    got = ours(text)
+    assert got["num_ranks"] == 2 and got["slices"][0]["layers"] == [1, 2]
 
 
 def test_first_document_only_like_yaml_cpp_load():
