@@ -118,9 +118,11 @@ def _plain_ok(s):
 def _scalar(rng, s, indent):
     """One rendering of string s: plain, single-quoted, double-quoted (with escapes), or a
     block scalar (only where a block value may start)."""
-    k = rng.randrange(5)
+    k = rng.randrange(6)
     if k == 0 and _plain_ok(s):
         return s
+    if k == 5 and indent is not None and " " in s and _plain_ok(s.replace(" ", "")):
+        return s.replace(" ", "\n" + " " * (indent + 2), 1)  # plain scalar continued (folded to a space)
     if k == 1:
         return "'" + s.replace("'", "''") + "'"
     if k == 2:
@@ -240,7 +242,7 @@ def random_recipe(rng):
 
 def test_random_renderings_parse_like_a_yaml_reader():
     rng = random.Random(2602)
-    for case in range(400):
+    for case in range(600):
         rec = random_recipe(rng)
         text = render(rng, rec)
         doc = yaml.safe_load(text.lstrip("\ufeff"))
