@@ -7,7 +7,7 @@
 // conversions, as in yaml-cpp), %directives, --- / ... markers (the first document, as
 // YAML::Load), BOM and CRLF — and an emitter in yaml-cpp's block style. Schema errors
 // name the offending field, as the reference's do. tests/test_recipe_yaml.py checks the
-// reader against PyYAML on fixed and 400 randomly rendered recipes.
+// reader against PyYAML on fixed and 600 randomly rendered recipes.
 #include <cctype>
 #include <cstdint>
 #include <map>
