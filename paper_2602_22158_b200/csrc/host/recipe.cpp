@@ -558,7 +558,8 @@ std::vector<Line> logical_lines(const std::string& text_in) {
     for (std::size_t i = 0; i < raw.size(); ++i) {
         std::string r = raw[i];
         const int number = static_cast<int>(i) + 1;
-        const auto marker = [&](const char* m) { return r.rfind(m, 0) == 0 && (r.size() == 3 || is_ws(r[3])); };
+        const auto marker_in = [](const std::string& x, const char* m) { return x.rfind(m, 0) == 0 && (x.size() == 3 || is_ws(x[3])); };
+        const auto marker = [&](const char* m) { return marker_in(r, m); };
         if (!content && !in_doc && !r.empty() && r[0] == '%') continue; // directive
         if (marker("---")) {
             if (content || in_doc) break; // a second document
@@ -581,7 +582,7 @@ std::vector<Line> logical_lines(const std::string& text_in) {
         int pending_breaks = 0;
         while ((q || depth > 0) && i + 1 < raw.size()) {
             const std::string nl = raw[++i];
-            if (marker("---") || marker("...")) yaml_error("document marker inside a flow or quoted node");
+            if (marker_in(nl, "---") || marker_in(nl, "...")) yaml_error("document marker inside a flow or quoted node");
             if (q) {
                 std::string c = trim(nl);
                 if (c.empty()) {

@@ -103,6 +103,7 @@ def test_first_document_only_like_yaml_cpp_load():
     "merge_method: passthrough\nnum_ranks: 2\nbase_checkpoint: \"abc\n",         # unterminated quote
     "merge_method: passthrough\nnum_ranks: 2\nbase_checkpoint: ~\n",             # null is not a scalar
     "merge_method: passthrough\nnum_ranks: 2\nbase_checkpoint: NULL\n",
+    "merge_method: passthrough\nnum_ranks: 2\nslices: [\n---\n]\n",             # marker inside a flow node
 ])
 def test_malformed_or_null_are_recipe_errors(text):
     with pytest.raises(t.TailorError) as e:
