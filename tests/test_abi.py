@@ -67,6 +67,12 @@ def test_null_handles_are_errors_not_crashes():
         assert rc != 0
         assert b"null" in L.tg_last_error()
     assert L.tg_layout_num_modules(None) == 0
+    # communicator arguments are checked before any device or NCCL call
+    uid = (ctypes.c_uint8 * 128)()
+    assert not L.tg_comm_create(uid, 2, 5, 0)
+    assert b"rank out of range" in L.tg_last_error()
+    assert not L.tg_comm_create(None, 2, 0, 0)
+    assert b"null id" in L.tg_last_error()
     dirs = (ctypes.c_char_p * 2)(b"/nonexistent-a", None)
     buf = ctypes.create_string_buffer(64)
     rc = L.tg_select_recipe(dirs, 2, 0.5, None, 0, buf, 64, None, None, None)
