@@ -57,15 +57,17 @@ std::string trim(const std::string& s) {
     return rtrim(s.substr(b));
 }
 
-// A quote opens a quoted scalar only where a node starts (line start, after "- ", ": ",
-// "[", "{", ","); elsewhere ' and " are plain characters ("/runs/bob's/ck-100").
-bool quote_opens(const std::string& s, std::size_t i) {
+// A quote (or a flow bracket) opens a node only where a node starts; elsewhere ' " [ {
+// are plain characters ("/runs/bob's/ck-100", "/data/[v2]"). In block context (depth 0)
+// a node starts at the line start or after "- ", ": ", "? "; inside a flow collection
+// also after "[", "{", ",".
+bool node_starts(const std::string& s, std::size_t i, int depth) {
     std::size_t j = i;
     while (j > 0 && is_ws(s[j - 1])) --j;
     if (j == 0) return true;
     const char p = s[j - 1];
-    if (p == '[' || p == '{' || p == ',') return true;
-    return (p == ':' || p == '-' || p == '?') && j < i; // "key: 'v'", "- 'v'"
+    if (depth > 0 && (p == '[' || p == '{' || p == ',')) return true;
+    return (p == ':' || p == '-' || p == '?') && j < i && (j == 1 || depth > 0 || p != '-' || is_ws(s[j - 2])); // "key: 'v'", "- 'v'"
 }
 
 // Scans s from state (quote, depth): returns where a comment starts (npos if none) and
@@ -87,9 +89,9 @@ std::size_t scan(const std::string& s, char& quote, int& depth) {
             }
             continue;
         }
-        if ((c == '"' || c == '\'') && quote_opens(s, i)) quote = c;
+        if ((c == '"' || c == '\'') && node_starts(s, i, depth)) quote = c;
         else if (c == '#' && (i == 0 || is_ws(s[i - 1]))) return i;
-        else if (c == '[' || c == '{') ++depth;
+        else if ((c == '[' || c == '{') && (depth > 0 || node_starts(s, i, 0))) ++depth; // mid-scalar brackets are plain text
         else if ((c == ']' || c == '}') && depth > 0) --depth;
     }
     return std::string::npos;
@@ -363,9 +365,9 @@ bool split_key(const std::string& t, std::string& key, std::string& rest) {
             }
             continue;
         }
-        if ((c == '"' || c == '\'') && quote_opens(t, i)) quote = c;
-        else if (c == '[' || c == '{') ++depth;
-        else if (c == ']' || c == '}') --depth;
+        if ((c == '"' || c == '\'') && node_starts(t, i, depth)) quote = c;
+        else if ((c == '[' || c == '{') && (depth > 0 || node_starts(t, i, 0))) ++depth;
+        else if ((c == ']' || c == '}') && depth > 0) --depth;
         else if (c == ':' && depth == 0 && (i + 1 == t.size() || is_ws(t[i + 1]))) {
             std::string k = trim(t.substr(0, i));
             if (k.size() >= 2 && (k.front() == '"' || k.front() == '\'') && k.back() == k.front()) {

@@ -249,3 +249,28 @@ def test_random_renderings_parse_like_a_yaml_reader():
         doc = yaml.safe_load(text.lstrip("\ufeff"))
         assert expected(doc) == rec, (case, text)  # the rendering itself is right
         assert ours(text) == rec, (case, text)
+
+
+def test_emitter_round_trips_awkward_strings():
+    """recipe_to_yaml quotes what a YAML reader would not read back as the same string
+    (indicators, brackets, quotes, '#', ': ', tabs, newlines, unicode): our reader and
+    PyYAML both recover every string."""
+    rng = random.Random(7)
+    alphabet = list("abcXYZ019/-_.:#&*!|>'\"%@`,[]{}? \t\\é✓") + ["\n"]
+    for _ in range(3000):
+        s = "".join(rng.choice(alphabet) for _ in range(rng.randrange(1, 12)))
+        rec = t.MergeRecipe(num_ranks=2, base_checkpoint=s, aux={"norm": s})
+        y = rec.to_yaml()
+        assert t.parse_recipe(y) == rec, y
+        d = yaml.safe_load(y)
+        assert str(d["aux"]["norm"]) == s or isinstance(d["aux"]["norm"], (int, float)), y  # 1.1 typing of "9"
+
+
+@pytest.mark.parametrize("text,value", [
+    ("base_checkpoint: /data/[v2]/ck\n", "/data/[v2]/ck"),
+    ("base_checkpoint: a{b'c\n", "a{b'c"),
+    ("base_checkpoint: x-'y'\n", "x-'y'"),
+    ("base_checkpoint: /p/[[x\n", "/p/[[x"),
+])
+def test_brackets_and_quotes_inside_plain_scalars_are_text(text, value):
+    assert ours("merge_method: passthrough\nnum_ranks: 2\n" + text)["base_checkpoint"] == value
