@@ -237,6 +237,38 @@ def test_recipe_from_manifests_matches_reference(tmp_path, strategy, steps, inte
     assert t.recipe_from_manifests(str(tmp_path / "run"), fail_at) == t.MergeRecipe.from_json(json.dumps(ref))
 
 
+@pytest.mark.parametrize("seed", range(16))
+def test_recipe_from_manifests_random_runs_match_reference(tmp_path, seed):
+    """Random reference training runs (strategy, interval, filter knobs, ranks, tied, an
+    injected failure) planned at random failure steps: the same recipe as the reference's
+    recipe_from_manifests (R/src/merge.cpp:359-418), or the same error kind."""
+    _need_ref()
+    rng = random.Random(seed)
+    spec = dict(num_layers=rng.randrange(1, 9), hidden_dim=8, ffn_dim=16, vocab_size=32,
+                weight_tied=rng.random() < 0.3, seed=100 + seed)
+    strategy = rng.choice(["full", "parity", "filter"])
+    steps, interval = rng.randrange(10, 121), rng.randrange(3, 31)
+    run = tmp_path / "run"
+    args = ["train", *spec_args(spec), "--strategy", strategy, "--steps", steps, "--interval", interval,
+            "--ranks", rng.randrange(1, 4), "--out", run]
+    if strategy == "filter":
+        head = rng.randrange(0, min(3, spec["num_layers"] + 1))  # the reference refuses head + tail > L
+        tail = rng.randrange(0, min(3, spec["num_layers"] - head + 1))
+        args += ["--head", head, "--tail", tail, "--sparse-multiple", rng.randrange(1, 6)]
+    if rng.random() < 0.5:
+        args += ["--fail-at", rng.randrange(0, steps + 10)]
+    ref_tool(*args)
+    for fs in sorted({rng.randrange(0, steps + 15) for _ in range(6)} | {steps}):
+        rc, out, err = ref_tool("plan", "--run", run, "--failure-step", fs, check=False)
+        if rc == 0:
+            assert t.recipe_from_manifests(str(run), fs) == t.MergeRecipe.from_json(json.dumps(out["recipe"])), fs
+        else:
+            kind = json.loads(err.strip().splitlines()[-1])["error"]
+            with pytest.raises(t.TailorError) as e:
+                t.recipe_from_manifests(str(run), fs)
+            assert str(e.value).startswith(kind), (fs, kind, str(e.value))
+
+
 def test_parse_config_reads_reference_config(tmp_path):
     _need_ref()
     spec = dict(num_layers=3, hidden_dim=8, ffn_dim=16, vocab_size=32, weight_tied=True, seed=77)
