@@ -33,12 +33,12 @@ def entries(prefix: bytes):
     return {k: tuple(v["data_offsets"]) for k, v in h.items()}
 
 
-@pytest.mark.parametrize("name", ["cfg3", "cfg2"])
-def test_full_size_rank_partition(name):
+@pytest.mark.parametrize("name,r", [("cfg3", 3), ("cfg3", 7), ("cfg2", 5), ("cfg2", 0)])
+def test_full_size_rank_partition(name, r):
+    """r = 7 is the last ZeRO rank (it holds every group's padding), r = 0 the first."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     spec, N, K = CONFIGS[name]
-    r = 3 if name == "cfg3" else 5
     fam = t.SynthFamily(spec, N, K)
     M = fam.num_modules
     dev = torch.device("cuda")
